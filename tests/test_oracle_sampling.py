@@ -1,0 +1,179 @@
+"""Oracle pins for the integer half of the path: Philox, Feistel positive permutation, joint negatives,
+corruption schedule, dedup, relation partition, init law. CPU only (no GPU).
+
+Citations: PAPER.md:260-261 (Sec. 2, mini-batches of b triplets), 317-318 (Sec. 3.1 step 1), 417-428 (Sec. 3.3 joint
+negative sampling), 476-495 (Sec. 3.4 relation partitioning); readings c.1-c.6, c.13 in DESIGN.md.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_philox_known_answers():
+    kat = json.load(open(os.path.join(GOLD, "philox_kat.json")))
+    for v in kat["vectors"]:
+        ctr = [int(x, 16) for x in v["ctr"]]
+        key = [int(x, 16) for x in v["key"]]
+        assert O.philox(ctr, key) == [int(x, 16) for x in v["out"]]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 16, 17, 255, 256, 257, 1000, 4097, 65536, 65537])
+def test_feistel_is_bijection(n):
+    # each triple exactly once per epoch -> pi_e must permute [0, n)
+    for epoch in (0, 1, 7):
+        img = [O.feistel_index(n, 1234, epoch, p) for p in range(n)]
+        assert sorted(img) == list(range(n))
+
+
+def test_feistel_large_n_sample_is_injective():
+    # the Freebase list size: check a bounded sample is injective and in range
+    n = 338_586_276
+    ps = list(range(0, n, n // 2000))[:2000]
+    img = [O.feistel_index(n, 1, 0, p) for p in ps]
+    assert len(set(img)) == len(img)
+    assert all(0 <= x < n for x in img)
+
+
+def test_epochs_differ():
+    n = 1000
+    a = [O.feistel_index(n, 5, 0, p) for p in range(n)]
+    b = [O.feistel_index(n, 5, 1, p) for p in range(n)]
+    assert a != b
+
+
+def test_positives_cover_each_triple_once_per_epoch():
+    # B=16 divides N_t=64 -> 4 steps = 1 epoch; every triple appears exactly once
+    n_t = 64
+    h = np.arange(n_t) % 10
+    r = np.arange(n_t) % 3
+    t = (np.arange(n_t) * 7) % 10
+    tr = O.Trainer("transe_l2", 10, 3, 8, batch=16, chunk=8, neg_k=4, triples=(h, r, t))
+    seen = np.concatenate([tr.sample(s)[0] for s in range(4)])
+    assert sorted(seen.tolist()) == list(range(n_t))
+    seen2 = np.concatenate([tr.sample(s)[0] for s in range(4, 8)])
+    assert sorted(seen2.tolist()) == list(range(n_t))
+
+
+def test_neg_ids_in_range_and_uniform():
+    # chi^2 uniformity over 10^6 draws passes at p > 0.01 (here 2^20 draws, 64 bins)
+    n_ent = 1000
+    seed = 99
+    draws = []
+    for s in range(8):
+        for cg in range(4):
+            draws += [O.neg_id(seed, n_ent, s, cg, j) for j in range(4096)]
+    draws = np.array(draws)
+    assert draws.min() >= 0 and draws.max() < n_ent
+    # 1000 ids folded into 50 bins of 20 ids each
+    counts = np.bincount(draws // 20, minlength=50)
+    exp = len(draws) / 50
+    chi2 = ((counts - exp) ** 2 / exp).sum()
+    # 49 dof: 99th percentile ~ 74.9
+    assert chi2 < 74.9, chi2
+
+
+def test_neg_id_range_map_is_mulhi():
+    # id = floor(u * N / 2^64) with u = w1<<32|w0 (even j) or w3<<32|w2 (odd j)
+    seed, n_ent = (0x1234_5678_9ABC_DEF0, 86_054_151)
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    for (s, cg, j) in [(0, 0, 0), (0, 0, 1), (5, 3, 200), (123456, 7, 255)]:
+        o = O.philox([j // 2, cg, s, 1], key)
+        u = (o[3] << 32 | o[2]) if j & 1 else (o[1] << 32 | o[0])
+        assert O.neg_id(seed, n_ent, s, cg, j) == (u * n_ent) >> 64
+
+
+def test_mode_schedule():
+    # c.4: ALTERNATE -> TAIL iff (s + cg) even; alternates within a step (C even) and flips every step
+    assert [O.mode(O.ALTERNATE, 0, c) for c in range(4)] == [0, 1, 0, 1]
+    assert [O.mode(O.ALTERNATE, 1, c) for c in range(4)] == [1, 0, 1, 0]
+    assert all(O.mode(O.TAIL, s, c) == 0 for s in range(3) for c in range(3))
+    assert all(O.mode(O.HEAD, s, c) == 1 for s in range(3) for c in range(3))
+
+
+def test_distinct_row_bound():
+    # distinct entity rows <= 2B + (B/g)k, distinct relations <= B
+    rng = np.random.default_rng(0)
+    n_t = 500
+    h, r, t = rng.integers(0, 50, n_t), rng.integers(0, 7, n_t), rng.integers(0, 50, n_t)
+    tr = O.Trainer("distmult", 50, 7, 8, batch=32, chunk=8, neg_k=16, triples=(h, r, t))
+    for s in range(5):
+        e, rr = tr.occurrences(s)
+        assert len(e) == 2 * 32 + 4 * 16
+        assert len(np.unique(e)) <= 2 * 32 + 4 * 16
+        assert len(np.unique(rr)) <= 32
+
+
+def test_dedup_matches_brute_force():
+    rng = np.random.default_rng(1)
+    for n in (1, 2, 50, 3072):
+        ids = rng.integers(0, max(2, n // 3), n)
+        uniq, inv, seg_off, seg_occ = O.dedup(ids)
+        assert np.array_equal(uniq, np.unique(ids))
+        assert np.array_equal(uniq[inv], ids)
+        # segments: occurrences of each id in increasing occurrence index (stable)
+        for u in range(len(uniq)):
+            occ = seg_occ[seg_off[u]:seg_off[u + 1]]
+            assert np.array_equal(occ, np.nonzero(ids == uniq[u])[0])
+
+
+def test_relation_partition_spec_example():
+    # counts [5,4,3,2], W=2 -> 5->0, 4->1, 3->1, 2->0, loads [7,7]
+    rels = np.repeat(np.arange(4), [5, 4, 3, 2])
+    owner, ns = O.relation_partition(rels, 4, 2)
+    assert ns == 0
+    assert owner.tolist() == [0, 1, 1, 0]
+    loads = [len(O.rank_triples(rels, 4, 2, w)) for w in range(2)]
+    assert loads == [7, 7]
+
+
+def test_relation_partition_single_relation_splits():
+    # a single relation at W=4 -> SPLIT, loads equal +-1
+    rels = np.zeros(103, np.int64)
+    owner, ns = O.relation_partition(rels, 1, 4)
+    assert ns == 1 and owner[0] == -1
+    loads = [len(O.rank_triples(rels, 1, 4, w)) for w in range(4)]
+    assert max(loads) - min(loads) <= 1 and sum(loads) == 103
+
+
+def test_relation_partition_is_a_partition_and_balanced():
+    # each relation on exactly one partition (unless split); greedy balance bound
+    rng = np.random.default_rng(3)
+    n_rel = 300
+    rels = np.minimum((rng.zipf(1.6, 20000) - 1), n_rel - 1)
+    for P in (2, 4, 8):
+        owner, _ = O.relation_partition(rels, n_rel, P)
+        lists = [O.rank_triples(rels, n_rel, P, w) for w in range(P)]
+        allidx = np.sort(np.concatenate(lists))
+        assert np.array_equal(allidx, np.arange(len(rels)))
+        for w, l in enumerate(lists):
+            assert np.all(np.diff(l) > 0)
+            for rr in np.unique(rels[l]):
+                assert owner[rr] == w or owner[rr] == -1
+        counts = np.bincount(rels, minlength=n_rel)
+        non_split_max = counts[owner >= 0].max()
+        loads = [len(l) for l in lists]
+        assert max(loads) - min(loads) <= non_split_max + 1
+
+
+def test_init_law():
+    # c.6: v = bound * ((float)(int32)u * 2^-31), u = Philox(ctr=(col,row_lo,row_hi^(tab<<24),INIT))[0]
+    seed, bound = 7, O.default_bound(12.0, 400)
+    assert bound == np.float32(np.float32(14.0) / np.float32(400.0))
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    for (tab, row, col) in [(0, 0, 0), (0, 86_054_150, 399), (1, 3, 17), (2, 5, 39999)]:
+        u = O.philox([col, row & 0xFFFFFFFF, (row >> 32) ^ (tab << 24), 3], key)[0]
+        i32 = np.int32(np.uint32(u).view(np.int32))
+        expect = np.float32(bound) * (np.float32(i32) * np.float32(2.0 ** -31))
+        assert O.init_value(seed, tab, row, col, bound) == expect
+    vals = np.array([O.init_value(seed, 0, r, c, 1.0) for r in range(200) for c in range(100)])
+    # SPEC.md:351 moments of U[-b,b]: mean 0, variance b^2/3
+    assert abs(vals.mean()) < 0.02 and abs(vals.var() - 1 / 3) < 0.02
+    assert vals.min() >= -1.0 and vals.max() < 1.0
+    assert O.default_bound(0.0, 64) == np.float32(1.0) / np.float32(8.0)
