@@ -1,0 +1,312 @@
+"""Benchmark of the B200-native DGL-KE mini-batch training step (BASELINE.json metric: positive triples/sec at
+d=400, k=256; fraction of the HBM / tensor roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload freebase|fb15k|wn18|tiny] [--model M]
+                  [--precision tf32|fp32] [--impl ours|reference]
+
+Workload at N=1 (default): configs[4], the Freebase-shaped synthetic graph (86,054,151 entities, 14,824 relations,
+338,586,276 triples), TransE-L2, d=400, B=1024, g=256, k=256 -- the north_star's target configuration; it fits one
+B200 (137.7 GB entity table). Inputs are seeded synthetic data (synth/, Zipf-skewed).
+A step = one pass of the whole hot path: sample -> gather -> positive + chunked negative score fwd/bwd -> dedup-sum ->
+sparse Adagrad, on one batch of B positives per GPU. The 137.7 GB table is far larger than L2 (126 MB), so no L2
+flush is needed between steps ("inputs larger than L2").
+
+--impl reference times the CPU oracle (oracle/, plain C++) on the host cores on a bounded sample of the same workload
+(rank 0 only); its ratio to ours divides by a deliberately slow program -- parity and the roofline fraction are the
+headline, not that ratio.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (graph, model, d, B, g, k)
+    "freebase": ("freebase", "transe_l2", 400, 1024, 256, 256),
+    "fb15k": ("fb15k", "distmult", 400, 1024, 256, 256),
+    "wn18": ("wn18", "rotate", 400, 1024, 256, 256),
+    "tiny": ("tiny", "transe_l2", 64, 256, 64, 64),
+}
+METRIC = "positive triples/sec (d=400, k=256) at 1/2/4/8 B200; % of HBM/tensor roofline"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def algorithmic_bytes(n_uniq_ent, n_uniq_rel, d, drel):
+    """A = sum_tables U * (2*w*4 + 2*4): each touched row and its Adagrad state read once + written once."""
+    return n_uniq_ent * (2 * d * 4 + 8) + n_uniq_rel * (2 * drel * 4 + 8)
+
+
+def cpu_baseline(args, wl, budget_s=20.0):
+    """The oracle as it stands, timed on the host on a bounded sample of the same workload (1 thread)."""
+    import oracle as O
+    import synth
+    gname, model, d, B, g, k = wl
+    gr = synth.graph(gname)
+    lazy = gr.n_entities > 1_000_000
+    t0 = time.perf_counter()
+    orc = O.Trainer(model, gr.n_entities, gr.n_relations, d, B, g, k, gamma=12.0, lr=0.1, seed=1, graph=gr,
+                    lazy_rows=lazy) if lazy else O.Trainer(model, gr.n_entities, gr.n_relations, d, B, g, k,
+                                                           gamma=12.0, lr=0.1, seed=1, triples=gr.triples())
+    setup = time.perf_counter() - t0
+    steps, t_total = 0, 0.0
+    while t_total < budget_s and steps < args.steps:
+        t1 = time.perf_counter()
+        orc.train(1)
+        t_total += time.perf_counter() - t1
+        steps += 1
+    return {"value": B * steps / t_total, "unit": "positive triples/s", "cores": 1, "kind": "oracle",
+            "sample": f"{steps} training steps of {gname} {model} d={d} B={B} g={g} k={k} in double on 1 host thread "
+                      f"({'lazily materialised rows' if lazy else 'dense tables'}); setup {setup:.1f}s excluded",
+            "steps": steps, "seconds": t_total}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.workload]
+    budget = max(5.0, min(60.0, 4.0 * args.steps))
+    cb = cpu_baseline(args, wl, budget_s=budget)
+    gname, model, d, B, g, k = wl
+    line = {"metric": METRIC, "value": cb["value"], "unit": "positive triples/s", "n_gpus": args.gpus,
+            "steps": cb["steps"], "warmup": 0, "ms_per_step": 1000.0 * cb["seconds"] / max(1, cb["steps"]),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{gname} (BASELINE.json configs)", "model": model, "dim": d, "batch": B,
+                       "chunk": g, "neg_k": k},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "positive triples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--workload", default="freebase", choices=sorted(WORKLOADS))
+    ap.add_argument("--model", default=None)
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    wl = list(WORKLOADS[args.workload])
+    if args.model:
+        wl[1] = args.model
+    wl = tuple(wl)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import synth
+    from paper_2004_08532_b200 import kge
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    gname, model, d, B, g, k = wl
+    gr = synth.graph(gname)
+    t0 = time.perf_counter()
+    h_, r_, t_ = gr.triples()
+    t_gen = time.perf_counter() - t0
+    cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=d, batch_size=B,
+                     chunk_size=g, neg_k=k, gamma=12.0, lr=0.1, seed=1 + rank, neg_precision=args.precision)
+    stream = torch.cuda.Stream()  # the library enqueues on this stream; events below are recorded on it
+    t0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        H = kge.init(cfg, h_, r_, t_)
+    torch.cuda.synchronize()
+    t_init = time.perf_counter() - t0
+
+    # warm-up + a full per-kernel profile to find the dominant kernel and its share of the step
+    H.train_step(args.warmup, return_loss=False)
+    H.sync()
+    H.profile_begin()
+    H.train_step(min(50, args.steps), return_loss=False)
+    prof = H.profile_end()
+    step_kernels = {kname: v for kname, v in prof.items() if v[1] > 0 and kname != "k_sample"}
+    dominant = max(step_kernels, key=lambda n: step_kernels[n][0])
+    H.sync()
+
+    # ---- timed region: K steps, device-timed with CUDA events; barrier + sync on both sides ----
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    launches0 = H.launch_count
+    with Clocks(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        e0.record(stream)
+        H.train_step(args.steps, return_loss=False)
+        e1.record(stream)
+        stream.synchronize()
+        wall = time.perf_counter() - w0
+    ms_dev = e0.elapsed_time(e1)
+    gpu_launches = H.launch_count - launches0
+    ms = max(ms_dev, 0.0)
+    if pg:
+        t = torch.tensor([ms], device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ws * B * args.steps / (ms / 1000.0)
+
+    # ---- roofline of the dominant kernel: its own CUDA-event time over a K-step region ----
+    H.profile_begin()
+    H.train_step(args.steps, return_loss=False)
+    prof2 = H.profile_end()
+    dom_ms, dom_n = prof2[dominant]
+    s = H.sample(H.step)
+    n_ue, n_ur = len(s["uniq_ent"]), len(s["uniq_rel"])
+    drel = d // 2 if model == "rotate" else d
+    hbm_gbs, bf16_tf, bf16_tf_sust, src = peaks()
+    flops_neg = 2.0 * B * k * d  # one contraction of the chunked negatives
+    if dominant in ("k_update", "k_gather"):
+        traffic_alg = algorithmic_bytes(n_ue, n_ur, d, drel) if dominant == "k_update" else \
+            (n_ue * d * 4 + n_ur * drel * 4)
+        ach = traffic_alg / (dom_ms / 1000.0) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
+                "traffic": None, "kernel": dominant, "alg_bytes_per_launch": traffic_alg}
+    elif args.precision == "tf32" and model in ("transe_l2", "distmult", "complex"):
+        fl = flops_neg * (1 if dominant == "k_neg_fwd" else 2)
+        ach = fl / (dom_ms / 1000.0) / 1e12
+        peak = bf16_tf * 0.5  # TF32 = half the dense bf16 rate (B200_PROFILING.md nominal ratio 1.1 / 2.25)
+        roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "traffic": None, "kernel": dominant, "peak_note": f"tf32 = 0.5 x {src} bf16 burst"}
+    else:
+        # FFMA path: plain ALU bound; peak = 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz
+        fl = flops_neg * (1 if dominant == "k_neg_fwd" else 2)
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        ach = fl / (dom_ms / 1000.0) / 1e12
+        roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "traffic": None, "kernel": dominant, "peak_note": "148 SM x 128 FP32 lanes x FMA x 1.965 GHz"}
+    roof["share_of_step"] = dom_ms * dom_n / sum(v[0] * v[1] for v in prof2.values())
+    roof["per_kernel_ms"] = {k_: v[0] for k_, v in prof2.items()}
+    roof["peak_source"] = src
+
+    # ---- e2e: caller-supplied batch from pinned host memory through kge_train_batch, loss read back ----
+    e2e_steps = min(args.e2e_steps, args.steps)
+    pinned = torch.empty((3, e2e_steps, B), dtype=torch.int64, pin_memory=True)
+    base = (rank * 7919 * B) % max(1, gr.n_triples - e2e_steps * B)
+    for a, arr in enumerate((h_, r_, t_)):
+        pinned[a].copy_(torch.from_numpy(np.ascontiguousarray(arr[base:base + e2e_steps * B]).reshape(e2e_steps, B)))
+    loss_buf = torch.empty(1, dtype=torch.float32, pin_memory=True)
+    H.sync()
+    if pg:
+        pg.barrier()
+    w0 = time.perf_counter()
+    for st in range(e2e_steps):
+        H.train_batch_ptr(pinned[0, st].data_ptr(), pinned[1, st].data_ptr(), pinned[2, st].data_ptr(),
+                          loss_buf.data_ptr())
+    H.sync()
+    e2e_s = time.perf_counter() - w0
+    if pg:
+        t = torch.tensor([e2e_s], device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": ws * B * e2e_steps / e2e_s, "unit": "positive triples/s", "h2d_bytes_per_step": 3 * B * 4,
+           "d2h_bytes_per_step": 4, "steps": e2e_steps,
+           "how": "kge_train_batch per step: host int64 (h,r,t)[B] from pinned memory, narrowed to int32 and copied "
+                  "H2D inside the call; loss read back D2H every step (synchronous); host wall clock"}
+
+    if rank == 0:
+        cb = None
+        if not args.no_cpu_baseline and ws == 1:
+            try:
+                cb = cpu_baseline(args, wl, budget_s=20.0)
+            except Exception as ex:  # the baseline is context; never fail the bench on it
+                cb = {"error": str(ex)}
+        clocks = clk.summary()
+        line = {"metric": METRIC, "value": value, "unit": "positive triples/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "tf32", "data": "synthetic",
+                "config": {"workload": f"{gname}-shaped synthetic (BASELINE.json configs)", "model": model, "dim": d,
+                           "batch": B, "chunk": g, "neg_k": k, "n_entities": gr.n_entities,
+                           "n_relations": gr.n_relations, "n_triples": gr.n_triples,
+                           "l2": "inputs larger than L2 (entity table >> 126 MB)" if gr.n_entities * d * 4 > 2e9
+                           else "tables L2-resident (no flush)"},
+                "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
+                "wall_s_timed": wall, "setup": {"graph_gen_s": t_gen, "init_s": t_init},
+                "uniq_rows_per_step": {"entity": n_ue, "relation": n_ur}}
+        print(json.dumps(line), flush=True)
+    H.destroy()
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,162 @@
+/* kge.h -- C-ABI of libkge.so, the B200-native (sm_100a) DGL-KE mini-batch KGE training step.
+ *
+ * The operation is the four-step mini-batch loop of PAPER.md:314-344 (Sec. 3.1):
+ *   (1) sample b positive triplets of the local partition and their negatives (joint negative
+ *       sampling PAPER.md:417-428, Sec. 3.3: chunks of g positives share k uniformly drawn corrupting entities),
+ *   (2) fetch the entity and relation rows the batch touches,
+ *   (3) forward + backward of the Table-1 score (Sec. 2) under the logistic loss,
+ *       negatives scored as a generalised matrix product o x t'^T,
+ *   (4) apply sparse row-wise Adagrad to the touched rows (sparse updates PAPER.md:262-266,
+ *       472-474), duplicate-row gradients summed by sort + segmented reduce first.
+ * Readings of the paper where it is silent (RNG, positive order, head/tail schedule, margin placement, loss
+ * normalisation, init, optimizer) are DESIGN.md "Readings" = SURVEY.md 8(c) c.1-c.14; the CPU oracle in oracle/
+ * implements the same readings independently.
+ *
+ * Conventions for every entry point:
+ *  - Return value is a kge_status; nothing throws across the ABI. On a non-OK return kge_last_error() gives a
+ *    thread-local message. A failed call leaves the handle usable unless it returns KGE_ECUDA / KGE_ENCCL.
+ *  - Host pointers are caller-owned and only read / written during the call. Device memory (tables, triples,
+ *    workspaces) is owned by the handle, allocated through cfg.dev_alloc / dev_free when given (PyTorch's caching
+ *    allocator in the Python binding) else cudaMalloc, and freed by kge_destroy.
+ *  - Work is enqueued on cfg.cuda_stream (NULL -> a stream the handle creates). Calls that only enqueue return
+ *    before the GPU finishes; calls with host outputs synchronise that stream before returning.
+ *  - Ids are int64 at the ABI; the device stores int32, so n_entities, n_relations, n_triples must be < 2^31.
+ *  - Not thread-safe per handle. With world_size > 1, kge_init and kge_train_step are collective (every rank calls
+ *    them in the same order, NCCL semantics).
+ *  - There is no CPU fallback: without a usable sm_100 device kge_init returns KGE_ECUDA.
+ */
+#ifndef KGE_H
+#define KGE_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KGE_ABI_VERSION 1
+
+typedef struct kge_handle kge_handle; /* opaque, library-owned */
+
+/* Table 1 models. RESCAL is out of scope. */
+typedef enum {
+  KGE_TRANSE_L1 = 0, /* gamma - ||h + r - t||_1 */
+  KGE_TRANSE_L2 = 1, /* gamma - ||h + r - t||_2 (not squared) */
+  KGE_DISTMULT = 2,  /* h^T diag(r) t */
+  KGE_COMPLEX = 3,   /* Re(h^T diag(r) conj(t)); rows [re(d/2) | im(d/2)] */
+  KGE_ROTATE = 4,    /* gamma - ||h o e^{i theta} - t||^2 (variant 1: gamma - sum_j |.|); relation = d/2 phases */
+  KGE_TRANSR = 5     /* gamma - ||M_r h + r - M_r t||_2^2, M_r d x d row-major */
+} kge_model;
+
+typedef enum {
+  KGE_OK = 0,
+  KGE_EINVAL = -1,       /* bad configuration / argument (g does not divide B, odd d for ComplEx/RotatE, k<=0, ...) */
+  KGE_ERANGE = -2,       /* an id out of range, or a size >= 2^31 */
+  KGE_ENOMEM = -3,       /* device allocation failed */
+  KGE_ECUDA = -4,        /* CUDA error (incl. no sm_100 device); handle should be destroyed */
+  KGE_ENCCL = -5,        /* NCCL error */
+  KGE_ENONFINITE = -6,   /* a step produced a non-finite loss; that step's update was skipped on the device */
+  KGE_ESTATE = -7,       /* call not valid in the handle's state */
+  KGE_EUNSUPPORTED = -8  /* valid request this build does not implement */
+} kge_status;
+
+/* Corruption schedule (reading c.4; "corrupt the head entities in a similar fashion"). */
+typedef enum { KGE_CORRUPT_TAIL = 0, KGE_CORRUPT_HEAD = 1, KGE_CORRUPT_ALTERNATE = 2 } kge_corrupt;
+
+/* Arithmetic of the chunked negative contraction. FP32 = FFMA (all models; the parity path);
+ * TF32 = tcgen05 tensor cores with TMEM accumulators (DistMult, ComplEx, TransE-L2 via ||o||^2 - 2 o.x + ||x||^2). */
+typedef enum { KGE_PREC_FP32 = 0, KGE_PREC_TF32 = 1 } kge_precision;
+
+typedef struct {
+  int32_t abi_version;     /* = KGE_ABI_VERSION */
+  int32_t model;           /* kge_model */
+  int64_t n_entities;      /* |V| */
+  int64_t n_relations;     /* number of relation types */
+  int32_t dim;             /* d: floats per entity row; multiple of 4 (of 8 for ComplEx/RotatE) */
+  int32_t batch_size;      /* b positives per step per rank */
+  int32_t chunk_size;      /* g positives sharing one negative set; must divide batch_size */
+  int32_t neg_k;           /* k negatives per chunk */
+  float gamma;             /* margin gamma; enters f = gamma + f_T1 for distance models (reading Q7) */
+  float lr;                /* Adagrad learning rate */
+  float adagrad_eps;       /* epsilon inside sqrt(state + eps); <= 0 -> 1e-10 */
+  float init_bound;        /* <= 0 -> (gamma+2)/d if gamma > 0 else 1/sqrt(d) (reading c.6) */
+  uint64_t seed;           /* Philox key for sampling and init (reading c.1) */
+  int32_t corrupt;         /* kge_corrupt */
+  int32_t neg_precision;   /* kge_precision */
+  int32_t rotate_variant;  /* RotatE: 0 = Table-1 squared (default), 1 = modulus sum */
+  int32_t lag;             /* 0 = synchronous (reading c.12); other values -> KGE_EUNSUPPORTED in this build */
+  int32_t world_size;      /* P ranks (one process per GPU) */
+  int32_t rank;            /* this rank */
+  void* nccl_comm;         /* ncclComm_t shared with the caller, or NULL */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId when nccl_comm == NULL and world_size > 1 */
+  void* cuda_stream;       /* cudaStream_t to enqueue on, or NULL */
+  void* (*dev_alloc)(size_t bytes, void* ctx); /* optional device allocator */
+  void (*dev_free)(void* ptr, void* ctx);
+  void* alloc_ctx;
+} kge_config;
+
+/* Fill *cfg with defaults (ABI version, TransE-L2, d=400, B=1024, g=256, k=256, gamma=12, lr=0.1, eps=1e-10,
+ * seed=1, ALTERNATE, TF32, P=1). Never fails. */
+void kge_config_default(kge_config* cfg);
+
+/* Create a handle: validate cfg, copy the triples (h, r, t) of the whole graph to the device,
+ * compute this rank's triple list (relation partitioning PAPER.md:476-495 when world_size > 1), allocate and
+ * Philox-initialise the tables (reading c.6) and zero the Adagrad states.
+ * heads/rels/tails: host int64[n_triples], caller-owned, read during the call only.
+ * Errors: KGE_EINVAL (config), KGE_ERANGE (id out of range / sizes >= 2^31), KGE_ENOMEM, KGE_ECUDA, KGE_ENCCL. */
+int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, const int64_t* rels, const int64_t* tails,
+             int64_t n_triples);
+
+/* Run the sampler of step `step` (steps (1) of Sec. 3.1 and the dedup of the touched rows) and copy its results to
+ * host buffers; any pointer may be NULL. Sizes: pos_idx[B] (triple indices), neg[C*k] (C = B/g, chunk-major),
+ * mode[C] (0 tail, 1 head), uniq_ent[2B+C*k] (ascending distinct entity ids over occurrences
+ * [h_0..h_{B-1}, t_0..t_{B-1}, neg...]), inv_ent[2B+C*k] (position of each occurrence's id in uniq_ent),
+ * uniq_rel[B], inv_rel[B] likewise for [r_0..r_{B-1}]. Synchronous. Does not advance the step counter. */
+int kge_sample(kge_handle* h, int64_t step, int64_t* pos_idx, int64_t* neg, int8_t* mode, int64_t* uniq_ent,
+               int64_t* n_uniq_ent, int32_t* inv_ent, int64_t* uniq_rel, int64_t* n_uniq_rel, int32_t* inv_rel);
+
+/* Enqueue n_steps training steps (sample -> gather -> score fwd/bwd -> dedup-sum -> Adagrad), advancing the step
+ * counter. loss_out: host float[n_steps] receiving each step's loss (then the call synchronises), or NULL (the call
+ * returns after enqueueing). KGE_ENONFINITE is reported by the first synchronising call after the offending step. */
+int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out);
+
+/* One step on a caller-supplied batch of B positive triples (host int64 heads/rels/tails[B]); negatives are still
+ * drawn on the device for the current step counter. Copies the batch host->device, runs the step, and (if loss_out
+ * is not NULL) reads the loss back. This is the end-to-end entry for a host-side sampler. */
+int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails, float* loss_out);
+
+/* Scores f(h, r, t) of n triples with the current tables (Table 1 with the margin of reading Q7). out: host
+ * float[n]. Synchronous. KGE_ERANGE on an out-of-range id. */
+int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, float* out);
+
+/* Read / overwrite rows of a table: 0 entity [N_e x d], 1 relation [N_r x d_r] (d_r = d, or d/2 for RotatE),
+ * 2 TransR projection [N_r x d*d], 3 entity Adagrad state [N_e x 1], 4 relation state, 5 projection state.
+ * ids: host int64[n]; out/in: host float[n x width]. Synchronous. KGE_EINVAL for a table the model lacks. */
+int kge_get_rows(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, float* out);
+int kge_set_rows(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, const float* in);
+int32_t kge_table_width(const kge_handle* h, int32_t table);
+
+/* Next step index (steps are counter-based: (seed, step) fixes every sample, so resume is exact). */
+int64_t kge_step(const kge_handle* h);
+int kge_set_step(kge_handle* h, int64_t step);
+
+/* Wait for all enqueued work; reports KGE_ENONFINITE if any step since the last check had a non-finite loss. */
+int kge_sync(kge_handle* h);
+
+/* Diagnostics. Kernel ids for kge_profile_end. Between begin and end every kernel launch of the step is bracketed by
+ * CUDA events on the handle's stream; end synchronises and returns the average device duration (ms) and the number
+ * of launches per kernel id. kge_launch_count: total kernel launches the handle has issued. */
+enum { KGE_K_SAMPLE = 0, KGE_K_GATHER = 1, KGE_K_NEG_FWD = 2, KGE_K_NEG_BWD = 3, KGE_K_CHAIN = 4, KGE_K_UPDATE = 5,
+       KGE_K_COUNT = 6 };
+int kge_profile_begin(kge_handle* h);
+int kge_profile_end(kge_handle* h, int32_t n_kernels, double* avg_ms, int64_t* launches);
+int64_t kge_launch_count(const kge_handle* h);
+
+void kge_destroy(kge_handle* h);
+const char* kge_last_error(void);
+const char* kge_kernel_name(int32_t kernel_id);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,628 @@
+// api.cu -- the C-ABI of include/kge.h: validation, device memory, table init, the step loop and diagnostics.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kge_internal.h"
+
+namespace kge {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return KGE_ECUDA;
+}
+
+void launch_begin(kge_handle* h, int kid) {
+  ++h->launches;
+  if (!h->prof.on) return;
+  if (h->prof.used + 2 > h->prof.ev.size()) {
+    h->prof.ev.push_back(nullptr);
+    h->prof.ev.push_back(nullptr);
+    cudaEventCreate(&h->prof.ev[h->prof.ev.size() - 2]);
+    cudaEventCreate(&h->prof.ev[h->prof.ev.size() - 1]);
+  }
+  cudaEventRecord(h->prof.ev[h->prof.used], h->stream);
+  h->prof.kid.push_back(kid);
+}
+
+void launch_end(kge_handle* h, int kid) {
+  (void)kid;
+  if (!h->prof.on) return;
+  cudaEventRecord(h->prof.ev[h->prof.used + 1], h->stream);
+  h->prof.used += 2;
+}
+
+static void* dalloc(kge_handle* h, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~size_t(255);
+  void* p = nullptr;
+  if (h->cfg.dev_alloc) {
+    p = h->cfg.dev_alloc(bytes, h->cfg.alloc_ctx);
+  } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+  }
+  if (p) h->allocs.push_back(p);
+  return p;
+}
+
+static void free_all(kge_handle* h) {
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->allocs) {
+    if (h->cfg.dev_free)
+      h->cfg.dev_free(p, h->cfg.alloc_ctx);
+    else
+      cudaFree(p);
+  }
+  h->allocs.clear();
+}
+
+#define CK(expr)                                         \
+  do {                                                   \
+    cudaError_t e_ = (expr);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
+  } while (0)
+
+static float default_bound(float gamma, int dim) {
+  if (gamma > 0.f) {
+    volatile float num = gamma + 2.0f;
+    volatile float v = num / (float)dim;
+    return v;
+  }
+  volatile float sd = std::sqrt((float)dim);
+  volatile float v = 1.0f / sd;
+  return v;
+}
+
+static int validate(const kge_config* c) {
+  if (!c) { set_error("cfg is NULL"); return KGE_EINVAL; }
+  if (c->abi_version != KGE_ABI_VERSION) { set_error("abi_version mismatch"); return KGE_EINVAL; }
+  if (c->model < 0 || c->model > KGE_TRANSR) { set_error("unknown model"); return KGE_EINVAL; }
+  if (c->dim <= 0 || c->dim % 4 != 0) { set_error("dim must be a positive multiple of 4"); return KGE_EINVAL; }
+  if ((c->model == KGE_COMPLEX || c->model == KGE_ROTATE) && c->dim % 8 != 0) {
+    set_error("ComplEx/RotatE need dim % 8 == 0 (d/2 complex coordinates, float4 halves)");
+    return KGE_EINVAL;
+  }
+  if (c->dim > 1024) { set_error("dim > 1024 not supported"); return KGE_EINVAL; }
+  if (c->batch_size <= 0 || c->chunk_size <= 0 || c->batch_size % c->chunk_size != 0) {
+    set_error("chunk_size must divide batch_size (SPEC.md:209)");
+    return KGE_EINVAL;
+  }
+  if (c->neg_k <= 0) { set_error("neg_k must be > 0"); return KGE_EINVAL; }
+  const int64_t n_occ = 2 * (int64_t)c->batch_size + (int64_t)(c->batch_size / c->chunk_size) * c->neg_k;
+  if (n_occ > 16384) { set_error("2B + (B/g)k must be <= 16384 (single-CTA dedup)"); return KGE_EINVAL; }
+  if (c->n_entities <= 0 || c->n_relations <= 0) { set_error("empty vocabulary"); return KGE_EINVAL; }
+  if (c->n_entities >= (1ll << 31) || c->n_relations >= (1ll << 31)) {
+    set_error("n_entities / n_relations must be < 2^31");
+    return KGE_ERANGE;
+  }
+  if (c->corrupt < 0 || c->corrupt > 2) { set_error("bad corrupt"); return KGE_EINVAL; }
+  if (c->neg_precision < 0 || c->neg_precision > 1) { set_error("bad neg_precision"); return KGE_EINVAL; }
+  if (c->lag != 0) { set_error("lag != 0 not implemented in this build"); return KGE_EUNSUPPORTED; }
+  if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size) { set_error("bad world_size/rank"); return KGE_EINVAL; }
+  if (c->world_size > 1) { set_error("world_size > 1 not implemented in this build"); return KGE_EUNSUPPORTED; }
+  if (c->model == KGE_TRANSR) { set_error("TransR not implemented in this build"); return KGE_EUNSUPPORTED; }
+  return KGE_OK;
+}
+
+static int alloc_slot(kge_handle* h, Slot& s) {
+  const Dims& d = h->dims;
+  const int n_occ = d.n_occ, B = d.B;
+  size_t n = (size_t)B * 4 + (size_t)d.C * d.k + d.C + 1 + (size_t)n_occ * 3 + (n_occ + 1) + 1 + (size_t)B * 3 + (B + 1);
+  int32_t* p = (int32_t*)dalloc(h, n * sizeof(int32_t));
+  if (!p) return KGE_ENOMEM;
+  s.pos = p; p += B;
+  s.ph = p; p += B;
+  s.pr = p; p += B;
+  s.pt = p; p += B;
+  s.neg = p; p += (size_t)d.C * d.k;
+  s.mode = p; p += d.C;
+  s.ent_n = p; p += 1;
+  s.ent_uniq = p; p += n_occ;
+  s.ent_inv = p; p += n_occ;
+  s.ent_off = p; p += n_occ + 1;
+  s.ent_occ = p; p += n_occ;
+  s.rel_n = p; p += 1;
+  s.rel_uniq = p; p += B;
+  s.rel_inv = p; p += B;
+  s.rel_off = p; p += B + 1;
+  s.rel_occ = p; p += B;
+  return KGE_OK;
+}
+
+static SampleParams sample_params(const kge_handle* h, bool given) {
+  SampleParams p{};
+  p.th = h->th;
+  p.tr = h->tr;
+  p.tt = h->tt;
+  p.list = h->list;
+  p.n_list = h->n_list;
+  if (given) {
+    p.given_h = h->given;
+    p.given_r = h->given + h->dims.B;
+    p.given_t = h->given + 2 * h->dims.B;
+  }
+  p.n_entities = h->dims.n_entities;
+  p.B = h->dims.B;
+  p.g = h->dims.g;
+  p.C = h->dims.C;
+  p.k = h->dims.k;
+  p.n_occ = h->dims.n_occ;
+  p.n_pad = h->n_pad;
+  p.k0 = h->k0;
+  p.k1 = h->k1;
+  p.corrupt = h->cfg.corrupt;
+  p.cg_base = (uint32_t)(h->cfg.rank * h->dims.C);
+  return p;
+}
+
+// device copy of the slot table: stored right after flags[4] in the same allocation (see kge_init)
+static Slot* d_slots(kge_handle* h) { return reinterpret_cast<Slot*>(h->buf.flags + 4); }
+
+}  // namespace kge
+
+using namespace kge;
+
+extern "C" {
+
+void kge_config_default(kge_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->abi_version = KGE_ABI_VERSION;
+  c->model = KGE_TRANSE_L2;
+  c->n_entities = 0;
+  c->n_relations = 0;
+  c->dim = 400;
+  c->batch_size = 1024;
+  c->chunk_size = 256;
+  c->neg_k = 256;
+  c->gamma = 12.0f;
+  c->lr = 0.1f;
+  c->adagrad_eps = 1e-10f;
+  c->init_bound = 0.0f;
+  c->seed = 1;
+  c->corrupt = KGE_CORRUPT_ALTERNATE;
+  c->neg_precision = KGE_PREC_TF32;
+  c->rotate_variant = 0;
+  c->lag = 0;
+  c->world_size = 1;
+  c->rank = 0;
+}
+
+const char* kge_last_error(void) { return g_err.c_str(); }
+
+const char* kge_kernel_name(int32_t id) {
+  static const char* names[] = {"k_sample", "k_gather", "k_neg_fwd", "k_neg_bwd", "k_chain", "k_update"};
+  return (id >= 0 && id < KGE_K_COUNT) ? names[id] : "?";
+}
+
+int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, const int64_t* rels, const int64_t* tails,
+             int64_t n_triples) {
+  if (!out) { set_error("out is NULL"); return KGE_EINVAL; }
+  *out = nullptr;
+  int rc = validate(cfg);
+  if (rc != KGE_OK) return rc;
+  if (!heads || !rels || !tails || n_triples <= 0) { set_error("no triples"); return KGE_EINVAL; }
+  if (n_triples >= (1ll << 31)) { set_error("n_triples must be < 2^31"); return KGE_ERANGE; }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device (this library has no CPU fallback)");
+    return KGE_ECUDA;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, dev);
+  if (prop.major != 10) {
+    set_error("libkge.so is built for sm_100a (B200); device is sm_" + std::to_string(prop.major * 10 + prop.minor));
+    return KGE_ECUDA;
+  }
+
+  kge_handle* h = new kge_handle();
+  h->cfg = *cfg;
+  if (h->cfg.adagrad_eps <= 0.f) h->cfg.adagrad_eps = 1e-10f;
+  h->device = dev;
+  Dims& dm = h->dims;
+  dm.model = cfg->model;
+  dm.variant = cfg->rotate_variant;
+  dm.family = family_of(cfg->model, cfg->rotate_variant);
+  dm.d = cfg->dim;
+  dm.drel = cfg->model == KGE_ROTATE ? cfg->dim / 2 : cfg->dim;
+  dm.B = cfg->batch_size;
+  dm.g = cfg->chunk_size;
+  dm.C = dm.B / dm.g;
+  dm.k = cfg->neg_k;
+  dm.n_occ = 2 * dm.B + dm.C * dm.k;
+  dm.gamma = cfg->gamma;
+  dm.lr = cfg->lr;
+  dm.eps = h->cfg.adagrad_eps;
+  dm.n_entities = cfg->n_entities;
+  dm.n_relations = cfg->n_relations;
+  h->k0 = (uint32_t)cfg->seed;
+  h->k1 = (uint32_t)(cfg->seed >> 32);
+  h->n_pad = 1;
+  while (h->n_pad < dm.n_occ) h->n_pad <<= 1;
+  h->ring = 64;
+  h->n_triples = n_triples;
+
+  auto fail = [&](int code) {
+    free_all(h);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return code;
+  };
+
+  if (cfg->cuda_stream) {
+    h->stream = (cudaStream_t)cfg->cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "stream"));
+    h->own_stream = true;
+  }
+
+  // ---- triples -> device int32 (checked) ----
+  h->th = (int32_t*)dalloc(h, n_triples * 4);
+  h->tr = (int32_t*)dalloc(h, n_triples * 4);
+  h->tt = (int32_t*)dalloc(h, n_triples * 4);
+  int32_t* d_bad = (int32_t*)dalloc(h, 16);
+  if (!h->th || !h->tr || !h->tt || !d_bad) { set_error("out of device memory (triples)"); return fail(KGE_ENOMEM); }
+  {
+    const int64_t chunk = 1 << 24;  // 16M ids (128 MB) staging
+    int64_t* stage = nullptr;
+    int64_t* d_stage = (int64_t*)dalloc(h, (size_t)std::min(chunk, n_triples) * 8);
+    if (!d_stage || cudaMallocHost(&stage, (size_t)std::min(chunk, n_triples) * 8) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("staging allocation failed");
+      return fail(KGE_ENOMEM);
+    }
+    if (cudaMemsetAsync(d_bad, 0, 16, h->stream) != cudaSuccess) { cudaFreeHost(stage); return fail(cuda_fail(cudaGetLastError(), "memset")); }
+    const int64_t* srcs[3] = {heads, rels, tails};
+    int32_t* dsts[3] = {h->th, h->tr, h->tt};
+    const int64_t lim[3] = {cfg->n_entities, cfg->n_relations, cfg->n_entities};
+    for (int a = 0; a < 3; ++a) {
+      for (int64_t b = 0; b < n_triples; b += chunk) {
+        const int64_t m = std::min(chunk, n_triples - b);
+        cudaStreamSynchronize(h->stream);  // staging buffer reuse
+        std::memcpy(stage, srcs[a] + b, (size_t)m * 8);
+        e = cudaMemcpyAsync(d_stage, stage, (size_t)m * 8, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess) e = launch_convert_ids(h, d_stage, dsts[a] + b, m, lim[a], d_bad);
+        if (e != cudaSuccess) { cudaFreeHost(stage); return fail(cuda_fail(e, "triple upload")); }
+      }
+    }
+    int32_t bad = 0;
+    e = cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFreeHost(stage);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "triple upload"));
+    if (bad) { set_error("triple id out of range"); return fail(KGE_ERANGE); }
+  }
+  h->list = nullptr;  // P = 1: identity list
+  h->n_list = n_triples;
+
+  // ---- tables ----
+  const int64_t Ne = cfg->n_entities, Nr = cfg->n_relations;
+  h->ent = (float*)dalloc(h, (size_t)Ne * dm.d * 4);
+  h->ent_st = (float*)dalloc(h, (size_t)Ne * 4);
+  h->rel = (float*)dalloc(h, (size_t)Nr * dm.drel * 4);
+  h->rel_st = (float*)dalloc(h, (size_t)Nr * 4);
+  if (!h->ent || !h->ent_st || !h->rel || !h->rel_st) { set_error("out of device memory (tables)"); return fail(KGE_ENOMEM); }
+  const float bound = cfg->init_bound > 0.f ? cfg->init_bound : default_bound(cfg->gamma, cfg->dim);
+  const float rbound = cfg->model == KGE_ROTATE ? (float)M_PI : bound;
+  e = launch_init_table(h, h->ent, Ne, dm.d, 0, bound);
+  if (e == cudaSuccess) e = launch_init_table(h, h->rel, Nr, dm.drel, 1, rbound);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->ent_st, 0, (size_t)Ne * 4, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->rel_st, 0, (size_t)Nr * 4, h->stream);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "table init"));
+
+  // ---- sample ring + debug slot ----
+  h->slots.resize(h->ring);
+  for (int i = 0; i < h->ring; ++i)
+    if (alloc_slot(h, h->slots[i]) != KGE_OK) { set_error("out of device memory (ring)"); return fail(KGE_ENOMEM); }
+  if (alloc_slot(h, h->debug_slot) != KGE_OK) return fail(KGE_ENOMEM);
+  h->given = (int32_t*)dalloc(h, (size_t)3 * dm.B * 4);
+  if (cudaMallocHost(&h->pinned_given, (size_t)3 * dm.B * 8) != cudaSuccess ||
+      cudaMallocHost(&h->pinned_loss, (size_t)h->ring * 4) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(KGE_ENOMEM);
+  }
+
+  // ---- step buffers ----
+  StepBuffers& b = h->buf;
+  const int64_t nneg = (int64_t)dm.C * dm.k;
+  h->n_neg_parts = dm.C * ((dm.g + 63) / 64) * ((dm.k + 63) / 64);
+  const int64_t tc_parts = (int64_t)dm.C * ((dm.g + 127) / 128) * 8;  // room for the TC epilogue partials
+  b.O = (float*)dalloc(h, (size_t)dm.B * dm.d * 4);
+  b.onorm = (float*)dalloc(h, (size_t)dm.B * 4);
+  b.X = (float*)dalloc(h, (size_t)nneg * dm.d * 4);
+  b.xnorm = (float*)dalloc(h, (size_t)nneg * 4);
+  b.W = (float*)dalloc(h, (size_t)dm.B * dm.k * 4);
+  b.wpos = (float*)dalloc(h, (size_t)dm.B * 4);
+  b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
+  b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(h->n_neg_parts, tc_parts) * 4);
+  b.rowsumW = (float*)dalloc(h, (size_t)dm.B * 4);
+  b.colsumW = (float*)dalloc(h, (size_t)nneg * 4);
+  b.dO = (float*)dalloc(h, (size_t)dm.B * dm.d * 4);
+  b.Gocc = (float*)dalloc(h, (size_t)dm.n_occ * dm.d * 4);
+  b.Grel = (float*)dalloc(h, (size_t)dm.B * dm.drel * 4);
+  b.loss = (float*)dalloc(h, (size_t)h->ring * 4);
+  b.flags = (int32_t*)dalloc(h, 16 + sizeof(Slot) * (h->ring + 1));  // flags[4] then the slot table
+  if (!b.O || !b.onorm || !b.X || !b.xnorm || !b.W || !b.wpos || !b.lpos || !b.lneg || !b.rowsumW || !b.colsumW ||
+      !b.dO || !b.Gocc || !b.Grel || !b.loss || !b.flags) {
+    set_error("out of device memory (workspace)");
+    return fail(KGE_ENOMEM);
+  }
+  e = cudaMemsetAsync(b.flags, 0, 16, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b.Gocc, 0, (size_t)dm.n_occ * dm.d * 4, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h), h->slots.data(), sizeof(Slot) * h->ring, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h) + h->ring, &h->debug_slot, sizeof(Slot), cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return fail(cuda_fail(e, "workspace init"));
+  *out = h;
+  return KGE_OK;
+}
+
+static int ensure_sampled(kge_handle* h, int64_t s) {
+  if (h->ring_first >= 0 && s >= h->ring_first && s < h->ring_first + h->ring) return KGE_OK;
+  SampleParams p = sample_params(h, false);
+  cudaError_t e = launch_sample(h, p, d_slots(h), s, h->ring);
+  if (e != cudaSuccess) return cuda_fail(e, "sample");
+  h->ring_first = s;
+  return KGE_OK;
+}
+
+static int check_flags(kge_handle* h) {
+  int32_t f[4];
+  cudaError_t e = cudaMemcpyAsync(f, h->buf.flags, 16, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sync");
+  if (f[0]) {
+    cudaMemsetAsync(h->buf.flags, 0, 4, h->stream);
+    set_error("a step produced a non-finite loss; its update was skipped");
+    return KGE_ENONFINITE;
+  }
+  return KGE_OK;
+}
+
+int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
+  if (!h) { set_error("NULL handle"); return KGE_EINVAL; }
+  if (n_steps < 0) { set_error("n_steps < 0"); return KGE_EINVAL; }
+  for (int64_t it = 0; it < n_steps; ++it) {
+    const int64_t s = h->step;
+    if (s >= (1ll << 32)) { set_error("step index exceeds 2^32 (one Philox counter word)"); return KGE_ERANGE; }
+    int rc = ensure_sampled(h, s);
+    if (rc != KGE_OK) return rc;
+    cudaError_t e = launch_step(h, h->slots[s % h->ring], s);
+    if (e != cudaSuccess) return cuda_fail(e, "step");
+    if (loss_out) {
+      e = cudaMemcpyAsync(h->pinned_loss + (it % h->ring), h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost, h->stream);
+      if (e != cudaSuccess) return cuda_fail(e, "loss readback");
+    }
+    h->step = s + 1;
+    if (loss_out && ((it + 1) % h->ring == 0 || it + 1 == n_steps)) {
+      e = cudaStreamSynchronize(h->stream);
+      if (e != cudaSuccess) return cuda_fail(e, "sync");
+      const int64_t first = it - (it % h->ring);
+      for (int64_t q = first; q <= it; ++q) loss_out[q] = h->pinned_loss[q % h->ring];
+    }
+  }
+  if (loss_out) return check_flags(h);
+  return KGE_OK;
+}
+
+int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails, float* loss_out) {
+  if (!h || !heads || !rels || !tails) { set_error("NULL argument"); return KGE_EINVAL; }
+  const int B = h->dims.B;
+  const int64_t s = h->step;
+  // host-side range check + int32 narrowing into pinned staging, then one H2D copy
+  int32_t* st = h->pinned_given;
+  cudaError_t e = cudaStreamSynchronize(h->stream);  // staging reuse
+  if (e != cudaSuccess) return cuda_fail(e, "sync");
+  for (int i = 0; i < B; ++i) {
+    if (heads[i] < 0 || heads[i] >= h->dims.n_entities || tails[i] < 0 || tails[i] >= h->dims.n_entities ||
+        rels[i] < 0 || rels[i] >= h->dims.n_relations) {
+      set_error("batch id out of range");
+      return KGE_ERANGE;
+    }
+    st[i] = (int32_t)heads[i];
+    st[B + i] = (int32_t)rels[i];
+    st[2 * B + i] = (int32_t)tails[i];
+  }
+  e = cudaMemcpyAsync(h->given, st, (size_t)3 * B * 4, cudaMemcpyHostToDevice, h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "batch upload");
+  // sample negatives + dedup for this step into the debug slot, from the given positives
+  SampleParams p = sample_params(h, true);
+  e = launch_sample(h, p, d_slots(h) + h->ring, s, 1);
+  if (e != cudaSuccess) return cuda_fail(e, "sample");
+  e = launch_step(h, h->debug_slot, s);
+  if (e != cudaSuccess) return cuda_fail(e, "step");
+  h->step = s + 1;
+  if (h->ring_first >= 0 && s >= h->ring_first && s < h->ring_first + h->ring) h->ring_first = -1;
+  if (loss_out) {
+    e = cudaMemcpyAsync(h->pinned_loss, h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "loss readback");
+    *loss_out = h->pinned_loss[0];
+    return check_flags(h);
+  }
+  return KGE_OK;
+}
+
+int kge_sample(kge_handle* h, int64_t step, int64_t* pos_idx, int64_t* neg, int8_t* mode, int64_t* uniq_ent,
+               int64_t* n_uniq_ent, int32_t* inv_ent, int64_t* uniq_rel, int64_t* n_uniq_rel, int32_t* inv_rel) {
+  if (!h) { set_error("NULL handle"); return KGE_EINVAL; }
+  if (step < 0 || step >= (1ll << 32)) { set_error("step out of range"); return KGE_ERANGE; }
+  SampleParams p = sample_params(h, false);
+  cudaError_t e = launch_sample(h, p, d_slots(h) + h->ring, step, 1);
+  if (e != cudaSuccess) return cuda_fail(e, "sample");
+  const Dims& d = h->dims;
+  const Slot& s = h->debug_slot;
+  std::vector<int32_t> pos(d.B), ng((size_t)d.C * d.k), md(d.C), ue(d.n_occ), ie(d.n_occ), ur(d.B), ir(d.B);
+  int32_t ne = 0, nr = 0;
+  e = cudaMemcpyAsync(pos.data(), s.pos, d.B * 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ng.data(), s.neg, ng.size() * 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(md.data(), s.mode, d.C * 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ue.data(), s.ent_uniq, d.n_occ * 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ie.data(), s.ent_inv, d.n_occ * 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ur.data(), s.rel_uniq, d.B * 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ir.data(), s.rel_inv, d.B * 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&ne, s.ent_n, 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&nr, s.rel_n, 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sample readback");
+  if (pos_idx) for (int i = 0; i < d.B; ++i) pos_idx[i] = pos[i];
+  if (neg) for (size_t i = 0; i < ng.size(); ++i) neg[i] = ng[i];
+  if (mode) for (int i = 0; i < d.C; ++i) mode[i] = (int8_t)md[i];
+  if (uniq_ent) for (int i = 0; i < ne; ++i) uniq_ent[i] = ue[i];
+  if (n_uniq_ent) *n_uniq_ent = ne;
+  if (inv_ent) std::memcpy(inv_ent, ie.data(), ie.size() * 4);
+  if (uniq_rel) for (int i = 0; i < nr; ++i) uniq_rel[i] = ur[i];
+  if (n_uniq_rel) *n_uniq_rel = nr;
+  if (inv_rel) std::memcpy(inv_rel, ir.data(), ir.size() * 4);
+  return KGE_OK;
+}
+
+static float* table_ptr(kge_handle* h, int32_t table, int32_t* w, int64_t* rows) {
+  const Dims& d = h->dims;
+  switch (table) {
+    case 0: *w = d.d; *rows = d.n_entities; return h->ent;
+    case 1: *w = d.drel; *rows = d.n_relations; return h->rel;
+    case 2: *w = d.d * d.d; *rows = d.n_relations; return h->proj;
+    case 3: *w = 1; *rows = d.n_entities; return h->ent_st;
+    case 4: *w = 1; *rows = d.n_relations; return h->rel_st;
+    case 5: *w = 1; *rows = d.n_relations; return h->proj_st;
+  }
+  return nullptr;
+}
+
+int32_t kge_table_width(const kge_handle* h, int32_t table) {
+  if (!h) return 0;
+  int32_t w = 0;
+  int64_t rows = 0;
+  float* p = table_ptr(const_cast<kge_handle*>(h), table, &w, &rows);
+  return p ? w : 0;
+}
+
+static int rows_io(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, float* host, bool write) {
+  if (!h || (n > 0 && (!ids || !host))) { set_error("NULL argument"); return KGE_EINVAL; }
+  int32_t w;
+  int64_t rows;
+  float* tab = table_ptr(h, table, &w, &rows);
+  if (!tab) { set_error("table not present for this model"); return KGE_EINVAL; }
+  if (n == 0) return KGE_OK;
+  std::vector<int32_t> ids32(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= rows) { set_error("row id out of range"); return KGE_ERANGE; }
+    ids32[i] = (int32_t)ids[i];
+  }
+  int32_t* d_ids = nullptr;
+  float* d_buf = nullptr;
+  CK(cudaMallocAsync((void**)&d_ids, n * 4, h->stream));
+  CK(cudaMallocAsync((void**)&d_buf, (size_t)n * w * 4, h->stream));
+  CK(cudaMemcpyAsync(d_ids, ids32.data(), n * 4, cudaMemcpyHostToDevice, h->stream));
+  if (write) CK(cudaMemcpyAsync(d_buf, host, (size_t)n * w * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(launch_rows(h, tab, w, d_ids, n, d_buf, write));
+  if (!write) CK(cudaMemcpyAsync(host, d_buf, (size_t)n * w * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaFreeAsync(d_ids, h->stream));
+  CK(cudaFreeAsync(d_buf, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return KGE_OK;
+}
+
+int kge_get_rows(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, float* out) {
+  return rows_io(h, table, ids, n, out, false);
+}
+int kge_set_rows(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, const float* in) {
+  return rows_io(h, table, ids, n, const_cast<float*>(in), true);
+}
+
+int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, float* out) {
+  if (!h || (n > 0 && (!hs || !rs || !ts || !out))) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (n == 0) return KGE_OK;
+  std::vector<int32_t> ids((size_t)3 * n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (hs[i] < 0 || hs[i] >= h->dims.n_entities || ts[i] < 0 || ts[i] >= h->dims.n_entities || rs[i] < 0 ||
+        rs[i] >= h->dims.n_relations) {
+      set_error("triple id out of range");
+      return KGE_ERANGE;
+    }
+    ids[i] = (int32_t)hs[i];
+    ids[n + i] = (int32_t)rs[i];
+    ids[2 * n + i] = (int32_t)ts[i];
+  }
+  int32_t* d_ids = nullptr;
+  float* d_out = nullptr;
+  CK(cudaMallocAsync((void**)&d_ids, (size_t)3 * n * 4, h->stream));
+  CK(cudaMallocAsync((void**)&d_out, (size_t)n * 4, h->stream));
+  CK(cudaMemcpyAsync(d_ids, ids.data(), (size_t)3 * n * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(launch_score(h, d_ids, d_ids + n, d_ids + 2 * n, n, d_out));
+  CK(cudaMemcpyAsync(out, d_out, (size_t)n * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaFreeAsync(d_ids, h->stream));
+  CK(cudaFreeAsync(d_out, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return KGE_OK;
+}
+
+int64_t kge_step(const kge_handle* h) { return h ? h->step : -1; }
+
+int kge_set_step(kge_handle* h, int64_t step) {
+  if (!h || step < 0) { set_error("bad argument"); return KGE_EINVAL; }
+  h->step = step;
+  return KGE_OK;
+}
+
+int kge_sync(kge_handle* h) {
+  if (!h) { set_error("NULL handle"); return KGE_EINVAL; }
+  return check_flags(h);
+}
+
+int kge_profile_begin(kge_handle* h) {
+  if (!h) { set_error("NULL handle"); return KGE_EINVAL; }
+  h->prof.on = true;
+  h->prof.used = 0;
+  h->prof.kid.clear();
+  return KGE_OK;
+}
+
+int kge_profile_end(kge_handle* h, int32_t n_kernels, double* avg_ms, int64_t* launches) {
+  if (!h || !h->prof.on) { set_error("profiling not active"); return KGE_ESTATE; }
+  h->prof.on = false;
+  CK(cudaStreamSynchronize(h->stream));
+  std::vector<double> sum(KGE_K_COUNT, 0.0);
+  std::vector<int64_t> cnt(KGE_K_COUNT, 0);
+  for (size_t p = 0; p < h->prof.kid.size(); ++p) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->prof.ev[2 * p], h->prof.ev[2 * p + 1]));
+    sum[h->prof.kid[p]] += ms;
+    cnt[h->prof.kid[p]] += 1;
+  }
+  for (int k = 0; k < n_kernels && k < KGE_K_COUNT; ++k) {
+    if (avg_ms) avg_ms[k] = cnt[k] ? sum[k] / cnt[k] : 0.0;
+    if (launches) launches[k] = cnt[k];
+  }
+  return KGE_OK;
+}
+
+int64_t kge_launch_count(const kge_handle* h) { return h ? h->launches : 0; }
+
+void kge_destroy(kge_handle* h) {
+  if (!h) return;
+  free_all(h);
+  for (cudaEvent_t ev : h->prof.ev)
+    if (ev) cudaEventDestroy(ev);
+  if (h->pinned_given) cudaFreeHost(h->pinned_given);
+  if (h->pinned_loss) cudaFreeHost(h->pinned_loss);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+}  // extern "C"

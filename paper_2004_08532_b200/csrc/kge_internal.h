@@ -1,0 +1,163 @@
+// kge_internal.h -- host-side state of a kge_handle and the launchers each .cu file exports.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/kge.h"
+
+namespace kge {
+
+enum Family : int32_t {  // pair-score family of the chunked negative contraction
+  FAM_DOT = 0,   // DistMult, ComplEx: f = o . x
+  FAM_L2 = 1,    // TransE-L2: f = gamma - sqrt(sum (o-x)^2)
+  FAM_L2SQ = 2,  // RotatE (Table 1, squared), TransR: f = gamma - sum (o-x)^2
+  FAM_L1 = 3,    // TransE-L1: f = gamma - sum |o-x|
+  FAM_CMOD = 4   // RotatE modulus variant: f = gamma - sum_c |z_c|
+};
+
+inline Family family_of(int model, int rotate_variant) {
+  switch (model) {
+    case KGE_TRANSE_L1: return FAM_L1;
+    case KGE_TRANSE_L2: return FAM_L2;
+    case KGE_DISTMULT:
+    case KGE_COMPLEX: return FAM_DOT;
+    case KGE_ROTATE: return rotate_variant ? FAM_CMOD : FAM_L2SQ;
+    default: return FAM_L2SQ;
+  }
+}
+
+// Per-step sample slot (device pointers into one ring allocation).
+struct Slot {
+  int32_t* pos;      // [B] triple index
+  int32_t* ph;       // [B]
+  int32_t* pr;       // [B]
+  int32_t* pt;       // [B]
+  int32_t* neg;      // [C*k]
+  int32_t* mode;     // [C]
+  int32_t* ent_n;    // [1] number of unique entities
+  int32_t* ent_uniq; // [n_occ]
+  int32_t* ent_inv;  // [n_occ]
+  int32_t* ent_off;  // [n_occ + 1]
+  int32_t* ent_occ;  // [n_occ] occurrences sorted by (id, occ)
+  int32_t* rel_n;    // [1]
+  int32_t* rel_uniq; // [B]
+  int32_t* rel_inv;  // [B]
+  int32_t* rel_off;  // [B + 1]
+  int32_t* rel_occ;  // [B]
+};
+
+struct SampleParams {
+  const int32_t* th;
+  const int32_t* tr;
+  const int32_t* tt;
+  const int32_t* list;   // rank's triple list, or nullptr for identity
+  int64_t n_list;
+  const int32_t* given_h;  // caller-supplied positives (kge_train_batch), or nullptr
+  const int32_t* given_r;
+  const int32_t* given_t;
+  int64_t n_entities;
+  int32_t B, g, C, k, n_occ, n_pad;  // n_pad: power of two >= n_occ
+  uint32_t k0, k1;
+  int32_t corrupt;
+  uint32_t cg_base;  // rank * C
+};
+
+struct StepBuffers {
+  float* O;        // [B x d] combined o_i
+  float* onorm;    // [B] ||o_i||^2 (TC L2 path)
+  float* X;        // [C*k x d] gathered negative rows
+  float* xnorm;    // [C*k]
+  float* W;        // [B x k] dL/dS coefficient (C chunks of g x k)
+  float* wpos;     // [B] dL/df+
+  float* lpos;     // [B] per-positive loss term
+  float* lneg;     // [n_neg_parts] per-tile negative loss partials
+  float* rowsumW;  // [B]
+  float* colsumW;  // [C*k]
+  float* dO;       // [B x d]
+  float* Gocc;     // [n_occ x d] per-occurrence entity gradients
+  float* Grel;     // [B x d_r]
+  float* Gproj;    // [B x d*d] (TransR)
+  float* loss;     // [ring] per-step loss
+  int32_t* flags;  // [4]: [0] non-finite seen
+};
+
+struct Dims {
+  int32_t model, family, variant;
+  int32_t d, drel, B, g, C, k, n_occ;
+  float gamma, lr, eps;
+  int64_t n_entities, n_relations;
+};
+
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;  // pairs
+  std::vector<int32_t> kid;
+  size_t used = 0;
+};
+
+}  // namespace kge
+
+struct kge_handle {
+  kge_config cfg{};
+  kge::Dims dims{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // tables
+  float* ent = nullptr;
+  float* rel = nullptr;
+  float* proj = nullptr;
+  float* ent_st = nullptr;
+  float* rel_st = nullptr;
+  float* proj_st = nullptr;
+  // graph
+  int32_t* th = nullptr;
+  int32_t* tr = nullptr;
+  int32_t* tt = nullptr;
+  int32_t* list = nullptr;
+  int64_t n_triples = 0, n_list = 0;
+  // sampling ring
+  int32_t ring = 0;
+  int64_t ring_first = -1;  // steps [ring_first, ring_first + ring) are in the ring
+  std::vector<kge::Slot> slots;
+  kge::Slot debug_slot{};
+  int32_t* given = nullptr;  // [3 x B] device copy of caller positives
+  int32_t* pinned_given = nullptr;  // host pinned staging
+  float* pinned_loss = nullptr;
+  // step
+  kge::StepBuffers buf{};
+  int32_t n_neg_parts = 0;
+  int64_t step = 0;
+  int64_t launches = 0;
+  kge::Profiler prof;
+  std::vector<void*> allocs;
+  // sizes
+  uint32_t k0 = 0, k1 = 0;
+  int32_t n_pad = 0;
+  size_t sample_smem = 0;
+};
+
+namespace kge {
+
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+// launch bracketing for the profiler / launch counter
+void launch_begin(kge_handle* h, int kid);
+void launch_end(kge_handle* h, int kid);
+
+// sample.cu
+size_t sample_smem_bytes(int n_pad);
+cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev_array, int64_t step0, int n_steps);
+cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound);
+cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, int64_t n, int64_t limit, int32_t* bad);
+
+// step.cu
+cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step);
+cudaError_t launch_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, float* out);
+cudaError_t launch_rows(kge_handle* h, float* tab, int32_t w, const int32_t* ids, int64_t n, float* buf, bool write);
+
+}  // namespace kge

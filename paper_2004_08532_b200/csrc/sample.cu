@@ -1,0 +1,219 @@
+// sample.cu -- step (1) of the mini-batch loop (Sec. 3.1) on the device:
+//   positives by a keyed Feistel permutation per epoch (reading c.2), joint negatives (reading
+//   c.3), head/tail schedule (reading c.4), and the dedup of the rows the step touches (sort + segment, reading c.5)
+//   -- all integer work, bit-exact with the oracle. Plus the table-init (reading c.6) and id-conversion kernels.
+//
+// Design (B200): sampling depends only on (seed, step), so one launch samples a whole window of steps ahead of the
+// compute (grid.x = steps, grid.y = {entity, relation} dedup). Each CTA sorts its step's (id<<32 | occurrence) keys
+// with an in-shared-memory bitonic network (n <= 16384 keys, one CTA, no global atomics), then a block scan turns
+// the sorted run boundaries into unique ids, inverse map and segment offsets.
+#include <cstdio>
+
+#include "device_common.cuh"
+#include "kge_internal.h"
+
+namespace kge {
+
+constexpr int kSampleThreads = 1024;
+
+struct SampleArgs {
+  SampleParams p;
+  uint32_t fe_half;
+  const Slot* slots;  // device array [ring]
+  int32_t ring;
+  int64_t step0;
+};
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int nw = blockDim.x >> 5;
+    int t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) warp_tot[lane] = t;  // inclusive
+    if (lane == 31) *total = t;
+  }
+  __syncthreads();
+  const int base = wid ? warp_tot[wid - 1] : 0;
+  return base + x - v;
+}
+
+__global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
+  extern __shared__ unsigned long long keys[];
+  __shared__ int warp_tot[32];
+  __shared__ int total;
+  const SampleParams& p = a.p;
+  const int64_t s = a.step0 + blockIdx.x;
+  const Slot slot = a.slots[s % a.ring];
+  const bool ent_side = blockIdx.y == 0;
+  const int tid = threadIdx.x;
+  const int n = ent_side ? p.n_occ : p.B;
+  const FeistelDomain dom{a.fe_half, (uint64_t)p.n_list};
+
+  for (int i = tid; i < p.B; i += blockDim.x) {
+    int32_t trip = -1, hv, rv, tv;
+    if (p.given_h) {
+      hv = p.given_h[i];
+      rv = p.given_r[i];
+      tv = p.given_t[i];
+    } else {
+      const uint64_t q = (uint64_t)s * (uint64_t)p.B + (uint64_t)i;
+      const uint32_t epoch = (uint32_t)(q / (uint64_t)p.n_list);
+      const uint64_t pp = q % (uint64_t)p.n_list;
+      const uint64_t idx = feistel_index(dom, p.k0, p.k1, epoch, pp);
+      trip = p.list ? p.list[idx] : (int32_t)idx;
+      hv = p.th[trip];
+      rv = p.tr[trip];
+      tv = p.tt[trip];
+    }
+    if (ent_side) {
+      slot.pos[i] = trip;
+      slot.ph[i] = hv;
+      slot.pr[i] = rv;
+      slot.pt[i] = tv;
+      keys[i] = ((unsigned long long)(uint32_t)hv << 32) | (uint32_t)i;
+      keys[p.B + i] = ((unsigned long long)(uint32_t)tv << 32) | (uint32_t)(p.B + i);
+    } else {
+      keys[i] = ((unsigned long long)(uint32_t)rv << 32) | (uint32_t)i;
+    }
+  }
+  if (ent_side) {
+    const int nneg = p.C * p.k;
+    for (int q = tid; q < nneg; q += blockDim.x) {
+      const int c = q / p.k, j = q - c * p.k;
+      const uint32_t id = neg_entity(p.k0, p.k1, (uint64_t)p.n_entities, (uint32_t)s, p.cg_base + c, (uint32_t)j);
+      slot.neg[q] = (int32_t)id;
+      keys[2 * p.B + q] = ((unsigned long long)id << 32) | (uint32_t)(2 * p.B + q);
+    }
+    for (int c = tid; c < p.C; c += blockDim.x) slot.mode[c] = corrupt_mode(p.corrupt, (uint32_t)s, p.cg_base + c);
+  }
+  // pad to a power of two
+  int np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  for (int q = n + tid; q < np2; q += blockDim.x) keys[q] = ~0ull;
+  __syncthreads();
+
+  // bitonic sort, ascending
+  for (int kk = 2; kk <= np2; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (np2 >> 1); t += blockDim.x) {
+        const int lo = (t / j) * 2 * j + (t % j);
+        const int hi = lo + j;
+        const bool up = (lo & kk) == 0;
+        const unsigned long long x = keys[lo], y = keys[hi];
+        if ((x > y) == up) {
+          keys[lo] = y;
+          keys[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // run boundaries -> unique ids, inverse map, segments (reading c.5)
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
+  int cnt = 0;
+  for (int q = b0; q < b1; ++q)
+    if (q == 0 || (keys[q] >> 32) != (keys[q - 1] >> 32)) ++cnt;
+  int uid = block_exclusive_scan(cnt, warp_tot, &total) - 1;
+  int32_t* uniq = ent_side ? slot.ent_uniq : slot.rel_uniq;
+  int32_t* inv = ent_side ? slot.ent_inv : slot.rel_inv;
+  int32_t* off = ent_side ? slot.ent_off : slot.rel_off;
+  int32_t* occ = ent_side ? slot.ent_occ : slot.rel_occ;
+  for (int q = b0; q < b1; ++q) {
+    const unsigned long long kv = keys[q];
+    if (q == 0 || (kv >> 32) != (keys[q - 1] >> 32)) {
+      ++uid;
+      uniq[uid] = (int32_t)(kv >> 32);
+      off[uid] = q;
+    }
+    const int32_t o = (int32_t)(kv & 0xffffffffu);
+    occ[q] = o;
+    inv[o] = uid;
+  }
+  if (tid == 0) {
+    off[total] = n;
+    if (ent_side)
+      *slot.ent_n = total;
+    else
+      *slot.rel_n = total;
+  }
+}
+
+size_t sample_smem_bytes(int n_pad) { return (size_t)n_pad * sizeof(unsigned long long); }
+
+cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev, int64_t step0, int n_steps) {
+  SampleArgs a;
+  a.p = p;
+  a.fe_half = make_feistel_domain((uint64_t)p.n_list).half;
+  a.slots = slots_dev;
+  a.ring = slots_dev == nullptr ? 1 : h->ring;
+  a.step0 = step0;
+  size_t smem = sample_smem_bytes(p.n_pad);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  launch_begin(h, KGE_K_SAMPLE);
+  k_sample<<<dim3(n_steps, 2), kSampleThreads, smem, h->stream>>>(a);
+  launch_end(h, KGE_K_SAMPLE);
+  return cudaGetLastError();
+}
+
+// ---- table init (reading c.6) ----
+__global__ void k_init_table(float* __restrict__ tab, int64_t n_elem, int32_t w, uint32_t k0, uint32_t k1,
+                             uint32_t table_id, float bound) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_elem; i += stride) {
+    const uint64_t row = (uint64_t)(i / w);
+    const uint32_t col = (uint32_t)(i - (int64_t)row * w);
+    tab[i] = init_value(k0, k1, table_id, row, col, bound);
+  }
+}
+
+cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound) {
+  const int64_t n = rows * (int64_t)w;
+  if (n == 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 64);
+  k_init_table<<<blocks, 256, 0, h->stream>>>(tab, n, w, h->k0, h->k1, table_id, bound);
+  ++h->launches;
+  return cudaGetLastError();
+}
+
+__global__ void k_convert_ids(const int64_t* __restrict__ src, int32_t* __restrict__ dst, int64_t n, int64_t limit,
+                              int32_t* bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t v = src[i];
+    if (v < 0 || v >= limit) {
+      atomicOr(bad, 1);
+      dst[i] = 0;
+    } else {
+      dst[i] = (int32_t)v;
+    }
+  }
+}
+
+cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, int64_t n, int64_t limit, int32_t* bad) {
+  if (n == 0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 32);
+  k_convert_ids<<<blocks, 256, 0, h->stream>>>(src, dst, n, limit, bad);
+  ++h->launches;
+  return cudaGetLastError();
+}
+
+}  // namespace kge

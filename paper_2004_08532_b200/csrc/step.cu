@@ -1,0 +1,832 @@
+// step.cu -- steps (2)-(4) of the mini-batch loop (Sec. 3.1) on the device, FP32 path.
+//
+//   k_gather     : per positive i, o_i = combine(h_i, r_i) (tail) / combine'(r_i, t_i) (head) -- "o is computed as
+//                  before because there are only b pairs" -- and f+_i = pair(o_i, t_i | h_i);
+//                  per negative slot, the gathered row x'_j. One warp per row, 128-bit coalesced row access.
+//   k_neg_fwd    : per chunk, S = pair(O_c, X'_c) for all g x k pairs ("converted into a
+//                  generalized matrix multiplication"), shared-memory tiled, 4x4 register micro-tiles, FFMA;
+//                  fused epilogue: f-, logistic loss and dL/dS.
+//   k_neg_bwd    : dO = sum_j W_ij dpair/do, dX' = sum_i W_ij dpair/dx' (the transpose contractions), same tiling.
+//   k_chain      : per positive: positive-score gradient + chain rule of dO through combine -> per-occurrence grads;
+//                  one extra CTA reduces the loss in a fixed order (deterministic) and flags non-finite steps.
+//   k_update     : per unique row: segmented sum of its occurrence gradients in sorted-occurrence order (no float
+//                  atomics) fused with the sparse row-wise Adagrad update (reading c.11).
+// The tensor-core variant of k_neg_fwd / k_neg_bwd for the GEMM-shaped families lives in tc.cu.
+#include <algorithm>
+
+#include "device_common.cuh"
+#include "kge_internal.h"
+
+namespace kge {
+
+// ------------------------------------------------------------------------------------------------
+// row helpers (one warp per row, float4 lanes)
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ float4 ld4(const float* p, int v) { return reinterpret_cast<const float4*>(p)[v]; }
+__device__ __forceinline__ void st4(float* p, int v, float4 x) { reinterpret_cast<float4*>(p)[v] = x; }
+
+#define F4MAP(out, a, b, expr)            \
+  do {                                    \
+    { float A = a.x, Bv = b.x; out.x = expr; } \
+    { float A = a.y, Bv = b.y; out.y = expr; } \
+    { float A = a.z, Bv = b.z; out.z = expr; } \
+    { float A = a.w, Bv = b.w; out.w = expr; } \
+  } while (0)
+
+__device__ __forceinline__ bool is_complex_model(int model) { return model == KGE_COMPLEX || model == KGE_ROTATE; }
+
+// o = combine(h, r) (mode 0, tail corruption) or combine'(r, t) (mode 1, head corruption); reading c.8 table.
+__device__ void combine_row(int model, int mode, const float* __restrict__ h, const float* __restrict__ r,
+                            const float* __restrict__ t, float* __restrict__ o, int d, int lane) {
+  if (!is_complex_model(model)) {
+    const int d4 = d >> 2;
+    for (int v = lane; v < d4; v += 32) {
+      const float4 rv = ld4(r, v);
+      float4 ov;
+      if (model == KGE_DISTMULT) {
+        const float4 xv = mode == 0 ? ld4(h, v) : ld4(t, v);
+        F4MAP(ov, xv, rv, A * Bv);
+      } else {  // TransE: h + r | t - r
+        if (mode == 0) {
+          const float4 hv = ld4(h, v);
+          F4MAP(ov, hv, rv, A + Bv);
+        } else {
+          const float4 tv = ld4(t, v);
+          F4MAP(ov, tv, rv, A - Bv);
+        }
+      }
+      st4(o, v, ov);
+    }
+    return;
+  }
+  const int n4 = d >> 3;
+  for (int v = lane; v < n4; v += 32) {
+    const float4 xr = mode == 0 ? ld4(h, v) : ld4(t, v);
+    const float4 xi = mode == 0 ? ld4(h, v + n4) : ld4(t, v + n4);
+    float4 orr, oi;
+    float cr[4], ci[4];
+    if (model == KGE_COMPLEX) {
+      const float4 rr = ld4(r, v), ri = ld4(r, v + n4);
+      cr[0] = rr.x; cr[1] = rr.y; cr[2] = rr.z; cr[3] = rr.w;
+      ci[0] = ri.x; ci[1] = ri.y; ci[2] = ri.z; ci[3] = ri.w;
+    } else {  // RotatE: r = e^{i theta}; head mode uses e^{-i theta}
+      const float4 th = ld4(r, v);
+      const float tt[4] = {th.x, th.y, th.z, th.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sincosf(tt[u], &ci[u], &cr[u]);
+    }
+    const float a[4] = {xr.x, xr.y, xr.z, xr.w}, b[4] = {xi.x, xi.y, xi.z, xi.w};
+    float outr[4], outi[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (model == KGE_COMPLEX) {
+        if (mode == 0) {  // h * r
+          outr[u] = a[u] * cr[u] - b[u] * ci[u];
+          outi[u] = a[u] * ci[u] + b[u] * cr[u];
+        } else {  // conj-side: [rr tr + ri ti | rr ti - ri tr]
+          outr[u] = cr[u] * a[u] + ci[u] * b[u];
+          outi[u] = cr[u] * b[u] - ci[u] * a[u];
+        }
+      } else {
+        if (mode == 0) {  // h e^{i theta}
+          outr[u] = a[u] * cr[u] - b[u] * ci[u];
+          outi[u] = a[u] * ci[u] + b[u] * cr[u];
+        } else {  // t e^{-i theta}
+          outr[u] = a[u] * cr[u] + b[u] * ci[u];
+          outi[u] = -a[u] * ci[u] + b[u] * cr[u];
+        }
+      }
+    }
+    orr = make_float4(outr[0], outr[1], outr[2], outr[3]);
+    oi = make_float4(outi[0], outi[1], outi[2], outi[3]);
+    st4(o, v, orr);
+    st4(o, v + n4, oi);
+  }
+}
+
+// per-lane partial of the pair statistic: DOT sum o.x ; L2/L2SQ sum (o-x)^2 ; L1 sum |o-x| ; CMOD sum |z_c|
+__device__ float pair_partial(int fam, const float* __restrict__ o, const float* __restrict__ x, int d, int lane) {
+  float acc = 0.f;
+  if (fam == FAM_CMOD) {
+    const int n4 = d >> 3;
+    for (int v = lane; v < n4; v += 32) {
+      const float4 orr = ld4(o, v), oi = ld4(o, v + n4), xr = ld4(x, v), xi = ld4(x, v + n4);
+      float4 ur, ui;
+      F4MAP(ur, orr, xr, A - Bv);
+      F4MAP(ui, oi, xi, A - Bv);
+      acc += sqrtf(ur.x * ur.x + ui.x * ui.x) + sqrtf(ur.y * ur.y + ui.y * ui.y) +
+             sqrtf(ur.z * ur.z + ui.z * ui.z) + sqrtf(ur.w * ur.w + ui.w * ui.w);
+    }
+    return acc;
+  }
+  const int d4 = d >> 2;
+  for (int v = lane; v < d4; v += 32) {
+    const float4 ov = ld4(o, v), xv = ld4(x, v);
+    if (fam == FAM_DOT) {
+      acc += ov.x * xv.x + ov.y * xv.y + ov.z * xv.z + ov.w * xv.w;
+    } else if (fam == FAM_L1) {
+      acc += fabsf(ov.x - xv.x) + fabsf(ov.y - xv.y) + fabsf(ov.z - xv.z) + fabsf(ov.w - xv.w);
+    } else {
+      float4 u;
+      F4MAP(u, ov, xv, A - Bv);
+      acc += u.x * u.x + u.y * u.y + u.z * u.z + u.w * u.w;
+    }
+  }
+  return acc;
+}
+
+// f from the pair statistic (Table 1 + margin, reading Q7)
+__device__ __forceinline__ float pair_score_from(int fam, float stat, float gamma) {
+  switch (fam) {
+    case FAM_DOT: return stat;
+    case FAM_L2: return gamma - sqrtf(stat);
+    default: return gamma - stat;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_gather: positives (o, f+, dL/df+) and negative rows
+// ------------------------------------------------------------------------------------------------
+struct GatherArgs {
+  Dims dm;
+  Slot s;
+  const float* ent;
+  const float* rel;
+  StepBuffers b;
+};
+
+__global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
+  const Dims& dm = a.dm;
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int n_neg = dm.C * dm.k;
+  if (row < dm.B) {
+    const int i = row, mode = a.s.mode[i / dm.g];
+    const float* h = a.ent + (int64_t)a.s.ph[i] * dm.d;
+    const float* t = a.ent + (int64_t)a.s.pt[i] * dm.d;
+    const float* r = a.rel + (int64_t)a.s.pr[i] * dm.drel;
+    float* o = a.b.O + (int64_t)i * dm.d;
+    combine_row(dm.model, mode, h, r, t, o, dm.d, lane);
+    __syncwarp();
+    const float* other = mode == 0 ? t : h;
+    const float stat = warp_sum(pair_partial(dm.family, o, other, dm.d, lane));
+    const float on = warp_sum(pair_partial(FAM_DOT, o, o, dm.d, lane));
+    if (lane == 0) {
+      const float f = pair_score_from(dm.family, stat, dm.gamma);
+      a.b.wpos[i] = -sigmoid(-f) / (float)dm.B;  // dL/df+ (reading c.9)
+      a.b.lpos[i] = -log_sigmoid(f);
+      a.b.onorm[i] = on;
+    }
+  } else if (row < dm.B + n_neg) {
+    const int q = row - dm.B;
+    const float* x = a.ent + (int64_t)a.s.neg[q] * dm.d;
+    float* X = a.b.X + (int64_t)q * dm.d;
+    float acc = 0.f;
+    for (int v = lane; v < (dm.d >> 2); v += 32) {
+      const float4 xv = ld4(x, v);
+      st4(X, v, xv);
+      acc += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) a.b.xnorm[q] = acc;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_neg_fwd (FFMA): S_c = pair(O_c, X'_c), 64x64 tiles, K-chunks of 32 floats, 4x4 micro-tiles
+// ------------------------------------------------------------------------------------------------
+constexpr int TM = 64, TN = 64, TK = 32, TPAD = 4;
+
+struct NegArgs {
+  Dims dm;
+  StepBuffers b;
+  float* Gocc;  // dX' destination (occurrence rows 2B + q)
+};
+
+// Load a [64 rows x 32 k] tile of a row-major [rows x d] matrix, transposed into smem T[k][row].
+// CMOD: k-chunk = 16 real parts from column kc and 16 imaginary parts from column d/2 + kc.
+template <bool CPLX>
+__device__ __forceinline__ void load_tile_T(float (*T)[TM + TPAD], const float* __restrict__ base, int row0,
+                                            int nrows, int kc, int d) {
+  // 64 rows x 8 float4 = 512 float4 per tile; 256 threads x 2
+  for (int idx = threadIdx.x; idx < TM * (TK / 4); idx += blockDim.x) {
+    const int r = idx / (TK / 4), v = idx % (TK / 4);
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    int col;
+    if (CPLX) {
+      const int half = d >> 1;
+      const int cc = kc + (v & 3) * 4;  // complex index
+      col = (v < 4) ? cc : half + cc;
+      if (row0 + r < nrows && cc < half) x = *reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * d + col);
+    } else {
+      col = kc + v * 4;
+      if (row0 + r < nrows && col < d) x = *reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * d + col);
+    }
+    T[v * 4 + 0][r] = x.x;
+    T[v * 4 + 1][r] = x.y;
+    T[v * 4 + 2][r] = x.z;
+    T[v * 4 + 3][r] = x.w;
+  }
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(256) k_neg_fwd(NegArgs a) {
+  constexpr bool CPLX = FAM == FAM_CMOD;
+  const Dims& dm = a.dm;
+  __shared__ __align__(16) float As[TK][TM + TPAD];
+  __shared__ __align__(16) float Bs[TK][TN + TPAD];
+  __shared__ float red[8];
+  const int c = blockIdx.z, i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const float* Oc = a.b.O + (int64_t)c * dm.g * dm.d;
+  const float* Xc = a.b.X + (int64_t)c * dm.k * dm.d;
+  float acc[4][4] = {};
+  const int kend = CPLX ? (dm.d >> 1) : dm.d;
+  const int kstep = CPLX ? TK / 2 : TK;
+  for (int kc = 0; kc < kend; kc += kstep) {
+    load_tile_T<CPLX>(As, Oc, i0, dm.g, kc, dm.d);
+    load_tile_T<CPLX>(Bs, Xc, j0, dm.k, kc, dm.d);
+    __syncthreads();
+    if (CPLX) {
+#pragma unroll 4
+      for (int e = 0; e < TK / 2; ++e) {
+        const float4 ar = *reinterpret_cast<const float4*>(&As[e][ty * 4]);
+        const float4 ai = *reinterpret_cast<const float4*>(&As[e + TK / 2][ty * 4]);
+        const float4 br = *reinterpret_cast<const float4*>(&Bs[e][tx * 4]);
+        const float4 bi = *reinterpret_cast<const float4*>(&Bs[e + TK / 2][tx * 4]);
+        const float arr[4] = {ar.x, ar.y, ar.z, ar.w}, aii[4] = {ai.x, ai.y, ai.z, ai.w};
+        const float brr[4] = {br.x, br.y, br.z, br.w}, bii[4] = {bi.x, bi.y, bi.z, bi.w};
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const float ur = arr[ii] - brr[jj], ui = aii[ii] - bii[jj];
+            acc[ii][jj] += sqrtf(ur * ur + ui * ui);
+          }
+      }
+    } else {
+#pragma unroll 8
+      for (int e = 0; e < TK; ++e) {
+        const float4 av = *reinterpret_cast<const float4*>(&As[e][ty * 4]);
+        const float4 bv = *reinterpret_cast<const float4*>(&Bs[e][tx * 4]);
+        const float ar[4] = {av.x, av.y, av.z, av.w}, br[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            if (FAM == FAM_DOT) {
+              acc[ii][jj] = fmaf(ar[ii], br[jj], acc[ii][jj]);
+            } else if (FAM == FAM_L1) {
+              acc[ii][jj] += fabsf(ar[ii] - br[jj]);
+            } else {
+              const float u = ar[ii] - br[jj];
+              acc[ii][jj] = fmaf(u, u, acc[ii][jj]);
+            }
+          }
+      }
+    }
+    __syncthreads();
+  }
+  // epilogue: f-, dL/dS coefficient, loss partial
+  const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
+  float lsum = 0.f;
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int i = i0 + ty * 4 + ii;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = j0 + tx * 4 + jj;
+      if (i < dm.g && j < dm.k) {
+        const float st = acc[ii][jj];
+        float f, coef;
+        const float dLdf = sigmoid(pair_score_from(FAM, st, dm.gamma)) * inv_bk;
+        f = pair_score_from(FAM, st, dm.gamma);
+        if (FAM == FAM_DOT) {
+          coef = dLdf;
+        } else if (FAM == FAM_L2) {
+          coef = -dLdf / fmaxf(sqrtf(st), 1e-12f);
+        } else if (FAM == FAM_L2SQ) {
+          coef = -2.f * dLdf;
+        } else {
+          coef = -dLdf;
+        }
+        a.b.W[((int64_t)c * dm.g + i) * dm.k + j] = coef;
+        lsum += -log_sigmoid(-f);
+      }
+    }
+  }
+  lsum = warp_sum(lsum);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    a.b.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_neg_bwd (FFMA): blockIdx.z < C -> dO tiles of chunk z ; blockIdx.z >= C -> dX' tiles of chunk z - C.
+//   dO[i][e]  = sum_j W_ij phi_o(o_ie, x_je)      phi_o: DOT x ; L2/L2SQ (o-x) ; L1 sgn(o-x) ; CMOD (o-x)/|z|
+//   dX'[j][e] = sum_i W_ij phi_x(o_ie, x_je)      phi_x: DOT o ; others -phi_o
+// Columns of a tile: 64 floats (CMOD: 32 complex elements -> re and im halves).
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ float sgnf(float u) { return u > 0.f ? 1.f : (u < 0.f ? -1.f : 0.f); }
+
+template <int FAM>
+__global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
+  constexpr bool CPLX = FAM == FAM_CMOD;
+  const Dims& dm = a.dm;
+  __shared__ __align__(16) float Ws[TK][TM + TPAD];  // [K index][row index of the output]
+  __shared__ __align__(16) float Vs[TK][TN + TPAD];  // [K index][column]  (CPLX: re cols 0..31, im cols 32..63)
+  const bool pass_x = blockIdx.z >= (unsigned)dm.C;
+  const int c = pass_x ? blockIdx.z - dm.C : blockIdx.z;
+  const int nrows = pass_x ? dm.k : dm.g;        // output rows: j (dX') or i (dO)
+  const int nk = pass_x ? dm.g : dm.k;           // contraction: i or j
+  const int r0 = blockIdx.y * TM;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int half = dm.d >> 1;
+  const float* Oc = a.b.O + (int64_t)c * dm.g * dm.d;
+  const float* Xc = a.b.X + (int64_t)c * dm.k * dm.d;
+  const float* Wc = a.b.W + (int64_t)c * dm.g * dm.k;
+  const float* Self = pass_x ? Xc : Oc;   // the matrix whose rows are the output rows
+  const float* Other = pass_x ? Oc : Xc;  // streamed over the contraction index
+  // output columns of this thread
+  int col[4];
+  bool colok[4];
+  const int cb = blockIdx.x * (CPLX ? TN / 2 : TN);
+#pragma unroll
+  for (int ee = 0; ee < 4; ++ee) {
+    if (CPLX) {
+      const int cc = cb + (tx & 7) * 4 + ee;  // complex index
+      col[ee] = cc;
+      colok[ee] = cc < half;
+    } else {
+      col[ee] = cb + tx * 4 + ee;
+      colok[ee] = col[ee] < dm.d;
+    }
+  }
+  const bool imag_lane = CPLX && tx >= 8;  // CPLX: tx<8 own re columns, tx>=8 own the matching im columns
+  // own values (self rows x own columns); CPLX needs both parts of own complex entries
+  float sv[4][4], si[4][4];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int rr = r0 + ty * 4 + ii;
+#pragma unroll
+    for (int ee = 0; ee < 4; ++ee) {
+      const bool ok = rr < nrows && colok[ee];
+      if (CPLX) {
+        sv[ii][ee] = ok ? Self[(int64_t)rr * dm.d + col[ee]] : 0.f;
+        si[ii][ee] = ok ? Self[(int64_t)rr * dm.d + half + col[ee]] : 0.f;
+      } else {
+        sv[ii][ee] = ok ? Self[(int64_t)rr * dm.d + col[ee]] : 0.f;
+        si[ii][ee] = 0.f;
+      }
+    }
+  }
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < nk; k0 += TK) {
+    // Ws[kk][r] = W for (output row r0+r, contraction k0+kk)
+    for (int idx = threadIdx.x; idx < TK * TM; idx += blockDim.x) {
+      const int kk = idx / TM, r = idx % TM;
+      const int orow = r0 + r, kidx = k0 + kk;
+      float w = 0.f;
+      if (orow < nrows && kidx < nk) w = pass_x ? Wc[(int64_t)kidx * dm.k + orow] : Wc[(int64_t)orow * dm.k + kidx];
+      Ws[kk][r] = w;
+    }
+    // Vs[kk][col] = Other row (k0+kk), this tile's columns
+    for (int idx = threadIdx.x; idx < TK * TN; idx += blockDim.x) {
+      const int kk = idx / TN, cl = idx % TN;
+      const int kidx = k0 + kk;
+      float v = 0.f;
+      if (kidx < nk) {
+        if (CPLX) {
+          const int cc = cb + (cl & 31);
+          if (cc < half) v = Other[(int64_t)kidx * dm.d + (cl < 32 ? cc : half + cc)];
+        } else {
+          const int gcol = cb + cl;
+          if (gcol < dm.d) v = Other[(int64_t)kidx * dm.d + gcol];
+        }
+      }
+      Vs[kk][cl] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < TK; ++kk) {
+      const float4 wv = *reinterpret_cast<const float4*>(&Ws[kk][ty * 4]);
+      const float w[4] = {wv.x, wv.y, wv.z, wv.w};
+      float ov[4], oi[4];
+      if (CPLX) {
+        const int cl = (tx & 7) * 4;
+        const float4 a_ = *reinterpret_cast<const float4*>(&Vs[kk][cl]);
+        const float4 b_ = *reinterpret_cast<const float4*>(&Vs[kk][32 + cl]);
+        ov[0] = a_.x; ov[1] = a_.y; ov[2] = a_.z; ov[3] = a_.w;
+        oi[0] = b_.x; oi[1] = b_.y; oi[2] = b_.z; oi[3] = b_.w;
+      } else {
+        const float4 a_ = *reinterpret_cast<const float4*>(&Vs[kk][tx * 4]);
+        ov[0] = a_.x; ov[1] = a_.y; ov[2] = a_.z; ov[3] = a_.w;
+        oi[0] = oi[1] = oi[2] = oi[3] = 0.f;
+      }
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int ee = 0; ee < 4; ++ee) {
+          // o = (pass_x ? other : self), x = (pass_x ? self : other)
+          const float s_ = sv[ii][ee], t_ = ov[ee];
+          if (FAM == FAM_DOT) {
+            acc[ii][ee] = fmaf(w[ii], t_, acc[ii][ee]);
+          } else if (FAM == FAM_L1) {
+            const float u = pass_x ? (t_ - s_) : (s_ - t_);  // o - x
+            acc[ii][ee] = fmaf(w[ii], pass_x ? -sgnf(u) : sgnf(u), acc[ii][ee]);
+          } else if (FAM == FAM_CMOD) {
+            const float ur = pass_x ? (t_ - s_) : (s_ - t_);
+            const float ui = pass_x ? (oi[ee] - si[ii][ee]) : (si[ii][ee] - oi[ee]);
+            const float inv = 1.f / fmaxf(sqrtf(ur * ur + ui * ui), 1e-12f);
+            const float comp = imag_lane ? ui : ur;
+            acc[ii][ee] = fmaf(w[ii], (pass_x ? -comp : comp) * inv, acc[ii][ee]);
+          } else {  // L2, L2SQ: phi_o = o - x
+            const float u = s_ - t_;  // self - other: = (o - x) for dO, = (x - o) = -phi_o for dX'
+            acc[ii][ee] = fmaf(w[ii], u, acc[ii][ee]);
+          }
+        }
+    }
+    __syncthreads();
+  }
+  // store
+  float* dst = pass_x ? a.Gocc + ((int64_t)2 * dm.B + (int64_t)c * dm.k) * dm.d : a.b.dO + (int64_t)c * dm.g * dm.d;
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int rr = r0 + ty * 4 + ii;
+    if (rr >= nrows) continue;
+#pragma unroll
+    for (int ee = 0; ee < 4; ++ee) {
+      if (!colok[ee]) continue;
+      const int gcol = CPLX ? (imag_lane ? half + col[ee] : col[ee]) : col[ee];
+      dst[(int64_t)rr * dm.d + gcol] = acc[ii][ee];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_chain: per positive, total d/do and d/d(other) = dO (negatives) + w+ * dpair(o, other), then the chain rule of
+// combine -> per-occurrence gradients Gocc[i] (head row), Gocc[B+i] (tail row), Grel[i]. Last CTA: loss.
+// ------------------------------------------------------------------------------------------------
+struct ChainArgs {
+  Dims dm;
+  Slot s;
+  const float* ent;
+  const float* rel;
+  StepBuffers b;
+  int32_t n_neg_parts;
+  int32_t loss_slot;
+};
+
+__device__ __forceinline__ void dpair(int fam, float o, float x, float scale, float& go, float& gx) {
+  // derivative of the pair score f w.r.t. o and x, times scale (scale folds 1/D for L2)
+  switch (fam) {
+    case FAM_DOT: go = scale * x; gx = scale * o; return;
+    case FAM_L1: { const float s = sgnf(o - x); go = -scale * s; gx = scale * s; return; }
+    case FAM_L2: { const float u = o - x; go = -scale * u; gx = scale * u; return; }
+    default: { const float u = o - x; go = -2.f * scale * u; gx = 2.f * scale * u; return; }  // L2SQ
+  }
+}
+
+__global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
+  const Dims& dm = a.dm;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == gridDim.x - 1) {
+    // deterministic loss: fixed lane assignment, fixed warp order (reading c.9 normalisation)
+    if (threadIdx.x < 32) {
+      float sp = 0.f, sn = 0.f;
+      for (int i = lane; i < dm.B; i += 32) sp += a.b.lpos[i];
+      for (int q = lane; q < a.n_neg_parts; q += 32) sn += a.b.lneg[q];
+      sp = warp_sum(sp);
+      sn = warp_sum(sn);
+      if (lane == 0) {
+        const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
+        a.b.loss[a.loss_slot] = L;
+        const bool bad = !isfinite(L);
+        a.b.flags[1] = bad ? 1 : 0;
+        if (bad) a.b.flags[0] = 1;
+      }
+    }
+    return;
+  }
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= dm.B) return;
+  const int mode = a.s.mode[i / dm.g];
+  const float* h = a.ent + (int64_t)a.s.ph[i] * dm.d;
+  const float* t = a.ent + (int64_t)a.s.pt[i] * dm.d;
+  const float* r = a.rel + (int64_t)a.s.pr[i] * dm.drel;
+  const float* o = a.b.O + (int64_t)i * dm.d;
+  const float* dO = a.b.dO + (int64_t)i * dm.d;
+  const float* other = mode == 0 ? t : h;
+  float* gH = a.b.Gocc + (int64_t)i * dm.d;
+  float* gT = a.b.Gocc + (int64_t)(dm.B + i) * dm.d;
+  float* gR = a.b.Grel + (int64_t)i * dm.drel;
+  float* gOther = mode == 0 ? gT : gH;  // the non-combined side
+  const float wp = a.b.wpos[i];
+  float scale = wp;
+  if (dm.family == FAM_L2) {
+    const float st = warp_sum(pair_partial(FAM_L2, o, other, dm.d, lane));
+    scale = wp / fmaxf(sqrtf(st), 1e-12f);
+  }
+  const int model = dm.model;
+  if (!is_complex_model(model)) {
+    const int d4 = dm.d >> 2;
+    for (int v = lane; v < d4; v += 32) {
+      const float4 ov = ld4(o, v), xv = ld4(other, v), dv = ld4(dO, v);
+      const float oo[4] = {ov.x, ov.y, ov.z, ov.w}, xx[4] = {xv.x, xv.y, xv.z, xv.w};
+      const float dd[4] = {dv.x, dv.y, dv.z, dv.w};
+      float go[4], gx[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        dpair(dm.family, oo[u], xx[u], scale, go[u], gx[u]);
+        go[u] += dd[u];
+      }
+      st4(gOther, v, make_float4(gx[0], gx[1], gx[2], gx[3]));
+      float4 gc, gr;  // grads of the combined entity side and of r
+      if (model == KGE_DISTMULT) {
+        // tail o = h*r : dh = go*r, dr = go*h ; head o = r*t : dt = go*r, dr = go*t
+        const float4 rv = ld4(r, v);
+        const float4 ev = mode == 0 ? ld4(h, v) : ld4(t, v);
+        gc = make_float4(go[0] * rv.x, go[1] * rv.y, go[2] * rv.z, go[3] * rv.w);
+        gr = make_float4(go[0] * ev.x, go[1] * ev.y, go[2] * ev.z, go[3] * ev.w);
+      } else {  // TransE: tail o = h + r ; head o = t - r
+        gc = make_float4(go[0], go[1], go[2], go[3]);
+        gr = mode == 0 ? gc : make_float4(-go[0], -go[1], -go[2], -go[3]);
+      }
+      st4(mode == 0 ? gH : gT, v, gc);
+      st4(gR, v, gr);
+    }
+    return;
+  }
+  // complex models: lanes own complex element groups (re at v, im at v + n4)
+  const int n4 = dm.d >> 3;
+  float scale_c = scale;
+  for (int v = lane; v < n4; v += 32) {
+    const float4 orv = ld4(o, v), oiv = ld4(o, v + n4), xrv = ld4(other, v), xiv = ld4(other, v + n4);
+    const float4 drv = ld4(dO, v), div = ld4(dO, v + n4);
+    const float4 crv = mode == 0 ? ld4(h, v) : ld4(t, v);  // combined-side entity (re, im)
+    const float4 civ = mode == 0 ? ld4(h, v + n4) : ld4(t, v + n4);
+    const float o_r[4] = {orv.x, orv.y, orv.z, orv.w}, o_i[4] = {oiv.x, oiv.y, oiv.z, oiv.w};
+    const float x_r[4] = {xrv.x, xrv.y, xrv.z, xrv.w}, x_i[4] = {xiv.x, xiv.y, xiv.z, xiv.w};
+    const float d_r[4] = {drv.x, drv.y, drv.z, drv.w}, d_i[4] = {div.x, div.y, div.z, div.w};
+    const float e_r[4] = {crv.x, crv.y, crv.z, crv.w}, e_i[4] = {civ.x, civ.y, civ.z, civ.w};
+    float gxr[4], gxi[4], ger[4], gei[4], grr[4], gri[4];
+    float rr_[4], ri_[4];
+    if (model == KGE_COMPLEX) {
+      const float4 a_ = ld4(r, v), b_ = ld4(r, v + n4);
+      rr_[0] = a_.x; rr_[1] = a_.y; rr_[2] = a_.z; rr_[3] = a_.w;
+      ri_[0] = b_.x; ri_[1] = b_.y; ri_[2] = b_.z; ri_[3] = b_.w;
+    } else {
+      const float4 th = ld4(r, v);
+      const float tt[4] = {th.x, th.y, th.z, th.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sincosf(tt[u], &ri_[u], &rr_[u]);  // (cos, sin)
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float gor, goi;
+      if (dm.family == FAM_CMOD) {
+        const float ur = o_r[u] - x_r[u], ui = o_i[u] - x_i[u];
+        const float inv = scale_c / fmaxf(sqrtf(ur * ur + ui * ui), 1e-12f);
+        gor = -inv * ur; goi = -inv * ui;
+        gxr[u] = inv * ur; gxi[u] = inv * ui;
+      } else {
+        dpair(dm.family, o_r[u], x_r[u], scale_c, gor, gxr[u]);
+        dpair(dm.family, o_i[u], x_i[u], scale_c, goi, gxi[u]);
+      }
+      gor += d_r[u];
+      goi += d_i[u];
+      const float c = rr_[u], s = ri_[u], a = e_r[u], b = e_i[u];
+      if (model == KGE_COMPLEX) {
+        if (mode == 0) {  // o = (a c - b s, a s + b c) with r = c + i s
+          ger[u] = gor * c + goi * s;
+          gei[u] = -gor * s + goi * c;
+          grr[u] = gor * a + goi * b;
+          gri[u] = -gor * b + goi * a;
+        } else {  // o = (c a + s b, c b - s a) with t = a + i b
+          ger[u] = gor * c - goi * s;
+          gei[u] = gor * s + goi * c;
+          grr[u] = gor * a + goi * b;
+          gri[u] = gor * b - goi * a;
+        }
+      } else {  // RotatE, r = e^{i theta}
+        if (mode == 0) {  // o = (a c - b s, a s + b c)
+          ger[u] = gor * c + goi * s;
+          gei[u] = -gor * s + goi * c;
+          grr[u] = gor * (-a * s - b * c) + goi * (a * c - b * s);
+        } else {  // o = (a c + b s, -a s + b c)
+          ger[u] = gor * c - goi * s;
+          gei[u] = gor * s + goi * c;
+          grr[u] = gor * (-a * s + b * c) + goi * (-a * c - b * s);
+        }
+        gri[u] = 0.f;
+      }
+    }
+    float* gC = mode == 0 ? gH : gT;
+    st4(gOther, v, make_float4(gxr[0], gxr[1], gxr[2], gxr[3]));
+    st4(gOther, v + n4, make_float4(gxi[0], gxi[1], gxi[2], gxi[3]));
+    st4(gC, v, make_float4(ger[0], ger[1], ger[2], ger[3]));
+    st4(gC, v + n4, make_float4(gei[0], gei[1], gei[2], gei[3]));
+    st4(gR, v, make_float4(grr[0], grr[1], grr[2], grr[3]));
+    if (model == KGE_COMPLEX) st4(gR, v + n4, make_float4(gri[0], gri[1], gri[2], gri[3]));
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_update: segmented reduce (sorted occurrence order) fused with sparse row-wise Adagrad (reading c.11)
+//   state += mean_j G_j^2 ; row -= lr * G / sqrt(state + eps)
+// ------------------------------------------------------------------------------------------------
+struct UpdateArgs {
+  Dims dm;
+  Slot s;
+  float* ent;
+  float* ent_st;
+  float* rel;
+  float* rel_st;
+  StepBuffers b;
+};
+
+constexpr int kMaxV = 8;  // float4 per lane: rows up to 32*8*4 = 1024 floats
+
+__device__ __forceinline__ void seg_adagrad(float* __restrict__ row, float* __restrict__ st,
+                                            const float* __restrict__ G, const int32_t* __restrict__ occ, int p0,
+                                            int p1, int w, float lr, float eps, int lane) {
+  const int w4 = w >> 2;
+  float4 g[kMaxV];
+#pragma unroll
+  for (int m = 0; m < kMaxV; ++m) g[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int p = p0; p < p1; ++p) {
+    const float* src = G + (int64_t)occ[p] * w;
+#pragma unroll
+    for (int m = 0; m < kMaxV; ++m) {
+      const int v = lane + 32 * m;
+      if (v < w4) {
+        const float4 x = ld4(src, v);
+        g[m].x += x.x; g[m].y += x.y; g[m].z += x.z; g[m].w += x.w;
+      }
+    }
+  }
+  float sq = 0.f;
+#pragma unroll
+  for (int m = 0; m < kMaxV; ++m)
+    if (lane + 32 * m < w4) sq += g[m].x * g[m].x + g[m].y * g[m].y + g[m].z * g[m].z + g[m].w * g[m].w;
+  sq = warp_sum(sq);
+  float s = 0.f;
+  if (lane == 0) {
+    s = *st + sq / (float)w;
+    *st = s;
+  }
+  s = __shfl_sync(0xffffffffu, s, 0);
+  const float step = lr / sqrtf(s + eps);
+#pragma unroll
+  for (int m = 0; m < kMaxV; ++m) {
+    const int v = lane + 32 * m;
+    if (v < w4) {
+      float4 x = ld4(row, v);
+      x.x -= step * g[m].x; x.y -= step * g[m].y; x.z -= step * g[m].z; x.w -= step * g[m].w;
+      st4(row, v, x);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
+  const Dims& dm = a.dm;
+  if (a.b.flags[1]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w < dm.n_occ) {
+    if (w >= *a.s.ent_n) return;
+    const int32_t id = a.s.ent_uniq[w];
+    seg_adagrad(a.ent + (int64_t)id * dm.d, a.ent_st + id, a.b.Gocc, a.s.ent_occ, a.s.ent_off[w], a.s.ent_off[w + 1],
+                dm.d, dm.lr, dm.eps, lane);
+  } else {
+    const int u = w - dm.n_occ;
+    if (u >= *a.s.rel_n) return;
+    const int32_t id = a.s.rel_uniq[u];
+    seg_adagrad(a.rel + (int64_t)id * dm.drel, a.rel_st + id, a.b.Grel, a.s.rel_occ, a.s.rel_off[u],
+                a.s.rel_off[u + 1], dm.drel, dm.lr, dm.eps, lane);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// host launchers
+// ------------------------------------------------------------------------------------------------
+template <int FAM>
+static void launch_neg(kge_handle* h, const NegArgs& na) {
+  const Dims& dm = h->dims;
+  dim3 gf((dm.k + TN - 1) / TN, (dm.g + TM - 1) / TM, dm.C);
+  launch_begin(h, KGE_K_NEG_FWD);
+  k_neg_fwd<FAM><<<gf, 256, 0, h->stream>>>(na);
+  launch_end(h, KGE_K_NEG_FWD);
+  const int cols_per_tile = FAM == FAM_CMOD ? TN / 2 : TN;
+  const int ncols = FAM == FAM_CMOD ? dm.d / 2 : dm.d;
+  dim3 gb((ncols + cols_per_tile - 1) / cols_per_tile, (std::max(dm.g, dm.k) + TM - 1) / TM, 2 * dm.C);
+  launch_begin(h, KGE_K_NEG_BWD);
+  k_neg_bwd<FAM><<<gb, 256, 0, h->stream>>>(na);
+  launch_end(h, KGE_K_NEG_BWD);
+}
+
+cudaError_t launch_tc_neg(kge_handle* h, const Slot& s);  // tc.cu
+bool tc_supported(const kge_handle* h);
+
+cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
+  const Dims& dm = h->dims;
+  GatherArgs ga{dm, s, h->ent, h->rel, h->buf};
+  const int rows = dm.B + dm.C * dm.k;
+  launch_begin(h, KGE_K_GATHER);
+  k_gather<<<(rows + 7) / 8, 256, 0, h->stream>>>(ga);
+  launch_end(h, KGE_K_GATHER);
+
+  NegArgs na{dm, h->buf, h->buf.Gocc};
+  if (h->cfg.neg_precision == KGE_PREC_TF32 && tc_supported(h)) {
+    cudaError_t e = launch_tc_neg(h, s);
+    if (e != cudaSuccess) return e;
+  } else {
+    switch (dm.family) {
+      case FAM_DOT: launch_neg<FAM_DOT>(h, na); break;
+      case FAM_L2: launch_neg<FAM_L2>(h, na); break;
+      case FAM_L2SQ: launch_neg<FAM_L2SQ>(h, na); break;
+      case FAM_L1: launch_neg<FAM_L1>(h, na); break;
+      case FAM_CMOD: launch_neg<FAM_CMOD>(h, na); break;
+    }
+  }
+  ChainArgs ca{dm, s, h->ent, h->rel, h->buf, h->n_neg_parts, (int32_t)(step % h->ring)};
+  launch_begin(h, KGE_K_CHAIN);
+  k_chain<<<(dm.B + 7) / 8 + 1, 256, 0, h->stream>>>(ca);
+  launch_end(h, KGE_K_CHAIN);
+
+  UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, h->buf};
+  const int warps = dm.n_occ + dm.B;
+  launch_begin(h, KGE_K_UPDATE);
+  k_update<<<(warps + 7) / 8, 256, 0, h->stream>>>(ua);
+  launch_end(h, KGE_K_UPDATE);
+  return cudaGetLastError();
+}
+
+// ---- kge_score: f(h, r, t) per triple (tail-mode decomposition: f = pair(combine(h, r), t)) ----
+struct ScoreArgs {
+  Dims dm;
+  const float* ent;
+  const float* rel;
+  const int32_t* hs;
+  const int32_t* rs;
+  const int32_t* ts;
+  int64_t n;
+  float* o_scratch;  // [n x d]
+  float* out;
+};
+
+__global__ void __launch_bounds__(256) k_score(ScoreArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= a.n) return;
+  const Dims& dm = a.dm;
+  const float* h = a.ent + (int64_t)a.hs[i] * dm.d;
+  const float* t = a.ent + (int64_t)a.ts[i] * dm.d;
+  const float* r = a.rel + (int64_t)a.rs[i] * dm.drel;
+  float* o = a.o_scratch + i * dm.d;
+  combine_row(dm.model, 0, h, r, t, o, dm.d, lane);
+  __syncwarp();
+  const float st = warp_sum(pair_partial(dm.family, o, t, dm.d, lane));
+  if (lane == 0) a.out[i] = pair_score_from(dm.family, st, dm.gamma);
+}
+
+cudaError_t launch_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, float* out) {
+  // scratch: reuse the X buffer in chunks of its capacity
+  const int64_t cap = (int64_t)h->dims.C * h->dims.k;
+  for (int64_t b = 0; b < n; b += cap) {
+    const int64_t m = std::min(cap, n - b);
+    ScoreArgs sa{h->dims, h->ent, h->rel, hs + b, rs + b, ts + b, m, h->buf.X, out + b};
+    k_score<<<(unsigned)((m + 7) / 8), 256, 0, h->stream>>>(sa);
+    ++h->launches;
+  }
+  return cudaGetLastError();
+}
+
+// ---- row get / set ----
+__global__ void k_rows(float* __restrict__ tab, int32_t w, const int32_t* __restrict__ ids, int64_t n,
+                       float* __restrict__ buf, int write) {
+  const int64_t total = n * w;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / w, c = q - i * w;
+    float* p = tab + (int64_t)ids[i] * w + c;
+    if (write)
+      *p = buf[q];
+    else
+      buf[q] = *p;
+  }
+}
+
+cudaError_t launch_rows(kge_handle* h, float* tab, int32_t w, const int32_t* ids, int64_t n, float* buf, bool write) {
+  if (n == 0) return cudaSuccess;
+  const int64_t total = n * w;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_rows<<<blocks, 256, 0, h->stream>>>(tab, w, ids, n, buf, write ? 1 : 0);
+  ++h->launches;
+  return cudaGetLastError();
+}
+
+}  // namespace kge

@@ -1,0 +1,288 @@
+"""Thin ctypes binding of libkge.so (include/kge.h): argument marshalling only.
+
+Every step of the training path runs in the library's CUDA kernels; this module converts numpy arrays to host
+pointers, hands PyTorch's caching allocator and current stream to the library, and raises KgeError on a non-OK status.
+There is no CPU fallback: if libkge.so is missing or no sm_100 device is present, calls raise.
+Names mirror the C entry points: init (kge_init), Handle.sample (kge_sample), Handle.train_step (kge_train_step),
+Handle.train_batch (kge_train_batch), Handle.score (kge_score), get_rows / set_rows, step, sync, destroy.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .build import LIB
+
+MODELS = {"transe_l1": 0, "transe_l2": 1, "distmult": 2, "complex": 3, "rotate": 4, "transr": 5}
+CORRUPT = {"tail": 0, "head": 1, "alternate": 2}
+PRECISION = {"fp32": 0, "tf32": 1}
+STATUS = {0: "KGE_OK", -1: "KGE_EINVAL", -2: "KGE_ERANGE", -3: "KGE_ENOMEM", -4: "KGE_ECUDA", -5: "KGE_ENCCL",
+          -6: "KGE_ENONFINITE", -7: "KGE_ESTATE", -8: "KGE_EUNSUPPORTED"}
+KERNELS = ["k_sample", "k_gather", "k_neg_fwd", "k_neg_bwd", "k_chain", "k_update"]
+
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class KgeError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_int32), ("model", ctypes.c_int32),
+                ("n_entities", ctypes.c_int64), ("n_relations", ctypes.c_int64),
+                ("dim", ctypes.c_int32), ("batch_size", ctypes.c_int32), ("chunk_size", ctypes.c_int32),
+                ("neg_k", ctypes.c_int32), ("gamma", ctypes.c_float), ("lr", ctypes.c_float),
+                ("adagrad_eps", ctypes.c_float), ("init_bound", ctypes.c_float), ("seed", ctypes.c_uint64),
+                ("corrupt", ctypes.c_int32), ("neg_precision", ctypes.c_int32), ("rotate_variant", ctypes.c_int32),
+                ("lag", ctypes.c_int32), ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("nccl_comm", ctypes.c_void_p), ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p),
+                ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_ctx", ctypes.c_void_p)]
+
+
+_lib = None
+P = ctypes.POINTER
+_i64p = P(ctypes.c_int64)
+_i32p = P(ctypes.c_int32)
+_fp = P(ctypes.c_float)
+
+
+def lib():
+    """Load libkge.so. Raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise RuntimeError(f"libkge.so not built at {LIB}; run __graft_entry__.build() (there is no CPU fallback)")
+        L = ctypes.CDLL(LIB)
+        L.kge_config_default.argtypes = [P(_Config)]
+        L.kge_init.argtypes = [P(ctypes.c_void_p), P(_Config), _i64p, _i64p, _i64p, ctypes.c_int64]
+        L.kge_sample.argtypes = [ctypes.c_void_p, ctypes.c_int64, _i64p, _i64p, P(ctypes.c_int8), _i64p, _i64p, _i32p,
+                                 _i64p, _i64p, _i32p]
+        L.kge_train_step.argtypes = [ctypes.c_void_p, ctypes.c_int64, _fp]
+        L.kge_train_batch.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, _fp]
+        L.kge_score.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, _fp]
+        L.kge_get_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
+        L.kge_set_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
+        L.kge_table_width.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        L.kge_table_width.restype = ctypes.c_int32
+        L.kge_step.argtypes = [ctypes.c_void_p]
+        L.kge_step.restype = ctypes.c_int64
+        L.kge_set_step.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        L.kge_sync.argtypes = [ctypes.c_void_p]
+        L.kge_profile_begin.argtypes = [ctypes.c_void_p]
+        L.kge_profile_end.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_double), _i64p]
+        L.kge_launch_count.argtypes = [ctypes.c_void_p]
+        L.kge_launch_count.restype = ctypes.c_int64
+        L.kge_destroy.argtypes = [ctypes.c_void_p]
+        L.kge_last_error.restype = ctypes.c_char_p
+        L.kge_kernel_name.argtypes = [ctypes.c_int32]
+        L.kge_kernel_name.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise KgeError(rc, lib().kge_last_error().decode())
+    return rc
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(P(ct)) if a is not None else None
+
+
+@dataclass
+class Config:
+    """Mirror of kge_config (include/kge.h); defaults = kge_config_default."""
+    model: str = "transe_l2"
+    n_entities: int = 0
+    n_relations: int = 0
+    dim: int = 400
+    batch_size: int = 1024
+    chunk_size: int = 256
+    neg_k: int = 256
+    gamma: float = 12.0
+    lr: float = 0.1
+    adagrad_eps: float = 1e-10
+    init_bound: float = 0.0
+    seed: int = 1
+    corrupt: str = "alternate"
+    neg_precision: str = "tf32"
+    rotate_variant: int = 0
+    lag: int = 0
+    world_size: int = 1
+    rank: int = 0
+
+    @property
+    def C(self):
+        return self.batch_size // self.chunk_size
+
+    @property
+    def n_occ(self):
+        return 2 * self.batch_size + self.C * self.neg_k
+
+
+class _TorchAllocator:
+    """Hands PyTorch's caching allocator to the library (kge_config.dev_alloc / dev_free)."""
+
+    def __init__(self, device, stream):
+        import torch
+        self._torch = torch
+        self.device = device
+        self.stream = stream
+
+        def alloc(nbytes, ctx):
+            try:
+                return self._torch.cuda.caching_allocator_alloc(int(nbytes), self.device, self.stream)
+            except Exception:
+                return None
+
+        def free(ptr, ctx):
+            self._torch.cuda.caching_allocator_delete(ptr)
+
+        self.alloc_fn = ALLOC_FN(alloc)
+        self.free_fn = FREE_FN(free)
+
+
+class Handle:
+    def __init__(self, ptr, cfg: Config, keep):
+        self._h = ptr
+        self.cfg = cfg
+        self._keep = keep
+
+    def __del__(self):
+        self.destroy()
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            lib().kge_destroy(self._h)
+            self._h = None
+
+    # kge_sample
+    def sample(self, step):
+        c = self.cfg
+        pos = np.zeros(c.batch_size, np.int64)
+        neg = np.zeros(c.C * c.neg_k, np.int64)
+        mode = np.zeros(c.C, np.int8)
+        ue = np.zeros(c.n_occ, np.int64)
+        ie = np.zeros(c.n_occ, np.int32)
+        ur = np.zeros(c.batch_size, np.int64)
+        ir = np.zeros(c.batch_size, np.int32)
+        ne, nr = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().kge_sample(self._h, step, _ptr(pos, ctypes.c_int64), _ptr(neg, ctypes.c_int64),
+                                _ptr(mode, ctypes.c_int8), _ptr(ue, ctypes.c_int64), ctypes.byref(ne),
+                                _ptr(ie, ctypes.c_int32), _ptr(ur, ctypes.c_int64), ctypes.byref(nr),
+                                _ptr(ir, ctypes.c_int32)))
+        return dict(pos=pos, neg=neg, mode=mode, uniq_ent=ue[:ne.value], inv_ent=ie, uniq_rel=ur[:nr.value],
+                    inv_rel=ir)
+
+    # kge_train_step
+    def train_step(self, n_steps=1, return_loss=True):
+        if return_loss:
+            out = np.zeros(n_steps, np.float32)
+            _check(lib().kge_train_step(self._h, n_steps, _ptr(out, ctypes.c_float)))
+            return out
+        _check(lib().kge_train_step(self._h, n_steps, None))
+        return None
+
+    # kge_train_batch
+    def train_batch(self, heads, rels, tails, return_loss=True):
+        h, r, t = _i64(heads), _i64(rels), _i64(tails)
+        assert len(h) == self.cfg.batch_size
+        if return_loss:
+            out = np.zeros(1, np.float32)
+            _check(lib().kge_train_batch(self._h, _ptr(h, ctypes.c_int64), _ptr(r, ctypes.c_int64),
+                                         _ptr(t, ctypes.c_int64), _ptr(out, ctypes.c_float)))
+            return float(out[0])
+        _check(lib().kge_train_batch(self._h, _ptr(h, ctypes.c_int64), _ptr(r, ctypes.c_int64),
+                                     _ptr(t, ctypes.c_int64), None))
+        return None
+
+    def train_batch_ptr(self, hp, rp, tp, loss_ptr):
+        """Raw-pointer variant (host int64 buffers, e.g. pinned torch tensors)."""
+        _check(lib().kge_train_batch(self._h, ctypes.cast(hp, _i64p), ctypes.cast(rp, _i64p), ctypes.cast(tp, _i64p),
+                                     ctypes.cast(loss_ptr, _fp) if loss_ptr else None))
+
+    # kge_score
+    def score(self, hs, rs, ts):
+        hs, rs, ts = _i64(hs), _i64(rs), _i64(ts)
+        out = np.zeros(len(hs), np.float32)
+        _check(lib().kge_score(self._h, _ptr(hs, ctypes.c_int64), _ptr(rs, ctypes.c_int64), _ptr(ts, ctypes.c_int64),
+                               len(hs), _ptr(out, ctypes.c_float)))
+        return out
+
+    def width(self, table):
+        return lib().kge_table_width(self._h, table)
+
+    def get_rows(self, table, ids):
+        ids = _i64(ids)
+        out = np.zeros((len(ids), self.width(table)), np.float32)
+        _check(lib().kge_get_rows(self._h, table, _ptr(ids, ctypes.c_int64), len(ids), _ptr(out, ctypes.c_float)))
+        return out
+
+    def set_rows(self, table, ids, rows):
+        ids = _i64(ids)
+        rows = np.ascontiguousarray(rows, dtype=np.float32)
+        _check(lib().kge_set_rows(self._h, table, _ptr(ids, ctypes.c_int64), len(ids), _ptr(rows, ctypes.c_float)))
+
+    @property
+    def step(self):
+        return lib().kge_step(self._h)
+
+    def set_step(self, s):
+        _check(lib().kge_set_step(self._h, s))
+
+    def sync(self):
+        _check(lib().kge_sync(self._h))
+
+    def profile_begin(self):
+        _check(lib().kge_profile_begin(self._h))
+
+    def profile_end(self):
+        avg = (ctypes.c_double * len(KERNELS))()
+        cnt = (ctypes.c_int64 * len(KERNELS))()
+        _check(lib().kge_profile_end(self._h, len(KERNELS), avg, cnt))
+        return {KERNELS[i]: (avg[i], cnt[i]) for i in range(len(KERNELS))}
+
+    @property
+    def launch_count(self):
+        return lib().kge_launch_count(self._h)
+
+
+def init(cfg: Config, heads, rels, tails, use_torch_allocator=True, stream=None) -> Handle:
+    """kge_init. heads/rels/tails: host int64 arrays of the whole graph (copied to the device)."""
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("kge.init needs a CUDA (sm_100a) device; there is no CPU fallback")
+    c = _Config()
+    lib().kge_config_default(ctypes.byref(c))
+    c.model = MODELS[cfg.model] if isinstance(cfg.model, str) else cfg.model
+    c.n_entities, c.n_relations, c.dim = cfg.n_entities, cfg.n_relations, cfg.dim
+    c.batch_size, c.chunk_size, c.neg_k = cfg.batch_size, cfg.chunk_size, cfg.neg_k
+    c.gamma, c.lr, c.adagrad_eps, c.init_bound = cfg.gamma, cfg.lr, cfg.adagrad_eps, cfg.init_bound
+    c.seed = cfg.seed
+    c.corrupt = CORRUPT[cfg.corrupt] if isinstance(cfg.corrupt, str) else cfg.corrupt
+    c.neg_precision = PRECISION[cfg.neg_precision] if isinstance(cfg.neg_precision, str) else cfg.neg_precision
+    c.rotate_variant, c.lag, c.world_size, c.rank = cfg.rotate_variant, cfg.lag, cfg.world_size, cfg.rank
+    dev = torch.cuda.current_device()
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    c.cuda_stream = s.cuda_stream
+    keep = [c]
+    if use_torch_allocator:
+        al = _TorchAllocator(dev, s)
+        c.dev_alloc, c.dev_free = al.alloc_fn, al.free_fn
+        keep.append(al)
+    h, r, t = _i64(heads), _i64(rels), _i64(tails)
+    out = ctypes.c_void_p()
+    _check(lib().kge_init(ctypes.byref(out), ctypes.byref(c), _ptr(h, ctypes.c_int64), _ptr(r, ctypes.c_int64),
+                          _ptr(t, ctypes.c_int64), len(h)))
+    return Handle(out.value, cfg, keep)

@@ -1,0 +1,189 @@
+"""CUDA path (libkge.so through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star; reading c.14 in DESIGN.md):
+  - sampled positives, negatives, modes, unique entity / relation sets and inverse maps: bit-exact;
+  - initial tables: bit-exact (same float init law, reading c.6);
+  - per-triple scores and loss, FP32 path: |x - x_ref| <= 1e-5 * max(|x_ref|, S) (S = scale of the sum: sum of
+    |terms| for dot models, gamma + distance for distance models); loss plain relative 1e-5;
+  - embedding rows after 100 steps, FP32 path: <= 1e-4 absolute.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from paper_2004_08532_b200 import kge
+
+pytestmark = pytest.mark.gpu
+
+MODELS = ["transe_l1", "transe_l2", "distmult", "complex", "rotate"]
+
+
+def _pair(model, n_e, n_r, trip, dim, B, g, k, gamma=12.0, lr=0.1, seed=1, variant=0, precision="fp32",
+          corrupt="alternate", lazy=False, graph=None):
+    cfg = kge.Config(model=model, n_entities=n_e, n_relations=n_r, dim=dim, batch_size=B, chunk_size=g, neg_k=k,
+                     gamma=gamma, lr=lr, seed=seed, rotate_variant=variant, neg_precision=precision, corrupt=corrupt)
+    gpu = kge.init(cfg, *trip)
+    orc = O.Trainer(model, n_e, n_r, dim, B, g, k, gamma=gamma, lr=lr, seed=seed, rotate_variant=variant,
+                    corrupt={"tail": 0, "head": 1, "alternate": 2}[corrupt],
+                    triples=trip if graph is None else None, graph=graph, lazy_rows=lazy)
+    return gpu, orc
+
+
+def _tiny(model="transe_l2", dim=64, B=256, g=64, k=64, **kw):
+    gr = synth.graph("tiny")
+    trip = gr.triples()
+    return _pair(model, gr.n_entities, gr.n_relations, trip, dim, B, g, k, **kw) + (trip,)
+
+
+# ---------------------------------------------------------------- integer half: bit-exact
+@pytest.mark.parametrize("shape", [(256, 64, 64), (96, 24, 50), (64, 64, 64), (64, 1, 16), (1024, 256, 256)])
+def test_sampling_bit_exact(shape):
+    B, g, k = shape
+    gpu, orc, trip = _tiny(B=B, g=g, k=k)
+    for step in [0, 1, 2, 38, 39, 40, 1000, 123457]:  # N_t = 10,000, B=256: epoch boundary inside step 39
+        s = gpu.sample(step)
+        pos, neg, mode = orc.sample(step)
+        assert np.array_equal(s["pos"], pos), step
+        assert np.array_equal(s["neg"], neg), step
+        assert np.array_equal(s["mode"], mode), step
+        e_occ, r_occ = orc.occurrences(step)
+        ue, inv, _, _ = O.dedup(e_occ)
+        ur, invr, _, _ = O.dedup(r_occ)
+        assert np.array_equal(s["uniq_ent"], ue) and np.array_equal(s["inv_ent"], inv)
+        assert np.array_equal(s["uniq_rel"], ur) and np.array_equal(s["inv_rel"], invr)
+
+
+def test_sampling_fb15k_shape_bit_exact():
+    gr = synth.graph("fb15k")
+    trip = gr.triples()
+    gpu, orc = _pair("distmult", gr.n_entities, gr.n_relations, trip, 16, 1024, 256, 256)
+    for step in [0, 471, 472, 10_000]:  # 483,142 / 1024 = 471.8 steps per epoch
+        s = gpu.sample(step)
+        pos, neg, mode = orc.sample(step)
+        assert np.array_equal(s["pos"], pos) and np.array_equal(s["neg"], neg) and np.array_equal(s["mode"], mode)
+
+
+@pytest.mark.parametrize("model", MODELS)
+def test_init_bit_exact(model):
+    gpu, orc, _ = _tiny(model, dim=32)
+    ids = np.arange(1000)
+    assert np.array_equal(gpu.get_rows(0, ids), orc.get_rows(0, ids).astype(np.float32))
+    rids = np.arange(20)
+    assert np.array_equal(gpu.get_rows(1, rids), orc.get_rows(1, rids).astype(np.float32))
+    assert np.all(gpu.get_rows(3, ids) == 0)
+
+
+# ---------------------------------------------------------------- float half
+def _scale(model, orc, hs, rs, ts, gamma, f_ref):
+    E = lambda ids: orc.get_rows(0, ids)
+    R = orc.get_rows(1, rs)
+    h, t = E(hs), E(ts)
+    d = h.shape[1]
+    if model == "distmult":
+        return np.abs(h * R * t).sum(1)
+    if model == "complex":
+        n = d // 2
+        hr, hi, rr, ri, tr, ti = h[:, :n], h[:, n:], R[:, :n], R[:, n:], t[:, :n], t[:, n:]
+        return (np.abs(hr * rr * tr) + np.abs(hi * rr * ti) + np.abs(hr * ri * ti) + np.abs(hi * ri * tr)).sum(1)
+    return gamma + np.abs(gamma - f_ref)  # gamma + distance
+
+
+def _check_scores(model, gpu, orc, rng, n=2000, gamma=12.0, rtol=1e-5):
+    hs = rng.integers(0, orc.cfg.n_entities, n)
+    rs = rng.integers(0, orc.cfg.n_relations, n)
+    ts = rng.integers(0, orc.cfg.n_entities, n)
+    f = gpu.score(hs, rs, ts).astype(np.float64)
+    ref = orc.score_triples(hs, rs, ts)
+    S = _scale(model, orc, hs, rs, ts, gamma, ref)
+    err = np.abs(f - ref) / np.maximum(np.abs(ref), S)
+    assert err.max() <= rtol, (model, err.max())
+
+
+@pytest.mark.parametrize("model", MODELS)
+@pytest.mark.parametrize("variant", [0, 1])
+def test_train_parity_fp32_100_steps(model, variant):
+    if variant and model != "rotate":
+        pytest.skip("variant only for RotatE")
+    gpu, orc, trip = _tiny(model, dim=64, variant=variant)
+    rng = np.random.default_rng(0)
+    _check_scores(model, gpu, orc, rng)
+    lg = gpu.train_step(100)
+    lo = orc.train(100)
+    rel = np.abs(lg - lo) / np.abs(lo)
+    assert rel.max() <= 1e-5, (model, rel.max(), np.argmax(rel))
+    ids = np.arange(orc.cfg.n_entities)
+    dE = np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max()
+    rids = np.arange(orc.cfg.n_relations)
+    dR = np.abs(gpu.get_rows(1, rids) - orc.get_rows(1, rids)).max()
+    assert dE <= 1e-4 and dR <= 1e-4, (model, dE, dR)
+    _check_scores(model, gpu, orc, rng)
+    assert gpu.step == 100
+
+
+@pytest.mark.parametrize("model", ["transe_l2", "complex", "transe_l1"])
+@pytest.mark.parametrize("corrupt", ["tail", "head"])
+def test_train_parity_ragged_shapes(model, corrupt):
+    # ragged tiles: g, k not multiples of 64, d not a multiple of 32; single chunk per corruption side
+    gr = synth.graph("tiny")
+    trip = gr.triples()
+    d = 40 if model == "complex" else 44
+    gpu, orc = _pair(model, gr.n_entities, gr.n_relations, trip, d, 72, 24, 50, corrupt=corrupt, lr=0.05)
+    lg, lo = gpu.train_step(20), orc.train(20)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5
+    ids = np.arange(gr.n_entities)
+    assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 1e-4
+
+
+def test_train_batch_equals_sampled_step():
+    # kge_train_batch with the sampler's own positives reproduces kge_train_step exactly
+    gpu_a, _, trip = _tiny("distmult", dim=32)
+    gpu_b, _, _ = _tiny("distmult", dim=32)
+    h, r, t = [np.asarray(a) for a in trip]
+    for _ in range(5):
+        pos = gpu_b.sample(gpu_b.step)["pos"]
+        lb = gpu_b.train_batch(h[pos], r[pos], t[pos])
+        la = gpu_a.train_step(1)[0]
+        assert la == lb
+    ids = np.arange(1000)
+    assert np.array_equal(gpu_a.get_rows(0, ids), gpu_b.get_rows(0, ids))
+
+
+def test_deterministic():
+    a, _, _ = _tiny("rotate", dim=32)
+    b, _, _ = _tiny("rotate", dim=32)
+    la, lb = a.train_step(30), b.train_step(30)
+    assert np.array_equal(la, lb)
+    ids = np.arange(1000)
+    assert np.array_equal(a.get_rows(0, ids), b.get_rows(0, ids))
+
+
+def test_nonfinite_step_is_skipped():
+    gpu, _, _ = _tiny("transe_l2", dim=32)
+    s = gpu.sample(0)
+    bad = s["uniq_ent"][0]
+    row = gpu.get_rows(0, [bad])
+    row[0, 0] = np.nan
+    gpu.set_rows(0, [bad], row)
+    before = gpu.get_rows(0, np.arange(1000))
+    with pytest.raises(kge.KgeError) as ei:
+        gpu.train_step(1)
+    assert ei.value.status == -6
+    after = gpu.get_rows(0, np.arange(1000))
+    assert np.array_equal(np.isnan(before), np.isnan(after))
+    assert np.array_equal(np.nan_to_num(before), np.nan_to_num(after))
+
+
+def test_rows_roundtrip_and_range_errors():
+    gpu, _, _ = _tiny("complex", dim=32)
+    ids = np.array([0, 5, 999])
+    rows = np.random.default_rng(1).normal(size=(3, 32)).astype(np.float32)
+    gpu.set_rows(0, ids, rows)
+    assert np.array_equal(gpu.get_rows(0, ids), rows)
+    with pytest.raises(kge.KgeError) as ei:
+        gpu.get_rows(0, [1000])
+    assert ei.value.status == -2
+    with pytest.raises(kge.KgeError):
+        gpu.score([0], [20], [0])
+    with pytest.raises(kge.KgeError):
+        gpu.get_rows(2, [0])  # no projection table for ComplEx
