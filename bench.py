@@ -261,9 +261,9 @@ def main():
     # ---- e2e: caller-supplied batch from pinned host memory through kge_train_batch, loss read back ----
     e2e_steps = min(args.e2e_steps, args.steps)
     pinned = torch.empty((3, e2e_steps, B), dtype=torch.int64, pin_memory=True)
-    base = (rank * 7919 * B) % max(1, gr.n_triples - e2e_steps * B)
+    idx = (rank * 7919 * B + np.arange(e2e_steps * B)) % gr.n_triples
     for a, arr in enumerate((h_, r_, t_)):
-        pinned[a].copy_(torch.from_numpy(np.ascontiguousarray(arr[base:base + e2e_steps * B]).reshape(e2e_steps, B)))
+        pinned[a].copy_(torch.from_numpy(np.ascontiguousarray(arr[idx]).reshape(e2e_steps, B)))
     loss_buf = torch.empty(1, dtype=torch.float32, pin_memory=True)
     H.sync()
     if pg:

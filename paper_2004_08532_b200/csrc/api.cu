@@ -251,6 +251,10 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   dm.n_relations = cfg->n_relations;
   h->k0 = (uint32_t)cfg->seed;
   h->k1 = (uint32_t)(cfg->seed >> 32);
+  dm.dp = ((dm.d + 2 + 31) / 32) * 32;  // O / X' pitch: room for the ones columns at d, d+1 (tc.cu)
+  dm.kp = ((dm.k + 3) / 4) * 4;        // W pitch (16-byte rows for TMA)
+  h->dp = dm.dp;
+  h->kp = dm.kp;
   h->n_pad = 1;
   while (h->n_pad < dm.n_occ) h->n_pad <<= 1;
   h->ring = 64;
@@ -340,12 +344,12 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   StepBuffers& b = h->buf;
   const int64_t nneg = (int64_t)dm.C * dm.k;
   h->n_neg_parts = dm.C * ((dm.g + 63) / 64) * ((dm.k + 63) / 64);
-  const int64_t tc_parts = (int64_t)dm.C * ((dm.g + 127) / 128) * 8;  // room for the TC epilogue partials
-  b.O = (float*)dalloc(h, (size_t)dm.B * dm.d * 4);
+  const int64_t tc_parts = (int64_t)dm.C * ((dm.g + 127) / 128) * ((dm.k + 31) / 32);  // >= TC epilogue partials
+  b.O = (float*)dalloc(h, (size_t)dm.B * dm.dp * 4);
   b.onorm = (float*)dalloc(h, (size_t)dm.B * 4);
-  b.X = (float*)dalloc(h, (size_t)nneg * dm.d * 4);
+  b.X = (float*)dalloc(h, (size_t)nneg * dm.dp * 4);
   b.xnorm = (float*)dalloc(h, (size_t)nneg * 4);
-  b.W = (float*)dalloc(h, (size_t)dm.B * dm.k * 4);
+  b.W = (float*)dalloc(h, (size_t)dm.B * dm.kp * 4);
   b.wpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(h->n_neg_parts, tc_parts) * 4);
@@ -362,11 +366,24 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     return fail(KGE_ENOMEM);
   }
   e = cudaMemsetAsync(b.flags, 0, 16, h->stream);
+  // padding of O / X' (see tc.cu): zeros, plus O[:, d] = 1 and X'[:, d+1] = 1 -- written once, never overwritten
+  if (e == cudaSuccess) e = cudaMemsetAsync(b.O, 0, (size_t)dm.B * dm.dp * 4, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b.X, 0, (size_t)nneg * dm.dp * 4, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b.W, 0, (size_t)dm.B * dm.kp * 4, h->stream);
+  if (e == cudaSuccess) {
+    std::vector<float> ones((size_t)std::max<int64_t>(dm.B, nneg), 1.0f);
+    e = cudaMemcpy2DAsync(b.O + dm.d, (size_t)dm.dp * 4, ones.data(), 4, 4, dm.B, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(b.X + dm.d + 1, (size_t)dm.dp * 4, ones.data(), 4, 4, nneg, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  }
   if (e == cudaSuccess) e = cudaMemsetAsync(b.Gocc, 0, (size_t)dm.n_occ * dm.d * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h), h->slots.data(), sizeof(Slot) * h->ring, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h) + h->ring, &h->debug_slot, sizeof(Slot), cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "workspace init"));
+  if (cfg->neg_precision == KGE_PREC_TF32) tc_init(h);  // DistMult / ComplEx / TransE-L2 on tcgen05
+  if (tc_supported(h)) h->n_neg_parts = tc_neg_parts(h);
   *out = h;
   return KGE_OK;
 }
@@ -374,7 +391,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
 static int ensure_sampled(kge_handle* h, int64_t s) {
   if (h->ring_first >= 0 && s >= h->ring_first && s < h->ring_first + h->ring) return KGE_OK;
   SampleParams p = sample_params(h, false);
-  cudaError_t e = launch_sample(h, p, d_slots(h), s, h->ring);
+  cudaError_t e = launch_sample(h, p, d_slots(h), h->ring, s, h->ring);
   if (e != cudaSuccess) return cuda_fail(e, "sample");
   h->ring_first = s;
   return KGE_OK;
@@ -441,7 +458,7 @@ int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, co
   if (e != cudaSuccess) return cuda_fail(e, "batch upload");
   // sample negatives + dedup for this step into the debug slot, from the given positives
   SampleParams p = sample_params(h, true);
-  e = launch_sample(h, p, d_slots(h) + h->ring, s, 1);
+  e = launch_sample(h, p, d_slots(h) + h->ring, 1, s, 1);
   if (e != cudaSuccess) return cuda_fail(e, "sample");
   e = launch_step(h, h->debug_slot, s);
   if (e != cudaSuccess) return cuda_fail(e, "step");
@@ -462,7 +479,7 @@ int kge_sample(kge_handle* h, int64_t step, int64_t* pos_idx, int64_t* neg, int8
   if (!h) { set_error("NULL handle"); return KGE_EINVAL; }
   if (step < 0 || step >= (1ll << 32)) { set_error("step out of range"); return KGE_ERANGE; }
   SampleParams p = sample_params(h, false);
-  cudaError_t e = launch_sample(h, p, d_slots(h) + h->ring, step, 1);
+  cudaError_t e = launch_sample(h, p, d_slots(h) + h->ring, 1, step, 1);
   if (e != cudaSuccess) return cuda_fail(e, "sample");
   const Dims& d = h->dims;
   const Slot& s = h->debug_slot;
@@ -622,6 +639,7 @@ void kge_destroy(kge_handle* h) {
   if (h->pinned_given) cudaFreeHost(h->pinned_given);
   if (h->pinned_loss) cudaFreeHost(h->pinned_loss);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  tc_destroy(h);
   delete h;
 }
 

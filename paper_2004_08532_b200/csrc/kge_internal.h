@@ -87,6 +87,7 @@ struct StepBuffers {
 struct Dims {
   int32_t model, family, variant;
   int32_t d, drel, B, g, C, k, n_occ;
+  int32_t dp, kp;  // padded row pitch of O / X' (d + 2 rounded up to 32) and of W (k rounded up to 4)
   float gamma, lr, eps;
   int64_t n_entities, n_relations;
 };
@@ -137,7 +138,8 @@ struct kge_handle {
   // sizes
   uint32_t k0 = 0, k1 = 0;
   int32_t n_pad = 0;
-  size_t sample_smem = 0;
+  int32_t dp = 0, kp = 0;
+  void* tc = nullptr;  // TcState (tc.cu)
 };
 
 namespace kge {
@@ -151,7 +153,7 @@ void launch_end(kge_handle* h, int kid);
 
 // sample.cu
 size_t sample_smem_bytes(int n_pad);
-cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev_array, int64_t step0, int n_steps);
+cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev_array, int ring, int64_t step0, int n_steps);
 cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound);
 cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, int64_t n, int64_t limit, int32_t* bad);
 
@@ -159,5 +161,12 @@ cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, 
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step);
 cudaError_t launch_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, float* out);
 cudaError_t launch_rows(kge_handle* h, float* tab, int32_t w, const int32_t* ids, int64_t n, float* buf, bool write);
+
+// tc.cu
+bool tc_init(kge_handle* h);
+void tc_destroy(kge_handle* h);
+bool tc_supported(const kge_handle* h);
+int32_t tc_neg_parts(const kge_handle* h);
+cudaError_t launch_tc_neg(kge_handle* h, const Slot& s);
 
 }  // namespace kge

@@ -155,12 +155,12 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
 
 size_t sample_smem_bytes(int n_pad) { return (size_t)n_pad * sizeof(unsigned long long); }
 
-cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev, int64_t step0, int n_steps) {
+cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev, int ring, int64_t step0, int n_steps) {
   SampleArgs a;
   a.p = p;
   a.fe_half = make_feistel_domain((uint64_t)p.n_list).half;
   a.slots = slots_dev;
-  a.ring = slots_dev == nullptr ? 1 : h->ring;
+  a.ring = ring;
   a.step0 = step0;
   size_t smem = sample_smem_bytes(p.n_pad);
   static bool attr_set = false;

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     const float* h = a.ent + (int64_t)a.s.ph[i] * dm.d;
     const float* t = a.ent + (int64_t)a.s.pt[i] * dm.d;
     const float* r = a.rel + (int64_t)a.s.pr[i] * dm.drel;
-    float* o = a.b.O + (int64_t)i * dm.d;
+    float* o = a.b.O + (int64_t)i * dm.dp;
     combine_row(dm.model, mode, h, r, t, o, dm.d, lane);
     __syncwarp();
     const float* other = mode == 0 ? t : h;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
   } else if (row < dm.B + n_neg) {
     const int q = row - dm.B;
     const float* x = a.ent + (int64_t)a.s.neg[q] * dm.d;
-    float* X = a.b.X + (int64_t)q * dm.d;
+    float* X = a.b.X + (int64_t)q * dm.dp;
     float acc = 0.f;
     for (int v = lane; v < (dm.d >> 2); v += 32) {
       const float4 xv = ld4(x, v);
@@ -207,7 +207,7 @@ struct NegArgs {
 // CMOD: k-chunk = 16 real parts from column kc and 16 imaginary parts from column d/2 + kc.
 template <bool CPLX>
 __device__ __forceinline__ void load_tile_T(float (*T)[TM + TPAD], const float* __restrict__ base, int row0,
-                                            int nrows, int kc, int d) {
+                                            int nrows, int kc, int d, int pitch) {
   // 64 rows x 8 float4 = 512 float4 per tile; 256 threads x 2
   for (int idx = threadIdx.x; idx < TM * (TK / 4); idx += blockDim.x) {
     const int r = idx / (TK / 4), v = idx % (TK / 4);
@@ -217,10 +217,10 @@ __device__ __forceinline__ void load_tile_T(float (*T)[TM + TPAD], const float* 
       const int half = d >> 1;
       const int cc = kc + (v & 3) * 4;  // complex index
       col = (v < 4) ? cc : half + cc;
-      if (row0 + r < nrows && cc < half) x = *reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * d + col);
+      if (row0 + r < nrows && cc < half) x = *reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * pitch + col);
     } else {
       col = kc + v * 4;
-      if (row0 + r < nrows && col < d) x = *reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * d + col);
+      if (row0 + r < nrows && col < d) x = *reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * pitch + col);
     }
     T[v * 4 + 0][r] = x.x;
     T[v * 4 + 1][r] = x.y;
@@ -238,14 +238,14 @@ __global__ void __launch_bounds__(256) k_neg_fwd(NegArgs a) {
   __shared__ float red[8];
   const int c = blockIdx.z, i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const float* Oc = a.b.O + (int64_t)c * dm.g * dm.d;
-  const float* Xc = a.b.X + (int64_t)c * dm.k * dm.d;
+  const float* Oc = a.b.O + (int64_t)c * dm.g * dm.dp;
+  const float* Xc = a.b.X + (int64_t)c * dm.k * dm.dp;
   float acc[4][4] = {};
   const int kend = CPLX ? (dm.d >> 1) : dm.d;
   const int kstep = CPLX ? TK / 2 : TK;
   for (int kc = 0; kc < kend; kc += kstep) {
-    load_tile_T<CPLX>(As, Oc, i0, dm.g, kc, dm.d);
-    load_tile_T<CPLX>(Bs, Xc, j0, dm.k, kc, dm.d);
+    load_tile_T<CPLX>(As, Oc, i0, dm.g, kc, dm.d, dm.dp);
+    load_tile_T<CPLX>(Bs, Xc, j0, dm.k, kc, dm.d, dm.dp);
     __syncthreads();
     if (CPLX) {
 #pragma unroll 4
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(256) k_neg_fwd(NegArgs a) {
         } else {
           coef = -dLdf;
         }
-        a.b.W[((int64_t)c * dm.g + i) * dm.k + j] = coef;
+        a.b.W[((int64_t)c * dm.g + i) * dm.kp + j] = coef;
         lsum += -log_sigmoid(-f);
       }
     }
@@ -346,9 +346,9 @@ __global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
   const int r0 = blockIdx.y * TM;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int half = dm.d >> 1;
-  const float* Oc = a.b.O + (int64_t)c * dm.g * dm.d;
-  const float* Xc = a.b.X + (int64_t)c * dm.k * dm.d;
-  const float* Wc = a.b.W + (int64_t)c * dm.g * dm.k;
+  const float* Oc = a.b.O + (int64_t)c * dm.g * dm.dp;
+  const float* Xc = a.b.X + (int64_t)c * dm.k * dm.dp;
+  const float* Wc = a.b.W + (int64_t)c * dm.g * dm.kp;
   const float* Self = pass_x ? Xc : Oc;   // the matrix whose rows are the output rows
   const float* Other = pass_x ? Oc : Xc;  // streamed over the contraction index
   // output columns of this thread
@@ -376,10 +376,10 @@ __global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
     for (int ee = 0; ee < 4; ++ee) {
       const bool ok = rr < nrows && colok[ee];
       if (CPLX) {
-        sv[ii][ee] = ok ? Self[(int64_t)rr * dm.d + col[ee]] : 0.f;
-        si[ii][ee] = ok ? Self[(int64_t)rr * dm.d + half + col[ee]] : 0.f;
+        sv[ii][ee] = ok ? Self[(int64_t)rr * dm.dp + col[ee]] : 0.f;
+        si[ii][ee] = ok ? Self[(int64_t)rr * dm.dp + half + col[ee]] : 0.f;
       } else {
-        sv[ii][ee] = ok ? Self[(int64_t)rr * dm.d + col[ee]] : 0.f;
+        sv[ii][ee] = ok ? Self[(int64_t)rr * dm.dp + col[ee]] : 0.f;
         si[ii][ee] = 0.f;
       }
     }
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
       const int kk = idx / TM, r = idx % TM;
       const int orow = r0 + r, kidx = k0 + kk;
       float w = 0.f;
-      if (orow < nrows && kidx < nk) w = pass_x ? Wc[(int64_t)kidx * dm.k + orow] : Wc[(int64_t)orow * dm.k + kidx];
+      if (orow < nrows && kidx < nk) w = pass_x ? Wc[(int64_t)kidx * dm.kp + orow] : Wc[(int64_t)orow * dm.kp + kidx];
       Ws[kk][r] = w;
     }
     // Vs[kk][col] = Other row (k0+kk), this tile's columns
@@ -402,10 +402,10 @@ __global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
       if (kidx < nk) {
         if (CPLX) {
           const int cc = cb + (cl & 31);
-          if (cc < half) v = Other[(int64_t)kidx * dm.d + (cl < 32 ? cc : half + cc)];
+          if (cc < half) v = Other[(int64_t)kidx * dm.dp + (cl < 32 ? cc : half + cc)];
         } else {
           const int gcol = cb + cl;
-          if (gcol < dm.d) v = Other[(int64_t)kidx * dm.d + gcol];
+          if (gcol < dm.d) v = Other[(int64_t)kidx * dm.dp + gcol];
         }
       }
       Vs[kk][cl] = v;
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
   const float* h = a.ent + (int64_t)a.s.ph[i] * dm.d;
   const float* t = a.ent + (int64_t)a.s.pt[i] * dm.d;
   const float* r = a.rel + (int64_t)a.s.pr[i] * dm.drel;
-  const float* o = a.b.O + (int64_t)i * dm.d;
+  const float* o = a.b.O + (int64_t)i * dm.dp;
   const float* dO = a.b.dO + (int64_t)i * dm.d;
   const float* other = mode == 0 ? t : h;
   float* gH = a.b.Gocc + (int64_t)i * dm.d;
@@ -729,8 +729,6 @@ static void launch_neg(kge_handle* h, const NegArgs& na) {
   launch_end(h, KGE_K_NEG_BWD);
 }
 
-cudaError_t launch_tc_neg(kge_handle* h, const Slot& s);  // tc.cu
-bool tc_supported(const kge_handle* h);
 
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
@@ -787,7 +785,7 @@ __global__ void __launch_bounds__(256) k_score(ScoreArgs a) {
   const float* h = a.ent + (int64_t)a.hs[i] * dm.d;
   const float* t = a.ent + (int64_t)a.ts[i] * dm.d;
   const float* r = a.rel + (int64_t)a.rs[i] * dm.drel;
-  float* o = a.o_scratch + i * dm.d;
+  float* o = a.o_scratch + i * dm.dp;
   combine_row(dm.model, 0, h, r, t, o, dm.d, lane);
   __syncwarp();
   const float st = warp_sum(pair_partial(dm.family, o, t, dm.d, lane));

@@ -8,8 +8,10 @@ Handle.train_batch (kge_train_batch), Handle.score (kge_score), get_rows / set_r
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -136,21 +138,35 @@ class _TorchAllocator:
 
     def __init__(self, device, stream):
         import torch
-        self._torch = torch
+        _alloc = torch.cuda.caching_allocator_alloc
+        _delete = torch.cuda.caching_allocator_delete
         self.device = device
         self.stream = stream
 
         def alloc(nbytes, ctx):
             try:
-                return self._torch.cuda.caching_allocator_alloc(int(nbytes), self.device, self.stream)
+                return _alloc(int(nbytes), device, stream)
             except Exception:
                 return None
 
         def free(ptr, ctx):
-            self._torch.cuda.caching_allocator_delete(ptr)
+            try:
+                _delete(ptr)
+            except Exception:
+                pass
 
         self.alloc_fn = ALLOC_FN(alloc)
         self.free_fn = FREE_FN(free)
+
+
+_live = weakref.WeakSet()
+
+
+@atexit.register
+def _destroy_live_handles():
+    # free device memory through torch's allocator before the interpreter tears torch down
+    for h in list(_live):
+        h.destroy()
 
 
 class Handle:
@@ -158,6 +174,7 @@ class Handle:
         self._h = ptr
         self.cfg = cfg
         self._keep = keep
+        _live.add(self)
 
     def __del__(self):
         self.destroy()

@@ -105,7 +105,14 @@ def _check_scores(model, gpu, orc, rng, n=2000, gamma=12.0, rtol=1e-5):
 def test_train_parity_fp32_100_steps(model, variant):
     if variant and model != "rotate":
         pytest.skip("variant only for RotatE")
-    gpu, orc, trip = _tiny(model, dim=64, variant=variant)
+    if model == "transe_l1":
+        # sgn(h+r-t) is discontinuous: over 100 free-running steps of 256x64 pairs x 64 dims, some |h+r-t| falls below
+        # one fp32 ulp, the fp32 and fp64 sign decisions legitimately differ, and Adagrad amplifies the flip
+        # (reading R-L1). The free-running bar is applied at a shape with ~100x fewer pair-coordinates;
+        # the full shape is gated step by step in test_train_parity_teacher_forced.
+        gpu, orc, trip = _tiny(model, dim=32, B=64, g=16, k=16)
+    else:
+        gpu, orc, trip = _tiny(model, dim=64, variant=variant)
     rng = np.random.default_rng(0)
     _check_scores(model, gpu, orc, rng)
     lg = gpu.train_step(100)
@@ -119,6 +126,24 @@ def test_train_parity_fp32_100_steps(model, variant):
     assert dE <= 1e-4 and dR <= 1e-4, (model, dE, dR)
     _check_scores(model, gpu, orc, rng)
     assert gpu.step == 100
+
+
+@pytest.mark.parametrize("model", MODELS)
+def test_train_parity_teacher_forced(model):
+    # every step starts from the oracle's tables (rounded to fp32): one step's loss and updated rows must match;
+    # 100 consecutive steps at the full C0 shape (several tiles per chunk side: g = k = 64, d = 64)
+    gpu, orc, trip = _tiny(model, dim=64)
+    ids, rids = np.arange(orc.cfg.n_entities), np.arange(orc.cfg.n_relations)
+    worst_row, worst_loss = 0.0, 0.0
+    for s in range(100):
+        for tab, ii in ((0, ids), (1, rids), (3, ids), (4, rids)):
+            gpu.set_rows(tab, ii, orc.get_rows(tab, ii))
+        lg = gpu.train_step(1)[0]
+        lo = orc.train(1)[0]
+        worst_loss = max(worst_loss, abs(lg - lo) / abs(lo))
+        worst_row = max(worst_row, np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max(),
+                        np.abs(gpu.get_rows(1, rids) - orc.get_rows(1, rids)).max())
+    assert worst_loss <= 1e-5 and worst_row <= 1e-4, (model, worst_loss, worst_row)
 
 
 @pytest.mark.parametrize("model", ["transe_l2", "complex", "transe_l1"])
@@ -187,3 +212,49 @@ def test_rows_roundtrip_and_range_errors():
         gpu.score([0], [20], [0])
     with pytest.raises(kge.KgeError):
         gpu.get_rows(2, [0])  # no projection table for ComplEx
+
+
+# ---------------------------------------------------------------- tcgen05 (TF32) path: <= 2e-3 relative
+TC_MODELS = ["transe_l2", "distmult", "complex"]
+
+
+@pytest.mark.parametrize("model", TC_MODELS)
+@pytest.mark.parametrize("shape", [(256, 64, 64, 64), (1024, 256, 256, 400), (72, 24, 50, 48), (128, 128, 200, 96)])
+def test_tc_train_parity(model, shape):
+    B, g, k, d = shape
+    gr = synth.graph("tiny")
+    trip = gr.triples()
+    gpu, orc = _pair(model, gr.n_entities, gr.n_relations, trip, d, B, g, k, precision="tf32")
+    n = 30 if B >= 1024 else 100
+    lg, lo = gpu.train_step(n), orc.train(n)
+    rel = np.abs(lg - lo) / np.abs(lo)
+    assert rel.max() <= 2e-3, (model, shape, rel.max(), int(np.argmax(rel)))
+    ids = np.arange(gr.n_entities)
+    drift = np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max()
+    print(f"tf32 {model} {shape}: loss rel max {rel.max():.2e}, row drift after {n} steps {drift:.2e}")
+
+
+@pytest.mark.parametrize("model", TC_MODELS)
+def test_tc_teacher_forced_rows(model):
+    gpu, orc, trip = _tiny(model, dim=64, precision="tf32")
+    ids, rids = np.arange(orc.cfg.n_entities), np.arange(orc.cfg.n_relations)
+    worst_row, worst_loss = 0.0, 0.0
+    for s in range(30):
+        for tab, ii in ((0, ids), (1, rids), (3, ids), (4, rids)):
+            gpu.set_rows(tab, ii, orc.get_rows(tab, ii))
+        lg = gpu.train_step(1)[0]
+        lo = orc.train(1)[0]
+        worst_loss = max(worst_loss, abs(lg - lo) / abs(lo))
+        worst_row = max(worst_row, np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max())
+    # rows are not gated by the north_star on the TC path (reading c.14); this bound documents the TF32 effect: a
+    # ~2^-11 relative error in the gradient terms, magnified where a coordinate's sum cancels, times the O(lr) Adagrad
+    # first-touch step
+    assert worst_loss <= 2e-3 and worst_row <= 5e-3, (model, worst_loss, worst_row)
+
+
+def test_tc_matches_fp32_path_closely():
+    # same step on both negative-contraction paths: the TF32 result is within TF32 error of the FFMA result
+    a, _, _ = _tiny("distmult", dim=64, precision="tf32")
+    b, _, _ = _tiny("distmult", dim=64, precision="fp32")
+    la, lb = a.train_step(5), b.train_step(5)
+    assert np.max(np.abs(la - lb) / np.abs(lb)) <= 2e-3
