@@ -352,6 +352,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.W = (float*)dalloc(h, (size_t)dm.B * dm.kp * 4);
   b.wpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
+  b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(h->n_neg_parts, tc_parts) * 4);
   b.rowsumW = (float*)dalloc(h, (size_t)dm.B * 4);
   b.colsumW = (float*)dalloc(h, (size_t)nneg * 4);
@@ -360,7 +361,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.Grel = (float*)dalloc(h, (size_t)dm.B * dm.drel * 4);
   b.loss = (float*)dalloc(h, (size_t)h->ring * 4);
   b.flags = (int32_t*)dalloc(h, 16 + sizeof(Slot) * (h->ring + 1));  // flags[4] then the slot table
-  if (!b.O || !b.onorm || !b.X || !b.xnorm || !b.W || !b.wpos || !b.lpos || !b.lneg || !b.rowsumW || !b.colsumW ||
+  if (!b.O || !b.onorm || !b.X || !b.xnorm || !b.W || !b.wpos || !b.lpos || !b.pstat || !b.lneg || !b.rowsumW || !b.colsumW ||
       !b.dO || !b.Gocc || !b.Grel || !b.loss || !b.flags) {
     set_error("out of device memory (workspace)");
     return fail(KGE_ENOMEM);

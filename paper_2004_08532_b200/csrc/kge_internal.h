@@ -73,6 +73,7 @@ struct StepBuffers {
   float* W;        // [B x k] dL/dS coefficient (C chunks of g x k)
   float* wpos;     // [B] dL/df+
   float* lpos;     // [B] per-positive loss term
+  float* pstat;    // [B] pair statistic of each positive (L2: squared distance)
   float* lneg;     // [n_neg_parts] per-tile negative loss partials
   float* rowsumW;  // [B]
   float* colsumW;  // [C*k]

@@ -36,8 +36,13 @@ __device__ __forceinline__ void st4(float* p, int v, float4 x) { reinterpret_cas
 __device__ __forceinline__ bool is_complex_model(int model) { return model == KGE_COMPLEX || model == KGE_ROTATE; }
 
 // o = combine(h, r) (mode 0, tail corruption) or combine'(r, t) (mode 1, head corruption); reading c.8 table.
+// While writing o it accumulates (per lane) the pair statistic of o against `other` (family `fam`, see pair_partial)
+// and ||o||^2, so callers need no second pass over o.
 __device__ void combine_row(int model, int mode, const float* __restrict__ h, const float* __restrict__ r,
-                            const float* __restrict__ t, float* __restrict__ o, int d, int lane) {
+                            const float* __restrict__ t, float* __restrict__ o, int d, int lane,
+                            const float* __restrict__ other, int fam, float& stat, float& onorm) {
+  stat = 0.f;
+  onorm = 0.f;
   if (!is_complex_model(model)) {
     const int d4 = d >> 2;
     for (int v = lane; v < d4; v += 32) {
@@ -56,6 +61,17 @@ __device__ void combine_row(int model, int mode, const float* __restrict__ h, co
         }
       }
       st4(o, v, ov);
+      const float4 xv = ld4(other, v);
+      onorm += ov.x * ov.x + ov.y * ov.y + ov.z * ov.z + ov.w * ov.w;
+      if (fam == FAM_DOT) {
+        stat += ov.x * xv.x + ov.y * xv.y + ov.z * xv.z + ov.w * xv.w;
+      } else if (fam == FAM_L1) {
+        stat += fabsf(ov.x - xv.x) + fabsf(ov.y - xv.y) + fabsf(ov.z - xv.z) + fabsf(ov.w - xv.w);
+      } else {
+        float4 u;
+        F4MAP(u, ov, xv, A - Bv);
+        stat += u.x * u.x + u.y * u.y + u.z * u.z + u.w * u.w;
+      }
     }
     return;
   }
@@ -101,6 +117,21 @@ __device__ void combine_row(int model, int mode, const float* __restrict__ h, co
     oi = make_float4(outi[0], outi[1], outi[2], outi[3]);
     st4(o, v, orr);
     st4(o, v + n4, oi);
+    const float4 xr4 = ld4(other, v), xi4 = ld4(other, v + n4);
+    const float xr_[4] = {xr4.x, xr4.y, xr4.z, xr4.w}, xi_[4] = {xi4.x, xi4.y, xi4.z, xi4.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      onorm += outr[u] * outr[u] + outi[u] * outi[u];
+      const float ur = outr[u] - xr_[u], ui = outi[u] - xi_[u];
+      if (fam == FAM_DOT)
+        stat += outr[u] * xr_[u] + outi[u] * xi_[u];
+      else if (fam == FAM_CMOD)
+        stat += sqrtf(ur * ur + ui * ui);
+      else if (fam == FAM_L1)
+        stat += fabsf(ur) + fabsf(ui);
+      else
+        stat += ur * ur + ui * ui;
+    }
   }
 }
 
@@ -166,12 +197,12 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     const float* t = a.ent + (int64_t)a.s.pt[i] * dm.d;
     const float* r = a.rel + (int64_t)a.s.pr[i] * dm.drel;
     float* o = a.b.O + (int64_t)i * dm.dp;
-    combine_row(dm.model, mode, h, r, t, o, dm.d, lane);
-    __syncwarp();
-    const float* other = mode == 0 ? t : h;
-    const float stat = warp_sum(pair_partial(dm.family, o, other, dm.d, lane));
-    const float on = warp_sum(pair_partial(FAM_DOT, o, o, dm.d, lane));
+    float stat, on;
+    combine_row(dm.model, mode, h, r, t, o, dm.d, lane, mode == 0 ? t : h, dm.family, stat, on);
+    stat = warp_sum(stat);
+    on = warp_sum(on);
     if (lane == 0) {
+      a.b.pstat[i] = stat;
       const float f = pair_score_from(dm.family, stat, dm.gamma);
       a.b.wpos[i] = -sigmoid(-f) / (float)dm.B;  // dL/df+ (reading c.9)
       a.b.lpos[i] = -log_sigmoid(f);
@@ -527,10 +558,7 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
   float* gOther = mode == 0 ? gT : gH;  // the non-combined side
   const float wp = a.b.wpos[i];
   float scale = wp;
-  if (dm.family == FAM_L2) {
-    const float st = warp_sum(pair_partial(FAM_L2, o, other, dm.d, lane));
-    scale = wp / fmaxf(sqrtf(st), 1e-12f);
-  }
+  if (dm.family == FAM_L2) scale = wp / fmaxf(sqrtf(a.b.pstat[i]), 1e-12f);
   const int model = dm.model;
   if (!is_complex_model(model)) {
     const int d4 = dm.d >> 2;
@@ -649,66 +677,124 @@ struct UpdateArgs {
   StepBuffers b;
 };
 
-constexpr int kMaxV = 8;  // float4 per lane: rows up to 32*8*4 = 1024 floats
+// Segment sum of one unique row's occurrence gradients, in sorted-occurrence order, V float4 per lane.
+// Loads of UNR consecutive occurrences are issued together (memory-level parallelism); the additions still happen
+// in occurrence order, so the sum is the same as a serial loop.
+template <int V>
+struct RowAcc {
+  float4 g[V];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int m = 0; m < V; ++m) g[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __device__ __forceinline__ void add(const float4& x, int m) {
+    g[m].x += x.x; g[m].y += x.y; g[m].z += x.z; g[m].w += x.w;
+  }
+};
 
-__device__ __forceinline__ void seg_adagrad(float* __restrict__ row, float* __restrict__ st,
-                                            const float* __restrict__ G, const int32_t* __restrict__ occ, int p0,
-                                            int p1, int w, float lr, float eps, int lane) {
-  const int w4 = w >> 2;
-  float4 g[kMaxV];
+template <int V>
+__device__ __forceinline__ void seg_sum(RowAcc<V>& acc, const float* __restrict__ G, const int32_t* __restrict__ occ,
+                                        int p0, int p1, int pstep, int w4, int w, int lane) {
+  constexpr int UNR = 4;
+  for (int p = p0; p < p1; p += UNR * pstep) {
+    float4 x[UNR][V];
 #pragma unroll
-  for (int m = 0; m < kMaxV; ++m) g[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int p = p0; p < p1; ++p) {
-    const float* src = G + (int64_t)occ[p] * w;
+    for (int u = 0; u < UNR; ++u) {
+      const int pp = p + u * pstep;
+      const float* src = pp < p1 ? G + (int64_t)__ldg(occ + pp) * w : nullptr;
 #pragma unroll
-    for (int m = 0; m < kMaxV; ++m) {
-      const int v = lane + 32 * m;
-      if (v < w4) {
-        const float4 x = ld4(src, v);
-        g[m].x += x.x; g[m].y += x.y; g[m].z += x.z; g[m].w += x.w;
+      for (int m = 0; m < V; ++m) {
+        const int v = lane + 32 * m;
+        x[u][m] = (src && v < w4) ? ld4(src, v) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+      for (int m = 0; m < V; ++m) acc.add(x[u][m], m);
   }
+}
+
+// Adagrad on one row given its summed gradient (reading c.11): state += mean(G^2); row -= lr G / sqrt(state + eps).
+// row_v / st0 were prefetched before the segment sum.
+template <int V>
+__device__ __forceinline__ void adagrad_row(float* __restrict__ row, float* __restrict__ st, const RowAcc<V>& acc,
+                                            float4 (&row_v)[V], float st0, int w4, int w, float lr, float eps,
+                                            int lane) {
   float sq = 0.f;
 #pragma unroll
-  for (int m = 0; m < kMaxV; ++m)
-    if (lane + 32 * m < w4) sq += g[m].x * g[m].x + g[m].y * g[m].y + g[m].z * g[m].z + g[m].w * g[m].w;
+  for (int m = 0; m < V; ++m)
+    if (lane + 32 * m < w4)
+      sq += acc.g[m].x * acc.g[m].x + acc.g[m].y * acc.g[m].y + acc.g[m].z * acc.g[m].z + acc.g[m].w * acc.g[m].w;
   sq = warp_sum(sq);
-  float s = 0.f;
-  if (lane == 0) {
-    s = *st + sq / (float)w;
-    *st = s;
-  }
-  s = __shfl_sync(0xffffffffu, s, 0);
+  const float s = st0 + sq / (float)w;
+  if (lane == 0) *st = s;
   const float step = lr / sqrtf(s + eps);
 #pragma unroll
-  for (int m = 0; m < kMaxV; ++m) {
+  for (int m = 0; m < V; ++m) {
     const int v = lane + 32 * m;
     if (v < w4) {
-      float4 x = ld4(row, v);
-      x.x -= step * g[m].x; x.y -= step * g[m].y; x.z -= step * g[m].z; x.w -= step * g[m].w;
+      float4 x = row_v[m];
+      x.x -= step * acc.g[m].x; x.y -= step * acc.g[m].y; x.z -= step * acc.g[m].z; x.w -= step * acc.g[m].w;
       st4(row, v, x);
     }
   }
 }
 
-__global__ void __launch_bounds__(256) k_update(UpdateArgs a) {
+template <int V>
+__device__ __forceinline__ void prefetch_row(const float* __restrict__ row, float4 (&row_v)[V], int w4, int lane) {
+#pragma unroll
+  for (int m = 0; m < V; ++m) {
+    const int v = lane + 32 * m;
+    row_v[m] = v < w4 ? ld4(row, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// Grid: [n_ent_blocks blocks: 8 warps, one unique entity row per warp] + [B blocks: one unique relation per CTA,
+// its occurrences strided over the 8 warps (hub relations carry ~10% of a Zipf batch), partials combined in fixed
+// warp order -> deterministic].
+template <int V>
+__global__ void __launch_bounds__(256) k_update(UpdateArgs a, int n_ent_blocks) {
   const Dims& dm = a.dm;
   if (a.b.flags[1]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
-  const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w < dm.n_occ) {
-    if (w >= *a.s.ent_n) return;
-    const int32_t id = a.s.ent_uniq[w];
-    seg_adagrad(a.ent + (int64_t)id * dm.d, a.ent_st + id, a.b.Gocc, a.s.ent_occ, a.s.ent_off[w], a.s.ent_off[w + 1],
-                dm.d, dm.lr, dm.eps, lane);
-  } else {
-    const int u = w - dm.n_occ;
-    if (u >= *a.s.rel_n) return;
-    const int32_t id = a.s.rel_uniq[u];
-    seg_adagrad(a.rel + (int64_t)id * dm.drel, a.rel_st + id, a.b.Grel, a.s.rel_occ, a.s.rel_off[u],
-                a.s.rel_off[u + 1], dm.drel, dm.lr, dm.eps, lane);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if ((int)blockIdx.x < n_ent_blocks) {
+    const int u = blockIdx.x * 8 + warp;
+    if (u >= *a.s.ent_n) return;
+    const int32_t id = a.s.ent_uniq[u];
+    const int w4 = dm.d >> 2;
+    float* row = a.ent + (int64_t)id * dm.d;
+    float4 row_v[V];
+    prefetch_row<V>(row, row_v, w4, lane);
+    const float st0 = a.ent_st[id];
+    RowAcc<V> acc;
+    acc.zero();
+    seg_sum<V>(acc, a.b.Gocc, a.s.ent_occ, a.s.ent_off[u], a.s.ent_off[u + 1], 1, w4, dm.d, lane);
+    adagrad_row<V>(row, a.ent_st + id, acc, row_v, st0, w4, dm.d, dm.lr, dm.eps, lane);
+    return;
   }
+  const int u = blockIdx.x - n_ent_blocks;
+  if (u >= *a.s.rel_n) return;  // uniform per CTA
+  __shared__ float4 part[8][32 * V];
+  const int32_t id = a.s.rel_uniq[u];
+  const int w = dm.drel, w4 = w >> 2;
+  float* row = a.rel + (int64_t)id * w;
+  float4 row_v[V];
+  if (warp == 0) prefetch_row<V>(row, row_v, w4, lane);
+  const float st0 = a.rel_st[id];
+  RowAcc<V> acc;
+  acc.zero();
+  seg_sum<V>(acc, a.b.Grel, a.s.rel_occ, a.s.rel_off[u] + warp, a.s.rel_off[u + 1], 8, w4, w, lane);
+#pragma unroll
+  for (int m = 0; m < V; ++m) part[warp][lane + 32 * m] = acc.g[m];
+  __syncthreads();
+  if (warp != 0) return;
+  RowAcc<V> tot;
+  tot.zero();
+  for (int ww = 0; ww < 8; ++ww)
+#pragma unroll
+    for (int m = 0; m < V; ++m) tot.add(part[ww][lane + 32 * m], m);
+  adagrad_row<V>(row, a.rel_st + id, tot, row_v, st0, w4, w, dm.lr, dm.eps, lane);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -757,9 +843,18 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   launch_end(h, KGE_K_CHAIN);
 
   UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, h->buf};
-  const int warps = dm.n_occ + dm.B;
+  const int n_ent_blocks = (dm.n_occ + 7) / 8;
+  const int grid = n_ent_blocks + dm.B;
+  const int w4 = dm.d / 4;
   launch_begin(h, KGE_K_UPDATE);
-  k_update<<<(warps + 7) / 8, 256, 0, h->stream>>>(ua);
+  if (w4 <= 32)
+    k_update<1><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+  else if (w4 <= 64)
+    k_update<2><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+  else if (w4 <= 128)
+    k_update<4><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+  else
+    k_update<8><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
   launch_end(h, KGE_K_UPDATE);
   return cudaGetLastError();
 }
@@ -786,9 +881,9 @@ __global__ void __launch_bounds__(256) k_score(ScoreArgs a) {
   const float* t = a.ent + (int64_t)a.ts[i] * dm.d;
   const float* r = a.rel + (int64_t)a.rs[i] * dm.drel;
   float* o = a.o_scratch + i * dm.dp;
-  combine_row(dm.model, 0, h, r, t, o, dm.d, lane);
-  __syncwarp();
-  const float st = warp_sum(pair_partial(dm.family, o, t, dm.d, lane));
+  float st, on;
+  combine_row(dm.model, 0, h, r, t, o, dm.d, lane, t, dm.family, st, on);
+  st = warp_sum(st);
   if (lane == 0) a.out[i] = pair_score_from(dm.family, st, dm.gamma);
 }
 

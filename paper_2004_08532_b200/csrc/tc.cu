@@ -35,7 +35,8 @@ struct TcState {
 constexpr int kNT = 64;         // negatives per forward CTA
 constexpr int kFwdStages = 4;
 constexpr int kBwdStages = 3;
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;  // 8 warps: warp 0 lane 0 = TMA, warp 1 lane 0 = MMA; all 8 run the epilogue
+// (warps w and w+4 read the same 32 TMEM lanes, different column halves)
 
 struct TcArgs {
   Dims dm;
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t full[kFwdStages], empty[kFwdStages], done;
   __shared__ uint32_t tbase;
   __shared__ float s_xn[kNT];
-  __shared__ float s_red[4];
+  __shared__ float s_red[8];
   const Dims& dm = a.dm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.z, i0 = blockIdx.y * 128, j0 = blockIdx.x * kNT;
@@ -126,34 +127,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   mbar_wait(&done, 0);
   tc_fence_after();
 
-  // epilogue: thread <-> row i (TMEM lane), 32 columns per tcgen05.ld
-  const int i = i0 + warp * 32 + lane;
+  // epilogue: thread <-> row i (TMEM lane 32*(warp%4) + lane); warp/4 selects the column half
+  const int lg = warp & 3, half = warp >> 2;
+  const int i = i0 + lg * 32 + lane;
   const bool iok = i < dm.g;
   const float on = iok && FAM == FAM_L2 ? a.onorm[(int64_t)c * dm.g + i] : 0.f;
   const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
   float lsum = 0.f;
   float* wrow = a.W + ((int64_t)c * dm.g + i) * a.kp;
 #pragma unroll 1
-  for (int q = 0; q < kNT; q += 32) {
+  for (int q = half * (kNT / 2); q < (half + 1) * (kNT / 2); q += 32) {
     float v[32];
-    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + q, v);
+    tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + q, v);
 #pragma unroll
     for (int jj = 0; jj < 32; ++jj) {
       const int j = j0 + q + jj;
       float coef = 0.f;
       if (iok && j < dm.k) {
-        float f, dLdf;
+        float f, D = 1.f;
         if (FAM == FAM_DOT) {
           f = v[jj];
-          dLdf = sigmoid(f) * inv_bk;
-          coef = dLdf;
         } else {  // TransE-L2 by expansion, clamped at 0 before the root (reading c.8)
-          const float D = sqrtf(fmaxf(on - 2.f * v[jj] + s_xn[q + jj], 0.f));
+          D = sqrtf(fmaxf(on - 2.f * v[jj] + s_xn[q + jj], 0.f));
           f = dm.gamma - D;
-          dLdf = sigmoid(f) * inv_bk;
-          coef = -dLdf / fmaxf(D, 1e-12f);
         }
-        lsum += -log_sigmoid(-f);
+        // one exp serves both: e = exp(-|f|); sigma(f) = f>=0 ? 1/(1+e) : e/(1+e); -log sigma(-f) = max(f,0)+log1p(e)
+        const float e = expf(-fabsf(f));
+        const float r1 = 1.f / (1.f + e);
+        const float sig = f >= 0.f ? r1 : e * r1;
+        lsum += fmaxf(f, 0.f) + log1pf(e);
+        const float dLdf = sig * inv_bk;
+        coef = FAM == FAM_DOT ? dLdf : -dLdf / fmaxf(D, 1e-12f);
       }
       v[jj] = coef;
     }
@@ -171,8 +175,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (lane == 0) s_red[warp] = lsum;
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0)
-    a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s_red[0] + s_red[1] + s_red[2] + s_red[3];
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += s_red[w];
+    a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+  }
   if (warp == 0) tmem_dealloc(tmem, kNT);
 }
 
@@ -250,10 +257,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   mbar_wait(&done, 0);
   tc_fence_after();
 
-  // epilogue: thread <-> output row r (TMEM lane)
-  const int r = r0 + warp * 32 + lane;
+  // epilogue: thread <-> output row r (TMEM lane 32*(warp%4) + lane); warp/4 selects half of the column chunks
+  const int lg = warp & 3, half = warp >> 2;
+  const int r = r0 + lg * 32 + lane;
   const bool rok = r < nrows;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16);
   const int d = dm.d;
   float corr = 0.f;  // rowsum(W) (dO) or colsum(W) (dX'), read from the ones column
   if (FAM == FAM_L2) {
@@ -264,16 +272,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   const float* self = pass_x ? a.X + ((int64_t)c * dm.k + r) * a.dp : a.O + ((int64_t)c * dm.g + r) * a.dp;
   float* dst = pass_x ? a.Gocc + ((int64_t)2 * dm.B + (int64_t)c * dm.k + r) * d : a.dO + ((int64_t)c * dm.g + r) * d;
+  const int nch = (d + 31) / 32, ch0 = half ? (nch + 1) / 2 : 0, ch1 = half ? nch : (nch + 1) / 2;
 #pragma unroll 1
-  for (int e0 = 0; e0 < d; e0 += 32) {
+  for (int ch = ch0; ch < ch1; ++ch) {
+    const int e0 = ch * 32;
     float v[32];
     tmem_ld32(trow + e0, v);
     if (!rok) continue;
     const int ne = min(32, d - e0);
-    if (FAM == FAM_L2) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D)
-      for (int u = 0; u < ne; ++u) v[u] = corr * self[e0 + u] - v[u];
-    } else if (pass_x == false) {
-      // DOT: dO = W X'
+    if (FAM == FAM_L2) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D); self pitch dp
+      const float4* s4 = reinterpret_cast<const float4*>(self + e0);
+      float4 sv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sv[u] = s4[u];  // dp >= d + 2 keeps this in bounds
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[4 * u] = corr * sv[u].x - v[4 * u];
+        v[4 * u + 1] = corr * sv[u].y - v[4 * u + 1];
+        v[4 * u + 2] = corr * sv[u].z - v[4 * u + 2];
+        v[4 * u + 3] = corr * sv[u].w - v[4 * u + 3];
+      }
     }
     if (ne == 32) {
       float4* o4 = reinterpret_cast<float4*>(dst + e0);
