@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -35,7 +36,11 @@ void launch_begin(kge_handle* h, int kid) {
 }
 
 void launch_end(kge_handle* h, int kid) {
-  (void)kid;
+  static const bool dbg = getenv("KGE_DEBUG_SYNC") != nullptr;
+  if (dbg) {
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    fprintf(stderr, "[kge] %s -> %s\n", kge_kernel_name(kid), cudaGetErrorString(e));
+  }
   if (!h->prof.on) return;
   cudaEventRecord(h->prof.ev[h->prof.used + 1], h->stream);
   h->prof.used += 2;
@@ -110,7 +115,7 @@ static int validate(const kge_config* c) {
   if (c->lag != 0) { set_error("lag != 0 not implemented in this build"); return KGE_EUNSUPPORTED; }
   if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size) { set_error("bad world_size/rank"); return KGE_EINVAL; }
   if (c->world_size > 1) { set_error("world_size > 1 not implemented in this build"); return KGE_EUNSUPPORTED; }
-  if (c->model == KGE_TRANSR) { set_error("TransR not implemented in this build"); return KGE_EUNSUPPORTED; }
+  if (c->model == KGE_TRANSR && c->dim > 512) { set_error("TransR supports dim <= 512"); return KGE_EINVAL; }
   return KGE_OK;
 }
 
@@ -327,6 +332,33 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (e == cudaSuccess) e = cudaMemsetAsync(h->ent_st, 0, (size_t)Ne * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->rel_st, 0, (size_t)Nr * 4, h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "table init"));
+  if (cfg->model == KGE_TRANSR) {  // M_r, d x d row-major, same uniform law (reading c.6 / Q12)
+    h->proj = (float*)dalloc(h, (size_t)Nr * dm.d * dm.d * 4);
+    h->proj_st = (float*)dalloc(h, (size_t)Nr * 4);
+    if (!h->proj || !h->proj_st) { set_error("out of device memory (TransR projections)"); return fail(KGE_ENOMEM); }
+    e = launch_init_table(h, h->proj, Nr, dm.d * dm.d, 2, bound);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->proj_st, 0, (size_t)Nr * 4, h->stream);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "projection init"));
+    TrBuffers& T = h->tr_buf;
+    const size_t B = dm.B;
+    int32_t* ib = (int32_t*)dalloc(h, (1 + 4 * B + (B + 1) + (dm.C + 1) + B) * 4);
+    T.QX = (float*)dalloc(h, B * dm.k * dm.d * 4);
+    T.dQ = (float*)dalloc(h, B * dm.k * dm.d * 4);
+    T.dM = (float*)dalloc(h, B * dm.d * dm.d * 4);
+    T.Pv = (float*)dalloc(h, B * dm.d * 4);
+    T.U = (float*)dalloc(h, 2 * B * dm.d * 4);
+    T.H = (float*)dalloc(h, 2 * B * dm.d * 4);
+    if (!ib || !T.QX || !T.dQ || !T.dM || !T.Pv || !T.U || !T.H) { set_error("out of device memory (TransR)"); return fail(KGE_ENOMEM); }
+    T.n_groups = ib; ib += 1;
+    T.grp_u = ib; ib += B;
+    T.grp_c = ib; ib += B;
+    T.grp_p0 = ib; ib += B;
+    T.grp_p1 = ib; ib += B;
+    T.rg_off = ib; ib += B + 1;
+    T.cg_off = ib; ib += dm.C + 1;
+    T.cg_list = ib; ib += B;
+    if (!transr_init(h)) { set_error("TransR kernel setup failed"); return fail(KGE_ECUDA); }
+  }
 
   // ---- sample ring + debug slot ----
   h->slots.resize(h->ring);
@@ -353,7 +385,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.wpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
-  b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(h->n_neg_parts, tc_parts) * 4);
+  b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(std::max<int64_t>(h->n_neg_parts, tc_parts), dm.B) * 4);
   b.rowsumW = (float*)dalloc(h, (size_t)dm.B * 4);
   b.colsumW = (float*)dalloc(h, (size_t)nneg * 4);
   b.dO = (float*)dalloc(h, (size_t)dm.B * dm.d * 4);
@@ -383,7 +415,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h) + h->ring, &h->debug_slot, sizeof(Slot), cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "workspace init"));
-  if (cfg->neg_precision == KGE_PREC_TF32) tc_init(h);  // DistMult / ComplEx / TransE-L2 on tcgen05
+  if (cfg->model == KGE_TRANSR) h->n_neg_parts = dm.B;  // one loss partial per (relation, chunk) group
+  if (cfg->neg_precision == KGE_PREC_TF32 && cfg->model != KGE_TRANSR) tc_init(h);  // DistMult / ComplEx / TransE-L2 on tcgen05
   if (tc_supported(h)) h->n_neg_parts = tc_neg_parts(h);
   *out = h;
   return KGE_OK;

@@ -85,6 +85,24 @@ struct StepBuffers {
   int32_t* flags;  // [4]: [0] non-finite seen
 };
 
+// TransR scratch (transr.cu)
+struct TrBuffers {
+  int32_t* n_groups;  // [1]
+  int32_t* grp_u;     // [B] unique-relation index of group
+  int32_t* grp_c;     // [B] chunk of group
+  int32_t* grp_p0;    // [B] first position in rel_occ
+  int32_t* grp_p1;    // [B]
+  int32_t* rg_off;    // [B + 1] groups of unique relation u: [rg_off[u], rg_off[u+1])
+  int32_t* cg_off;    // [C + 1]
+  int32_t* cg_list;   // [B] groups of each chunk, ascending id
+  float* QX;          // [B x k x d] projected negatives per group (then P_g)
+  float* dQ;          // [B x k x d]
+  float* dM;          // [B x d x d] per unique relation
+  float* Pv;          // [B x d]  p = Mh + r - Mt
+  float* U;           // [2B x d] gMh, gMt rows (relation-sorted)
+  float* H;           // [2B x d] h, t rows (relation-sorted)
+};
+
 struct Dims {
   int32_t model, family, variant;
   int32_t d, drel, B, g, C, k, n_occ;
@@ -141,6 +159,7 @@ struct kge_handle {
   int32_t n_pad = 0;
   int32_t dp = 0, kp = 0;
   void* tc = nullptr;  // TcState (tc.cu)
+  kge::TrBuffers tr_buf{};
 };
 
 namespace kge {
@@ -162,6 +181,13 @@ cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, 
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step);
 cudaError_t launch_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, float* out);
 cudaError_t launch_rows(kge_handle* h, float* tab, int32_t w, const int32_t* ids, int64_t n, float* buf, bool write);
+
+cudaError_t launch_gather_neg(kge_handle* h, const Slot& s);
+cudaError_t launch_update(kge_handle* h, const Slot& s);
+
+// transr.cu
+cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step);
+bool transr_init(kge_handle* h);
 
 // tc.cu
 bool tc_init(kge_handle* h);

@@ -184,12 +184,13 @@ struct GatherArgs {
   const float* ent;
   const float* rel;
   StepBuffers b;
+  int32_t first_row;  // B: negatives only (TransR handles its positives in transr.cu)
 };
 
 __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
   const Dims& dm = a.dm;
   const int lane = threadIdx.x & 31;
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int row = a.first_row + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int n_neg = dm.C * dm.k;
   if (row < dm.B) {
     const int i = row, mode = a.s.mode[i / dm.g];
@@ -816,9 +817,37 @@ static void launch_neg(kge_handle* h, const NegArgs& na) {
 }
 
 
+cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
+  const Dims& dm = h->dims;
+  GatherArgs ga{dm, s, h->ent, h->rel, h->buf, dm.B};
+  const int rows = dm.C * dm.k;
+  k_gather<<<(rows + 7) / 8, 256, 0, h->stream>>>(ga);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(kge_handle* h, const Slot& s) {
+  const Dims& dm = h->dims;
+  UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, h->buf};
+  const int n_ent_blocks = (dm.n_occ + 7) / 8;
+  const int grid = n_ent_blocks + dm.B;
+  const int w4 = dm.d / 4;
+  launch_begin(h, KGE_K_UPDATE);
+  if (w4 <= 32)
+    k_update<1><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+  else if (w4 <= 64)
+    k_update<2><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+  else if (w4 <= 128)
+    k_update<4><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+  else
+    k_update<8><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+  launch_end(h, KGE_K_UPDATE);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
-  GatherArgs ga{dm, s, h->ent, h->rel, h->buf};
+  if (dm.model == KGE_TRANSR) return launch_transr_step(h, s, step);
+  GatherArgs ga{dm, s, h->ent, h->rel, h->buf, 0};
   const int rows = dm.B + dm.C * dm.k;
   launch_begin(h, KGE_K_GATHER);
   k_gather<<<(rows + 7) / 8, 256, 0, h->stream>>>(ga);
@@ -842,21 +871,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   k_chain<<<(dm.B + 7) / 8 + 1, 256, 0, h->stream>>>(ca);
   launch_end(h, KGE_K_CHAIN);
 
-  UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, h->buf};
-  const int n_ent_blocks = (dm.n_occ + 7) / 8;
-  const int grid = n_ent_blocks + dm.B;
-  const int w4 = dm.d / 4;
-  launch_begin(h, KGE_K_UPDATE);
-  if (w4 <= 32)
-    k_update<1><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
-  else if (w4 <= 64)
-    k_update<2><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
-  else if (w4 <= 128)
-    k_update<4><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
-  else
-    k_update<8><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
-  launch_end(h, KGE_K_UPDATE);
-  return cudaGetLastError();
+  return launch_update(h, s);
 }
 
 // ---- kge_score: f(h, r, t) per triple (tail-mode decomposition: f = pair(combine(h, r), t)) ----
@@ -887,7 +902,11 @@ __global__ void __launch_bounds__(256) k_score(ScoreArgs a) {
   if (lane == 0) a.out[i] = pair_score_from(dm.family, st, dm.gamma);
 }
 
+cudaError_t launch_transr_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n,
+                                float* out);  // transr.cu
+
 cudaError_t launch_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, float* out) {
+  if (h->dims.model == KGE_TRANSR) return launch_transr_score(h, hs, rs, ts, n, out);
   // scratch: reuse the X buffer in chunks of its capacity
   const int64_t cap = (int64_t)h->dims.C * h->dims.k;
   for (int64_t b = 0; b < n; b += cap) {

@@ -1,0 +1,578 @@
+// transr.cu -- the TransR step (Table 1: f = gamma - ||M_r h + r - M_r t||_2^2; M_r is d x d).
+//
+// TransR is "d times more computationally expensive than TransE" because every negative must be
+// projected by the relation of each positive it is scored against. With joint negatives the
+// projections are shared by all positives of a chunk that carry the same relation, so the step is organised around
+// groups (relation u, chunk c) = the runs of the relation-sorted occurrence list (reading c.5) that fall in one chunk:
+//
+//   k_tr_groups : (1 CTA) group table from the relation dedup segments: per group (u, c, positions); per chunk the
+//                 ordered list of its groups; per unique relation the range of its groups.
+//   k_tr_pos    : per positive (relation-sorted order): Mh, Mt, p = Mh + r - Mt, f+ = gamma - ||p||^2, o = Mh + r (tail)
+//                 or Mt - r (head)  [the decomposition of PAPER.md:429-435 with q_j = M x'_j]
+//   k_tr_gemm<0>: QX_g = X'_c M_u^T                                     (per group, k x d x d)
+//   k_tr_score  : per group: f_ij = gamma - ||o_i - QX_g[j]||^2, loss partial, dO_i, dQ_g (sums in fixed order)
+//   k_tr_gemm<1>: P_g = dQ_g M_u  (dL/dx'_j = M_u^T dq_j)              (per group)
+//   k_tr_reduce : dX'_c = sum over the chunk's groups, in group order, of P_g -> per-occurrence rows (no atomics)
+//   k_tr_chain  : per positive: gMh, gMt, dr; dh = M^T gMh, dt = M^T gMt; rows for the dM outer products; loss CTA
+//   k_tr_gemm<2>: dM_u = sum_g dQ_g^T X'_c + sum_{i in u} (gMh_i h_i^T + gMt_i t_i^T)   (per unique relation)
+//   k_tr_proj   : Adagrad on M_u with one state per matrix (reading c.11, w = d*d)
+// FP32 FFMA throughout (64x64 tiles, 4x4 micro-tiles). The grouped GEMMs are the natural next tcgen05 target.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "device_common.cuh"
+#include "kge_internal.h"
+
+namespace kge {
+
+struct TrArgs {
+  Dims dm;
+  Slot s;
+  const float* ent;
+  const float* rel;
+  float* proj;
+  float* proj_st;
+  StepBuffers b;
+  TrBuffers t;
+  int32_t loss_slot;
+  int32_t n_neg_parts;
+};
+
+// ------------------------------------------------------------------------------------------------
+// group table
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
+  const Dims& dm = a.dm;
+  const TrBuffers& T = a.t;
+  __shared__ int warp_tot[32];
+  __shared__ int s_total;
+  const int B = dm.B, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int per = (B + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(B, tid * per), b1 = min(B, b0 + per);
+  auto key_u = [&](int p) { return a.s.rel_inv[a.s.rel_occ[p]]; };
+  auto key_c = [&](int p) { return a.s.rel_occ[p] / dm.g; };
+  auto is_new = [&](int p) { return p == 0 || key_u(p) != key_u(p - 1) || key_c(p) != key_c(p - 1); };
+  auto scan = [&](int v) {  // block exclusive scan, total in s_total
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;
+      if (lane == 31) s_total = t;
+    }
+    __syncthreads();
+    const int r = (wid ? warp_tot[wid - 1] : 0) + x - v;
+    __syncthreads();
+    return r;
+  };
+  int cnt = 0;
+  for (int p = b0; p < b1; ++p) cnt += is_new(p);
+  int gid = scan(cnt) - 1;
+  const int n_groups = s_total;
+  for (int p = b0; p < b1; ++p) {
+    if (is_new(p)) {
+      ++gid;
+      T.grp_u[gid] = key_u(p);
+      T.grp_c[gid] = key_c(p);
+      T.grp_p0[gid] = p;
+    }
+  }
+  __syncthreads();
+  for (int q = tid; q < n_groups; q += blockDim.x) T.grp_p1[q] = q + 1 < n_groups ? T.grp_p0[q + 1] : B;
+  // per unique relation: first group (groups are sorted by (u, c))
+  const int n_rel = *a.s.rel_n;
+  for (int q = tid; q < n_groups; q += blockDim.x)
+    if (q == 0 || T.grp_u[q] != T.grp_u[q - 1]) T.rg_off[T.grp_u[q]] = q;
+  if (tid == 0) {
+    T.rg_off[n_rel] = n_groups;
+    *T.n_groups = n_groups;
+  }
+  // per chunk: its groups in increasing group id (stable), via one scan per chunk
+  __syncthreads();
+  const int per_g = (n_groups + blockDim.x - 1) / blockDim.x;
+  const int g0 = min(n_groups, tid * per_g), g1 = min(n_groups, g0 + per_g);
+  int base = 0;
+  for (int c = 0; c < dm.C; ++c) {
+    int cc = 0;
+    for (int q = g0; q < g1; ++q) cc += T.grp_c[q] == c;
+    int pos = scan(cc);
+    const int tot = s_total;
+    for (int q = g0; q < g1; ++q)
+      if (T.grp_c[q] == c) T.cg_list[base + pos++] = q;
+    if (tid == 0) T.cg_off[c] = base;
+    base += tot;
+  }
+  if (tid == 0) T.cg_off[dm.C] = base;
+}
+
+// ------------------------------------------------------------------------------------------------
+// positives: one CTA per relation-sorted position p
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_tr_pos(TrArgs a) {
+  const Dims& dm = a.dm;
+  extern __shared__ float sm[];
+  float* sh = sm;             // h [d]
+  float* st = sm + dm.d;      // t [d]
+  float* smh = st + dm.d;     // Mh [d]
+  float* smt = smh + dm.d;    // Mt [d]
+  __shared__ float red[8];
+  const int p = blockIdx.x, i = a.s.rel_occ[p];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, d = dm.d;
+  const int r = a.s.pr[i], mode = a.s.mode[i / dm.g];
+  const float* M = a.proj + (int64_t)r * d * d;
+  const float* hrow = a.ent + (int64_t)a.s.ph[i] * d;
+  const float* trow = a.ent + (int64_t)a.s.pt[i] * d;
+  const float* rv = a.rel + (int64_t)r * d;
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    sh[e] = hrow[e];
+    st[e] = trow[e];
+  }
+  __syncthreads();
+  for (int row = warp; row < d; row += 8) {
+    const float* mr = M + (int64_t)row * d;
+    float ah = 0.f, at = 0.f;
+    for (int b = lane; b < d; b += 32) {
+      const float m = mr[b];
+      ah = fmaf(m, sh[b], ah);
+      at = fmaf(m, st[b], at);
+    }
+    ah = warp_sum(ah);
+    at = warp_sum(at);
+    if (lane == 0) {
+      smh[row] = ah;
+      smt[row] = at;
+    }
+  }
+  __syncthreads();
+  float sq = 0.f;
+  float* o = a.b.O + (int64_t)i * dm.dp;
+  float* pv = a.t.Pv + (int64_t)i * d;
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    const float pe = smh[e] + rv[e] - smt[e];
+    pv[e] = pe;
+    sq += pe * pe;
+    o[e] = mode == 0 ? smh[e] + rv[e] : smt[e] - rv[e];
+  }
+  sq = warp_sum(sq);
+  if (lane == 0) red[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    const float f = dm.gamma - s;
+    a.b.wpos[i] = -sigmoid(-f) / (float)dm.B;
+    a.b.lpos[i] = -log_sigmoid(f);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// grouped GEMMs (FFMA, 64x64 tiles, K-chunks of 16, 4x4 micro-tiles)
+//   MODE 0: C[k x d]  = X'_c[k x d] * M_u^T                 group = pair group g       -> QX_g
+//   MODE 1: C[k x d]  = dQ_g[k x d] * M_u                    group = pair group g       -> P_g (stored in QX_g)
+//   MODE 2: C[d x d]  = sum_g dQ_g^T X'_c + U^T H            group = unique relation u  -> dM_u
+// ------------------------------------------------------------------------------------------------
+constexpr int GT = 64, GK = 16;
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_tr_gemm(TrArgs a) {
+  const Dims& dm = a.dm;
+  const TrBuffers& T = a.t;
+  const int grp = blockIdx.z;
+  const int d = dm.d, k = dm.k;
+  if (MODE < 2) {
+    if (grp >= *T.n_groups) return;
+  } else {
+    if (grp >= *a.s.rel_n) return;
+  }
+  const int Mrows = MODE == 2 ? d : k, Ncols = d;
+  const int m0 = blockIdx.y * GT, n0 = blockIdx.x * GT;
+  if (m0 >= Mrows || n0 >= Ncols) return;
+  __shared__ __align__(16) float As[GK][GT + 4];
+  __shared__ __align__(16) float Bs[GK][GT + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+
+  // A(m, kk) and B(kk, n) accessors for one term; a term is (A base, A pitch, A transposed?, B base, B pitch, B
+  // transposed?, K)
+  auto run_term = [&](const float* Ab, int lda, bool At, const float* Bb, int ldb, bool Bt, int K) {
+    for (int k0 = 0; k0 < K; k0 += GK) {
+      for (int idx = threadIdx.x; idx < GK * GT; idx += blockDim.x) {
+        const int kk = idx / GT, mm = idx % GT;
+        const int gk = k0 + kk;
+        float va = 0.f, vb = 0.f;
+        if (gk < K) {
+          const int gm = m0 + mm, gn = n0 + mm;
+          if (gm < Mrows) va = At ? Ab[(int64_t)gk * lda + gm] : Ab[(int64_t)gm * lda + gk];
+          if (gn < Ncols) vb = Bt ? Bb[(int64_t)gn * ldb + gk] : Bb[(int64_t)gk * ldb + gn];
+        }
+        As[kk][mm] = va;
+        Bs[kk][mm] = vb;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < GK; ++kk) {
+        const float4 av = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+        const float4 bv = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+        const float ar[4] = {av.x, av.y, av.z, av.w}, br[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fmaf(ar[ii], br[jj], acc[ii][jj]);
+      }
+      __syncthreads();
+    }
+  };
+
+  float* out;
+  if (MODE == 0) {
+    const int u = T.grp_u[grp], c = T.grp_c[grp];
+    const int r = a.s.rel_uniq[u];
+    run_term(a.b.X + (int64_t)c * k * dm.dp, dm.dp, false, a.proj + (int64_t)r * d * d, d, true, d);
+    out = T.QX + (int64_t)grp * k * d;
+  } else if (MODE == 1) {
+    const int u = T.grp_u[grp];
+    const int r = a.s.rel_uniq[u];
+    run_term(T.dQ + (int64_t)grp * k * d, d, false, a.proj + (int64_t)r * d * d, d, false, d);
+    out = T.QX + (int64_t)grp * k * d;  // QX_g is dead after k_tr_score
+  } else {
+    const int u = grp;
+    for (int g = T.rg_off[u]; g < T.rg_off[u + 1]; ++g) {
+      const int c = T.grp_c[g];
+      run_term(T.dQ + (int64_t)g * k * d, d, true, a.b.X + (int64_t)c * k * dm.dp, dm.dp, false, k);
+    }
+    const int q0 = 2 * a.s.rel_off[u], q1 = 2 * a.s.rel_off[u + 1];
+    run_term(T.U + (int64_t)q0 * d, d, true, T.H + (int64_t)q0 * d, d, false, q1 - q0);
+    out = T.dM + (int64_t)u * d * d;
+  }
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int m = m0 + ty * 4 + ii;
+    if (m >= Mrows) continue;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int n = n0 + tx * 4 + jj;
+      if (n < Ncols) out[(int64_t)m * Ncols + n] = acc[ii][jj];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// per-group scores: rows of the group in blocks of RB, negatives in tiles of JB
+// ------------------------------------------------------------------------------------------------
+constexpr int RB = 16, JB = 32;
+
+__global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
+  const Dims& dm = a.dm;
+  const TrBuffers& T = a.t;
+  const int grp = blockIdx.x;
+  __shared__ float red[8];
+  if (grp >= *T.n_groups) {
+    if (threadIdx.x == 0) a.b.lneg[grp] = 0.f;
+    return;
+  }
+  extern __shared__ float sm[];
+  const int d = dm.d, k = dm.k;
+  float* so = sm;                 // [RB][d]
+  float* sq = so + RB * d;        // [JB][d]
+  float* sdo = sq + JB * d;       // [RB][d]
+  float* scf = sdo + RB * d;      // [RB][JB]
+  const int p0 = T.grp_p0[grp], p1 = T.grp_p1[grp];
+  const float* QX = T.QX + (int64_t)grp * k * d;
+  float* dQ = T.dQ + (int64_t)grp * k * d;
+  const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
+  float lsum = 0.f;
+  for (int rb = p0; rb < p1; rb += RB) {
+    const int nr = min(RB, p1 - rb);
+    for (int idx = threadIdx.x; idx < RB * d; idx += blockDim.x) {
+      const int rr = idx / d, e = idx % d;
+      so[idx] = rr < nr ? a.b.O[(int64_t)a.s.rel_occ[rb + rr] * dm.dp + e] : 0.f;
+      sdo[idx] = 0.f;
+    }
+    for (int j0 = 0; j0 < k; j0 += JB) {
+      const int nj = min(JB, k - j0);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < JB * d; idx += blockDim.x) {
+        const int jj = idx / d;
+        sq[idx] = jj < nj ? QX[(int64_t)(j0 + jj) * d + idx % d] : 0.f;
+      }
+      __syncthreads();
+      // pair statistics: RB x JB pairs, 2 per thread
+      for (int pr = threadIdx.x; pr < RB * JB; pr += blockDim.x) {
+        const int rr = pr / JB, jj = pr % JB;
+        float coef = 0.f;
+        if (rr < nr && jj < nj) {
+          float s2 = 0.f;
+          const float* ov = so + rr * d;
+          const float* qv = sq + jj * d;
+          for (int e = 0; e < d; ++e) {
+            const float u = ov[e] - qv[e];
+            s2 = fmaf(u, u, s2);
+          }
+          const float f = dm.gamma - s2;
+          coef = -2.f * sigmoid(f) * inv_bk;  // dL/df * df/d(s2)
+          lsum += -log_sigmoid(-f);
+        }
+        scf[rr * JB + jj] = coef;
+      }
+      __syncthreads();
+      // dO rows: sum_j coef (o - q);   dQ rows: sum_i coef (q - o)  (fixed summation order)
+      for (int idx = threadIdx.x; idx < RB * d; idx += blockDim.x) {
+        const int rr = idx / d, e = idx % d;
+        if (rr >= nr) continue;
+        float acc = sdo[idx];
+        const float ov = so[idx];
+        for (int jj = 0; jj < nj; ++jj) acc = fmaf(scf[rr * JB + jj], ov - sq[jj * d + e], acc);
+        sdo[idx] = acc;
+      }
+      for (int idx = threadIdx.x; idx < JB * d; idx += blockDim.x) {
+        const int jj = idx / d, e = idx % d;
+        if (jj >= nj) continue;
+        float acc = rb == p0 ? 0.f : dQ[(int64_t)(j0 + jj) * d + e];
+        const float qv = sq[idx];
+        for (int rr = 0; rr < nr; ++rr) acc = fmaf(scf[rr * JB + jj], qv - so[rr * d + e], acc);
+        dQ[(int64_t)(j0 + jj) * d + e] = acc;
+      }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < RB * d; idx += blockDim.x) {
+      const int rr = idx / d, e = idx % d;
+      if (rr < nr) a.b.dO[(int64_t)a.s.rel_occ[rb + rr] * d + e] = sdo[idx];
+    }
+    __syncthreads();
+  }
+  lsum = warp_sum(lsum);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    a.b.lneg[grp] = t;
+  }
+}
+
+// dX'_c[j][e] = sum over the chunk's groups (ascending group id) of P_g[j][e]  -> occurrence rows 2B + c*k + j
+__global__ void k_tr_reduce(TrArgs a) {
+  const Dims& dm = a.dm;
+  const TrBuffers& T = a.t;
+  const int64_t total = (int64_t)dm.C * dm.k * dm.d;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(q / ((int64_t)dm.k * dm.d));
+    const int64_t je = q - (int64_t)c * dm.k * dm.d;
+    float acc = 0.f;
+    for (int l = T.cg_off[c]; l < T.cg_off[c + 1]; ++l) acc += T.QX[(int64_t)T.cg_list[l] * dm.k * dm.d + je];
+    a.b.Gocc[((int64_t)2 * dm.B + (int64_t)c * dm.k) * dm.d + je] = acc;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// chain: one CTA per relation-sorted position p (+ one CTA for the loss)
+//   tail: o = Mh + r : gMh = dO - 2w p, gMt = 2w p, dr = gMh
+//   head: o = Mt - r : gMh = -2w p,     gMt = dO + 2w p, dr = -gMt
+//   dh = M^T gMh, dt = M^T gMt ; dM_u += gMh h^T + gMt t^T (rows U/H at 2p, 2p+1)
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
+  const Dims& dm = a.dm;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == gridDim.x - 1) {
+    if (threadIdx.x < 32) {
+      float sp = 0.f, sn = 0.f;
+      for (int i = lane; i < dm.B; i += 32) sp += a.b.lpos[i];
+      for (int q = lane; q < a.n_neg_parts; q += 32) sn += a.b.lneg[q];
+      sp = warp_sum(sp);
+      sn = warp_sum(sn);
+      if (lane == 0) {
+        const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
+        a.b.loss[a.loss_slot] = L;
+        const bool bad = !isfinite(L);
+        a.b.flags[1] = bad ? 1 : 0;
+        if (bad) a.b.flags[0] = 1;
+      }
+    }
+    return;
+  }
+  extern __shared__ float sm[];
+  const int d = dm.d;
+  float* sgh = sm;
+  float* sgt = sm + d;
+  const int p = blockIdx.x, i = a.s.rel_occ[p];
+  const int r = a.s.pr[i], mode = a.s.mode[i / dm.g];
+  const float w = a.b.wpos[i];
+  const float* pv = a.t.Pv + (int64_t)i * d;
+  const float* dO = a.b.dO + (int64_t)i * d;
+  float* gR = a.b.Grel + (int64_t)i * dm.drel;
+  float* U = a.t.U + (int64_t)2 * p * d;
+  float* H = a.t.H + (int64_t)2 * p * d;
+  const float* hrow = a.ent + (int64_t)a.s.ph[i] * d;
+  const float* trow = a.ent + (int64_t)a.s.pt[i] * d;
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    const float tp = 2.f * w * pv[e];
+    const float gh = mode == 0 ? dO[e] - tp : -tp;
+    const float gt = mode == 0 ? tp : dO[e] + tp;
+    sgh[e] = gh;
+    sgt[e] = gt;
+    gR[e] = mode == 0 ? gh : -gt;
+    U[e] = gh;
+    U[d + e] = gt;
+    H[e] = hrow[e];
+    H[d + e] = trow[e];
+  }
+  __syncthreads();
+  const float* M = a.proj + (int64_t)r * d * d;
+  float* gH = a.b.Gocc + (int64_t)i * d;
+  float* gT = a.b.Gocc + (int64_t)(dm.B + i) * d;
+  for (int b = threadIdx.x; b < d; b += blockDim.x) {
+    float ah = 0.f, at = 0.f;
+    for (int row = 0; row < d; ++row) {
+      const float m = M[(int64_t)row * d + b];
+      ah = fmaf(m, sgh[row], ah);
+      at = fmaf(m, sgt[row], at);
+    }
+    gH[b] = ah;
+    gT[b] = at;
+  }
+}
+
+// Adagrad on M_u, one state per matrix (w = d*d)
+__global__ void __launch_bounds__(256) k_tr_proj(TrArgs a) {
+  const Dims& dm = a.dm;
+  if (a.b.flags[1]) return;
+  const int u = blockIdx.x;
+  if (u >= *a.s.rel_n) return;
+  __shared__ float red[8];
+  __shared__ float s_step;
+  const int r = a.s.rel_uniq[u];
+  const int64_t w = (int64_t)dm.d * dm.d;
+  const float* G = a.t.dM + (int64_t)u * w;
+  float sq = 0.f;
+  for (int64_t q = threadIdx.x; q < w; q += blockDim.x) sq = fmaf(G[q], G[q], sq);
+  sq = warp_sum(sq);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int ww = 0; ww < 8; ++ww) s += red[ww];
+    const float st = a.proj_st[r] + s / (float)w;
+    a.proj_st[r] = st;
+    s_step = dm.lr / sqrtf(st + dm.eps);
+  }
+  __syncthreads();
+  float* Mr = a.proj + (int64_t)r * w;
+  for (int64_t q = threadIdx.x; q < w; q += blockDim.x) Mr[q] -= s_step * G[q];
+}
+
+// ------------------------------------------------------------------------------------------------
+cudaError_t launch_gather_neg(kge_handle* h, const Slot& s);                      // step.cu
+cudaError_t launch_update(kge_handle* h, const Slot& s);                          // step.cu
+
+static void dbg(kge_handle* h, const char* what) {
+  static const bool on = getenv("KGE_DEBUG_SYNC") != nullptr;
+  if (!on) return;
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  fprintf(stderr, "[kge] %s -> %s\n", what, cudaGetErrorString(e));
+}
+
+cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
+  const Dims& dm = h->dims;
+  TrArgs a{dm, s, h->ent, h->rel, h->proj, h->proj_st, h->buf, h->tr_buf, (int32_t)(step % h->ring), dm.B};
+  cudaError_t e;
+  launch_begin(h, KGE_K_GATHER);
+  k_tr_groups<<<1, 1024, 0, h->stream>>>(a); dbg(h, "k_tr_groups");
+  e = launch_gather_neg(h, s);
+  dbg(h, "gather_neg");
+  if (e != cudaSuccess) return e;
+  k_tr_pos<<<dm.B, 256, 4 * dm.d * sizeof(float), h->stream>>>(a); dbg(h, "k_tr_pos");
+  launch_end(h, KGE_K_GATHER);
+  const dim3 gk((dm.d + GT - 1) / GT, (dm.k + GT - 1) / GT, dm.B);
+  launch_begin(h, KGE_K_NEG_FWD);
+  k_tr_gemm<0><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<0>");
+  const size_t score_smem = (size_t)(2 * RB * dm.d + JB * dm.d + RB * JB) * sizeof(float);
+  k_tr_score<<<dm.B, 256, score_smem, h->stream>>>(a); dbg(h, "k_tr_score");
+  launch_end(h, KGE_K_NEG_FWD);
+  launch_begin(h, KGE_K_NEG_BWD);
+  k_tr_gemm<1><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<1>");
+  const int64_t tot = (int64_t)dm.C * dm.k * dm.d;
+  k_tr_reduce<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, h->stream>>>(a); dbg(h, "k_tr_reduce");
+  launch_end(h, KGE_K_NEG_BWD);
+  launch_begin(h, KGE_K_CHAIN);
+  k_tr_chain<<<dm.B + 1, 256, 2 * dm.d * sizeof(float), h->stream>>>(a); dbg(h, "k_tr_chain");
+  const dim3 gm((dm.d + GT - 1) / GT, (dm.d + GT - 1) / GT, dm.B);
+  k_tr_gemm<2><<<gm, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<2>");
+  launch_end(h, KGE_K_CHAIN);
+  e = launch_update(h, s);
+  dbg(h, "update");
+  if (e != cudaSuccess) return e;
+  k_tr_proj<<<dm.B, 256, 0, h->stream>>>(a); dbg(h, "k_tr_proj");
+  h->launches += 9;
+  return cudaGetLastError();
+}
+
+// kge_score for TransR: f = gamma - ||M_r h + r - M_r t||^2 per triple (CTA per triple)
+__global__ void __launch_bounds__(256) k_tr_score_triples(Dims dm, const float* ent, const float* rel, const float* proj,
+                                                          const int32_t* hs, const int32_t* rs, const int32_t* ts,
+                                                          float* out) {
+  __shared__ float sh[512], st[512], red[8];
+  const int i = blockIdx.x, d = dm.d, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* M = proj + (int64_t)rs[i] * d * d;
+  const float* rv = rel + (int64_t)rs[i] * d;
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    sh[e] = ent[(int64_t)hs[i] * d + e];
+    st[e] = ent[(int64_t)ts[i] * d + e];
+  }
+  __syncthreads();
+  float sq = 0.f;
+  for (int row = warp; row < d; row += 8) {
+    const float* mr = M + (int64_t)row * d;
+    float ah = 0.f, at = 0.f;
+    for (int b = lane; b < d; b += 32) {
+      ah = fmaf(mr[b], sh[b], ah);
+      at = fmaf(mr[b], st[b], at);
+    }
+    ah = warp_sum(ah);
+    at = warp_sum(at);
+    const float pe = ah + rv[row] - at;
+    sq += lane == 0 ? pe * pe : 0.f;
+  }
+  sq = warp_sum(sq);
+  if (lane == 0) red[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    out[i] = dm.gamma - s;
+  }
+}
+
+cudaError_t launch_transr_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n,
+                                float* out) {
+  for (int64_t b = 0; b < n; b += 65535) {
+    const int64_t m = std::min<int64_t>(65535, n - b);
+    k_tr_score_triples<<<(unsigned)m, 256, 0, h->stream>>>(h->dims, h->ent, h->rel, h->proj, hs + b, rs + b, ts + b,
+                                                           out + b);
+    ++h->launches;
+  }
+  return cudaGetLastError();
+}
+
+size_t transr_score_smem(int d) { return (size_t)(2 * RB * d + JB * d + RB * JB) * sizeof(float); }
+
+bool transr_init(kge_handle* h) {
+  cudaError_t e = cudaFuncSetAttribute(k_tr_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)transr_score_smem(h->dims.d));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
+}  // namespace kge

@@ -261,6 +261,31 @@ def test_tc_teacher_forced_rows(model):
     assert worst_loss <= 2e-3 and worst_row <= 5e-3, (model, worst_loss, worst_row)
 
 
+@pytest.mark.parametrize("graph,shape,steps", [("tiny", (64, 16, 16, 32), 30), ("fb15k", (256, 64, 64, 32), 10),
+                                               ("tiny", (96, 24, 50, 40), 10)])
+def test_transr_parity(graph, shape, steps):
+    # configs[3] TransR: M_r d x d, grouped (relation, chunk) projections; FP32 bars of the north_star
+    B, g, k, d = shape
+    gr = synth.graph(graph)
+    trip = gr.triples()
+    gpu, orc = _pair("transr", gr.n_entities, gr.n_relations, trip, d, B, g, k, lr=0.05)
+    rng = np.random.default_rng(3)
+    hs, rs, ts = rng.integers(0, gr.n_entities, 500), rng.integers(0, gr.n_relations, 500), \
+        rng.integers(0, gr.n_entities, 500)
+    f, ref = gpu.score(hs, rs, ts), orc.score_triples(hs, rs, ts)
+    assert np.max(np.abs(f - ref) / np.maximum(np.abs(ref), 12.0 + np.abs(12.0 - ref))) <= 1e-5
+    lg, lo = gpu.train_step(steps), orc.train(steps)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5, (lg, lo)
+    s = gpu.sample(0)
+    ids = np.unique(np.concatenate([s["uniq_ent"], np.arange(min(gr.n_entities, 2000))]))
+    rids = np.arange(gr.n_relations)
+    assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 1e-4
+    assert np.abs(gpu.get_rows(1, rids) - orc.get_rows(1, rids)).max() <= 1e-4
+    touched = np.unique(s["uniq_rel"])
+    assert np.abs(gpu.get_rows(2, touched) - orc.get_rows(2, touched)).max() <= 1e-4
+    assert np.abs(gpu.get_rows(5, rids) - orc.get_rows(5, rids)).max() <= 1e-6
+
+
 def test_tc_matches_fp32_path_closely():
     # same step on both negative-contraction paths: the TF32 result is within TF32 error of the FFMA result
     a, _, _ = _tiny("distmult", dim=64, precision="tf32")

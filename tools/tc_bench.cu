@@ -97,8 +97,14 @@ int main() {
   cudaMalloc(&X, (size_t)C * k * dp * 4);
   cudaMalloc(&out, 64 * 128 * 4);
   cudaMalloc(&stamps, 64 * 64 * 8);
-  cudaMemset(O, 0, (size_t)C * g * dp * 4);
-  cudaMemset(X, 0, (size_t)C * k * dp * 4);
+  {
+    std::vector<float> hO((size_t)C * g * dp), hX((size_t)C * k * dp);
+    for (auto& x : hO) x = (rand() % 2001 - 1000) / 1000.0f;
+    for (auto& x : hX) x = (rand() % 2001 - 1000) / 1000.0f;
+    if (getenv("ZERO")) { std::fill(hO.begin(), hO.end(), 0.f); std::fill(hX.begin(), hX.end(), 0.f); }
+    cudaMemcpy(O, hO.data(), hO.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(X, hX.data(), hX.size() * 4, cudaMemcpyHostToDevice);
+  }
   CUtensorMap mO, mX;
   auto mk = [&](CUtensorMap* m, float* p, int rows, int box_rows, CUtensorMapL2promotion pr) {
     cuuint64_t dims[3] = {(cuuint64_t)dp, (cuuint64_t)rows, (cuuint64_t)C};
