@@ -143,6 +143,27 @@ int kge_set_step(kge_handle* h, int64_t step);
 /* Wait for all enqueued work; reports KGE_ENONFINITE if any step since the last check had a non-finite loss. */
 int kge_sync(kge_handle* h);
 
+/* Losses of recent steps (the last 64) from the device ring; synchronises. For the single-process multi-rank emulation,
+ * where a per-call loss readback would block the other ranks' progress. */
+int kge_read_losses(kge_handle* h, int64_t first_step, int64_t n, float* out);
+
+/* ---- P > 1 ranks (one process per GPU of one node) ----
+ * Partition (reading c.13; PAPER.md:476-495 [3.4]): relations with count > N_t/P are split and their triples dealt
+ * round-robin; the others go, by frequency, to the lightest rank. Entity rows are sharded owner = e mod P, local row =
+ * e div P. After kge_init, every rank exports the IPC handles of its shard and exchange block
+ * (kge_export), the caller gathers the P blobs (e.g. torch.distributed.all_gather_object) and passes them, in rank
+ * order, to kge_connect. kge_train_step is then collective: gather reads rows from their owners over NVLink, owners pull
+ * the per-rank gradient sums of their rows and apply one Adagrad step per row (the union-batch semantics of c.13).
+ * For table 0 / 3, kge_get_rows / kge_set_rows take global ids owned by this rank. */
+int kge_partition(const int64_t* rels, int64_t n_triples, int64_t n_relations, int32_t world_size, int32_t rank,
+                  int32_t* owner_out /* [n_relations] rank or -1 = split, or NULL */,
+                  int64_t* list_out /* this rank's triple indices (ascending), or NULL */, int64_t* n_list);
+int kge_export(kge_handle* h, void* blob, size_t* blob_bytes); /* blob == NULL: *blob_bytes <- size needed */
+int kge_connect(kge_handle* h, const void* blobs /* world_size blobs, rank order */, int32_t world_size);
+/* Single-process emulation: ranks 0..P-1 as P handles on one device, connected directly (tests / one-GPU parity). */
+int kge_connect_local(kge_handle** hs, int32_t world_size);
+int kge_relation_owner(const kge_handle* h, int64_t relation); /* rank, -1 = split (replicated), -2 = bad id */
+
 /* Diagnostics. Kernel ids for kge_profile_end. Between begin and end every kernel launch of the step is bracketed by
  * CUDA events on the handle's stream; end synchronises and returns the average device duration (ms) and the number
  * of launches per kernel id. kge_launch_count: total kernel launches the handle has issued. */

@@ -114,17 +114,31 @@ static int validate(const kge_config* c) {
   if (c->neg_precision < 0 || c->neg_precision > 1) { set_error("bad neg_precision"); return KGE_EINVAL; }
   if (c->lag != 0) { set_error("lag != 0 not implemented in this build"); return KGE_EUNSUPPORTED; }
   if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size) { set_error("bad world_size/rank"); return KGE_EINVAL; }
-  if (c->world_size > 1) { set_error("world_size > 1 not implemented in this build"); return KGE_EUNSUPPORTED; }
+  if (c->world_size > kMaxRanks) { set_error("world_size > 8 (one node) not supported"); return KGE_EINVAL; }
+  if (c->world_size > 1 && c->model == KGE_TRANSR) { set_error("TransR with world_size > 1 is not built yet"); return KGE_EUNSUPPORTED; }
   if (c->model == KGE_TRANSR && c->dim > 512) { set_error("TransR supports dim <= 512"); return KGE_EINVAL; }
   return KGE_OK;
 }
 
-static int alloc_slot(kge_handle* h, Slot& s) {
+static size_t slot_ints(const Dims& d) {
+  const size_t n_occ = d.n_occ, B = d.B;
+  size_t n = B * 4 + (size_t)d.C * d.k + d.C + 1 + n_occ * 3 + (n_occ + 1) + 1 + B * 3 + (B + 1);
+  return (n + 63) & ~size_t(63);  // 256-byte aligned slots
+}
+
+static void* rawalloc(kge_handle* h, size_t bytes) {  // plain cudaMalloc: IPC-exportable (P > 1)
+  void* p = nullptr;
+  if (cudaMalloc(&p, (bytes + 255) & ~size_t(255)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  h->dist.raw_allocs.push_back(p);
+  return p;
+}
+
+static int carve_slot(kge_handle* h, int32_t* p, Slot& s) {
   const Dims& d = h->dims;
   const int n_occ = d.n_occ, B = d.B;
-  size_t n = (size_t)B * 4 + (size_t)d.C * d.k + d.C + 1 + (size_t)n_occ * 3 + (n_occ + 1) + 1 + (size_t)B * 3 + (B + 1);
-  int32_t* p = (int32_t*)dalloc(h, n * sizeof(int32_t));
-  if (!p) return KGE_ENOMEM;
   s.pos = p; p += B;
   s.ph = p; p += B;
   s.pr = p; p += B;
@@ -315,21 +329,53 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     if (e != cudaSuccess) return fail(cuda_fail(e, "triple upload"));
     if (bad) { set_error("triple id out of range"); return fail(KGE_ERANGE); }
   }
+  h->P = cfg->world_size;
+  h->rank = cfg->rank;
   h->list = nullptr;  // P = 1: identity list
   h->n_list = n_triples;
+  if (h->P > 1) {  // relation partition (reading c.13) -> this rank's triple list
+    std::vector<int32_t> owner, lst;
+    relation_partition(rels, n_triples, cfg->n_relations, h->P, owner);
+    rank_list(rels, n_triples, cfg->n_relations, h->P, h->rank, owner, &lst);
+    if (lst.empty()) { set_error("this rank received no triples"); return fail(KGE_EINVAL); }
+    h->list = (int32_t*)dalloc(h, lst.size() * 4);
+    std::vector<int32_t> split_list, split_index((size_t)cfg->n_relations, -1);
+    for (int64_t r = 0; r < cfg->n_relations; ++r)
+      if (owner[(size_t)r] < 0) {
+        split_index[(size_t)r] = (int32_t)split_list.size();
+        split_list.push_back((int32_t)r);
+      }
+    h->dist.n_split = (int32_t)split_list.size();
+    h->dist.split_list = (int32_t*)dalloc(h, std::max<size_t>(1, split_list.size()) * 4);
+    h->dist.split_index = (int32_t*)dalloc(h, (size_t)cfg->n_relations * 4);
+    if (!h->list || !h->dist.split_list || !h->dist.split_index) return fail(KGE_ENOMEM);
+    e = cudaMemcpy(h->list, lst.data(), lst.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !split_list.empty())
+      e = cudaMemcpy(h->dist.split_list, split_list.data(), split_list.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(h->dist.split_index, split_index.data(), split_index.size() * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "partition upload"));
+    h->n_list = (int64_t)lst.size();
+    h->dist.rel_owner = owner;
+  }
 
   // ---- tables ----
   const int64_t Ne = cfg->n_entities, Nr = cfg->n_relations;
-  h->ent = (float*)dalloc(h, (size_t)Ne * dm.d * 4);
-  h->ent_st = (float*)dalloc(h, (size_t)Ne * 4);
+  h->ent_rows = h->P > 1 ? (Ne - h->rank + h->P - 1) / h->P : Ne;  // shard: owner e mod P, local row e div P
+  h->ent = (float*)(h->P > 1 ? rawalloc(h, (size_t)h->ent_rows * dm.d * 4) : dalloc(h, (size_t)Ne * dm.d * 4));
+  h->ent_st = (float*)dalloc(h, (size_t)h->ent_rows * 4);
   h->rel = (float*)dalloc(h, (size_t)Nr * dm.drel * 4);
   h->rel_st = (float*)dalloc(h, (size_t)Nr * 4);
   if (!h->ent || !h->ent_st || !h->rel || !h->rel_st) { set_error("out of device memory (tables)"); return fail(KGE_ENOMEM); }
   const float bound = cfg->init_bound > 0.f ? cfg->init_bound : default_bound(cfg->gamma, cfg->dim);
   const float rbound = cfg->model == KGE_ROTATE ? (float)M_PI : bound;
-  e = launch_init_table(h, h->ent, Ne, dm.d, 0, bound);
+  e = launch_init_table(h, h->ent, h->ent_rows, dm.d, 0, bound, h->P, h->rank);
   if (e == cudaSuccess) e = launch_init_table(h, h->rel, Nr, dm.drel, 1, rbound);
-  if (e == cudaSuccess) e = cudaMemsetAsync(h->ent_st, 0, (size_t)Ne * 4, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->ent_st, 0, (size_t)h->ent_rows * 4, h->stream);
+  h->rows = EntRows{};
+  h->rows.base[0] = h->ent;
+  h->rows.P = 1;
+  h->rows.d = dm.d;
   if (e == cudaSuccess) e = cudaMemsetAsync(h->rel_st, 0, (size_t)Nr * 4, h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "table init"));
   if (cfg->model == KGE_TRANSR) {  // M_r, d x d row-major, same uniform law (reading c.6 / Q12)
@@ -361,10 +407,43 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   }
 
   // ---- sample ring + debug slot ----
+  // sample ring (+ the debug slot) and the flags/slot-table block; for P > 1 they live in the exported shared block
+  // together with the barrier flags and the per-unique gradient sums that peers read
+  const size_t sl = slot_ints(dm);
+  const size_t flags_bytes = ((16 + sizeof(Slot) * (h->ring + 1)) + 255) & ~size_t(255);
+  const size_t ring_bytes = sl * 4 * (h->ring + 1);
+  int32_t* ring_base = nullptr;
+  if (h->P > 1) {
+    Dist& D = h->dist;
+    const size_t gu_bytes = ((size_t)dm.n_occ * dm.d * 4 + 255) & ~size_t(255);
+    const size_t gs_bytes = ((size_t)std::max(1, D.n_split) * dm.drel * 4 + 255) & ~size_t(255);
+    D.shared_bytes = 256 + flags_bytes + ring_bytes + gu_bytes + gs_bytes;
+    char* sb = (char*)rawalloc(h, D.shared_bytes);
+    if (!sb) { set_error("out of device memory (shared block)"); return fail(KGE_ENOMEM); }
+    D.shared = sb;
+    D.flags = (uint64_t*)sb;
+    h->buf.flags = (int32_t*)(sb + 256);
+    ring_base = (int32_t*)(sb + 256 + flags_bytes);
+    D.gu = (float*)(sb + 256 + flags_bytes + ring_bytes);
+    D.grel_split = (float*)(sb + 256 + flags_bytes + ring_bytes + gu_bytes);
+    e = cudaMemset(sb, 0, D.shared_bytes);
+    const size_t max_slots = (size_t)h->P * dm.n_occ;
+    D.mark = (int32_t*)dalloc(h, (size_t)h->ent_rows * 4);
+    D.contrib = (int32_t*)dalloc(h, max_slots * h->P * 4);
+    D.slot_row = (int32_t*)dalloc(h, max_slots * 4);
+    D.n_slots = (int32_t*)dalloc(h, 16);
+    if (!D.mark || !D.contrib || !D.slot_row || !D.n_slots) return fail(KGE_ENOMEM);
+    if (e == cudaSuccess) e = cudaMemset(D.mark, 0xFF, (size_t)h->ent_rows * 4);
+    if (e == cudaSuccess) e = cudaMemset(D.contrib, 0xFF, max_slots * h->P * 4);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "shared block init"));
+  } else {
+    ring_base = (int32_t*)dalloc(h, ring_bytes);
+    h->buf.flags = (int32_t*)dalloc(h, flags_bytes);  // flags[4] then the device slot table
+    if (!ring_base || !h->buf.flags) { set_error("out of device memory (ring)"); return fail(KGE_ENOMEM); }
+  }
   h->slots.resize(h->ring);
-  for (int i = 0; i < h->ring; ++i)
-    if (alloc_slot(h, h->slots[i]) != KGE_OK) { set_error("out of device memory (ring)"); return fail(KGE_ENOMEM); }
-  if (alloc_slot(h, h->debug_slot) != KGE_OK) return fail(KGE_ENOMEM);
+  for (int i = 0; i < h->ring; ++i) carve_slot(h, ring_base + sl * i, h->slots[i]);
+  carve_slot(h, ring_base + sl * h->ring, h->debug_slot);
   h->given = (int32_t*)dalloc(h, (size_t)3 * dm.B * 4);
   if (cudaMallocHost(&h->pinned_given, (size_t)3 * dm.B * 8) != cudaSuccess ||
       cudaMallocHost(&h->pinned_loss, (size_t)h->ring * 4) != cudaSuccess) {
@@ -392,7 +471,6 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.Gocc = (float*)dalloc(h, (size_t)dm.n_occ * dm.d * 4);
   b.Grel = (float*)dalloc(h, (size_t)dm.B * dm.drel * 4);
   b.loss = (float*)dalloc(h, (size_t)h->ring * 4);
-  b.flags = (int32_t*)dalloc(h, 16 + sizeof(Slot) * (h->ring + 1));  // flags[4] then the slot table
   if (!b.O || !b.onorm || !b.X || !b.xnorm || !b.W || !b.wpos || !b.lpos || !b.pstat || !b.lneg || !b.rowsumW || !b.colsumW ||
       !b.dO || !b.Gocc || !b.Grel || !b.loss || !b.flags) {
     set_error("out of device memory (workspace)");
@@ -415,6 +493,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h) + h->ring, &h->debug_slot, sizeof(Slot), cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "workspace init"));
+  if (sample_init() != cudaSuccess || step_preload() != cudaSuccess || dist_preload() != cudaSuccess)
+    return fail(cuda_fail(cudaGetLastError(), "kernel preload"));
   if (cfg->model == KGE_TRANSR) h->n_neg_parts = dm.B;  // one loss partial per (relation, chunk) group
   if (cfg->neg_precision == KGE_PREC_TF32 && cfg->model != KGE_TRANSR) tc_init(h);  // DistMult / ComplEx / TransE-L2 on tcgen05
   if (tc_supported(h)) h->n_neg_parts = tc_neg_parts(h);
@@ -447,12 +527,21 @@ static int check_flags(kge_handle* h) {
 int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
   if (!h) { set_error("NULL handle"); return KGE_EINVAL; }
   if (n_steps < 0) { set_error("n_steps < 0"); return KGE_EINVAL; }
+  if (h->P > 1 && !h->dist.connected) { set_error("world_size > 1: call kge_connect first"); return KGE_ESTATE; }
   for (int64_t it = 0; it < n_steps; ++it) {
     const int64_t s = h->step;
     if (s >= (1ll << 32)) { set_error("step index exceeds 2^32 (one Philox counter word)"); return KGE_ERANGE; }
+    if (h->P > 1) {
+      // B1: every owner has applied step s-1 before anyone gathers rows or overwrites a slot peers read
+      cudaError_t e = dist_barrier(h);
+      if (e == cudaSuccess && h->dist.n_split > 0)
+        e = cudaMemsetAsync(h->dist.grel_split, 0, (size_t)h->dist.n_split * h->dims.drel * 4, h->stream);
+      if (e != cudaSuccess) return cuda_fail(e, "barrier");
+    }
     int rc = ensure_sampled(h, s);
     if (rc != KGE_OK) return rc;
     cudaError_t e = launch_step(h, h->slots[s % h->ring], s);
+    if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, h->slots[s % h->ring]);
     if (e != cudaSuccess) return cuda_fail(e, "step");
     if (loss_out) {
       e = cudaMemcpyAsync(h->pinned_loss + (it % h->ring), h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost, h->stream);
@@ -472,6 +561,7 @@ int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
 
 int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails, float* loss_out) {
   if (!h || !heads || !rels || !tails) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (h->P > 1) { set_error("kge_train_batch is single-rank in this build"); return KGE_EUNSUPPORTED; }
   const int B = h->dims.B;
   const int64_t s = h->step;
   // host-side range check + int32 narrowing into pinned staging, then one H2D copy
@@ -571,9 +661,11 @@ static int rows_io(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, 
   if (!tab) { set_error("table not present for this model"); return KGE_EINVAL; }
   if (n == 0) return KGE_OK;
   std::vector<int32_t> ids32(n);
+  const bool sharded = h->P > 1 && (table == 0 || table == 3);
   for (int64_t i = 0; i < n; ++i) {
     if (ids[i] < 0 || ids[i] >= rows) { set_error("row id out of range"); return KGE_ERANGE; }
-    ids32[i] = (int32_t)ids[i];
+    if (sharded && ids[i] % h->P != h->rank) { set_error("entity row not owned by this rank (owner = id mod P)"); return KGE_ERANGE; }
+    ids32[i] = (int32_t)(sharded ? ids[i] / h->P : ids[i]);
   }
   int32_t* d_ids = nullptr;
   float* d_buf = nullptr;
@@ -598,6 +690,7 @@ int kge_set_rows(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, co
 
 int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, float* out) {
   if (!h || (n > 0 && (!hs || !rs || !ts || !out))) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (h->P > 1 && !h->dist.connected) { set_error("world_size > 1: call kge_connect first"); return KGE_ESTATE; }
   if (n == 0) return KGE_OK;
   std::vector<int32_t> ids((size_t)3 * n);
   for (int64_t i = 0; i < n; ++i) {
@@ -624,6 +717,19 @@ int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t
 }
 
 int64_t kge_step(const kge_handle* h) { return h ? h->step : -1; }
+
+int kge_read_losses(kge_handle* h, int64_t first_step, int64_t n, float* out) {
+  if (!h || (n > 0 && !out)) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (first_step < 0 || first_step + n > h->step || first_step < h->step - h->ring) {
+    set_error("losses are kept for the last 64 steps only");
+    return KGE_ERANGE;
+  }
+  std::vector<float> ring(h->ring);
+  CK(cudaMemcpyAsync(ring.data(), h->buf.loss, (size_t)h->ring * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  for (int64_t i = 0; i < n; ++i) out[i] = ring[(first_step + i) % h->ring];
+  return check_flags(h);
+}
 
 int kge_set_step(kge_handle* h, int64_t step) {
   if (!h || step < 0) { set_error("bad argument"); return KGE_EINVAL; }
@@ -667,6 +773,10 @@ int64_t kge_launch_count(const kge_handle* h) { return h ? h->launches : 0; }
 
 void kge_destroy(kge_handle* h) {
   if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->dist.ipc_opened) cudaIpcCloseMemHandle(p);
+  for (void* p : h->dist.raw_allocs) cudaFree(p);
+  h->dist.raw_allocs.clear();
   free_all(h);
   for (cudaEvent_t ev : h->prof.ev)
     if (ev) cudaEventDestroy(ev);

@@ -1,0 +1,422 @@
+// dist.cu -- P > 1 ranks (one process per GPU of one node, or P handles on one device for the single-GPU emulation).
+//
+// Partitioning (PAPER.md:306-313 [3.1], 476-495 [3.4]; reading c.13):
+//   * triples by relation: relations with count > N_t/P are SPLIT and their triples dealt round-robin per relation;
+//     the rest go, by (count desc, id asc), to the currently lightest rank ("we sort the relations based on their
+//     frequency ... greedily assign a relation to the partition with the smallest number of triplets so far").
+//   * entity rows strided over the ranks ("strides them across all KVStore servers"): owner(e) =
+//     e mod P, local row = e div P.
+//   * relation rows replicated; a non-split relation is touched by its owner rank only (its rows "stay local and need
+//     no communication", north_star); split relations are touched by every rank and their gradients summed in rank order.
+// Exchange, fused into the kernels over peer memory (NVLink P2P through CUDA IPC mappings) instead of NCCL all-to-all:
+//   * forward: k_gather / k_chain read an entity row straight from its owner's shard (EntRows accessor);
+//   * gradient return: each rank writes one segment-summed gradient per unique entity it touched (Gu); after a device
+//     barrier the owner pulls the gradients of its rows from every rank (k_owner_collect), sums them in rank order and
+//     applies one Adagrad step per row (k_owner_update) -- the union-batch semantics of reading c.13;
+//   * split relations: per-rank sums in GrelSplit, pulled and summed in rank order by every replica (k_split_rel).
+// Device barriers (k_barrier: release/acquire flags at system scope in every peer) order the phases; a protocol bug
+// traps after ~2 s instead of hanging.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "device_common.cuh"
+#include "kge_internal.h"
+
+namespace kge {
+
+// ------------------------------------------------------------------------------------------------
+// host: relation partition (reading c.13)
+// ------------------------------------------------------------------------------------------------
+int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<int32_t>& owner) {
+  std::vector<int64_t> cnt((size_t)nr, 0);
+  for (int64_t i = 0; i < nt; ++i) cnt[(size_t)rels[i]]++;
+  owner.assign((size_t)nr, 0);
+  std::vector<int64_t> load((size_t)P, 0);
+  std::vector<int64_t> rest;
+  int32_t n_split = 0;
+  for (int64_t r = 0; r < nr; ++r) {
+    if (P > 1 && cnt[(size_t)r] * P > nt) {  // count > N_t / P, exact in integers
+      owner[(size_t)r] = -1;
+      ++n_split;
+      for (int32_t w = 0; w < P; ++w) load[(size_t)w] += cnt[(size_t)r] / P + (w < cnt[(size_t)r] % P ? 1 : 0);
+    } else {
+      rest.push_back(r);
+    }
+  }
+  std::stable_sort(rest.begin(), rest.end(), [&](int64_t a, int64_t b) {
+    return cnt[(size_t)a] != cnt[(size_t)b] ? cnt[(size_t)a] > cnt[(size_t)b] : a < b;
+  });
+  for (int64_t r : rest) {
+    int32_t best = 0;
+    for (int32_t w = 1; w < P; ++w)
+      if (load[(size_t)w] < load[(size_t)best]) best = w;
+    owner[(size_t)r] = best;
+    load[(size_t)best] += cnt[(size_t)r];
+  }
+  return n_split;
+}
+
+int64_t rank_list(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, int32_t rank, const std::vector<int32_t>& owner,
+                  std::vector<int32_t>* out) {
+  std::vector<int64_t> dealt((size_t)nr, 0);
+  int64_t n = 0;
+  for (int64_t i = 0; i < nt; ++i) {
+    const int64_t r = rels[i];
+    int32_t o = owner[(size_t)r];
+    if (o < 0) o = (int32_t)(dealt[(size_t)r]++ % P);
+    if (o == rank) {
+      if (out) out->push_back((int32_t)i);
+      ++n;
+    }
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------------------------------------
+// device: barrier, owner-side gradient collection and update, split relations
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct PeerFlags {
+  uint64_t* f[kMaxRanks];  // rank q's flag array (P entries, one per writer)
+};
+
+__global__ void k_barrier(PeerFlags pf, int P, int rank, uint64_t epoch) {
+  const int q = threadIdx.x;
+  if (q < P) {
+    __threadfence_system();
+    st_release_sys(pf.f[q] + rank, epoch);
+  }
+  __syncthreads();
+  if (q < P) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys(pf.f[rank] + q) < epoch) {
+      if (clock64() - t0 > 4000000000ll) __trap();  // a missing peer is an error, not a hang
+    }
+  }
+  __syncthreads();
+}
+
+struct OwnerArgs {
+  Slot peer[kMaxRanks];         // every rank's sample slot of this step (peer pointers)
+  const float* gu[kMaxRanks];   // every rank's per-unique gradient rows [n_occ x d]
+  const int32_t* lossflag[kMaxRanks];  // every rank's flags array ([1] = this step non-finite)
+  int32_t P, rank, n_occ, d;
+  float lr, eps;
+  int32_t* mark;     // [rows_local] slot of a touched local row, -1 otherwise
+  int32_t* contrib;  // [P*n_occ x P] index of the row in rank w's unique list, -1 if absent
+  int32_t* slot_row; // [P*n_occ] local row of a slot
+  int32_t* n_slots;  // [1]
+  float* ent;        // local shard
+  float* ent_st;
+};
+
+// E1: every (rank w, unique index u) whose entity this rank owns claims a slot for its local row
+__global__ void k_owner_collect(OwnerArgs a) {
+  const int w = blockIdx.y;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= a.n_occ || u >= *a.peer[w].ent_n) return;
+  const int32_t e = a.peer[w].ent_uniq[u];
+  if (e % a.P != a.rank) return;
+  const int32_t l = e / a.P;
+  int32_t s = atomicCAS(a.mark + l, -1, -2);
+  if (s == -1) {  // first claimant allocates the slot and publishes it
+    s = atomicAdd(a.n_slots, 1);
+    a.slot_row[s] = l;
+    __threadfence();
+    atomicExch(a.mark + l, s);
+  } else {
+    const long long t0 = clock64();
+    while ((s = *(volatile int32_t*)(a.mark + l)) == -2) {
+      if (clock64() - t0 > 4000000000ll) __trap();
+    }
+  }
+  a.contrib[(int64_t)s * a.P + w] = u;
+}
+
+// E2: per claimed slot (warp): G = sum over ranks in rank order of their segment sums; one Adagrad step (c.11, c.13)
+__global__ void __launch_bounds__(256) k_owner_update(OwnerArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= *a.n_slots) return;
+  bool skip = false;  // a non-finite loss on any rank skips the step's update everywhere
+  for (int w = 0; w < a.P; ++w) skip |= a.lossflag[w][1] != 0;
+  const int32_t l = a.slot_row[s];
+  const int d = a.d, d4 = d >> 2;
+  float* row = a.ent + (int64_t)l * d;
+  if (!skip) {
+    float4 g[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) g[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int w = 0; w < a.P; ++w) {
+      const int32_t u = a.contrib[(int64_t)s * a.P + w];
+      if (u < 0) continue;
+      const float4* src = reinterpret_cast<const float4*>(a.gu[w] + (int64_t)u * d);
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int v = lane + 32 * m;
+        if (v < d4) {
+          const float4 x = src[v];
+          g[m].x += x.x; g[m].y += x.y; g[m].z += x.z; g[m].w += x.w;
+        }
+      }
+    }
+    float sq = 0.f;
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+      if (lane + 32 * m < d4) sq += g[m].x * g[m].x + g[m].y * g[m].y + g[m].z * g[m].z + g[m].w * g[m].w;
+    sq = warp_sum(sq);
+    const float st = a.ent_st[l] + sq / (float)d;
+    if (lane == 0) a.ent_st[l] = st;
+    const float step = a.lr / sqrtf(st + a.eps);
+    float4* r4 = reinterpret_cast<float4*>(row);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int v = lane + 32 * m;
+      if (v < d4) {
+        float4 x = r4[v];
+        x.x -= step * g[m].x; x.y -= step * g[m].y; x.z -= step * g[m].z; x.w -= step * g[m].w;
+        r4[v] = x;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < a.P) a.contrib[(int64_t)s * a.P + lane] = -1;
+  if (lane == 0) a.mark[l] = -1;
+}
+
+struct SplitArgs {
+  const float* gs[kMaxRanks];          // every rank's GrelSplit [n_split x drel]
+  const int32_t* lossflag[kMaxRanks];
+  const int32_t* split_list;           // [n_split] relation ids
+  int32_t P, n_split, w;
+  float lr, eps;
+  float* rel;
+  float* rel_st;
+};
+
+// split relations: every replica applies the same update from the rank-ordered sum (warp per relation)
+__global__ void __launch_bounds__(256) k_split_rel(SplitArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (s >= a.n_split) return;
+  for (int w = 0; w < a.P; ++w)
+    if (a.lossflag[w][1]) return;
+  const int wd = a.w;
+  float sq = 0.f;
+  float* row = a.rel + (int64_t)a.split_list[s] * wd;
+  // pass 1: squared norm of the summed gradient; pass 2: update (w <= 1024 floats; recompute the sums)
+  for (int e = lane; e < wd; e += 32) {
+    float g = 0.f;
+    for (int q = 0; q < a.P; ++q) g += a.gs[q][(int64_t)s * wd + e];
+    sq += g * g;
+  }
+  sq = warp_sum(sq);
+  if (sq == 0.f) return;  // untouched this step on every rank: no update (exactly as the union step)
+  const float st = a.rel_st[a.split_list[s]] + sq / (float)wd;
+  const float step = a.lr / sqrtf(st + a.eps);
+  for (int e = lane; e < wd; e += 32) {
+    float g = 0.f;
+    for (int q = 0; q < a.P; ++q) g += a.gs[q][(int64_t)s * wd + e];
+    row[e] -= step * g;
+  }
+  if (lane == 0) a.rel_st[a.split_list[s]] = st;
+}
+
+// ------------------------------------------------------------------------------------------------
+// host orchestration
+// ------------------------------------------------------------------------------------------------
+static PeerFlags peer_flags(const kge_handle* h) {
+  PeerFlags pf{};
+  for (int q = 0; q < h->P; ++q) pf.f[q] = h->dist.peer_flags[q];
+  return pf;
+}
+
+cudaError_t dist_preload() {  // see step_preload (lazy loading vs spinning barriers)
+  cudaFuncAttributes at;
+  cudaError_t e = cudaFuncGetAttributes(&at, (const void*)k_barrier);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, (const void*)k_owner_collect);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, (const void*)k_owner_update);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, (const void*)k_split_rel);
+  return e;
+}
+
+cudaError_t dist_barrier(kge_handle* h) {
+  ++h->dist.epoch;
+  k_barrier<<<1, 32, 0, h->stream>>>(peer_flags(h), h->P, h->rank, h->dist.epoch);
+  ++h->launches;
+  return cudaGetLastError();
+}
+
+// Slot with every pointer moved from my shared block to rank q's mapping of the same layout
+static Slot peer_slot(const kge_handle* h, const Slot& mine, int q) {
+  const char* base = (const char*)h->dist.shared;
+  const char* pb = (const char*)h->dist.peer_shared[q];
+  Slot s = mine;
+  int32_t** f = reinterpret_cast<int32_t**>(&s);
+  for (size_t i = 0; i < sizeof(Slot) / sizeof(int32_t*); ++i) f[i] = (int32_t*)(pb + ((const char*)f[i] - base));
+  return s;
+}
+
+cudaError_t dist_exchange_update(kge_handle* h, const Slot& s) {
+  const Dims& dm = h->dims;
+  Dist& D = h->dist;
+  cudaError_t e = dist_barrier(h);  // B2: every rank's Gu / GrelSplit / sample slot is complete
+  if (e != cudaSuccess) return e;
+  OwnerArgs oa{};
+  const char* base = (const char*)D.shared;
+  for (int q = 0; q < h->P; ++q) {
+    oa.peer[q] = peer_slot(h, s, q);
+    oa.gu[q] = (const float*)((const char*)D.peer_shared[q] + ((const char*)D.gu - base));
+    oa.lossflag[q] = (const int32_t*)((const char*)D.peer_shared[q] + ((const char*)h->buf.flags - base));
+  }
+  oa.P = h->P;
+  oa.rank = h->rank;
+  oa.n_occ = dm.n_occ;
+  oa.d = dm.d;
+  oa.lr = dm.lr;
+  oa.eps = dm.eps;
+  oa.mark = D.mark;
+  oa.contrib = D.contrib;
+  oa.slot_row = D.slot_row;
+  oa.n_slots = D.n_slots;
+  oa.ent = h->ent;
+  oa.ent_st = h->ent_st;
+  e = cudaMemsetAsync(D.n_slots, 0, 4, h->stream);
+  if (e != cudaSuccess) return e;
+  launch_begin(h, KGE_K_UPDATE);
+  k_owner_collect<<<dim3((dm.n_occ + 255) / 256, h->P), 256, 0, h->stream>>>(oa);
+  const int max_slots = h->P * dm.n_occ;
+  k_owner_update<<<(max_slots + 7) / 8, 256, 0, h->stream>>>(oa);
+  if (D.n_split > 0) {
+    SplitArgs sa{};
+    for (int q = 0; q < h->P; ++q) {
+      sa.gs[q] = (const float*)((const char*)D.peer_shared[q] + ((const char*)D.grel_split - base));
+      sa.lossflag[q] = oa.lossflag[q];
+    }
+    sa.split_list = D.split_list;
+    sa.P = h->P;
+    sa.n_split = D.n_split;
+    sa.w = dm.drel;
+    sa.lr = dm.lr;
+    sa.eps = dm.eps;
+    sa.rel = h->rel;
+    sa.rel_st = h->rel_st;
+    k_split_rel<<<(D.n_split + 7) / 8, 256, 0, h->stream>>>(sa);
+    ++h->launches;
+  }
+  launch_end(h, KGE_K_UPDATE);
+  h->launches += 2;
+  return cudaGetLastError();
+}
+
+}  // namespace kge
+
+using namespace kge;
+
+extern "C" {
+
+int kge_partition(const int64_t* rels, int64_t n_triples, int64_t n_relations, int32_t world_size, int32_t rank,
+                  int32_t* owner_out, int64_t* list_out, int64_t* n_list) {
+  if (!rels || n_triples <= 0 || n_relations <= 0 || world_size < 1 || rank < 0 || rank >= world_size) {
+    set_error("bad partition arguments");
+    return KGE_EINVAL;
+  }
+  for (int64_t i = 0; i < n_triples; ++i)
+    if (rels[i] < 0 || rels[i] >= n_relations) {
+      set_error("relation id out of range");
+      return KGE_ERANGE;
+    }
+  std::vector<int32_t> owner;
+  relation_partition(rels, n_triples, n_relations, world_size, owner);
+  if (owner_out) std::copy(owner.begin(), owner.end(), owner_out);
+  std::vector<int32_t> lst;
+  const int64_t n = rank_list(rels, n_triples, n_relations, world_size, rank, owner, list_out ? &lst : nullptr);
+  if (list_out) for (int64_t i = 0; i < n; ++i) list_out[i] = lst[(size_t)i];
+  if (n_list) *n_list = n;
+  return KGE_OK;
+}
+
+int kge_export(kge_handle* h, void* blob, size_t* blob_bytes) {
+  if (!h || !blob_bytes) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (h->P < 2) { set_error("kge_export needs world_size > 1"); return KGE_ESTATE; }
+  const size_t need = 2 * sizeof(cudaIpcMemHandle_t);
+  if (!blob) { *blob_bytes = need; return KGE_OK; }
+  if (*blob_bytes < need) { set_error("blob too small"); return KGE_EINVAL; }
+  cudaIpcMemHandle_t hs[2];
+  cudaError_t e = cudaIpcGetMemHandle(&hs[0], h->ent);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hs[1], h->dist.shared);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  std::memcpy(blob, hs, need);
+  *blob_bytes = need;
+  return KGE_OK;
+}
+
+static int finish_connect(kge_handle* h) {
+  Dist& D = h->dist;
+  for (int q = 0; q < h->P; ++q) {
+    h->rows.base[q] = D.peer_ent[q];
+    D.peer_flags[q] = (uint64_t*)D.peer_shared[q];  // flags live at offset 0 of the shared block
+  }
+  h->rows.P = h->P;
+  D.connected = true;
+  return KGE_OK;
+}
+
+int kge_connect(kge_handle* h, const void* blobs, int32_t world_size) {
+  if (!h || !blobs) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (world_size != h->P) { set_error("world_size mismatch"); return KGE_EINVAL; }
+  const cudaIpcMemHandle_t* hs = (const cudaIpcMemHandle_t*)blobs;
+  Dist& D = h->dist;
+  for (int q = 0; q < h->P; ++q) {
+    if (q == h->rank) {
+      D.peer_ent[q] = h->ent;
+      D.peer_shared[q] = D.shared;
+      continue;
+    }
+    void *pe = nullptr, *ps = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&pe, hs[2 * q], cudaIpcMemLazyEnablePeerAccess);
+    if (e == cudaSuccess) e = cudaIpcOpenMemHandle(&ps, hs[2 * q + 1], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    D.peer_ent[q] = (float*)pe;
+    D.peer_shared[q] = ps;
+    D.ipc_opened.push_back(pe);
+    D.ipc_opened.push_back(ps);
+  }
+  return finish_connect(h);
+}
+
+int kge_connect_local(kge_handle** hs, int32_t P) {
+  if (!hs || P < 2 || P > kMaxRanks) { set_error("bad arguments"); return KGE_EINVAL; }
+  for (int w = 0; w < P; ++w) {
+    if (!hs[w] || hs[w]->P != P || hs[w]->rank != w) { set_error("handles must be ranks 0..P-1 of one world"); return KGE_EINVAL; }
+    if (hs[w]->device != hs[0]->device) { set_error("kge_connect_local needs all handles on one device"); return KGE_EINVAL; }
+  }
+  for (int w = 0; w < P; ++w) {
+    for (int q = 0; q < P; ++q) {
+      hs[w]->dist.peer_ent[q] = hs[q]->ent;
+      hs[w]->dist.peer_shared[q] = hs[q]->dist.shared;
+    }
+    finish_connect(hs[w]);
+  }
+  return KGE_OK;
+}
+
+int kge_relation_owner(const kge_handle* h, int64_t relation) {
+  if (!h || relation < 0 || relation >= h->dims.n_relations) return -2;
+  if (h->P == 1) return 0;
+  return h->dist.rel_owner[(size_t)relation];
+}
+
+}  // extern "C"

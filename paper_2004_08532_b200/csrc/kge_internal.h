@@ -29,6 +29,19 @@ inline Family family_of(int model, int rotate_variant) {
   }
 }
 
+constexpr int kMaxRanks = 8;
+
+// Entity-row accessor: P == 1 -> the local table; P > 1 -> owner (e mod P) shard, local row e div P (possibly a peer
+// mapping over NVLink).
+struct EntRows {
+  const float* base[kMaxRanks];
+  int32_t P;
+  int32_t d;
+  __host__ __device__ __forceinline__ const float* row(int64_t e) const {
+    return P == 1 ? base[0] + e * d : base[e % P] + (e / P) * (int64_t)d;
+  }
+};
+
 // Per-step sample slot (device pointers into one ring allocation).
 struct Slot {
   int32_t* pos;      // [B] triple index
@@ -103,6 +116,30 @@ struct TrBuffers {
   float* H;           // [2B x d] h, t rows (relation-sorted)
 };
 
+// multi-rank state (dist.cu)
+struct Dist {
+  void* shared = nullptr;       // cudaMalloc'd block exported to peers: flags | ring | Gu | GrelSplit
+  size_t shared_bytes = 0;
+  uint64_t* flags = nullptr;    // [kMaxRanks] barrier epochs written by each rank
+  float* gu = nullptr;          // [n_occ x d] per-unique entity gradient sums of this step
+  float* grel_split = nullptr;  // [n_split x drel]
+  int32_t n_split = 0;
+  int32_t* split_list = nullptr;   // [n_split] device
+  int32_t* split_index = nullptr;  // [n_relations] device, -1 if not split
+  std::vector<int32_t> rel_owner;  // host copy of the relation partition
+  int32_t* mark = nullptr;      // [rows_local]
+  int32_t* contrib = nullptr;   // [P*n_occ x P]
+  int32_t* slot_row = nullptr;  // [P*n_occ]
+  int32_t* n_slots = nullptr;   // [1]
+  float* peer_ent[kMaxRanks] = {};
+  void* peer_shared[kMaxRanks] = {};
+  uint64_t* peer_flags[kMaxRanks] = {};
+  std::vector<void*> ipc_opened;
+  std::vector<void*> raw_allocs;  // cudaMalloc'd (IPC-exportable) allocations
+  uint64_t epoch = 0;
+  bool connected = false;
+};
+
 struct Dims {
   int32_t model, family, variant;
   int32_t d, drel, B, g, C, k, n_occ;
@@ -160,6 +197,11 @@ struct kge_handle {
   int32_t dp = 0, kp = 0;
   void* tc = nullptr;  // TcState (tc.cu)
   kge::TrBuffers tr_buf{};
+  // ranks
+  int32_t P = 1, rank = 0;
+  int64_t ent_rows = 0;  // rows of the local entity table (shard when P > 1)
+  kge::EntRows rows{};
+  kge::Dist dist;
 };
 
 namespace kge {
@@ -173,8 +215,10 @@ void launch_end(kge_handle* h, int kid);
 
 // sample.cu
 size_t sample_smem_bytes(int n_pad);
+cudaError_t sample_init();
 cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev_array, int ring, int64_t step0, int n_steps);
-cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound);
+cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound,
+                              int64_t row_stride = 1, int64_t row_offset = 0);
 cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, int64_t n, int64_t limit, int32_t* bad);
 
 // step.cu
@@ -188,6 +232,15 @@ cudaError_t launch_update(kge_handle* h, const Slot& s);
 // transr.cu
 cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step);
 bool transr_init(kge_handle* h);
+
+// dist.cu
+int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<int32_t>& owner);
+int64_t rank_list(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, int32_t rank,
+                  const std::vector<int32_t>& owner, std::vector<int32_t>* out);
+cudaError_t dist_barrier(kge_handle* h);
+cudaError_t dist_preload();
+cudaError_t step_preload();
+cudaError_t dist_exchange_update(kge_handle* h, const Slot& s);
 
 // tc.cu
 bool tc_init(kge_handle* h);

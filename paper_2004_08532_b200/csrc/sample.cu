@@ -155,6 +155,10 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
 
 size_t sample_smem_bytes(int n_pad) { return (size_t)n_pad * sizeof(unsigned long long); }
 
+cudaError_t sample_init() {
+  return cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
 cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev, int ring, int64_t step0, int n_steps) {
   SampleArgs a;
   a.p = p;
@@ -162,12 +166,8 @@ cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slot
   a.slots = slots_dev;
   a.ring = ring;
   a.step0 = step0;
-  size_t smem = sample_smem_bytes(p.n_pad);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  size_t smem = sample_smem_bytes(p.n_pad);  // opt-in raised once by sample_init (never in the step path: the call
+                                              // may synchronise, which would stall the multi-rank emulation)
   launch_begin(h, KGE_K_SAMPLE);
   k_sample<<<dim3(n_steps, 2), kSampleThreads, smem, h->stream>>>(a);
   launch_end(h, KGE_K_SAMPLE);
@@ -175,21 +175,23 @@ cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slot
 }
 
 // ---- table init (reading c.6) ----
+// local row l holds global row l * row_stride + row_offset (entity shards: stride P, offset rank)
 __global__ void k_init_table(float* __restrict__ tab, int64_t n_elem, int32_t w, uint32_t k0, uint32_t k1,
-                             uint32_t table_id, float bound) {
+                             uint32_t table_id, float bound, int64_t row_stride, int64_t row_offset) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_elem; i += stride) {
-    const uint64_t row = (uint64_t)(i / w);
-    const uint32_t col = (uint32_t)(i - (int64_t)row * w);
-    tab[i] = init_value(k0, k1, table_id, row, col, bound);
+    const int64_t lrow = i / w;
+    const uint32_t col = (uint32_t)(i - lrow * w);
+    tab[i] = init_value(k0, k1, table_id, (uint64_t)(lrow * row_stride + row_offset), col, bound);
   }
 }
 
-cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound) {
+cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound,
+                              int64_t row_stride, int64_t row_offset) {
   const int64_t n = rows * (int64_t)w;
   if (n == 0) return cudaSuccess;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 64);
-  k_init_table<<<blocks, 256, 0, h->stream>>>(tab, n, w, h->k0, h->k1, table_id, bound);
+  k_init_table<<<blocks, 256, 0, h->stream>>>(tab, n, w, h->k0, h->k1, table_id, bound, row_stride, row_offset);
   ++h->launches;
   return cudaGetLastError();
 }

@@ -181,7 +181,7 @@ __device__ __forceinline__ float pair_score_from(int fam, float stat, float gamm
 struct GatherArgs {
   Dims dm;
   Slot s;
-  const float* ent;
+  EntRows ent;
   const float* rel;
   StepBuffers b;
   int32_t first_row;  // B: negatives only (TransR handles its positives in transr.cu)
@@ -194,8 +194,8 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
   const int n_neg = dm.C * dm.k;
   if (row < dm.B) {
     const int i = row, mode = a.s.mode[i / dm.g];
-    const float* h = a.ent + (int64_t)a.s.ph[i] * dm.d;
-    const float* t = a.ent + (int64_t)a.s.pt[i] * dm.d;
+    const float* h = a.ent.row(a.s.ph[i]);
+    const float* t = a.ent.row(a.s.pt[i]);
     const float* r = a.rel + (int64_t)a.s.pr[i] * dm.drel;
     float* o = a.b.O + (int64_t)i * dm.dp;
     float stat, on;
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     }
   } else if (row < dm.B + n_neg) {
     const int q = row - dm.B;
-    const float* x = a.ent + (int64_t)a.s.neg[q] * dm.d;
+    const float* x = a.ent.row(a.s.neg[q]);
     float* X = a.b.X + (int64_t)q * dm.dp;
     float acc = 0.f;
     for (int v = lane; v < (dm.d >> 2); v += 32) {
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
 struct ChainArgs {
   Dims dm;
   Slot s;
-  const float* ent;
+  EntRows ent;
   const float* rel;
   StepBuffers b;
   int32_t n_neg_parts;
@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= dm.B) return;
   const int mode = a.s.mode[i / dm.g];
-  const float* h = a.ent + (int64_t)a.s.ph[i] * dm.d;
-  const float* t = a.ent + (int64_t)a.s.pt[i] * dm.d;
+  const float* h = a.ent.row(a.s.ph[i]);
+  const float* t = a.ent.row(a.s.pt[i]);
   const float* r = a.rel + (int64_t)a.s.pr[i] * dm.drel;
   const float* o = a.b.O + (int64_t)i * dm.dp;
   const float* dO = a.b.dO + (int64_t)i * dm.d;
@@ -676,6 +676,9 @@ struct UpdateArgs {
   float* rel;
   float* rel_st;
   StepBuffers b;
+  float* gu;                   // P > 1: per-unique entity gradient sums go here (the owner applies Adagrad)
+  const int32_t* split_index;  // P > 1: relation -> index among split relations, -1 if not split
+  float* grel_split;           // P > 1: per-rank sums of split relations
 };
 
 // Segment sum of one unique row's occurrence gradients, in sorted-occurrence order, V float4 per lane.
@@ -764,6 +767,16 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a, int n_ent_blocks) 
     if (u >= *a.s.ent_n) return;
     const int32_t id = a.s.ent_uniq[u];
     const int w4 = dm.d >> 2;
+    if (a.gu) {  // P > 1: segment sum only; rows live at their owner (dist.cu)
+      RowAcc<V> acc;
+      acc.zero();
+      seg_sum<V>(acc, a.b.Gocc, a.s.ent_occ, a.s.ent_off[u], a.s.ent_off[u + 1], 1, w4, dm.d, lane);
+      float* dst = a.gu + (int64_t)u * dm.d;
+#pragma unroll
+      for (int m = 0; m < V; ++m)
+        if (lane + 32 * m < w4) st4(dst, lane + 32 * m, acc.g[m]);
+      return;
+    }
     float* row = a.ent + (int64_t)id * dm.d;
     float4 row_v[V];
     prefetch_row<V>(row, row_v, w4, lane);
@@ -779,7 +792,8 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a, int n_ent_blocks) 
   __shared__ float4 part[8][32 * V];
   const int32_t id = a.s.rel_uniq[u];
   const int w = dm.drel, w4 = w >> 2;
-  float* row = a.rel + (int64_t)id * w;
+  const int sidx = a.split_index ? a.split_index[id] : -1;
+  float* row = sidx >= 0 ? a.grel_split + (int64_t)sidx * w : a.rel + (int64_t)id * w;
   float4 row_v[V];
   if (warp == 0) prefetch_row<V>(row, row_v, w4, lane);
   const float st0 = a.rel_st[id];
@@ -795,6 +809,12 @@ __global__ void __launch_bounds__(256) k_update(UpdateArgs a, int n_ent_blocks) 
   for (int ww = 0; ww < 8; ++ww)
 #pragma unroll
     for (int m = 0; m < V; ++m) tot.add(part[ww][lane + 32 * m], m);
+  if (sidx >= 0) {  // split relation (P > 1): this rank's sum; every replica updates from the rank-ordered total
+#pragma unroll
+    for (int m = 0; m < V; ++m)
+      if (lane + 32 * m < w4) st4(row, lane + 32 * m, tot.g[m]);
+    return;
+  }
   adagrad_row<V>(row, a.rel_st + id, tot, row_v, st0, w4, w, dm.lr, dm.eps, lane);
 }
 
@@ -819,7 +839,7 @@ static void launch_neg(kge_handle* h, const NegArgs& na) {
 
 cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
-  GatherArgs ga{dm, s, h->ent, h->rel, h->buf, dm.B};
+  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, dm.B};
   const int rows = dm.C * dm.k;
   k_gather<<<(rows + 7) / 8, 256, 0, h->stream>>>(ga);
   return cudaGetLastError();
@@ -827,7 +847,8 @@ cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
 
 cudaError_t launch_update(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
-  UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, h->buf};
+  UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, h->buf, h->P > 1 ? h->dist.gu : nullptr,
+                h->P > 1 ? h->dist.split_index : nullptr, h->dist.grel_split};
   const int n_ent_blocks = (dm.n_occ + 7) / 8;
   const int grid = n_ent_blocks + dm.B;
   const int w4 = dm.d / 4;
@@ -847,7 +868,7 @@ cudaError_t launch_update(kge_handle* h, const Slot& s) {
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
   if (dm.model == KGE_TRANSR) return launch_transr_step(h, s, step);
-  GatherArgs ga{dm, s, h->ent, h->rel, h->buf, 0};
+  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0};
   const int rows = dm.B + dm.C * dm.k;
   launch_begin(h, KGE_K_GATHER);
   k_gather<<<(rows + 7) / 8, 256, 0, h->stream>>>(ga);
@@ -866,7 +887,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
       case FAM_CMOD: launch_neg<FAM_CMOD>(h, na); break;
     }
   }
-  ChainArgs ca{dm, s, h->ent, h->rel, h->buf, h->n_neg_parts, (int32_t)(step % h->ring)};
+  ChainArgs ca{dm, s, h->rows, h->rel, h->buf, h->n_neg_parts, (int32_t)(step % h->ring)};
   launch_begin(h, KGE_K_CHAIN);
   k_chain<<<(dm.B + 7) / 8 + 1, 256, 0, h->stream>>>(ca);
   launch_end(h, KGE_K_CHAIN);
@@ -877,7 +898,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
 // ---- kge_score: f(h, r, t) per triple (tail-mode decomposition: f = pair(combine(h, r), t)) ----
 struct ScoreArgs {
   Dims dm;
-  const float* ent;
+  EntRows ent;
   const float* rel;
   const int32_t* hs;
   const int32_t* rs;
@@ -892,8 +913,8 @@ __global__ void __launch_bounds__(256) k_score(ScoreArgs a) {
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= a.n) return;
   const Dims& dm = a.dm;
-  const float* h = a.ent + (int64_t)a.hs[i] * dm.d;
-  const float* t = a.ent + (int64_t)a.ts[i] * dm.d;
+  const float* h = a.ent.row(a.hs[i]);
+  const float* t = a.ent.row(a.ts[i]);
   const float* r = a.rel + (int64_t)a.rs[i] * dm.drel;
   float* o = a.o_scratch + i * dm.dp;
   float st, on;
@@ -911,7 +932,7 @@ cudaError_t launch_score(kge_handle* h, const int32_t* hs, const int32_t* rs, co
   const int64_t cap = (int64_t)h->dims.C * h->dims.k;
   for (int64_t b = 0; b < n; b += cap) {
     const int64_t m = std::min(cap, n - b);
-    ScoreArgs sa{h->dims, h->ent, h->rel, hs + b, rs + b, ts + b, m, h->buf.X, out + b};
+    ScoreArgs sa{h->dims, h->rows, h->rel, hs + b, rs + b, ts + b, m, h->buf.X, out + b};
     k_score<<<(unsigned)((m + 7) / 8), 256, 0, h->stream>>>(sa);
     ++h->launches;
   }
@@ -939,6 +960,37 @@ cudaError_t launch_rows(kge_handle* h, float* tab, int32_t w, const int32_t* ids
   k_rows<<<blocks, 256, 0, h->stream>>>(tab, w, ids, n, buf, write ? 1 : 0);
   ++h->launches;
   return cudaGetLastError();
+}
+
+// Force-load every kernel of this file at init: with CUDA's lazy module loading, the first launch of a kernel may wait
+// for running kernels -- a deadlock when a peer's device barrier is spinning (multi-rank emulation on one device).
+template <typename F>
+static void preload(F f, cudaError_t& e) {
+  cudaFuncAttributes at;
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, (const void*)f);
+}
+
+cudaError_t step_preload() {
+  cudaError_t e = cudaSuccess;
+  preload(k_gather, e);
+  preload(k_chain, e);
+  preload(k_score, e);
+  preload(k_rows, e);
+  preload(k_update<1>, e);
+  preload(k_update<2>, e);
+  preload(k_update<4>, e);
+  preload(k_update<8>, e);
+  preload(k_neg_fwd<FAM_DOT>, e);
+  preload(k_neg_fwd<FAM_L2>, e);
+  preload(k_neg_fwd<FAM_L2SQ>, e);
+  preload(k_neg_fwd<FAM_L1>, e);
+  preload(k_neg_fwd<FAM_CMOD>, e);
+  preload(k_neg_bwd<FAM_DOT>, e);
+  preload(k_neg_bwd<FAM_L2>, e);
+  preload(k_neg_bwd<FAM_L2SQ>, e);
+  preload(k_neg_bwd<FAM_L1>, e);
+  preload(k_neg_bwd<FAM_CMOD>, e);
+  return e;
 }
 
 }  // namespace kge

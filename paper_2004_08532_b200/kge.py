@@ -18,6 +18,10 @@ import numpy as np
 
 from .build import LIB
 
+# Kernels are force-loaded at kge_init; eager loading (when set before CUDA initialises) is belt and braces for the
+# multi-rank device barriers (a lazily loaded kernel may wait for a spinning barrier kernel).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 MODELS = {"transe_l1": 0, "transe_l2": 1, "distmult": 2, "complex": 3, "rotate": 4, "transr": 5}
 CORRUPT = {"tail": 0, "head": 1, "alternate": 2}
 PRECISION = {"fp32": 0, "tf32": 1}
@@ -81,6 +85,14 @@ def lib():
         L.kge_launch_count.argtypes = [ctypes.c_void_p]
         L.kge_launch_count.restype = ctypes.c_int64
         L.kge_destroy.argtypes = [ctypes.c_void_p]
+        L.kge_read_losses.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, _fp]
+        L.kge_partition.argtypes = [_i64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _i32p, _i64p,
+                                    _i64p]
+        L.kge_export.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P(ctypes.c_size_t)]
+        L.kge_connect.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
+        L.kge_connect_local.argtypes = [P(ctypes.c_void_p), ctypes.c_int32]
+        L.kge_relation_owner.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        L.kge_relation_owner.restype = ctypes.c_int
         L.kge_last_error.restype = ctypes.c_char_p
         L.kge_kernel_name.argtypes = [ctypes.c_int32]
         L.kge_kernel_name.restype = ctypes.c_char_p
@@ -255,6 +267,26 @@ class Handle:
     def step(self):
         return lib().kge_step(self._h)
 
+    def read_losses(self, first_step, n):
+        out = np.zeros(n, np.float32)
+        _check(lib().kge_read_losses(self._h, first_step, n, _ptr(out, ctypes.c_float)))
+        return out
+
+    def relation_owner(self, r):
+        return lib().kge_relation_owner(self._h, int(r))
+
+    def export(self) -> bytes:
+        n = ctypes.c_size_t(0)
+        _check(lib().kge_export(self._h, None, ctypes.byref(n)))
+        buf = (ctypes.c_char * n.value)()
+        _check(lib().kge_export(self._h, buf, ctypes.byref(n)))
+        return bytes(buf)
+
+    def connect(self, blobs):
+        joined = b"".join(blobs)
+        buf = ctypes.create_string_buffer(joined, len(joined))
+        _check(lib().kge_connect(self._h, buf, len(blobs)))
+
     def set_step(self, s):
         _check(lib().kge_set_step(self._h, s))
 
@@ -303,3 +335,50 @@ def init(cfg: Config, heads, rels, tails, use_torch_allocator=True, stream=None)
     _check(lib().kge_init(ctypes.byref(out), ctypes.byref(c), _ptr(h, ctypes.c_int64), _ptr(r, ctypes.c_int64),
                           _ptr(t, ctypes.c_int64), len(h)))
     return Handle(out.value, cfg, keep)
+
+
+def partition(rels, n_relations, world_size, rank):
+    """kge_partition (host-only, no GPU needed): relation owner per relation (-1 = split) and this rank's triples."""
+    rels = _i64(rels)
+    owner = np.zeros(n_relations, np.int32)
+    n = ctypes.c_int64()
+    _check(lib().kge_partition(_ptr(rels, ctypes.c_int64), len(rels), n_relations, world_size, rank,
+                               _ptr(owner, ctypes.c_int32), None, ctypes.byref(n)))
+    lst = np.zeros(n.value, np.int64)
+    _check(lib().kge_partition(_ptr(rels, ctypes.c_int64), len(rels), n_relations, world_size, rank, None,
+                               _ptr(lst, ctypes.c_int64), ctypes.byref(n)))
+    return owner, lst
+
+
+def exchange_and_connect(handle: Handle, all_gather_object):
+    """World-size > 1: gather every rank's IPC blob with the caller's collective (torch.distributed.all_gather_object)
+    and connect. Host-side plumbing only; the exchange itself runs in the library's kernels over NVLink."""
+    mine = handle.export()
+    world = handle.cfg.world_size
+    blobs = [None] * world
+    all_gather_object(blobs, mine)
+    handle.connect(blobs)
+    return blobs
+
+
+def init_distributed(cfg: Config, heads, rels, tails, stream=None) -> Handle:
+    """One process per GPU (torchrun): kge_init on this rank, then IPC exchange through torch.distributed."""
+    import torch.distributed as dist
+    h = init(cfg, heads, rels, tails, use_torch_allocator=True, stream=stream)
+    exchange_and_connect(h, dist.all_gather_object)
+    return h
+
+
+def init_local_group(cfg: Config, world_size: int, heads, rels, tails):
+    """Single-process emulation of world_size ranks on the current device (one handle and stream per rank), connected
+    directly (kge_connect_local). Used by the one-GPU parity tests of the multi-rank path."""
+    import dataclasses
+
+    import torch
+    hs = []
+    for w in range(world_size):
+        c = dataclasses.replace(cfg, world_size=world_size, rank=w)
+        hs.append(init(c, heads, rels, tails, stream=torch.cuda.Stream()))
+    arr = (ctypes.c_void_p * world_size)(*[h._h for h in hs])
+    _check(lib().kge_connect_local(arr, world_size))
+    return hs

@@ -1,0 +1,78 @@
+"""P > 1 ranks on one GPU (single-process emulation: P handles, one stream each, connected directly) against the
+oracle's P-rank simulation (reading c.13: one step over the union of the rank batches, losses summed; entity gradients
+summed at the owner before one Adagrad step; split relations summed in rank order). The kernels are the multi-process
+ones: rows are read through the owner's shard pointer, owners pull gradients, device barriers order the phases."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from paper_2004_08532_b200 import kge
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(model, P, shape, steps, precision="fp32", graph="tiny", variant=0):
+    B, g, k, d = shape
+    gr = synth.graph(graph)
+    trip = gr.triples()
+    cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=d, batch_size=B,
+                     chunk_size=g, neg_k=k, neg_precision=precision, rotate_variant=variant)
+    hs = kge.init_local_group(cfg, P, *trip)
+    orc = O.Trainer(model, gr.n_entities, gr.n_relations, d, B, g, k, world_size=P, triples=trip,
+                    rotate_variant=variant)
+    # integer half per rank: bit-exact
+    for w in range(P):
+        s = hs[w].sample(3)
+        pos, neg, mode = orc.sample(3, w)
+        assert np.array_equal(s["pos"], pos) and np.array_equal(s["neg"], neg) and np.array_equal(s["mode"], mode)
+    for _ in range(steps):
+        for h in hs:
+            h.train_step(1, return_loss=False)
+    for h in hs:
+        h.sync()
+    lg = sum(h.read_losses(0, steps).astype(np.float64) for h in hs)
+    lo = orc.train(steps)
+    return gr, hs, orc, lg, lo
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("model", ["transe_l2", "distmult", "rotate"])
+def test_dist_parity_fp32(model, P):
+    gr, hs, orc, lg, lo = _run(model, P, (128, 32, 32, 32), 30)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5, (lg[:5], lo[:5])
+    ids = np.arange(gr.n_entities)
+    got = np.stack([hs[e % P].get_rows(0, [e])[0] for e in ids])
+    assert np.abs(got - orc.get_rows(0, ids)).max() <= 1e-4
+    rids = np.arange(gr.n_relations)
+    owners = [hs[0].relation_owner(r) for r in rids]
+    rel = np.stack([hs[max(o, 0)].get_rows(1, [r])[0] for r, o in zip(rids, owners)])
+    assert np.abs(rel - orc.get_rows(1, rids)).max() <= 1e-4
+    st = np.stack([hs[e % P].get_rows(3, [e])[0] for e in ids])
+    assert np.abs(st[:, 0] - orc.get_rows(3, ids)[:, 0]).max() <= 1e-6
+
+
+def test_dist_split_relations_and_tf32():
+    # tiny has 20 Zipf relations: at P = 8 the heavy ones exceed N_t/P and are split (replicated, summed in rank order)
+    gr, hs, orc, lg, lo = _run("transe_l2", 8, (256, 64, 64, 64), 20, precision="tf32")
+    assert any(hs[0].relation_owner(r) == -1 for r in range(gr.n_relations))
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 2e-3
+    # split relation replicas agree exactly on every rank
+    for r in range(gr.n_relations):
+        if hs[0].relation_owner(r) == -1:
+            rows = [h.get_rows(1, [r]) for h in hs]
+            assert all(np.array_equal(rows[0], x) for x in rows[1:])
+
+
+def test_dist_requires_connect_and_owner_rows():
+    gr = synth.graph("tiny")
+    trip = gr.triples()
+    cfg = kge.Config(model="transe_l2", n_entities=gr.n_entities, n_relations=gr.n_relations, dim=32, batch_size=64,
+                     chunk_size=16, neg_k=16, world_size=2, rank=1)
+    h = kge.init(cfg, *trip)
+    with pytest.raises(kge.KgeError) as ei:
+        h.train_step(1)
+    assert ei.value.status == -7
+    with pytest.raises(kge.KgeError):
+        h.get_rows(0, [0])  # entity 0 is owned by rank 0
+    assert h.get_rows(0, [1]).shape == (1, 32)
