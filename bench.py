@@ -49,44 +49,51 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi clock / throttle sampling during the timed region (B200_PROFILING.md clocks line): one streaming
+    nvidia-smi process (-lms 50) started before the region and stopped after it."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index=0):
         self.gpu = gpu_index
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._p = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "50"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let it start sampling before the region begins
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(0.06)
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=10)
+        except Exception:
+            self._p.kill()
+            out = ""
+        for line in (out or "").splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        num = lambda x: float(x) if x.replace(".", "").isdigit() else None
+        sm = [num(s[0]) for s in self.samples if num(s[0]) is not None]
+        mx = [num(s[1]) for s in self.samples if num(s[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]
-                          and "Not" not in s[2 + i]})
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if "Active" in s[2 + i] and "Not" not in s[2 + i]})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.samples)}
 
@@ -148,7 +155,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--steps", type=int, default=4000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--workload", default="freebase", choices=sorted(WORKLOADS))
     ap.add_argument("--model", default=None)
@@ -172,11 +179,15 @@ def main():
     from paper_2004_08532_b200 import kge
 
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    device = int(os.environ.get("KGE_BENCH_DEVICE", local))  # override only for single-GPU plumbing checks
+    torch.cuda.set_device(device)
     pg = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("KGE_BENCH_DEVICE") is not None:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
         pg = dist
     gname, model, d, B, g, k = wl
     gr = synth.graph(gname)
@@ -184,11 +195,15 @@ def main():
     h_, r_, t_ = gr.triples()
     t_gen = time.perf_counter() - t0
     cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=d, batch_size=B,
-                     chunk_size=g, neg_k=k, gamma=12.0, lr=0.1, seed=1 + rank, neg_precision=args.precision)
+                     chunk_size=g, neg_k=k, gamma=12.0, lr=0.1, seed=1, neg_precision=args.precision,
+                     world_size=ws, rank=rank)
     stream = torch.cuda.Stream()  # the library enqueues on this stream; events below are recorded on it
     t0 = time.perf_counter()
     with torch.cuda.stream(stream):
-        H = kge.init(cfg, h_, r_, t_)
+        if ws > 1:  # sharded entity table, relation partition, exchange over NVLink peer memory (dist.cu)
+            H = kge.init_distributed(cfg, h_, r_, t_, stream=stream)
+        else:
+            H = kge.init(cfg, h_, r_, t_, stream=stream)
     torch.cuda.synchronize()
     t_init = time.perf_counter() - t0
 
@@ -207,7 +222,7 @@ def main():
         pg.barrier()
     torch.cuda.synchronize()
     launches0 = H.launch_count
-    with Clocks(local) as clk:
+    with Clocks(device) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         w0 = time.perf_counter()
@@ -220,7 +235,7 @@ def main():
     gpu_launches = H.launch_count - launches0
     ms = max(ms_dev, 0.0)
     if pg:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if pg.get_backend() == "nccl" else "cpu")
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ms = float(t.item())
     value = ws * B * args.steps / (ms / 1000.0)
@@ -275,7 +290,7 @@ def main():
     H.sync()
     e2e_s = time.perf_counter() - w0
     if pg:
-        t = torch.tensor([e2e_s], device="cuda")
+        t = torch.tensor([e2e_s], device="cuda" if pg.get_backend() == "nccl" else "cpu")
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = {"value": ws * B * e2e_steps / e2e_s, "unit": "positive triples/s", "h2d_bytes_per_step": 3 * B * 4,
@@ -297,6 +312,8 @@ def main():
                 "config": {"workload": f"{gname}-shaped synthetic (BASELINE.json configs)", "model": model, "dim": d,
                            "batch": B, "chunk": g, "neg_k": k, "n_entities": gr.n_entities,
                            "n_relations": gr.n_relations, "n_triples": gr.n_triples,
+                           "parallelism": f"dp{ws}" + (" (relation-partitioned triples, entity rows sharded e mod P, "
+                                                       "exchange over NVLink peer memory)" if ws > 1 else ""),
                            "l2": "inputs larger than L2 (entity table >> 126 MB)" if gr.n_entities * d * 4 > 2e9
                            else "tables L2-resident (no flush)"},
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,

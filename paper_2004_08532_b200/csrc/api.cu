@@ -561,7 +561,7 @@ int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
 
 int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails, float* loss_out) {
   if (!h || !heads || !rels || !tails) { set_error("NULL argument"); return KGE_EINVAL; }
-  if (h->P > 1) { set_error("kge_train_batch is single-rank in this build"); return KGE_EUNSUPPORTED; }
+  if (h->P > 1 && !h->dist.connected) { set_error("world_size > 1: call kge_connect first"); return KGE_ESTATE; }
   const int B = h->dims.B;
   const int64_t s = h->step;
   // host-side range check + int32 narrowing into pinned staging, then one H2D copy
@@ -578,6 +578,12 @@ int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, co
     st[B + i] = (int32_t)rels[i];
     st[2 * B + i] = (int32_t)tails[i];
   }
+  if (h->P > 1) {  // B1 (see kge_train_step); every rank must call kge_train_batch for this step
+    e = dist_barrier(h);
+    if (e == cudaSuccess && h->dist.n_split > 0)
+      e = cudaMemsetAsync(h->dist.grel_split, 0, (size_t)h->dist.n_split * h->dims.drel * 4, h->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "barrier");
+  }
   e = cudaMemcpyAsync(h->given, st, (size_t)3 * B * 4, cudaMemcpyHostToDevice, h->stream);
   if (e != cudaSuccess) return cuda_fail(e, "batch upload");
   // sample negatives + dedup for this step into the debug slot, from the given positives
@@ -585,6 +591,7 @@ int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, co
   e = launch_sample(h, p, d_slots(h) + h->ring, 1, s, 1);
   if (e != cudaSuccess) return cuda_fail(e, "sample");
   e = launch_step(h, h->debug_slot, s);
+  if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, h->debug_slot);
   if (e != cudaSuccess) return cuda_fail(e, "step");
   h->step = s + 1;
   if (h->ring_first >= 0 && s >= h->ring_first && s < h->ring_first + h->ring) h->ring_first = -1;
