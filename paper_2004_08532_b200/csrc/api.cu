@@ -465,8 +465,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(std::max<int64_t>(h->n_neg_parts, tc_parts), dm.B) * 4);
-  b.rowsumW = (float*)dalloc(h, (size_t)dm.B * 4);
-  b.colsumW = (float*)dalloc(h, (size_t)nneg * 4);
+  b.rowsumW = (float*)dalloc(h, (size_t)dm.B * ((dm.k + 31) / 32) * 4);       // tc.cu partial row sums of W
+  b.colsumW = (float*)dalloc(h, (size_t)nneg * ((dm.g + 127) / 128) * 4);     // tc.cu partial column sums of W
   b.dO = (float*)dalloc(h, (size_t)dm.B * dm.d * 4);
   b.Gocc = (float*)dalloc(h, (size_t)dm.n_occ * dm.d * 4);
   b.Grel = (float*)dalloc(h, (size_t)dm.B * dm.drel * 4);

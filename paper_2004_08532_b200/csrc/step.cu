@@ -187,6 +187,113 @@ struct GatherArgs {
   int32_t first_row;  // B: negatives only (TransR handles its positives in transr.cu)
 };
 
+// Register-staged rows: every lane issues all of its row loads before any arithmetic or store, so a warp has its whole
+// row in flight at once (the per-iteration loop otherwise serialises on load latency, since the stores to O / X'
+// may alias the next iteration's loads as far as the compiler knows). V = float4 per lane (d <= 128 * V).
+template <int V>
+struct Row4 {
+  float4 v[V];
+  __device__ __forceinline__ void load(const float* __restrict__ p, int lane, int n4) {
+#pragma unroll
+    for (int m = 0; m < V; ++m) {
+      const int q = lane + 32 * m;
+      v[m] = q < n4 ? ld4(p, q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+};
+
+__device__ __forceinline__ void f4_to(const float4& a, float* x) {
+  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+}
+
+template <int V>
+__device__ __forceinline__ void combine_stage(int model, int mode, const float* __restrict__ h, const float* __restrict__ r,
+                                              const float* __restrict__ t, const float* __restrict__ other,
+                                              float* __restrict__ o, int d, int lane, int fam, float& stat, float& onorm) {
+  stat = 0.f;
+  onorm = 0.f;
+  if (!is_complex_model(model)) {
+    const int d4 = d >> 2;
+    Row4<V> X, R, Y;
+    X.load(mode == 0 ? h : t, lane, d4);
+    R.load(r, lane, d4);
+    Y.load(other, lane, d4);
+#pragma unroll
+    for (int m = 0; m < V; ++m) {
+      const int q = lane + 32 * m;
+      if (q >= d4) continue;
+      float xv[4], rv[4], yv[4], ov[4];
+      f4_to(X.v[m], xv);
+      f4_to(R.v[m], rv);
+      f4_to(Y.v[m], yv);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ov[u] = model == KGE_DISTMULT ? xv[u] * rv[u] : (mode == 0 ? xv[u] + rv[u] : xv[u] - rv[u]);
+        onorm += ov[u] * ov[u];
+        const float df = ov[u] - yv[u];
+        stat += fam == FAM_DOT ? ov[u] * yv[u] : (fam == FAM_L1 ? fabsf(df) : df * df);
+      }
+      st4(o, q, make_float4(ov[0], ov[1], ov[2], ov[3]));
+    }
+    return;
+  }
+  const int n4 = d >> 3;
+  const float* e = mode == 0 ? h : t;
+  Row4<V> A, Bm, R1, R2, XR, XI;
+  A.load(e, lane, n4);
+  Bm.load(e + 4 * n4, lane, n4);
+  R1.load(r, lane, n4);
+  if (model == KGE_COMPLEX) R2.load(r + 4 * n4, lane, n4);
+  XR.load(other, lane, n4);
+  XI.load(other + 4 * n4, lane, n4);
+#pragma unroll
+  for (int m = 0; m < V; ++m) {
+    const int q = lane + 32 * m;
+    if (q >= n4) continue;
+    float a[4], b[4], c1[4], c2[4], xr[4], xi[4], outr[4], outi[4];
+    f4_to(A.v[m], a);
+    f4_to(Bm.v[m], b);
+    f4_to(R1.v[m], c1);
+    f4_to(XR.v[m], xr);
+    f4_to(XI.v[m], xi);
+    if (model == KGE_COMPLEX) {
+      f4_to(R2.v[m], c2);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float sn, cs;
+        sincosf(c1[u], &sn, &cs);
+        c1[u] = cs;
+        c2[u] = sn;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      // c1 = Re r (or cos theta), c2 = Im r (or sin theta)
+      if (mode == 0) {  // h * r
+        outr[u] = a[u] * c1[u] - b[u] * c2[u];
+        outi[u] = a[u] * c2[u] + b[u] * c1[u];
+      } else {          // ComplEx: [rr tr + ri ti | rr ti - ri tr];  RotatE: t e^{-i theta} (same formula)
+        outr[u] = c1[u] * a[u] + c2[u] * b[u];
+        outi[u] = c1[u] * b[u] - c2[u] * a[u];
+      }
+      onorm += outr[u] * outr[u] + outi[u] * outi[u];
+      const float ur = outr[u] - xr[u], ui = outi[u] - xi[u];
+      if (fam == FAM_DOT)
+        stat += outr[u] * xr[u] + outi[u] * xi[u];
+      else if (fam == FAM_CMOD)
+        stat += sqrtf(ur * ur + ui * ui);
+      else if (fam == FAM_L1)
+        stat += fabsf(ur) + fabsf(ui);
+      else
+        stat += ur * ur + ui * ui;
+    }
+    st4(o, q, make_float4(outr[0], outr[1], outr[2], outr[3]));
+    st4(o, q + n4, make_float4(outi[0], outi[1], outi[2], outi[3]));
+  }
+}
+
+template <int V>
 __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
   const Dims& dm = a.dm;
   const int lane = threadIdx.x & 31;
@@ -199,7 +306,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     const float* r = a.rel + (int64_t)a.s.pr[i] * dm.drel;
     float* o = a.b.O + (int64_t)i * dm.dp;
     float stat, on;
-    combine_row(dm.model, mode, h, r, t, o, dm.d, lane, mode == 0 ? t : h, dm.family, stat, on);
+    combine_stage<V>(dm.model, mode, h, r, t, mode == 0 ? t : h, o, dm.d, lane, dm.family, stat, on);
     stat = warp_sum(stat);
     on = warp_sum(on);
     if (lane == 0) {
@@ -211,13 +318,19 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     }
   } else if (row < dm.B + n_neg) {
     const int q = row - dm.B;
-    const float* x = a.ent.row(a.s.neg[q]);
+    const int d4 = dm.d >> 2;
+    Row4<V> Xr;
+    Xr.load(a.ent.row(a.s.neg[q]), lane, d4);
     float* X = a.b.X + (int64_t)q * dm.dp;
     float acc = 0.f;
-    for (int v = lane; v < (dm.d >> 2); v += 32) {
-      const float4 xv = ld4(x, v);
-      st4(X, v, xv);
-      acc += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
+#pragma unroll
+    for (int m = 0; m < V; ++m) {
+      const int v = lane + 32 * m;
+      if (v < d4) {
+        const float4 xv = Xr.v[m];
+        st4(X, v, xv);
+        acc += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
+      }
     }
     acc = warp_sum(acc);
     if (lane == 0) a.b.xnorm[q] = acc;
@@ -523,6 +636,7 @@ __device__ __forceinline__ void dpair(int fam, float o, float x, float scale, fl
   }
 }
 
+template <int V>
 __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
   const Dims& dm = a.dm;
   const int lane = threadIdx.x & 31;
@@ -553,108 +667,131 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
   const float* o = a.b.O + (int64_t)i * dm.dp;
   const float* dO = a.b.dO + (int64_t)i * dm.d;
   const float* other = mode == 0 ? t : h;
+  const float* ent_c = mode == 0 ? h : t;  // the combined entity side
   float* gH = a.b.Gocc + (int64_t)i * dm.d;
   float* gT = a.b.Gocc + (int64_t)(dm.B + i) * dm.d;
   float* gR = a.b.Grel + (int64_t)i * dm.drel;
-  float* gOther = mode == 0 ? gT : gH;  // the non-combined side
+  float* gOther = mode == 0 ? gT : gH;
+  float* gC = mode == 0 ? gH : gT;
   const float wp = a.b.wpos[i];
-  float scale = wp;
-  if (dm.family == FAM_L2) scale = wp / fmaxf(sqrtf(a.b.pstat[i]), 1e-12f);
+  const float scale = dm.family == FAM_L2 ? wp / fmaxf(sqrtf(a.b.pstat[i]), 1e-12f) : wp;
   const int model = dm.model;
   if (!is_complex_model(model)) {
     const int d4 = dm.d >> 2;
-    for (int v = lane; v < d4; v += 32) {
-      const float4 ov = ld4(o, v), xv = ld4(other, v), dv = ld4(dO, v);
-      const float oo[4] = {ov.x, ov.y, ov.z, ov.w}, xx[4] = {xv.x, xv.y, xv.z, xv.w};
-      const float dd[4] = {dv.x, dv.y, dv.z, dv.w};
-      float go[4], gx[4];
+    Row4<V> Ov, Xv, Dv, Rv, Ev;
+    Ov.load(o, lane, d4);
+    Xv.load(other, lane, d4);
+    Dv.load(dO, lane, d4);
+    if (model == KGE_DISTMULT) {
+      Rv.load(r, lane, d4);
+      Ev.load(ent_c, lane, d4);
+    }
+#pragma unroll
+    for (int m = 0; m < V; ++m) {
+      const int v = lane + 32 * m;
+      if (v >= d4) continue;
+      float oo[4], xx[4], dd[4], go[4], gx[4];
+      f4_to(Ov.v[m], oo);
+      f4_to(Xv.v[m], xx);
+      f4_to(Dv.v[m], dd);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         dpair(dm.family, oo[u], xx[u], scale, go[u], gx[u]);
         go[u] += dd[u];
       }
       st4(gOther, v, make_float4(gx[0], gx[1], gx[2], gx[3]));
-      float4 gc, gr;  // grads of the combined entity side and of r
-      if (model == KGE_DISTMULT) {
-        // tail o = h*r : dh = go*r, dr = go*h ; head o = r*t : dt = go*r, dr = go*t
-        const float4 rv = ld4(r, v);
-        const float4 ev = mode == 0 ? ld4(h, v) : ld4(t, v);
+      float4 gc, gr;
+      if (model == KGE_DISTMULT) {  // tail o = h*r: dh = go*r, dr = go*h ; head o = r*t: dt = go*r, dr = go*t
+        const float4 rv = Rv.v[m], ev = Ev.v[m];
         gc = make_float4(go[0] * rv.x, go[1] * rv.y, go[2] * rv.z, go[3] * rv.w);
         gr = make_float4(go[0] * ev.x, go[1] * ev.y, go[2] * ev.z, go[3] * ev.w);
       } else {  // TransE: tail o = h + r ; head o = t - r
         gc = make_float4(go[0], go[1], go[2], go[3]);
         gr = mode == 0 ? gc : make_float4(-go[0], -go[1], -go[2], -go[3]);
       }
-      st4(mode == 0 ? gH : gT, v, gc);
+      st4(gC, v, gc);
       st4(gR, v, gr);
     }
     return;
   }
   // complex models: lanes own complex element groups (re at v, im at v + n4)
   const int n4 = dm.d >> 3;
-  float scale_c = scale;
-  for (int v = lane; v < n4; v += 32) {
-    const float4 orv = ld4(o, v), oiv = ld4(o, v + n4), xrv = ld4(other, v), xiv = ld4(other, v + n4);
-    const float4 drv = ld4(dO, v), div = ld4(dO, v + n4);
-    const float4 crv = mode == 0 ? ld4(h, v) : ld4(t, v);  // combined-side entity (re, im)
-    const float4 civ = mode == 0 ? ld4(h, v + n4) : ld4(t, v + n4);
-    const float o_r[4] = {orv.x, orv.y, orv.z, orv.w}, o_i[4] = {oiv.x, oiv.y, oiv.z, oiv.w};
-    const float x_r[4] = {xrv.x, xrv.y, xrv.z, xrv.w}, x_i[4] = {xiv.x, xiv.y, xiv.z, xiv.w};
-    const float d_r[4] = {drv.x, drv.y, drv.z, drv.w}, d_i[4] = {div.x, div.y, div.z, div.w};
-    const float e_r[4] = {crv.x, crv.y, crv.z, crv.w}, e_i[4] = {civ.x, civ.y, civ.z, civ.w};
-    float gxr[4], gxi[4], ger[4], gei[4], grr[4], gri[4];
-    float rr_[4], ri_[4];
-    if (model == KGE_COMPLEX) {
-      const float4 a_ = ld4(r, v), b_ = ld4(r, v + n4);
-      rr_[0] = a_.x; rr_[1] = a_.y; rr_[2] = a_.z; rr_[3] = a_.w;
-      ri_[0] = b_.x; ri_[1] = b_.y; ri_[2] = b_.z; ri_[3] = b_.w;
-    } else {
-      const float4 th = ld4(r, v);
-      const float tt[4] = {th.x, th.y, th.z, th.w};
+  Row4<V> OR, OI, XR, XI, DR, DI, ER, EI, R1, R2;
+  OR.load(o, lane, n4);
+  OI.load(o + 4 * n4, lane, n4);
+  XR.load(other, lane, n4);
+  XI.load(other + 4 * n4, lane, n4);
+  DR.load(dO, lane, n4);
+  DI.load(dO + 4 * n4, lane, n4);
+  ER.load(ent_c, lane, n4);
+  EI.load(ent_c + 4 * n4, lane, n4);
+  R1.load(r, lane, n4);
+  if (model == KGE_COMPLEX) R2.load(r + 4 * n4, lane, n4);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) sincosf(tt[u], &ri_[u], &rr_[u]);  // (cos, sin)
+  for (int m = 0; m < V; ++m) {
+    const int v = lane + 32 * m;
+    if (v >= n4) continue;
+    float o_r[4], o_i[4], x_r[4], x_i[4], d_r[4], d_i[4], e_r[4], e_i[4], rr_[4], ri_[4];
+    f4_to(OR.v[m], o_r);
+    f4_to(OI.v[m], o_i);
+    f4_to(XR.v[m], x_r);
+    f4_to(XI.v[m], x_i);
+    f4_to(DR.v[m], d_r);
+    f4_to(DI.v[m], d_i);
+    f4_to(ER.v[m], e_r);
+    f4_to(EI.v[m], e_i);
+    if (model == KGE_COMPLEX) {
+      f4_to(R1.v[m], rr_);
+      f4_to(R2.v[m], ri_);
+    } else {
+      float th[4];
+      f4_to(R1.v[m], th);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sincosf(th[u], &ri_[u], &rr_[u]);  // (cos, sin)
     }
+    float gxr[4], gxi[4], ger[4], gei[4], grr[4], gri[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       float gor, goi;
       if (dm.family == FAM_CMOD) {
         const float ur = o_r[u] - x_r[u], ui = o_i[u] - x_i[u];
-        const float inv = scale_c / fmaxf(sqrtf(ur * ur + ui * ui), 1e-12f);
-        gor = -inv * ur; goi = -inv * ui;
-        gxr[u] = inv * ur; gxi[u] = inv * ui;
+        const float inv = scale / fmaxf(sqrtf(ur * ur + ui * ui), 1e-12f);
+        gor = -inv * ur;
+        goi = -inv * ui;
+        gxr[u] = inv * ur;
+        gxi[u] = inv * ui;
       } else {
-        dpair(dm.family, o_r[u], x_r[u], scale_c, gor, gxr[u]);
-        dpair(dm.family, o_i[u], x_i[u], scale_c, goi, gxi[u]);
+        dpair(dm.family, o_r[u], x_r[u], scale, gor, gxr[u]);
+        dpair(dm.family, o_i[u], x_i[u], scale, goi, gxi[u]);
       }
       gor += d_r[u];
       goi += d_i[u];
-      const float c = rr_[u], s = ri_[u], a = e_r[u], b = e_i[u];
+      const float c = rr_[u], sn = ri_[u], ea = e_r[u], eb = e_i[u];
       if (model == KGE_COMPLEX) {
         if (mode == 0) {  // o = (a c - b s, a s + b c) with r = c + i s
-          ger[u] = gor * c + goi * s;
-          gei[u] = -gor * s + goi * c;
-          grr[u] = gor * a + goi * b;
-          gri[u] = -gor * b + goi * a;
+          ger[u] = gor * c + goi * sn;
+          gei[u] = -gor * sn + goi * c;
+          grr[u] = gor * ea + goi * eb;
+          gri[u] = -gor * eb + goi * ea;
         } else {  // o = (c a + s b, c b - s a) with t = a + i b
-          ger[u] = gor * c - goi * s;
-          gei[u] = gor * s + goi * c;
-          grr[u] = gor * a + goi * b;
-          gri[u] = gor * b - goi * a;
+          ger[u] = gor * c - goi * sn;
+          gei[u] = gor * sn + goi * c;
+          grr[u] = gor * ea + goi * eb;
+          gri[u] = gor * eb - goi * ea;
         }
       } else {  // RotatE, r = e^{i theta}
         if (mode == 0) {  // o = (a c - b s, a s + b c)
-          ger[u] = gor * c + goi * s;
-          gei[u] = -gor * s + goi * c;
-          grr[u] = gor * (-a * s - b * c) + goi * (a * c - b * s);
+          ger[u] = gor * c + goi * sn;
+          gei[u] = -gor * sn + goi * c;
+          grr[u] = gor * (-ea * sn - eb * c) + goi * (ea * c - eb * sn);
         } else {  // o = (a c + b s, -a s + b c)
-          ger[u] = gor * c - goi * s;
-          gei[u] = gor * s + goi * c;
-          grr[u] = gor * (-a * s + b * c) + goi * (-a * c - b * s);
+          ger[u] = gor * c - goi * sn;
+          gei[u] = gor * sn + goi * c;
+          grr[u] = gor * (-ea * sn + eb * c) + goi * (-ea * c - eb * sn);
         }
         gri[u] = 0.f;
       }
     }
-    float* gC = mode == 0 ? gH : gT;
     st4(gOther, v, make_float4(gxr[0], gxr[1], gxr[2], gxr[3]));
     st4(gOther, v + n4, make_float4(gxi[0], gxi[1], gxi[2], gxi[3]));
     st4(gC, v, make_float4(ger[0], ger[1], ger[2], ger[3]));
@@ -837,11 +974,26 @@ static void launch_neg(kge_handle* h, const NegArgs& na) {
 }
 
 
+static int row_v(int d) {  // float4 per lane for a d-float row
+  const int d4 = d / 4;
+  return d4 <= 32 ? 1 : (d4 <= 64 ? 2 : (d4 <= 128 ? 4 : 8));
+}
+
+static void launch_gather_v(kge_handle* h, const GatherArgs& ga, int rows) {
+  const unsigned grid = (rows + 7) / 8;
+  switch (row_v(h->dims.d)) {
+    case 1: k_gather<1><<<grid, 256, 0, h->stream>>>(ga); break;
+    case 2: k_gather<2><<<grid, 256, 0, h->stream>>>(ga); break;
+    case 4: k_gather<4><<<grid, 256, 0, h->stream>>>(ga); break;
+    default: k_gather<8><<<grid, 256, 0, h->stream>>>(ga); break;
+  }
+}
+
 cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
   GatherArgs ga{dm, s, h->rows, h->rel, h->buf, dm.B};
   const int rows = dm.C * dm.k;
-  k_gather<<<(rows + 7) / 8, 256, 0, h->stream>>>(ga);
+  launch_gather_v(h, ga, rows);
   return cudaGetLastError();
 }
 
@@ -871,7 +1023,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0};
   const int rows = dm.B + dm.C * dm.k;
   launch_begin(h, KGE_K_GATHER);
-  k_gather<<<(rows + 7) / 8, 256, 0, h->stream>>>(ga);
+  launch_gather_v(h, ga, rows);
   launch_end(h, KGE_K_GATHER);
 
   NegArgs na{dm, h->buf, h->buf.Gocc};
@@ -889,7 +1041,13 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   }
   ChainArgs ca{dm, s, h->rows, h->rel, h->buf, h->n_neg_parts, (int32_t)(step % h->ring)};
   launch_begin(h, KGE_K_CHAIN);
-  k_chain<<<(dm.B + 7) / 8 + 1, 256, 0, h->stream>>>(ca);
+  const unsigned cgrid = (dm.B + 7) / 8 + 1;
+  switch (row_v(dm.d)) {
+    case 1: k_chain<1><<<cgrid, 256, 0, h->stream>>>(ca); break;
+    case 2: k_chain<2><<<cgrid, 256, 0, h->stream>>>(ca); break;
+    case 4: k_chain<4><<<cgrid, 256, 0, h->stream>>>(ca); break;
+    default: k_chain<8><<<cgrid, 256, 0, h->stream>>>(ca); break;
+  }
   launch_end(h, KGE_K_CHAIN);
 
   return launch_update(h, s);
@@ -972,8 +1130,14 @@ static void preload(F f, cudaError_t& e) {
 
 cudaError_t step_preload() {
   cudaError_t e = cudaSuccess;
-  preload(k_gather, e);
-  preload(k_chain, e);
+  preload(k_gather<1>, e);
+  preload(k_gather<2>, e);
+  preload(k_gather<4>, e);
+  preload(k_gather<8>, e);
+  preload(k_chain<1>, e);
+  preload(k_chain<2>, e);
+  preload(k_chain<4>, e);
+  preload(k_chain<8>, e);
   preload(k_score, e);
   preload(k_rows, e);
   preload(k_update<1>, e);

@@ -5,11 +5,12 @@
 //
 //   k_tc_fwd : S_c = O_c X'_c^T (M = 128 rows of O, N = NT negatives, K = dp); fused epilogue straight from TMEM:
 //              f-, logistic-loss partial, dL/dS coefficient W (reading c.9).
-//   k_tc_bwd : z = 0: dO_c = W_c X'_c   (M = 128 positives, N = dp, K = k; A K-major, B MN-major)
-//              z = 1: dX'_c = W_c^T O_c (M = 128 negatives, N = dp, K = g; A and B MN-major)
-//              The L2 corrections rowsum(W) o and colsum(W) x' come out of the same MMAs: O carries a ones column at
-//              d and X' a ones column at d+1 (zero elsewhere in the padding), so TMEM column d+1 of dO is rowsum(W)
-//              and column d of dX' is colsum(W), while the forward product sees 1*0 + 0*1 there.
+//   k_tc_bwd : z = 0: dO_c = W_c X'_c   (M = 128 positives, N = a quarter of dp, K = k; A K-major, B MN-major)
+//              z = 1: dX'_c = W_c^T O_c (M = 128 negatives, N = a quarter of dp, K = g; A and B MN-major)
+//              TransE-L2 corrections dO = rowsum(W) o - W X', dX' = colsum(W) x' - W^T O take rowsum / colsum from
+//              deterministic partial sums the forward epilogue writes (fixed summation order).
+// Grids are sized for parallelism (64 CTAs each at the Freebase shape): every CTA of this latency-bound step streams
+// its operands at the per-SM TMA rate, so more, smaller tiles finish sooner.
 // Operand formats and descriptors: tc_ptx.cuh. MN-major tf32 needs the SWIZZLE_128B_BASE32B layout (TMA
 // CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B; 4-row K atoms, SBO = 512 B) -- verified by tools/tc_probe.cu.
 #include <cuda.h>
@@ -32,11 +33,11 @@ struct TcState {
   bool ok = false;
 };
 
-constexpr int kNT = 64;         // negatives per forward CTA
+constexpr int kNT = 32;         // negatives per forward CTA
 constexpr int kFwdStages = 4;
-constexpr int kBwdStages = 3;
-constexpr int kThreads = 256;  // 8 warps: warp 0 lane 0 = TMA, warp 1 lane 0 = MMA; all 8 run the epilogue
-// (warps w and w+4 read the same 32 TMEM lanes, different column halves)
+constexpr int kBwdStages = 4;
+constexpr int kNSplit = 4;      // column ranges of dp per backward tile
+constexpr int kThreads = 128;   // 4 warps: warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer; all 4 = epilogue
 
 struct TcArgs {
   Dims dm;
@@ -49,6 +50,9 @@ struct TcArgs {
   float* lneg;
   float* dO;
   float* Gocc;
+  float* rowsum_part;  // [B x nrp]   partial sums of W over the forward CTA's 32 negatives
+  float* colsum_part;  // [C*k x ncp] partial sums of W over the forward CTA's 128 positives
+  int32_t nrp, ncp;
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -75,7 +79,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t full[kFwdStages], empty[kFwdStages], done;
   __shared__ uint32_t tbase;
   __shared__ float s_xn[kNT];
-  __shared__ float s_red[8];
+  __shared__ float s_red[4];
+  __shared__ float s_col[4][kNT];
   const Dims& dm = a.dm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.z, i0 = blockIdx.y * 128, j0 = blockIdx.x * kNT;
@@ -90,10 +95,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&mO);
     tma_prefetch(&mX);
   }
-  if (warp == 0) tmem_alloc(&tbase, kNT);
-  for (int j = threadIdx.x; j < kNT; j += kThreads) {
-    const int jj = j0 + j;
-    s_xn[j] = jj < dm.k ? a.xnorm[(int64_t)c * dm.k + jj] : 0.f;
+  if (warp == 0) tmem_alloc(&tbase, 32);
+  if (threadIdx.x < kNT) {
+    const int jj = j0 + threadIdx.x;
+    s_xn[threadIdx.x] = jj < dm.k ? a.xnorm[(int64_t)c * dm.k + jj] : 0.f;
   }
   tc_fence_before();
   __syncthreads();
@@ -127,70 +132,82 @@ __global__ void __launch_bounds__(kThreads, 1)
   mbar_wait(&done, 0);
   tc_fence_after();
 
-  // epilogue: thread <-> row i (TMEM lane 32*(warp%4) + lane); warp/4 selects the column half
-  const int lg = warp & 3, half = warp >> 2;
-  const int i = i0 + lg * 32 + lane;
+  // epilogue: thread <-> row i (TMEM lane 32*warp + lane), its 32 negatives in registers
+  const int i = i0 + warp * 32 + lane;
   const bool iok = i < dm.g;
   const float on = iok && FAM == FAM_L2 ? a.onorm[(int64_t)c * dm.g + i] : 0.f;
   const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
-  float lsum = 0.f;
-  float* wrow = a.W + ((int64_t)c * dm.g + i) * a.kp;
-#pragma unroll 1
-  for (int q = half * (kNT / 2); q < (half + 1) * (kNT / 2); q += 32) {
-    float v[32];
-    tmem_ld32(tmem + ((uint32_t)(lg * 32) << 16) + q, v);
+  float v[32];
+  tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), v);
+  float lsum = 0.f, rsum = 0.f;
 #pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      const int j = j0 + q + jj;
-      float coef = 0.f;
-      if (iok && j < dm.k) {
-        float f, D = 1.f;
-        if (FAM == FAM_DOT) {
-          f = v[jj];
-        } else {  // TransE-L2 by expansion, clamped at 0 before the root (reading c.8)
-          D = sqrtf(fmaxf(on - 2.f * v[jj] + s_xn[q + jj], 0.f));
-          f = dm.gamma - D;
-        }
-        // one exp serves both: e = exp(-|f|); sigma(f) = f>=0 ? 1/(1+e) : e/(1+e); -log sigma(-f) = max(f,0)+log1p(e)
-        const float e = expf(-fabsf(f));
-        const float r1 = 1.f / (1.f + e);
-        const float sig = f >= 0.f ? r1 : e * r1;
-        lsum += fmaxf(f, 0.f) + log1pf(e);
-        const float dLdf = sig * inv_bk;
-        coef = FAM == FAM_DOT ? dLdf : -dLdf / fmaxf(D, 1e-12f);
+  for (int jj = 0; jj < 32; ++jj) {
+    const int j = j0 + jj;
+    float coef = 0.f;
+    if (iok && j < dm.k) {
+      float f, rD = 1.f;
+      if (FAM == FAM_DOT) {
+        f = v[jj];
+      } else {  // TransE-L2 by expansion, clamped at 0 before the root (reading c.8)
+        const float D2 = fmaxf(on - 2.f * v[jj] + s_xn[jj], 0.f);
+        rD = fminf(rsqrtf(D2), 1e12f);
+        f = dm.gamma - D2 * rD;
       }
-      v[jj] = coef;
+      // e = exp(-|f|): sigma(f) = f>=0 ? 1/(1+e) : e/(1+e);  -log sigma(-f) = max(f,0) + log1p(e)
+      const float e = __expf(-fabsf(f));
+      const float r1 = __fdividef(1.f, 1.f + e);
+      lsum += fmaxf(f, 0.f) + __logf(1.f + e);
+      const float dLdf = (f >= 0.f ? r1 : e * r1) * inv_bk;
+      coef = FAM == FAM_DOT ? dLdf : -dLdf * rD;
     }
-    if (iok) {
-      if (j0 + q + 32 <= dm.k && (a.kp & 3) == 0) {
-        float4* dst = reinterpret_cast<float4*>(wrow + j0 + q);
+    v[jj] = coef;
+    rsum += coef;
+  }
+  if (iok) {
+    float* wrow = a.W + ((int64_t)c * dm.g + i) * a.kp + j0;
+    if (j0 + 32 <= dm.k && (a.kp & 3) == 0) {
+      float4* dst = reinterpret_cast<float4*>(wrow);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-      } else {
-        for (int jj = 0; jj < 32 && j0 + q + jj < dm.k; ++jj) wrow[j0 + q + jj] = v[jj];
+      for (int u = 0; u < 8; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+    } else {
+      for (int jj = 0; jj < 32 && j0 + jj < dm.k; ++jj) wrow[jj] = v[jj];
+    }
+    if (FAM == FAM_L2) a.rowsum_part[((int64_t)c * dm.g + i) * a.nrp + blockIdx.x] = rsum;
+  }
+  if (FAM == FAM_L2) {
+    // column sums over this warp's 32 rows: transposing butterfly (fixed order); lane l ends with column l
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+      for (int q = 0; q < off; ++q) {
+        const bool upper = (lane & off) != 0;
+        const float send = upper ? v[q] : v[q + off];
+        const float keep = upper ? v[q + off] : v[q];
+        v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
       }
     }
+    s_col[warp][lane] = v[0];
   }
   lsum = warp_sum(lsum);
   if (lane == 0) s_red[warp] = lsum;
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < 8; ++w) t += s_red[w];
-    a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
-  }
-  if (warp == 0) tmem_dealloc(tmem, kNT);
+  if (FAM == FAM_L2 && threadIdx.x < kNT && j0 + (int)threadIdx.x < dm.k)
+    a.colsum_part[((int64_t)c * dm.k + j0 + threadIdx.x) * a.ncp + blockIdx.y] =
+        ((s_col[0][threadIdx.x] + s_col[1][threadIdx.x]) + s_col[2][threadIdx.x]) + s_col[3][threadIdx.x];
+  if (threadIdx.x == 0)
+    a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = ((s_red[0] + s_red[1]) + s_red[2]) + s_red[3];
+  if (warp == 0) tmem_dealloc(tmem, 32);
 }
 
 // ------------------------------------------------------------------------------------------------
-// backward: z = 0 -> dO tile (128 positives of chunk y), z = 1 -> dX' tile (128 negatives of chunk y)
+// backward: z = 0 -> dO tile (128 positives of chunk y), z = 1 -> dX' tile (128 negatives of chunk y);
+// blockIdx.x = (row tile, column part)
 // ------------------------------------------------------------------------------------------------
 template <int FAM>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_bwd(const __grid_constant__ CUtensorMap mW_K, const __grid_constant__ CUtensorMap mW_MN,
-             const __grid_constant__ CUtensorMap mX_MN, const __grid_constant__ CUtensorMap mO_MN, TcArgs a,
-             uint32_t tmem_cols) {
+             const __grid_constant__ CUtensorMap mX_MN, const __grid_constant__ CUtensorMap mO_MN, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   __shared__ uint64_t full[kBwdStages], empty[kBwdStages], done;
@@ -198,13 +215,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const Dims& dm = a.dm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool pass_x = blockIdx.z == 1;
-  const int c = blockIdx.y, r0 = blockIdx.x * 128;  // output rows: i (dO) or j (dX')
+  const int c = blockIdx.y, part = blockIdx.x % kNSplit, r0 = (blockIdx.x / kNSplit) * 128;
   const int nrows = pass_x ? dm.k : dm.g;
-  if (r0 >= nrows) return;  // uniform per CTA, before any barrier / TMEM use
+  const int nb_all = a.dp / 32;
+  const int b0 = part * nb_all / kNSplit, b1 = (part + 1) * nb_all / kNSplit;  // this CTA's column blocks
+  const int nb = b1 - b0;
+  if (r0 >= nrows || nb == 0 || b0 * 32 >= dm.d) return;  // uniform per CTA, before any barrier / TMEM use
   const int nk = pass_x ? dm.g : dm.k;  // contraction length
   const int nkb = (nk + 31) / 32;
-  const int nb = a.dp / 32;  // column blocks of the MN-major B operand
-  const uint32_t A_BYTES = 128 * 128, B_BYTES = (uint32_t)nb * 4096, STAGE = A_BYTES + B_BYTES;
+  const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)nb * 4096;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kBwdStages; ++s) {
       mbar_init(&full[s], 1);
@@ -213,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&done, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(&tbase, tmem_cols);
+  if (warp == 0) tmem_alloc(&tbase, 128);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -227,14 +246,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint8_t* sb = sa + A_BYTES;
       mbar_arrive_expect_tx(&full[s], STAGE);
       if (!pass_x) {
-        tma_load_3d(sa, &mW_K, &full[s], kb * 32, r0, c);                       // W[i0.., j-block]
-        for (int b = 0; b < nb; ++b) tma_load_3d(sb + b * 4096, &mX_MN, &full[s], b * 32, kb * 32, c);  // X'[j-blk, :]
+        tma_load_3d(sa, &mW_K, &full[s], kb * 32, r0, c);  // W[i0.., j-block]
+        for (int b = 0; b < nb; ++b) tma_load_3d(sb + b * 4096, &mX_MN, &full[s], (b0 + b) * 32, kb * 32, c);
       } else {
-        for (int b = 0; b < 4; ++b) tma_load_3d(sa + b * 4096, &mW_MN, &full[s], r0 + b * 32, kb * 32, c);  // W[i-blk, j0..]
-        for (int b = 0; b < nb; ++b) tma_load_3d(sb + b * 4096, &mO_MN, &full[s], b * 32, kb * 32, c);      // O[i-blk, :]
+        for (int b = 0; b < 4; ++b) tma_load_3d(sa + b * 4096, &mW_MN, &full[s], r0 + b * 32, kb * 32, c);
+        for (int b = 0; b < nb; ++b) tma_load_3d(sb + b * 4096, &mO_MN, &full[s], (b0 + b) * 32, kb * 32, c);
       }
     }
   } else if (warp == 1 && lane == 0) {  // MMA issuer
+    const uint32_t idesc = idesc_tf32(128, nb * 32, pass_x, true);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kBwdStages;
       mbar_wait(&full[s], (kb / kBwdStages) & 1);
@@ -243,11 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t ad = pass_x ? sdesc_mn(sa + kk * 1024, 4096) : sdesc(sa + kk * 32, 16, 1024);
-        for (int n0 = 0; n0 < a.dp; n0 += 256) {
-          const int nn = min(256, a.dp - n0);
-          const uint64_t bd = sdesc_mn(sb + (n0 / 32) * 4096 + kk * 1024, 4096);
-          mma_tf32(tmem + n0, ad, bd, idesc_tf32(128, nn, pass_x, true), (kb | kk) ? 1u : 0u);
-        }
+        mma_tf32(tmem, ad, sdesc_mn(sb + kk * 1024, 4096), idesc, (kb | kk) ? 1u : 0u);
       }
       mma_commit(&empty[s]);
     }
@@ -257,34 +273,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   mbar_wait(&done, 0);
   tc_fence_after();
 
-  // epilogue: thread <-> output row r (TMEM lane 32*(warp%4) + lane); warp/4 selects half of the column chunks
-  const int lg = warp & 3, half = warp >> 2;
-  const int r = r0 + lg * 32 + lane;
+  // epilogue: thread <-> output row r (TMEM lane 32*warp + lane)
+  const int r = r0 + warp * 32 + lane;
   const bool rok = r < nrows;
-  const uint32_t trow = tmem + ((uint32_t)(lg * 32) << 16);
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   const int d = dm.d;
-  float corr = 0.f;  // rowsum(W) (dO) or colsum(W) (dX'), read from the ones column
-  if (FAM == FAM_L2) {
-    const int cc = pass_x ? d : d + 1;
-    float v[32];
-    tmem_ld32(trow + (cc & ~31), v);
-    corr = v[cc & 31];
+  float corr = 0.f;  // rowsum(W) for dO, colsum(W) for dX' -- partials summed in a fixed order
+  if (FAM == FAM_L2 && rok) {
+    if (!pass_x) {
+      const float* rp = a.rowsum_part + ((int64_t)c * dm.g + r) * a.nrp;
+      for (int q = 0; q < a.nrp; ++q) corr += rp[q];
+    } else {
+      const float* cp = a.colsum_part + ((int64_t)c * dm.k + r) * a.ncp;
+      for (int q = 0; q < a.ncp; ++q) corr += cp[q];
+    }
   }
   const float* self = pass_x ? a.X + ((int64_t)c * dm.k + r) * a.dp : a.O + ((int64_t)c * dm.g + r) * a.dp;
   float* dst = pass_x ? a.Gocc + ((int64_t)2 * dm.B + (int64_t)c * dm.k + r) * d : a.dO + ((int64_t)c * dm.g + r) * d;
-  const int nch = (d + 31) / 32, ch0 = half ? (nch + 1) / 2 : 0, ch1 = half ? nch : (nch + 1) / 2;
 #pragma unroll 1
-  for (int ch = ch0; ch < ch1; ++ch) {
-    const int e0 = ch * 32;
+  for (int b = 0; b < nb; ++b) {
+    const int e0 = (b0 + b) * 32;
     float v[32];
-    tmem_ld32(trow + e0, v);
-    if (!rok) continue;
+    tmem_ld32(trow + b * 32, v);
+    if (!rok || e0 >= d) continue;
     const int ne = min(32, d - e0);
     if (FAM == FAM_L2) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D); self pitch dp
       const float4* s4 = reinterpret_cast<const float4*>(self + e0);
       float4 sv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) sv[u] = s4[u];  // dp >= d + 2 keeps this in bounds
+      for (int u = 0; u < 8; ++u) sv[u] = s4[u];  // within the dp-padded row
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         v[4 * u] = corr * sv[u].x - v[4 * u];
@@ -303,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, tmem_cols);
+  if (warp == 0) tmem_dealloc(tmem, 128);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -341,7 +358,10 @@ static bool make_map(CUtensorMap* m, const float* base, int cols, int rows, int 
 }
 
 static size_t fwd_smem() { return (size_t)kFwdStages * (128 * 128 + kNT * 128) + 1024; }
-static size_t bwd_smem(int dp) { return (size_t)kBwdStages * (128 * 128 + (size_t)(dp / 32) * 4096) + 1024; }
+static size_t bwd_smem(int dp) {
+  const int nb_max = (dp / 32 + kNSplit - 1) / kNSplit;
+  return (size_t)kBwdStages * (128 * 128 + (size_t)nb_max * 4096) + 1024;
+}
 
 bool tc_init(kge_handle* h) {
   const Dims& dm = h->dims;
@@ -397,12 +417,10 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
   const TcState* st = static_cast<const TcState*>(h->tc);
   TcArgs a{dm, h->dp, h->kp, h->buf.O, h->buf.X, h->buf.onorm, h->buf.xnorm, h->buf.W, h->buf.lneg, h->buf.dO,
-           h->buf.Gocc};
+           h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, (dm.k + kNT - 1) / kNT, (dm.g + 127) / 128};
   dim3 gf((dm.k + kNT - 1) / kNT, (dm.g + 127) / 128, dm.C);
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
-  dim3 gb(tiles, dm.C, 2);
-  uint32_t tcols = 32;
-  while ((int)tcols < h->dp) tcols <<= 1;
+  dim3 gb(tiles * kNSplit, dm.C, 2);
   launch_begin(h, KGE_K_NEG_FWD);
   if (dm.family == FAM_DOT)
     k_tc_fwd<FAM_DOT><<<gf, kThreads, fwd_smem(), h->stream>>>(st->mO_K, st->mX_K, a);
@@ -413,9 +431,9 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
   if (e != cudaSuccess) return e;
   launch_begin(h, KGE_K_NEG_BWD);
   if (dm.family == FAM_DOT)
-    k_tc_bwd<FAM_DOT><<<gb, kThreads, bwd_smem(h->dp), h->stream>>>(st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN, a, tcols);
+    k_tc_bwd<FAM_DOT><<<gb, kThreads, bwd_smem(h->dp), h->stream>>>(st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN, a);
   else
-    k_tc_bwd<FAM_L2><<<gb, kThreads, bwd_smem(h->dp), h->stream>>>(st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN, a, tcols);
+    k_tc_bwd<FAM_L2><<<gb, kThreads, bwd_smem(h->dp), h->stream>>>(st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN, a);
   launch_end(h, KGE_K_NEG_BWD);
   return cudaGetLastError();
 }
