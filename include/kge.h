@@ -172,6 +172,9 @@ enum { KGE_K_SAMPLE = 0, KGE_K_GATHER = 1, KGE_K_NEG_FWD = 2, KGE_K_NEG_BWD = 3,
 int kge_profile_begin(kge_handle* h);
 int kge_profile_end(kge_handle* h, int32_t n_kernels, double* avg_ms, int64_t* launches);
 int64_t kge_launch_count(const kge_handle* h);
+/* Diagnostics (handle created with KGE_TRACE=1 in the environment): per kernel id, per CTA (2048), 8 globaltimer stamps
+ * of the latest launch (slot 0 = CTA start, 7 = end, 1-2 = setup / main-loop done for the tensor-core kernels). */
+int kge_debug_trace(kge_handle* h, uint64_t* out, int64_t n);
 
 void kge_destroy(kge_handle* h);
 const char* kge_last_error(void);

@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "device_common.cuh"
 #include "kge_internal.h"
 
 namespace kge {
@@ -268,6 +269,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   dm.eps = h->cfg.adagrad_eps;
   dm.n_entities = cfg->n_entities;
   dm.n_relations = cfg->n_relations;
+  dm.trace = nullptr;
   h->k0 = (uint32_t)cfg->seed;
   h->k1 = (uint32_t)(cfg->seed >> 32);
   dm.dp = ((dm.d + 2 + 31) / 32) * 32;  // O / X' pitch: room for the ones columns at d, d+1 (tc.cu)
@@ -465,7 +467,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(std::max<int64_t>(h->n_neg_parts, tc_parts), dm.B) * 4);
-  b.rowsumW = (float*)dalloc(h, (size_t)dm.B * ((dm.k + 31) / 32) * 4);       // tc.cu partial row sums of W
+  b.rowsumW = (float*)dalloc(h, (size_t)dm.B * 2 * ((dm.k + 31) / 32) * 4);   // tc.cu partial row sums of W
   b.colsumW = (float*)dalloc(h, (size_t)nneg * ((dm.g + 127) / 128) * 4);     // tc.cu partial column sums of W
   b.dO = (float*)dalloc(h, (size_t)dm.B * dm.d * 4);
   b.Gocc = (float*)dalloc(h, (size_t)dm.n_occ * dm.d * 4);
@@ -493,6 +495,11 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h) + h->ring, &h->debug_slot, sizeof(Slot), cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "workspace init"));
+  if (getenv("KGE_TRACE")) {  // diagnostics: per-CTA stamps, read with kge_debug_trace
+    const size_t tb = (size_t)KGE_K_COUNT * kTraceCtas * kTraceSlots * 8;
+    dm.trace = (uint64_t*)dalloc(h, tb);
+    if (!dm.trace || cudaMemset(dm.trace, 0, tb) != cudaSuccess) return fail(KGE_ENOMEM);
+  }
   if (sample_init() != cudaSuccess || step_preload() != cudaSuccess || dist_preload() != cudaSuccess)
     return fail(cuda_fail(cudaGetLastError(), "kernel preload"));
   if (cfg->model == KGE_TRANSR) h->n_neg_parts = dm.B;  // one loss partial per (relation, chunk) group
@@ -777,6 +784,15 @@ int kge_profile_end(kge_handle* h, int32_t n_kernels, double* avg_ms, int64_t* l
 }
 
 int64_t kge_launch_count(const kge_handle* h) { return h ? h->launches : 0; }
+
+int kge_debug_trace(kge_handle* h, uint64_t* out, int64_t n) {
+  if (!h || !out) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (!h->dims.trace) { set_error("start with KGE_TRACE=1 in the environment"); return KGE_ESTATE; }
+  const int64_t total = (int64_t)KGE_K_COUNT * kTraceCtas * kTraceSlots;
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaMemcpy(out, h->dims.trace, (size_t)std::min(n, total) * 8, cudaMemcpyDeviceToHost));
+  return KGE_OK;
+}
 
 void kge_destroy(kge_handle* h) {
   if (!h) return;

@@ -81,6 +81,22 @@ __device__ __forceinline__ float init_value(uint32_t k0, uint32_t k1, uint32_t t
   return __fmul_rn(bound, __fmul_rn(f, 0x1p-31f));
 }
 
+// ---- diagnostics: per-CTA globaltimer stamps (slot 0 = CTA start, 1..6 = kernel-defined phases, 7 = end) ----
+constexpr int kTraceCtas = 2048, kTraceSlots = 8;
+__device__ __forceinline__ void trace_stamp(uint64_t* trace, int kid, int slot) {
+  if (trace == nullptr || threadIdx.x != 0) return;
+  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (cta >= kTraceCtas) return;
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  trace[((size_t)kid * kTraceCtas + cta) * kTraceSlots + slot] = t;
+}
+
+// ---- programmatic dependent launch: kernels of the step are launched with PDL so the next kernel's CTAs launch and
+// run their prologue while this one drains; every kernel waits for its predecessor before touching its outputs ----
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- small helpers ----
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

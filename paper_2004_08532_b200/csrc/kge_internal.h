@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/kge.h"
@@ -141,6 +142,7 @@ struct Dist {
 };
 
 struct Dims {
+  uint64_t* trace;  // diagnostics (KGE_TRACE=1 at init): per-kernel, per-CTA globaltimer stamps, else nullptr
   int32_t model, family, variant;
   int32_t d, drel, B, g, C, k, n_occ;
   int32_t dp, kp;  // padded row pitch of O / X' (d + 2 rounded up to 32) and of W (k rounded up to 4)
@@ -205,6 +207,23 @@ struct kge_handle {
 };
 
 namespace kge {
+
+// Launch with programmatic stream serialization (PDL); see pdl_wait / pdl_trigger in device_common.cuh.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 void set_error(const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);

@@ -54,6 +54,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
   extern __shared__ unsigned long long keys[];
   __shared__ int warp_tot[32];
   __shared__ int total;
+  pdl_wait();  // the ring slots it overwrites may still be read by the previous step's kernels
+  pdl_trigger();
   const SampleParams& p = a.p;
   const int64_t s = a.step0 + blockIdx.x;
   const Slot slot = a.slots[s % a.ring];

@@ -296,6 +296,9 @@ __device__ __forceinline__ void combine_stage(int model, int mode, const float* 
 template <int V>
 __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
   const Dims& dm = a.dm;
+  trace_stamp(dm.trace, KGE_K_GATHER, 0);
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int row = a.first_row + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int n_neg = dm.C * dm.k;
@@ -335,6 +338,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     acc = warp_sum(acc);
     if (lane == 0) a.b.xnorm[q] = acc;
   }
+  trace_stamp(dm.trace, KGE_K_GATHER, 7);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -378,6 +382,8 @@ template <int FAM>
 __global__ void __launch_bounds__(256) k_neg_fwd(NegArgs a) {
   constexpr bool CPLX = FAM == FAM_CMOD;
   const Dims& dm = a.dm;
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(16) float As[TK][TM + TPAD];
   __shared__ __align__(16) float Bs[TK][TN + TPAD];
   __shared__ float red[8];
@@ -482,6 +488,8 @@ template <int FAM>
 __global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
   constexpr bool CPLX = FAM == FAM_CMOD;
   const Dims& dm = a.dm;
+  pdl_wait();
+  pdl_trigger();
   __shared__ __align__(16) float Ws[TK][TM + TPAD];  // [K index][row index of the output]
   __shared__ __align__(16) float Vs[TK][TN + TPAD];  // [K index][column]  (CPLX: re cols 0..31, im cols 32..63)
   const bool pass_x = blockIdx.z >= (unsigned)dm.C;
@@ -639,6 +647,9 @@ __device__ __forceinline__ void dpair(int fam, float o, float x, float scale, fl
 template <int V>
 __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
   const Dims& dm = a.dm;
+  trace_stamp(dm.trace, KGE_K_CHAIN, 0);
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == gridDim.x - 1) {
     // deterministic loss: fixed lane assignment, fixed warp order (reading c.9 normalisation)
@@ -897,6 +908,9 @@ __device__ __forceinline__ void prefetch_row(const float* __restrict__ row, floa
 template <int V>
 __global__ void __launch_bounds__(256) k_update(UpdateArgs a, int n_ent_blocks) {
   const Dims& dm = a.dm;
+  trace_stamp(dm.trace, KGE_K_UPDATE, 0);
+  pdl_wait();
+  pdl_trigger();
   if (a.b.flags[1]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if ((int)blockIdx.x < n_ent_blocks) {
@@ -963,13 +977,13 @@ static void launch_neg(kge_handle* h, const NegArgs& na) {
   const Dims& dm = h->dims;
   dim3 gf((dm.k + TN - 1) / TN, (dm.g + TM - 1) / TM, dm.C);
   launch_begin(h, KGE_K_NEG_FWD);
-  k_neg_fwd<FAM><<<gf, 256, 0, h->stream>>>(na);
+  launch_pdl(k_neg_fwd<FAM>, gf, 256, 0, h->stream, na);
   launch_end(h, KGE_K_NEG_FWD);
   const int cols_per_tile = FAM == FAM_CMOD ? TN / 2 : TN;
   const int ncols = FAM == FAM_CMOD ? dm.d / 2 : dm.d;
   dim3 gb((ncols + cols_per_tile - 1) / cols_per_tile, (std::max(dm.g, dm.k) + TM - 1) / TM, 2 * dm.C);
   launch_begin(h, KGE_K_NEG_BWD);
-  k_neg_bwd<FAM><<<gb, 256, 0, h->stream>>>(na);
+  launch_pdl(k_neg_bwd<FAM>, gb, 256, 0, h->stream, na);
   launch_end(h, KGE_K_NEG_BWD);
 }
 
@@ -982,10 +996,10 @@ static int row_v(int d) {  // float4 per lane for a d-float row
 static void launch_gather_v(kge_handle* h, const GatherArgs& ga, int rows) {
   const unsigned grid = (rows + 7) / 8;
   switch (row_v(h->dims.d)) {
-    case 1: k_gather<1><<<grid, 256, 0, h->stream>>>(ga); break;
-    case 2: k_gather<2><<<grid, 256, 0, h->stream>>>(ga); break;
-    case 4: k_gather<4><<<grid, 256, 0, h->stream>>>(ga); break;
-    default: k_gather<8><<<grid, 256, 0, h->stream>>>(ga); break;
+    case 1: launch_pdl(k_gather<1>, grid, 256, 0, h->stream, ga); break;
+    case 2: launch_pdl(k_gather<2>, grid, 256, 0, h->stream, ga); break;
+    case 4: launch_pdl(k_gather<4>, grid, 256, 0, h->stream, ga); break;
+    default: launch_pdl(k_gather<8>, grid, 256, 0, h->stream, ga); break;
   }
 }
 
@@ -1006,13 +1020,13 @@ cudaError_t launch_update(kge_handle* h, const Slot& s) {
   const int w4 = dm.d / 4;
   launch_begin(h, KGE_K_UPDATE);
   if (w4 <= 32)
-    k_update<1><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+    launch_pdl(k_update<1>, grid, 256, 0, h->stream, ua, n_ent_blocks);
   else if (w4 <= 64)
-    k_update<2><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+    launch_pdl(k_update<2>, grid, 256, 0, h->stream, ua, n_ent_blocks);
   else if (w4 <= 128)
-    k_update<4><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+    launch_pdl(k_update<4>, grid, 256, 0, h->stream, ua, n_ent_blocks);
   else
-    k_update<8><<<grid, 256, 0, h->stream>>>(ua, n_ent_blocks);
+    launch_pdl(k_update<8>, grid, 256, 0, h->stream, ua, n_ent_blocks);
   launch_end(h, KGE_K_UPDATE);
   return cudaGetLastError();
 }
@@ -1043,10 +1057,10 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   launch_begin(h, KGE_K_CHAIN);
   const unsigned cgrid = (dm.B + 7) / 8 + 1;
   switch (row_v(dm.d)) {
-    case 1: k_chain<1><<<cgrid, 256, 0, h->stream>>>(ca); break;
-    case 2: k_chain<2><<<cgrid, 256, 0, h->stream>>>(ca); break;
-    case 4: k_chain<4><<<cgrid, 256, 0, h->stream>>>(ca); break;
-    default: k_chain<8><<<cgrid, 256, 0, h->stream>>>(ca); break;
+    case 1: launch_pdl(k_chain<1>, cgrid, 256, 0, h->stream, ca); break;
+    case 2: launch_pdl(k_chain<2>, cgrid, 256, 0, h->stream, ca); break;
+    case 4: launch_pdl(k_chain<4>, cgrid, 256, 0, h->stream, ca); break;
+    default: launch_pdl(k_chain<8>, cgrid, 256, 0, h->stream, ca); break;
   }
   launch_end(h, KGE_K_CHAIN);
 

@@ -30,6 +30,7 @@ struct TcState {
   CUtensorMap mW_K;          // dO operand A (K-major), box {32, 128}
   CUtensorMap mX_MN, mO_MN;  // B operands of dO / dX' (MN-major, 128B_ATOM_32B), box {32, 32}
   CUtensorMap mW_MN;         // A operand of dX' (MN-major), box {32, 32}
+  CUtensorMap mX_E;          // dX' epilogue operand (X' rows, K-major SW128), box {32, 128}
   bool ok = false;
 };
 
@@ -38,6 +39,8 @@ constexpr int kFwdStages = 4;
 constexpr int kBwdStages = 4;
 constexpr int kNSplit = 4;      // column ranges of dp per backward tile
 constexpr int kThreads = 128;   // 4 warps: warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer; all 4 = epilogue
+constexpr int kFwdThreads = 256;  // forward: 8 epilogue warps (two per TMEM lane quarter, 16 negatives each) so the
+                                  // transcendental chains of the loss epilogue have latency hiding
 
 struct TcArgs {
   Dims dm;
@@ -71,7 +74,7 @@ __device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo) {
 // forward
 // ------------------------------------------------------------------------------------------------
 template <int FAM>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     k_tc_fwd(const __grid_constant__ CUtensorMap mO, const __grid_constant__ CUtensorMap mX, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -79,9 +82,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t full[kFwdStages], empty[kFwdStages], done;
   __shared__ uint32_t tbase;
   __shared__ float s_xn[kNT];
-  __shared__ float s_red[4];
+  __shared__ float s_red[8];
   __shared__ float s_col[4][kNT];
   const Dims& dm = a.dm;
+  trace_stamp(dm.trace, KGE_K_NEG_FWD, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.z, i0 = blockIdx.y * 128, j0 = blockIdx.x * kNT;
   const int nkb = a.dp / 32;
@@ -96,6 +100,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&mX);
   }
   if (warp == 0) tmem_alloc(&tbase, 32);
+  pdl_wait();  // predecessor (gather) complete: O, X', norms are final
+  pdl_trigger();
   if (threadIdx.x < kNT) {
     const int jj = j0 + threadIdx.x;
     s_xn[threadIdx.x] = jj < dm.k ? a.xnorm[(int64_t)c * dm.k + jj] : 0.f;
@@ -104,6 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tbase;
+  trace_stamp(dm.trace, KGE_K_NEG_FWD, 1);
 
   if (warp == 0 && lane == 0) {  // TMA producer
     for (int kb = 0; kb < nkb; ++kb) {
@@ -129,27 +136,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     mma_commit(&done);
   }
   __syncwarp();
+  // epilogue: thread <-> row i (TMEM lane 32*(warp%4) + lane); warp/4 picks 16 of the CTA's 32 negatives
+  const int lg = warp & 3, hf = warp >> 2;
+  const int i = i0 + lg * 32 + lane;
+  const bool iok = i < dm.g;
+  const float on = iok && FAM == FAM_L2 ? a.onorm[(int64_t)c * dm.g + i] : 0.f;  // loaded while the MMAs run
   mbar_wait(&done, 0);
   tc_fence_after();
-
-  // epilogue: thread <-> row i (TMEM lane 32*warp + lane), its 32 negatives in registers
-  const int i = i0 + warp * 32 + lane;
-  const bool iok = i < dm.g;
-  const float on = iok && FAM == FAM_L2 ? a.onorm[(int64_t)c * dm.g + i] : 0.f;
+  trace_stamp(dm.trace, KGE_K_NEG_FWD, 2);
   const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
-  float v[32];
-  tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16), v);
+  float v[16];
+  tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + hf * 16, v);
+  trace_stamp(dm.trace, KGE_K_NEG_FWD, 3);
   float lsum = 0.f, rsum = 0.f;
 #pragma unroll
-  for (int jj = 0; jj < 32; ++jj) {
-    const int j = j0 + jj;
+  for (int jj = 0; jj < 16; ++jj) {
+    const int j = j0 + hf * 16 + jj;
     float coef = 0.f;
     if (iok && j < dm.k) {
       float f, rD = 1.f;
       if (FAM == FAM_DOT) {
         f = v[jj];
       } else {  // TransE-L2 by expansion, clamped at 0 before the root (reading c.8)
-        const float D2 = fmaxf(on - 2.f * v[jj] + s_xn[jj], 0.f);
+        const float D2 = fmaxf(on - 2.f * v[jj] + s_xn[hf * 16 + jj], 0.f);
         rD = fminf(rsqrtf(D2), 1e12f);
         f = dm.gamma - D2 * rD;
       }
@@ -163,21 +172,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     v[jj] = coef;
     rsum += coef;
   }
+  trace_stamp(dm.trace, KGE_K_NEG_FWD, 4);
   if (iok) {
-    float* wrow = a.W + ((int64_t)c * dm.g + i) * a.kp + j0;
-    if (j0 + 32 <= dm.k && (a.kp & 3) == 0) {
+    float* wrow = a.W + ((int64_t)c * dm.g + i) * a.kp + j0 + hf * 16;
+    if (j0 + hf * 16 + 16 <= dm.k && (a.kp & 3) == 0) {
       float4* dst = reinterpret_cast<float4*>(wrow);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+      for (int u = 0; u < 4; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
     } else {
-      for (int jj = 0; jj < 32 && j0 + jj < dm.k; ++jj) wrow[jj] = v[jj];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj)  // static indices keep v[] in registers
+        if (j0 + hf * 16 + jj < dm.k) wrow[jj] = v[jj];
     }
-    if (FAM == FAM_L2) a.rowsum_part[((int64_t)c * dm.g + i) * a.nrp + blockIdx.x] = rsum;
+    if (FAM == FAM_L2) a.rowsum_part[((int64_t)c * dm.g + i) * a.nrp + 2 * blockIdx.x + hf] = rsum;
   }
   if (FAM == FAM_L2) {
-    // column sums over this warp's 32 rows: transposing butterfly (fixed order); lane l ends with column l
+    // column sums over this warp's 32 rows for its 16 columns: transposing butterfly (fixed order) over the low 4
+    // lane bits, then the two 16-lane halves are added; lane l (< 16) ends with column l
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
+    for (int off = 8; off >= 1; off >>= 1) {
 #pragma unroll
       for (int q = 0; q < off; ++q) {
         const bool upper = (lane & off) != 0;
@@ -186,8 +199,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
       }
     }
-    s_col[warp][lane] = v[0];
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
+    if (lane < 16) s_col[lg][hf * 16 + lane] = v[0];
   }
+  trace_stamp(dm.trace, KGE_K_NEG_FWD, 5);
   lsum = warp_sum(lsum);
   if (lane == 0) s_red[warp] = lsum;
   tc_fence_before();
@@ -195,9 +210,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (FAM == FAM_L2 && threadIdx.x < kNT && j0 + (int)threadIdx.x < dm.k)
     a.colsum_part[((int64_t)c * dm.k + j0 + threadIdx.x) * a.ncp + blockIdx.y] =
         ((s_col[0][threadIdx.x] + s_col[1][threadIdx.x]) + s_col[2][threadIdx.x]) + s_col[3][threadIdx.x];
-  if (threadIdx.x == 0)
-    a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = ((s_red[0] + s_red[1]) + s_red[2]) + s_red[3];
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += s_red[w];
+    a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+  }
+  trace_stamp(dm.trace, KGE_K_NEG_FWD, 6);
   if (warp == 0) tmem_dealloc(tmem, 32);
+  trace_stamp(dm.trace, KGE_K_NEG_FWD, 7);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -207,12 +227,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int FAM>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_bwd(const __grid_constant__ CUtensorMap mW_K, const __grid_constant__ CUtensorMap mW_MN,
-             const __grid_constant__ CUtensorMap mX_MN, const __grid_constant__ CUtensorMap mO_MN, TcArgs a) {
+             const __grid_constant__ CUtensorMap mX_MN, const __grid_constant__ CUtensorMap mO_MN,
+             const __grid_constant__ CUtensorMap mO_E, const __grid_constant__ CUtensorMap mX_E, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  __shared__ uint64_t full[kBwdStages], empty[kBwdStages], done;
+  __shared__ uint64_t full[kBwdStages], empty[kBwdStages], done, selfbar;
   __shared__ uint32_t tbase;
   const Dims& dm = a.dm;
+  trace_stamp(dm.trace, KGE_K_NEG_BWD, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool pass_x = blockIdx.z == 1;
   const int c = blockIdx.y, part = blockIdx.x % kNSplit, r0 = (blockIdx.x / kNSplit) * 128;
@@ -220,25 +242,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nb_all = a.dp / 32;
   const int b0 = part * nb_all / kNSplit, b1 = (part + 1) * nb_all / kNSplit;  // this CTA's column blocks
   const int nb = b1 - b0;
-  if (r0 >= nrows || nb == 0 || b0 * 32 >= dm.d) return;  // uniform per CTA, before any barrier / TMEM use
+  if (r0 >= nrows || nb == 0 || b0 * 32 >= dm.d) {  // uniform per CTA, before any barrier / TMEM use
+    pdl_trigger();
+    return;
+  }
   const int nk = pass_x ? dm.g : dm.k;  // contraction length
   const int nkb = (nk + 31) / 32;
   const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)nb * 4096;
+  // epilogue operand (L2): this CTA's rows x column blocks of O (dO) or X' (dX'), TMA'd at the start so the load
+  // overlaps the main loop; block b at self_smem + b * 16 KB, 128-byte rows, 16-byte chunks swizzled by (row % 8)
+  uint8_t* self_smem = smem + kBwdStages * STAGE;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kBwdStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(&done, 1);
+    mbar_init(&selfbar, 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(&tbase, 128);
+  pdl_wait();  // predecessor (forward) complete: W and the row / column partial sums are final
+  pdl_trigger();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tbase;
+  trace_stamp(dm.trace, KGE_K_NEG_BWD, 1);
 
   if (warp == 0 && lane == 0) {  // TMA producer
+    if (FAM == FAM_L2) {
+      mbar_arrive_expect_tx(&selfbar, (uint32_t)nb * 16384);
+      for (int b = 0; b < nb; ++b)
+        tma_load_3d(self_smem + b * 16384, pass_x ? &mX_E : &mO_E, &selfbar, (b0 + b) * 32, r0, c);
+    }
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kBwdStages;
       if (kb >= kBwdStages) mbar_wait(&empty[s], ((kb / kBwdStages) - 1) & 1);
@@ -270,15 +307,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     mma_commit(&done);
   }
   __syncwarp();
-  mbar_wait(&done, 0);
-  tc_fence_after();
-
-  // epilogue: thread <-> output row r (TMEM lane 32*warp + lane)
+  // epilogue prologue while the MMAs run: row r (TMEM lane 32*warp + lane) and its correction factor,
+  // rowsum(W) for dO, colsum(W) for dX' -- partials summed in a fixed order
   const int r = r0 + warp * 32 + lane;
   const bool rok = r < nrows;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   const int d = dm.d;
-  float corr = 0.f;  // rowsum(W) for dO, colsum(W) for dX' -- partials summed in a fixed order
+  float corr = 0.f;
   if (FAM == FAM_L2 && rok) {
     if (!pass_x) {
       const float* rp = a.rowsum_part + ((int64_t)c * dm.g + r) * a.nrp;
@@ -288,8 +322,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int q = 0; q < a.ncp; ++q) corr += cp[q];
     }
   }
-  const float* self = pass_x ? a.X + ((int64_t)c * dm.k + r) * a.dp : a.O + ((int64_t)c * dm.g + r) * a.dp;
+  mbar_wait(&done, 0);
+  tc_fence_after();
+  trace_stamp(dm.trace, KGE_K_NEG_BWD, 2);
+  if (FAM == FAM_L2) mbar_wait(&selfbar, 0);
+  trace_stamp(dm.trace, KGE_K_NEG_BWD, 3);
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   float* dst = pass_x ? a.Gocc + ((int64_t)2 * dm.B + (int64_t)c * dm.k + r) * d : a.dO + ((int64_t)c * dm.g + r) * d;
+  const int rl = warp * 32 + lane;  // row within the tile
 #pragma unroll 1
   for (int b = 0; b < nb; ++b) {
     const int e0 = (b0 + b) * 32;
@@ -297,17 +337,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_ld32(trow + b * 32, v);
     if (!rok || e0 >= d) continue;
     const int ne = min(32, d - e0);
-    if (FAM == FAM_L2) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D); self pitch dp
-      const float4* s4 = reinterpret_cast<const float4*>(self + e0);
-      float4 sv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) sv[u] = s4[u];  // within the dp-padded row
+    if (FAM == FAM_L2) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D)
+      const uint8_t* rowp = self_smem + b * 16384 + rl * 128;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        v[4 * u] = corr * sv[u].x - v[4 * u];
-        v[4 * u + 1] = corr * sv[u].y - v[4 * u + 1];
-        v[4 * u + 2] = corr * sv[u].z - v[4 * u + 2];
-        v[4 * u + 3] = corr * sv[u].w - v[4 * u + 3];
+        const float4 sv = *reinterpret_cast<const float4*>(rowp + ((u ^ (rl & 7)) << 4));
+        v[4 * u] = corr * sv.x - v[4 * u];
+        v[4 * u + 1] = corr * sv.y - v[4 * u + 1];
+        v[4 * u + 2] = corr * sv.z - v[4 * u + 2];
+        v[4 * u + 3] = corr * sv.w - v[4 * u + 3];
       }
     }
     if (ne == 32) {
@@ -315,12 +353,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int u = 0; u < 8; ++u) o4[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
     } else {
-      for (int u = 0; u < ne; ++u) dst[e0 + u] = v[u];
+#pragma unroll
+      for (int u = 0; u < 32; ++u)  // static indices keep v[] in registers
+        if (u < ne) dst[e0 + u] = v[u];
     }
+    if (b == 0) trace_stamp(dm.trace, KGE_K_NEG_BWD, 4);
   }
+  trace_stamp(dm.trace, KGE_K_NEG_BWD, 5);
   tc_fence_before();
   __syncthreads();
+  trace_stamp(dm.trace, KGE_K_NEG_BWD, 6);
   if (warp == 0) tmem_dealloc(tmem, 128);
+  trace_stamp(dm.trace, KGE_K_NEG_BWD, 7);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -360,7 +404,7 @@ static bool make_map(CUtensorMap* m, const float* base, int cols, int rows, int 
 static size_t fwd_smem() { return (size_t)kFwdStages * (128 * 128 + kNT * 128) + 1024; }
 static size_t bwd_smem(int dp) {
   const int nb_max = (dp / 32 + kNSplit - 1) / kNSplit;
-  return (size_t)kBwdStages * (128 * 128 + (size_t)nb_max * 4096) + 1024;
+  return (size_t)kBwdStages * (128 * 128 + (size_t)nb_max * 4096) + (size_t)nb_max * 16384 + 1024;
 }
 
 bool tc_init(kge_handle* h) {
@@ -376,6 +420,7 @@ bool tc_init(kge_handle* h) {
   ok &= make_map(&st->mX_MN, b.X, h->dp, dm.k, dm.C, h->dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   ok &= make_map(&st->mO_MN, b.O, h->dp, dm.g, dm.C, h->dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   ok &= make_map(&st->mW_MN, b.W, dm.k, dm.g, dm.C, h->kp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  ok &= make_map(&st->mX_E, b.X, h->dp, dm.k, dm.C, h->dp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!ok) {
     delete st;
     return false;
@@ -417,23 +462,25 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
   const TcState* st = static_cast<const TcState*>(h->tc);
   TcArgs a{dm, h->dp, h->kp, h->buf.O, h->buf.X, h->buf.onorm, h->buf.xnorm, h->buf.W, h->buf.lneg, h->buf.dO,
-           h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, (dm.k + kNT - 1) / kNT, (dm.g + 127) / 128};
+           h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128};
   dim3 gf((dm.k + kNT - 1) / kNT, (dm.g + 127) / 128, dm.C);
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(tiles * kNSplit, dm.C, 2);
   launch_begin(h, KGE_K_NEG_FWD);
   if (dm.family == FAM_DOT)
-    k_tc_fwd<FAM_DOT><<<gf, kThreads, fwd_smem(), h->stream>>>(st->mO_K, st->mX_K, a);
+    launch_pdl(k_tc_fwd<FAM_DOT>, gf, kFwdThreads, fwd_smem(), h->stream, st->mO_K, st->mX_K, a);
   else
-    k_tc_fwd<FAM_L2><<<gf, kThreads, fwd_smem(), h->stream>>>(st->mO_K, st->mX_K, a);
+    launch_pdl(k_tc_fwd<FAM_L2>, gf, kFwdThreads, fwd_smem(), h->stream, st->mO_K, st->mX_K, a);
   launch_end(h, KGE_K_NEG_FWD);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   launch_begin(h, KGE_K_NEG_BWD);
   if (dm.family == FAM_DOT)
-    k_tc_bwd<FAM_DOT><<<gb, kThreads, bwd_smem(h->dp), h->stream>>>(st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN, a);
+    launch_pdl(k_tc_bwd<FAM_DOT>, gb, kThreads, bwd_smem(h->dp), h->stream, st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN,
+               st->mO_K, st->mX_E, a);
   else
-    k_tc_bwd<FAM_L2><<<gb, kThreads, bwd_smem(h->dp), h->stream>>>(st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN, a);
+    launch_pdl(k_tc_bwd<FAM_L2>, gb, kThreads, bwd_smem(h->dp), h->stream, st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN,
+               st->mO_K, st->mX_E, a);
   launch_end(h, KGE_K_NEG_BWD);
   return cudaGetLastError();
 }

@@ -1,0 +1,47 @@
+"""Per-CTA timeline of one training step (KGE_TRACE=1): kernel spans, CTA start spread, TC phases."""
+import ctypes, os, sys
+os.environ["KGE_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import synth
+from paper_2004_08532_b200 import kge
+wl = sys.argv[1] if len(sys.argv) > 1 else "freebase"
+gr = synth.graph(wl)
+trip = gr.triples()
+cfg = kge.Config(model="transe_l2", n_entities=gr.n_entities, n_relations=gr.n_relations, dim=400, batch_size=1024,
+                 chunk_size=256, neg_k=256, neg_precision="tf32")
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    h = kge.init(cfg, *trip, stream=s)
+h.train_step(70, return_loss=False)
+h.sync()
+h.train_step(1, return_loss=False)
+h.sync()
+L = kge.lib()
+L.kge_debug_trace.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]
+n = 6 * 2048 * 8
+buf = np.zeros(n, np.uint64)
+L.kge_debug_trace(h._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n)
+T = buf.reshape(6, 2048, 8).astype(np.int64)
+names = kge.KERNELS
+t0 = min(T[k][:, 0][T[k][:, 0] > 0].min() for k in range(1, 6) if (T[k][:, 0] > 0).any())
+for k in range(1, 6):
+    st = T[k][:, 0]
+    m = st > 0
+    if not m.any():
+        continue
+    st = st[m] - t0
+    en = T[k][:, 7][m]
+    en = en[en > 0] - t0 if (en > 0).any() else np.array([0])
+    line = f"{names[k]:10s} ctas={m.sum():5d} start[min/med/max]={st.min()/1e3:6.2f}/{np.median(st)/1e3:6.2f}/{st.max()/1e3:6.2f} us  end max={en.max()/1e3:6.2f} us"
+    if k in (2, 3):
+        s1 = T[k][:, 1][m] - t0
+        s2 = T[k][:, 2][m] - t0
+        s2 = s2[T[k][:, 2][m] > 0]
+        line += f" | setup done med {np.median(s1)/1e3:6.2f}, mainloop done med/max {np.median(s2)/1e3:6.2f}/{s2.max()/1e3:6.2f}"
+        for sl in (3, 4, 5, 6):
+            x = T[k][:, sl][m]
+            x = x[x > 0] - t0
+            if len(x):
+                line += f" | s{sl} med {np.median(x)/1e3:6.2f}"
+    print(line)
