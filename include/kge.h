@@ -125,6 +125,13 @@ int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out);
  * is not NULL) reads the loss back. This is the end-to-end entry for a host-side sampler. */
 int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails, float* loss_out);
 
+/* Asynchronous kge_train_batch for a pipelined host loop: the batch is range-checked and staged synchronously (the
+ * caller's arrays may be reused on return), the H2D copy, the step and -- if loss_host is not NULL -- the D2H copy of
+ * the step's loss into loss_host are enqueued and the call returns. loss_host should be pinned (cudaMallocHost /
+ * torch pin_memory) and is valid after the next kge_sync; KGE_ENONFINITE is reported by that kge_sync. */
+int kge_train_batch_async(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails,
+                          float* loss_host);
+
 /* Scores f(h, r, t) of n triples with the current tables (Table 1 with the margin of reading Q7). out: host
  * float[n]. Synchronous. KGE_ERANGE on an out-of-range id. */
 int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, float* out);

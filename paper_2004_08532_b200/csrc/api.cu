@@ -276,7 +276,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   dm.kp = ((dm.k + 3) / 4) * 4;        // W pitch (16-byte rows for TMA)
   h->dp = dm.dp;
   h->kp = dm.kp;
-  h->n_pad = 1;
+  h->n_pad = 64;  // the sampler's warp-level sort stages work on 64-key blocks
   while (h->n_pad < dm.n_occ) h->n_pad <<= 1;
   h->ring = 64;
   h->n_triples = n_triples;
@@ -447,7 +447,12 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   for (int i = 0; i < h->ring; ++i) carve_slot(h, ring_base + sl * i, h->slots[i]);
   carve_slot(h, ring_base + sl * h->ring, h->debug_slot);
   h->given = (int32_t*)dalloc(h, (size_t)3 * dm.B * 4);
-  if (cudaMallocHost(&h->pinned_given, (size_t)3 * dm.B * 8) != cudaSuccess ||
+  for (int i = 0; i < kge_handle::kStage; ++i)
+    if (cudaEventCreateWithFlags(&h->stage_ev[i], cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(KGE_ECUDA);
+    }
+  if (cudaMallocHost(&h->pinned_given, (size_t)kge_handle::kStage * 3 * dm.B * 4) != cudaSuccess ||
       cudaMallocHost(&h->pinned_loss, (size_t)h->ring * 4) != cudaSuccess) {
     cudaGetLastError();
     return fail(KGE_ENOMEM);
@@ -473,8 +478,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.Gocc = (float*)dalloc(h, (size_t)dm.n_occ * dm.d * 4);
   b.Grel = (float*)dalloc(h, (size_t)dm.B * dm.drel * 4);
   b.loss = (float*)dalloc(h, (size_t)h->ring * 4);
+  h->seg_cnt = (int32_t*)dalloc(h, (size_t)(dm.B + dm.n_occ) * 4);
   if (!b.O || !b.onorm || !b.X || !b.xnorm || !b.W || !b.wpos || !b.lpos || !b.pstat || !b.lneg || !b.rowsumW || !b.colsumW ||
-      !b.dO || !b.Gocc || !b.Grel || !b.loss || !b.flags) {
+      !b.dO || !b.Gocc || !b.Grel || !b.loss || !b.flags || !h->seg_cnt) {
     set_error("out of device memory (workspace)");
     return fail(KGE_ENOMEM);
   }
@@ -491,6 +497,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   }
   if (e == cudaSuccess) e = cudaMemsetAsync(b.Gocc, 0, (size_t)dm.n_occ * dm.d * 4, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->seg_cnt, 0, (size_t)(dm.B + dm.n_occ) * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h), h->slots.data(), sizeof(Slot) * h->ring, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h) + h->ring, &h->debug_slot, sizeof(Slot), cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
@@ -566,15 +573,19 @@ int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
   return KGE_OK;
 }
 
-int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails, float* loss_out) {
+// Enqueue one step on a caller-supplied batch; loss_dev_to: host destination of an async loss copy (or NULL).
+static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails,
+                               float* loss_host) {
   if (!h || !heads || !rels || !tails) { set_error("NULL argument"); return KGE_EINVAL; }
   if (h->P > 1 && !h->dist.connected) { set_error("world_size > 1: call kge_connect first"); return KGE_ESTATE; }
   const int B = h->dims.B;
   const int64_t s = h->step;
-  // host-side range check + int32 narrowing into pinned staging, then one H2D copy
-  int32_t* st = h->pinned_given;
-  cudaError_t e = cudaStreamSynchronize(h->stream);  // staging reuse
-  if (e != cudaSuccess) return cuda_fail(e, "sync");
+  // host-side range check + int32 narrowing into a pinned staging buffer (ring of kStage; a buffer is reused only
+  // after its previous H2D copy completed), then one H2D copy
+  const int si = h->stage_i;
+  int32_t* st = h->pinned_given + (size_t)si * 3 * B;
+  cudaError_t e = cudaEventSynchronize(h->stage_ev[si]);
+  if (e != cudaSuccess) return cuda_fail(e, "staging reuse");
   for (int i = 0; i < B; ++i) {
     if (heads[i] < 0 || heads[i] >= h->dims.n_entities || tails[i] < 0 || tails[i] >= h->dims.n_entities ||
         rels[i] < 0 || rels[i] >= h->dims.n_relations) {
@@ -592,7 +603,9 @@ int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, co
     if (e != cudaSuccess) return cuda_fail(e, "barrier");
   }
   e = cudaMemcpyAsync(h->given, st, (size_t)3 * B * 4, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaEventRecord(h->stage_ev[si], h->stream);
   if (e != cudaSuccess) return cuda_fail(e, "batch upload");
+  h->stage_i = (si + 1) % kge_handle::kStage;
   // sample negatives + dedup for this step into the debug slot, from the given positives
   SampleParams p = sample_params(h, true);
   e = launch_sample(h, p, d_slots(h) + h->ring, 1, s, 1);
@@ -602,14 +615,25 @@ int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, co
   if (e != cudaSuccess) return cuda_fail(e, "step");
   h->step = s + 1;
   if (h->ring_first >= 0 && s >= h->ring_first && s < h->ring_first + h->ring) h->ring_first = -1;
-  if (loss_out) {
-    e = cudaMemcpyAsync(h->pinned_loss, h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost, h->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (loss_host) {
+    e = cudaMemcpyAsync(loss_host, h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "loss readback");
-    *loss_out = h->pinned_loss[0];
-    return check_flags(h);
   }
   return KGE_OK;
+}
+
+int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails, float* loss_out) {
+  const int rc = train_batch_enqueue(h, heads, rels, tails, loss_out ? h->pinned_loss : nullptr);
+  if (rc != KGE_OK || !loss_out) return rc;
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "loss readback");
+  *loss_out = h->pinned_loss[0];
+  return check_flags(h);
+}
+
+int kge_train_batch_async(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails,
+                          float* loss_host) {
+  return train_batch_enqueue(h, heads, rels, tails, loss_host);
 }
 
 int kge_sample(kge_handle* h, int64_t step, int64_t* pos_idx, int64_t* neg, int8_t* mode, int64_t* uniq_ent,
@@ -804,6 +828,8 @@ void kge_destroy(kge_handle* h) {
   for (cudaEvent_t ev : h->prof.ev)
     if (ev) cudaEventDestroy(ev);
   if (h->pinned_given) cudaFreeHost(h->pinned_given);
+  for (int i = 0; i < kge_handle::kStage; ++i)
+    if (h->stage_ev[i]) cudaEventDestroy(h->stage_ev[i]);
   if (h->pinned_loss) cudaFreeHost(h->pinned_loss);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   tc_destroy(h);

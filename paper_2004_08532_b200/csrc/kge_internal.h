@@ -184,7 +184,10 @@ struct kge_handle {
   std::vector<kge::Slot> slots;
   kge::Slot debug_slot{};
   int32_t* given = nullptr;  // [3 x B] device copy of caller positives
-  int32_t* pinned_given = nullptr;  // host pinned staging
+  static constexpr int kStage = 4;
+  int32_t* pinned_given = nullptr;  // host pinned staging: kStage buffers of 3B int32 (caller-supplied batches)
+  cudaEvent_t stage_ev[kStage] = {};  // recorded after each staging buffer's H2D copy
+  int32_t stage_i = 0;
   float* pinned_loss = nullptr;
   // step
   kge::StepBuffers buf{};
@@ -202,6 +205,7 @@ struct kge_handle {
   // ranks
   int32_t P = 1, rank = 0;
   int64_t ent_rows = 0;  // rows of the local entity table (shard when P > 1)
+  int32_t* seg_cnt = nullptr;  // [B + n_occ] k_update segment arrival counters
   kge::EntRows rows{};
   kge::Dist dist;
 };
@@ -222,6 +226,27 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// PDL launch with a thread-block cluster of (cx, 1, 1)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                      unsigned cx, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = cx;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
@@ -266,6 +291,9 @@ bool tc_init(kge_handle* h);
 void tc_destroy(kge_handle* h);
 bool tc_supported(const kge_handle* h);
 int32_t tc_neg_parts(const kge_handle* h);
-cudaError_t launch_tc_neg(kge_handle* h, const Slot& s);
+// loss_slot: ring slot of the step's loss; when tc_fuses_chain(h) the backward kernel also applies the positive chain
+// rule and reduces the loss (k_chain is not launched)
+cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot);
+bool tc_fuses_chain(const kge_handle* h);
 
 }  // namespace kge

@@ -102,16 +102,20 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
     for (int c = tid; c < p.C; c += blockDim.x) slot.mode[c] = corrupt_mode(p.corrupt, (uint32_t)s, p.cg_base + c);
   }
   // pad to a power of two
-  int np2 = 1;
+  int np2 = 64;  // >= one 64-key block of the warp-level stages (n_pad >= 64 on the host)
   while (np2 < n) np2 <<= 1;
   for (int q = n + tid; q < np2; q += blockDim.x) keys[q] = ~0ull;
   __syncthreads();
 
-  // bitonic sort, ascending
+  // bitonic sort, ascending. Stages with distance j >= 32 exchange through shared memory (one barrier each); the
+  // j < 32 stages of each merge run warp-synchronously on 64-key blocks held 2 per lane (no block barrier).
+  const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   for (int kk = 2; kk <= np2; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
+    int j = kk >> 1;
+    for (; j >= 32; j >>= 1) {
+      const int lj = __ffs(j) - 1;
       for (int t = tid; t < (np2 >> 1); t += blockDim.x) {
-        const int lo = (t / j) * 2 * j + (t % j);
+        const int lo = ((t >> lj) << (lj + 1)) | (t & (j - 1));
         const int hi = lo + j;
         const bool up = (lo & kk) == 0;
         const unsigned long long x = keys[lo], y = keys[hi];
@@ -122,6 +126,25 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
       }
       __syncthreads();
     }
+    // remaining stages j = min(kk/2, 16) .. 1 stay inside aligned 64-key blocks: lane holds keys b+lane, b+lane+32
+    for (int b = wid * 64; b < np2; b += nw * 64) {
+      unsigned long long k0 = keys[b + lane], k1 = keys[b + lane + 32];
+      const bool up = ((b + lane) & kk) == 0;  // direction of this kk-block (kk >= 64: same for the whole 64-block)
+      for (int jj = j; jj > 0; jj >>= 1) {
+        // element index e = b + lane (+32); partner e ^ jj lies in the same 32-half for jj <= 16
+        const unsigned long long p0 = __shfl_xor_sync(0xffffffffu, k0, jj);
+        const unsigned long long p1 = __shfl_xor_sync(0xffffffffu, k1, jj);
+        const bool low = (lane & jj) == 0;
+        const bool up0 = kk >= 64 ? up : (((b + lane) & kk) == 0);
+        const bool up1 = kk >= 64 ? up : (((b + lane + 32) & kk) == 0);
+        // keep min if (low == up) else max
+        k0 = (low == up0) ? (p0 < k0 ? p0 : k0) : (p0 > k0 ? p0 : k0);
+        k1 = (low == up1) ? (p1 < k1 ? p1 : k1) : (p1 > k1 ? p1 : k1);
+      }
+      keys[b + lane] = k0;
+      keys[b + lane + 32] = k1;
+    }
+    __syncthreads();
   }
 
   // run boundaries -> unique ids, inverse map, segments (reading c.5)

@@ -827,11 +827,10 @@ struct UpdateArgs {
   float* gu;                   // P > 1: per-unique entity gradient sums go here (the owner applies Adagrad)
   const int32_t* split_index;  // P > 1: relation -> index among split relations, -1 if not split
   float* grel_split;           // P > 1: per-rank sums of split relations
+  int32_t* seg_cnt;            // [B + n_occ] per-unique-row segment arrival counters (zero between steps)
 };
 
-// Segment sum of one unique row's occurrence gradients, in sorted-occurrence order, V float4 per lane.
-// Loads of UNR consecutive occurrences are issued together (memory-level parallelism); the additions still happen
-// in occurrence order, so the sum is the same as a serial loop.
+// Row accumulator: V float4 per lane.
 template <int V>
 struct RowAcc {
   float4 g[V];
@@ -843,29 +842,6 @@ struct RowAcc {
     g[m].x += x.x; g[m].y += x.y; g[m].z += x.z; g[m].w += x.w;
   }
 };
-
-template <int V>
-__device__ __forceinline__ void seg_sum(RowAcc<V>& acc, const float* __restrict__ G, const int32_t* __restrict__ occ,
-                                        int p0, int p1, int pstep, int w4, int w, int lane) {
-  constexpr int UNR = 4;
-  for (int p = p0; p < p1; p += UNR * pstep) {
-    float4 x[UNR][V];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int pp = p + u * pstep;
-      const float* src = pp < p1 ? G + (int64_t)__ldg(occ + pp) * w : nullptr;
-#pragma unroll
-      for (int m = 0; m < V; ++m) {
-        const int v = lane + 32 * m;
-        x[u][m] = (src && v < w4) ? ld4(src, v) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u)
-#pragma unroll
-      for (int m = 0; m < V; ++m) acc.add(x[u][m], m);
-  }
-}
 
 // Adagrad on one row given its summed gradient (reading c.11): state += mean(G^2); row -= lr G / sqrt(state + eps).
 // row_v / st0 were prefetched before the segment sum.
@@ -902,71 +878,127 @@ __device__ __forceinline__ void prefetch_row(const float* __restrict__ row, floa
   }
 }
 
-// Grid: [n_ent_blocks blocks: 8 warps, one unique entity row per warp] + [B blocks: one unique relation per CTA,
-// its occurrences strided over the 8 warps (hub relations carry ~10% of a Zipf batch), partials combined in fixed
-// warp order -> deterministic].
+// One warp per SEGMENT: the sorted occurrence list of each unique row is cut into segments of kSeg consecutive
+// positions; the warp whose position starts a segment sums that segment in occurrence order. A row with one segment is
+// updated by that warp directly. A row with several (hub relations carry ~10% of a Zipf batch) parks each segment sum
+// in the gradient row of the segment's first occurrence (read by no other warp), bumps a per-row arrival counter, and
+// the last arriver adds the segment sums in segment order (deterministic: the association is fixed, no float
+// atomics) and applies Adagrad. Warps: [B relation positions][n_occ entity positions]; relation warps first.
+// Everything not produced by the backward pass (sample-slot indices, current rows and Adagrad state -- written by
+// kernels that completed before the forward pass started) is loaded before griddepcontrol.wait.
+constexpr int kSeg = 8;
+
 template <int V>
-__global__ void __launch_bounds__(256) k_update(UpdateArgs a, int n_ent_blocks) {
+__global__ void __launch_bounds__(256, V >= 8 ? 1 : (V >= 4 ? 3 : 4)) k_update(UpdateArgs a) {
   const Dims& dm = a.dm;
   trace_stamp(dm.trace, KGE_K_UPDATE, 0);
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const bool rel = gw < dm.B;
+  const int p = rel ? gw : gw - dm.B;
+  const int npos = rel ? dm.B : dm.n_occ;
+  const int32_t* occ_sorted = rel ? a.s.rel_occ : a.s.ent_occ;
+  const int32_t* off = rel ? a.s.rel_off : a.s.ent_off;
+  float* G = rel ? a.b.Grel : a.b.Gocc;
+  const int w = rel ? dm.drel : dm.d, w4 = w >> 2;
+  bool live = p < npos;
+  int u = 0, r0 = 0, r1 = 0;
+  if (live) {
+    u = (rel ? a.s.rel_inv : a.s.ent_inv)[occ_sorted[p]];
+    r0 = off[u];
+    r1 = off[u + 1];
+    live = (p - r0) % kSeg == 0;
+  }
+  if (__syncthreads_or(live) == 0) return;  // no segment starts in this CTA: leave before the wait
+  if (!live) return;
+  const int n = min(kSeg, r1 - p);  // this segment: positions [p, p + n)
+  const int oj = lane < n ? occ_sorted[p + lane] : 0;
+  const int nseg = (r1 - r0 + kSeg - 1) / kSeg;
+  const int32_t id = (rel ? a.s.rel_uniq : a.s.ent_uniq)[u];
+  float* row;
+  float* st;
+  bool plain_sum;  // write the sum (P > 1 entity sum for the owner / split-relation rank sum) instead of Adagrad
+  if (rel) {
+    const int sidx = a.split_index ? a.split_index[id] : -1;
+    plain_sum = sidx >= 0;
+    row = plain_sum ? a.grel_split + (int64_t)sidx * w : a.rel + (int64_t)id * w;
+    st = a.rel_st + id;
+  } else {
+    plain_sum = a.gu != nullptr;
+    row = plain_sum ? a.gu + (int64_t)u * w : a.ent + (int64_t)id * w;
+    st = a.ent_st + id;
+  }
+  if (!plain_sum) {  // warm L2 with the row and its state (HBM latency off the critical path; no registers held)
+    if (lane * 32 < w + 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + min(lane * 32, w - 1)));
+    if (lane == 31) asm volatile("prefetch.global.L2 [%0];" ::"l"(st));
+  }
   pdl_wait();
   pdl_trigger();
+  trace_stamp(dm.trace, KGE_K_UPDATE, 1);
   if (a.b.flags[1]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if ((int)blockIdx.x < n_ent_blocks) {
-    const int u = blockIdx.x * 8 + warp;
-    if (u >= *a.s.ent_n) return;
-    const int32_t id = a.s.ent_uniq[u];
-    const int w4 = dm.d >> 2;
-    if (a.gu) {  // P > 1: segment sum only; rows live at their owner (dist.cu)
-      RowAcc<V> acc;
-      acc.zero();
-      seg_sum<V>(acc, a.b.Gocc, a.s.ent_occ, a.s.ent_off[u], a.s.ent_off[u + 1], 1, w4, dm.d, lane);
-      float* dst = a.gu + (int64_t)u * dm.d;
-#pragma unroll
-      for (int m = 0; m < V; ++m)
-        if (lane + 32 * m < w4) st4(dst, lane + 32 * m, acc.g[m]);
-      return;
-    }
-    float* row = a.ent + (int64_t)id * dm.d;
-    float4 row_v[V];
-    prefetch_row<V>(row, row_v, w4, lane);
-    const float st0 = a.ent_st[id];
-    RowAcc<V> acc;
-    acc.zero();
-    seg_sum<V>(acc, a.b.Gocc, a.s.ent_occ, a.s.ent_off[u], a.s.ent_off[u + 1], 1, w4, dm.d, lane);
-    adagrad_row<V>(row, a.ent_st + id, acc, row_v, st0, w4, dm.d, dm.lr, dm.eps, lane);
-    return;
-  }
-  const int u = blockIdx.x - n_ent_blocks;
-  if (u >= *a.s.rel_n) return;  // uniform per CTA
-  __shared__ float4 part[8][32 * V];
-  const int32_t id = a.s.rel_uniq[u];
-  const int w = dm.drel, w4 = w >> 2;
-  const int sidx = a.split_index ? a.split_index[id] : -1;
-  float* row = sidx >= 0 ? a.grel_split + (int64_t)sidx * w : a.rel + (int64_t)id * w;
-  float4 row_v[V];
-  if (warp == 0) prefetch_row<V>(row, row_v, w4, lane);
-  const float st0 = a.rel_st[id];
   RowAcc<V> acc;
   acc.zero();
-  seg_sum<V>(acc, a.b.Grel, a.s.rel_occ, a.s.rel_off[u] + warp, a.s.rel_off[u + 1], 8, w4, w, lane);
+  constexpr int UNR = 4;
+  for (int j = 0; j < n; j += UNR) {  // loads of UNR occurrences in flight, additions in occurrence order
+    float4 x[UNR][V];
 #pragma unroll
-  for (int m = 0; m < V; ++m) part[warp][lane + 32 * m] = acc.g[m];
-  __syncthreads();
-  if (warp != 0) return;
-  RowAcc<V> tot;
-  tot.zero();
-  for (int ww = 0; ww < 8; ++ww)
+    for (int q = 0; q < UNR; ++q) {
+      const int o = __shfl_sync(0xffffffffu, oj, (j + q) & 31);
+      const float* src = j + q < n ? G + (int64_t)o * w : nullptr;
 #pragma unroll
-    for (int m = 0; m < V; ++m) tot.add(part[ww][lane + 32 * m], m);
-  if (sidx >= 0) {  // split relation (P > 1): this rank's sum; every replica updates from the rank-ordered total
+      for (int m = 0; m < V; ++m) {
+        const int v = lane + 32 * m;
+        x[q][m] = (src && v < w4) ? ld4(src, v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < UNR; ++q)
+#pragma unroll
+      for (int m = 0; m < V; ++m) acc.add(x[q][m], m);
+  }
+  trace_stamp(dm.trace, KGE_K_UPDATE, 2);
+  if (nseg > 1) {
+    float* home = G + (int64_t)__shfl_sync(0xffffffffu, oj, 0) * w;
 #pragma unroll
     for (int m = 0; m < V; ++m)
-      if (lane + 32 * m < w4) st4(row, lane + 32 * m, tot.g[m]);
+      if (lane + 32 * m < w4) st4(home, lane + 32 * m, acc.g[m]);
+    __threadfence();
+    int32_t* cnt = a.seg_cnt + (rel ? 0 : dm.B) + u;
+    int last = 0;
+    if (lane == 0) last = atomicAdd(cnt, 1) == nseg - 1;
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    __threadfence();
+    if (lane == 0) *cnt = 0;  // ready for the next step
+    acc.zero();
+    constexpr int UNR2 = V >= 4 ? 2 : 4;
+    for (int q0 = 0; q0 < nseg; q0 += UNR2) {  // segment sums, in segment order
+      float4 x[UNR2][V];
+#pragma unroll
+      for (int q = 0; q < UNR2; ++q) {
+        const float* src = q0 + q < nseg ? G + (int64_t)occ_sorted[r0 + (q0 + q) * kSeg] * w : nullptr;
+#pragma unroll
+        for (int m = 0; m < V; ++m) {
+          const int v = lane + 32 * m;
+          x[q][m] = (src && v < w4) ? __ldcg(reinterpret_cast<const float4*>(src) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < UNR2; ++q)
+#pragma unroll
+        for (int m = 0; m < V; ++m) acc.add(x[q][m], m);
+    }
+  }
+  if (plain_sum) {
+#pragma unroll
+    for (int m = 0; m < V; ++m)
+      if (lane + 32 * m < w4) st4(row, lane + 32 * m, acc.g[m]);
     return;
   }
-  adagrad_row<V>(row, a.rel_st + id, tot, row_v, st0, w4, w, dm.lr, dm.eps, lane);
+  float4 row_v[V];
+  prefetch_row<V>(row, row_v, w4, lane);
+  const float st0 = *st;
+  adagrad_row<V>(row, st, acc, row_v, st0, w4, w, dm.lr, dm.eps, lane);
+  trace_stamp(dm.trace, KGE_K_UPDATE, 7);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1014,19 +1046,18 @@ cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
 cudaError_t launch_update(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
   UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, h->buf, h->P > 1 ? h->dist.gu : nullptr,
-                h->P > 1 ? h->dist.split_index : nullptr, h->dist.grel_split};
-  const int n_ent_blocks = (dm.n_occ + 7) / 8;
-  const int grid = n_ent_blocks + dm.B;
-  const int w4 = dm.d / 4;
+                h->P > 1 ? h->dist.split_index : nullptr, h->dist.grel_split, h->seg_cnt};
+  const int grid = (dm.B + dm.n_occ + 7) / 8;
+  const int w4 = std::max(dm.d, dm.drel) / 4;
   launch_begin(h, KGE_K_UPDATE);
   if (w4 <= 32)
-    launch_pdl(k_update<1>, grid, 256, 0, h->stream, ua, n_ent_blocks);
+    launch_pdl(k_update<1>, grid, 256, 0, h->stream, ua);
   else if (w4 <= 64)
-    launch_pdl(k_update<2>, grid, 256, 0, h->stream, ua, n_ent_blocks);
+    launch_pdl(k_update<2>, grid, 256, 0, h->stream, ua);
   else if (w4 <= 128)
-    launch_pdl(k_update<4>, grid, 256, 0, h->stream, ua, n_ent_blocks);
+    launch_pdl(k_update<4>, grid, 256, 0, h->stream, ua);
   else
-    launch_pdl(k_update<8>, grid, 256, 0, h->stream, ua, n_ent_blocks);
+    launch_pdl(k_update<8>, grid, 256, 0, h->stream, ua);
   launch_end(h, KGE_K_UPDATE);
   return cudaGetLastError();
 }
@@ -1041,9 +1072,11 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   launch_end(h, KGE_K_GATHER);
 
   NegArgs na{dm, h->buf, h->buf.Gocc};
+  const int32_t loss_slot = (int32_t)(step % h->ring);
   if (h->cfg.neg_precision == KGE_PREC_TF32 && tc_supported(h)) {
-    cudaError_t e = launch_tc_neg(h, s);
+    cudaError_t e = launch_tc_neg(h, s, loss_slot);
     if (e != cudaSuccess) return e;
+    if (tc_fuses_chain(h)) return launch_update(h, s);  // chain rule + loss done in the backward epilogue
   } else {
     switch (dm.family) {
       case FAM_DOT: launch_neg<FAM_DOT>(h, na); break;
@@ -1053,7 +1086,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
       case FAM_CMOD: launch_neg<FAM_CMOD>(h, na); break;
     }
   }
-  ChainArgs ca{dm, s, h->rows, h->rel, h->buf, h->n_neg_parts, (int32_t)(step % h->ring)};
+  ChainArgs ca{dm, s, h->rows, h->rel, h->buf, h->n_neg_parts, loss_slot};
   launch_begin(h, KGE_K_CHAIN);
   const unsigned cgrid = (dm.B + 7) / 8 + 1;
   switch (row_v(dm.d)) {

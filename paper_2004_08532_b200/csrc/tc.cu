@@ -26,18 +26,22 @@ namespace kge {
 using namespace tc;
 
 struct TcState {
-  CUtensorMap mO_K, mX_K;    // fwd operands (K-major, SW128), boxes {32, 128 | NT}
+  CUtensorMap mO_K, mX_K;    // O (K-major, SW128), box {32, 128}; fwd X' operand, box {32, NT}
+  CUtensorMap mO_F;          // fwd O operand: box {32, 128 / fwd_cx} (this CTA's multicast slice)
   CUtensorMap mW_K;          // dO operand A (K-major), box {32, 128}
   CUtensorMap mX_MN, mO_MN;  // B operands of dO / dX' (MN-major, 128B_ATOM_32B), box {32, 32}
   CUtensorMap mW_MN;         // A operand of dX' (MN-major), box {32, 32}
   CUtensorMap mX_E;          // dX' epilogue operand (X' rows, K-major SW128), box {32, 128}
+  CUtensorMap mG_S, mR_S, mD_S;
+  int fwd_cx = 1;  // backward TMA-store targets: Gocc, Grel, dO (SW128), box {32, 32}
   bool ok = false;
 };
 
 constexpr int kNT = 32;         // negatives per forward CTA
-constexpr int kFwdStages = 4;
-constexpr int kBwdStages = 4;
+constexpr int kFwdStages = 8;
+constexpr int kBwdStages = 5;
 constexpr int kNSplit = 4;      // column ranges of dp per backward tile
+constexpr uint32_t kBwdStaging = 4 * 24576;  // backward epilogue store staging (reuses the pipeline stages)
 constexpr int kThreads = 128;   // 4 warps: warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer; all 4 = epilogue
 constexpr int kFwdThreads = 256;  // forward: 8 epilogue warps (two per TMEM lane quarter, 16 negatives each) so the
                                   // transcendental chains of the loss epilogue have latency hiding
@@ -56,6 +60,19 @@ struct TcArgs {
   float* rowsum_part;  // [B x nrp]   partial sums of W over the forward CTA's 32 negatives
   float* colsum_part;  // [C*k x ncp] partial sums of W over the forward CTA's 128 positives
   int32_t nrp, ncp;
+  // fused positive chain rule (TransE-L2): the dO epilogue adds the positive-score gradient and applies the chain rule
+  // through o = h + r / t - r itself, writing Gocc (H, T rows) and Grel instead of dO; CTA 0 reduces the loss
+  int32_t fuse;
+  Slot s;
+  EntRows ent;
+  const float* wpos;
+  const float* pstat;
+  const float* lpos;
+  float* Grel;
+  float* loss;
+  int32_t* flags;
+  int32_t loss_slot, n_neg_parts;
+  int32_t fwd_cx;  // forward cluster size along x: the CTAs of one 128-positive tile share its O tile by TMA multicast
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -89,10 +106,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.z, i0 = blockIdx.y * 128, j0 = blockIdx.x * kNT;
   const int nkb = a.dp / 32;
+  // cluster of cx CTAs along x (same positives, different negatives): CTA `crank` loads rows [crank*128/cx, +128/cx)
+  // of each O k-block and multicasts them; a stage is refilled only after all cx CTAs' MMAs released it
+  const int cx = a.fwd_cx;
+  const uint32_t crank = cx > 1 ? cluster_ctarank() : 0;
+  const uint16_t cmask = (uint16_t)((1u << cx) - 1);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kFwdStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], cx);
     }
     mbar_init(&done, 1);
     fence_mbar_init();
@@ -109,6 +131,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (cx > 1) cluster_sync();  // every CTA's barriers are initialised before any multicast lands
   const uint32_t tmem = tbase;
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 1);
 
@@ -118,7 +141,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (kb >= kFwdStages) mbar_wait(&empty[s], ((kb / kFwdStages) - 1) & 1);
       uint8_t* sa = smem + s * STAGE;
       mbar_arrive_expect_tx(&full[s], STAGE);
-      tma_load_3d(sa, &mO, &full[s], kb * 32, i0, c);
+      if (cx > 1)
+        tma_load_3d_mc(sa + crank * (A_BYTES / cx), &mO, &full[s], kb * 32, i0 + (int)crank * (128 / cx), c, cmask);
+      else
+        tma_load_3d(sa, &mO, &full[s], kb * 32, i0, c);
       tma_load_3d(sa + A_BYTES, &mX, &full[s], kb * 32, j0, c);
     }
   } else if (warp == 1 && lane == 0) {  // MMA issuer
@@ -131,7 +157,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
         mma_tf32(tmem, sdesc(sa + kk * 32, 16, 1024), sdesc(sb + kk * 32, 16, 1024), idesc, (kb | kk) ? 1u : 0u);
-      mma_commit(&empty[s]);
+      if (cx > 1)
+        mma_commit_mc(&empty[s], cmask);
+      else
+        mma_commit(&empty[s]);
     }
     mma_commit(&done);
   }
@@ -216,6 +245,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
   }
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 6);
+  if (cx > 1) cluster_sync();  // no CTA leaves while a peer's MMA commit may still arrive on its barriers
   if (warp == 0) tmem_dealloc(tmem, 32);
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 7);
 }
@@ -228,7 +258,9 @@ template <int FAM>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_bwd(const __grid_constant__ CUtensorMap mW_K, const __grid_constant__ CUtensorMap mW_MN,
              const __grid_constant__ CUtensorMap mX_MN, const __grid_constant__ CUtensorMap mO_MN,
-             const __grid_constant__ CUtensorMap mO_E, const __grid_constant__ CUtensorMap mX_E, TcArgs a) {
+             const __grid_constant__ CUtensorMap mO_E, const __grid_constant__ CUtensorMap mX_E,
+             const __grid_constant__ CUtensorMap mG_S, const __grid_constant__ CUtensorMap mR_S,
+             const __grid_constant__ CUtensorMap mD_S, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   __shared__ uint64_t full[kBwdStages], empty[kBwdStages], done, selfbar;
@@ -251,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)nb * 4096;
   // epilogue operand (L2): this CTA's rows x column blocks of O (dO) or X' (dX'), TMA'd at the start so the load
   // overlaps the main loop; block b at self_smem + b * 16 KB, 128-byte rows, 16-byte chunks swizzled by (row % 8)
-  uint8_t* self_smem = smem + kBwdStages * STAGE;
+  uint8_t* self_smem = smem + max(kBwdStages * STAGE, kBwdStaging);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kBwdStages; ++s) {
       mbar_init(&full[s], 1);
@@ -322,43 +354,133 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int q = 0; q < a.ncp; ++q) corr += cp[q];
     }
   }
+  const bool fuse = FAM == FAM_L2 && a.fuse && !pass_x;
+  int loss_part = 0;  // the loss is reduced by the first CTA of (row tile 0, chunk 0) that has columns to process
+  while (loss_part + 1 < kNSplit && ((loss_part + 1) * nb_all / kNSplit == loss_part * nb_all / kNSplit ||
+                                     loss_part * nb_all / kNSplit * 32 >= d))
+    ++loss_part;
+  if (fuse && blockIdx.x == loss_part && blockIdx.y == 0 && warp == 3) {
+    // deterministic loss (reading c.9): fixed lane assignment and order, identical to the unfused k_chain
+    float sp = 0.f, sn = 0.f;
+    for (int i = lane; i < dm.B; i += 32) sp += a.lpos[i];
+    for (int q = lane; q < a.n_neg_parts; q += 32) sn += a.lneg[q];
+    sp = warp_sum(sp);
+    sn = warp_sum(sn);
+    if (lane == 0) {
+      const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
+      a.loss[a.loss_slot] = L;
+      const bool bad = !isfinite(L);
+      a.flags[1] = bad ? 1 : 0;
+      if (bad) a.flags[0] = 1;
+    }
+  }
+  // fused chain: positive i of this row; x = the uncorrupted "other" entity row (t for tail mode, h for head mode),
+  // prefetched for all column blocks while the MMAs run
+  const int pi = c * dm.g + r;
+  const int mode = fuse ? a.s.mode[c] : 0;
+  float pscale = 0.f;
+  float4 xr[4][8];
+  if (fuse && rok) {
+    pscale = a.wpos[pi] / fmaxf(sqrtf(a.pstat[pi]), 1e-12f);
+    const float* xrow = a.ent.row(mode == 0 ? a.s.pt[pi] : a.s.ph[pi]);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int e0 = (b0 + b) * 32;
+      if (b < nb && e0 < d) {
+        const float4* x4 = reinterpret_cast<const float4*>(xrow + e0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xr[b][u] = 4 * u < d - e0 ? __ldg(x4 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  // output tiles of this warp's 32 rows: t = 0 the primary (dO | dX' | fused: gradient of the combined entity),
+  // fused only: t = 1 gradient of the other entity, t = 2 relation gradient. Full 32-row warps stage each
+  // 32 x 32 tile in (free) pipeline shared memory in the SW128 layout and TMA-store it (coalesced, asynchronous);
+  // a ragged warp (chunk shorter than its rows) stores its valid rows directly.
+  const int wrow0 = r0 + warp * 32;
+  const bool wtma = wrow0 + 32 <= nrows;
+  const int ntile = fuse ? 3 : 1;
+  const CUtensorMap* tmap0 = pass_x || fuse ? &mG_S : &mD_S;
+  int trow0[3];
+  trow0[0] = pass_x ? 2 * dm.B + c * dm.k + wrow0 : (fuse && mode == 1 ? dm.B : 0) + c * dm.g + wrow0;
+  trow0[1] = (mode == 0 ? dm.B : 0) + c * dm.g + wrow0;
+  trow0[2] = c * dm.g + wrow0;
+  float* gdst[3];
+  gdst[0] = pass_x ? a.Gocc + ((int64_t)2 * dm.B + (int64_t)c * dm.k + r) * d
+                   : fuse ? a.Gocc + ((int64_t)(mode == 0 ? 0 : dm.B) + pi) * d : a.dO + (int64_t)pi * d;
+  gdst[1] = a.Gocc + ((int64_t)(mode == 0 ? dm.B : 0) + pi) * d;
+  gdst[2] = a.Grel + (int64_t)pi * dm.drel;
+  const float rsign = mode == 0 ? 1.f : -1.f;
+  uint8_t* stg = smem + warp * 24576;  // 2 buffers x 3 tiles x 4 KB per warp (the MMAs are done with this memory)
   mbar_wait(&done, 0);
   tc_fence_after();
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 2);
   if (FAM == FAM_L2) mbar_wait(&selfbar, 0);
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 3);
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  float* dst = pass_x ? a.Gocc + ((int64_t)2 * dm.B + (int64_t)c * dm.k + r) * d : a.dO + ((int64_t)c * dm.g + r) * d;
   const int rl = warp * 32 + lane;  // row within the tile
-#pragma unroll 1
-  for (int b = 0; b < nb; ++b) {
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    if (b >= nb) break;
     const int e0 = (b0 + b) * 32;
     float v[32];
     tmem_ld32(trow + b * 32, v);
-    if (!rok || e0 >= d) continue;
+    if (e0 >= d) continue;
     const int ne = min(32, d - e0);
-    if (FAM == FAM_L2) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D)
+    uint8_t* buf = stg + (b & 1) * 12288;
+    if (wtma && b >= 2) {  // the buffer written two blocks ago must have been read by its TMA store
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+    }
+    if (rok) {
       const uint8_t* rowp = self_smem + b * 16384 + rl * 128;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float4 sv = *reinterpret_cast<const float4*>(rowp + ((u ^ (rl & 7)) << 4));
-        v[4 * u] = corr * sv.x - v[4 * u];
-        v[4 * u + 1] = corr * sv.y - v[4 * u + 1];
-        v[4 * u + 2] = corr * sv.z - v[4 * u + 2];
-        v[4 * u + 3] = corr * sv.w - v[4 * u + 3];
+        float4 t0 = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]), t1, t2;
+        if (FAM == FAM_L2) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D)
+          const float4 sv = *reinterpret_cast<const float4*>(rowp + ((u ^ (rl & 7)) << 4));
+          t0 = make_float4(corr * sv.x - t0.x, corr * sv.y - t0.y, corr * sv.z - t0.z, corr * sv.w - t0.w);
+          if (fuse) {
+            // go = dO + w+ df/do, gx = w+ df/dx; f = gamma - ||o - x||: go = dO - s u, gx = s u (u = o - x, s = w+/D)
+            // tail (o = h + r): gH = go, gR = go, gT = gx ; head (o = t - r): gT = go, gR = -go, gH = gx
+            const float4 xv = xr[b][u];
+            t1 = make_float4(pscale * (sv.x - xv.x), pscale * (sv.y - xv.y), pscale * (sv.z - xv.z),
+                             pscale * (sv.w - xv.w));
+            t0 = make_float4(-t1.x + t0.x, -t1.y + t0.y, -t1.z + t0.z, -t1.w + t0.w);
+            t2 = make_float4(rsign * t0.x, rsign * t0.y, rsign * t0.z, rsign * t0.w);
+          }
+        }
+        if (wtma) {
+          const int off = lane * 128 + ((u ^ (lane & 7)) << 4);
+          *reinterpret_cast<float4*>(buf + off) = t0;
+          if (fuse) {
+            *reinterpret_cast<float4*>(buf + 4096 + off) = t1;
+            *reinterpret_cast<float4*>(buf + 8192 + off) = t2;
+          }
+        } else if (4 * u < ne) {
+          reinterpret_cast<float4*>(gdst[0] + e0)[u] = t0;
+          if (fuse) {
+            reinterpret_cast<float4*>(gdst[1] + e0)[u] = t1;
+            reinterpret_cast<float4*>(gdst[2] + e0)[u] = t2;
+          }
+        }
       }
     }
-    if (ne == 32) {
-      float4* o4 = reinterpret_cast<float4*>(dst + e0);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) o4[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
-    } else {
-#pragma unroll
-      for (int u = 0; u < 32; ++u)  // static indices keep v[] in registers
-        if (u < ne) dst[e0 + u] = v[u];
+    if (wtma) {
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(tmap0, buf, e0, trow0[0], 0);
+        if (ntile > 1) {
+          tma_store_3d(&mG_S, buf + 4096, e0, trow0[1], 0);
+          tma_store_3d(&mR_S, buf + 8192, e0, trow0[2], 0);
+        }
+        bulk_commit();
+      }
     }
     if (b == 0) trace_stamp(dm.trace, KGE_K_NEG_BWD, 4);
   }
+  if (wtma && lane == 0) bulk_wait_all();
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 5);
   tc_fence_before();
   __syncthreads();
@@ -404,7 +526,8 @@ static bool make_map(CUtensorMap* m, const float* base, int cols, int rows, int 
 static size_t fwd_smem() { return (size_t)kFwdStages * (128 * 128 + kNT * 128) + 1024; }
 static size_t bwd_smem(int dp) {
   const int nb_max = (dp / 32 + kNSplit - 1) / kNSplit;
-  return (size_t)kBwdStages * (128 * 128 + (size_t)nb_max * 4096) + (size_t)nb_max * 16384 + 1024;
+  return std::max((size_t)kBwdStages * (128 * 128 + (size_t)nb_max * 4096), (size_t)kBwdStaging) +
+         (size_t)nb_max * 16384 + 1024;
 }
 
 bool tc_init(kge_handle* h) {
@@ -414,13 +537,19 @@ bool tc_init(kge_handle* h) {
   TcState* st = new TcState();
   const StepBuffers& b = h->buf;
   bool ok = true;
+  const int fx = (dm.k + kNT - 1) / kNT;
+  st->fwd_cx = fx % 8 == 0 ? 8 : fx % 4 == 0 ? 4 : fx % 2 == 0 ? 2 : 1;
   ok &= make_map(&st->mO_K, b.O, h->dp, dm.g, dm.C, h->dp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&st->mO_F, b.O, h->dp, dm.g, dm.C, h->dp, 128 / st->fwd_cx, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mX_K, b.X, h->dp, dm.k, dm.C, h->dp, kNT, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mW_K, b.W, dm.k, dm.g, dm.C, h->kp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mX_MN, b.X, h->dp, dm.k, dm.C, h->dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   ok &= make_map(&st->mO_MN, b.O, h->dp, dm.g, dm.C, h->dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   ok &= make_map(&st->mW_MN, b.W, dm.k, dm.g, dm.C, h->kp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   ok &= make_map(&st->mX_E, b.X, h->dp, dm.k, dm.C, h->dp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&st->mG_S, b.Gocc, dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&st->mR_S, b.Grel, dm.drel, dm.B, 1, dm.drel, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&st->mD_S, b.dO, dm.d, dm.B, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!ok) {
     delete st;
     return false;
@@ -457,30 +586,33 @@ int32_t tc_neg_parts(const kge_handle* h) {
   return dm.C * ((dm.g + 127) / 128) * ((dm.k + kNT - 1) / kNT);
 }
 
-cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
-  (void)s;
+bool tc_fuses_chain(const kge_handle* h) { return h->dims.model == KGE_TRANSE_L2; }
+
+cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
   const Dims& dm = h->dims;
   const TcState* st = static_cast<const TcState*>(h->tc);
   TcArgs a{dm, h->dp, h->kp, h->buf.O, h->buf.X, h->buf.onorm, h->buf.xnorm, h->buf.W, h->buf.lneg, h->buf.dO,
-           h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128};
+           h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128,
+           tc_fuses_chain(h) ? 1 : 0, s, h->rows, h->buf.wpos, h->buf.pstat, h->buf.lpos, h->buf.Grel,
+           h->buf.loss, h->buf.flags, loss_slot, h->n_neg_parts, st->fwd_cx};
   dim3 gf((dm.k + kNT - 1) / kNT, (dm.g + 127) / 128, dm.C);
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(tiles * kNSplit, dm.C, 2);
   launch_begin(h, KGE_K_NEG_FWD);
   if (dm.family == FAM_DOT)
-    launch_pdl(k_tc_fwd<FAM_DOT>, gf, kFwdThreads, fwd_smem(), h->stream, st->mO_K, st->mX_K, a);
+    launch_pdl_cluster(k_tc_fwd<FAM_DOT>, gf, kFwdThreads, fwd_smem(), h->stream, st->fwd_cx, st->mO_F, st->mX_K, a);
   else
-    launch_pdl(k_tc_fwd<FAM_L2>, gf, kFwdThreads, fwd_smem(), h->stream, st->mO_K, st->mX_K, a);
+    launch_pdl_cluster(k_tc_fwd<FAM_L2>, gf, kFwdThreads, fwd_smem(), h->stream, st->fwd_cx, st->mO_F, st->mX_K, a);
   launch_end(h, KGE_K_NEG_FWD);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   launch_begin(h, KGE_K_NEG_BWD);
   if (dm.family == FAM_DOT)
     launch_pdl(k_tc_bwd<FAM_DOT>, gb, kThreads, bwd_smem(h->dp), h->stream, st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN,
-               st->mO_K, st->mX_E, a);
+               st->mO_K, st->mX_E, st->mG_S, st->mR_S, st->mD_S, a);
   else
     launch_pdl(k_tc_bwd<FAM_L2>, gb, kThreads, bwd_smem(h->dp), h->stream, st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN,
-               st->mO_K, st->mX_E, a);
+               st->mO_K, st->mX_E, st->mG_S, st->mR_S, st->mD_S, a);
   launch_end(h, KGE_K_NEG_BWD);
   return cudaGetLastError();
 }

@@ -71,6 +71,7 @@ def lib():
                                  _i64p, _i64p, _i32p]
         L.kge_train_step.argtypes = [ctypes.c_void_p, ctypes.c_int64, _fp]
         L.kge_train_batch.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, _fp]
+        L.kge_train_batch_async.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, _fp]
         L.kge_score.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, _fp]
         L.kge_get_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_set_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
@@ -240,6 +241,13 @@ class Handle:
         """Raw-pointer variant (host int64 buffers, e.g. pinned torch tensors)."""
         _check(lib().kge_train_batch(self._h, ctypes.cast(hp, _i64p), ctypes.cast(rp, _i64p), ctypes.cast(tp, _i64p),
                                      ctypes.cast(loss_ptr, _fp) if loss_ptr else None))
+
+    # kge_train_batch_async
+    def train_batch_async_ptr(self, hp, rp, tp, loss_ptr):
+        """Pipelined variant: enqueue the step (H2D batch, step, D2H loss into the pinned float at loss_ptr) and
+        return; the loss is valid after sync()."""
+        _check(lib().kge_train_batch_async(self._h, ctypes.cast(hp, _i64p), ctypes.cast(rp, _i64p),
+                                           ctypes.cast(tp, _i64p), ctypes.cast(loss_ptr, _fp) if loss_ptr else None))
 
     # kge_score
     def score(self, hs, rs, ts):

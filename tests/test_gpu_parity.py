@@ -183,6 +183,27 @@ def test_train_batch_equals_sampled_step():
     assert np.array_equal(gpu_a.get_rows(0, ids), gpu_b.get_rows(0, ids))
 
 
+def test_train_batch_async_equals_sync():
+    # the pipelined entry (staging ring, async loss copies, one sync) computes exactly what the synchronous one does
+    import torch
+    gpu_a, _, trip = _tiny("transe_l2", dim=32)
+    gpu_b, _, _ = _tiny("transe_l2", dim=32)
+    h, r, t = [np.asarray(a) for a in trip]
+    n = 9  # more steps than staging buffers
+    pos = [gpu_a.sample(s)["pos"] for s in range(n)]
+    hp = torch.from_numpy(np.stack([h[p] for p in pos])).pin_memory()
+    rp = torch.from_numpy(np.stack([r[p] for p in pos])).pin_memory()
+    tp = torch.from_numpy(np.stack([t[p] for p in pos])).pin_memory()
+    losses = torch.full((n,), float("nan"), dtype=torch.float32).pin_memory()
+    for s in range(n):
+        gpu_a.train_batch_async_ptr(hp[s].data_ptr(), rp[s].data_ptr(), tp[s].data_ptr(), losses[s:].data_ptr())
+    gpu_a.sync()
+    ref = [gpu_b.train_batch(h[p], r[p], t[p]) for p in pos]
+    assert np.array_equal(losses.numpy(), np.asarray(ref, np.float32))
+    ids = np.arange(1000)
+    assert np.array_equal(gpu_a.get_rows(0, ids), gpu_b.get_rows(0, ids))
+
+
 def test_deterministic():
     a, _, _ = _tiny("rotate", dim=32)
     b, _, _ = _tiny("rotate", dim=32)

@@ -45,3 +45,23 @@ for k in range(1, 6):
             if len(x):
                 line += f" | s{sl} med {np.median(x)/1e3:6.2f}"
     print(line)
+# backward split by pass (z = 0: dO / fused chain, z = 1: dX'); CTAs are numbered x + gx*(y + gy*z)
+k = 3
+m = T[k][:, 0] > 0
+n = m.sum()
+for z, sl in ((0, slice(0, n // 2)), (1, slice(n // 2, n))):
+    R = T[k][:n][sl] - t0
+    cols = " ".join(f"s{j} {np.median(R[:, j])/1e3:6.2f}/{R[:, j].max()/1e3:6.2f}" for j in range(8))
+    print(f"  bwd z={z}: med/max {cols}")
+# update: entity CTAs first (n_occ / 8 of them), then one CTA per unique relation
+k = 5
+U = T[k]
+nr = 1024  # relation CTAs first (one per possible unique relation), then the entity CTAs
+for name, sl in (("relation", slice(0, nr)), ("entity", slice(nr, 2048))):
+    R = U[sl]
+    m = R[:, 7] > 0
+    if not m.any():
+        continue
+    R = R[m] - t0
+    cols = " ".join(f"s{j} {np.median(R[:, j])/1e3:6.2f}/{R[:, j].max()/1e3:6.2f}" for j in (0, 1, 2, 3, 7) if (U[sl][m][:, j] > 0).all())
+    print(f"  update {name:8s} n={m.sum():4d}: med/max {cols}")
