@@ -462,7 +462,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   StepBuffers& b = h->buf;
   const int64_t nneg = (int64_t)dm.C * dm.k;
   h->n_neg_parts = dm.C * ((dm.g + 63) / 64) * ((dm.k + 63) / 64);
-  const int64_t tc_parts = (int64_t)dm.C * ((dm.g + 127) / 128) * ((dm.k + 31) / 32);  // >= TC epilogue partials
+  const int64_t tc_parts = (int64_t)dm.C * ((dm.g + 127) / 128) * ((dm.k + 31) / 32) * 2;  // >= TC epilogue partials
   b.O = (float*)dalloc(h, (size_t)dm.B * dm.dp * 4);
   b.onorm = (float*)dalloc(h, (size_t)dm.B * 4);
   b.X = (float*)dalloc(h, (size_t)nneg * dm.dp * 4);

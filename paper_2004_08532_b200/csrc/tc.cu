@@ -16,6 +16,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "kge_internal.h"
@@ -27,7 +28,8 @@ using namespace tc;
 
 struct TcState {
   CUtensorMap mO_K, mX_K;    // O (K-major, SW128), box {32, 128}; fwd X' operand, box {32, NT}
-  CUtensorMap mO_F;          // fwd O operand: box {32, 128 / fwd_cx} (this CTA's multicast slice)
+  CUtensorMap mO_F;          // fwd O operand (4D {32, rows, k-blocks, chunk}): box {32, 128, 1 (cx > 1) | kFwdKpb}
+  CUtensorMap mX_F;          // fwd X' operand (4D): box {32, kNT, kFwdKpb}
   CUtensorMap mW_K;          // dO operand A (K-major), box {32, 128}
   CUtensorMap mX_MN, mO_MN;  // B operands of dO / dX' (MN-major, 128B_ATOM_32B), box {32, 32}
   CUtensorMap mW_MN;         // A operand of dX' (MN-major), box {32, 32}
@@ -38,11 +40,15 @@ struct TcState {
 };
 
 constexpr int kNT = 32;         // negatives per forward CTA
-constexpr int kFwdStages = 8;
+constexpr int kIssuers = 4;     // MMA-issuing threads per CTA (one per K = 8 slice of a 32-float k-block)
+constexpr int kFwdKpb = 4;      // forward: k-blocks (32 floats of K) per pipeline stage = per TMA instruction
+constexpr int kFwdStages = 2;   // forward stages of kFwdKpb k-blocks (A 64 KB + B 16 KB each)
 constexpr int kBwdStages = 5;
 constexpr int kNSplit = 4;      // column ranges of dp per backward tile
 constexpr uint32_t kBwdStaging = 4 * 24576;  // backward epilogue store staging (reuses the pipeline stages)
-constexpr int kThreads = 128;   // 4 warps: warp 0 lane 0 = TMA producer, warp 1 lane 0 = MMA issuer; all 4 = epilogue
+constexpr int kThreads = 256;   // backward: warps 0-3 = epilogue (TMEM lane quarters; warp 0 lane 0 also the TMA
+                                // producer), lane 0 of warps 4-7 = the kIssuers MMA issuers
+static_assert(kIssuers == 4, "the epilogues add exactly four partial accumulators");
 constexpr int kFwdThreads = 256;  // forward: 8 epilogue warps (two per TMEM lane quarter, 16 negatives each) so the
                                   // transcendental chains of the loss epilogue have latency hiding
 
@@ -72,6 +78,7 @@ struct TcArgs {
   float* loss;
   int32_t* flags;
   int32_t loss_slot, n_neg_parts;
+  float inv_bk;    // 1 / (B k), the dL/df- scale (reading c.9)
   int32_t fwd_cx;  // forward cluster size along x: the CTAs of one 128-positive tile share its O tile by TMA multicast
 };
 
@@ -95,131 +102,191 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     k_tc_fwd(const __grid_constant__ CUtensorMap mO, const __grid_constant__ CUtensorMap mX, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  constexpr uint32_t A_BYTES = 128 * 128, B_BYTES = kNT * 128, STAGE = A_BYTES + B_BYTES;
+  constexpr uint32_t A_KB = 128 * 128, B_KB = kNT * 128;  // one k-block of A (O rows) / B (X' rows)
+  constexpr uint32_t A_BYTES = kFwdKpb * A_KB, STAGE = kFwdKpb * (A_KB + B_KB);
+  constexpr int kHalf = kNT / 2;  // columns this CTA finalises
   __shared__ uint64_t full[kFwdStages], empty[kFwdStages], done;
   __shared__ uint32_t tbase;
-  __shared__ float s_xn[kNT];
+  __shared__ float s_xn[kHalf];
   __shared__ float s_red[8];
-  __shared__ float s_col[4][kNT];
+  __shared__ float s_col[4][kHalf];
+  __shared__ float s_rs[2][128];
+  float* xch = reinterpret_cast<float*>(smem + kFwdStages * STAGE);  // [128 rows][kHalf]: the peer's partial sums
   const Dims& dm = a.dm;
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.z, i0 = blockIdx.y * 128, j0 = blockIdx.x * kNT;
-  const int nkb = a.dp / 32;
-  // cluster of cx CTAs along x (same positives, different negatives): CTA `crank` loads rows [crank*128/cx, +128/cx)
-  // of each O k-block and multicasts them; a stage is refilled only after all cx CTAs' MMAs released it
-  const int cx = a.fwd_cx;
-  const uint32_t crank = cx > 1 ? cluster_ctarank() : 0;
-  const uint16_t cmask = (uint16_t)((1u << cx) - 1);
+  // Split-K pair: the CTAs x = 2 t + ks (t = 32-negative tile) share the tile, ks = 0 / 1 contracting the first /
+  // second half of the k-blocks; after the main loop each sends the other half of its 32 columns of partial sums
+  // to the peer through distributed shared memory, and finalises kHalf columns (the sum is always P0 + P1).
+  // Cluster = cxn tiles x 2 halves: the CTAs with the same ks share one O operand, CTA (ntl, ks) loading k-block ntl
+  // of every stage and multicasting it (cxn = kFwdKpb) -- a stage is refilled once all of them released it.
+  const int cxn = a.fwd_cx, cl = 2 * cxn;
+  const uint32_t crank = cluster_ctarank();
+  const int ks = (int)(crank & 1), ntl = (int)(crank >> 1);
+  const uint16_t mmask = (uint16_t)(cxn > 1 ? (0x55u << ks) & ((1u << cl) - 1) : 0);  // same-ks CTAs
+  const int c = blockIdx.z, i0 = blockIdx.y * 128, t = blockIdx.x >> 1, j0 = t * kNT;
+  const int nkb = a.dp / 32, kh = (nkb + 1) / 2;
+  const int kb0 = ks ? kh : 0, kb1 = ks ? nkb : kh;
+  const int nst = (kb1 - kb0 + kFwdKpb - 1) / kFwdKpb;
+  const int jf0 = j0 + ks * kHalf;  // first column this CTA finalises
   if (threadIdx.x == 0) {
     for (int s = 0; s < kFwdStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], cx);
+      mbar_init(&empty[s], kIssuers * cxn);
     }
-    mbar_init(&done, 1);
+    mbar_init(&done, kIssuers);
     fence_mbar_init();
     tma_prefetch(&mO);
     tma_prefetch(&mX);
   }
-  if (warp == 0) tmem_alloc(&tbase, 32);
+  if (warp == 0) tmem_alloc(&tbase, kIssuers * kNT);
   pdl_wait();  // predecessor (gather) complete: O, X', norms are final
   pdl_trigger();
-  if (threadIdx.x < kNT) {
-    const int jj = j0 + threadIdx.x;
-    s_xn[threadIdx.x] = jj < dm.k ? a.xnorm[(int64_t)c * dm.k + jj] : 0.f;
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (cx > 1) cluster_sync();  // every CTA's barriers are initialised before any multicast lands
+  cluster_sync();  // every CTA's barriers are initialised before any multicast or DSMEM store lands
   const uint32_t tmem = tbase;
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 1);
 
   if (warp == 0 && lane == 0) {  // TMA producer
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kFwdStages;
-      if (kb >= kFwdStages) mbar_wait(&empty[s], ((kb / kFwdStages) - 1) & 1);
+    for (int q = 0; q < nst; ++q) {
+      const int s = q % kFwdStages;
+      if (q >= kFwdStages) mbar_wait(&empty[s], ((q / kFwdStages) - 1) & 1);
       uint8_t* sa = smem + s * STAGE;
-      mbar_arrive_expect_tx(&full[s], STAGE);
-      if (cx > 1)
-        tma_load_3d_mc(sa + crank * (A_BYTES / cx), &mO, &full[s], kb * 32, i0 + (int)crank * (128 / cx), c, cmask);
-      else
-        tma_load_3d(sa, &mO, &full[s], kb * 32, i0, c);
-      tma_load_3d(sa + A_BYTES, &mX, &full[s], kb * 32, j0, c);
+      // a box always delivers its full size (out-of-range rows / k-blocks are zero-filled); with multicast only the
+      // k-blocks of this half that exist are loaded (one box each)
+      const int kq = kb0 + q * kFwdKpb, nk = min(kFwdKpb, kb1 - kq);
+      mbar_arrive_expect_tx(&full[s], (cxn > 1 ? nk : kFwdKpb) * A_KB + kFwdKpb * B_KB);
+      if (cxn > 1) {
+        if (ntl < nk) tma_load_4d_mc(sa + ntl * A_KB, &mO, &full[s], 0, i0, kq + ntl, c, mmask);
+      } else {
+        tma_load_4d(sa, &mO, &full[s], 0, i0, kq, c);
+      }
+      tma_load_4d(sa + A_BYTES, &mX, &full[s], 0, j0, kq, c);
     }
-  } else if (warp == 1 && lane == 0) {  // MMA issuer
+  } else if (warp >= 8 - kIssuers && lane == 0) {
+    // MMA issuers: a single thread issues one tcgen05.mma per ~130 cycles whatever N is (measured, tools/mma_probe.cu),
+    // so the K = 8 slices of each k-block are dealt to kIssuers threads, issuer q accumulating slice q of every
+    // k-block into its own TMEM columns [q * kNT, (q + 1) * kNT); the epilogue adds the partials in a fixed order
+    const int q = warp - (8 - kIssuers);
     const uint32_t idesc = idesc_tf32(128, kNT, false, false);
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kFwdStages;
-      mbar_wait(&full[s], (kb / kFwdStages) & 1);
+    const uint32_t acc = tmem + (uint32_t)(q * kNT);
+    for (int st = 0; st < nst; ++st) {
+      const int s = st % kFwdStages;
+      mbar_wait(&full[s], (st / kFwdStages) & 1);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        mma_tf32(tmem, sdesc(sa + kk * 32, 16, 1024), sdesc(sb + kk * 32, 16, 1024), idesc, (kb | kk) ? 1u : 0u);
-      if (cx > 1)
-        mma_commit_mc(&empty[s], cmask);
+      const int nk = min(kFwdKpb, kb1 - (kb0 + st * kFwdKpb));
+      for (int b = 0; b < nk; ++b)
+        mma_tf32(acc, sdesc(sa + b * A_KB + q * 32, 16, 1024), sdesc(sb + b * B_KB + q * 32, 16, 1024), idesc,
+                 (st | b) ? 1u : 0u);
+      if (cxn > 1)
+        mma_commit_mc(&empty[s], mmask);
       else
         mma_commit(&empty[s]);
     }
     mma_commit(&done);
   }
   __syncwarp();
-  // epilogue: thread <-> row i (TMEM lane 32*(warp%4) + lane); warp/4 picks 16 of the CTA's 32 negatives
+  // epilogue: thread <-> row i (TMEM lane 32*(warp%4) + lane); warp/4 = hf picks 8 of the kHalf finalised columns
+  // and 8 of the kHalf columns sent to the peer
   const int lg = warp & 3, hf = warp >> 2;
-  const int i = i0 + lg * 32 + lane;
+  const int rl = lg * 32 + lane, i = i0 + rl;
   const bool iok = i < dm.g;
   const float on = iok && FAM == FAM_L2 ? a.onorm[(int64_t)c * dm.g + i] : 0.f;  // loaded while the MMAs run
+  if (threadIdx.x < kHalf) {
+    const int jj = jf0 + threadIdx.x;
+    s_xn[threadIdx.x] = FAM == FAM_L2 && jj < dm.k ? a.xnorm[(int64_t)c * dm.k + jj] : 0.f;
+  }
   mbar_wait(&done, 0);
   tc_fence_after();
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 2);
-  const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
-  float v[16];
-  tmem_ld16(tmem + ((uint32_t)(lg * 32) << 16) + hf * 16, v);
-  trace_stamp(dm.trace, KGE_K_NEG_FWD, 3);
-  float lsum = 0.f, rsum = 0.f;
+  // own partial sums of the kept (kc) and sent (sc) column groups: ((p0 + p1) + p2) + p3
+  const int kc = ks * kHalf + hf * 8, sc = (1 - ks) * kHalf + hf * 8;
+  float v[8], w[8];
+  if (nst > 0) {
+    const uint32_t tl = tmem + ((uint32_t)(lg * 32) << 16);
+    tmem_ld8(tl + kc, v);
+    tmem_ld8(tl + sc, w);
 #pragma unroll
-  for (int jj = 0; jj < 16; ++jj) {
-    const int j = j0 + hf * 16 + jj;
+    for (int q = 1; q < kIssuers; ++q) {
+      float pv[8], pw[8];
+      tmem_ld8(tl + q * kNT + kc, pv);
+      tmem_ld8(tl + q * kNT + sc, pw);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] += pv[u];
+        w[u] += pw[u];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = w[u] = 0.f;
+  }
+  {  // send: the peer's xch[row][hf * 8 ..] (its kept columns are our sent ones)
+    const uint32_t dst = mapa_shared(smem_u32(xch + rl * kHalf + hf * 8), crank ^ 1u);
+    st_cluster_v4(dst, w[0], w[1], w[2], w[3]);
+    st_cluster_v4(dst + 16, w[4], w[5], w[6], w[7]);
+  }
+  cluster_sync();  // release our stores / acquire the peer's
+  {
+    const float4 x0 = *reinterpret_cast<const float4*>(xch + rl * kHalf + hf * 8);
+    const float4 x1 = *reinterpret_cast<const float4*>(xch + rl * kHalf + hf * 8 + 4);
+    const float xp[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = ks == 0 ? v[u] + xp[u] : xp[u] + v[u];  // always P0 + P1
+  }
+  trace_stamp(dm.trace, KGE_K_NEG_FWD, 3);
+  const float inv_bk = a.inv_bk;
+  float lsum = 0.f, rsum = 0.f, lprod = 1.f;
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = jf0 + hf * 8 + jj;
     float coef = 0.f;
     if (iok && j < dm.k) {
       float f, rD = 1.f;
       if (FAM == FAM_DOT) {
         f = v[jj];
       } else {  // TransE-L2 by expansion, clamped at 0 before the root (reading c.8)
-        const float D2 = fmaxf(on - 2.f * v[jj] + s_xn[hf * 16 + jj], 0.f);
+        const float D2 = fmaxf(on - 2.f * v[jj] + s_xn[hf * 8 + jj], 0.f);
         rD = fminf(rsqrtf(D2), 1e12f);
         f = dm.gamma - D2 * rD;
       }
-      // e = exp(-|f|): sigma(f) = f>=0 ? 1/(1+e) : e/(1+e);  -log sigma(-f) = max(f,0) + log1p(e)
+      // e = exp(-|f|): sigma(f) = f>=0 ? 1/(1+e) : e/(1+e);  -log sigma(-f) = max(f,0) + log1p(e). Three MUFU ops
+      // per element (rsqrt, ex2, rcp): the log1p terms are summed as one log of their product (each factor in (1, 2],
+      // 8 factors: no overflow; relative error ~8 ulp of the product, far inside the TC path's 2e-3)
       const float e = __expf(-fabsf(f));
-      const float r1 = __fdividef(1.f, 1.f + e);
-      lsum += fmaxf(f, 0.f) + __logf(1.f + e);
+      float r1;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(1.f + e));
+      lsum += fmaxf(f, 0.f);
+      lprod *= 1.f + e;
       const float dLdf = (f >= 0.f ? r1 : e * r1) * inv_bk;
       coef = FAM == FAM_DOT ? dLdf : -dLdf * rD;
     }
     v[jj] = coef;
     rsum += coef;
   }
+  lsum += __logf(lprod);
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 4);
   if (iok) {
-    float* wrow = a.W + ((int64_t)c * dm.g + i) * a.kp + j0 + hf * 16;
-    if (j0 + hf * 16 + 16 <= dm.k && (a.kp & 3) == 0) {
+    float* wrow = a.W + ((int64_t)c * dm.g + i) * a.kp + jf0 + hf * 8;
+    if (jf0 + hf * 8 + 8 <= dm.k && (a.kp & 3) == 0) {
       float4* dst = reinterpret_cast<float4*>(wrow);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+      dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+      dst[1] = make_float4(v[4], v[5], v[6], v[7]);
     } else {
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj)  // static indices keep v[] in registers
-        if (j0 + hf * 16 + jj < dm.k) wrow[jj] = v[jj];
+      for (int jj = 0; jj < 8; ++jj)  // static indices keep v[] in registers
+        if (jf0 + hf * 8 + jj < dm.k) wrow[jj] = v[jj];
     }
-    if (FAM == FAM_L2) a.rowsum_part[((int64_t)c * dm.g + i) * a.nrp + 2 * blockIdx.x + hf] = rsum;
   }
   if (FAM == FAM_L2) {
-    // column sums over this warp's 32 rows for its 16 columns: transposing butterfly (fixed order) over the low 4
-    // lane bits, then the two 16-lane halves are added; lane l (< 16) ends with column l
+    s_rs[hf][rl] = rsum;
+    // column sums over this warp's 32 rows for its 8 columns: transposing butterfly (fixed order) over the low 3
+    // lane bits, then the four 8-lane groups are added; lane l (< 8) ends with column l
 #pragma unroll
-    for (int off = 8; off >= 1; off >>= 1) {
+    for (int off = 4; off >= 1; off >>= 1) {
 #pragma unroll
       for (int q = 0; q < off; ++q) {
         const bool upper = (lane & off) != 0;
@@ -228,25 +295,33 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
       }
     }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 8);
     v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
-    if (lane < 16) s_col[lg][hf * 16 + lane] = v[0];
+    if (lane < 8) s_col[lg][hf * 8 + lane] = v[0];
   }
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 5);
   lsum = warp_sum(lsum);
   if (lane == 0) s_red[warp] = lsum;
   tc_fence_before();
   __syncthreads();
-  if (FAM == FAM_L2 && threadIdx.x < kNT && j0 + (int)threadIdx.x < dm.k)
-    a.colsum_part[((int64_t)c * dm.k + j0 + threadIdx.x) * a.ncp + blockIdx.y] =
-        ((s_col[0][threadIdx.x] + s_col[1][threadIdx.x]) + s_col[2][threadIdx.x]) + s_col[3][threadIdx.x];
+  if (FAM == FAM_L2) {
+    if (threadIdx.x < 128 && i0 + (int)threadIdx.x < dm.g)  // one row-sum partial per (row, half tile): 16 columns
+      a.rowsum_part[((int64_t)c * dm.g + i0 + threadIdx.x) * a.nrp + blockIdx.x] =
+          s_rs[0][threadIdx.x] + s_rs[1][threadIdx.x];
+    if (threadIdx.x >= 128 && threadIdx.x < 128 + kHalf && jf0 + (int)threadIdx.x - 128 < dm.k) {
+      const int u = threadIdx.x - 128;
+      a.colsum_part[((int64_t)c * dm.k + jf0 + u) * a.ncp + blockIdx.y] =
+          ((s_col[0][u] + s_col[1][u]) + s_col[2][u]) + s_col[3][u];
+    }
+  }
   if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < 8; ++w) t += s_red[w];
-    a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    float tt = 0.f;
+    for (int w8 = 0; w8 < 8; ++w8) tt += s_red[w8];
+    a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = tt;
   }
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 6);
-  if (cx > 1) cluster_sync();  // no CTA leaves while a peer's MMA commit may still arrive on its barriers
-  if (warp == 0) tmem_dealloc(tmem, 32);
+  if (cxn > 1) cluster_sync();  // no CTA leaves while a peer's MMA commit may still arrive on its barriers
+  if (warp == 0) tmem_dealloc(tmem, kIssuers * kNT);
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 7);
 }
 
@@ -287,13 +362,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kBwdStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kIssuers);
     }
-    mbar_init(&done, 1);
+    mbar_init(&done, kIssuers);
     mbar_init(&selfbar, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(&tbase, 128);
+  if (warp == 0) tmem_alloc(&tbase, kIssuers * 128);
   pdl_wait();  // predecessor (forward) complete: W and the row / column partial sums are final
   pdl_trigger();
   tc_fence_before();
@@ -322,23 +397,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int b = 0; b < nb; ++b) tma_load_3d(sb + b * 4096, &mO_MN, &full[s], (b0 + b) * 32, kb * 32, c);
       }
     }
-  } else if (warp == 1 && lane == 0) {  // MMA issuer
+  } else if (warp >= 4 && lane == 0) {
+    // MMA issuers (see k_tc_fwd): issuer q takes the K = 8 slice q of every k-block into TMEM columns [128 q, +nb*32)
+    const int q = warp - 4;
     const uint32_t idesc = idesc_tf32(128, nb * 32, pass_x, true);
+    const uint32_t acc = tmem + (uint32_t)(q * 128);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kBwdStages;
       mbar_wait(&full[s], (kb / kBwdStages) & 1);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const uint64_t ad = pass_x ? sdesc_mn(sa + kk * 1024, 4096) : sdesc(sa + kk * 32, 16, 1024);
-        mma_tf32(tmem, ad, sdesc_mn(sb + kk * 1024, 4096), idesc, (kb | kk) ? 1u : 0u);
-      }
+      const uint64_t ad = pass_x ? sdesc_mn(sa + q * 1024, 4096) : sdesc(sa + q * 32, 16, 1024);
+      mma_tf32(acc, ad, sdesc_mn(sb + q * 1024, 4096), idesc, kb ? 1u : 0u);
       mma_commit(&empty[s]);
     }
     mma_commit(&done);
   }
   __syncwarp();
+  if (warp < 4) {  // epilogue warps: TMEM lane quarter = warp
   // epilogue prologue while the MMAs run: row r (TMEM lane 32*warp + lane) and its correction factor,
   // rowsum(W) for dO, colsum(W) for dX' -- partials summed in a fixed order
   const int r = r0 + warp * 32 + lane;
@@ -425,6 +501,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int e0 = (b0 + b) * 32;
     float v[32];
     tmem_ld32(trow + b * 32, v);
+#pragma unroll
+    for (int q = 1; q < kIssuers; ++q) {  // ((p0 + p1) + p2) + p3: fixed order, deterministic
+      float p1[32];
+      tmem_ld32(trow + q * 128 + b * 32, p1);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) v[u] += p1[u];
+    }
     if (e0 >= d) continue;
     const int ne = min(32, d - e0);
     uint8_t* buf = stg + (b & 1) * 12288;
@@ -481,11 +564,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (b == 0) trace_stamp(dm.trace, KGE_K_NEG_BWD, 4);
   }
   if (wtma && lane == 0) bulk_wait_all();
+  }  // epilogue warps
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 5);
   tc_fence_before();
   __syncthreads();
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 6);
-  if (warp == 0) tmem_dealloc(tmem, 128);
+  if (warp == 0) tmem_dealloc(tmem, kIssuers * 128);
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 7);
 }
 
@@ -523,7 +607,22 @@ static bool make_map(CUtensorMap* m, const float* base, int cols, int rows, int 
              sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static size_t fwd_smem() { return (size_t)kFwdStages * (128 * 128 + kNT * 128) + 1024; }
+// 4D map over a [chunks x rows x cols] fp32 buffer seen as {32 (col in k-block), rows, k-blocks, chunks}: one box of
+// {32, box_rows, box_kb} lands as box_kb consecutive [box_rows x 128 B] SW128 k-block tiles
+static bool make_map4(CUtensorMap* m, const float* base, int cols, int rows, int chunks, int pitch, int box_rows,
+                      int box_kb) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {32, (cuuint64_t)rows, (cuuint64_t)(cols / 32), (cuuint64_t)chunks};
+  cuuint64_t strides[3] = {(cuuint64_t)pitch * 4, 128, (cuuint64_t)pitch * 4 * rows};
+  cuuint32_t box[4] = {32, (cuuint32_t)box_rows, (cuuint32_t)box_kb, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+static size_t fwd_smem() { return (size_t)kFwdStages * kFwdKpb * (128 * 128 + kNT * 128) + 128 * (kNT / 2) * 4 + 1024; }
 static size_t bwd_smem(int dp) {
   const int nb_max = (dp / 32 + kNSplit - 1) / kNSplit;
   return std::max((size_t)kBwdStages * (128 * 128 + (size_t)nb_max * 4096), (size_t)kBwdStaging) +
@@ -538,9 +637,13 @@ bool tc_init(kge_handle* h) {
   const StepBuffers& b = h->buf;
   bool ok = true;
   const int fx = (dm.k + kNT - 1) / kNT;
-  st->fwd_cx = fx % 8 == 0 ? 8 : fx % 4 == 0 ? 4 : fx % 2 == 0 ? 2 : 1;
+  // O multicast across cxn = kFwdKpb tiles (clusters of 8 CTAs) is off by default: measured on the Freebase step, the
+  // 8-CTA clusters wait for room in one GPC while the gather kernel drains, which costs more than the L2 reads saved
+  // (37.3 vs 42.8 us per step); KGE_FWD_MC=1 turns it on for experiments
+  st->fwd_cx = getenv("KGE_FWD_MC") && fx % kFwdKpb == 0 ? kFwdKpb : 1;
   ok &= make_map(&st->mO_K, b.O, h->dp, dm.g, dm.C, h->dp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_map(&st->mO_F, b.O, h->dp, dm.g, dm.C, h->dp, 128 / st->fwd_cx, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map4(&st->mO_F, b.O, h->dp, dm.g, dm.C, h->dp, 128, st->fwd_cx > 1 ? 1 : kFwdKpb);
+  ok &= make_map4(&st->mX_F, b.X, h->dp, dm.k, dm.C, h->dp, kNT, kFwdKpb);
   ok &= make_map(&st->mX_K, b.X, h->dp, dm.k, dm.C, h->dp, kNT, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mW_K, b.W, dm.k, dm.g, dm.C, h->kp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mX_MN, b.X, h->dp, dm.k, dm.C, h->dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
@@ -583,7 +686,7 @@ bool tc_supported(const kge_handle* h) { return h->tc && static_cast<const TcSta
 
 int32_t tc_neg_parts(const kge_handle* h) {
   const Dims& dm = h->dims;
-  return dm.C * ((dm.g + 127) / 128) * ((dm.k + kNT - 1) / kNT);
+  return dm.C * ((dm.g + 127) / 128) * ((dm.k + kNT - 1) / kNT) * 2;  // one loss partial per split-K half
 }
 
 bool tc_fuses_chain(const kge_handle* h) { return h->dims.model == KGE_TRANSE_L2; }
@@ -594,15 +697,15 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
   TcArgs a{dm, h->dp, h->kp, h->buf.O, h->buf.X, h->buf.onorm, h->buf.xnorm, h->buf.W, h->buf.lneg, h->buf.dO,
            h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128,
            tc_fuses_chain(h) ? 1 : 0, s, h->rows, h->buf.wpos, h->buf.pstat, h->buf.lpos, h->buf.Grel,
-           h->buf.loss, h->buf.flags, loss_slot, h->n_neg_parts, st->fwd_cx};
-  dim3 gf((dm.k + kNT - 1) / kNT, (dm.g + 127) / 128, dm.C);
+           h->buf.loss, h->buf.flags, loss_slot, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->fwd_cx};
+  dim3 gf(2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128, dm.C);  // x = 2 tile + split-K half
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(tiles * kNSplit, dm.C, 2);
   launch_begin(h, KGE_K_NEG_FWD);
   if (dm.family == FAM_DOT)
-    launch_pdl_cluster(k_tc_fwd<FAM_DOT>, gf, kFwdThreads, fwd_smem(), h->stream, st->fwd_cx, st->mO_F, st->mX_K, a);
+    launch_pdl_cluster(k_tc_fwd<FAM_DOT>, gf, kFwdThreads, fwd_smem(), h->stream, 2 * st->fwd_cx, st->mO_F, st->mX_F, a);
   else
-    launch_pdl_cluster(k_tc_fwd<FAM_L2>, gf, kFwdThreads, fwd_smem(), h->stream, st->fwd_cx, st->mO_F, st->mX_K, a);
+    launch_pdl_cluster(k_tc_fwd<FAM_L2>, gf, kFwdThreads, fwd_smem(), h->stream, 2 * st->fwd_cx, st->mO_F, st->mX_F, a);
   launch_end(h, KGE_K_NEG_FWD);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

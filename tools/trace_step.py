@@ -13,9 +13,13 @@ cfg = kge.Config(model="transe_l2", n_entities=gr.n_entities, n_relations=gr.n_r
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
     h = kge.init(cfg, *trip, stream=s)
-h.train_step(70, return_loss=False)
-h.sync()
-h.train_step(1, return_loss=False)
+steady = "steady" in sys.argv  # steady: the traced step is the last of a back-to-back run (host far ahead)
+if steady:
+    h.train_step(71, return_loss=False)
+else:
+    h.train_step(70, return_loss=False)
+    h.sync()
+    h.train_step(1, return_loss=False)
 h.sync()
 L = kge.lib()
 L.kge_debug_trace.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]
