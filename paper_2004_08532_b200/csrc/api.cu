@@ -273,7 +273,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   h->k0 = (uint32_t)cfg->seed;
   h->k1 = (uint32_t)(cfg->seed >> 32);
   dm.dp = ((dm.d + 2 + 31) / 32) * 32;  // O / X' pitch: room for the ones columns at d, d+1 (tc.cu)
-  dm.kp = ((dm.k + 3) / 4) * 4;        // W pitch (16-byte rows for TMA)
+  dm.kp = ((dm.k + 31) / 32) * 32;     // W pitch: whole 32-float k-blocks (tc.cu 4D maps; the pad stays zero)
   h->dp = dm.dp;
   h->kp = dm.kp;
   h->n_pad = 64;  // the sampler's warp-level sort stages work on 64-key blocks

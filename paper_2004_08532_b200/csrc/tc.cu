@@ -27,13 +27,14 @@ namespace kge {
 using namespace tc;
 
 struct TcState {
-  CUtensorMap mO_K, mX_K;    // O (K-major, SW128), box {32, 128}; fwd X' operand, box {32, NT}
+  CUtensorMap mO_E;          // dO epilogue operand (O rows, 4D K-major SW128), box {32, 64, 4}
   CUtensorMap mO_F;          // fwd O operand (4D {32, rows, k-blocks, chunk}): box {32, 128, 1 (cx > 1) | kFwdKpb}
   CUtensorMap mX_F;          // fwd X' operand (4D): box {32, kNT, kFwdKpb}
   CUtensorMap mW_K;          // dO operand A (K-major), box {32, 128}
   CUtensorMap mX_MN, mO_MN;  // B operands of dO / dX' (MN-major, 128B_ATOM_32B), box {32, 32}
   CUtensorMap mW_MN;         // A operand of dX' (MN-major), box {32, 32}
-  CUtensorMap mX_E;          // dX' epilogue operand (X' rows, K-major SW128), box {32, 128}
+  CUtensorMap mX_E;          // dX' epilogue operand (X' rows, 4D K-major SW128), box {32, 64, 4}
+  float4* xbuf = nullptr;    // split-K exchange of the backward pairs (L2-resident scratch)
   CUtensorMap mG_S, mR_S, mD_S;
   int fwd_cx = 1;  // backward TMA-store targets: Gocc, Grel, dO (SW128), box {32, 32}
   bool ok = false;
@@ -43,11 +44,12 @@ constexpr int kNT = 32;         // negatives per forward CTA
 constexpr int kIssuers = 4;     // MMA-issuing threads per CTA (one per K = 8 slice of a 32-float k-block)
 constexpr int kFwdKpb = 4;      // forward: k-blocks (32 floats of K) per pipeline stage = per TMA instruction
 constexpr int kFwdStages = 2;   // forward stages of kFwdKpb k-blocks (A 64 KB + B 16 KB each)
-constexpr int kBwdStages = 5;
+constexpr int kBwdKpb = 2;      // backward: k-blocks per stage (one 4D box per operand)
+constexpr int kBwdStages = 2;   // stages of kBwdKpb k-blocks: each split-K half (K = 128) is exactly two
 constexpr int kNSplit = 4;      // column ranges of dp per backward tile
-constexpr uint32_t kBwdStaging = 4 * 24576;  // backward epilogue store staging (reuses the pipeline stages)
-constexpr int kThreads = 256;   // backward: warps 0-3 = epilogue (TMEM lane quarters; warp 0 lane 0 also the TMA
-                                // producer), lane 0 of warps 4-7 = the kIssuers MMA issuers
+constexpr int kThreads = (9 + 4) * 32;  // backward: warps 0-7 = finalise (they alone run the prologue loads, so no
+                                       // role thread waits at a reconvergence point behind a load), lane 0 of warp 8
+                                       // = TMA producer, lane 0 of warps 9-12 = the kIssuers MMA issuers
 static_assert(kIssuers == 4, "the epilogues add exactly four partial accumulators");
 constexpr int kFwdThreads = 256;  // forward: 8 epilogue warps (two per TMEM lane quarter, 16 negatives each) so the
                                   // transcendental chains of the loss epilogue have latency hiding
@@ -79,6 +81,7 @@ struct TcArgs {
   int32_t* flags;
   int32_t loss_slot, n_neg_parts;
   float inv_bk;    // 1 / (B k), the dL/df- scale (reading c.9)
+  float4* xbuf;    // backward split-K exchange scratch
   int32_t fwd_cx;  // forward cluster size along x: the CTAs of one 128-positive tile share its O tile by TMA multicast
 };
 
@@ -327,7 +330,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
 // ------------------------------------------------------------------------------------------------
 // backward: z = 0 -> dO tile (128 positives of chunk y), z = 1 -> dX' tile (128 negatives of chunk y);
-// blockIdx.x = (row tile, column part)
+// blockIdx.x = 2 (row tile * kNSplit + column part) + ks. Split-K pair (cluster of 2): ks = 0 / 1 contracts the first /
+// second half of K; each CTA then hands the peer the 64 rows the peer finalises (through L2, coalesced float4 columns)
+// and finalises its own 64 rows of the 128 x (nb * 32) tile -- the sum is always P0 + P1.
 // ------------------------------------------------------------------------------------------------
 template <int FAM>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -344,21 +349,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool pass_x = blockIdx.z == 1;
-  const int c = blockIdx.y, part = blockIdx.x % kNSplit, r0 = (blockIdx.x / kNSplit) * 128;
+  const int ks = blockIdx.x & 1, tp = blockIdx.x >> 1;
+  const int c = blockIdx.y, part = tp % kNSplit, r0 = (tp / kNSplit) * 128;
   const int nrows = pass_x ? dm.k : dm.g;
   const int nb_all = a.dp / 32;
   const int b0 = part * nb_all / kNSplit, b1 = (part + 1) * nb_all / kNSplit;  // this CTA's column blocks
   const int nb = b1 - b0;
-  if (r0 >= nrows || nb == 0 || b0 * 32 >= dm.d) {  // uniform per CTA, before any barrier / TMEM use
+  if (r0 >= nrows || nb == 0 || b0 * 32 >= dm.d) {  // uniform per CTA pair, before any barrier / TMEM use
     pdl_trigger();
     return;
   }
   const int nk = pass_x ? dm.g : dm.k;  // contraction length
-  const int nkb = (nk + 31) / 32;
-  const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)nb * 4096;
-  // epilogue operand (L2): this CTA's rows x column blocks of O (dO) or X' (dX'), TMA'd at the start so the load
-  // overlaps the main loop; block b at self_smem + b * 16 KB, 128-byte rows, 16-byte chunks swizzled by (row % 8)
-  uint8_t* self_smem = smem + max(kBwdStages * STAGE, kBwdStaging);
+  const int nkb = (nk + 31) / 32, kh = (nkb + 1) / 2;
+  const int kb0 = ks ? kh : 0, kb1 = ks ? nkb : kh;
+  const int nst = (kb1 - kb0 + kBwdKpb - 1) / kBwdKpb;
+  constexpr uint32_t A_BYTES = kBwdKpb * 16384, B_BYTES = kBwdKpb * 4 * 4096, STAGE = A_BYTES + B_BYTES;
+  constexpr uint32_t KROWS_B = kBwdKpb * 32 * 128;  // bytes between 32-column blocks of an MN-major stage operand
+  // shared memory: [stages][self: this CTA's 64 finalised rows x 4 column blocks of O (dO) / X' (dX'), SW128]
+  // after the main loop the stage area holds xown ([32 float4 columns][64 rows]) and the TMA-store staging
+  uint8_t* self_smem = smem + kBwdStages * STAGE;
+  float4* xown = reinterpret_cast<float4*>(smem);
+  uint8_t* stg = smem + 32768 + warp * 12288;  // 3 tiles x 4 KB per warp
+  const int rfin0 = ks * 64;                    // first tile row this CTA finalises
   if (threadIdx.x == 0) {
     for (int s = 0; s < kBwdStages; ++s) {
       mbar_init(&full[s], 1);
@@ -377,65 +389,56 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tbase;
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 1);
 
-  if (warp == 0 && lane == 0) {  // TMA producer
-    if (FAM == FAM_L2) {
-      mbar_arrive_expect_tx(&selfbar, (uint32_t)nb * 16384);
-      for (int b = 0; b < nb; ++b)
-        tma_load_3d(self_smem + b * 16384, pass_x ? &mX_E : &mO_E, &selfbar, (b0 + b) * 32, r0, c);
-    }
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kBwdStages;
-      if (kb >= kBwdStages) mbar_wait(&empty[s], ((kb / kBwdStages) - 1) & 1);
-      uint8_t* sa = smem + s * STAGE;
-      uint8_t* sb = sa + A_BYTES;
-      mbar_arrive_expect_tx(&full[s], STAGE);
-      if (!pass_x) {
-        tma_load_3d(sa, &mW_K, &full[s], kb * 32, r0, c);  // W[i0.., j-block]
-        for (int b = 0; b < nb; ++b) tma_load_3d(sb + b * 4096, &mX_MN, &full[s], (b0 + b) * 32, kb * 32, c);
-      } else {
-        for (int b = 0; b < 4; ++b) tma_load_3d(sa + b * 4096, &mW_MN, &full[s], r0 + b * 32, kb * 32, c);
-        for (int b = 0; b < nb; ++b) tma_load_3d(sb + b * 4096, &mO_MN, &full[s], (b0 + b) * 32, kb * 32, c);
-      }
-    }
-  } else if (warp >= 4 && lane == 0) {
-    // MMA issuers (see k_tc_fwd): issuer q takes the K = 8 slice q of every k-block into TMEM columns [128 q, +nb*32)
-    const int q = warp - 4;
-    const uint32_t idesc = idesc_tf32(128, nb * 32, pass_x, true);
-    const uint32_t acc = tmem + (uint32_t)(q * 128);
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kBwdStages;
-      mbar_wait(&full[s], (kb / kBwdStages) & 1);
-      tc_fence_after();
-      const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
-      const uint64_t ad = pass_x ? sdesc_mn(sa + q * 1024, 4096) : sdesc(sa + q * 32, 16, 1024);
-      mma_tf32(acc, ad, sdesc_mn(sb + q * 1024, 4096), idesc, kb ? 1u : 0u);
-      mma_commit(&empty[s]);
-    }
-    mma_commit(&done);
-  }
-  __syncwarp();
-  if (warp < 4) {  // epilogue warps: TMEM lane quarter = warp
-  // epilogue prologue while the MMAs run: row r (TMEM lane 32*warp + lane) and its correction factor,
-  // rowsum(W) for dO, colsum(W) for dX' -- partials summed in a fixed order
-  const int r = r0 + warp * 32 + lane;
+  // ---- finalise prologue, issued before the main loop so its global loads (row / column partial sums of W, the
+  // positive's scale and the uncorrupted entity row) overlap the MMAs: warp w finalises rows rfin0 + 32 (w / 4) +
+  // lane of column block w % 4 ----
+  const int b = warp & 3, fr = (warp >> 2) * 32 + lane;
+  const int rl = rfin0 + fr, r = r0 + rl;
   const bool rok = r < nrows;
   const int d = dm.d;
-  float corr = 0.f;
-  if (FAM == FAM_L2 && rok) {
-    if (!pass_x) {
-      const float* rp = a.rowsum_part + ((int64_t)c * dm.g + r) * a.nrp;
-      for (int q = 0; q < a.nrp; ++q) corr += rp[q];
-    } else {
-      const float* cp = a.colsum_part + ((int64_t)c * dm.k + r) * a.ncp;
-      for (int q = 0; q < a.ncp; ++q) corr += cp[q];
-    }
-  }
   const bool fuse = FAM == FAM_L2 && a.fuse && !pass_x;
+  const int e0 = (b0 + b) * 32;
+  const bool bok = warp < 8 && b < nb && e0 < d;
+  // The loads are issued by every thread except the TMA producer and the MMA issuers, which run their loops first
+  // and load afterwards; the additions happen at finalise time so nothing here waits on a load.
+  const bool role = warp >= 8;
+  float4 cpart[4];  // rowsum(W) partials (nrp = 16 -> 4 float4) for dO, colsum(W) partials (ncp) for dX'
+  const int pi = c * dm.g + r;
+  int mode = 0;
+  float pscale = 0.f;
+  float4 xr[8];
+  auto prologue = [&]() {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cpart[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (FAM == FAM_L2 && rok && bok) {
+      const int np = pass_x ? a.ncp : a.nrp;
+      const float* pp = pass_x ? a.colsum_part + ((int64_t)c * dm.k + r) * a.ncp
+                               : a.rowsum_part + ((int64_t)c * dm.g + r) * a.nrp;
+      if (np == 16) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cpart[q] = __ldcg(reinterpret_cast<const float4*>(pp) + q);
+      } else {
+        float t = 0.f;
+        for (int q = 0; q < np; ++q) t += pp[q];
+        cpart[0].x = t;
+      }
+    }
+    // fused chain: positive i of this row; x = the uncorrupted "other" entity row (t for tail, h for head mode)
+    mode = fuse ? a.s.mode[c] : 0;
+    if (fuse && rok && bok) {
+      pscale = a.wpos[pi] / fmaxf(sqrtf(a.pstat[pi]), 1e-12f);
+      const float4* x4 = reinterpret_cast<const float4*>(a.ent.row(mode == 0 ? a.s.pt[pi] : a.s.ph[pi]) + e0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xr[u] = 4 * u < d - e0 ? __ldg(x4 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  if (!role) prologue();
+
   int loss_part = 0;  // the loss is reduced by the first CTA of (row tile 0, chunk 0) that has columns to process
   while (loss_part + 1 < kNSplit && ((loss_part + 1) * nb_all / kNSplit == loss_part * nb_all / kNSplit ||
                                      loss_part * nb_all / kNSplit * 32 >= d))
     ++loss_part;
-  if (fuse && blockIdx.x == loss_part && blockIdx.y == 0 && warp == 3) {
+  if (fuse && tp == loss_part && ks == 0 && blockIdx.y == 0 && warp == 1) {
     // deterministic loss (reading c.9): fixed lane assignment and order, identical to the unfused k_chain
     float sp = 0.f, sn = 0.f;
     for (int i = lane; i < dm.B; i += 32) sp += a.lpos[i];
@@ -450,83 +453,128 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (bad) a.flags[0] = 1;
     }
   }
-  // fused chain: positive i of this row; x = the uncorrupted "other" entity row (t for tail mode, h for head mode),
-  // prefetched for all column blocks while the MMAs run
-  const int pi = c * dm.g + r;
-  const int mode = fuse ? a.s.mode[c] : 0;
-  float pscale = 0.f;
-  float4 xr[4][8];
-  if (fuse && rok) {
-    pscale = a.wpos[pi] / fmaxf(sqrtf(a.pstat[pi]), 1e-12f);
-    const float* xrow = a.ent.row(mode == 0 ? a.s.pt[pi] : a.s.ph[pi]);
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int e0 = (b0 + b) * 32;
-      if (b < nb && e0 < d) {
-        const float4* x4 = reinterpret_cast<const float4*>(xrow + e0);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) xr[b][u] = 4 * u < d - e0 ? __ldg(x4 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+  if (warp == 8 && lane == 0) {  // TMA producer: one box per operand per stage
+    if (FAM == FAM_L2) {
+      mbar_arrive_expect_tx(&selfbar, 4 * 8192);
+      tma_load_4d(self_smem, pass_x ? &mX_E : &mO_E, &selfbar, 0, r0 + rfin0, b0, c);
     }
+    for (int q = 0; q < nst; ++q) {
+      const int s = q % kBwdStages;
+      if (q >= kBwdStages) mbar_wait(&empty[s], ((q / kBwdStages) - 1) & 1);
+      uint8_t* sa = smem + s * STAGE;
+      uint8_t* sb = sa + A_BYTES;
+      const int kq = kb0 + q * kBwdKpb;
+      mbar_arrive_expect_tx(&full[s], STAGE);
+      if (!pass_x)
+        tma_load_4d(sa, &mW_K, &full[s], 0, r0, kq, c);  // W[rows, k-blocks kq..]: [kb][128 rows][128 B]
+      else
+        tma_load_4d(sa, &mW_MN, &full[s], 0, kq * 32, r0 / 32, c);  // W^T: [4 j-blocks][K rows][128 B]
+      tma_load_4d(sb, pass_x ? &mO_MN : &mX_MN, &full[s], 0, kq * 32, b0, c);  // [4 col blocks][K rows][128 B]
+    }
+  } else if (warp >= 9 && lane == 0) {
+    // MMA issuers (see k_tc_fwd): issuer q takes the K = 8 slice q of every k-block into TMEM columns [128 q, +nb*32)
+    const int q = warp - 9;
+    const uint32_t idesc = idesc_tf32(128, nb * 32, pass_x, true);
+    const uint32_t acc = tmem + (uint32_t)(q * 128);
+    for (int st = 0; st < nst; ++st) {
+      const int s = st % kBwdStages;
+      mbar_wait(&full[s], (st / kBwdStages) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
+      const int nkq = min(kBwdKpb, kb1 - (kb0 + st * kBwdKpb));
+      for (int b = 0; b < nkq; ++b) {
+        const uint32_t koff = (uint32_t)(b * 32 + q * 8) * 128;  // K rows of an MN-major operand
+        const uint64_t ad = pass_x ? sdesc_mn(sa + koff, KROWS_B) : sdesc(sa + b * 16384 + q * 32, 16, 1024);
+        mma_tf32(acc, ad, sdesc_mn(sb + koff, KROWS_B), idesc, (st | b) ? 1u : 0u);
+      }
+      mma_commit(&empty[s]);
+    }
+    mma_commit(&done);
   }
-  // output tiles of this warp's 32 rows: t = 0 the primary (dO | dX' | fused: gradient of the combined entity),
-  // fused only: t = 1 gradient of the other entity, t = 2 relation gradient. Full 32-row warps stage each
-  // 32 x 32 tile in (free) pipeline shared memory in the SW128 layout and TMA-store it (coalesced, asynchronous);
-  // a ragged warp (chunk shorter than its rows) stores its valid rows directly.
-  const int wrow0 = r0 + warp * 32;
-  const bool wtma = wrow0 + 32 <= nrows;
-  const int ntile = fuse ? 3 : 1;
-  const CUtensorMap* tmap0 = pass_x || fuse ? &mG_S : &mD_S;
-  int trow0[3];
-  trow0[0] = pass_x ? 2 * dm.B + c * dm.k + wrow0 : (fuse && mode == 1 ? dm.B : 0) + c * dm.g + wrow0;
-  trow0[1] = (mode == 0 ? dm.B : 0) + c * dm.g + wrow0;
-  trow0[2] = c * dm.g + wrow0;
-  float* gdst[3];
-  gdst[0] = pass_x ? a.Gocc + ((int64_t)2 * dm.B + (int64_t)c * dm.k + r) * d
-                   : fuse ? a.Gocc + ((int64_t)(mode == 0 ? 0 : dm.B) + pi) * d : a.dO + (int64_t)pi * d;
-  gdst[1] = a.Gocc + ((int64_t)(mode == 0 ? dm.B : 0) + pi) * d;
-  gdst[2] = a.Grel + (int64_t)pi * dm.drel;
-  const float rsign = mode == 0 ? 1.f : -1.f;
-  uint8_t* stg = smem + warp * 24576;  // 2 buffers x 3 tiles x 4 KB per warp (the MMAs are done with this memory)
+  __syncwarp();
+  // ---- partial sums out of TMEM: warp w reads lane quarter w % 4, column blocks 2 (w / 4) + {0, 1} ----
+  const int pair = tp + (gridDim.x >> 1) * (c + gridDim.y * blockIdx.z);
+  float4* xsend = a.xbuf + ((int64_t)pair * 2 + ks) * (32 * 64);  // [32 float4 columns][64 rows] for the peer
+  const float4* xpeer = a.xbuf + ((int64_t)pair * 2 + (1 - ks)) * (32 * 64);
   mbar_wait(&done, 0);
   tc_fence_after();
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 2);
-  if (FAM == FAM_L2) mbar_wait(&selfbar, 0);
+  if (warp < 8) {
+    const int lq = warp & 3, rl = lq * 32 + lane;
+    const bool mine = (rl >> 6) == ks;
+    const int fr = rl & 63;
+    const uint32_t trow = tmem + ((uint32_t)(lq * 32) << 16);
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) {
+      const int b = (warp >> 2) * 2 + bb;
+      if (b >= nb) break;
+      float v[32];
+      if (nst > 0) {
+        tmem_ld32(trow + b * 32, v);
+#pragma unroll
+        for (int q = 1; q < kIssuers; ++q) {  // ((p0 + p1) + p2) + p3: fixed order, deterministic
+          float p1[32];
+          tmem_ld32(trow + q * 128 + b * 32, p1);
+#pragma unroll
+          for (int u = 0; u < 32; ++u) v[u] += p1[u];
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 32; ++u) v[u] = 0.f;
+      }
+      float4* dst = mine ? xown : xsend;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        dst[(b * 8 + u) * 64 + fr] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();  // xown complete
+  cluster_sync();   // release xsend (global, cluster scope) / acquire the peer's
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 3);
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  const int rl = warp * 32 + lane;  // row within the tile
+
+  // ---- finalise ----
+  if (bok) {
+    // correction factor: the rowsum / colsum partials of W added in a fixed order
+    float corr = cpart[0].x;
+    if (FAM == FAM_L2 && (pass_x ? a.ncp : a.nrp) == 16) {
+      corr = 0.f;
 #pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    if (b >= nb) break;
-    const int e0 = (b0 + b) * 32;
-    float v[32];
-    tmem_ld32(trow + b * 32, v);
-#pragma unroll
-    for (int q = 1; q < kIssuers; ++q) {  // ((p0 + p1) + p2) + p3: fixed order, deterministic
-      float p1[32];
-      tmem_ld32(trow + q * 128 + b * 32, p1);
-#pragma unroll
-      for (int u = 0; u < 32; ++u) v[u] += p1[u];
+      for (int q = 0; q < 4; ++q) corr = (((corr + cpart[q].x) + cpart[q].y) + cpart[q].z) + cpart[q].w;
     }
-    if (e0 >= d) continue;
+    // output tiles of these 32 rows: t = 0 the primary (dO | dX' | fused: gradient of the combined entity),
+    // fused only: t = 1 gradient of the other entity, t = 2 relation gradient. Full 32-row warps stage each
+    // 32 x 32 tile in shared memory in the SW128 layout and TMA-store it; a ragged warp stores its valid rows directly.
+    const int wrow0 = r0 + rfin0 + (warp >> 2) * 32;
+    const bool wtma = wrow0 + 32 <= nrows;
     const int ne = min(32, d - e0);
-    uint8_t* buf = stg + (b & 1) * 12288;
-    if (wtma && b >= 2) {  // the buffer written two blocks ago must have been read by its TMA store
-      if (lane == 0) bulk_wait_read<1>();
-      __syncwarp();
-    }
+    int trow0[3];
+    trow0[0] = pass_x ? 2 * dm.B + c * dm.k + wrow0 : (fuse && mode == 1 ? dm.B : 0) + c * dm.g + wrow0;
+    trow0[1] = (mode == 0 ? dm.B : 0) + c * dm.g + wrow0;
+    trow0[2] = c * dm.g + wrow0;
+    float* gdst[3];
+    gdst[0] = pass_x ? a.Gocc + ((int64_t)2 * dm.B + (int64_t)c * dm.k + r) * d
+                     : fuse ? a.Gocc + ((int64_t)(mode == 0 ? 0 : dm.B) + pi) * d : a.dO + (int64_t)pi * d;
+    gdst[1] = a.Gocc + ((int64_t)(mode == 0 ? dm.B : 0) + pi) * d;
+    gdst[2] = a.Grel + (int64_t)pi * dm.drel;
+    const float rsign = mode == 0 ? 1.f : -1.f;
+    if (FAM == FAM_L2) mbar_wait(&selfbar, 0);
     if (rok) {
-      const uint8_t* rowp = self_smem + b * 16384 + rl * 128;
+      const uint8_t* rowp = self_smem + b * 8192 + fr * 128;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        float4 t0 = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]), t1, t2;
+        const float4 po = xown[(b * 8 + u) * 64 + fr];
+        const float4 pp = __ldcg(xpeer + (b * 8 + u) * 64 + fr);
+        float4 t0 = ks == 0 ? make_float4(po.x + pp.x, po.y + pp.y, po.z + pp.z, po.w + pp.w)
+                            : make_float4(pp.x + po.x, pp.y + po.y, pp.z + po.z, pp.w + po.w);
+        float4 t1, t2;
         if (FAM == FAM_L2) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D)
-          const float4 sv = *reinterpret_cast<const float4*>(rowp + ((u ^ (rl & 7)) << 4));
+          const float4 sv = *reinterpret_cast<const float4*>(rowp + ((u ^ (fr & 7)) << 4));
           t0 = make_float4(corr * sv.x - t0.x, corr * sv.y - t0.y, corr * sv.z - t0.z, corr * sv.w - t0.w);
           if (fuse) {
             // go = dO + w+ df/do, gx = w+ df/dx; f = gamma - ||o - x||: go = dO - s u, gx = s u (u = o - x, s = w+/D)
             // tail (o = h + r): gH = go, gR = go, gT = gx ; head (o = t - r): gT = go, gR = -go, gH = gx
-            const float4 xv = xr[b][u];
+            const float4 xv = xr[u];
             t1 = make_float4(pscale * (sv.x - xv.x), pscale * (sv.y - xv.y), pscale * (sv.z - xv.z),
                              pscale * (sv.w - xv.w));
             t0 = make_float4(-t1.x + t0.x, -t1.y + t0.y, -t1.z + t0.z, -t1.w + t0.w);
@@ -535,10 +583,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (wtma) {
           const int off = lane * 128 + ((u ^ (lane & 7)) << 4);
-          *reinterpret_cast<float4*>(buf + off) = t0;
+          *reinterpret_cast<float4*>(stg + off) = t0;
           if (fuse) {
-            *reinterpret_cast<float4*>(buf + 4096 + off) = t1;
-            *reinterpret_cast<float4*>(buf + 8192 + off) = t2;
+            *reinterpret_cast<float4*>(stg + 4096 + off) = t1;
+            *reinterpret_cast<float4*>(stg + 8192 + off) = t2;
           }
         } else if (4 * u < ne) {
           reinterpret_cast<float4*>(gdst[0] + e0)[u] = t0;
@@ -549,22 +597,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    trace_stamp(dm.trace, KGE_K_NEG_BWD, 4);
     if (wtma) {
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        tma_store_3d(tmap0, buf, e0, trow0[0], 0);
-        if (ntile > 1) {
-          tma_store_3d(&mG_S, buf + 4096, e0, trow0[1], 0);
-          tma_store_3d(&mR_S, buf + 8192, e0, trow0[2], 0);
+        tma_store_3d(pass_x || fuse ? &mG_S : &mD_S, stg, e0, trow0[0], 0);
+        if (fuse) {
+          tma_store_3d(&mG_S, stg + 4096, e0, trow0[1], 0);
+          tma_store_3d(&mR_S, stg + 8192, e0, trow0[2], 0);
         }
         bulk_commit();
+        bulk_wait_all();
       }
     }
-    if (b == 0) trace_stamp(dm.trace, KGE_K_NEG_BWD, 4);
   }
-  if (wtma && lane == 0) bulk_wait_all();
-  }  // epilogue warps
   trace_stamp(dm.trace, KGE_K_NEG_BWD, 5);
   tc_fence_before();
   __syncthreads();
@@ -610,7 +657,7 @@ static bool make_map(CUtensorMap* m, const float* base, int cols, int rows, int 
 // 4D map over a [chunks x rows x cols] fp32 buffer seen as {32 (col in k-block), rows, k-blocks, chunks}: one box of
 // {32, box_rows, box_kb} lands as box_kb consecutive [box_rows x 128 B] SW128 k-block tiles
 static bool make_map4(CUtensorMap* m, const float* base, int cols, int rows, int chunks, int pitch, int box_rows,
-                      int box_kb) {
+                      int box_kb, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[4] = {32, (cuuint64_t)rows, (cuuint64_t)(cols / 32), (cuuint64_t)chunks};
@@ -618,21 +665,20 @@ static bool make_map4(CUtensorMap* m, const float* base, int cols, int rows, int
   cuuint32_t box[4] = {32, (cuuint32_t)box_rows, (cuuint32_t)box_kb, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
+             sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static size_t fwd_smem() { return (size_t)kFwdStages * kFwdKpb * (128 * 128 + kNT * 128) + 128 * (kNT / 2) * 4 + 1024; }
 static size_t bwd_smem(int dp) {
-  const int nb_max = (dp / 32 + kNSplit - 1) / kNSplit;
-  return std::max((size_t)kBwdStages * (128 * 128 + (size_t)nb_max * 4096), (size_t)kBwdStaging) +
-         (size_t)nb_max * 16384 + 1024;
+  (void)dp;
+  return (size_t)kBwdStages * kBwdKpb * (16384 + 4 * 4096) + 4 * 8192 + 1024;
 }
 
 bool tc_init(kge_handle* h) {
   const Dims& dm = h->dims;
   if (!(dm.family == FAM_DOT || dm.family == FAM_L2)) return false;
-  if (h->dp > 512 || bwd_smem(h->dp) > 227 * 1024) return false;
+  if (h->dp > 512 || bwd_smem(h->dp) > 227 * 1024 || (dm.dp / 32 + kNSplit - 1) / kNSplit > 4 || h->kp % 32)
+    return false;
   TcState* st = new TcState();
   const StepBuffers& b = h->buf;
   bool ok = true;
@@ -641,15 +687,17 @@ bool tc_init(kge_handle* h) {
   // 8-CTA clusters wait for room in one GPC while the gather kernel drains, which costs more than the L2 reads saved
   // (37.3 vs 42.8 us per step); KGE_FWD_MC=1 turns it on for experiments
   st->fwd_cx = getenv("KGE_FWD_MC") && fx % kFwdKpb == 0 ? kFwdKpb : 1;
-  ok &= make_map(&st->mO_K, b.O, h->dp, dm.g, dm.C, h->dp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map4(&st->mO_F, b.O, h->dp, dm.g, dm.C, h->dp, 128, st->fwd_cx > 1 ? 1 : kFwdKpb);
   ok &= make_map4(&st->mX_F, b.X, h->dp, dm.k, dm.C, h->dp, kNT, kFwdKpb);
-  ok &= make_map(&st->mX_K, b.X, h->dp, dm.k, dm.C, h->dp, kNT, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_map(&st->mW_K, b.W, dm.k, dm.g, dm.C, h->kp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_map(&st->mX_MN, b.X, h->dp, dm.k, dm.C, h->dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  ok &= make_map(&st->mO_MN, b.O, h->dp, dm.g, dm.C, h->dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  ok &= make_map(&st->mW_MN, b.W, dm.k, dm.g, dm.C, h->kp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  ok &= make_map(&st->mX_E, b.X, h->dp, dm.k, dm.C, h->dp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  // backward operands (4D {32, rows, 32-column blocks, chunk}): W K-major (dO's A), W / X' / O MN-major with K = rows
+  // (dX''s A and both B operands), and the epilogue rows of O / X' (64 finalised rows x 4 column blocks)
+  const CUtensorMapSwizzle mn = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+  ok &= make_map4(&st->mW_K, b.W, h->kp, dm.g, dm.C, h->kp, 128, kBwdKpb);
+  ok &= make_map4(&st->mW_MN, b.W, h->kp, dm.g, dm.C, h->kp, 32 * kBwdKpb, 4, mn);
+  ok &= make_map4(&st->mX_MN, b.X, h->dp, dm.k, dm.C, h->dp, 32 * kBwdKpb, 4, mn);
+  ok &= make_map4(&st->mO_MN, b.O, h->dp, dm.g, dm.C, h->dp, 32 * kBwdKpb, 4, mn);
+  ok &= make_map4(&st->mO_E, b.O, h->dp, dm.g, dm.C, h->dp, 64, 4);
+  ok &= make_map4(&st->mX_E, b.X, h->dp, dm.k, dm.C, h->dp, 64, 4);
   ok &= make_map(&st->mG_S, b.Gocc, dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mR_S, b.Grel, dm.drel, dm.B, 1, dm.drel, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mD_S, b.dO, dm.d, dm.B, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -672,12 +720,22 @@ bool tc_init(kge_handle* h) {
     delete st;
     return false;
   }
+  {
+    const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
+    const size_t pairs = (size_t)tiles * kNSplit * dm.C * 2;
+    if (cudaMalloc(&st->xbuf, pairs * 2 * 32 * 64 * sizeof(float4)) != cudaSuccess) {
+      cudaGetLastError();
+      delete st;
+      return false;
+    }
+  }
   st->ok = true;
   h->tc = st;
   return true;
 }
 
 void tc_destroy(kge_handle* h) {
+  if (h->tc && static_cast<TcState*>(h->tc)->xbuf) cudaFree(static_cast<TcState*>(h->tc)->xbuf);
   delete static_cast<TcState*>(h->tc);
   h->tc = nullptr;
 }
@@ -697,10 +755,10 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
   TcArgs a{dm, h->dp, h->kp, h->buf.O, h->buf.X, h->buf.onorm, h->buf.xnorm, h->buf.W, h->buf.lneg, h->buf.dO,
            h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128,
            tc_fuses_chain(h) ? 1 : 0, s, h->rows, h->buf.wpos, h->buf.pstat, h->buf.lpos, h->buf.Grel,
-           h->buf.loss, h->buf.flags, loss_slot, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->fwd_cx};
+           h->buf.loss, h->buf.flags, loss_slot, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->xbuf, st->fwd_cx};
   dim3 gf(2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128, dm.C);  // x = 2 tile + split-K half
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
-  dim3 gb(tiles * kNSplit, dm.C, 2);
+  dim3 gb(2 * tiles * kNSplit, dm.C, 2);  // x = 2 (row tile * kNSplit + column part) + split-K half
   launch_begin(h, KGE_K_NEG_FWD);
   if (dm.family == FAM_DOT)
     launch_pdl_cluster(k_tc_fwd<FAM_DOT>, gf, kFwdThreads, fwd_smem(), h->stream, 2 * st->fwd_cx, st->mO_F, st->mX_F, a);
@@ -711,11 +769,11 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
   if (e != cudaSuccess) return e;
   launch_begin(h, KGE_K_NEG_BWD);
   if (dm.family == FAM_DOT)
-    launch_pdl(k_tc_bwd<FAM_DOT>, gb, kThreads, bwd_smem(h->dp), h->stream, st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN,
-               st->mO_K, st->mX_E, st->mG_S, st->mR_S, st->mD_S, a);
+    launch_pdl_cluster(k_tc_bwd<FAM_DOT>, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN,
+                       st->mO_MN, st->mO_E, st->mX_E, st->mG_S, st->mR_S, st->mD_S, a);
   else
-    launch_pdl(k_tc_bwd<FAM_L2>, gb, kThreads, bwd_smem(h->dp), h->stream, st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN,
-               st->mO_K, st->mX_E, st->mG_S, st->mR_S, st->mD_S, a);
+    launch_pdl_cluster(k_tc_bwd<FAM_L2>, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN,
+                       st->mO_MN, st->mO_E, st->mX_E, st->mG_S, st->mR_S, st->mD_S, a);
   launch_end(h, KGE_K_NEG_BWD);
   return cudaGetLastError();
 }
