@@ -185,6 +185,8 @@ struct GatherArgs {
   const float* rel;
   StepBuffers b;
   int32_t first_row;  // B: negatives only (TransR handles its positives in transr.cu)
+  int32_t fuse_pos;   // TransE-L2 on the tcgen05 path: also write the positive-score gradient of the uncorrupted
+                      // entity, gx = w+ (o - x) / ||o - x||, into its occurrence row of Gocc (read back by k_tc_bwd)
 };
 
 // Register-staged rows: every lane issues all of its row loads before any arithmetic or store, so a warp has its whole
@@ -299,10 +301,64 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
   trace_stamp(dm.trace, KGE_K_GATHER, 0);
   pdl_wait();
   pdl_trigger();
+  trace_stamp(dm.trace, KGE_K_GATHER, 1);
   const int lane = threadIdx.x & 31;
   const int row = a.first_row + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int n_neg = dm.C * dm.k;
-  if (row < dm.B) {
+  if (row < dm.B && a.fuse_pos) {
+    // TransE-L2 (tail: o = h + r, x = t; head: o = t - r, x = h): o, its norm and pair statistic as below, plus
+    // gx = s (o - x), s = w+ / max(||o - x||, 1e-12) -- the positive term of the uncorrupted entity's gradient
+    // (reading c.10) -- written to that entity's occurrence row (t: B + i in tail mode, h: i in head mode)
+    const int i = row, mode = a.s.mode[i / dm.g];
+    const float* e = a.ent.row(mode == 0 ? a.s.ph[i] : a.s.pt[i]);
+    const float* x = a.ent.row(mode == 0 ? a.s.pt[i] : a.s.ph[i]);
+    const float* r = a.rel + (int64_t)a.s.pr[i] * dm.drel;
+    float* o = a.b.O + (int64_t)i * dm.dp;
+    const int d4 = dm.d >> 2;
+    Row4<V> X, R, Y;
+    X.load(e, lane, d4);
+    R.load(r, lane, d4);
+    Y.load(x, lane, d4);
+    float stat = 0.f, on = 0.f;
+#pragma unroll
+    for (int m = 0; m < V; ++m) {
+      const int q = lane + 32 * m;
+      if (q >= d4) continue;
+      float xv[4], rv[4], yv[4], ov[4];
+      f4_to(X.v[m], xv);
+      f4_to(R.v[m], rv);
+      f4_to(Y.v[m], yv);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ov[u] = mode == 0 ? xv[u] + rv[u] : xv[u] - rv[u];
+        on += ov[u] * ov[u];
+        const float df = ov[u] - yv[u];
+        stat += df * df;
+      }
+      const float4 o4 = make_float4(ov[0], ov[1], ov[2], ov[3]);
+      st4(o, q, o4);
+      X.v[m] = o4;  // keep o for the gradient below
+    }
+    stat = warp_sum(stat);
+    on = warp_sum(on);
+    const float f = pair_score_from(dm.family, stat, dm.gamma);
+    const float wp = -sigmoid(-f) / (float)dm.B;  // dL/df+ (reading c.9)
+    if (lane == 0) {
+      a.b.pstat[i] = stat;
+      a.b.wpos[i] = wp;
+      a.b.lpos[i] = -log_sigmoid(f);
+      a.b.onorm[i] = on;
+    }
+    const float ps = wp / fmaxf(sqrtf(stat), 1e-12f);
+    float* gx = a.b.Gocc + ((int64_t)(mode == 0 ? dm.B : 0) + i) * dm.d;
+#pragma unroll
+    for (int m = 0; m < V; ++m) {
+      const int q = lane + 32 * m;
+      if (q >= d4) continue;
+      const float4 ov = X.v[m], yv = Y.v[m];
+      st4(gx, q, make_float4(ps * (ov.x - yv.x), ps * (ov.y - yv.y), ps * (ov.z - yv.z), ps * (ov.w - yv.w)));
+    }
+  } else if (row < dm.B) {
     const int i = row, mode = a.s.mode[i / dm.g];
     const float* h = a.ent.row(a.s.ph[i]);
     const float* t = a.ent.row(a.s.pt[i]);
@@ -889,7 +945,7 @@ __device__ __forceinline__ void prefetch_row(const float* __restrict__ row, floa
 constexpr int kSeg = 8;
 
 template <int V>
-__global__ void __launch_bounds__(256, V >= 8 ? 1 : (V >= 4 ? 3 : 4)) k_update(UpdateArgs a) {
+__global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
   const Dims& dm = a.dm;
   trace_stamp(dm.trace, KGE_K_UPDATE, 0);
   const int lane = threadIdx.x & 31;
@@ -938,8 +994,10 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : (V >= 4 ? 3 : 4)) k_update(U
   if (a.b.flags[1]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
   RowAcc<V> acc;
   acc.zero();
-  constexpr int UNR = 4;
-  for (int j = 0; j < n; j += UNR) {  // loads of UNR occurrences in flight, additions in occurrence order
+  // loads of UNR occurrences in flight, additions in occurrence order; V = 4 (d <= 512) keeps two in flight so the
+  // kernel fits 4 CTAs (32 warps) per SM: the whole grid (B + n_occ warps) is resident in one wave
+  constexpr int UNR = V >= 4 ? 2 : 4;
+  for (int j = 0; j < n; j += UNR) {
     float4 x[UNR][V];
 #pragma unroll
     for (int q = 0; q < UNR; ++q) {
@@ -970,7 +1028,7 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : (V >= 4 ? 3 : 4)) k_update(U
     __threadfence();
     if (lane == 0) *cnt = 0;  // ready for the next step
     acc.zero();
-    constexpr int UNR2 = V >= 4 ? 2 : 4;
+    constexpr int UNR2 = V >= 4 ? 1 : 4;
     for (int q0 = 0; q0 < nseg; q0 += UNR2) {  // segment sums, in segment order
       float4 x[UNR2][V];
 #pragma unroll
@@ -1037,7 +1095,7 @@ static void launch_gather_v(kge_handle* h, const GatherArgs& ga, int rows) {
 
 cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
-  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, dm.B};
+  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, dm.B, 0};
   const int rows = dm.C * dm.k;
   launch_gather_v(h, ga, rows);
   return cudaGetLastError();
@@ -1065,7 +1123,8 @@ cudaError_t launch_update(kge_handle* h, const Slot& s) {
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
   if (dm.model == KGE_TRANSR) return launch_transr_step(h, s, step);
-  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0};
+  const bool tc = h->cfg.neg_precision == KGE_PREC_TF32 && tc_supported(h);
+  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0, tc && tc_fuses_chain(h) ? 1 : 0};
   const int rows = dm.B + dm.C * dm.k;
   launch_begin(h, KGE_K_GATHER);
   launch_gather_v(h, ga, rows);

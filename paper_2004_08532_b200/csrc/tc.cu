@@ -36,6 +36,7 @@ struct TcState {
   CUtensorMap mX_E;          // dX' epilogue operand (X' rows, 4D K-major SW128), box {32, 64, 4}
   float4* xbuf = nullptr;    // split-K exchange of the backward pairs (L2-resident scratch)
   CUtensorMap mG_S, mR_S, mD_S;
+  CUtensorMap mG_L;          // fused chain: gx rows of Gocc (written by k_gather), box {32, 64}
   int fwd_cx = 1;  // backward TMA-store targets: Gocc, Grel, dO (SW128), box {32, 32}
   bool ok = false;
 };
@@ -47,9 +48,9 @@ constexpr int kFwdStages = 2;   // forward stages of kFwdKpb k-blocks (A 64 KB +
 constexpr int kBwdKpb = 2;      // backward: k-blocks per stage (one 4D box per operand)
 constexpr int kBwdStages = 2;   // stages of kBwdKpb k-blocks: each split-K half (K = 128) is exactly two
 constexpr int kNSplit = 4;      // column ranges of dp per backward tile
-constexpr int kThreads = (9 + 4) * 32;  // backward: warps 0-7 = finalise (they alone run the prologue loads, so no
-                                       // role thread waits at a reconvergence point behind a load), lane 0 of warp 8
-                                       // = TMA producer, lane 0 of warps 9-12 = the kIssuers MMA issuers
+constexpr int kThreads = (8 + 4) * 32;  // backward: warps 0-7 = finalise (they alone run the prologue loads, so no
+                                       // role thread waits at a reconvergence point behind a load), lane 0 of warps
+                                       // 8-11 = the kIssuers MMA issuers, the first of them also the TMA producer
 static_assert(kIssuers == 4, "the epilogues add exactly four partial accumulators");
 constexpr int kFwdThreads = 256;  // forward: 8 epilogue warps (two per TMEM lane quarter, 16 negatives each) so the
                                   // transcendental chains of the loss epilogue have latency hiding
@@ -210,19 +211,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   float v[8], w[8];
   if (nst > 0) {
     const uint32_t tl = tmem + ((uint32_t)(lg * 32) << 16);
-    tmem_ld8(tl + kc, v);
-    tmem_ld8(tl + sc, w);
+    uint32_t pv[kIssuers][8], pw[kIssuers][8];  // all eight loads in flight, one wait
 #pragma unroll
-    for (int q = 1; q < kIssuers; ++q) {
-      float pv[8], pw[8];
-      tmem_ld8(tl + q * kNT + kc, pv);
-      tmem_ld8(tl + q * kNT + sc, pw);
+    for (int q = 0; q < kIssuers; ++q) {
+      tmem_ld8_nw(tl + q * kNT + kc, pv[q]);
+      tmem_ld8_nw(tl + q * kNT + sc, pw[q]);
+    }
+    tmem_wait_ld();
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      v[u] = __uint_as_float(pv[0][u]);
+      w[u] = __uint_as_float(pw[0][u]);
+    }
+#pragma unroll
+    for (int q = 1; q < kIssuers; ++q)
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        v[u] += pv[u];
-        w[u] += pw[u];
+        v[u] += __uint_as_float(pv[q][u]);
+        w[u] += __uint_as_float(pw[q][u]);
       }
-    }
   } else {
 #pragma unroll
     for (int u = 0; u < 8; ++u) v[u] = w[u] = 0.f;
@@ -340,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
              const __grid_constant__ CUtensorMap mX_MN, const __grid_constant__ CUtensorMap mO_MN,
              const __grid_constant__ CUtensorMap mO_E, const __grid_constant__ CUtensorMap mX_E,
              const __grid_constant__ CUtensorMap mG_S, const __grid_constant__ CUtensorMap mR_S,
-             const __grid_constant__ CUtensorMap mD_S, TcArgs a) {
+             const __grid_constant__ CUtensorMap mD_S, const __grid_constant__ CUtensorMap mG_L, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   __shared__ uint64_t full[kBwdStages], empty[kBwdStages], done, selfbar;
@@ -405,8 +412,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   float4 cpart[4];  // rowsum(W) partials (nrp = 16 -> 4 float4) for dO, colsum(W) partials (ncp) for dX'
   const int pi = c * dm.g + r;
   int mode = 0;
-  float pscale = 0.f;
-  float4 xr[8];
   auto prologue = [&]() {
 #pragma unroll
     for (int q = 0; q < 4; ++q) cpart[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -423,14 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         cpart[0].x = t;
       }
     }
-    // fused chain: positive i of this row; x = the uncorrupted "other" entity row (t for tail, h for head mode)
     mode = fuse ? a.s.mode[c] : 0;
-    if (fuse && rok && bok) {
-      pscale = a.wpos[pi] / fmaxf(sqrtf(a.pstat[pi]), 1e-12f);
-      const float4* x4 = reinterpret_cast<const float4*>(a.ent.row(mode == 0 ? a.s.pt[pi] : a.s.ph[pi]) + e0);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) xr[u] = 4 * u < d - e0 ? __ldg(x4 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
   };
   if (!role) prologue();
 
@@ -453,31 +451,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (bad) a.flags[0] = 1;
     }
   }
-  if (warp == 8 && lane == 0) {  // TMA producer: one box per operand per stage
-    if (FAM == FAM_L2) {
-      mbar_arrive_expect_tx(&selfbar, 4 * 8192);
-      tma_load_4d(self_smem, pass_x ? &mX_E : &mO_E, &selfbar, 0, r0 + rfin0, b0, c);
+  if (warp >= 8 && lane == 0) {
+    // MMA issuers (see k_tc_fwd): issuer q takes the K = 8 slice q of every k-block into TMEM columns [128 q, +nb*32).
+    // Issuer 0 is also the TMA producer (one box per operand per stage), keeping kBwdStages stages in flight: it only
+    // ever waits for a stage its own previous MMAs already released, so the shared thread cannot deadlock.
+    const int q = warp - 8;
+    int issued = 0;
+    auto produce = [&](int upto) {
+      for (; issued < upto && issued < nst; ++issued) {
+        const int s = issued % kBwdStages;
+        if (issued >= kBwdStages) mbar_wait(&empty[s], ((issued / kBwdStages) - 1) & 1);
+        uint8_t* sa = smem + s * STAGE;
+        uint8_t* sb = sa + A_BYTES;
+        const int kq = kb0 + issued * kBwdKpb;
+        mbar_arrive_expect_tx(&full[s], STAGE);
+        if (!pass_x)
+          tma_load_4d(sa, &mW_K, &full[s], 0, r0, kq, c);  // W[rows, k-blocks kq..]: [kb][128 rows][128 B]
+        else
+          tma_load_4d(sa, &mW_MN, &full[s], 0, kq * 32, r0 / 32, c);  // W^T: [4 j-blocks][K rows][128 B]
+        tma_load_4d(sb, pass_x ? &mO_MN : &mX_MN, &full[s], 0, kq * 32, b0, c);  // [4 col blocks][K rows][128 B]
+      }
+    };
+    if (q == 0) {
+      produce(kBwdStages);
+      if (FAM == FAM_L2) {
+        const bool fz = a.fuse && !pass_x;
+        mbar_arrive_expect_tx(&selfbar, (fz ? 8 : 4) * 8192);
+        tma_load_4d(self_smem, pass_x ? &mX_E : &mO_E, &selfbar, 0, r0 + rfin0, b0, c);
+        if (fz) {  // gx rows of the uncorrupted entities (written by k_gather): [4 col blocks][64 rows][128 B]
+          const int orow = (a.s.mode[c] == 0 ? dm.B : 0) + c * dm.g + r0 + rfin0;
+          for (int bb = 0; bb < 4; ++bb) tma_load_3d(self_smem + (4 + bb) * 8192, &mG_L, &selfbar, (b0 + bb) * 32, orow, 0);
+        }
+      }
     }
-    for (int q = 0; q < nst; ++q) {
-      const int s = q % kBwdStages;
-      if (q >= kBwdStages) mbar_wait(&empty[s], ((q / kBwdStages) - 1) & 1);
-      uint8_t* sa = smem + s * STAGE;
-      uint8_t* sb = sa + A_BYTES;
-      const int kq = kb0 + q * kBwdKpb;
-      mbar_arrive_expect_tx(&full[s], STAGE);
-      if (!pass_x)
-        tma_load_4d(sa, &mW_K, &full[s], 0, r0, kq, c);  // W[rows, k-blocks kq..]: [kb][128 rows][128 B]
-      else
-        tma_load_4d(sa, &mW_MN, &full[s], 0, kq * 32, r0 / 32, c);  // W^T: [4 j-blocks][K rows][128 B]
-      tma_load_4d(sb, pass_x ? &mO_MN : &mX_MN, &full[s], 0, kq * 32, b0, c);  // [4 col blocks][K rows][128 B]
-    }
-  } else if (warp >= 9 && lane == 0) {
-    // MMA issuers (see k_tc_fwd): issuer q takes the K = 8 slice q of every k-block into TMEM columns [128 q, +nb*32)
-    const int q = warp - 9;
     const uint32_t idesc = idesc_tf32(128, nb * 32, pass_x, true);
     const uint32_t acc = tmem + (uint32_t)(q * 128);
     for (int st = 0; st < nst; ++st) {
       const int s = st % kBwdStages;
+      if (q == 0 && st > 0) produce(st + kBwdStages);  // stage st + S - 1 needs stage st - 1 released
       mbar_wait(&full[s], (st / kBwdStages) & 1);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
@@ -509,15 +520,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b = (warp >> 2) * 2 + bb;
       if (b >= nb) break;
       float v[32];
-      if (nst > 0) {
-        tmem_ld32(trow + b * 32, v);
+      if (nst > 0) {  // ((p0 + p1) + p2) + p3: fixed order, deterministic; two loads in flight per wait
+        uint32_t pa[32], pb[32];
+        tmem_ld32_nw(trow + b * 32, pa);
+        tmem_ld32_nw(trow + 128 + b * 32, pb);
+        tmem_wait_ld();
 #pragma unroll
-        for (int q = 1; q < kIssuers; ++q) {  // ((p0 + p1) + p2) + p3: fixed order, deterministic
-          float p1[32];
-          tmem_ld32(trow + q * 128 + b * 32, p1);
+        for (int u = 0; u < 32; ++u) v[u] = __uint_as_float(pa[u]) + __uint_as_float(pb[u]);
+        tmem_ld32_nw(trow + 256 + b * 32, pa);
+        tmem_ld32_nw(trow + 384 + b * 32, pb);
+        tmem_wait_ld();
 #pragma unroll
-          for (int u = 0; u < 32; ++u) v[u] += p1[u];
-        }
+        for (int u = 0; u < 32; ++u) v[u] = (v[u] + __uint_as_float(pa[u])) + __uint_as_float(pb[u]);
       } else {
 #pragma unroll
         for (int u = 0; u < 32; ++u) v[u] = 0.f;
@@ -573,10 +587,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           t0 = make_float4(corr * sv.x - t0.x, corr * sv.y - t0.y, corr * sv.z - t0.z, corr * sv.w - t0.w);
           if (fuse) {
             // go = dO + w+ df/do, gx = w+ df/dx; f = gamma - ||o - x||: go = dO - s u, gx = s u (u = o - x, s = w+/D)
-            // tail (o = h + r): gH = go, gR = go, gT = gx ; head (o = t - r): gT = go, gR = -go, gH = gx
-            const float4 xv = xr[u];
-            t1 = make_float4(pscale * (sv.x - xv.x), pscale * (sv.y - xv.y), pscale * (sv.z - xv.z),
-                             pscale * (sv.w - xv.w));
+            // tail (o = h + r): gH = go, gR = go, gT = gx ; head (o = t - r): gT = go, gR = -go, gH = gx.
+            // gx was written to the uncorrupted entity's occurrence row by k_gather (fuse_pos); read it back (L2)
+            t1 = *reinterpret_cast<const float4*>(rowp + 4 * 8192 + ((u ^ (fr & 7)) << 4));
             t0 = make_float4(-t1.x + t0.x, -t1.y + t0.y, -t1.z + t0.z, -t1.w + t0.w);
             t2 = make_float4(rsign * t0.x, rsign * t0.y, rsign * t0.z, rsign * t0.w);
           }
@@ -584,16 +597,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (wtma) {
           const int off = lane * 128 + ((u ^ (lane & 7)) << 4);
           *reinterpret_cast<float4*>(stg + off) = t0;
-          if (fuse) {
-            *reinterpret_cast<float4*>(stg + 4096 + off) = t1;
-            *reinterpret_cast<float4*>(stg + 8192 + off) = t2;
-          }
+          if (fuse) *reinterpret_cast<float4*>(stg + 8192 + off) = t2;
         } else if (4 * u < ne) {
           reinterpret_cast<float4*>(gdst[0] + e0)[u] = t0;
-          if (fuse) {
-            reinterpret_cast<float4*>(gdst[1] + e0)[u] = t1;
-            reinterpret_cast<float4*>(gdst[2] + e0)[u] = t2;
-          }
+          if (fuse) reinterpret_cast<float4*>(gdst[2] + e0)[u] = t2;
         }
       }
     }
@@ -603,10 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         tma_store_3d(pass_x || fuse ? &mG_S : &mD_S, stg, e0, trow0[0], 0);
-        if (fuse) {
-          tma_store_3d(&mG_S, stg + 4096, e0, trow0[1], 0);
-          tma_store_3d(&mR_S, stg + 8192, e0, trow0[2], 0);
-        }
+        if (fuse) tma_store_3d(&mR_S, stg + 8192, e0, trow0[2], 0);
         bulk_commit();
         bulk_wait_all();
       }
@@ -671,7 +675,7 @@ static bool make_map4(CUtensorMap* m, const float* base, int cols, int rows, int
 static size_t fwd_smem() { return (size_t)kFwdStages * kFwdKpb * (128 * 128 + kNT * 128) + 128 * (kNT / 2) * 4 + 1024; }
 static size_t bwd_smem(int dp) {
   (void)dp;
-  return (size_t)kBwdStages * kBwdKpb * (16384 + 4 * 4096) + 4 * 8192 + 1024;
+  return (size_t)kBwdStages * kBwdKpb * (16384 + 4 * 4096) + 8 * 8192 + 1024;
 }
 
 bool tc_init(kge_handle* h) {
@@ -701,6 +705,7 @@ bool tc_init(kge_handle* h) {
   ok &= make_map(&st->mG_S, b.Gocc, dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mR_S, b.Grel, dm.drel, dm.B, 1, dm.drel, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mD_S, b.dO, dm.d, dm.B, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&st->mG_L, b.Gocc, dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 64, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!ok) {
     delete st;
     return false;
@@ -770,10 +775,10 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
   launch_begin(h, KGE_K_NEG_BWD);
   if (dm.family == FAM_DOT)
     launch_pdl_cluster(k_tc_bwd<FAM_DOT>, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN,
-                       st->mO_MN, st->mO_E, st->mX_E, st->mG_S, st->mR_S, st->mD_S, a);
+                       st->mO_MN, st->mO_E, st->mX_E, st->mG_S, st->mR_S, st->mD_S, st->mG_L, a);
   else
     launch_pdl_cluster(k_tc_bwd<FAM_L2>, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN,
-                       st->mO_MN, st->mO_E, st->mX_E, st->mG_S, st->mR_S, st->mD_S, a);
+                       st->mO_MN, st->mO_E, st->mX_E, st->mG_S, st->mR_S, st->mD_S, st->mG_L, a);
   launch_end(h, KGE_K_NEG_BWD);
   return cudaGetLastError();
 }

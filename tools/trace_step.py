@@ -37,7 +37,11 @@ for k in range(1, 6):
     st = st[m] - t0
     en = T[k][:, 7][m]
     en = en[en > 0] - t0 if (en > 0).any() else np.array([0])
-    line = f"{names[k]:10s} ctas={m.sum():5d} start[min/med/max]={st.min()/1e3:6.2f}/{np.median(st)/1e3:6.2f}/{st.max()/1e3:6.2f} us  end max={en.max()/1e3:6.2f} us"
+    line = f"{names[k]:10s} ctas={m.sum():5d} start[min/med/max]={st.min()/1e3:6.2f}/{np.median(st)/1e3:6.2f}/{st.max()/1e3:6.2f} us  end med/max={np.median(en)/1e3:6.2f}/{en.max()/1e3:6.2f} us"
+    if k == 1 and (T[k][:, 1][m] > 0).any():
+        s1 = T[k][:, 1][m]
+        s1 = s1[s1 > 0] - t0
+        line += f" | after pdl_wait min/med/max {s1.min()/1e3:6.2f}/{np.median(s1)/1e3:6.2f}/{s1.max()/1e3:6.2f}"
     if k in (2, 3):
         s1 = T[k][:, 1][m] - t0
         s2 = T[k][:, 2][m] - t0
@@ -60,7 +64,7 @@ for z, sl in ((0, slice(0, n // 2)), (1, slice(n // 2, n))):
 # update: entity CTAs first (n_occ / 8 of them), then one CTA per unique relation
 k = 5
 U = T[k]
-nr = 1024  # relation CTAs first (one per possible unique relation), then the entity CTAs
+nr = 1024 // 8  # warp per segment start: relation positions first (B / 8 CTAs), then the entity positions
 for name, sl in (("relation", slice(0, nr)), ("entity", slice(nr, 2048))):
     R = U[sl]
     m = R[:, 7] > 0
