@@ -412,8 +412,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   // sample ring (+ the debug slot) and the flags/slot-table block; for P > 1 they live in the exported shared block
   // together with the barrier flags and the per-unique gradient sums that peers read
   const size_t sl = slot_ints(dm);
-  const size_t flags_bytes = ((16 + sizeof(Slot) * (h->ring + 1)) + 255) & ~size_t(255);
-  const size_t ring_bytes = sl * 4 * (h->ring + 1);
+  const int nslot = h->ring + 1 + kge_handle::kGiven;  // ring, debug slot, given-batch slots
+  const size_t flags_bytes = ((16 + sizeof(Slot) * nslot) + 255) & ~size_t(255);
+  const size_t ring_bytes = sl * 4 * nslot;
   int32_t* ring_base = nullptr;
   if (h->P > 1) {
     Dist& D = h->dist;
@@ -446,6 +447,16 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   h->slots.resize(h->ring);
   for (int i = 0; i < h->ring; ++i) carve_slot(h, ring_base + sl * i, h->slots[i]);
   carve_slot(h, ring_base + sl * h->ring, h->debug_slot);
+  for (int i = 0; i < kge_handle::kGiven; ++i) carve_slot(h, ring_base + sl * (h->ring + 1 + i), h->given_slots[i]);
+  if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "side stream"));
+  for (int i = 0; i < 2; ++i)
+    if (cudaEventCreateWithFlags(&h->ev_samp[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_free[i], cudaEventDisableTiming) != cudaSuccess)
+      return fail(cuda_fail(cudaGetLastError(), "events"));
+  for (int i = 0; i < kge_handle::kGiven; ++i)
+    if (cudaEventCreateWithFlags(&h->ev_gsamp[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_gfree[i], cudaEventDisableTiming) != cudaSuccess)
+      return fail(cuda_fail(cudaGetLastError(), "events"));
   h->given = (int32_t*)dalloc(h, (size_t)3 * dm.B * 4);
   for (int i = 0; i < kge_handle::kStage; ++i)
     if (cudaEventCreateWithFlags(&h->stage_ev[i], cudaEventDisableTiming) != cudaSuccess) {
@@ -500,6 +511,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (e == cudaSuccess) e = cudaMemsetAsync(h->seg_cnt, 0, (size_t)(dm.B + dm.n_occ) * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h), h->slots.data(), sizeof(Slot) * h->ring, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h) + h->ring, &h->debug_slot, sizeof(Slot), cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_slots(h) + h->ring + 1, h->given_slots, sizeof(Slot) * kge_handle::kGiven, cudaMemcpyHostToDevice,
+                        h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "workspace init"));
   if (getenv("KGE_TRACE")) {  // diagnostics: per-CTA stamps, read with kge_debug_trace
@@ -517,11 +531,33 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
 }
 
 static int ensure_sampled(kge_handle* h, int64_t s) {
-  if (h->ring_first >= 0 && s >= h->ring_first && s < h->ring_first + h->ring) return KGE_OK;
+  const int H = h->ring / 2;
+  const int64_t hs = s - s % H;  // first step of s's ring half
+  const int q = (int)((hs / H) % 2);
   SampleParams p = sample_params(h, false);
-  cudaError_t e = launch_sample(h, p, d_slots(h), h->ring, s, h->ring);
-  if (e != cudaSuccess) return cuda_fail(e, "sample");
-  h->ring_first = s;
+  cudaError_t e = cudaSuccess;
+  if (h->half_first[q] != hs) {  // not sampled ahead (first call, kge_set_step, a caller batch): sample it in order
+    e = launch_sample(h, p, d_slots(h), h->ring, hs, H);
+    if (e != cudaSuccess) return cuda_fail(e, "sample");
+    h->half_first[q] = hs;
+    h->half_waited[q] = true;
+  } else if (!h->half_waited[q]) {
+    e = cudaStreamWaitEvent(h->stream, h->ev_samp[q], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "sample wait");
+    h->half_waited[q] = true;
+  }
+  if (h->P == 1 && h->half_first[1 - q] != hs + H) {
+    // the other half's slots were last read by steps < hs, all enqueued on the main stream before this point: fill
+    // them with steps [hs + H, hs + 2H). (P > 1 samples in order on the main stream: with several ranks sharing one
+    // device, as the emulated-rank tests do, side-stream samplers could hold the SMs the ranks' device barriers need.)
+    e = cudaEventRecord(h->ev_free[1 - q], h->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->side, h->ev_free[1 - q], 0);
+    if (e == cudaSuccess) e = launch_sample(h, p, d_slots(h), h->ring, hs + H, H, h->side);
+    if (e == cudaSuccess) e = cudaEventRecord(h->ev_samp[1 - q], h->side);
+    if (e != cudaSuccess) return cuda_fail(e, "sample ahead");
+    h->half_first[1 - q] = hs + H;
+    h->half_waited[1 - q] = false;
+  }
   return KGE_OK;
 }
 
@@ -602,19 +638,27 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
       e = cudaMemsetAsync(h->dist.grel_split, 0, (size_t)h->dist.n_split * h->dims.drel * 4, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "barrier");
   }
-  e = cudaMemcpyAsync(h->given, st, (size_t)3 * B * 4, cudaMemcpyHostToDevice, h->stream);
-  if (e == cudaSuccess) e = cudaEventRecord(h->stage_ev[si], h->stream);
+  // given slot gi of this step: upload + sample on the side stream (overlapping the previous step's kernels), after
+  // the step that last used the slot released it
+  // (P > 1: everything on the main stream, see ensure_sampled)
+  const int gi = (int)(s % kge_handle::kGiven);
+  cudaStream_t ss = h->P == 1 ? h->side : h->stream;
+  e = h->P == 1 ? cudaStreamWaitEvent(ss, h->ev_gfree[gi], 0) : cudaSuccess;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->given, st, (size_t)3 * B * 4, cudaMemcpyHostToDevice, ss);
+  if (e == cudaSuccess) e = cudaEventRecord(h->stage_ev[si], ss);
   if (e != cudaSuccess) return cuda_fail(e, "batch upload");
   h->stage_i = (si + 1) % kge_handle::kStage;
-  // sample negatives + dedup for this step into the debug slot, from the given positives
+  // sample negatives + dedup for this step from the given positives
   SampleParams p = sample_params(h, true);
-  e = launch_sample(h, p, d_slots(h) + h->ring, 1, s, 1);
+  e = launch_sample(h, p, d_slots(h) + h->ring + 1 + gi, 1, s, 1, ss);
+  if (e == cudaSuccess && h->P == 1) e = cudaEventRecord(h->ev_gsamp[gi], ss);
+  if (e == cudaSuccess && h->P == 1) e = cudaStreamWaitEvent(h->stream, h->ev_gsamp[gi], 0);
   if (e != cudaSuccess) return cuda_fail(e, "sample");
-  e = launch_step(h, h->debug_slot, s);
-  if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, h->debug_slot);
+  e = launch_step(h, h->given_slots[gi], s);
+  if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, h->given_slots[gi]);
+  if (e == cudaSuccess && h->P == 1) e = cudaEventRecord(h->ev_gfree[gi], h->stream);
   if (e != cudaSuccess) return cuda_fail(e, "step");
   h->step = s + 1;
-  if (h->ring_first >= 0 && s >= h->ring_first && s < h->ring_first + h->ring) h->ring_first = -1;
   if (loss_host) {
     e = cudaMemcpyAsync(loss_host, h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "loss readback");
@@ -831,6 +875,16 @@ void kge_destroy(kge_handle* h) {
   for (int i = 0; i < kge_handle::kStage; ++i)
     if (h->stage_ev[i]) cudaEventDestroy(h->stage_ev[i]);
   if (h->pinned_loss) cudaFreeHost(h->pinned_loss);
+  if (h->side) cudaStreamSynchronize(h->side);
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_samp[i]) cudaEventDestroy(h->ev_samp[i]);
+    if (h->ev_free[i]) cudaEventDestroy(h->ev_free[i]);
+  }
+  for (int i = 0; i < kge_handle::kGiven; ++i) {
+    if (h->ev_gsamp[i]) cudaEventDestroy(h->ev_gsamp[i]);
+    if (h->ev_gfree[i]) cudaEventDestroy(h->ev_gfree[i]);
+  }
+  if (h->side) cudaStreamDestroy(h->side);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   tc_destroy(h);
   delete h;

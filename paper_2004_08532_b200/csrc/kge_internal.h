@@ -145,7 +145,7 @@ struct Dims {
   uint64_t* trace;  // diagnostics (KGE_TRACE=1 at init): per-kernel, per-CTA globaltimer stamps, else nullptr
   int32_t model, family, variant;
   int32_t d, drel, B, g, C, k, n_occ;
-  int32_t dp, kp;  // padded row pitch of O / X' (d + 2 rounded up to 32) and of W (k rounded up to 4)
+  int32_t dp, kp;  // padded row pitch of O / X' (d + 2 rounded up to 32) and of W (k rounded up to 32)
   float gamma, lr, eps;
   int64_t n_entities, n_relations;
 };
@@ -180,9 +180,19 @@ struct kge_handle {
   int64_t n_triples = 0, n_list = 0;
   // sampling ring
   int32_t ring = 0;
-  int64_t ring_first = -1;  // steps [ring_first, ring_first + ring) are in the ring
   std::vector<kge::Slot> slots;
   kge::Slot debug_slot{};
+  // sampling runs on a side stream ahead of the steps (k_sample is a pure function of (seed, step)): the ring is two
+  // halves of ring/2 steps; while the main stream works through one half the side stream fills the other
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_samp[2] = {}, ev_free[2] = {};
+  int64_t half_first[2] = {-1, -1};  // first step held by each ring half (-1: none)
+  bool half_waited[2] = {false, false};
+  // caller-supplied batches (kge_train_batch): kGiven slots sampled on the side stream, so the sample of batch s+1
+  // overlaps step s
+  static constexpr int kGiven = 4;
+  kge::Slot given_slots[kGiven] = {};
+  cudaEvent_t ev_gsamp[kGiven] = {}, ev_gfree[kGiven] = {};
   int32_t* given = nullptr;  // [3 x B] device copy of caller positives
   static constexpr int kStage = 4;
   int32_t* pinned_given = nullptr;  // host pinned staging: kStage buffers of 3B int32 (caller-supplied batches)
@@ -260,7 +270,8 @@ void launch_end(kge_handle* h, int kid);
 // sample.cu
 size_t sample_smem_bytes(int n_pad);
 cudaError_t sample_init();
-cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev_array, int ring, int64_t step0, int n_steps);
+cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev_array, int ring, int64_t step0, int n_steps,
+                          cudaStream_t stream = nullptr);  // nullptr: h->stream
 cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound,
                               int64_t row_stride = 1, int64_t row_offset = 0);
 cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, int64_t n, int64_t limit, int32_t* bad);

@@ -184,7 +184,8 @@ cudaError_t sample_init() {
   return cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
-cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev, int ring, int64_t step0, int n_steps) {
+cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev, int ring, int64_t step0, int n_steps,
+                          cudaStream_t stream) {
   SampleArgs a;
   a.p = p;
   a.fe_half = make_feistel_domain((uint64_t)p.n_list).half;
@@ -193,9 +194,12 @@ cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slot
   a.step0 = step0;
   size_t smem = sample_smem_bytes(p.n_pad);  // opt-in raised once by sample_init (never in the step path: the call
                                               // may synchronise, which would stall the multi-rank emulation)
+  cudaStream_t main = h->stream;
+  if (stream) h->stream = stream;  // the profiler brackets the launch on the stream it runs on
   launch_begin(h, KGE_K_SAMPLE);
   k_sample<<<dim3(n_steps, 2), kSampleThreads, smem, h->stream>>>(a);
   launch_end(h, KGE_K_SAMPLE);
+  h->stream = main;
   return cudaGetLastError();
 }
 
