@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "device_common.cuh"
@@ -123,7 +124,7 @@ static int validate(const kge_config* c) {
 
 static size_t slot_ints(const Dims& d) {
   const size_t n_occ = d.n_occ, B = d.B;
-  size_t n = B * 4 + (size_t)d.C * d.k + d.C + 1 + n_occ * 3 + (n_occ + 1) + 1 + B * 3 + (B + 1);
+  size_t n = B * 4 + (size_t)d.C * d.k + d.C + 1 + n_occ * 3 + (n_occ + 1) + 1 + B * 3 + (B + 1) + 2;
   return (n + 63) & ~size_t(63);  // 256-byte aligned slots
 }
 
@@ -156,10 +157,11 @@ static int carve_slot(kge_handle* h, int32_t* p, Slot& s) {
   s.rel_inv = p; p += B;
   s.rel_off = p; p += B + 1;
   s.rel_occ = p; p += B;
+  s.info = p; p += 2;
   return KGE_OK;
 }
 
-static SampleParams sample_params(const kge_handle* h, bool given) {
+static SampleParams sample_params(const kge_handle* h, bool given, int gi = 0) {
   SampleParams p{};
   p.th = h->th;
   p.tr = h->tr;
@@ -167,9 +169,10 @@ static SampleParams sample_params(const kge_handle* h, bool given) {
   p.list = h->list;
   p.n_list = h->n_list;
   if (given) {
-    p.given_h = h->given;
-    p.given_r = h->given + h->dims.B;
-    p.given_t = h->given + 2 * h->dims.B;
+    const int32_t* gb = h->given + (size_t)gi * 3 * h->dims.B;
+    p.given_h = gb;
+    p.given_r = gb + h->dims.B;
+    p.given_t = gb + 2 * h->dims.B;
   }
   p.n_entities = h->dims.n_entities;
   p.B = h->dims.B;
@@ -448,7 +451,16 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   for (int i = 0; i < h->ring; ++i) carve_slot(h, ring_base + sl * i, h->slots[i]);
   carve_slot(h, ring_base + sl * h->ring, h->debug_slot);
   for (int i = 0; i < kge_handle::kGiven; ++i) carve_slot(h, ring_base + sl * (h->ring + 1 + i), h->given_slots[i]);
-  if (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess) return fail(cuda_fail(cudaGetLastError(), "side stream"));
+  {  // the side stream gets the highest priority: its sampler CTAs take the next free SM slot ahead of the step
+     // kernels' (PDL-launched, waiting) CTAs, so the sample of step s+1 really overlaps step s
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, hi) != cudaSuccess)
+      return fail(cuda_fail(cudaGetLastError(), "side stream"));
+    for (int i = 0; i < kge_handle::kGiven; ++i)
+      if (cudaStreamCreateWithPriority(&h->gside[i], cudaStreamNonBlocking, hi) != cudaSuccess)
+        return fail(cuda_fail(cudaGetLastError(), "side stream"));
+  }
   for (int i = 0; i < 2; ++i)
     if (cudaEventCreateWithFlags(&h->ev_samp[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_free[i], cudaEventDisableTiming) != cudaSuccess)
@@ -457,14 +469,15 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     if (cudaEventCreateWithFlags(&h->ev_gsamp[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_gfree[i], cudaEventDisableTiming) != cudaSuccess)
       return fail(cuda_fail(cudaGetLastError(), "events"));
-  h->given = (int32_t*)dalloc(h, (size_t)3 * dm.B * 4);
+  h->given = (int32_t*)dalloc(h, (size_t)kge_handle::kGiven * 3 * dm.B * 4);
   for (int i = 0; i < kge_handle::kStage; ++i)
     if (cudaEventCreateWithFlags(&h->stage_ev[i], cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
       return fail(KGE_ECUDA);
     }
   if (cudaMallocHost(&h->pinned_given, (size_t)kge_handle::kStage * 3 * dm.B * 4) != cudaSuccess ||
-      cudaMallocHost(&h->pinned_loss, (size_t)h->ring * 4) != cudaSuccess) {
+      cudaMallocHost(&h->pinned_loss, (size_t)h->ring * 4) != cudaSuccess ||
+      cudaMallocHost(&h->pinned_sink, 16) != cudaSuccess) {
     cudaGetLastError();
     return fail(KGE_ENOMEM);
   }
@@ -610,6 +623,87 @@ int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
 }
 
 // Enqueue one step on a caller-supplied batch; loss_dev_to: host destination of an async loss copy (or NULL).
+static bool use_graphs(const kge_handle* h) {
+  static const bool off = getenv("KGE_NO_GRAPHS") != nullptr || getenv("KGE_DEBUG_SYNC") != nullptr;
+  return h->P == 1 && !off && !h->prof.on && h->dims.trace == nullptr;
+}
+
+// capture `body` (launches on stream st) into an instantiated graph; the first node of the given type is returned
+static cudaError_t capture_graph(kge_handle* h, cudaStream_t st, const std::function<cudaError_t()>& body,
+                                 cudaGraphExec_t* exec, cudaGraphNodeType want, cudaGraphNode_t* node) {
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return e;
+  const int64_t l0 = h->launches;
+  cudaError_t eb = body();
+  cudaError_t ee = cudaStreamEndCapture(st, &g);
+  h->g_launches = (int32_t)(h->launches - l0);
+  h->launches = l0;
+  if (eb != cudaSuccess || ee != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return eb != cudaSuccess ? eb : ee;
+  }
+  size_t n = 0;
+  e = cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (e == cudaSuccess) e = cudaGraphGetNodes(g, nodes.data(), &n);
+  *node = nullptr;
+  for (size_t i = 0; e == cudaSuccess && i < n && !*node; ++i) {
+    cudaGraphNodeType t;
+    e = cudaGraphNodeGetType(nodes[i], &t);
+    if (e == cudaSuccess && t == want) *node = nodes[i];
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(exec, g, 0);
+  if (e == cudaSuccess)
+    h->graphs.push_back(g);  // kept alive: node parameter updates name nodes of the source graph
+  else
+    cudaGraphDestroy(g);
+  return e;
+}
+
+// graph path of train_batch_enqueue (P == 1): see kge_handle::g_samp / g_step
+#define KGE_GCHK(call, what)                        \
+  do {                                              \
+    cudaError_t _e = (call);                        \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+static int batch_graphs(kge_handle* h, int gi, int64_t s, float* loss_host) {
+  const int B = h->dims.B;
+  SampleParams p = sample_params(h, true, gi);
+  const Slot* gslot = d_slots(h) + h->ring + 1 + gi;
+  cudaStream_t ss = h->gside[gi];
+  if (!h->g_samp[gi]) {
+    int32_t* st = h->pinned_given + (size_t)gi * 3 * B;
+    int32_t* gb = h->given + (size_t)gi * 3 * B;
+    KGE_GCHK(capture_graph(h, ss, [&]() {
+               cudaError_t x = cudaMemcpyAsync(gb, st, (size_t)3 * B * 4, cudaMemcpyHostToDevice, ss);
+               return x == cudaSuccess ? launch_sample(h, p, gslot, 1, s, 1, ss) : x;
+             }, &h->g_samp[gi], cudaGraphNodeTypeKernel, &h->g_samp_node[gi]), "capture sample graph");
+  }
+  if (!h->g_step[gi]) {
+    KGE_GCHK(capture_graph(h, h->stream, [&]() {
+               cudaError_t x = launch_step(h, h->given_slots[gi], s);
+               return x == cudaSuccess ? cudaMemcpyAsync(h->pinned_sink, h->buf.loss, 4, cudaMemcpyDeviceToHost, h->stream)
+                                       : x;
+             }, &h->g_step[gi], cudaGraphNodeTypeMemcpy, &h->g_loss_node[gi]), "capture step graph");
+  }
+  const int32_t kernels = h->g_launches;
+  KGE_GCHK(cudaStreamWaitEvent(ss, h->ev_gfree[gi], 0), "wait slot");
+  KGE_GCHK(sample_graph_set(h, h->g_samp[gi], h->g_samp_node[gi], p, gslot, 1, s, 1), "sample node params");
+  KGE_GCHK(cudaGraphLaunch(h->g_samp[gi], ss), "sample graph launch");
+  KGE_GCHK(cudaEventRecord(h->stage_ev[gi], ss), "event");
+  KGE_GCHK(cudaEventRecord(h->ev_gsamp[gi], ss), "event");
+  KGE_GCHK(cudaStreamWaitEvent(h->stream, h->ev_gsamp[gi], 0), "wait sample");
+  KGE_GCHK(cudaGraphExecMemcpyNodeSetParams1D(h->g_step[gi], h->g_loss_node[gi], loss_host ? loss_host : h->pinned_sink,
+                                              h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost),
+           "loss node params");
+  KGE_GCHK(cudaGraphLaunch(h->g_step[gi], h->stream), "step graph launch");
+  KGE_GCHK(cudaEventRecord(h->ev_gfree[gi], h->stream), "event");
+  h->launches += 1 + kernels;
+  return KGE_OK;
+}
+#undef KGE_GCHK
+
 static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails,
                                float* loss_host) {
   if (!h || !heads || !rels || !tails) { set_error("NULL argument"); return KGE_EINVAL; }
@@ -618,7 +712,7 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
   const int64_t s = h->step;
   // host-side range check + int32 narrowing into a pinned staging buffer (ring of kStage; a buffer is reused only
   // after its previous H2D copy completed), then one H2D copy
-  const int si = h->stage_i;
+  const int si = (int)(s % kge_handle::kGiven);  // staging buffer = given slot (kStage == kGiven)
   int32_t* st = h->pinned_given + (size_t)si * 3 * B;
   cudaError_t e = cudaEventSynchronize(h->stage_ev[si]);
   if (e != cudaSuccess) return cuda_fail(e, "staging reuse");
@@ -638,18 +732,23 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
       e = cudaMemsetAsync(h->dist.grel_split, 0, (size_t)h->dist.n_split * h->dims.drel * 4, h->stream);
     if (e != cudaSuccess) return cuda_fail(e, "barrier");
   }
+  if (use_graphs(h)) {
+    const int rc = batch_graphs(h, si, s, loss_host);
+    if (rc != KGE_OK) return rc;
+    h->step = s + 1;
+    return KGE_OK;
+  }
   // given slot gi of this step: upload + sample on the side stream (overlapping the previous step's kernels), after
   // the step that last used the slot released it
   // (P > 1: everything on the main stream, see ensure_sampled)
   const int gi = (int)(s % kge_handle::kGiven);
-  cudaStream_t ss = h->P == 1 ? h->side : h->stream;
+  cudaStream_t ss = h->P == 1 ? h->gside[gi] : h->stream;
   e = h->P == 1 ? cudaStreamWaitEvent(ss, h->ev_gfree[gi], 0) : cudaSuccess;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(h->given, st, (size_t)3 * B * 4, cudaMemcpyHostToDevice, ss);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h->given + (size_t)gi * 3 * B, st, (size_t)3 * B * 4, cudaMemcpyHostToDevice, ss);
   if (e == cudaSuccess) e = cudaEventRecord(h->stage_ev[si], ss);
   if (e != cudaSuccess) return cuda_fail(e, "batch upload");
-  h->stage_i = (si + 1) % kge_handle::kStage;
   // sample negatives + dedup for this step from the given positives
-  SampleParams p = sample_params(h, true);
+  SampleParams p = sample_params(h, true, gi);
   e = launch_sample(h, p, d_slots(h) + h->ring + 1 + gi, 1, s, 1, ss);
   if (e == cudaSuccess && h->P == 1) e = cudaEventRecord(h->ev_gsamp[gi], ss);
   if (e == cudaSuccess && h->P == 1) e = cudaStreamWaitEvent(h->stream, h->ev_gsamp[gi], 0);
@@ -885,6 +984,17 @@ void kge_destroy(kge_handle* h) {
     if (h->ev_gfree[i]) cudaEventDestroy(h->ev_gfree[i]);
   }
   if (h->side) cudaStreamDestroy(h->side);
+  for (int i = 0; i < kge_handle::kGiven; ++i)
+    if (h->gside[i]) {
+      cudaStreamSynchronize(h->gside[i]);
+      cudaStreamDestroy(h->gside[i]);
+    }
+  for (int i = 0; i < kge_handle::kGiven; ++i) {
+    if (h->g_samp[i]) cudaGraphExecDestroy(h->g_samp[i]);
+    if (h->g_step[i]) cudaGraphExecDestroy(h->g_step[i]);
+  }
+  for (cudaGraph_t g : h->graphs) cudaGraphDestroy(g);
+  if (h->pinned_sink) cudaFreeHost(h->pinned_sink);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   tc_destroy(h);
   delete h;

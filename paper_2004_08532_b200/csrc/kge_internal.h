@@ -61,6 +61,8 @@ struct Slot {
   int32_t* rel_inv;  // [B]
   int32_t* rel_off;  // [B + 1]
   int32_t* rel_occ;  // [B]
+  int32_t* info;     // [2]: the step (mod 2^32) and its loss slot (step % loss ring), written by k_sample -- so the
+                     // step kernels' parameters depend on the slot only and one captured graph serves every step
 };
 
 struct SampleParams {
@@ -192,12 +194,22 @@ struct kge_handle {
   // overlaps step s
   static constexpr int kGiven = 4;
   kge::Slot given_slots[kGiven] = {};
+  cudaStream_t gside[kGiven] = {};  // one high-priority stream per given slot: the single-step samples of consecutive
+                                    // batches (~50 us each) run concurrently instead of queueing on one stream
   cudaEvent_t ev_gsamp[kGiven] = {}, ev_gfree[kGiven] = {};
-  int32_t* given = nullptr;  // [3 x B] device copy of caller positives
-  static constexpr int kStage = 4;
+  // CUDA graphs of the caller-batch path (P == 1, no profiler / trace / debug sync), one pair per given slot: the
+  // upload + sample (side stream) and the step kernels + loss readback (main stream); per launch only the sampler's
+  // step and the readback addresses change (node parameter updates), which keeps the host cost per step far below
+  // the device time
+  cudaGraphExec_t g_samp[kGiven] = {}, g_step[kGiven] = {};
+  cudaGraphNode_t g_samp_node[kGiven] = {}, g_loss_node[kGiven] = {};
+  std::vector<cudaGraph_t> graphs;  // source graphs of the instantiated ones
+  int32_t g_launches = 0;       // kernels per captured step (launch counter)
+  float* pinned_sink = nullptr;  // readback target when the caller passes no loss pointer
+  int32_t* given = nullptr;  // [kGiven][3 x B] device copies of caller positives (one per given slot)
+  static constexpr int kStage = kGiven;  // staging buffer i feeds given slot i (the captured upload reads it)
   int32_t* pinned_given = nullptr;  // host pinned staging: kStage buffers of 3B int32 (caller-supplied batches)
   cudaEvent_t stage_ev[kStage] = {};  // recorded after each staging buffer's H2D copy
-  int32_t stage_i = 0;
   float* pinned_loss = nullptr;
   // step
   kge::StepBuffers buf{};
@@ -272,6 +284,9 @@ size_t sample_smem_bytes(int n_pad);
 cudaError_t sample_init();
 cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev_array, int ring, int64_t step0, int n_steps,
                           cudaStream_t stream = nullptr);  // nullptr: h->stream
+// re-point a captured k_sample node at another first step
+cudaError_t sample_graph_set(kge_handle* h, cudaGraphExec_t exec, cudaGraphNode_t node, const SampleParams& p,
+                             const Slot* slots_dev_array, int ring, int64_t step0, int n_steps);
 cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound,
                               int64_t row_stride = 1, int64_t row_offset = 0);
 cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, int64_t n, int64_t limit, int32_t* bad);

@@ -21,7 +21,9 @@ struct SampleArgs {
   uint32_t fe_half;
   const Slot* slots;  // device array [ring]
   int32_t ring;
+  int32_t loss_ring;  // the handle's loss ring (Slot::info[1] = step % loss_ring)
   int64_t step0;
+  uint64_t* trace;    // KGE_TRACE diagnostics or nullptr
 };
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
@@ -54,11 +56,16 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
   extern __shared__ unsigned long long keys[];
   __shared__ int warp_tot[32];
   __shared__ int total;
+  trace_stamp(a.trace, KGE_K_SAMPLE, 0);
   pdl_wait();  // the ring slots it overwrites may still be read by the previous step's kernels
   pdl_trigger();
   const SampleParams& p = a.p;
   const int64_t s = a.step0 + blockIdx.x;
   const Slot slot = a.slots[s % a.ring];
+  if (blockIdx.y == 0 && threadIdx.x == 0) {
+    slot.info[0] = (int32_t)(uint32_t)s;
+    slot.info[1] = (int32_t)(s % a.loss_ring);
+  }
   const bool ent_side = blockIdx.y == 0;
   const int tid = threadIdx.x;
   const int n = ent_side ? p.n_occ : p.B;
@@ -106,6 +113,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
   while (np2 < n) np2 <<= 1;
   for (int q = n + tid; q < np2; q += blockDim.x) keys[q] = ~0ull;
   __syncthreads();
+  trace_stamp(a.trace, KGE_K_SAMPLE, 1);
 
   // bitonic sort, ascending. Stages with distance j >= 32 exchange through shared memory (one barrier each); the
   // j < 32 stages of each merge run warp-synchronously on 64-key blocks held 2 per lane (no block barrier).
@@ -147,6 +155,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
     __syncthreads();
   }
 
+  trace_stamp(a.trace, KGE_K_SAMPLE, 2);
   // run boundaries -> unique ids, inverse map, segments (reading c.5)
   const int per = (n + blockDim.x - 1) / blockDim.x;
   const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
@@ -176,6 +185,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
     else
       *slot.rel_n = total;
   }
+  trace_stamp(a.trace, KGE_K_SAMPLE, 7);
 }
 
 size_t sample_smem_bytes(int n_pad) { return (size_t)n_pad * sizeof(unsigned long long); }
@@ -191,7 +201,9 @@ cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slot
   a.fe_half = make_feistel_domain((uint64_t)p.n_list).half;
   a.slots = slots_dev;
   a.ring = ring;
+  a.loss_ring = h->ring;
   a.step0 = step0;
+  a.trace = h->dims.trace;
   size_t smem = sample_smem_bytes(p.n_pad);  // opt-in raised once by sample_init (never in the step path: the call
                                               // may synchronise, which would stall the multi-rank emulation)
   cudaStream_t main = h->stream;
@@ -201,6 +213,26 @@ cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slot
   launch_end(h, KGE_K_SAMPLE);
   h->stream = main;
   return cudaGetLastError();
+}
+
+cudaError_t sample_graph_set(kge_handle* h, cudaGraphExec_t exec, cudaGraphNode_t node, const SampleParams& p,
+                             const Slot* slots_dev, int ring, int64_t step0, int n_steps) {
+  SampleArgs a;
+  a.p = p;
+  a.fe_half = make_feistel_domain((uint64_t)p.n_list).half;
+  a.slots = slots_dev;
+  a.ring = ring;
+  a.loss_ring = h->ring;
+  a.step0 = step0;
+  a.trace = h->dims.trace;
+  void* args[] = {&a};
+  cudaKernelNodeParams kp = {};
+  kp.func = (void*)k_sample;
+  kp.gridDim = dim3(n_steps, 2);
+  kp.blockDim = dim3(kSampleThreads);
+  kp.sharedMemBytes = (unsigned)sample_smem_bytes(p.n_pad);
+  kp.kernelParams = args;
+  return cudaGraphExecKernelNodeSetParams(exec, node, &kp);
 }
 
 // ---- table init (reading c.6) ----

@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
       sn = warp_sum(sn);
       if (lane == 0) {
         const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
-        a.b.loss[a.loss_slot] = L;
+        a.b.loss[a.s.info[1]] = L;
         const bool bad = !isfinite(L);
         a.b.flags[1] = bad ? 1 : 0;
         if (bad) a.b.flags[0] = 1;

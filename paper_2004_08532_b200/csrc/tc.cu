@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sn = warp_sum(sn);
     if (lane == 0) {
       const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
-      a.loss[a.loss_slot] = L;
+      a.loss[a.s.info[1]] = L;
       const bool bad = !isfinite(L);
       a.flags[1] = bad ? 1 : 0;
       if (bad) a.flags[0] = 1;

@@ -1,2 +1,3 @@
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
-timeout 120 ./tools/tmem_probe > gpurun_out/tmem_probe.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 300 python tools/sample_trace.py > gpurun_out/sample_trace.txt 2>&1
