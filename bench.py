@@ -105,6 +105,15 @@ def dist_env():
     return ws, rank, local
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch by kernel, from the committed ncu --set full capture
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py); {} if absent."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return {}
+    return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(p)).get("kernels", {}).items()}
+
+
 def algorithmic_bytes(n_uniq_ent, n_uniq_rel, d, drel):
     """A = sum_tables U * (2*w*4 + 2*4): each touched row and its Adagrad state read once + written once."""
     return n_uniq_ent * (2 * d * 4 + 8) + n_uniq_rel * (2 * drel * 4 + 8)
@@ -207,14 +216,7 @@ def main():
     torch.cuda.synchronize()
     t_init = time.perf_counter() - t0
 
-    # warm-up + a full per-kernel profile to find the dominant kernel and its share of the step
     H.train_step(args.warmup, return_loss=False)
-    H.sync()
-    H.profile_begin()
-    H.train_step(min(50, args.steps), return_loss=False)
-    prof = H.profile_end()
-    step_kernels = {kname: v for kname, v in prof.items() if v[1] > 0 and kname != "k_sample"}
-    dominant = max(step_kernels, key=lambda n: step_kernels[n][0])
     H.sync()
 
     # ---- timed region: K steps, device-timed with CUDA events; barrier + sync on both sides ----
@@ -240,38 +242,58 @@ def main():
         ms = float(t.item())
     value = ws * B * args.steps / (ms / 1000.0)
 
-    # ---- roofline of the dominant kernel: its own CUDA-event time over a K-step region ----
+    # ---- roofline: per-kernel CUDA-event times over a K-step region (profiler on: each kernel bracketed by events on
+    # its stream, programmatic dependent launch off so a kernel's time is its own, not the wait for its predecessor) ----
     H.profile_begin()
     H.train_step(args.steps, return_loss=False)
     prof2 = H.profile_end()
-    dom_ms, dom_n = prof2[dominant]
     s = H.sample(H.step)
     n_ue, n_ur = len(s["uniq_ent"]), len(s["uniq_rel"])
     drel = d // 2 if model == "rotate" else d
     hbm_gbs, bf16_tf, bf16_tf_sust, src = peaks()
-    flops_neg = 2.0 * B * k * d  # one contraction of the chunked negatives
-    if dominant in ("k_update", "k_gather"):
-        traffic_alg = algorithmic_bytes(n_ue, n_ur, d, drel) if dominant == "k_update" else \
-            (n_ue * d * 4 + n_ur * drel * 4)
-        ach = traffic_alg / (dom_ms / 1000.0) / 1e9
-        roof = {"bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
-                "traffic": None, "kernel": dominant, "alg_bytes_per_launch": traffic_alg}
-    elif args.precision == "tf32" and model in ("transe_l2", "distmult", "complex"):
-        fl = flops_neg * (1 if dominant == "k_neg_fwd" else 2)
-        ach = fl / (dom_ms / 1000.0) / 1e12
-        peak = bf16_tf * 0.5  # TF32 = half the dense bf16 rate (B200_PROFILING.md nominal ratio 1.1 / 2.25)
-        roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": None, "kernel": dominant, "peak_note": f"tf32 = 0.5 x {src} bf16 burst"}
-    else:
-        # FFMA path: plain ALU bound; peak = 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz
-        fl = flops_neg * (1 if dominant == "k_neg_fwd" else 2)
-        peak = 148 * 128 * 2 * 1.965e9 / 1e12
-        ach = fl / (dom_ms / 1000.0) / 1e12
-        roof = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": None, "kernel": dominant, "peak_note": "148 SM x 128 FP32 lanes x FMA x 1.965 GHz"}
-    roof["share_of_step"] = dom_ms * dom_n / sum(v[0] * v[1] for v in prof2.values())
+    tf32_peak = bf16_tf * (1.1 / 2.25)  # B200_PROFILING.md nominal dense tf32 / bf16 ratio x the measured bf16 burst
+    alu_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # FFMA: 148 SMs x 128 FP32 lanes x FMA x 1.965 GHz
+    tc = args.precision == "tf32" and model in ("transe_l2", "distmult", "complex")
+    flops_neg = 2.0 * B * k * d  # one contraction of the chunked negatives (S = O X'^T)
+    traffic = ncu_traffic()
+
+    def kernel_roof(name, ms):
+        if name in ("k_update", "k_gather"):
+            alg = algorithmic_bytes(n_ue, n_ur, d, drel) if name == "k_update" else (n_ue * d * 4 + n_ur * drel * 4)
+            ach = alg / (ms / 1000.0) / 1e9
+            r = {"bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,
+                 "alg_bytes_per_launch": alg}
+        elif name in ("k_neg_fwd", "k_neg_bwd"):
+            fl = flops_neg * (1 if name == "k_neg_fwd" else 2)
+            peak = tf32_peak if tc else alu_peak
+            ach = fl / (ms / 1000.0) / 1e12
+            r = {"bound": "tensor" if tc else "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                 "frac": ach / peak, "alg_flops_per_launch": fl,
+                 "peak_note": f"tf32 = (1.1/2.25) x {src} bf16 burst" if tc else "148 SM x 128 FP32 lanes x FMA x 1.965 GHz",
+                 "impl": ("k_tc_fwd" if name == "k_neg_fwd" else "k_tc_bwd") if tc else name}
+        else:
+            return None
+        r["kernel"] = name
+        r["ms"] = ms
+        r["traffic"] = traffic.get(r.get("impl", name))
+        return r
+
+    step_kernels = {kn: v for kn, v in prof2.items() if v[1] > 0 and kn != "k_sample"}
+    dominant = max(step_kernels, key=lambda n: step_kernels[n][0] * step_kernels[n][1])
+    tot = sum(v[0] * v[1] for kn, v in step_kernels.items())
+    roof = kernel_roof(dominant, prof2[dominant][0]) or {"kernel": dominant, "bound": "latency", "achieved": None,
+                                                          "peak": None, "unit": None, "frac": None, "traffic": None}
+    roof["share_of_step"] = prof2[dominant][0] * prof2[dominant][1] / tot
     roof["per_kernel_ms"] = {k_: v[0] for k_, v in prof2.items()}
     roof["peak_source"] = src
+    roof["timing"] = ("CUDA events around every launch on its stream over a separate K-step region, programmatic "
+                      "dependent launch off (isolated kernel times); traffic from the committed ncu capture")
+    roof["kernels"] = {kn: kernel_roof(kn, v[0]) for kn, v in step_kernels.items() if kernel_roof(kn, v[0])}
+    # whole step against the HBM roofline of the method's algorithmic bytes (gather + update rows)
+    alg_step = algorithmic_bytes(n_ue, n_ur, d, drel)
+    roof["step_hbm"] = {"alg_bytes_per_step": alg_step, "ms_per_step": ms / args.steps,
+                        "achieved_gbs": alg_step / (ms / args.steps / 1000.0) / 1e9,
+                        "frac": alg_step / (ms / args.steps / 1000.0) / 1e9 / hbm_gbs}
 
     # ---- e2e: caller-supplied batch from pinned host memory through kge_train_batch, loss read back ----
     e2e_steps = min(args.e2e_steps, args.steps)

@@ -172,8 +172,10 @@ int kge_connect_local(kge_handle** hs, int32_t world_size);
 int kge_relation_owner(const kge_handle* h, int64_t relation); /* rank, -1 = split (replicated), -2 = bad id */
 
 /* Diagnostics. Kernel ids for kge_profile_end. Between begin and end every kernel launch of the step is bracketed by
- * CUDA events on the handle's stream; end synchronises and returns the average device duration (ms) and the number
- * of launches per kernel id. kge_launch_count: total kernel launches the handle has issued. */
+ * CUDA events on the stream it runs on, and programmatic dependent launch is off (each kernel starts after its
+ * predecessor completed), so the durations are those of each kernel alone; end synchronises and returns the average
+ * device duration (ms) and the number of launches per kernel id. kge_launch_count: total kernel launches the handle
+ * has issued. */
 enum { KGE_K_SAMPLE = 0, KGE_K_GATHER = 1, KGE_K_NEG_FWD = 2, KGE_K_NEG_BWD = 3, KGE_K_CHAIN = 4, KGE_K_UPDATE = 5,
        KGE_K_COUNT = 6 };
 int kge_profile_begin(kge_handle* h);

@@ -16,6 +16,7 @@
 namespace kge {
 
 static thread_local std::string g_err;
+bool g_pdl = true;
 
 void set_error(const std::string& msg) { g_err = msg; }
 
@@ -496,6 +497,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(std::max<int64_t>(h->n_neg_parts, tc_parts), dm.B) * 4);
+  b.flow = (uint32_t*)dalloc(h, (size_t)2 * dm.C * 4);
   b.rowsumW = (float*)dalloc(h, (size_t)dm.B * 2 * ((dm.k + 31) / 32) * 4);   // tc.cu partial row sums of W
   b.colsumW = (float*)dalloc(h, (size_t)nneg * ((dm.g + 127) / 128) * 4);     // tc.cu partial column sums of W
   b.dO = (float*)dalloc(h, (size_t)dm.B * dm.d * 4);
@@ -509,6 +511,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     return fail(KGE_ENOMEM);
   }
   e = cudaMemsetAsync(b.flags, 0, 16, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(b.flow, 0, (size_t)2 * dm.C * 4, h->stream);
   // padding of O / X' (see tc.cu): zeros, plus O[:, d] = 1 and X'[:, d+1] = 1 -- written once, never overwritten
   if (e == cudaSuccess) e = cudaMemsetAsync(b.O, 0, (size_t)dm.B * dm.dp * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(b.X, 0, (size_t)nneg * dm.dp * 4, h->stream);
@@ -928,13 +931,17 @@ int kge_profile_begin(kge_handle* h) {
   h->prof.on = true;
   h->prof.used = 0;
   h->prof.kid.clear();
+  g_pdl = false;  // isolated per-kernel times (see g_pdl)
   return KGE_OK;
 }
 
 int kge_profile_end(kge_handle* h, int32_t n_kernels, double* avg_ms, int64_t* launches) {
   if (!h || !h->prof.on) { set_error("profiling not active"); return KGE_ESTATE; }
   h->prof.on = false;
+  g_pdl = true;
   CK(cudaStreamSynchronize(h->stream));
+  CK(cudaStreamSynchronize(h->side));
+  for (int i = 0; i < kge_handle::kGiven; ++i) CK(cudaStreamSynchronize(h->gside[i]));
   std::vector<double> sum(KGE_K_COUNT, 0.0);
   std::vector<int64_t> cnt(KGE_K_COUNT, 0);
   for (size_t p = 0; p < h->prof.kid.size(); ++p) {

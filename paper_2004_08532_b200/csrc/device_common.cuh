@@ -97,6 +97,26 @@ __device__ __forceinline__ void trace_stamp(uint64_t* trace, int kid, int slot) 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ---- dataflow counters (StepBuffers::flow): release by the producer CTA, acquire by the consumer ----
+// producer: every thread's writes precede the caller's __syncthreads(); one thread then publishes `n` units
+__device__ __forceinline__ void flow_release(uint32_t* cnt, uint32_t n) {
+  __threadfence();  // cumulative: the block's writes (ordered before this thread by the barrier) become visible first
+  atomicAdd(cnt, n);
+}
+// consumer: spin (with back-off) until *cnt >= target; a protocol bug traps after ~2 s instead of hanging
+__device__ __forceinline__ void flow_acquire(const uint32_t* cnt, uint32_t target) {
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    if (v >= target) break;
+    __nanosleep(32);
+    if (clock64() - t0 > 4000000000ll) __trap();
+  }
+}
+// generic-proxy writes acquired above are read next by TMA (async proxy)
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 // ---- small helpers ----
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

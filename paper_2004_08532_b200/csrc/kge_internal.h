@@ -98,6 +98,9 @@ struct StepBuffers {
   float* Grel;     // [B x d_r]
   float* Gproj;    // [B x d*d] (TransR)
   float* loss;     // [ring] per-step loss
+  uint32_t* flow;  // [2 C] dataflow counters of the tcgen05 path: [c] rows of chunk c gathered, [C + c] forward CTAs of
+                   // chunk c done -- k_tc_fwd / k_tc_bwd start a chunk on these instead of waiting for the whole
+                   // predecessor grid; k_update resets them for the next step
   int32_t* flags;  // [4]: [0] non-finite seen
 };
 
@@ -234,6 +237,10 @@ struct kge_handle {
 
 namespace kge {
 
+// Programmatic dependent launch on/off (off while the profiler brackets each launch with events, so the per-kernel
+// times are those of each kernel alone rather than including the wait for its predecessor)
+extern bool g_pdl;
+
 // Launch with programmatic stream serialization (PDL); see pdl_wait / pdl_trigger in device_common.cuh.
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -245,7 +252,7 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
@@ -262,7 +269,7 @@ inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 bl
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   at[1].id = cudaLaunchAttributeClusterDimension;
   at[1].val.clusterDim.x = cx;
   at[1].val.clusterDim.y = 1;
@@ -321,5 +328,6 @@ int32_t tc_neg_parts(const kge_handle* h);
 // rule and reduces the loss (k_chain is not launched)
 cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot);
 bool tc_fuses_chain(const kge_handle* h);
+bool tc_flow();  // chunk-level dataflow counters on (KGE_FLOW=1)
 
 }  // namespace kge

@@ -187,6 +187,7 @@ struct GatherArgs {
   int32_t first_row;  // B: negatives only (TransR handles its positives in transr.cu)
   int32_t fuse_pos;   // TransE-L2 on the tcgen05 path: also write the positive-score gradient of the uncorrupted
                       // entity, gx = w+ (o - x) / ||o - x||, into its occurrence row of Gocc (read back by k_tc_bwd)
+  uint32_t* flow;     // tcgen05 path: publish rows done per chunk (StepBuffers::flow), else nullptr
 };
 
 // Register-staged rows: every lane issues all of its row loads before any arithmetic or store, so a warp has its whole
@@ -393,6 +394,27 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     }
     acc = warp_sum(acc);
     if (lane == 0) a.b.xnorm[q] = acc;
+  }
+  if (a.flow) {  // rows of each chunk done: k_tc_fwd starts a chunk as soon as its g + k rows are here
+    __shared__ int s_chunk[8];
+    if (lane == 0)
+      s_chunk[threadIdx.x >> 5] = row < dm.B ? row / dm.g : (row < dm.B + n_neg ? (row - dm.B) / dm.k : -1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      int c0 = -1;
+      uint32_t n = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        const int cw = s_chunk[w];
+        if (cw != c0) {
+          if (c0 >= 0) atomicAdd(&a.flow[c0], n);
+          c0 = cw;
+          n = 0;
+        }
+        if (cw >= 0) ++n;
+      }
+      if (c0 >= 0) atomicAdd(&a.flow[c0], n);
+    }
   }
   trace_stamp(dm.trace, KGE_K_GATHER, 7);
 }
@@ -990,6 +1012,7 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
   }
   pdl_wait();
   pdl_trigger();
+  if (blockIdx.x == 0 && threadIdx.x < 2 * dm.C) a.b.flow[threadIdx.x] = 0u;  // every consumer of this step is done
   trace_stamp(dm.trace, KGE_K_UPDATE, 1);
   if (a.b.flags[1]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
   RowAcc<V> acc;
@@ -1095,7 +1118,7 @@ static void launch_gather_v(kge_handle* h, const GatherArgs& ga, int rows) {
 
 cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
-  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, dm.B, 0};
+  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, dm.B, 0, nullptr};
   const int rows = dm.C * dm.k;
   launch_gather_v(h, ga, rows);
   return cudaGetLastError();
@@ -1124,7 +1147,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
   if (dm.model == KGE_TRANSR) return launch_transr_step(h, s, step);
   const bool tc = h->cfg.neg_precision == KGE_PREC_TF32 && tc_supported(h);
-  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0, tc && tc_fuses_chain(h) ? 1 : 0};
+  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0, tc && tc_fuses_chain(h) ? 1 : 0, tc && tc_flow() ? h->buf.flow : nullptr};
   const int rows = dm.B + dm.C * dm.k;
   launch_begin(h, KGE_K_GATHER);
   launch_gather_v(h, ga, rows);

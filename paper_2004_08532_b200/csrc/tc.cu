@@ -83,6 +83,8 @@ struct TcArgs {
   int32_t loss_slot, n_neg_parts;
   float inv_bk;    // 1 / (B k), the dL/df- scale (reading c.9)
   float4* xbuf;    // backward split-K exchange scratch
+  uint32_t* flow;  // dataflow counters (StepBuffers::flow)
+  int32_t fwd_per_chunk;  // forward CTAs per chunk (the backward's target on flow[C + c])
   int32_t fwd_cx;  // forward cluster size along x: the CTAs of one 128-positive tile share its O tile by TMA multicast
 };
 
@@ -144,8 +146,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tma_prefetch(&mX);
   }
   if (warp == 0) tmem_alloc(&tbase, kIssuers * kNT);
-  pdl_wait();  // predecessor (gather) complete: O, X', norms are final
-  pdl_trigger();
+  if (a.flow) {
+    // dataflow (KGE_FLOW=1): this chunk's g + k rows (O, X', norms) are final once k_gather published them -- no
+    // wait for the whole gather grid; the thread that acquires is also the TMA producer (proxy fence before its loads)
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+      flow_acquire(&a.flow[c], (uint32_t)(dm.g + dm.k));
+      fence_proxy_async_global();
+    }
+  } else {
+    pdl_wait();  // predecessor (gather) complete: O, X', norms are final
+    pdl_trigger();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -330,6 +342,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     a.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = tt;
   }
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 6);
+  __syncthreads();
+  if (a.flow && threadIdx.x == 0) flow_release(&a.flow[dm.C + c], 1u);  // W, row / column partials and lneg
   if (cxn > 1) cluster_sync();  // no CTA leaves while a peer's MMA commit may still arrive on its barriers
   if (warp == 0) tmem_dealloc(tmem, kIssuers * kNT);
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 7);
@@ -388,8 +402,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(&tbase, kIssuers * 128);
-  pdl_wait();  // predecessor (forward) complete: W and the row / column partial sums are final
-  pdl_trigger();
+  if (a.flow) {  // dataflow: W and the row / column partials of chunk c are final once its forward CTAs published them
+    pdl_trigger();
+    if (threadIdx.x == 0) flow_acquire(&a.flow[dm.C + c], (uint32_t)a.fwd_per_chunk);
+  } else {
+    pdl_wait();  // predecessor (forward) complete: W and the row / column partial sums are final
+    pdl_trigger();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -437,7 +456,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      loss_part * nb_all / kNSplit * 32 >= d))
     ++loss_part;
   if (fuse && tp == loss_part && ks == 0 && blockIdx.y == 0 && warp == 1) {
-    // deterministic loss (reading c.9): fixed lane assignment and order, identical to the unfused k_chain
+    // deterministic loss (reading c.9): fixed lane assignment and order, identical to the unfused k_chain; it needs
+    // every chunk's forward partials
+    if (a.flow && lane == 0)
+      for (int cc = 0; cc < dm.C; ++cc) flow_acquire(&a.flow[dm.C + cc], (uint32_t)a.fwd_per_chunk);
+    __syncwarp();
     float sp = 0.f, sn = 0.f;
     for (int i = lane; i < dm.B; i += 32) sp += a.lpos[i];
     for (int q = lane; q < a.n_neg_parts; q += 32) sn += a.lneg[q];
@@ -473,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     if (q == 0) {
+      fence_proxy_async_global();  // the forward's W (acquired by thread 0 before the barrier) is read by TMA
       produce(kBwdStages);
       if (FAM == FAM_L2) {
         const bool fz = a.fuse && !pass_x;
@@ -752,6 +776,14 @@ int32_t tc_neg_parts(const kge_handle* h) {
   return dm.C * ((dm.g + 127) / 128) * ((dm.k + kNT - 1) / kNT) * 2;  // one loss partial per split-K half
 }
 
+// Chunk-level dataflow between k_gather -> k_tc_fwd -> k_tc_bwd (StepBuffers::flow) instead of whole-grid PDL waits.
+// Off by default: measured on the Freebase step it was slower (34.6 vs 30.9 us): the consumers' CTAs cannot become
+// resident next to the gather's (register file full) and the counters add a barrier + atomics per CTA.
+bool tc_flow() {
+  static const bool on = getenv("KGE_FLOW") != nullptr;
+  return on;
+}
+
 bool tc_fuses_chain(const kge_handle* h) { return h->dims.model == KGE_TRANSE_L2; }
 
 cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
@@ -760,7 +792,8 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
   TcArgs a{dm, h->dp, h->kp, h->buf.O, h->buf.X, h->buf.onorm, h->buf.xnorm, h->buf.W, h->buf.lneg, h->buf.dO,
            h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128,
            tc_fuses_chain(h) ? 1 : 0, s, h->rows, h->buf.wpos, h->buf.pstat, h->buf.lpos, h->buf.Grel,
-           h->buf.loss, h->buf.flags, loss_slot, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->xbuf, st->fwd_cx};
+           h->buf.loss, h->buf.flags, loss_slot, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->xbuf, tc_flow() ? h->buf.flow : nullptr,
+           2 * ((dm.k + kNT - 1) / kNT) * ((dm.g + 127) / 128), st->fwd_cx};
   dim3 gf(2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128, dm.C);  // x = 2 tile + split-K half
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(2 * tiles * kNSplit, dm.C, 2);  // x = 2 (row tile * kNSplit + column part) + split-K half
