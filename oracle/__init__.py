@@ -30,7 +30,8 @@ class Config(ctypes.Structure):
                 ("neg_k", ctypes.c_int32),
                 ("gamma", ctypes.c_float), ("lr", ctypes.c_float), ("eps", ctypes.c_float),
                 ("init_bound", ctypes.c_float), ("seed", ctypes.c_uint64), ("corrupt", ctypes.c_int32),
-                ("rotate_variant", ctypes.c_int32), ("world_size", ctypes.c_int32), ("lazy_rows", ctypes.c_int32)]
+                ("rotate_variant", ctypes.c_int32), ("world_size", ctypes.c_int32), ("lazy_rows", ctypes.c_int32),
+                ("lag", ctypes.c_int32)]
 
 
 TRIPLE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, _i64p, _i64p, _i64p)
@@ -80,6 +81,7 @@ def lib():
         L.orc_sample.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, _i64p, _i64p, P(ctypes.c_int8)]
         L.orc_occurrences.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, _i64p, _i64p]
         L.orc_train.argtypes = [ctypes.c_void_p, ctypes.c_int64, _dp]
+        L.orc_flush.argtypes = [ctypes.c_void_p]
         L.orc_get_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _dp]
         L.orc_set_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _dp]
         L.orc_score_triples.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, _dp]
@@ -216,12 +218,12 @@ class Trainer:
 
     def __init__(self, model, n_entities, n_relations, dim, batch, chunk, neg_k, gamma=12.0, lr=0.1, eps=1e-10,
                  init_bound=0.0, seed=1, corrupt=ALTERNATE, rotate_variant=0, world_size=1, precision=0,
-                 triples=None, graph=None, lazy_rows=False):
+                 triples=None, graph=None, lazy_rows=False, lag=0):
         if isinstance(model, str):
             model = MODEL_IDS[model]
         self.model = model
         self.cfg = Config(model, precision, n_entities, n_relations, dim, batch, chunk, neg_k, gamma, lr, eps,
-                          init_bound, seed, corrupt, rotate_variant, world_size, int(lazy_rows))
+                          init_bound, seed, corrupt, rotate_variant, world_size, int(lazy_rows), int(lag))
         self._keep = []
         if triples is not None:
             h, r, t = [np.ascontiguousarray(a, dtype=np.int64) for a in triples]
@@ -267,6 +269,10 @@ class Trainer:
         losses = np.zeros(n_steps)
         lib().orc_train(self.h, n_steps, _p(losses, ctypes.c_double))
         return losses
+
+    def flush(self):
+        """lag = 1: apply the held-back entity update of the last step."""
+        lib().orc_flush(self.h)
 
     def width(self, table):
         return lib().orc_table_width(self.h, table)

@@ -431,6 +431,7 @@ struct Base {
   virtual int set_rows(int32_t table, const int64_t* ids, int64_t n, const double* in) = 0;
   virtual int score_triples(const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, double* out) = 0;
   virtual int32_t width(int32_t table) = 0;
+  virtual int flush() = 0;
 
   void triple(int64_t i, int64_t& h, int64_t& r, int64_t& t) const {
     if (fn) {
@@ -597,11 +598,32 @@ struct Trainer : Base {
           }
       }
       if (losses) losses[it] = (double)loss_total;
-      // (4) apply: dedup over the union (rank-major occurrence order), sum in segment order, Adagrad (c.11)
-      apply(ent, ent_st, ent_ids, Gent, d);
+      // (4) apply: dedup over the union (rank-major occurrence order), sum in segment order, Adagrad (c.11).
+      // lag = 1 (reading c.12): relations (and TransR projections) are updated now; the entity
+      // update of this step is held back and applied after the next step has computed its gradients, i.e. step s
+      // reads entity rows updated by steps <= s-2 -- the previous step's entity update is applied here, after this
+      // step's forward/backward
       apply(rel, rel_st, rel_ids, Grel, drel);
       if (has_proj) apply(proj, proj_st, rel_ids, Gproj, d * d);
+      if (cfg.lag == 1) {
+        flush();
+        pend_ids.swap(ent_ids);
+        pend_G.swap(Gent);
+        pending = true;
+      } else {
+        apply(ent, ent_st, ent_ids, Gent, d);
+      }
     }
+    return 0;
+  }
+
+  // lag = 1: the held-back entity update of the last step
+  std::vector<int64_t> pend_ids;
+  std::vector<T> pend_G;
+  bool pending = false;
+  int flush() override {
+    if (pending) apply(ent, ent_st, pend_ids, pend_G, d);
+    pending = false;
     return 0;
   }
 
@@ -823,6 +845,7 @@ void* orc_create(const orc_config* cfg, const int64_t* heads, const int64_t* rel
   if (!cfg || cfg->batch <= 0 || cfg->chunk <= 0 || cfg->batch % cfg->chunk != 0 || cfg->neg_k <= 0) return nullptr;
   if ((cfg->model == ORC_COMPLEX || cfg->model == ORC_ROTATE) && cfg->dim % 2 != 0) return nullptr;
   if (cfg->world_size < 1 || n_triples <= 0) return nullptr;
+  if (cfg->lag != 0 && cfg->lag != 1) return nullptr;
   Base* b;
   if (cfg->precision == 1) {
     auto* t = new Trainer<float>();
@@ -885,6 +908,7 @@ int orc_occurrences(void* hp, int64_t step, int32_t rank, int64_t* ent_occ, int6
   return 0;
 }
 int orc_train(void* h, int64_t n_steps, double* losses) { return static_cast<Base*>(h)->train(n_steps, losses); }
+int orc_flush(void* h) { return static_cast<Base*>(h)->flush(); }
 int orc_get_rows(void* h, int32_t table, const int64_t* ids, int64_t n, double* out) {
   return static_cast<Base*>(h)->get_rows(table, ids, n, out);
 }

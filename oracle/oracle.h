@@ -44,6 +44,8 @@ typedef struct {
   int32_t rotate_variant;   /* 0 = Table-1 squared, 1 = modulus sum */
   int32_t world_size;       /* P simulated ranks */
   int32_t lazy_rows;        /* 1: rows materialised on first touch (Freebase-sized N_e) */
+  int32_t lag;              /* 0: synchronous; 1: the entity-table update of step s is applied after step s+1 computed
+                               its gradients (deterministic form of PAPER.md:515-534; relations stay synchronous) */
 } orc_config;
 
 typedef void (*orc_triple_fn)(void* ctx, int64_t i, int64_t* h, int64_t* r, int64_t* t);
@@ -91,6 +93,8 @@ int orc_sample(void* h, int64_t step, int32_t rank, int64_t* pos_idx, int64_t* n
 /* entity occurrence ids of one rank-step [h..., t..., neg...] and relation occurrence ids [r...] */
 int orc_occurrences(void* h, int64_t step, int32_t rank, int64_t* ent_occ, int64_t* rel_occ);
 int orc_train(void* h, int64_t n_steps, double* losses);
+/* lag = 1: apply the pending entity update of the last step (no-op otherwise). */
+int orc_flush(void* h);
 int orc_get_rows(void* h, int32_t table, const int64_t* ids, int64_t n, double* out);
 int orc_set_rows(void* h, int32_t table, const int64_t* ids, int64_t n, const double* in);
 int orc_score_triples(void* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, double* out);
