@@ -172,6 +172,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--lag", type=int, default=0, choices=[0, 1],
+                    help="1: the paper's overlap of the entity update with the next step (reading c.12)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -205,7 +207,7 @@ def main():
     t_gen = time.perf_counter() - t0
     cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=d, batch_size=B,
                      chunk_size=g, neg_k=k, gamma=12.0, lr=0.1, seed=1, neg_precision=args.precision,
-                     world_size=ws, rank=rank)
+                     world_size=ws, rank=rank, lag=args.lag)
     stream = torch.cuda.Stream()  # the library enqueues on this stream; events below are recorded on it
     t0 = time.perf_counter()
     with torch.cuda.stream(stream):
@@ -335,7 +337,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "tf32", "data": "synthetic",
                 "config": {"workload": f"{gname}-shaped synthetic (BASELINE.json configs)", "model": model, "dim": d,
-                           "batch": B, "chunk": g, "neg_k": k, "n_entities": gr.n_entities,
+                           "batch": B, "chunk": g, "neg_k": k, "lag": args.lag, "n_entities": gr.n_entities,
                            "n_relations": gr.n_relations, "n_triples": gr.n_triples,
                            "parallelism": f"dp{ws}" + (" (relation-partitioned triples, entity rows sharded e mod P, "
                                                        "exchange over NVLink peer memory)" if ws > 1 else ""),

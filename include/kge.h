@@ -84,7 +84,10 @@ typedef struct {
   int32_t corrupt;         /* kge_corrupt */
   int32_t neg_precision;   /* kge_precision */
   int32_t rotate_variant;  /* RotatE: 0 = Table-1 squared (default), 1 = modulus sum */
-  int32_t lag;             /* 0 = synchronous (reading c.12); other values -> KGE_EUNSUPPORTED in this build */
+  int32_t lag;             /* 0 = synchronous (reading c.12). 1 = the paper's overlap of the entity update with the next
+                              mini-batch (PAPER.md:515-534 [3.5]) made deterministic: step s reads entity rows updated
+                              by steps <= s-2 and relation rows by steps <= s-1; the entity update of the last step
+                              is held back until the next step or kge_flush. P > 1 or TransR -> KGE_EUNSUPPORTED. */
   int32_t world_size;      /* P ranks (one process per GPU) */
   int32_t rank;            /* this rank */
   void* nccl_comm;         /* ncclComm_t shared with the caller, or NULL */
@@ -146,6 +149,8 @@ int32_t kge_table_width(const kge_handle* h, int32_t table);
 /* Next step index (steps are counter-based: (seed, step) fixes every sample, so resume is exact). */
 int64_t kge_step(const kge_handle* h);
 int kge_set_step(kge_handle* h, int64_t step);
+/* lag = 1: apply the held-back entity update of the last step now (no-op when none / lag = 0). kge_set_step flushes. */
+int kge_flush(kge_handle* h);
 
 /* Wait for all enqueued work; reports KGE_ENONFINITE if any step since the last check had a non-finite loss. */
 int kge_sync(kge_handle* h);

@@ -115,7 +115,11 @@ static int validate(const kge_config* c) {
   }
   if (c->corrupt < 0 || c->corrupt > 2) { set_error("bad corrupt"); return KGE_EINVAL; }
   if (c->neg_precision < 0 || c->neg_precision > 1) { set_error("bad neg_precision"); return KGE_EINVAL; }
-  if (c->lag != 0) { set_error("lag != 0 not implemented in this build"); return KGE_EUNSUPPORTED; }
+  if (c->lag != 0 && c->lag != 1) { set_error("lag must be 0 or 1"); return KGE_EINVAL; }
+  if (c->lag == 1 && (c->world_size > 1 || c->model == KGE_TRANSR)) {
+    set_error("lag = 1 is implemented for one rank and the non-TransR models");
+    return KGE_EUNSUPPORTED;
+  }
   if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size) { set_error("bad world_size/rank"); return KGE_EINVAL; }
   if (c->world_size > kMaxRanks) { set_error("world_size > 8 (one node) not supported"); return KGE_EINVAL; }
   if (c->world_size > 1 && c->model == KGE_TRANSR) { set_error("TransR with world_size > 1 is not built yet"); return KGE_EUNSUPPORTED; }
@@ -461,6 +465,10 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     for (int i = 0; i < kge_handle::kGiven; ++i)
       if (cudaStreamCreateWithPriority(&h->gside[i], cudaStreamNonBlocking, hi) != cudaSuccess)
         return fail(cuda_fail(cudaGetLastError(), "side stream"));
+    if (cudaStreamCreateWithFlags(&h->ustream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_eread, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_eupd, cudaEventDisableTiming) != cudaSuccess)
+      return fail(cuda_fail(cudaGetLastError(), "update stream"));
   }
   for (int i = 0; i < 2; ++i)
     if (cudaEventCreateWithFlags(&h->ev_samp[i], cudaEventDisableTiming) != cudaSuccess ||
@@ -501,7 +509,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.rowsumW = (float*)dalloc(h, (size_t)dm.B * 2 * ((dm.k + 31) / 32) * 4);   // tc.cu partial row sums of W
   b.colsumW = (float*)dalloc(h, (size_t)nneg * ((dm.g + 127) / 128) * 4);     // tc.cu partial column sums of W
   b.dO = (float*)dalloc(h, (size_t)dm.B * dm.d * 4);
-  b.Gocc = (float*)dalloc(h, (size_t)dm.n_occ * dm.d * 4);
+  b.Gocc = (float*)dalloc(h, (size_t)(cfg->lag == 1 ? 2 : 1) * dm.n_occ * dm.d * 4);
+  h->gocc2[0] = b.Gocc;
+  h->gocc2[1] = cfg->lag == 1 && b.Gocc ? b.Gocc + (size_t)dm.n_occ * dm.d : b.Gocc;
   b.Grel = (float*)dalloc(h, (size_t)dm.B * dm.drel * 4);
   b.loss = (float*)dalloc(h, (size_t)h->ring * 4);
   h->seg_cnt = (int32_t*)dalloc(h, (size_t)(dm.B + dm.n_occ) * 4);
@@ -523,7 +533,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
       e = cudaMemcpy2DAsync(b.X + dm.d + 1, (size_t)dm.dp * 4, ones.data(), 4, 4, nneg, cudaMemcpyHostToDevice, h->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   }
-  if (e == cudaSuccess) e = cudaMemsetAsync(b.Gocc, 0, (size_t)dm.n_occ * dm.d * 4, h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(b.Gocc, 0, (size_t)(cfg->lag == 1 ? 2 : 1) * dm.n_occ * dm.d * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->seg_cnt, 0, (size_t)(dm.B + dm.n_occ) * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h), h->slots.data(), sizeof(Slot) * h->ring, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_slots(h) + h->ring, &h->debug_slot, sizeof(Slot), cudaMemcpyHostToDevice, h->stream);
@@ -562,22 +573,13 @@ static int ensure_sampled(kge_handle* h, int64_t s) {
     if (e != cudaSuccess) return cuda_fail(e, "sample wait");
     h->half_waited[q] = true;
   }
-  if (h->P == 1 && h->half_first[1 - q] != hs + H) {
-    // the other half's slots were last read by steps < hs, all enqueued on the main stream before this point: fill
-    // them with steps [hs + H, hs + 2H). (P > 1 samples in order on the main stream: with several ranks sharing one
-    // device, as the emulated-rank tests do, side-stream samplers could hold the SMs the ranks' device barriers need.)
-    e = cudaEventRecord(h->ev_free[1 - q], h->stream);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->side, h->ev_free[1 - q], 0);
-    if (e == cudaSuccess) e = launch_sample(h, p, d_slots(h), h->ring, hs + H, H, h->side);
-    if (e == cudaSuccess) e = cudaEventRecord(h->ev_samp[1 - q], h->side);
-    if (e != cudaSuccess) return cuda_fail(e, "sample ahead");
-    h->half_first[1 - q] = hs + H;
-    h->half_waited[1 - q] = false;
-  }
   return KGE_OK;
 }
 
+static int join_updates(kge_handle* h);
 static int check_flags(kge_handle* h) {
+  const int rj = join_updates(h);
+  if (rj != KGE_OK) return rj;
   int32_t f[4];
   cudaError_t e = cudaMemcpyAsync(f, h->buf.flags, 16, cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
@@ -587,6 +589,79 @@ static int check_flags(kge_handle* h) {
     set_error("a step produced a non-finite loss; its update was skipped");
     return KGE_ENONFINITE;
   }
+  return KGE_OK;
+}
+
+// Fill the other ring half with steps [hs + H, hs + 2H) on the side stream. Its slots were last read by steps < hs,
+// all enqueued before this point on the main stream (and, lag = 1, by the held-back entity update enqueued with
+// step s on the update stream). (P > 1 samples in order on the main stream: with several ranks sharing one device,
+// as the emulated-rank tests do, side-stream samplers could hold the SMs the ranks' device barriers need.)
+static int prefetch_half(kge_handle* h, int64_t s) {
+  const int H = h->ring / 2;
+  const int64_t hs = s - s % H;
+  const int q = (int)((hs / H) % 2);
+  if (h->P != 1 || h->half_first[1 - q] == hs + H) return KGE_OK;
+  SampleParams p = sample_params(h, false);
+  cudaError_t e = cudaEventRecord(h->ev_free[1 - q], h->stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(h->side, h->ev_free[1 - q], 0);
+  if (e == cudaSuccess && h->eupd_enqueued) e = cudaStreamWaitEvent(h->side, h->ev_eupd, 0);
+  if (e == cudaSuccess) e = launch_sample(h, p, d_slots(h), h->ring, hs + H, H, h->side);
+  if (e == cudaSuccess) e = cudaEventRecord(h->ev_samp[1 - q], h->side);
+  if (e != cudaSuccess) return cuda_fail(e, "sample ahead");
+  h->half_first[1 - q] = hs + H;
+  h->half_waited[1 - q] = false;
+  return KGE_OK;
+}
+
+// One step on the main stream. lag = 1 (reading c.12): the step's gather waits for the entity update of step s-2;
+// the entity update of step s-1 is enqueued on the update stream behind this step's last entity-table read
+// (ev_eread) and the current step's is held back.
+static int enqueue_step(kge_handle* h, const Slot& slot, int64_t s, int gi) {
+  cudaError_t e = cudaSuccess;
+  if (h->cfg.lag == 1) {
+    if (h->eupd_enqueued) e = cudaStreamWaitEvent(h->stream, h->ev_eupd, 0);
+    h->buf.Gocc = h->gocc2[s & 1];
+  }
+  if (e == cudaSuccess) e = launch_step(h, slot, s);
+  if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, slot);
+  if (e != cudaSuccess) return cuda_fail(e, "step");
+  if (h->cfg.lag == 1) {
+    if (h->pend_step >= 0) {
+      const Dims& dm = h->dims;
+      e = cudaStreamWaitEvent(h->ustream, h->ev_eread, 0);
+      if (e == cudaSuccess)
+        e = launch_update_range(h, h->pend_slot, dm.B, dm.B + dm.n_occ, h->ustream, h->gocc2[h->pend_step & 1]);
+      if (e == cudaSuccess) e = cudaEventRecord(h->ev_eupd, h->ustream);
+      if (e == cudaSuccess && h->pend_gi >= 0) e = cudaEventRecord(h->ev_gfree[h->pend_gi], h->ustream);
+      if (e != cudaSuccess) return cuda_fail(e, "entity update");
+      h->eupd_enqueued = true;
+    }
+    h->pend_step = s;
+    h->pend_slot = slot;
+    h->pend_gi = gi;
+  }
+  return KGE_OK;
+}
+
+// the main stream waits for the update stream (table reads / writes from the host API see every enqueued update)
+static int join_updates(kge_handle* h) {
+  if (h->eupd_enqueued) {
+    cudaError_t e = cudaStreamWaitEvent(h->stream, h->ev_eupd, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "join");
+  }
+  return KGE_OK;
+}
+
+int kge_flush(kge_handle* h) {
+  if (!h) { set_error("NULL handle"); return KGE_EINVAL; }
+  int rc = join_updates(h);
+  if (rc != KGE_OK || h->pend_step < 0) return rc;
+  const Dims& dm = h->dims;
+  cudaError_t e = launch_update_range(h, h->pend_slot, dm.B, dm.B + dm.n_occ, h->stream, h->gocc2[h->pend_step & 1]);
+  if (e == cudaSuccess && h->pend_gi >= 0) e = cudaEventRecord(h->ev_gfree[h->pend_gi], h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "flush");
+  h->pend_step = -1;
+  h->pend_gi = -1;
   return KGE_OK;
 }
 
@@ -606,9 +681,11 @@ int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
     }
     int rc = ensure_sampled(h, s);
     if (rc != KGE_OK) return rc;
-    cudaError_t e = launch_step(h, h->slots[s % h->ring], s);
-    if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, h->slots[s % h->ring]);
-    if (e != cudaSuccess) return cuda_fail(e, "step");
+    rc = enqueue_step(h, h->slots[s % h->ring], s, -1);
+    if (rc != KGE_OK) return rc;
+    rc = prefetch_half(h, s);
+    if (rc != KGE_OK) return rc;
+    cudaError_t e = cudaSuccess;
     if (loss_out) {
       e = cudaMemcpyAsync(h->pinned_loss + (it % h->ring), h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost, h->stream);
       if (e != cudaSuccess) return cuda_fail(e, "loss readback");
@@ -628,7 +705,7 @@ int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
 // Enqueue one step on a caller-supplied batch; loss_dev_to: host destination of an async loss copy (or NULL).
 static bool use_graphs(const kge_handle* h) {
   static const bool off = getenv("KGE_NO_GRAPHS") != nullptr || getenv("KGE_DEBUG_SYNC") != nullptr;
-  return h->P == 1 && !off && !h->prof.on && h->dims.trace == nullptr;
+  return h->P == 1 && h->cfg.lag == 0 && !off && !h->prof.on && h->dims.trace == nullptr;
 }
 
 // capture `body` (launches on stream st) into an instantiated graph; the first node of the given type is returned
@@ -756,9 +833,9 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
   if (e == cudaSuccess && h->P == 1) e = cudaEventRecord(h->ev_gsamp[gi], ss);
   if (e == cudaSuccess && h->P == 1) e = cudaStreamWaitEvent(h->stream, h->ev_gsamp[gi], 0);
   if (e != cudaSuccess) return cuda_fail(e, "sample");
-  e = launch_step(h, h->given_slots[gi], s);
-  if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, h->given_slots[gi]);
-  if (e == cudaSuccess && h->P == 1) e = cudaEventRecord(h->ev_gfree[gi], h->stream);
+  const int rcs = enqueue_step(h, h->given_slots[gi], s, gi);
+  if (rcs != KGE_OK) return rcs;
+  if (h->P == 1 && h->cfg.lag == 0) e = cudaEventRecord(h->ev_gfree[gi], h->stream);  // lag 1: after its entity update
   if (e != cudaSuccess) return cuda_fail(e, "step");
   h->step = s + 1;
   if (loss_host) {
@@ -844,6 +921,8 @@ static int rows_io(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, 
   float* tab = table_ptr(h, table, &w, &rows);
   if (!tab) { set_error("table not present for this model"); return KGE_EINVAL; }
   if (n == 0) return KGE_OK;
+  const int rj = join_updates(h);
+  if (rj != KGE_OK) return rj;
   std::vector<int32_t> ids32(n);
   const bool sharded = h->P > 1 && (table == 0 || table == 3);
   for (int64_t i = 0; i < n; ++i) {
@@ -887,6 +966,8 @@ int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t
     ids[n + i] = (int32_t)rs[i];
     ids[2 * n + i] = (int32_t)ts[i];
   }
+  const int rj = join_updates(h);
+  if (rj != KGE_OK) return rj;
   int32_t* d_ids = nullptr;
   float* d_out = nullptr;
   CK(cudaMallocAsync((void**)&d_ids, (size_t)3 * n * 4, h->stream));
@@ -917,6 +998,8 @@ int kge_read_losses(kge_handle* h, int64_t first_step, int64_t n, float* out) {
 
 int kge_set_step(kge_handle* h, int64_t step) {
   if (!h || step < 0) { set_error("bad argument"); return KGE_EINVAL; }
+  const int rf = kge_flush(h);  // lag = 1: a held-back entity update belongs to the step sequence being left
+  if (rf != KGE_OK) return rf;
   h->step = step;
   return KGE_OK;
 }
@@ -982,6 +1065,12 @@ void kge_destroy(kge_handle* h) {
     if (h->stage_ev[i]) cudaEventDestroy(h->stage_ev[i]);
   if (h->pinned_loss) cudaFreeHost(h->pinned_loss);
   if (h->side) cudaStreamSynchronize(h->side);
+  if (h->ustream) {
+    cudaStreamSynchronize(h->ustream);
+    cudaStreamDestroy(h->ustream);
+  }
+  if (h->ev_eread) cudaEventDestroy(h->ev_eread);
+  if (h->ev_eupd) cudaEventDestroy(h->ev_eupd);
   for (int i = 0; i < 2; ++i) {
     if (h->ev_samp[i]) cudaEventDestroy(h->ev_samp[i]);
     if (h->ev_free[i]) cudaEventDestroy(h->ev_free[i]);

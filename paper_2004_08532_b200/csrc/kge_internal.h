@@ -190,6 +190,15 @@ struct kge_handle {
   // sampling runs on a side stream ahead of the steps (k_sample is a pure function of (seed, step)): the ring is two
   // halves of ring/2 steps; while the main stream works through one half the side stream fills the other
   cudaStream_t side = nullptr;
+  // lag = 1 (reading c.12): the entity update of step s runs on ustream after step s+1 stops reading the entity table
+  // (ev_eread) and before step s+2's gather (ev_eupd); Gocc is double-buffered by step parity
+  cudaStream_t ustream = nullptr;
+  cudaEvent_t ev_eread = nullptr, ev_eupd = nullptr;
+  int64_t pend_step = -1;   // step whose entity update is held back (-1: none)
+  kge::Slot pend_slot{};
+  int32_t pend_gi = -1;     // its caller-batch slot, or -1 (ring slot)
+  bool eupd_enqueued = false;
+  float* gocc2[2] = {};     // the two Gocc buffers (lag = 1), else both = buf.Gocc
   cudaEvent_t ev_samp[2] = {}, ev_free[2] = {};
   int64_t half_first[2] = {-1, -1};  // first step held by each ring half (-1: none)
   bool half_waited[2] = {false, false};
@@ -305,6 +314,7 @@ cudaError_t launch_rows(kge_handle* h, float* tab, int32_t w, const int32_t* ids
 
 cudaError_t launch_gather_neg(kge_handle* h, const Slot& s);
 cudaError_t launch_update(kge_handle* h, const Slot& s);
+cudaError_t launch_update_range(kge_handle* h, const Slot& s, int lo, int hi, cudaStream_t st, float* gocc);
 
 // transr.cu
 cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step);

@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
         const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
         a.b.loss[a.s.info[1]] = L;
         const bool bad = !isfinite(L);
-        a.b.flags[1] = bad ? 1 : 0;
+        a.b.flags[2 + (a.s.info[0] & 1)] = bad ? 1 : 0;
         if (bad) a.b.flags[0] = 1;
       }
     }
@@ -906,6 +906,7 @@ struct UpdateArgs {
   const int32_t* split_index;  // P > 1: relation -> index among split relations, -1 if not split
   float* grel_split;           // P > 1: per-rank sums of split relations
   int32_t* seg_cnt;            // [B + n_occ] per-unique-row segment arrival counters (zero between steps)
+  int32_t pos_lo, pos_hi;      // positions handled: [0, B) relations, [B, B + n_occ) entities (lag = 1 splits them)
 };
 
 // Row accumulator: V float4 per lane.
@@ -971,7 +972,7 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
   const Dims& dm = a.dm;
   trace_stamp(dm.trace, KGE_K_UPDATE, 0);
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int gw = a.pos_lo + blockIdx.x * 8 + (threadIdx.x >> 5);
   const bool rel = gw < dm.B;
   const int p = rel ? gw : gw - dm.B;
   const int npos = rel ? dm.B : dm.n_occ;
@@ -979,7 +980,7 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
   const int32_t* off = rel ? a.s.rel_off : a.s.ent_off;
   float* G = rel ? a.b.Grel : a.b.Gocc;
   const int w = rel ? dm.drel : dm.d, w4 = w >> 2;
-  bool live = p < npos;
+  bool live = p < npos && gw < a.pos_hi;
   int u = 0, r0 = 0, r1 = 0;
   if (live) {
     u = (rel ? a.s.rel_inv : a.s.ent_inv)[occ_sorted[p]];
@@ -1012,9 +1013,9 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
   }
   pdl_wait();
   pdl_trigger();
-  if (blockIdx.x == 0 && threadIdx.x < 2 * dm.C) a.b.flow[threadIdx.x] = 0u;  // every consumer of this step is done
+  if (a.pos_lo == 0 && blockIdx.x == 0 && threadIdx.x < 2 * dm.C) a.b.flow[threadIdx.x] = 0u;  // consumers done
   trace_stamp(dm.trace, KGE_K_UPDATE, 1);
-  if (a.b.flags[1]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
+  if (a.b.flags[2 + (a.s.info[0] & 1)]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
   RowAcc<V> acc;
   acc.zero();
   // loads of UNR occurrences in flight, additions in occurrence order; V = 4 (d <= 512) keeps two in flight so the
@@ -1124,23 +1125,36 @@ cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_update(kge_handle* h, const Slot& s) {
+cudaError_t launch_update_range(kge_handle* h, const Slot& s, int lo, int hi, cudaStream_t st, float* gocc) {
   const Dims& dm = h->dims;
-  UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, h->buf, h->P > 1 ? h->dist.gu : nullptr,
-                h->P > 1 ? h->dist.split_index : nullptr, h->dist.grel_split, h->seg_cnt};
-  const int grid = (dm.B + dm.n_occ + 7) / 8;
+  StepBuffers b = h->buf;
+  b.Gocc = gocc;
+  UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, b, h->P > 1 ? h->dist.gu : nullptr,
+                h->P > 1 ? h->dist.split_index : nullptr, h->dist.grel_split, h->seg_cnt, lo, hi};
+  const int grid = (hi - lo + 7) / 8;
+  if (grid <= 0) return cudaSuccess;
   const int w4 = std::max(dm.d, dm.drel) / 4;
+  cudaStream_t main = h->stream;
+  h->stream = st;  // the profiler brackets the launch on the stream it runs on
   launch_begin(h, KGE_K_UPDATE);
   if (w4 <= 32)
-    launch_pdl(k_update<1>, grid, 256, 0, h->stream, ua);
+    launch_pdl(k_update<1>, grid, 256, 0, st, ua);
   else if (w4 <= 64)
-    launch_pdl(k_update<2>, grid, 256, 0, h->stream, ua);
+    launch_pdl(k_update<2>, grid, 256, 0, st, ua);
   else if (w4 <= 128)
-    launch_pdl(k_update<4>, grid, 256, 0, h->stream, ua);
+    launch_pdl(k_update<4>, grid, 256, 0, st, ua);
   else
-    launch_pdl(k_update<8>, grid, 256, 0, h->stream, ua);
+    launch_pdl(k_update<8>, grid, 256, 0, st, ua);
   launch_end(h, KGE_K_UPDATE);
+  h->stream = main;
   return cudaGetLastError();
+}
+
+// lag = 0: every table; lag = 1: relations only -- the entity positions of this step are applied by the next step
+// (api.cu, reading c.12)
+cudaError_t launch_update(kge_handle* h, const Slot& s) {
+  const Dims& dm = h->dims;
+  return launch_update_range(h, s, 0, h->cfg.lag == 1 ? dm.B : dm.B + dm.n_occ, h->stream, h->buf.Gocc);
 }
 
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
@@ -1152,6 +1166,13 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   launch_begin(h, KGE_K_GATHER);
   launch_gather_v(h, ga, rows);
   launch_end(h, KGE_K_GATHER);
+  // lag = 1: the held-back entity update of the previous step may start once this step no longer reads the entity
+  // table -- after the gather on the fused tcgen05 path, after the chain rule otherwise
+  const bool fused_tc = tc && tc_fuses_chain(h);
+  if (h->cfg.lag == 1 && fused_tc) {
+    cudaError_t e = cudaEventRecord(h->ev_eread, h->stream);
+    if (e != cudaSuccess) return e;
+  }
 
   NegArgs na{dm, h->buf, h->buf.Gocc};
   const int32_t loss_slot = (int32_t)(step % h->ring);
@@ -1178,6 +1199,10 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
     default: launch_pdl(k_chain<8>, cgrid, 256, 0, h->stream, ca); break;
   }
   launch_end(h, KGE_K_CHAIN);
+  if (h->cfg.lag == 1) {
+    cudaError_t e = cudaEventRecord(h->ev_eread, h->stream);
+    if (e != cudaSuccess) return e;
+  }
 
   return launch_update(h, s);
 }

@@ -36,6 +36,7 @@ struct TcState {
   CUtensorMap mX_E;          // dX' epilogue operand (X' rows, 4D K-major SW128), box {32, 64, 4}
   float4* xbuf = nullptr;    // split-K exchange of the backward pairs (L2-resident scratch)
   CUtensorMap mG_S, mR_S, mD_S;
+  CUtensorMap mG_S1, mG_L1;  // lag = 1: the same maps over the second (odd-step) Gocc buffer
   CUtensorMap mG_L;          // fused chain: gx rows of Gocc (written by k_gather), box {32, 64}
   int fwd_cx = 1;  // backward TMA-store targets: Gocc, Grel, dO (SW128), box {32, 32}
   bool ok = false;
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
       a.loss[a.s.info[1]] = L;
       const bool bad = !isfinite(L);
-      a.flags[1] = bad ? 1 : 0;
+      a.flags[2 + (a.s.info[0] & 1)] = bad ? 1 : 0;
       if (bad) a.flags[0] = 1;
     }
   }
@@ -730,6 +731,8 @@ bool tc_init(kge_handle* h) {
   ok &= make_map(&st->mR_S, b.Grel, dm.drel, dm.B, 1, dm.drel, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mD_S, b.dO, dm.d, dm.B, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mG_L, b.Gocc, dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&st->mG_S1, h->gocc2[1], dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_map(&st->mG_L1, h->gocc2[1], dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 64, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!ok) {
     delete st;
     return false;
@@ -797,6 +800,7 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
   dim3 gf(2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128, dm.C);  // x = 2 tile + split-K half
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(2 * tiles * kNSplit, dm.C, 2);  // x = 2 (row tile * kNSplit + column part) + split-K half
+  const bool odd = h->buf.Gocc != h->gocc2[0];  // lag = 1: odd steps write the second Gocc buffer
   launch_begin(h, KGE_K_NEG_FWD);
   if (dm.family == FAM_DOT)
     launch_pdl_cluster(k_tc_fwd<FAM_DOT>, gf, kFwdThreads, fwd_smem(), h->stream, 2 * st->fwd_cx, st->mO_F, st->mX_F, a);
@@ -808,10 +812,12 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
   launch_begin(h, KGE_K_NEG_BWD);
   if (dm.family == FAM_DOT)
     launch_pdl_cluster(k_tc_bwd<FAM_DOT>, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN,
-                       st->mO_MN, st->mO_E, st->mX_E, st->mG_S, st->mR_S, st->mD_S, st->mG_L, a);
+                       st->mO_MN, st->mO_E, st->mX_E, odd ? st->mG_S1 : st->mG_S, st->mR_S, st->mD_S,
+                       odd ? st->mG_L1 : st->mG_L, a);
   else
     launch_pdl_cluster(k_tc_bwd<FAM_L2>, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN,
-                       st->mO_MN, st->mO_E, st->mX_E, st->mG_S, st->mR_S, st->mD_S, st->mG_L, a);
+                       st->mO_MN, st->mO_E, st->mX_E, odd ? st->mG_S1 : st->mG_S, st->mR_S, st->mD_S,
+                       odd ? st->mG_L1 : st->mG_L, a);
   launch_end(h, KGE_K_NEG_BWD);
   return cudaGetLastError();
 }

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
         const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
         a.b.loss[a.s.info[1]] = L;
         const bool bad = !isfinite(L);
-        a.b.flags[1] = bad ? 1 : 0;
+        a.b.flags[2 + (a.s.info[0] & 1)] = bad ? 1 : 0;
         if (bad) a.b.flags[0] = 1;
       }
     }
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
 // Adagrad on M_u, one state per matrix (w = d*d)
 __global__ void __launch_bounds__(256) k_tr_proj(TrArgs a) {
   const Dims& dm = a.dm;
-  if (a.b.flags[1]) return;
+  if (a.b.flags[2 + (a.s.info[0] & 1)]) return;
   const int u = blockIdx.x;
   if (u >= *a.s.rel_n) return;
   __shared__ float red[8];

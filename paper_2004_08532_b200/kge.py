@@ -80,6 +80,7 @@ def lib():
         L.kge_step.argtypes = [ctypes.c_void_p]
         L.kge_step.restype = ctypes.c_int64
         L.kge_set_step.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        L.kge_flush.argtypes = [ctypes.c_void_p]
         L.kge_sync.argtypes = [ctypes.c_void_p]
         L.kge_profile_begin.argtypes = [ctypes.c_void_p]
         L.kge_profile_end.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_double), _i64p]
@@ -294,6 +295,10 @@ class Handle:
         joined = b"".join(blobs)
         buf = ctypes.create_string_buffer(joined, len(joined))
         _check(lib().kge_connect(self._h, buf, len(blobs)))
+
+    def flush(self):
+        """kge_flush: lag = 1, apply the held-back entity update of the last step."""
+        _check(lib().kge_flush(self._h))
 
     def set_step(self, s):
         _check(lib().kge_set_step(self._h, s))
