@@ -36,6 +36,7 @@ WORKLOADS = {
     "fb15k": ("fb15k", "distmult", 400, 1024, 256, 256),
     "wn18": ("wn18", "rotate", 400, 1024, 256, 256),
     "tiny": ("tiny", "transe_l2", 64, 256, 64, 64),
+    "fb15k_transr": ("fb15k", "transr", 200, 1024, 256, 256),  # configs[3]: TransR, d = 200, M_r 200 x 200
 }
 METRIC = "positive triples/sec (d=400, k=256) at 1/2/4/8 B200; % of HBM/tensor roofline"
 

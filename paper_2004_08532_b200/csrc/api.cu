@@ -506,6 +506,13 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(std::max<int64_t>(h->n_neg_parts, tc_parts), dm.B) * 4);
   b.flow = (uint32_t*)dalloc(h, (size_t)2 * dm.C * 4);
+  {  // FFMA split-K scratch: tiles of the larger (backward) grid x up to 8 splits x 256 threads x 16 floats
+    const int64_t tiles = (int64_t)((dm.d + 63) / 64) * ((std::max(dm.g, dm.k) + 63) / 64) * 2 * dm.C;
+    h->ffma_ks_max = 8;
+    h->ffma_part = (float4*)dalloc(h, (size_t)tiles * h->ffma_ks_max * 4 * 256 * sizeof(float4));
+    h->ffma_cnt = (int32_t*)dalloc(h, (size_t)tiles * 4);
+    if (!h->ffma_part || !h->ffma_cnt) { set_error("out of device memory (FFMA scratch)"); return fail(KGE_ENOMEM); }
+  }
   b.rowsumW = (float*)dalloc(h, (size_t)dm.B * 2 * ((dm.k + 31) / 32) * 4);   // tc.cu partial row sums of W
   b.colsumW = (float*)dalloc(h, (size_t)nneg * ((dm.g + 127) / 128) * 4);     // tc.cu partial column sums of W
   b.dO = (float*)dalloc(h, (size_t)dm.B * dm.d * 4);
@@ -522,6 +529,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   }
   e = cudaMemsetAsync(b.flags, 0, 16, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(b.flow, 0, (size_t)2 * dm.C * 4, h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(h->ffma_cnt, 0, (size_t)((dm.d + 63) / 64) * ((std::max(dm.g, dm.k) + 63) / 64) * 2 * dm.C * 4,
+                        h->stream);
   // padding of O / X' (see tc.cu): zeros, plus O[:, d] = 1 and X'[:, d+1] = 1 -- written once, never overwritten
   if (e == cudaSuccess) e = cudaMemsetAsync(b.O, 0, (size_t)dm.B * dm.dp * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(b.X, 0, (size_t)nneg * dm.dp * 4, h->stream);

@@ -199,6 +199,10 @@ struct kge_handle {
   int32_t pend_gi = -1;     // its caller-batch slot, or -1 (ring slot)
   bool eupd_enqueued = false;
   float* gocc2[2] = {};     // the two Gocc buffers (lag = 1), else both = buf.Gocc
+  // FFMA negative kernels: deterministic split-K scratch (partial tiles + arrival counters)
+  float4* ffma_part = nullptr;
+  int32_t* ffma_cnt = nullptr;
+  int32_t ffma_ks_max = 1;  // the split factor the scratch was sized for
   cudaEvent_t ev_samp[2] = {}, ev_free[2] = {};
   int64_t half_first[2] = {-1, -1};  // first step held by each ring half (-1: none)
   bool half_waited[2] = {false, false};

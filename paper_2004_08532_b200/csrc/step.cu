@@ -428,36 +428,87 @@ struct NegArgs {
   Dims dm;
   StepBuffers b;
   float* Gocc;  // dX' destination (occurrence rows 2B + q)
+  float4* part;  // split-K partial tiles [tile][ks][4][256 threads] (float4), L2-resident scratch
+  int32_t* cnt;  // [tiles] arrival counters (zero between launches: the last CTA of a tile resets its counter)
+  int32_t ks;    // split-K factor of this launch
 };
 
-// Load a [64 rows x 32 k] tile of a row-major [rows x d] matrix, transposed into smem T[k][row].
-// CMOD: k-chunk = 16 real parts from column kc and 16 imaginary parts from column d/2 + kc.
+// Register-staged tile loader: a [64 rows x 32 k] tile of a row-major [rows x d] matrix is fetched as 2 float4 per
+// thread into registers (next chunk in flight while the current one is computed) and stored transposed into smem
+// T[k][row]. CMOD: k-chunk = 16 real parts from column kc and 16 imaginary parts from column d/2 + kc.
 template <bool CPLX>
-__device__ __forceinline__ void load_tile_T(float (*T)[TM + TPAD], const float* __restrict__ base, int row0,
-                                            int nrows, int kc, int d, int pitch) {
-  // 64 rows x 8 float4 = 512 float4 per tile; 256 threads x 2
-  for (int idx = threadIdx.x; idx < TM * (TK / 4); idx += blockDim.x) {
-    const int r = idx / (TK / 4), v = idx % (TK / 4);
-    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-    int col;
-    if (CPLX) {
-      const int half = d >> 1;
-      const int cc = kc + (v & 3) * 4;  // complex index
-      col = (v < 4) ? cc : half + cc;
-      if (row0 + r < nrows && cc < half) x = *reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * pitch + col);
-    } else {
-      col = kc + v * 4;
-      if (row0 + r < nrows && col < d) x = *reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * pitch + col);
+struct TileRegs {
+  float4 x[2];
+  __device__ __forceinline__ void load(const float* __restrict__ base, int row0, int nrows, int kc, int d, int pitch) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = threadIdx.x + q * 256;
+      const int r = idx / (TK / 4), v = idx % (TK / 4);
+      x[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (CPLX) {
+        const int half = d >> 1;
+        const int cc = kc + (v & 3) * 4;  // complex index
+        const int col = (v < 4) ? cc : half + cc;
+        if (row0 + r < nrows && cc < half) x[q] = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * pitch + col));
+      } else {
+        const int col = kc + v * 4;
+        if (row0 + r < nrows && col < d) x[q] = __ldcg(reinterpret_cast<const float4*>(base + (int64_t)(row0 + r) * pitch + col));
+      }
     }
-    T[v * 4 + 0][r] = x.x;
-    T[v * 4 + 1][r] = x.y;
-    T[v * 4 + 2][r] = x.z;
-    T[v * 4 + 3][r] = x.w;
   }
+  __device__ __forceinline__ void store(float (*T)[TM + TPAD]) const {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = threadIdx.x + q * 256;
+      const int r = idx / (TK / 4), v = idx % (TK / 4);
+      T[v * 4 + 0][r] = x[q].x;
+      T[v * 4 + 1][r] = x[q].y;
+      T[v * 4 + 2][r] = x[q].z;
+      T[v * 4 + 3][r] = x[q].w;
+    }
+  }
+};
+
+// Deterministic split-K: every CTA of a tile parks its 16 per-thread partial sums, the last to arrive adds all
+// ks partials in ks order (the result does not depend on arrival order) and runs the epilogue. Returns false for the
+// CTAs that leave. acc is overwritten with the full sum in the returning CTA.
+__device__ __forceinline__ bool splitk_reduce(float (&acc)[4][4], float4* __restrict__ part, int32_t* cnt, int tile,
+                                              int ks, int nks) {
+  if (nks == 1) return true;
+  __shared__ int s_last;
+  float4* mine = part + ((int64_t)tile * nks + ks) * 4 * 256;
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+    mine[ii * 256 + threadIdx.x] = make_float4(acc[ii][0], acc[ii][1], acc[ii][2], acc[ii][3]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&cnt[tile], 1) == nks - 1;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = 0.f;
+  for (int q = 0; q < nks; ++q) {
+    const float4* pq = part + ((int64_t)tile * nks + q) * 4 * 256;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const float4 v = __ldcg(pq + ii * 256 + threadIdx.x);
+      acc[ii][0] += v.x;
+      acc[ii][1] += v.y;
+      acc[ii][2] += v.z;
+      acc[ii][3] += v.w;
+    }
+  }
+  if (threadIdx.x == 0) cnt[tile] = 0;  // ready for the next launch
+  return true;
 }
 
 template <int FAM>
-__global__ void __launch_bounds__(256) k_neg_fwd(NegArgs a) {
+__global__ void __launch_bounds__(256, 2) k_neg_fwd(NegArgs a) {
   constexpr bool CPLX = FAM == FAM_CMOD;
   const Dims& dm = a.dm;
   pdl_wait();
@@ -465,17 +516,29 @@ __global__ void __launch_bounds__(256) k_neg_fwd(NegArgs a) {
   __shared__ __align__(16) float As[TK][TM + TPAD];
   __shared__ __align__(16) float Bs[TK][TN + TPAD];
   __shared__ float red[8];
-  const int c = blockIdx.z, i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
+  const int nks = a.ks, c = blockIdx.z / nks, ks = blockIdx.z % nks;
+  const int i0 = blockIdx.y * TM, j0 = blockIdx.x * TN;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const float* Oc = a.b.O + (int64_t)c * dm.g * dm.dp;
   const float* Xc = a.b.X + (int64_t)c * dm.k * dm.dp;
   float acc[4][4] = {};
   const int kend = CPLX ? (dm.d >> 1) : dm.d;
   const int kstep = CPLX ? TK / 2 : TK;
-  for (int kc = 0; kc < kend; kc += kstep) {
-    load_tile_T<CPLX>(As, Oc, i0, dm.g, kc, dm.d, dm.dp);
-    load_tile_T<CPLX>(Bs, Xc, j0, dm.k, kc, dm.d, dm.dp);
+  const int nch = (kend + kstep - 1) / kstep, per = (nch + nks - 1) / nks;
+  const int ch0 = min(nch, ks * per), ch1 = min(nch, ch0 + per);
+  TileRegs<CPLX> ra, rb;
+  if (ch0 < ch1) {
+    ra.load(Oc, i0, dm.g, ch0 * kstep, dm.d, dm.dp);
+    rb.load(Xc, j0, dm.k, ch0 * kstep, dm.d, dm.dp);
+  }
+  for (int ch = ch0; ch < ch1; ++ch) {
+    ra.store(As);
+    rb.store(Bs);
     __syncthreads();
+    if (ch + 1 < ch1) {  // next chunk's loads in flight during this chunk's arithmetic
+      ra.load(Oc, i0, dm.g, (ch + 1) * kstep, dm.d, dm.dp);
+      rb.load(Xc, j0, dm.k, (ch + 1) * kstep, dm.d, dm.dp);
+    }
     if (CPLX) {
 #pragma unroll 4
       for (int e = 0; e < TK / 2; ++e) {
@@ -516,6 +579,8 @@ __global__ void __launch_bounds__(256) k_neg_fwd(NegArgs a) {
     }
     __syncthreads();
   }
+  const int tile = (c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (!splitk_reduce(acc, a.part, a.cnt, tile, ks, nks)) return;
   // epilogue: f-, dL/dS coefficient, loss partial
   const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
   float lsum = 0.f;
@@ -548,9 +613,9 @@ __global__ void __launch_bounds__(256) k_neg_fwd(NegArgs a) {
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lsum;
   __syncthreads();
   if (threadIdx.x == 0) {
-    float s = 0.f;
-    for (int w = 0; w < 8; ++w) s += red[w];
-    a.b.lneg[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+    float sum = 0.f;
+    for (int w = 0; w < 8; ++w) sum += red[w];
+    a.b.lneg[tile] = sum;
   }
 }
 
@@ -563,15 +628,16 @@ __global__ void __launch_bounds__(256) k_neg_fwd(NegArgs a) {
 __device__ __forceinline__ float sgnf(float u) { return u > 0.f ? 1.f : (u < 0.f ? -1.f : 0.f); }
 
 template <int FAM>
-__global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
+__global__ void __launch_bounds__(256, 2) k_neg_bwd(NegArgs a) {
   constexpr bool CPLX = FAM == FAM_CMOD;
   const Dims& dm = a.dm;
   pdl_wait();
   pdl_trigger();
   __shared__ __align__(16) float Ws[TK][TM + TPAD];  // [K index][row index of the output]
   __shared__ __align__(16) float Vs[TK][TN + TPAD];  // [K index][column]  (CPLX: re cols 0..31, im cols 32..63)
-  const bool pass_x = blockIdx.z >= (unsigned)dm.C;
-  const int c = pass_x ? blockIdx.z - dm.C : blockIdx.z;
+  const int nks = a.ks, zz = blockIdx.z / nks, ks = blockIdx.z % nks;
+  const bool pass_x = zz >= dm.C;
+  const int c = pass_x ? zz - dm.C : zz;
   const int nrows = pass_x ? dm.k : dm.g;        // output rows: j (dX') or i (dO)
   const int nk = pass_x ? dm.g : dm.k;           // contraction: i or j
   const int r0 = blockIdx.y * TM;
@@ -615,33 +681,63 @@ __global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
       }
     }
   }
-  float acc[4][4] = {};
-  for (int k0 = 0; k0 < nk; k0 += TK) {
-    // Ws[kk][r] = W for (output row r0+r, contraction k0+kk)
-    for (int idx = threadIdx.x; idx < TK * TM; idx += blockDim.x) {
-      const int kk = idx / TM, r = idx % TM;
-      const int orow = r0 + r, kidx = k0 + kk;
-      float w = 0.f;
-      if (orow < nrows && kidx < nk) w = pass_x ? Wc[(int64_t)kidx * dm.kp + orow] : Wc[(int64_t)orow * dm.kp + kidx];
-      Ws[kk][r] = w;
-    }
-    // Vs[kk][col] = Other row (k0+kk), this tile's columns
-    for (int idx = threadIdx.x; idx < TK * TN; idx += blockDim.x) {
-      const int kk = idx / TN, cl = idx % TN;
-      const int kidx = k0 + kk;
-      float v = 0.f;
+  // register-staged tiles (2 float4 of W and 2 of V per thread), the next chunk in flight during the arithmetic.
+  // W chunk: 32 contraction x 64 output rows. dX' reads W[k][row] (rows contiguous); dO reads W[row][k] (k
+  // contiguous): each float4 then runs along k and is transposed on the smem store.
+  float4 wr[2], vr[2];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = threadIdx.x + q * 256;  // 512 float4 per operand tile
+      float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (pass_x) {  // kk = idx / 16, rows 4 * (idx % 16) .. +3
+        const int kk = idx >> 4, rq = (idx & 15) * 4, kidx = k0 + kk;
+        if (kidx < nk && r0 + rq < nrows) w = __ldcg(reinterpret_cast<const float4*>(Wc + (int64_t)kidx * dm.kp + r0 + rq));
+      } else {       // row = idx / 8, k 4 * (idx % 8) .. +3
+        const int rr = idx >> 3, kq = (idx & 7) * 4, kidx = k0 + kq;
+        if (kidx < nk && r0 + rr < nrows) w = __ldcg(reinterpret_cast<const float4*>(Wc + (int64_t)(r0 + rr) * dm.kp + kidx));
+      }
+      wr[q] = w;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int kk = idx >> 4, cq = (idx & 15) * 4, kidx = k0 + kk;  // Vs[kk][cq .. cq+3]
       if (kidx < nk) {
         if (CPLX) {
-          const int cc = cb + (cl & 31);
-          if (cc < half) v = Other[(int64_t)kidx * dm.dp + (cl < 32 ? cc : half + cc)];
+          const int cc = cb + (cq & 31);
+          if (cc < half) v = __ldcg(reinterpret_cast<const float4*>(Other + (int64_t)kidx * dm.dp + (cq < 32 ? cc : half + cc)));
         } else {
-          const int gcol = cb + cl;
-          if (gcol < dm.d) v = Other[(int64_t)kidx * dm.dp + gcol];
+          const int gcol = cb + cq;
+          if (gcol < dm.d) v = __ldcg(reinterpret_cast<const float4*>(Other + (int64_t)kidx * dm.dp + gcol));
         }
       }
-      Vs[kk][cl] = v;
+      vr[q] = v;
     }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int idx = threadIdx.x + q * 256;
+      if (pass_x) {
+        const int kk = idx >> 4, rq = (idx & 15) * 4;
+        *reinterpret_cast<float4*>(&Ws[kk][rq]) = wr[q];
+      } else {
+        const int rr = idx >> 3, kq = (idx & 7) * 4;
+        Ws[kq + 0][rr] = wr[q].x;
+        Ws[kq + 1][rr] = wr[q].y;
+        Ws[kq + 2][rr] = wr[q].z;
+        Ws[kq + 3][rr] = wr[q].w;
+      }
+      const int kk = idx >> 4, cq = (idx & 15) * 4;
+      *reinterpret_cast<float4*>(&Vs[kk][cq]) = vr[q];
+    }
+  };
+  float acc[4][4] = {};
+  const int nch = (nk + TK - 1) / TK, per = (nch + nks - 1) / nks;
+  const int ch0 = min(nch, ks * per), ch1 = min(nch, ch0 + per);
+  if (ch0 < ch1) load(ch0 * TK);
+  for (int ch = ch0; ch < ch1; ++ch) {
+    store();
     __syncthreads();
+    if (ch + 1 < ch1) load((ch + 1) * TK);
 #pragma unroll 4
     for (int kk = 0; kk < TK; ++kk) {
       const float4 wv = *reinterpret_cast<const float4*>(&Ws[kk][ty * 4]);
@@ -667,8 +763,10 @@ __global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
           if (FAM == FAM_DOT) {
             acc[ii][ee] = fmaf(w[ii], t_, acc[ii][ee]);
           } else if (FAM == FAM_L1) {
-            const float u = pass_x ? (t_ - s_) : (s_ - t_);  // o - x
-            acc[ii][ee] = fmaf(w[ii], pass_x ? -sgnf(u) : sgnf(u), acc[ii][ee]);
+            // w * sgn(o - x) with sgn(0) = 0 (reading c.10): (o > x) - (o < x), set as 1.0 / 0.0 in one instruction each
+            const float o_ = pass_x ? t_ : s_, x_ = pass_x ? s_ : t_;
+            const float sg = (o_ > x_ ? 1.f : 0.f) - (o_ < x_ ? 1.f : 0.f);
+            acc[ii][ee] = fmaf(w[ii], pass_x ? -sg : sg, acc[ii][ee]);
           } else if (FAM == FAM_CMOD) {
             const float ur = pass_x ? (t_ - s_) : (s_ - t_);
             const float ui = pass_x ? (oi[ee] - si[ii][ee]) : (si[ii][ee] - oi[ee]);
@@ -683,6 +781,8 @@ __global__ void __launch_bounds__(256) k_neg_bwd(NegArgs a) {
     }
     __syncthreads();
   }
+  const int tile = (zz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (!splitk_reduce(acc, a.part, a.cnt, tile, ks, nks)) return;
   // store
   float* dst = pass_x ? a.Gocc + ((int64_t)2 * dm.B + (int64_t)c * dm.k) * dm.d : a.b.dO + (int64_t)c * dm.g * dm.d;
 #pragma unroll
@@ -1086,16 +1186,31 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
 // ------------------------------------------------------------------------------------------------
 // host launchers
 // ------------------------------------------------------------------------------------------------
+// split-K factor: enough CTAs for ~2 per SM (the kernels are latency bound at one), at least 2 chunks per split
+static int ffma_splits(int tiles, int nchunks) {
+  int ks = 1;
+  while (ks < 8 && tiles * ks * 2 <= 2 * 148 && nchunks >= 4 * ks) ks *= 2;
+  return ks;
+}
+
 template <int FAM>
-static void launch_neg(kge_handle* h, const NegArgs& na) {
+static void launch_neg(kge_handle* h, const NegArgs& na0) {
   const Dims& dm = h->dims;
+  NegArgs na = na0;
+  na.part = h->ffma_part;
+  na.cnt = h->ffma_cnt;
+  const int kend = FAM == FAM_CMOD ? dm.d / 2 : dm.d, kstep = FAM == FAM_CMOD ? TK / 2 : TK;
   dim3 gf((dm.k + TN - 1) / TN, (dm.g + TM - 1) / TM, dm.C);
+  na.ks = std::min(ffma_splits(gf.x * gf.y * gf.z, (kend + kstep - 1) / kstep), h->ffma_ks_max);
+  gf.z *= na.ks;
   launch_begin(h, KGE_K_NEG_FWD);
   launch_pdl(k_neg_fwd<FAM>, gf, 256, 0, h->stream, na);
   launch_end(h, KGE_K_NEG_FWD);
   const int cols_per_tile = FAM == FAM_CMOD ? TN / 2 : TN;
   const int ncols = FAM == FAM_CMOD ? dm.d / 2 : dm.d;
   dim3 gb((ncols + cols_per_tile - 1) / cols_per_tile, (std::max(dm.g, dm.k) + TM - 1) / TM, 2 * dm.C);
+  na.ks = std::min(ffma_splits(gb.x * gb.y * gb.z, (std::min(dm.g, dm.k) + TK - 1) / TK), h->ffma_ks_max);
+  gb.z *= na.ks;
   launch_begin(h, KGE_K_NEG_BWD);
   launch_pdl(k_neg_bwd<FAM>, gb, 256, 0, h->stream, na);
   launch_end(h, KGE_K_NEG_BWD);
@@ -1174,7 +1289,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
     if (e != cudaSuccess) return e;
   }
 
-  NegArgs na{dm, h->buf, h->buf.Gocc};
+  NegArgs na{dm, h->buf, h->buf.Gocc, nullptr, nullptr, 1};
   const int32_t loss_slot = (int32_t)(step % h->ring);
   if (h->cfg.neg_precision == KGE_PREC_TF32 && tc_supported(h)) {
     cudaError_t e = launch_tc_neg(h, s, loss_slot);
