@@ -308,10 +308,11 @@ def main():
     H.sync()
     if pg:
         pg.barrier()
+    ph, pr, pt, pl = pinned[0].data_ptr(), pinned[1].data_ptr(), pinned[2].data_ptr(), loss_buf.data_ptr()
     w0 = time.perf_counter()
-    for st in range(e2e_steps):
-        H.train_batch_async_ptr(pinned[0, st].data_ptr(), pinned[1, st].data_ptr(), pinned[2, st].data_ptr(),
-                                loss_buf[st:].data_ptr())
+    for st in range(e2e_steps):  # the public per-step call, on this step's pinned host arrays
+        o = st * B * 8
+        H.train_batch_async_ptr(ph + o, pr + o, pt + o, pl + 4 * st)
     H.sync()
     e2e_s = time.perf_counter() - w0
     if pg:

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <functional>
 #include <vector>
@@ -129,7 +130,7 @@ static int validate(const kge_config* c) {
 
 static size_t slot_ints(const Dims& d) {
   const size_t n_occ = d.n_occ, B = d.B;
-  size_t n = B * 4 + (size_t)d.C * d.k + d.C + 1 + n_occ * 3 + (n_occ + 1) + 1 + B * 3 + (B + 1) + 2;
+  size_t n = B * 4 + (size_t)d.C * d.k + d.C + 1 + n_occ * 3 + (n_occ + 1) + 1 + B * 3 + (B + 1) + 4;
   return (n + 63) & ~size_t(63);  // 256-byte aligned slots
 }
 
@@ -162,7 +163,7 @@ static int carve_slot(kge_handle* h, int32_t* p, Slot& s) {
   s.rel_inv = p; p += B;
   s.rel_off = p; p += B + 1;
   s.rel_occ = p; p += B;
-  s.info = p; p += 2;
+  s.info = p; p += 4;
   return KGE_OK;
 }
 
@@ -778,15 +779,31 @@ static int batch_graphs(kge_handle* h, int gi, int64_t s, float* loss_host) {
              }, &h->g_step[gi], cudaGraphNodeTypeMemcpy, &h->g_loss_node[gi]), "capture step graph");
   }
   const int32_t kernels = h->g_launches;
+  // the loss goes straight from the kernel that reduces it to the caller's pinned (device-visible) float: a 4-byte
+  // D2H copy node costs ~10 us on the step's critical path. Pageable targets keep the copy.
+  uint64_t dst = 0;
+  if (loss_host) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, loss_host) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+      dst = (uint64_t)(uintptr_t)at.devicePointer;
+    else
+      cudaGetLastError();
+  }
   KGE_GCHK(cudaStreamWaitEvent(ss, h->ev_gfree[gi], 0), "wait slot");
-  KGE_GCHK(sample_graph_set(h, h->g_samp[gi], h->g_samp_node[gi], p, gslot, 1, s, 1), "sample node params");
+  KGE_GCHK(sample_graph_set(h, h->g_samp[gi], h->g_samp_node[gi], p, gslot, 1, s, 1, dst), "sample node params");
   KGE_GCHK(cudaGraphLaunch(h->g_samp[gi], ss), "sample graph launch");
   KGE_GCHK(cudaEventRecord(h->stage_ev[gi], ss), "event");
   KGE_GCHK(cudaEventRecord(h->ev_gsamp[gi], ss), "event");
   KGE_GCHK(cudaStreamWaitEvent(h->stream, h->ev_gsamp[gi], 0), "wait sample");
-  KGE_GCHK(cudaGraphExecMemcpyNodeSetParams1D(h->g_step[gi], h->g_loss_node[gi], loss_host ? loss_host : h->pinned_sink,
-                                              h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost),
-           "loss node params");
+  const bool copy = loss_host && !dst;
+  if (copy)
+    KGE_GCHK(cudaGraphExecMemcpyNodeSetParams1D(h->g_step[gi], h->g_loss_node[gi], loss_host, h->buf.loss + (s % h->ring),
+                                                4, cudaMemcpyDeviceToHost),
+             "loss node params");
+  if (copy != h->g_loss_on[gi]) {
+    KGE_GCHK(cudaGraphNodeSetEnabled(h->g_step[gi], h->g_loss_node[gi], copy ? 1 : 0), "loss node");
+    h->g_loss_on[gi] = copy;
+  }
   KGE_GCHK(cudaGraphLaunch(h->g_step[gi], h->stream), "step graph launch");
   KGE_GCHK(cudaEventRecord(h->ev_gfree[gi], h->stream), "event");
   h->launches += 1 + kernels;
@@ -804,8 +821,26 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
   // after its previous H2D copy completed), then one H2D copy
   const int si = (int)(s % kge_handle::kGiven);  // staging buffer = given slot (kStage == kGiven)
   int32_t* st = h->pinned_given + (size_t)si * 3 * B;
+  static const bool hprof = getenv("KGE_HOST_PROF") != nullptr;  // diagnostics: host time per phase
+  static double hp[4] = {0, 0, 0, 0};
+  static int64_t hn = 0;
+  auto now = []() { timespec t; clock_gettime(CLOCK_MONOTONIC, &t); return t.tv_sec * 1e6 + t.tv_nsec * 1e-3; };
+  const double t0 = hprof ? now() : 0.0;
   cudaError_t e = cudaEventSynchronize(h->stage_ev[si]);
   if (e != cudaSuccess) return cuda_fail(e, "staging reuse");
+  const double t1 = hprof ? now() : 0.0;
+  struct HostProf {
+    bool on; double t0, t1; double* hp; int64_t* hn; double (*now)();
+    double t2 = 0;
+    ~HostProf() {
+      if (!on) return;
+      const double t3 = now();
+      hp[0] += t1 - t0; hp[1] += t2 - t1; hp[2] += t3 - t2; ++*hn;
+      if (*hn % 1000 == 0)
+        fprintf(stderr, "[kge host] per call: event sync %.2f us, narrowing %.2f us, enqueue %.2f us (%lld calls)\n",
+                hp[0] / *hn, hp[1] / *hn, hp[2] / *hn, (long long)*hn);
+    }
+  } hpr{hprof, t0, t1, hp, &hn, +now};
   for (int i = 0; i < B; ++i) {
     if (heads[i] < 0 || heads[i] >= h->dims.n_entities || tails[i] < 0 || tails[i] >= h->dims.n_entities ||
         rels[i] < 0 || rels[i] >= h->dims.n_relations) {
@@ -816,6 +851,7 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
     st[B + i] = (int32_t)rels[i];
     st[2 * B + i] = (int32_t)tails[i];
   }
+  if (hprof) hpr.t2 = now();
   if (h->P > 1) {  // B1 (see kge_train_step); every rank must call kge_train_batch for this step
     e = dist_barrier(h);
     if (e == cudaSuccess && h->dist.n_split > 0)

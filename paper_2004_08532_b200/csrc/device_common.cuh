@@ -117,6 +117,13 @@ __device__ __forceinline__ void flow_acquire(const uint32_t* cnt, uint32_t targe
 // generic-proxy writes acquired above are read next by TMA (async proxy)
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
+// the step's loss: device ring slot + (Slot::info[2..3]) a device-visible host address, if the caller gave one
+__device__ __forceinline__ void store_loss(float* ring, const int32_t* info, float L) {
+  ring[info[1]] = L;
+  const uint64_t dst = ((uint64_t)(uint32_t)info[3] << 32) | (uint32_t)info[2];
+  if (dst) *reinterpret_cast<volatile float*>(dst) = L;
+}
+
 // ---- small helpers ----
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

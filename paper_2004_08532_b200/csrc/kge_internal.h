@@ -61,8 +61,9 @@ struct Slot {
   int32_t* rel_inv;  // [B]
   int32_t* rel_off;  // [B + 1]
   int32_t* rel_occ;  // [B]
-  int32_t* info;     // [2]: the step (mod 2^32) and its loss slot (step % loss ring), written by k_sample -- so the
-                     // step kernels' parameters depend on the slot only and one captured graph serves every step
+  int32_t* info;     // [4]: the step (mod 2^32), its loss slot (step % loss ring) and the 64-bit device-visible host
+                     // address its loss is also stored to (0: none), written by k_sample -- so the step kernels'
+                     // parameters depend on the slot only and one captured graph serves every step
 };
 
 struct SampleParams {
@@ -208,7 +209,7 @@ struct kge_handle {
   bool half_waited[2] = {false, false};
   // caller-supplied batches (kge_train_batch): kGiven slots sampled on the side stream, so the sample of batch s+1
   // overlaps step s
-  static constexpr int kGiven = 4;
+  static constexpr int kGiven = 8;
   kge::Slot given_slots[kGiven] = {};
   cudaStream_t gside[kGiven] = {};  // one high-priority stream per given slot: the single-step samples of consecutive
                                     // batches (~50 us each) run concurrently instead of queueing on one stream
@@ -219,6 +220,7 @@ struct kge_handle {
   // the device time
   cudaGraphExec_t g_samp[kGiven] = {}, g_step[kGiven] = {};
   cudaGraphNode_t g_samp_node[kGiven] = {}, g_loss_node[kGiven] = {};
+  bool g_loss_on[kGiven] = {true, true, true, true, true, true, true, true};  // state of each D2H loss node
   std::vector<cudaGraph_t> graphs;  // source graphs of the instantiated ones
   int32_t g_launches = 0;       // kernels per captured step (launch counter)
   float* pinned_sink = nullptr;  // readback target when the caller passes no loss pointer
@@ -303,10 +305,10 @@ void launch_end(kge_handle* h, int kid);
 size_t sample_smem_bytes(int n_pad);
 cudaError_t sample_init();
 cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev_array, int ring, int64_t step0, int n_steps,
-                          cudaStream_t stream = nullptr);  // nullptr: h->stream
+                          cudaStream_t stream = nullptr, uint64_t loss_dst = 0);  // nullptr: h->stream
 // re-point a captured k_sample node at another first step
 cudaError_t sample_graph_set(kge_handle* h, cudaGraphExec_t exec, cudaGraphNode_t node, const SampleParams& p,
-                             const Slot* slots_dev_array, int ring, int64_t step0, int n_steps);
+                             const Slot* slots_dev_array, int ring, int64_t step0, int n_steps, uint64_t loss_dst);
 cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound,
                               int64_t row_stride = 1, int64_t row_offset = 0);
 cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, int64_t n, int64_t limit, int32_t* bad);

@@ -14,7 +14,11 @@
 
 namespace kge {
 
-constexpr int kSampleThreads = 1024;
+constexpr int kSampleThreads = 1024;  // block size limit of k_sample (registers capped at 64 per thread)
+// Block size of a launch: a step sampled alone (caller batches; it runs next to the step kernels of the main stream)
+// uses 256 threads, so it fits on an SM beside them -- a 1024-thread block needs an SM's whole register file and
+// waited for a completely idle SM; the ring launches (32 steps ahead on the side stream) keep 1024.
+static int sample_block(int n_steps) { return n_steps == 1 ? 256 : kSampleThreads; }
 
 struct SampleArgs {
   SampleParams p;
@@ -24,6 +28,7 @@ struct SampleArgs {
   int32_t loss_ring;  // the handle's loss ring (Slot::info[1] = step % loss_ring)
   int64_t step0;
   uint64_t* trace;    // KGE_TRACE diagnostics or nullptr
+  uint64_t loss_dst;  // device-visible host address for the loss of step0 (n_steps == 1), or 0
 };
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
@@ -65,6 +70,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
   if (blockIdx.y == 0 && threadIdx.x == 0) {
     slot.info[0] = (int32_t)(uint32_t)s;
     slot.info[1] = (int32_t)(s % a.loss_ring);
+    slot.info[2] = (int32_t)(uint32_t)a.loss_dst;
+    slot.info[3] = (int32_t)(uint32_t)(a.loss_dst >> 32);
   }
   const bool ent_side = blockIdx.y == 0;
   const int tid = threadIdx.x;
@@ -195,7 +202,7 @@ cudaError_t sample_init() {
 }
 
 cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev, int ring, int64_t step0, int n_steps,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, uint64_t loss_dst) {
   SampleArgs a;
   a.p = p;
   a.fe_half = make_feistel_domain((uint64_t)p.n_list).half;
@@ -204,19 +211,20 @@ cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slot
   a.loss_ring = h->ring;
   a.step0 = step0;
   a.trace = h->dims.trace;
+  a.loss_dst = loss_dst;
   size_t smem = sample_smem_bytes(p.n_pad);  // opt-in raised once by sample_init (never in the step path: the call
                                               // may synchronise, which would stall the multi-rank emulation)
   cudaStream_t main = h->stream;
   if (stream) h->stream = stream;  // the profiler brackets the launch on the stream it runs on
   launch_begin(h, KGE_K_SAMPLE);
-  k_sample<<<dim3(n_steps, 2), kSampleThreads, smem, h->stream>>>(a);
+  k_sample<<<dim3(n_steps, 2), sample_block(n_steps), smem, h->stream>>>(a);
   launch_end(h, KGE_K_SAMPLE);
   h->stream = main;
   return cudaGetLastError();
 }
 
 cudaError_t sample_graph_set(kge_handle* h, cudaGraphExec_t exec, cudaGraphNode_t node, const SampleParams& p,
-                             const Slot* slots_dev, int ring, int64_t step0, int n_steps) {
+                             const Slot* slots_dev, int ring, int64_t step0, int n_steps, uint64_t loss_dst) {
   SampleArgs a;
   a.p = p;
   a.fe_half = make_feistel_domain((uint64_t)p.n_list).half;
@@ -225,11 +233,12 @@ cudaError_t sample_graph_set(kge_handle* h, cudaGraphExec_t exec, cudaGraphNode_
   a.loss_ring = h->ring;
   a.step0 = step0;
   a.trace = h->dims.trace;
+  a.loss_dst = loss_dst;
   void* args[] = {&a};
   cudaKernelNodeParams kp = {};
   kp.func = (void*)k_sample;
   kp.gridDim = dim3(n_steps, 2);
-  kp.blockDim = dim3(kSampleThreads);
+  kp.blockDim = dim3(sample_block(n_steps));
   kp.sharedMemBytes = (unsigned)sample_smem_bytes(p.n_pad);
   kp.kernelParams = args;
   return cudaGraphExecKernelNodeSetParams(exec, node, &kp);

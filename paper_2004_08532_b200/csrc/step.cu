@@ -424,6 +424,25 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
 // ------------------------------------------------------------------------------------------------
 constexpr int TM = 64, TN = 64, TK = 32, TPAD = 4;
 
+// Blackwell 2-wide FP32 (FADD2 / FFMA2 on a register pair; a scalar operand is broadcast for free): the FFMA
+// kernels process output columns in pairs for the families whose per-element work is add / fma only
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 struct NegArgs {
   Dims dm;
   StepBuffers b;
@@ -522,6 +541,7 @@ __global__ void __launch_bounds__(256, 2) k_neg_fwd(NegArgs a) {
   const float* Oc = a.b.O + (int64_t)c * dm.g * dm.dp;
   const float* Xc = a.b.X + (int64_t)c * dm.k * dm.dp;
   float acc[4][4] = {};
+  uint64_t acc2[4][2] = {};  // packed accumulators (DOT / L2 / L2SQ)
   const int kend = CPLX ? (dm.d >> 1) : dm.d;
   const int kstep = CPLX ? TK / 2 : TK;
   const int nch = (kend + kstep - 1) / kstep, per = (nch + nks - 1) / nks;
@@ -556,7 +576,7 @@ __global__ void __launch_bounds__(256, 2) k_neg_fwd(NegArgs a) {
             acc[ii][jj] += sqrtf(ur * ur + ui * ui);
           }
       }
-    } else {
+    } else if (FAM == FAM_L1) {
 #pragma unroll 8
       for (int e = 0; e < TK; ++e) {
         const float4 av = *reinterpret_cast<const float4*>(&As[e][ty * 4]);
@@ -565,19 +585,37 @@ __global__ void __launch_bounds__(256, 2) k_neg_fwd(NegArgs a) {
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            if (FAM == FAM_DOT) {
-              acc[ii][jj] = fmaf(ar[ii], br[jj], acc[ii][jj]);
-            } else if (FAM == FAM_L1) {
-              acc[ii][jj] += fabsf(ar[ii] - br[jj]);
-            } else {
-              const float u = ar[ii] - br[jj];
-              acc[ii][jj] = fmaf(u, u, acc[ii][jj]);
-            }
+          for (int jj = 0; jj < 4; ++jj) acc[ii][jj] += fabsf(ar[ii] - br[jj]);
+      }
+    } else {  // DOT / L2 / L2SQ on packed column pairs (same operations and order as the scalar form)
+#pragma unroll 8
+      for (int e = 0; e < TK; ++e) {
+        const float4 av = *reinterpret_cast<const float4*>(&As[e][ty * 4]);
+        const float4 bv = *reinterpret_cast<const float4*>(&Bs[e][tx * 4]);
+        const float ar[4] = {av.x, av.y, av.z, av.w};
+        const uint64_t b01 = pk2(bv.x, bv.y), b23 = pk2(bv.z, bv.w);
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          const uint64_t a2 = pk2(ar[ii], ar[ii]);
+          if (FAM == FAM_DOT) {
+            acc2[ii][0] = fma2(a2, b01, acc2[ii][0]);
+            acc2[ii][1] = fma2(a2, b23, acc2[ii][1]);
+          } else {
+            const uint64_t u0 = sub2(a2, b01), u1 = sub2(a2, b23);
+            acc2[ii][0] = fma2(u0, u0, acc2[ii][0]);
+            acc2[ii][1] = fma2(u1, u1, acc2[ii][1]);
           }
+        }
       }
     }
     __syncthreads();
+  }
+  if (!CPLX && FAM != FAM_L1) {
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      upk2(acc2[ii][0], acc[ii][0], acc[ii][1]);
+      upk2(acc2[ii][1], acc[ii][2], acc[ii][3]);
+    }
   }
   const int tile = (c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   if (!splitk_reduce(acc, a.part, a.cnt, tile, ks, nks)) return;
@@ -731,6 +769,12 @@ __global__ void __launch_bounds__(256, 2) k_neg_bwd(NegArgs a) {
     }
   };
   float acc[4][4] = {};
+  uint64_t acc2[4][2] = {}, sv2[4][2];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    sv2[ii][0] = pk2(sv[ii][0], sv[ii][1]);
+    sv2[ii][1] = pk2(sv[ii][2], sv[ii][3]);
+  }
   const int nch = (nk + TK - 1) / TK, per = (nch + nks - 1) / nks;
   const int ch0 = min(nch, ks * per), ch1 = min(nch, ch0 + per);
   if (ch0 < ch1) load(ch0 * TK);
@@ -754,6 +798,20 @@ __global__ void __launch_bounds__(256, 2) k_neg_bwd(NegArgs a) {
         ov[0] = a_.x; ov[1] = a_.y; ov[2] = a_.z; ov[3] = a_.w;
         oi[0] = oi[1] = oi[2] = oi[3] = 0.f;
       }
+      if (!CPLX && FAM != FAM_L1) {  // DOT / L2 / L2SQ on packed column pairs (same operations and order)
+        const uint64_t o01 = pk2(ov[0], ov[1]), o23 = pk2(ov[2], ov[3]);
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) {
+          const uint64_t w2 = pk2(w[ii], w[ii]);
+          if (FAM == FAM_DOT) {
+            acc2[ii][0] = fma2(w2, o01, acc2[ii][0]);
+            acc2[ii][1] = fma2(w2, o23, acc2[ii][1]);
+          } else {  // u = self - other
+            acc2[ii][0] = fma2(w2, sub2(sv2[ii][0], o01), acc2[ii][0]);
+            acc2[ii][1] = fma2(w2, sub2(sv2[ii][1], o23), acc2[ii][1]);
+          }
+        }
+      } else {
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
@@ -778,8 +836,16 @@ __global__ void __launch_bounds__(256, 2) k_neg_bwd(NegArgs a) {
             acc[ii][ee] = fmaf(w[ii], u, acc[ii][ee]);
           }
         }
+      }
     }
     __syncthreads();
+  }
+  if (!CPLX && FAM != FAM_L1) {
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      upk2(acc2[ii][0], acc[ii][0], acc[ii][1]);
+      upk2(acc2[ii][1], acc[ii][2], acc[ii][3]);
+    }
   }
   const int tile = (zz * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   if (!splitk_reduce(acc, a.part, a.cnt, tile, ks, nks)) return;
@@ -839,7 +905,7 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
       sn = warp_sum(sn);
       if (lane == 0) {
         const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
-        a.b.loss[a.s.info[1]] = L;
+        store_loss(a.b.loss, a.s.info, L);
         const bool bad = !isfinite(L);
         a.b.flags[2 + (a.s.info[0] & 1)] = bad ? 1 : 0;
         if (bad) a.b.flags[0] = 1;

@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     sn = warp_sum(sn);
     if (lane == 0) {
       const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
-      a.loss[a.s.info[1]] = L;
+      store_loss(a.loss, a.s.info, L);
       const bool bad = !isfinite(L);
       a.flags[2 + (a.s.info[0] & 1)] = bad ? 1 : 0;
       if (bad) a.flags[0] = 1;

@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
       sn = warp_sum(sn);
       if (lane == 0) {
         const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
-        a.b.loss[a.s.info[1]] = L;
+        store_loss(a.b.loss, a.s.info, L);
         const bool bad = !isfinite(L);
         a.b.flags[2 + (a.s.info[0] & 1)] = bad ? 1 : 0;
         if (bad) a.b.flags[0] = 1;

@@ -71,7 +71,10 @@ def lib():
                                  _i64p, _i64p, _i32p]
         L.kge_train_step.argtypes = [ctypes.c_void_p, ctypes.c_int64, _fp]
         L.kge_train_batch.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, _fp]
-        L.kge_train_batch_async.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, _fp]
+        # raw addresses (ints): the pipelined path is called once per step, ctypes.cast per argument costs more than
+        # the C call
+        L.kge_train_batch_async.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                            ctypes.c_void_p]
         L.kge_score.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, _fp]
         L.kge_get_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_set_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
@@ -186,6 +189,7 @@ def _destroy_live_handles():
 class Handle:
     def __init__(self, ptr, cfg: Config, keep):
         self._h = ptr
+        self._tba = lib().kge_train_batch_async  # bound once (per-step pipelined entry point)
         self.cfg = cfg
         self._keep = keep
         _live.add(self)
@@ -247,8 +251,9 @@ class Handle:
     def train_batch_async_ptr(self, hp, rp, tp, loss_ptr):
         """Pipelined variant: enqueue the step (H2D batch, step, D2H loss into the pinned float at loss_ptr) and
         return; the loss is valid after sync()."""
-        _check(lib().kge_train_batch_async(self._h, ctypes.cast(hp, _i64p), ctypes.cast(rp, _i64p),
-                                           ctypes.cast(tp, _i64p), ctypes.cast(loss_ptr, _fp) if loss_ptr else None))
+        rc = self._tba(self._h, hp, rp, tp, loss_ptr or None)
+        if rc:
+            _check(rc)
 
     # kge_score
     def score(self, hs, rs, ts):

@@ -1,3 +1,5 @@
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 300 python tools/sample_trace.py > gpurun_out/sample_trace.txt 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+KGE_HOST_PROF=1 timeout 300 python tools/e2e_probe.py > gpurun_out/e2e_probe.txt 2>&1
+timeout 600 python bench.py --steps 2000 --warmup 20 --no-cpu-baseline > gpurun_out/bench.log 2>&1
