@@ -172,7 +172,7 @@ def main():
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--e2e-steps", type=int, default=1000)
     ap.add_argument("--lag", type=int, default=0, choices=[0, 1],
                     help="1: the paper's overlap of the entity update with the next step (reading c.12)")
     args = ap.parse_args()
@@ -309,6 +309,9 @@ def main():
     if pg:
         pg.barrier()
     ph, pr, pt, pl = pinned[0].data_ptr(), pinned[1].data_ptr(), pinned[2].data_ptr(), loss_buf.data_ptr()
+    for st in range(min(16, e2e_steps)):  # warm-up: the per-slot CUDA graphs are captured on first use
+        H.train_batch_async_ptr(ph + st * B * 8, pr + st * B * 8, pt + st * B * 8, pl + 4 * st)
+    H.sync()
     w0 = time.perf_counter()
     for st in range(e2e_steps):  # the public per-step call, on this step's pinned host arrays
         o = st * B * 8
@@ -322,8 +325,9 @@ def main():
     e2e = {"value": ws * B * e2e_steps / e2e_s, "unit": "positive triples/s", "h2d_bytes_per_step": 3 * B * 4,
            "d2h_bytes_per_step": 4, "steps": e2e_steps,
            "how": "kge_train_batch_async per step: host int64 (h,r,t)[B] from pinned memory, range-checked and "
-                  "narrowed to int32 on the host, H2D copy + sample + step + D2H copy of the step's loss into pinned "
-                  "memory enqueued every step; one sync at the end; host wall clock"}
+                  "narrowed to int32 on the host, H2D copy + sample + step enqueued every step (CUDA graphs), the "
+                  "step's loss stored by the device into the caller's pinned float; one sync at the end; host wall "
+                  "clock after 16 warm-up calls"}
     if not np.all(np.isfinite(loss_buf.numpy())):
         raise RuntimeError("e2e: non-finite or missing loss")
 
