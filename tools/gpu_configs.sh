@@ -2,7 +2,7 @@
 # bench lines for every BASELINE.json config on one GPU (the default bench is configs[4], Freebase TransE-L2)
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-run() { echo "== $*"; timeout 600 python bench.py --steps 2000 --warmup 20 "$@" 2>&1 | grep '^{' ; }
+run() { echo "== $*"; timeout 600 python bench.py --steps 2000 --warmup 20 --e2e-steps 500 "$@" 2>&1 | grep '^{' ; }
 {
 run --workload tiny
 run --workload fb15k --model distmult
