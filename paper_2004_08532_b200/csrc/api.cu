@@ -633,6 +633,7 @@ static int enqueue_step(kge_handle* h, const Slot& slot, int64_t s, int gi) {
     if (h->eupd_enqueued) e = cudaStreamWaitEvent(h->stream, h->ev_eupd, 0);
     h->buf.Gocc = h->gocc2[s & 1];
   }
+  h->next_slot = gi >= 0 ? d_slots(h) + h->ring + 1 + (gi + 1) % kge_handle::kGiven : d_slots(h) + (s + 1) % h->ring;
   if (e == cudaSuccess) e = launch_step(h, slot, s);
   if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, slot);
   if (e != cudaSuccess) return cuda_fail(e, "step");
@@ -772,6 +773,7 @@ static int batch_graphs(kge_handle* h, int gi, int64_t s, float* loss_host) {
              }, &h->g_samp[gi], cudaGraphNodeTypeKernel, &h->g_samp_node[gi]), "capture sample graph");
   }
   if (!h->g_step[gi]) {
+    h->next_slot = d_slots(h) + h->ring + 1 + (gi + 1) % kge_handle::kGiven;
     KGE_GCHK(capture_graph(h, h->stream, [&]() {
                cudaError_t x = launch_step(h, h->given_slots[gi], s);
                return x == cudaSuccess ? cudaMemcpyAsync(h->pinned_sink, h->buf.loss, 4, cudaMemcpyDeviceToHost, h->stream)

@@ -204,6 +204,7 @@ struct kge_handle {
   float4* ffma_part = nullptr;
   int32_t* ffma_cnt = nullptr;
   int32_t ffma_ks_max = 1;  // the split factor the scratch was sized for
+  const kge::Slot* next_slot = nullptr;  // device slot of the step after the one being enqueued (row prefetch)
   cudaEvent_t ev_samp[2] = {}, ev_free[2] = {};
   int64_t half_first[2] = {-1, -1};  // first step held by each ring half (-1: none)
   bool half_waited[2] = {false, false};

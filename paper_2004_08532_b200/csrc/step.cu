@@ -1073,6 +1073,7 @@ struct UpdateArgs {
   float* grel_split;           // P > 1: per-rank sums of split relations
   int32_t* seg_cnt;            // [B + n_occ] per-unique-row segment arrival counters (zero between steps)
   int32_t pos_lo, pos_hi;      // positions handled: [0, B) relations, [B, B + n_occ) entities (lag = 1 splits them)
+  const Slot* next;            // device slot of the next step (P == 1), or nullptr: its entity rows are prefetched
 };
 
 // Row accumulator: V float4 per lane.
@@ -1153,6 +1154,20 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
     r0 = off[u];
     r1 = off[u + 1];
     live = (p - r0) % kSeg == 0;
+  }
+  if (a.next) {
+    // warm L2 and the TLBs with the next step's entity rows while this step's backward still runs: its gather follows
+    // this kernel and otherwise pays the page walks of random rows in a 137 GB table (the rows this update writes
+    // stay coherent in L2). One 128-byte line per thread.
+    const Slot nx = *a.next;
+    const int lines = (dm.d * 4 + 127) / 128;
+    const int n = dm.n_occ * lines;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+      const int o = q / lines, l = q - o * lines;
+      const int32_t e = o < dm.B ? nx.ph[o] : (o < 2 * dm.B ? nx.pt[o - dm.B] : nx.neg[o - 2 * dm.B]);
+      if (e >= 0 && e < dm.n_entities)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.ent + (int64_t)e * dm.d + l * 32));
+    }
   }
   if (__syncthreads_or(live) == 0) return;  // no segment starts in this CTA: leave before the wait
   if (!live) return;
@@ -1311,7 +1326,8 @@ cudaError_t launch_update_range(kge_handle* h, const Slot& s, int lo, int hi, cu
   StepBuffers b = h->buf;
   b.Gocc = gocc;
   UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, b, h->P > 1 ? h->dist.gu : nullptr,
-                h->P > 1 ? h->dist.split_index : nullptr, h->dist.grel_split, h->seg_cnt, lo, hi};
+                h->P > 1 ? h->dist.split_index : nullptr, h->dist.grel_split, h->seg_cnt, lo, hi,
+                lo == 0 && h->P == 1 ? h->next_slot : nullptr};
   const int grid = (hi - lo + 7) / 8;
   if (grid <= 0) return cudaSuccess;
   const int w4 = std::max(dm.d, dm.drel) / 4;

@@ -206,17 +206,17 @@ __global__ void __launch_bounds__(256) k_tr_gemm(TrArgs a) {
   // transposed?, K)
   auto run_term = [&](const float* Ab, int lda, bool At, const float* Bb, int ldb, bool Bt, int K) {
     for (int k0 = 0; k0 < K; k0 += GK) {
+      // coalesced: consecutive threads walk the operand's contiguous dimension (k for row-major A / transposed B,
+      // m / n otherwise)
       for (int idx = threadIdx.x; idx < GK * GT; idx += blockDim.x) {
-        const int kk = idx / GT, mm = idx % GT;
-        const int gk = k0 + kk;
+        const int kka = At ? idx / GT : idx % GK, mma = At ? idx % GT : idx / GK;
+        const int kkb = Bt ? idx % GK : idx / GT, nnb = Bt ? idx / GK : idx % GT;
         float va = 0.f, vb = 0.f;
-        if (gk < K) {
-          const int gm = m0 + mm, gn = n0 + mm;
-          if (gm < Mrows) va = At ? Ab[(int64_t)gk * lda + gm] : Ab[(int64_t)gm * lda + gk];
-          if (gn < Ncols) vb = Bt ? Bb[(int64_t)gn * ldb + gk] : Bb[(int64_t)gk * ldb + gn];
-        }
-        As[kk][mm] = va;
-        Bs[kk][mm] = vb;
+        const int gka = k0 + kka, gkb = k0 + kkb, gm = m0 + mma, gn = n0 + nnb;
+        if (gka < K && gm < Mrows) va = At ? Ab[(int64_t)gka * lda + gm] : Ab[(int64_t)gm * lda + gka];
+        if (gkb < K && gn < Ncols) vb = Bt ? Bb[(int64_t)gn * ldb + gkb] : Bb[(int64_t)gkb * ldb + gn];
+        As[kka][mma] = va;
+        Bs[kkb][nnb] = vb;
       }
       __syncthreads();
 #pragma unroll
@@ -430,6 +430,48 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
   const float* M = a.proj + (int64_t)r * d * d;
   float* gH = a.b.Gocc + (int64_t)i * d;
   float* gT = a.b.Gocc + (int64_t)(dm.B + i) * d;
+  // dh = M^T gMh, dt = M^T gMt: warp w takes rows w, w + 8, ... (coalesced row reads, 2 x kCol independent chains per
+  // lane), the 8 warp partials are added in warp order (deterministic)
+  constexpr int kCol = 8;  // columns per lane: d <= 256
+  float* part = sm + 2 * d;  // [8 warps][2][d]
+  const int wid = threadIdx.x >> 5;
+  if (d <= 32 * kCol) {
+    float ah[kCol], at[kCol];
+#pragma unroll
+    for (int j = 0; j < kCol; ++j) ah[j] = at[j] = 0.f;
+    for (int row = wid; row < d; row += 8) {
+      const float* mr = M + (int64_t)row * d;
+      const float gh = sgh[row], gt = sgt[row];
+#pragma unroll
+      for (int j = 0; j < kCol; ++j) {
+        const int b = lane + 32 * j;
+        if (b < d) {
+          const float m = __ldg(mr + b);
+          ah[j] = fmaf(m, gh, ah[j]);
+          at[j] = fmaf(m, gt, at[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kCol; ++j) {
+      const int b = lane + 32 * j;
+      if (b < d) {
+        part[(wid * 2) * d + b] = ah[j];
+        part[(wid * 2 + 1) * d + b] = at[j];
+      }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < d; b += blockDim.x) {
+      float sh = 0.f, st = 0.f;
+      for (int w8 = 0; w8 < 8; ++w8) {
+        sh += part[(w8 * 2) * d + b];
+        st += part[(w8 * 2 + 1) * d + b];
+      }
+      gH[b] = sh;
+      gT[b] = st;
+    }
+    return;
+  }
   for (int b = threadIdx.x; b < d; b += blockDim.x) {
     float ah = 0.f, at = 0.f;
     for (int row = 0; row < d; ++row) {
@@ -504,7 +546,7 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   k_tr_reduce<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, h->stream>>>(a); dbg(h, "k_tr_reduce");
   launch_end(h, KGE_K_NEG_BWD);
   launch_begin(h, KGE_K_CHAIN);
-  k_tr_chain<<<dm.B + 1, 256, 2 * dm.d * sizeof(float), h->stream>>>(a); dbg(h, "k_tr_chain");
+  k_tr_chain<<<dm.B + 1, 256, 18 * dm.d * sizeof(float), h->stream>>>(a); dbg(h, "k_tr_chain");
   const dim3 gm((dm.d + GT - 1) / GT, (dm.d + GT - 1) / GT, dm.B);
   k_tr_gemm<2><<<gm, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<2>");
   launch_end(h, KGE_K_CHAIN);
