@@ -341,9 +341,10 @@ bool tc_init(kge_handle* h);
 void tc_destroy(kge_handle* h);
 bool tc_supported(const kge_handle* h);
 int32_t tc_neg_parts(const kge_handle* h);
-// loss_slot: ring slot of the step's loss; when tc_fuses_chain(h) the backward kernel also applies the positive chain
+// the step's loss goes to the ring slot named by the sample slot (Slot::info); when tc_fuses_chain(h) the backward
+// kernel also applies the positive chain
 // rule and reduces the loss (k_chain is not launched)
-cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot);
+cudaError_t launch_tc_neg(kge_handle* h, const Slot& s);
 bool tc_fuses_chain(const kge_handle* h);
 bool tc_flow();  // chunk-level dataflow counters on (KGE_FLOW=1)
 

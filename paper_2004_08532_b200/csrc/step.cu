@@ -875,7 +875,6 @@ struct ChainArgs {
   const float* rel;
   StepBuffers b;
   int32_t n_neg_parts;
-  int32_t loss_slot;
 };
 
 __device__ __forceinline__ void dpair(int fam, float o, float x, float scale, float& go, float& gx) {
@@ -1372,9 +1371,8 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   }
 
   NegArgs na{dm, h->buf, h->buf.Gocc, nullptr, nullptr, 1};
-  const int32_t loss_slot = (int32_t)(step % h->ring);
   if (h->cfg.neg_precision == KGE_PREC_TF32 && tc_supported(h)) {
-    cudaError_t e = launch_tc_neg(h, s, loss_slot);
+    cudaError_t e = launch_tc_neg(h, s);
     if (e != cudaSuccess) return e;
     if (tc_fuses_chain(h)) return launch_update(h, s);  // chain rule + loss done in the backward epilogue
   } else {
@@ -1386,7 +1384,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
       case FAM_CMOD: launch_neg<FAM_CMOD>(h, na); break;
     }
   }
-  ChainArgs ca{dm, s, h->rows, h->rel, h->buf, h->n_neg_parts, loss_slot};
+  ChainArgs ca{dm, s, h->rows, h->rel, h->buf, h->n_neg_parts};
   launch_begin(h, KGE_K_CHAIN);
   const unsigned cgrid = (dm.B + 7) / 8 + 1;
   switch (row_v(dm.d)) {

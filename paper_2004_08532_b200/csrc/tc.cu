@@ -81,7 +81,7 @@ struct TcArgs {
   float* Grel;
   float* loss;
   int32_t* flags;
-  int32_t loss_slot, n_neg_parts;
+  int32_t n_neg_parts;
   float inv_bk;    // 1 / (B k), the dL/df- scale (reading c.9)
   float4* xbuf;    // backward split-K exchange scratch
   uint32_t* flow;  // dataflow counters (StepBuffers::flow)
@@ -789,13 +789,13 @@ bool tc_flow() {
 
 bool tc_fuses_chain(const kge_handle* h) { return h->dims.model == KGE_TRANSE_L2; }
 
-cudaError_t launch_tc_neg(kge_handle* h, const Slot& s, int32_t loss_slot) {
+cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
   const TcState* st = static_cast<const TcState*>(h->tc);
   TcArgs a{dm, h->dp, h->kp, h->buf.O, h->buf.X, h->buf.onorm, h->buf.xnorm, h->buf.W, h->buf.lneg, h->buf.dO,
            h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128,
            tc_fuses_chain(h) ? 1 : 0, s, h->rows, h->buf.wpos, h->buf.pstat, h->buf.lpos, h->buf.Grel,
-           h->buf.loss, h->buf.flags, loss_slot, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->xbuf, tc_flow() ? h->buf.flow : nullptr,
+           h->buf.loss, h->buf.flags, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->xbuf, tc_flow() ? h->buf.flow : nullptr,
            2 * ((dm.k + kNT - 1) / kNT) * ((dm.g + 127) / 128), st->fwd_cx};
   dim3 gf(2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128, dm.C);  // x = 2 tile + split-K half
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;

@@ -35,7 +35,6 @@ struct TrArgs {
   float* proj_st;
   StepBuffers b;
   TrBuffers t;
-  int32_t loss_slot;
   int32_t n_neg_parts;
 };
 
@@ -525,7 +524,8 @@ static void dbg(kge_handle* h, const char* what) {
 
 cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
-  TrArgs a{dm, s, h->ent, h->rel, h->proj, h->proj_st, h->buf, h->tr_buf, (int32_t)(step % h->ring), dm.B};
+  (void)step;
+  TrArgs a{dm, s, h->ent, h->rel, h->proj, h->proj_st, h->buf, h->tr_buf, dm.B};
   cudaError_t e;
   launch_begin(h, KGE_K_GATHER);
   k_tr_groups<<<1, 1024, 0, h->stream>>>(a); dbg(h, "k_tr_groups");
