@@ -562,7 +562,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (sample_init() != cudaSuccess || step_preload() != cudaSuccess || dist_preload() != cudaSuccess)
     return fail(cuda_fail(cudaGetLastError(), "kernel preload"));
   if (cfg->model == KGE_TRANSR) h->n_neg_parts = dm.B;  // one loss partial per (relation, chunk) group
-  if (cfg->neg_precision == KGE_PREC_TF32 && cfg->model != KGE_TRANSR) tc_init(h);  // DistMult / ComplEx / TransE-L2 on tcgen05
+  if (cfg->neg_precision == KGE_PREC_TF32 && cfg->model != KGE_TRANSR) tc_init(h);
+  if (cfg->model == KGE_TRANSR) transr_tc_init(h);  // DistMult / ComplEx / TransE-L2 on tcgen05
   if (tc_supported(h)) h->n_neg_parts = tc_neg_parts(h);
   *out = h;
   return KGE_OK;
@@ -1141,6 +1142,7 @@ void kge_destroy(kge_handle* h) {
   if (h->pinned_sink) cudaFreeHost(h->pinned_sink);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   tc_destroy(h);
+  transr_destroy(h);
   delete h;
 }
 

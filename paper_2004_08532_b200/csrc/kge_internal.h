@@ -1,5 +1,6 @@
 // kge_internal.h -- host-side state of a kge_handle and the launchers each .cu file exports.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -243,6 +244,7 @@ struct kge_handle {
   int32_t dp = 0, kp = 0;
   void* tc = nullptr;  // TcState (tc.cu)
   kge::TrBuffers tr_buf{};
+  void* tr_tc = nullptr;  // TransR tcgen05 projection state (transr.cu), or nullptr (FFMA)
   // ranks
   int32_t P = 1, rank = 0;
   int64_t ent_rows = 0;  // rows of the local entity table (shard when P > 1)
@@ -326,6 +328,8 @@ cudaError_t launch_update_range(kge_handle* h, const Slot& s, int lo, int hi, cu
 // transr.cu
 cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step);
 bool transr_init(kge_handle* h);
+void transr_destroy(kge_handle* h);
+void transr_tc_init(kge_handle* h);  // tcgen05 projections (TF32 negatives path)
 
 // dist.cu
 int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<int32_t>& owner);
@@ -347,5 +351,9 @@ int32_t tc_neg_parts(const kge_handle* h);
 cudaError_t launch_tc_neg(kge_handle* h, const Slot& s);
 bool tc_fuses_chain(const kge_handle* h);
 bool tc_flow();  // chunk-level dataflow counters on (KGE_FLOW=1)
+// 3D TMA map over a [chunks x rows x cols] fp32 buffer (row pitch in floats), box {32, box_rows, 1}; out-of-range
+// columns / rows read as zeros
+bool make_map(CUtensorMap* m, const float* base, int cols, int rows, int chunks, int pitch, int box_rows,
+              CUtensorMapSwizzle sw);
 
 }  // namespace kge

@@ -671,7 +671,7 @@ static EncodeFn encode_fn() {
 }
 
 // 3D map over a [chunks x rows x cols] fp32 buffer with row pitch `pitch` floats; box {32, box_rows, 1}
-static bool make_map(CUtensorMap* m, const float* base, int cols, int rows, int chunks, int pitch, int box_rows,
+bool make_map(CUtensorMap* m, const float* base, int cols, int rows, int chunks, int pitch, int box_rows,
                      CUtensorMapSwizzle sw) {
   EncodeFn enc = encode_fn();
   if (!enc) return false;

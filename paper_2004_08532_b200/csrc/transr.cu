@@ -23,6 +23,7 @@
 
 #include "device_common.cuh"
 #include "kge_internal.h"
+#include "tc_ptx.cuh"
 
 namespace kge {
 
@@ -263,6 +264,105 @@ __global__ void __launch_bounds__(256) k_tr_gemm(TrArgs a) {
       if (n < Ncols) out[(int64_t)m * Ncols + n] = acc[ii][jj];
     }
   }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_tr_qx_tc: QX_g = X'_c M_u^T on tcgen05 (kind::tf32, TF32 negatives path): CTA = 128 negatives x N = d (<= 256)
+// of one group, K = d streamed in 32-float k-blocks through a TMA -> mbarrier pipeline; two MMA-issuing threads own
+// alternate K = 8 slices of every k-block (private TMEM accumulators at columns 0 / 256, added in a fixed order).
+// Both operands are K-major: A = the chunk's X' rows, B = M_u's rows (M_u[a][b] is B[n = a][k = b]).
+// ------------------------------------------------------------------------------------------------
+struct TrTc {
+  CUtensorMap mX;  // X' [C*k rows x d cols] (pitch dp), box {32, 128}
+  CUtensorMap mM;  // proj [n_rel][d rows][d cols], box {32, N}
+  int N = 0;       // d rounded up to 16
+};
+constexpr int kTrStages = 4;
+
+__global__ void __launch_bounds__(128, 1)
+    k_tr_qx_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mM, TrArgs a, int N) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[kTrStages], empty[kTrStages], done;
+  __shared__ uint32_t tbase;
+  const Dims& dm = a.dm;
+  const TrBuffers& T = a.t;
+  const int grp = blockIdx.y;
+  if (grp >= *T.n_groups) return;  // uniform per CTA, before any barrier / TMEM use
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = dm.d, k = dm.k, m0 = blockIdx.x * 128;
+  const int u = T.grp_u[grp], c = T.grp_c[grp], r = a.s.rel_uniq[u];
+  const int nkb = (d + 31) / 32;
+  const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)N * 128;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTrStages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 2);
+    }
+    tc::mbar_init(&done, 2);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tbase, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (warp == 0 && lane == 0) {  // TMA producer
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kTrStages;
+      if (kb >= kTrStages) tc::mbar_wait(&empty[s], ((kb / kTrStages) - 1) & 1);
+      uint8_t* sa = smem + s * STAGE;
+      tc::mbar_arrive_expect_tx(&full[s], STAGE);
+      tc::tma_load_3d(sa, &mX, &full[s], kb * 32, c * k + m0, 0);
+      tc::tma_load_3d(sa + A_BYTES, &mM, &full[s], kb * 32, 0, r);
+    }
+  } else if (warp >= 2 && lane == 0) {  // MMA issuers q = 0, 1: slices 2q, 2q + 1 of each k-block
+    const int q = warp - 2;
+    const uint32_t idesc = tc::idesc_tf32(128, N, false, false);
+    const uint32_t acc = tmem + (uint32_t)(q * 256);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kTrStages;
+      tc::mbar_wait(&full[s], (kb / kTrStages) & 1);
+      tc::tc_fence_after();
+      const uint32_t sa = tc::smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int sl = 2 * q + h2;
+        tc::mma_tf32(acc, tc::sdesc(sa + sl * 32, 16, 1024), tc::sdesc(sb + sl * 32, 16, 1024), idesc,
+                     (kb | h2) ? 1u : 0u);
+      }
+      tc::mma_commit(&empty[s]);
+    }
+    tc::mma_commit(&done);
+  }
+  __syncwarp();
+  tc::mbar_wait(&done, 0);
+  tc::tc_fence_after();
+  // epilogue: thread <-> row m0 + 32 warp + lane; p0 + p1 per 32-column chunk, stored to QX_g (row pitch d)
+  const int row = m0 + warp * 32 + lane;
+  float* out = T.QX + (int64_t)grp * k * d + (int64_t)row * d;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  for (int cb = 0; cb * 32 < d; ++cb) {
+    uint32_t p0[32], p1[32];
+    tc::tmem_ld32_nw(trow + cb * 32, p0);
+    tc::tmem_ld32_nw(trow + 256 + cb * 32, p1);
+    tc::tmem_wait_ld();
+    if (row < k) {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int col = cb * 32 + 4 * v;
+        if (col < d)
+          *reinterpret_cast<float4*>(out + col) =
+              make_float4(__uint_as_float(p0[4 * v]) + __uint_as_float(p1[4 * v]),
+                          __uint_as_float(p0[4 * v + 1]) + __uint_as_float(p1[4 * v + 1]),
+                          __uint_as_float(p0[4 * v + 2]) + __uint_as_float(p1[4 * v + 2]),
+                          __uint_as_float(p0[4 * v + 3]) + __uint_as_float(p1[4 * v + 3]));
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -536,7 +636,14 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   launch_end(h, KGE_K_GATHER);
   const dim3 gk((dm.d + GT - 1) / GT, (dm.k + GT - 1) / GT, dm.B);
   launch_begin(h, KGE_K_NEG_FWD);
-  k_tr_gemm<0><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<0>");
+  if (h->tr_tc) {
+    const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
+    const size_t smem = (size_t)kTrStages * (128 * 128 + (size_t)tt->N * 128) + 1024;
+    k_tr_qx_tc<<<dim3((dm.k + 127) / 128, dm.B), 128, smem, h->stream>>>(tt->mX, tt->mM, a, tt->N);
+    dbg(h, "k_tr_qx_tc");
+  } else {
+    k_tr_gemm<0><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<0>");
+  }
   const size_t score_smem = (size_t)(2 * RB * dm.d + JB * dm.d + RB * JB) * sizeof(float);
   k_tr_score<<<dm.B, 256, score_smem, h->stream>>>(a); dbg(h, "k_tr_score");
   launch_end(h, KGE_K_NEG_FWD);
@@ -615,6 +722,31 @@ bool transr_init(kge_handle* h) {
     return false;
   }
   return true;
+}
+
+// after the step buffers exist (the maps name X' and the projection table)
+void transr_tc_init(kge_handle* h) {
+  // TF32 negatives path: the projections QX_g = X'_c M_u^T on tcgen05 (d <= 256), else FFMA
+  const Dims& dm = h->dims;
+  if (h->cfg.neg_precision == KGE_PREC_TF32 && dm.d <= 256 && dm.d % 4 == 0) {
+    TrTc* tt = new TrTc();
+    tt->N = (dm.d + 15) / 16 * 16;
+    bool ok = make_map(&tt->mX, h->buf.X, dm.d, dm.C * dm.k, 1, dm.dp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok = ok && make_map(&tt->mM, h->proj, dm.d, dm.d, (int)dm.n_relations, dm.d, tt->N, CU_TENSOR_MAP_SWIZZLE_128B);
+    const size_t smem = (size_t)kTrStages * (128 * 128 + (size_t)tt->N * 128) + 1024;
+    ok = ok && cudaFuncSetAttribute(k_tr_qx_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+    if (ok) {
+      h->tr_tc = tt;
+    } else {
+      cudaGetLastError();
+      delete tt;
+    }
+  }
+}
+
+void transr_destroy(kge_handle* h) {
+  delete static_cast<TrTc*>(h->tr_tc);
+  h->tr_tc = nullptr;
 }
 
 }  // namespace kge

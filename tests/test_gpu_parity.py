@@ -313,3 +313,16 @@ def test_tc_matches_fp32_path_closely():
     b, _, _ = _tiny("distmult", dim=64, precision="fp32")
     la, lb = a.train_step(5), b.train_step(5)
     assert np.max(np.abs(la - lb) / np.abs(lb)) <= 2e-3
+
+
+@pytest.mark.parametrize("graph,shape,steps", [("tiny", (64, 16, 16, 32), 20), ("fb15k", (256, 64, 64, 40), 10),
+                                               ("tiny", (96, 24, 200, 200), 5)])
+def test_transr_tf32_projections(graph, shape, steps):
+    # TF32 negatives path of configs[3]: the grouped projections QX_g = X'_c M_u^T on tcgen05 (k_tr_qx_tc; d not a
+    # multiple of 16 -> out-of-range rows / columns of the boxes read as zeros; k = 200 -> ragged 128-row tile)
+    B, g, k, d = shape
+    gr = synth.graph(graph)
+    trip = gr.triples()
+    gpu, orc = _pair("transr", gr.n_entities, gr.n_relations, trip, d, B, g, k, lr=0.05, precision="tf32")
+    lg, lo = gpu.train_step(steps), orc.train(steps)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 2e-3, (lg, lo)
