@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(128, 1)
 // per-group scores: rows of the group in blocks of RB, negatives in tiles of JB
 // ------------------------------------------------------------------------------------------------
 constexpr int RB = 16, JB = 32;
+size_t transr_score_smem(int d) { return (size_t)(2 * RB * (d | 1) + JB * (d | 1) + RB * JB) * sizeof(float); }
 
 __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
   const Dims& dm = a.dm;
@@ -381,10 +382,11 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
   }
   extern __shared__ float sm[];
   const int d = dm.d, k = dm.k;
-  float* so = sm;                 // [RB][d]
-  float* sq = so + RB * d;        // [JB][d]
-  float* sdo = sq + JB * d;       // [RB][d]
-  float* scf = sdo + RB * d;      // [RB][JB]
+  const int ds = d | 1;           // odd smem row stride: the pair loop's 32 lanes read 32 different rows conflict-free
+  float* so = sm;                 // [RB][ds]
+  float* sq = so + RB * ds;       // [JB][ds]
+  float* sdo = sq + JB * ds;      // [RB][ds]
+  float* scf = sdo + RB * ds;     // [RB][JB]
   const int p0 = T.grp_p0[grp], p1 = T.grp_p1[grp];
   const float* QX = T.QX + (int64_t)grp * k * d;
   float* dQ = T.dQ + (int64_t)grp * k * d;
@@ -394,15 +396,15 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
     const int nr = min(RB, p1 - rb);
     for (int idx = threadIdx.x; idx < RB * d; idx += blockDim.x) {
       const int rr = idx / d, e = idx % d;
-      so[idx] = rr < nr ? a.b.O[(int64_t)a.s.rel_occ[rb + rr] * dm.dp + e] : 0.f;
-      sdo[idx] = 0.f;
+      so[rr * ds + e] = rr < nr ? a.b.O[(int64_t)a.s.rel_occ[rb + rr] * dm.dp + e] : 0.f;
+      sdo[rr * ds + e] = 0.f;
     }
     for (int j0 = 0; j0 < k; j0 += JB) {
       const int nj = min(JB, k - j0);
       __syncthreads();
       for (int idx = threadIdx.x; idx < JB * d; idx += blockDim.x) {
-        const int jj = idx / d;
-        sq[idx] = jj < nj ? QX[(int64_t)(j0 + jj) * d + idx % d] : 0.f;
+        const int jj = idx / d, e = idx % d;
+        sq[jj * ds + e] = jj < nj ? QX[(int64_t)(j0 + jj) * d + e] : 0.f;
       }
       __syncthreads();
       // pair statistics: RB x JB pairs, 2 per thread
@@ -411,8 +413,8 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
         float coef = 0.f;
         if (rr < nr && jj < nj) {
           float s2 = 0.f;
-          const float* ov = so + rr * d;
-          const float* qv = sq + jj * d;
+          const float* ov = so + rr * ds;
+          const float* qv = sq + jj * ds;
           for (int e = 0; e < d; ++e) {
             const float u = ov[e] - qv[e];
             s2 = fmaf(u, u, s2);
@@ -428,24 +430,24 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
       for (int idx = threadIdx.x; idx < RB * d; idx += blockDim.x) {
         const int rr = idx / d, e = idx % d;
         if (rr >= nr) continue;
-        float acc = sdo[idx];
-        const float ov = so[idx];
-        for (int jj = 0; jj < nj; ++jj) acc = fmaf(scf[rr * JB + jj], ov - sq[jj * d + e], acc);
-        sdo[idx] = acc;
+        float acc = sdo[rr * ds + e];
+        const float ov = so[rr * ds + e];
+        for (int jj = 0; jj < nj; ++jj) acc = fmaf(scf[rr * JB + jj], ov - sq[jj * ds + e], acc);
+        sdo[rr * ds + e] = acc;
       }
       for (int idx = threadIdx.x; idx < JB * d; idx += blockDim.x) {
         const int jj = idx / d, e = idx % d;
         if (jj >= nj) continue;
         float acc = rb == p0 ? 0.f : dQ[(int64_t)(j0 + jj) * d + e];
-        const float qv = sq[idx];
-        for (int rr = 0; rr < nr; ++rr) acc = fmaf(scf[rr * JB + jj], qv - so[rr * d + e], acc);
+        const float qv = sq[jj * ds + e];
+        for (int rr = 0; rr < nr; ++rr) acc = fmaf(scf[rr * JB + jj], qv - so[rr * ds + e], acc);
         dQ[(int64_t)(j0 + jj) * d + e] = acc;
       }
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < RB * d; idx += blockDim.x) {
       const int rr = idx / d, e = idx % d;
-      if (rr < nr) a.b.dO[(int64_t)a.s.rel_occ[rb + rr] * d + e] = sdo[idx];
+      if (rr < nr) a.b.dO[(int64_t)a.s.rel_occ[rb + rr] * d + e] = sdo[rr * ds + e];
     }
     __syncthreads();
   }
@@ -644,7 +646,7 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   } else {
     k_tr_gemm<0><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<0>");
   }
-  const size_t score_smem = (size_t)(2 * RB * dm.d + JB * dm.d + RB * JB) * sizeof(float);
+  const size_t score_smem = transr_score_smem(dm.d);
   k_tr_score<<<dm.B, 256, score_smem, h->stream>>>(a); dbg(h, "k_tr_score");
   launch_end(h, KGE_K_NEG_FWD);
   launch_begin(h, KGE_K_NEG_BWD);
@@ -712,7 +714,6 @@ cudaError_t launch_transr_score(kge_handle* h, const int32_t* hs, const int32_t*
   return cudaGetLastError();
 }
 
-size_t transr_score_smem(int d) { return (size_t)(2 * RB * d + JB * d + RB * JB) * sizeof(float); }
 
 bool transr_init(kge_handle* h) {
   cudaError_t e = cudaFuncSetAttribute(k_tr_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
