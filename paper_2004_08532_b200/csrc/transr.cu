@@ -273,14 +273,26 @@ __global__ void __launch_bounds__(256) k_tr_gemm(TrArgs a) {
 // Both operands are K-major: A = the chunk's X' rows, B = M_u's rows (M_u[a][b] is B[n = a][k = b]).
 // ------------------------------------------------------------------------------------------------
 struct TrTc {
-  CUtensorMap mX;  // X' [C*k rows x d cols] (pitch dp), box {32, 128}
-  CUtensorMap mM;  // proj [n_rel][d rows][d cols], box {32, N}
-  int N = 0;       // d rounded up to 16
+  CUtensorMap mX;   // X' [C*k rows x d cols] (pitch dp), box {32, 128}
+  CUtensorMap mM;   // proj [n_rel][d rows][d cols], box {32, N}: B of QX (K-major)
+  CUtensorMap mMn;  // proj, box {32, 32}, SWIZZLE_128B_ATOM_32B: B of P = dQ M (MN-major, one box per 32-column block)
+  CUtensorMap mdQ;  // dQ [B groups][k rows][d cols], box {32, 128}
+  int N = 0;        // d rounded up to 16
 };
 constexpr int kTrStages = 4;
 
+__device__ __forceinline__ uint64_t sdesc_mn32(uint32_t saddr, uint32_t lbo) {
+  // tf32 MN-major: SWIZZLE_128B_BASE32B (layout type 1), SBO = 512 B between 4-row K atoms (see tc.cu)
+  uint64_t d = tc::sdesc(saddr, lbo, 512);
+  d &= ~((uint64_t)7 << 61);
+  d |= (uint64_t)1 << 61;
+  return d;
+}
+
+// MODE 0: QX_g = X'_c M_u^T (k_tr_gemm<0>); MODE 1: P_g = dQ_g M_u (k_tr_gemm<1>), both into T.QX + g k d
+template <int MODE>
 __global__ void __launch_bounds__(128, 1)
-    k_tr_qx_tc(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mM, TrArgs a, int N) {
+    k_tr_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, TrArgs a, int N) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kTrStages], empty[kTrStages], done;
@@ -292,8 +304,8 @@ __global__ void __launch_bounds__(128, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = dm.d, k = dm.k, m0 = blockIdx.x * 128;
   const int u = T.grp_u[grp], c = T.grp_c[grp], r = a.s.rel_uniq[u];
-  const int nkb = (d + 31) / 32;
-  const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)N * 128;
+  const int nkb = (d + 31) / 32, nnb = (N + 31) / 32;
+  const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)nnb * 4096;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTrStages; ++s) {
       tc::mbar_init(&full[s], 1);
@@ -312,13 +324,20 @@ __global__ void __launch_bounds__(128, 1)
       const int s = kb % kTrStages;
       if (kb >= kTrStages) tc::mbar_wait(&empty[s], ((kb / kTrStages) - 1) & 1);
       uint8_t* sa = smem + s * STAGE;
-      tc::mbar_arrive_expect_tx(&full[s], STAGE);
-      tc::tma_load_3d(sa, &mX, &full[s], kb * 32, c * k + m0, 0);
-      tc::tma_load_3d(sa + A_BYTES, &mM, &full[s], kb * 32, 0, r);
+      if (MODE == 0) {
+        tc::mbar_arrive_expect_tx(&full[s], A_BYTES + (uint32_t)N * 128);
+        tc::tma_load_3d(sa, &mA, &full[s], kb * 32, c * k + m0, 0);
+        tc::tma_load_3d(sa + A_BYTES, &mB, &full[s], kb * 32, 0, r);
+      } else {
+        tc::mbar_arrive_expect_tx(&full[s], STAGE);
+        tc::tma_load_3d(sa, &mA, &full[s], kb * 32, m0, grp);
+        for (int nb = 0; nb < nnb; ++nb)  // rows a = kb*32.., columns b = nb*32..: [32 K rows][32 N] per block
+          tc::tma_load_3d(sa + A_BYTES + nb * 4096, &mB, &full[s], nb * 32, kb * 32, r);
+      }
     }
   } else if (warp >= 2 && lane == 0) {  // MMA issuers q = 0, 1: slices 2q, 2q + 1 of each k-block
     const int q = warp - 2;
-    const uint32_t idesc = tc::idesc_tf32(128, N, false, false);
+    const uint32_t idesc = tc::idesc_tf32(128, N, false, MODE == 1);
     const uint32_t acc = tmem + (uint32_t)(q * 256);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kTrStages;
@@ -328,8 +347,8 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
         const int sl = 2 * q + h2;
-        tc::mma_tf32(acc, tc::sdesc(sa + sl * 32, 16, 1024), tc::sdesc(sb + sl * 32, 16, 1024), idesc,
-                     (kb | h2) ? 1u : 0u);
+        const uint64_t bd = MODE == 0 ? tc::sdesc(sb + sl * 32, 16, 1024) : sdesc_mn32(sb + sl * 1024, 4096);
+        tc::mma_tf32(acc, tc::sdesc(sa + sl * 32, 16, 1024), bd, idesc, (kb | h2) ? 1u : 0u);
       }
       tc::mma_commit(&empty[s]);
     }
@@ -338,7 +357,7 @@ __global__ void __launch_bounds__(128, 1)
   __syncwarp();
   tc::mbar_wait(&done, 0);
   tc::tc_fence_after();
-  // epilogue: thread <-> row m0 + 32 warp + lane; p0 + p1 per 32-column chunk, stored to QX_g (row pitch d)
+  // epilogue: thread <-> row m0 + 32 warp + lane; p0 + p1 per 32-column chunk, stored to row pitch d
   const int row = m0 + warp * 32 + lane;
   float* out = T.QX + (int64_t)grp * k * d + (int64_t)row * d;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
@@ -364,6 +383,8 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, 512);
 }
+
+static size_t tr_tc_smem(int N) { return (size_t)kTrStages * (128 * 128 + (size_t)((N + 31) / 32) * 4096) + 1024; }
 
 // ------------------------------------------------------------------------------------------------
 // per-group scores: rows of the group in blocks of RB, negatives in tiles of JB
@@ -640,9 +661,8 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   launch_begin(h, KGE_K_NEG_FWD);
   if (h->tr_tc) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
-    const size_t smem = (size_t)kTrStages * (128 * 128 + (size_t)tt->N * 128) + 1024;
-    k_tr_qx_tc<<<dim3((dm.k + 127) / 128, dm.B), 128, smem, h->stream>>>(tt->mX, tt->mM, a, tt->N);
-    dbg(h, "k_tr_qx_tc");
+    k_tr_tc<0><<<dim3((dm.k + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream>>>(tt->mX, tt->mM, a, tt->N);
+    dbg(h, "k_tr_tc<0>");
   } else {
     k_tr_gemm<0><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<0>");
   }
@@ -650,7 +670,13 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   k_tr_score<<<dm.B, 256, score_smem, h->stream>>>(a); dbg(h, "k_tr_score");
   launch_end(h, KGE_K_NEG_FWD);
   launch_begin(h, KGE_K_NEG_BWD);
-  k_tr_gemm<1><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<1>");
+  if (h->tr_tc) {
+    const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
+    k_tr_tc<1><<<dim3((dm.k + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream>>>(tt->mdQ, tt->mMn, a, tt->N);
+    dbg(h, "k_tr_tc<1>");
+  } else {
+    k_tr_gemm<1><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<1>");
+  }
   const int64_t tot = (int64_t)dm.C * dm.k * dm.d;
   k_tr_reduce<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, h->stream>>>(a); dbg(h, "k_tr_reduce");
   launch_end(h, KGE_K_NEG_BWD);
@@ -734,8 +760,12 @@ void transr_tc_init(kge_handle* h) {
     tt->N = (dm.d + 15) / 16 * 16;
     bool ok = make_map(&tt->mX, h->buf.X, dm.d, dm.C * dm.k, 1, dm.dp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     ok = ok && make_map(&tt->mM, h->proj, dm.d, dm.d, (int)dm.n_relations, dm.d, tt->N, CU_TENSOR_MAP_SWIZZLE_128B);
-    const size_t smem = (size_t)kTrStages * (128 * 128 + (size_t)tt->N * 128) + 1024;
-    ok = ok && cudaFuncSetAttribute(k_tr_qx_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+    ok = ok && make_map(&tt->mMn, h->proj, dm.d, dm.d, (int)dm.n_relations, dm.d, 32,
+                        CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    ok = ok && make_map(&tt->mdQ, h->tr_buf.dQ, dm.d, dm.k, dm.B, dm.d, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    const size_t smem = tr_tc_smem(tt->N);
+    ok = ok && cudaFuncSetAttribute(k_tr_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+    ok = ok && cudaFuncSetAttribute(k_tr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
     if (ok) {
       h->tr_tc = tt;
     } else {
