@@ -16,7 +16,8 @@
 //   k_tr_chain  : per positive: gMh, gMt, dr; dh = M^T gMh, dt = M^T gMt; rows for the dM outer products; loss CTA
 //   k_tr_gemm<2>: dM_u = sum_g dQ_g^T X'_c + sum_{i in u} (gMh_i h_i^T + gMt_i t_i^T)   (per unique relation)
 //   k_tr_proj   : Adagrad on M_u with one state per matrix (reading c.11, w = d*d)
-// FP32 FFMA throughout (64x64 tiles, 4x4 micro-tiles). The grouped GEMMs are the natural next tcgen05 target.
+// FP32 FFMA (64x64 tiles, 4x4 micro-tiles) on the FP32 path; on the TF32 negatives path the three grouped GEMMs run on
+// tcgen05 (k_tr_tc<0> / k_tr_tc<1> / k_tr_dm_tc, two MMA-issuing threads with private TMEM accumulators).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -277,6 +278,8 @@ struct TrTc {
   CUtensorMap mM;   // proj [n_rel][d rows][d cols], box {32, N}: B of QX (K-major)
   CUtensorMap mMn;  // proj, box {32, 32}, SWIZZLE_128B_ATOM_32B: B of P = dQ M (MN-major, one box per 32-column block)
   CUtensorMap mdQ;  // dQ [B groups][k rows][d cols], box {32, 128}
+  CUtensorMap mdQn;  // dQ, box {32, 32}, SWIZZLE_128B_ATOM_32B (A = dQ_g^T of dM, MN-major)
+  CUtensorMap mXn;   // X' [C*k rows x d cols], box {32, 32}, SWIZZLE_128B_ATOM_32B (B of dM, MN-major)
   int N = 0;        // d rounded up to 16
 };
 constexpr int kTrStages = 4;
@@ -377,6 +380,120 @@ __global__ void __launch_bounds__(128, 1)
                           __uint_as_float(p0[4 * v + 2]) + __uint_as_float(p1[4 * v + 2]),
                           __uint_as_float(p0[4 * v + 3]) + __uint_as_float(p1[4 * v + 3]));
       }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+}
+
+// dM_u = sum over the relation's groups g (in group order) of dQ_g^T X'_c  on tcgen05 (A = dQ_g^T and B = X'_c both
+// MN-major, accumulated in TMEM), then + sum_q U_q^T H_q over its positives (K = 2 n_u, a few rows) in FFMA in the
+// epilogue. CTA = 128 rows a of dM_u x N columns b; blockIdx.y = unique relation.
+__global__ void __launch_bounds__(128, 1)
+    k_tr_dm_tc(const __grid_constant__ CUtensorMap mdQn, const __grid_constant__ CUtensorMap mXn, TrArgs a, int N) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[kTrStages], empty[kTrStages], done;
+  __shared__ uint32_t tbase;
+  const Dims& dm = a.dm;
+  const TrBuffers& T = a.t;
+  const int u = blockIdx.y;
+  if (u >= *a.s.rel_n) return;  // uniform per CTA
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = dm.d, k = dm.k, m0 = blockIdx.x * 128;
+  const int g0 = T.rg_off[u], g1 = T.rg_off[u + 1];
+  const int nkg = (k + 31) / 32, nnb = (N + 31) / 32;
+  const int nk = (g1 - g0) * nkg;  // k-blocks over all groups of the relation
+  const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)nnb * 4096;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTrStages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 2);
+    }
+    tc::mbar_init(&done, 2);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tbase, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (warp == 0 && lane == 0) {  // TMA producer
+    for (int q = 0; q < nk; ++q) {
+      const int s = q % kTrStages;
+      if (q >= kTrStages) tc::mbar_wait(&empty[s], ((q / kTrStages) - 1) & 1);
+      const int g = g0 + q / nkg, kb = q % nkg, c = T.grp_c[g];
+      uint8_t* sa = smem + s * STAGE;
+      tc::mbar_arrive_expect_tx(&full[s], STAGE);
+      for (int b = 0; b < 4; ++b)  // A = dQ_g^T: [4 M-blocks of 32 a][32 K rows j][128 B]
+        tc::tma_load_3d(sa + b * 4096, &mdQn, &full[s], m0 + b * 32, kb * 32, g);
+      for (int nb = 0; nb < nnb; ++nb)  // B = X'_c: [N-blocks of 32 b][32 K rows j][128 B]
+        tc::tma_load_3d(sa + A_BYTES + nb * 4096, &mXn, &full[s], nb * 32, c * k + kb * 32, 0);
+    }
+  } else if (warp >= 2 && lane == 0) {  // MMA issuers q = 0, 1: slices 2q, 2q + 1 of each k-block
+    const int qi = warp - 2;
+    const uint32_t idesc = tc::idesc_tf32(128, N, true, true);
+    const uint32_t acc = tmem + (uint32_t)(qi * 256);
+    for (int q = 0; q < nk; ++q) {
+      const int s = q % kTrStages;
+      tc::mbar_wait(&full[s], (q / kTrStages) & 1);
+      tc::tc_fence_after();
+      const uint32_t sa = tc::smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int sl = 2 * qi + h2;
+        tc::mma_tf32(acc, sdesc_mn32(sa + sl * 1024, 4096), sdesc_mn32(sb + sl * 1024, 4096), idesc,
+                     (q | h2) ? 1u : 0u);
+      }
+      tc::mma_commit(&empty[s]);
+    }
+    tc::mma_commit(&done);
+  }
+  __syncwarp();
+  if (nk > 0) {
+    tc::mbar_wait(&done, 0);
+    tc::tc_fence_after();
+  }
+  // epilogue: row a = m0 + 32 warp + lane: TMEM p0 + p1, + sum_q U[q][a] H[q][b] over the relation's positives in q
+  // order. The H rows are staged 32 at a time in (free) pipeline shared memory by the whole CTA: a hub relation
+  // carries ~260 rows and per-thread global loads serialised it.
+  const int row = m0 + warp * 32 + lane;
+  const int q0 = 2 * a.s.rel_off[u], q1 = 2 * a.s.rel_off[u + 1];
+  float* out = T.dM + (int64_t)u * d * d + (int64_t)row * d;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  float* hs = reinterpret_cast<float*>(smem);  // [32 q][33]
+  for (int cb = 0; cb * 32 < d; ++cb) {
+    float v[32];
+    if (nk > 0) {
+      uint32_t p0[32], p1[32];
+      tc::tmem_ld32_nw(trow + cb * 32, p0);
+      tc::tmem_ld32_nw(trow + 256 + cb * 32, p1);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(p0[x]) + __uint_as_float(p1[x]);
+    } else {
+#pragma unroll
+      for (int x = 0; x < 32; ++x) v[x] = 0.f;
+    }
+    for (int qc = q0; qc < q1; qc += 32) {
+      const int nq = min(32, q1 - qc);
+      __syncthreads();  // the previous chunk's reads of hs are done
+      for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
+        const int qq = idx >> 5, x = idx & 31, col = cb * 32 + x;
+        hs[qq * 33 + x] = qq < nq && col < d ? T.H[(int64_t)(qc + qq) * d + col] : 0.f;
+      }
+      __syncthreads();
+      for (int qq = 0; qq < nq; ++qq) {
+        const float ua = row < d ? T.U[(int64_t)(qc + qq) * d + row] : 0.f;
+#pragma unroll
+        for (int x = 0; x < 32; ++x) v[x] = fmaf(ua, hs[qq * 33 + x], v[x]);
+      }
+    }
+    if (row < d) {
+#pragma unroll
+      for (int x = 0; x < 32; x += 4)
+        if (cb * 32 + x < d) *reinterpret_cast<float4*>(out + cb * 32 + x) = make_float4(v[x], v[x + 1], v[x + 2], v[x + 3]);
     }
   }
   tc::tc_fence_before();
@@ -683,7 +800,13 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   launch_begin(h, KGE_K_CHAIN);
   k_tr_chain<<<dm.B + 1, 256, 18 * dm.d * sizeof(float), h->stream>>>(a); dbg(h, "k_tr_chain");
   const dim3 gm((dm.d + GT - 1) / GT, (dm.d + GT - 1) / GT, dm.B);
-  k_tr_gemm<2><<<gm, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<2>");
+  if (h->tr_tc) {
+    const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
+    k_tr_dm_tc<<<dim3((dm.d + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream>>>(tt->mdQn, tt->mXn, a, tt->N);
+    dbg(h, "k_tr_dm_tc");
+  } else {
+    k_tr_gemm<2><<<gm, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<2>");
+  }
   launch_end(h, KGE_K_CHAIN);
   e = launch_update(h, s);
   dbg(h, "update");
@@ -763,9 +886,12 @@ void transr_tc_init(kge_handle* h) {
     ok = ok && make_map(&tt->mMn, h->proj, dm.d, dm.d, (int)dm.n_relations, dm.d, 32,
                         CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     ok = ok && make_map(&tt->mdQ, h->tr_buf.dQ, dm.d, dm.k, dm.B, dm.d, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok = ok && make_map(&tt->mdQn, h->tr_buf.dQ, dm.d, dm.k, dm.B, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    ok = ok && make_map(&tt->mXn, h->buf.X, dm.d, dm.C * dm.k, 1, dm.dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const size_t smem = tr_tc_smem(tt->N);
     ok = ok && cudaFuncSetAttribute(k_tr_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
     ok = ok && cudaFuncSetAttribute(k_tr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+    ok = ok && cudaFuncSetAttribute(k_tr_dm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
     if (ok) {
       h->tr_tc = tt;
     } else {
