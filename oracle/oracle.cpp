@@ -20,7 +20,7 @@ namespace {
 // ------------------------------------------------------------------------------------------------
 const uint32_t PHILOX_M0 = 0xD2511F53u, PHILOX_M1 = 0xCD9E8D57u;
 const uint32_t PHILOX_W0 = 0x9E3779B9u, PHILOX_W1 = 0xBB67AE85u;
-const uint32_t TAG_NEG = 1, TAG_PERM = 2, TAG_INIT = 3;
+const uint32_t TAG_NEG = 1, TAG_PERM = 2, TAG_INIT = 3, TAG_DEG = 4;
 
 void philox(const uint32_t in[4], const uint32_t key_in[2], uint32_t out[4]) {
   uint32_t x0 = in[0], x1 = in[1], x2 = in[2], x3 = in[3];
@@ -89,6 +89,21 @@ int64_t neg_id(uint64_t seed, int64_t n_ent, uint32_t step, uint32_t cg, uint32_
   philox(ctr, key, o);
   uint64_t u = (j & 1u) ? (((uint64_t)o[3] << 32) | o[2]) : (((uint64_t)o[1] << 32) | o[0]);
   unsigned __int128 prod = (unsigned __int128)u * (uint64_t)n_ent;
+  return (int64_t)(uint64_t)(prod >> 64);
+}
+
+// Degree-based in-batch negatives (PAPER.md:437-448 [3.3]: "uniformly sampling some of the mini-batch's triplets and
+// connecting the sampled head (tail) entities with the tail (head) entities of the mini-batch's triplets"; reading
+// c.3'): slot j < k_deg of chunk cg draws a batch position t = floor(u * B / 2^64) from Philox(ctr=(j/2, cg, s, DEG))
+// (words as in c.3); the negative is that triplet's tail (tail corruption) or head (head corruption), so an entity is
+// drawn with probability proportional to its degree in the mini-batch.
+int64_t deg_pos(uint64_t seed, int64_t B, uint32_t step, uint32_t cg, uint32_t j) {
+  uint32_t key[2];
+  seed_key(seed, key);
+  uint32_t ctr[4] = {j / 2u, cg, step, TAG_DEG}, o[4];
+  philox(ctr, key, o);
+  uint64_t u = (j & 1u) ? (((uint64_t)o[3] << 32) | o[2]) : (((uint64_t)o[1] << 32) | o[0]);
+  unsigned __int128 prod = (unsigned __int128)u * (uint64_t)B;
   return (int64_t)(uint64_t)(prod >> 64);
 }
 
@@ -457,9 +472,18 @@ struct Base {
     }
     for (int32_t c = 0; c < C(); ++c) {
       uint32_t cg = (uint32_t)(rank * C() + c);
-      if (mode) mode[c] = (int8_t)mode_of(cfg.corrupt, (uint32_t)s, cg);
+      const int32_t md = mode_of(cfg.corrupt, (uint32_t)s, cg);
+      if (mode) mode[c] = (int8_t)md;
       if (neg)
-        for (int64_t j = 0; j < k; ++j) neg[c * k + j] = neg_id(cfg.seed, cfg.n_entities, (uint32_t)s, cg, (uint32_t)j);
+        for (int64_t j = 0; j < k; ++j) {
+          if (j < cfg.neg_deg_k) {  // in-batch: the sampled triplet's tail (tail mode) / head (head mode)
+            int64_t hh, rr, tt;
+            triple(pos[deg_pos(cfg.seed, B, (uint32_t)s, cg, (uint32_t)j)], hh, rr, tt);
+            neg[c * k + j] = md == ORC_TAIL ? tt : hh;
+          } else {
+            neg[c * k + j] = neg_id(cfg.seed, cfg.n_entities, (uint32_t)s, cg, (uint32_t)j);
+          }
+        }
     }
   }
 };
@@ -846,6 +870,7 @@ void* orc_create(const orc_config* cfg, const int64_t* heads, const int64_t* rel
   if ((cfg->model == ORC_COMPLEX || cfg->model == ORC_ROTATE) && cfg->dim % 2 != 0) return nullptr;
   if (cfg->world_size < 1 || n_triples <= 0) return nullptr;
   if (cfg->lag != 0 && cfg->lag != 1) return nullptr;
+  if (cfg->neg_deg_k < 0 || cfg->neg_deg_k > cfg->neg_k) return nullptr;
   Base* b;
   if (cfg->precision == 1) {
     auto* t = new Trainer<float>();

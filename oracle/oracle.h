@@ -46,6 +46,8 @@ typedef struct {
   int32_t lazy_rows;        /* 1: rows materialised on first touch (Freebase-sized N_e) */
   int32_t lag;              /* 0: synchronous; 1: the entity-table update of step s is applied after step s+1 computed
                                its gradients (deterministic form of PAPER.md:515-534; relations stay synchronous) */
+  int32_t neg_deg_k;        /* slots j < neg_deg_k of each chunk are degree-based in-batch negatives,
+                               the rest uniform; 0 = all uniform */
 } orc_config;
 
 typedef void (*orc_triple_fn)(void* ctx, int64_t i, int64_t* h, int64_t* r, int64_t* t);
