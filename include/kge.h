@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define KGE_ABI_VERSION 1
+#define KGE_ABI_VERSION 2  /* 2: kge_config::neg_deg_k */
 
 typedef struct kge_handle kge_handle; /* opaque, library-owned */
 
@@ -96,6 +96,10 @@ typedef struct {
   void* (*dev_alloc)(size_t bytes, void* ctx); /* optional device allocator */
   void (*dev_free)(void* ptr, void* ctx);
   void* alloc_ctx;
+  int32_t neg_deg_k;       /* slots j < neg_deg_k of every chunk are degree-based in-batch negatives (PAPER.md:437-448
+                              [3.3]: the tail (tail corruption) / head (head corruption) of a uniformly drawn triplet
+                              of the mini-batch, Philox stream DEG = 4); the rest uniform. 0 (default) = all uniform;
+                              must be <= neg_k */
 } kge_config;
 
 /* Fill *cfg with defaults (ABI version, TransE-L2, d=400, B=1024, g=256, k=256, gamma=12, lr=0.1, eps=1e-10,

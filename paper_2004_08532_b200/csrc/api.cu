@@ -117,6 +117,7 @@ static int validate(const kge_config* c) {
   if (c->corrupt < 0 || c->corrupt > 2) { set_error("bad corrupt"); return KGE_EINVAL; }
   if (c->neg_precision < 0 || c->neg_precision > 1) { set_error("bad neg_precision"); return KGE_EINVAL; }
   if (c->lag != 0 && c->lag != 1) { set_error("lag must be 0 or 1"); return KGE_EINVAL; }
+  if (c->neg_deg_k < 0 || c->neg_deg_k > c->neg_k) { set_error("neg_deg_k must be in [0, neg_k]"); return KGE_EINVAL; }
   if (c->lag == 1 && (c->world_size > 1 || c->model == KGE_TRANSR)) {
     set_error("lag = 1 is implemented for one rank and the non-TransR models");
     return KGE_EUNSUPPORTED;
@@ -191,6 +192,7 @@ static SampleParams sample_params(const kge_handle* h, bool given, int gi = 0) {
   p.k1 = h->k1;
   p.corrupt = h->cfg.corrupt;
   p.cg_base = (uint32_t)(h->cfg.rank * h->dims.C);
+  p.kd = h->cfg.neg_deg_k;
   return p;
 }
 
@@ -223,6 +225,7 @@ void kge_config_default(kge_config* c) {
   c->neg_precision = KGE_PREC_TF32;
   c->rotate_variant = 0;
   c->lag = 0;
+  c->neg_deg_k = 0;
   c->world_size = 1;
   c->rank = 0;
 }

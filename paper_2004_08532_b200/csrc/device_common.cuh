@@ -8,7 +8,7 @@ namespace kge {
 // ---- Philox4x32-10 (reading c.1: the counter RNG the north_star names; Random123 constants) ----
 constexpr uint32_t kPhiloxM0 = 0xD2511F53u, kPhiloxM1 = 0xCD9E8D57u;
 constexpr uint32_t kPhiloxW0 = 0x9E3779B9u, kPhiloxW1 = 0xBB67AE85u;
-constexpr uint32_t kTagNeg = 1, kTagPerm = 2, kTagInit = 3;
+constexpr uint32_t kTagNeg = 1, kTagPerm = 2, kTagInit = 3, kTagDeg = 4;
 
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
@@ -64,6 +64,14 @@ __device__ __forceinline__ uint32_t neg_entity(uint32_t k0, uint32_t k1, uint64_
   const uint4 o = philox4x32_10(make_uint4(j >> 1, cg, step, kTagNeg), k0, k1);
   const uint64_t u = (j & 1u) ? (((uint64_t)o.w << 32) | o.z) : (((uint64_t)o.y << 32) | o.x);
   return (uint32_t)__umul64hi(u, n_ent);
+}
+
+// degree-based in-batch negatives: batch position of slot j < k_deg, t = mulhi64(u, B)
+__device__ __forceinline__ uint32_t deg_position(uint32_t k0, uint32_t k1, uint32_t B, uint32_t step, uint32_t cg,
+                                                 uint32_t j) {
+  const uint4 o = philox4x32_10(make_uint4(j >> 1, cg, step, kTagDeg), k0, k1);
+  const uint64_t u = (j & 1u) ? (((uint64_t)o.w << 32) | o.z) : (((uint64_t)o.y << 32) | o.x);
+  return (uint32_t)__umul64hi(u, (uint64_t)B);
 }
 
 // c.4 schedule: 0 = tail, 1 = head

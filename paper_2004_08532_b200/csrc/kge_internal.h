@@ -81,6 +81,7 @@ struct SampleParams {
   uint32_t k0, k1;
   int32_t corrupt;
   uint32_t cg_base;  // rank * C
+  int32_t kd;        // degree-based in-batch slots per chunk (kge_config::neg_deg_k)
 };
 
 struct StepBuffers {

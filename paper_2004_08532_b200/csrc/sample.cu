@@ -105,11 +105,18 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
       keys[i] = ((unsigned long long)(uint32_t)rv << 32) | (uint32_t)i;
     }
   }
+  __syncthreads();  // the batch's heads / tails (slot.ph / pt) are complete for the in-batch negatives
   if (ent_side) {
     const int nneg = p.C * p.k;
     for (int q = tid; q < nneg; q += blockDim.x) {
       const int c = q / p.k, j = q - c * p.k;
-      const uint32_t id = neg_entity(p.k0, p.k1, (uint64_t)p.n_entities, (uint32_t)s, p.cg_base + c, (uint32_t)j);
+      uint32_t id;
+      if (j < p.kd) {  // degree-based in-batch slot: the drawn triplet's tail (tail mode) / head (head mode)
+        const uint32_t t = deg_position(p.k0, p.k1, (uint32_t)p.B, (uint32_t)s, p.cg_base + c, (uint32_t)j);
+        id = (uint32_t)(corrupt_mode(p.corrupt, (uint32_t)s, p.cg_base + c) == 0 ? slot.pt[t] : slot.ph[t]);
+      } else {
+        id = neg_entity(p.k0, p.k1, (uint64_t)p.n_entities, (uint32_t)s, p.cg_base + c, (uint32_t)j);
+      }
       slot.neg[q] = (int32_t)id;
       keys[2 * p.B + q] = ((unsigned long long)id << 32) | (uint32_t)(2 * p.B + q);
     }

@@ -326,3 +326,28 @@ def test_transr_tf32_projections(graph, shape, steps):
     gpu, orc = _pair("transr", gr.n_entities, gr.n_relations, trip, d, B, g, k, lr=0.05, precision="tf32")
     lg, lo = gpu.train_step(steps), orc.train(steps)
     assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 2e-3, (lg, lo)
+
+
+@pytest.mark.parametrize("kd", [16, 64])
+def test_degree_negatives_bit_exact_and_training(kd):
+    # degree-based in-batch negatives: sampled ids bit-exact vs the oracle, FP32 training parity
+    gr = synth.graph("tiny")
+    trip = gr.triples()
+    cfg = kge.Config(model="distmult", n_entities=gr.n_entities, n_relations=gr.n_relations, dim=32, batch_size=256,
+                     chunk_size=64, neg_k=64, gamma=12.0, lr=0.1, seed=1, neg_precision="fp32", neg_deg_k=kd)
+    gpu = kge.init(cfg, *trip)
+    orc = O.Trainer("distmult", gr.n_entities, gr.n_relations, 32, 256, 64, 64, gamma=12.0, lr=0.1, seed=1,
+                    triples=trip, neg_deg_k=kd)
+    for step in [0, 1, 38, 39, 1000]:
+        s = gpu.sample(step)
+        pos, neg, mode = orc.sample(step)
+        assert np.array_equal(s["pos"], pos) and np.array_equal(s["neg"], neg) and np.array_equal(s["mode"], mode)
+    lg, lo = gpu.train_step(20), orc.train(20)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5
+    # the caller-batch path draws its in-batch negatives from the caller's batch
+    smp = gpu.sample(gpu.step)
+    p = smp["pos"]
+    gpu.train_batch(trip[0][p], trip[1][p], trip[2][p])
+    orc.train(1)
+    ids = np.arange(gr.n_entities)
+    assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 1e-4
