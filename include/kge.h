@@ -100,6 +100,9 @@ typedef struct {
                               [3.3]: the tail (tail corruption) / head (head corruption) of a uniformly drawn triplet
                               of the mini-batch, Philox stream DEG = 4); the rest uniform. 0 (default) = all uniform;
                               must be <= neg_k */
+  int32_t neg_local;       /* 1: with world_size > 1 the uniform negatives of rank w come from its own entity shard
+                              {e : e mod P == w} (PAPER.md:451-456 [3.3] local negatives: no remote rows for them);
+                              the draw of reading c.3 mapped to e = w + P * floor(u * n_w / 2^64). Default 0 */
 } kge_config;
 
 /* Fill *cfg with defaults (ABI version, TransE-L2, d=400, B=1024, g=256, k=256, gamma=12, lr=0.1, eps=1e-10,

@@ -31,7 +31,7 @@ class Config(ctypes.Structure):
                 ("gamma", ctypes.c_float), ("lr", ctypes.c_float), ("eps", ctypes.c_float),
                 ("init_bound", ctypes.c_float), ("seed", ctypes.c_uint64), ("corrupt", ctypes.c_int32),
                 ("rotate_variant", ctypes.c_int32), ("world_size", ctypes.c_int32), ("lazy_rows", ctypes.c_int32),
-                ("lag", ctypes.c_int32), ("neg_deg_k", ctypes.c_int32)]
+                ("lag", ctypes.c_int32), ("neg_deg_k", ctypes.c_int32), ("neg_local", ctypes.c_int32)]
 
 
 TRIPLE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, _i64p, _i64p, _i64p)
@@ -218,13 +218,13 @@ class Trainer:
 
     def __init__(self, model, n_entities, n_relations, dim, batch, chunk, neg_k, gamma=12.0, lr=0.1, eps=1e-10,
                  init_bound=0.0, seed=1, corrupt=ALTERNATE, rotate_variant=0, world_size=1, precision=0,
-                 triples=None, graph=None, lazy_rows=False, lag=0, neg_deg_k=0):
+                 triples=None, graph=None, lazy_rows=False, lag=0, neg_deg_k=0, neg_local=0):
         if isinstance(model, str):
             model = MODEL_IDS[model]
         self.model = model
         self.cfg = Config(model, precision, n_entities, n_relations, dim, batch, chunk, neg_k, gamma, lr, eps,
                           init_bound, seed, corrupt, rotate_variant, world_size, int(lazy_rows), int(lag),
-                          int(neg_deg_k))
+                          int(neg_deg_k), int(neg_local))
         self._keep = []
         if triples is not None:
             h, r, t = [np.ascontiguousarray(a, dtype=np.int64) for a in triples]

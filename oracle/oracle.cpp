@@ -480,6 +480,11 @@ struct Base {
             int64_t hh, rr, tt;
             triple(pos[deg_pos(cfg.seed, B, (uint32_t)s, cg, (uint32_t)j)], hh, rr, tt);
             neg[c * k + j] = md == ORC_TAIL ? tt : hh;
+          } else if (cfg.neg_local && cfg.world_size > 1) {
+            // local-shard negatives (PAPER.md:451-456 [3.3]: "sample entities from the local partition"; reading
+            // c.3''): the c.3 draw mapped onto rank w's shard e = w + P * m, m uniform in [0, n_w)
+            const int64_t P = cfg.world_size, n_w = (cfg.n_entities - rank + P - 1) / P;
+            neg[c * k + j] = rank + P * neg_id(cfg.seed, n_w, (uint32_t)s, cg, (uint32_t)j);
           } else {
             neg[c * k + j] = neg_id(cfg.seed, cfg.n_entities, (uint32_t)s, cg, (uint32_t)j);
           }

@@ -48,6 +48,8 @@ typedef struct {
                                its gradients (deterministic form of PAPER.md:515-534; relations stay synchronous) */
   int32_t neg_deg_k;        /* slots j < neg_deg_k of each chunk are degree-based in-batch negatives,
                                the rest uniform; 0 = all uniform */
+  int32_t neg_local;        /* 1: uniform negatives of rank w are drawn from its own entity shard {e : e mod P == w}
+                               ("local" negatives; no remote rows for them) */
 } orc_config;
 
 typedef void (*orc_triple_fn)(void* ctx, int64_t i, int64_t* h, int64_t* r, int64_t* t);

@@ -193,6 +193,8 @@ static SampleParams sample_params(const kge_handle* h, bool given, int gi = 0) {
   p.corrupt = h->cfg.corrupt;
   p.cg_base = (uint32_t)(h->cfg.rank * h->dims.C);
   p.kd = h->cfg.neg_deg_k;
+  p.local_P = h->cfg.neg_local && h->P > 1 ? h->P : 0;
+  p.local_rank = h->rank;
   return p;
 }
 
@@ -226,6 +228,7 @@ void kge_config_default(kge_config* c) {
   c->rotate_variant = 0;
   c->lag = 0;
   c->neg_deg_k = 0;
+  c->neg_local = 0;
   c->world_size = 1;
   c->rank = 0;
 }

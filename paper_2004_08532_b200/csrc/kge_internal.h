@@ -82,6 +82,7 @@ struct SampleParams {
   int32_t corrupt;
   uint32_t cg_base;  // rank * C
   int32_t kd;        // degree-based in-batch slots per chunk (kge_config::neg_deg_k)
+  int32_t local_P, local_rank;  // local-shard negatives (kge_config::neg_local): P > 1 and this rank, else local_P = 0
 };
 
 struct StepBuffers {

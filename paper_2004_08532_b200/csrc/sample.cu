@@ -114,6 +114,10 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
       if (j < p.kd) {  // degree-based in-batch slot: the drawn triplet's tail (tail mode) / head (head mode)
         const uint32_t t = deg_position(p.k0, p.k1, (uint32_t)p.B, (uint32_t)s, p.cg_base + c, (uint32_t)j);
         id = (uint32_t)(corrupt_mode(p.corrupt, (uint32_t)s, p.cg_base + c) == 0 ? slot.pt[t] : slot.ph[t]);
+      } else if (p.local_P > 1) {  // local-shard negatives: rank w's shard {w + P m}
+        const uint64_t n_w = (uint64_t)((p.n_entities - p.local_rank + p.local_P - 1) / p.local_P);
+        id = (uint32_t)p.local_rank +
+             (uint32_t)p.local_P * neg_entity(p.k0, p.k1, n_w, (uint32_t)s, p.cg_base + c, (uint32_t)j);
       } else {
         id = neg_entity(p.k0, p.k1, (uint64_t)p.n_entities, (uint32_t)s, p.cg_base + c, (uint32_t)j);
       }

@@ -12,15 +12,16 @@ from paper_2004_08532_b200 import kge
 pytestmark = pytest.mark.gpu
 
 
-def _run(model, P, shape, steps, precision="fp32", graph="tiny", variant=0):
+def _run(model, P, shape, steps, precision="fp32", graph="tiny", variant=0, neg_local=0, neg_deg_k=0):
     B, g, k, d = shape
     gr = synth.graph(graph)
     trip = gr.triples()
     cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=d, batch_size=B,
-                     chunk_size=g, neg_k=k, neg_precision=precision, rotate_variant=variant)
+                     chunk_size=g, neg_k=k, neg_precision=precision, rotate_variant=variant, neg_local=neg_local,
+                     neg_deg_k=neg_deg_k)
     hs = kge.init_local_group(cfg, P, *trip)
     orc = O.Trainer(model, gr.n_entities, gr.n_relations, d, B, g, k, world_size=P, triples=trip,
-                    rotate_variant=variant)
+                    rotate_variant=variant, neg_local=neg_local, neg_deg_k=neg_deg_k)
     # integer half per rank: bit-exact
     for w in range(P):
         s = hs[w].sample(3)
@@ -76,3 +77,15 @@ def test_dist_requires_connect_and_owner_rows():
     with pytest.raises(kge.KgeError):
         h.get_rows(0, [0])  # entity 0 is owned by rank 0
     assert h.get_rows(0, [1]).shape == (1, 32)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_dist_local_and_degree_negatives(P):
+    # local-shard negatives + degree-based in-batch slots on the P-rank path
+    gr, hs, orc, lg, lo = _run("transe_l2", P, (128, 32, 32, 32), 20, neg_local=1, neg_deg_k=8)
+    for w in range(P):
+        assert np.all(hs[w].sample(4)["neg"].reshape(4, 32)[:, 8:] % P == w)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5
+    ids = np.arange(gr.n_entities)
+    got = np.stack([hs[e % P].get_rows(0, [e])[0] for e in ids])
+    assert np.abs(got - orc.get_rows(0, ids)).max() <= 1e-4

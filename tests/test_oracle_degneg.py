@@ -55,3 +55,23 @@ def test_in_batch_frequency_proportional_to_batch_degree():
 def test_training_with_degree_negatives_is_finite():
     _, _, t = _tr(32)
     assert np.all(np.isfinite(t.train(5)))
+
+
+def test_local_shard_negatives():
+    # local negatives: rank w draws uniform negatives from {e : e mod P == w} only; P = 1 unchanged
+    gr = synth.graph("tiny")
+    trip = gr.triples()
+    mk = lambda P, loc: O.Trainer("transe_l2", gr.n_entities, gr.n_relations, 16, 64, 16, 16, seed=7, world_size=P,
+                                  triples=trip, neg_local=loc)
+    a, b = mk(1, 1), mk(1, 0)
+    assert np.array_equal(a.sample(5)[1], b.sample(5)[1])
+    for P in (2, 4):
+        t = mk(P, 1)
+        for w in range(P):
+            counts = np.zeros(gr.n_entities)
+            for s in range(200):
+                _, neg, _ = t.sample(s, w)
+                assert np.all(neg % P == w), (P, w)
+                np.add.at(counts, neg, 1)
+            shard = counts[w::P]
+            assert (shard > 0).mean() > 0.9  # covers the shard (12,800 draws over ~1000 / P ids)
