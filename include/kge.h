@@ -146,6 +146,15 @@ int kge_train_batch_async(kge_handle* h, const int64_t* heads, const int64_t* re
  * float[n]. Synchronous. KGE_ERANGE on an out-of-range id. */
 int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, float* out);
 
+/* Link-prediction ranks (PAPER.md:652-665 [5.3] evaluation protocol), raw setting: for each test
+ * triple the true tail (corrupt_head = 0) or head (corrupt_head = 1) is scored against every entity of the graph with
+ * the current tables; ranks_out[i] = 1 + #{e : f(candidate e) > f(true)} (exact ties are not counted). Candidates and
+ * the true triple are scored by the same arithmetic (o = combine(h, r) or combine'(r, t), then the pair score).
+ * hs/rs/ts: host int64[n]; ranks_out: host int64[n]. Synchronous. KGE_ERANGE on an out-of-range id;
+ * KGE_EUNSUPPORTED for TransR or world_size > 1. MR / MRR / Hit@k follow from the ranks (kge.link_metrics). */
+int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, int32_t corrupt_head,
+             int64_t* ranks_out);
+
 /* Read / overwrite rows of a table: 0 entity [N_e x d], 1 relation [N_r x d_r] (d_r = d, or d/2 for RotatE),
  * 2 TransR projection [N_r x d*d], 3 entity Adagrad state [N_e x 1], 4 relation state, 5 projection state.
  * ids: host int64[n]; out/in: host float[n x width]. Synchronous. KGE_EINVAL for a table the model lacks. */

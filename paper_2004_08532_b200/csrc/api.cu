@@ -1036,6 +1036,40 @@ int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t
   return KGE_OK;
 }
 
+int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, int32_t corrupt_head,
+             int64_t* ranks_out) {
+  if (!h || (n > 0 && (!hs || !rs || !ts || !ranks_out))) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (h->dims.model == KGE_TRANSR || h->P > 1) {
+    set_error("kge_rank: TransR and world_size > 1 are not supported");
+    return KGE_EUNSUPPORTED;
+  }
+  if (n == 0) return KGE_OK;
+  std::vector<int32_t> ids((size_t)3 * n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (hs[i] < 0 || hs[i] >= h->dims.n_entities || ts[i] < 0 || ts[i] >= h->dims.n_entities || rs[i] < 0 ||
+        rs[i] >= h->dims.n_relations) {
+      set_error("triple id out of range");
+      return KGE_ERANGE;
+    }
+    ids[i] = (int32_t)hs[i];
+    ids[n + i] = (int32_t)rs[i];
+    ids[2 * n + i] = (int32_t)ts[i];
+  }
+  const int rj = join_updates(h);
+  if (rj != KGE_OK) return rj;
+  int32_t* d_ids = nullptr;
+  int64_t* d_out = nullptr;
+  CK(cudaMallocAsync((void**)&d_ids, (size_t)3 * n * 4, h->stream));
+  CK(cudaMallocAsync((void**)&d_out, (size_t)n * 8, h->stream));
+  CK(cudaMemcpyAsync(d_ids, ids.data(), (size_t)3 * n * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(launch_rank(h, d_ids, d_ids + n, d_ids + 2 * n, n, corrupt_head ? 1 : 0, d_out));
+  CK(cudaMemcpyAsync(ranks_out, d_out, (size_t)n * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaFreeAsync(d_ids, h->stream));
+  CK(cudaFreeAsync(d_out, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return KGE_OK;
+}
+
 int64_t kge_step(const kge_handle* h) { return h ? h->step : -1; }
 
 int kge_read_losses(kge_handle* h, int64_t first_step, int64_t n, float* out) {

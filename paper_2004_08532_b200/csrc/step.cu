@@ -1442,6 +1442,90 @@ __global__ void __launch_bounds__(256) k_score(ScoreArgs a) {
 cudaError_t launch_transr_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n,
                                 float* out);  // transr.cu
 
+// ------------------------------------------------------------------------------------------------
+// k_rank: link-prediction rank of the true entity among all entities (raw setting), one CTA per test triple
+// ------------------------------------------------------------------------------------------------
+struct RankArgs {
+  Dims dm;
+  EntRows ent;
+  const float* rel;
+  const int32_t* hs;
+  const int32_t* rs;
+  const int32_t* ts;
+  int32_t head;      // 0: candidates replace the tail, 1: the head
+  int64_t* ranks;
+};
+
+// pair statistic of o (shared memory) and an entity row x, reduced over the warp (families of step.cu)
+__device__ __forceinline__ float pair_stat_row(int fam, const float* o, const float* __restrict__ x, int d, int lane) {
+  float st = 0.f;
+  if (fam == FAM_CMOD) {
+    const int hlf = d >> 1;
+    for (int c = lane; c < hlf; c += 32) {
+      const float ur = o[c] - x[c], ui = o[c + hlf] - x[c + hlf];
+      st += sqrtf(ur * ur + ui * ui);
+    }
+  } else {
+    for (int v = lane; v < (d >> 2); v += 32) {
+      const float4 ov = reinterpret_cast<const float4*>(o)[v];
+      const float4 xv = ld4(x, v);
+      if (fam == FAM_DOT) {
+        st += ov.x * xv.x + ov.y * xv.y + ov.z * xv.z + ov.w * xv.w;
+      } else if (fam == FAM_L1) {
+        st += fabsf(ov.x - xv.x) + fabsf(ov.y - xv.y) + fabsf(ov.z - xv.z) + fabsf(ov.w - xv.w);
+      } else {
+        const float a = ov.x - xv.x, b = ov.y - xv.y, c = ov.z - xv.z, e = ov.w - xv.w;
+        st += a * a + b * b + c * c + e * e;
+      }
+    }
+  }
+  return warp_sum(st);
+}
+
+__global__ void __launch_bounds__(256) k_rank(RankArgs a) {
+  extern __shared__ __align__(16) float osm[];  // o = combine(h, r) (tail) | combine'(r, t) (head), d floats
+  __shared__ float s_true;
+  __shared__ int s_cnt[8];
+  const Dims& dm = a.dm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.x;
+  const float* h = a.ent.row(a.hs[i]);
+  const float* t = a.ent.row(a.ts[i]);
+  const float* r = a.rel + (int64_t)a.rs[i] * dm.drel;
+  const int mode = a.head ? 1 : 0;
+  if (warp == 0) {
+    float st, on;
+    combine_row(dm.model, mode, h, r, t, osm, dm.d, lane, mode == 0 ? t : h, dm.family, st, on);
+  }
+  __syncthreads();
+  if (warp == 0) {  // the true entity through the same arithmetic as every candidate
+    const float st = pair_stat_row(dm.family, osm, mode == 0 ? t : h, dm.d, lane);
+    if (lane == 0) s_true = pair_score_from(dm.family, st, dm.gamma);
+  }
+  __syncthreads();
+  const float ft = s_true;
+  int cnt = 0;
+  for (int64_t e = warp; e < dm.n_entities; e += 8) {
+    const float f = pair_score_from(dm.family, pair_stat_row(dm.family, osm, a.ent.row(e), dm.d, lane), dm.gamma);
+    cnt += f > ft ? 1 : 0;
+  }
+  if (lane == 0) s_cnt[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t c = 0;
+    for (int w = 0; w < 8; ++w) c += s_cnt[w];
+    a.ranks[i] = 1 + c;
+  }
+}
+
+cudaError_t launch_rank(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, int head,
+                        int64_t* ranks) {
+  RankArgs ra{h->dims, h->rows, h->rel, hs, rs, ts, head, ranks};
+  k_rank<<<(unsigned)n, 256, (size_t)h->dims.dp * 4, h->stream>>>(ra);
+  ++h->launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, float* out) {
   if (h->dims.model == KGE_TRANSR) return launch_transr_score(h, hs, rs, ts, n, out);
   // scratch: reuse the X buffer in chunks of its capacity

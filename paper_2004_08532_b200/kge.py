@@ -77,6 +77,7 @@ def lib():
         L.kge_train_batch_async.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                             ctypes.c_void_p]
         L.kge_score.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, _fp]
+        L.kge_rank.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int32, _i64p]
         L.kge_get_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_set_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_table_width.argtypes = [ctypes.c_void_p, ctypes.c_int32]
@@ -258,6 +259,15 @@ class Handle:
         if rc:
             _check(rc)
 
+    # kge_rank
+    def rank(self, hs, rs, ts, head=False):
+        """Raw link-prediction ranks of the true tail (head=True: head) among all entities."""
+        hs, rs, ts = _i64(hs), _i64(rs), _i64(ts)
+        out = np.zeros(len(hs), np.int64)
+        _check(lib().kge_rank(self._h, _ptr(hs, ctypes.c_int64), _ptr(rs, ctypes.c_int64), _ptr(ts, ctypes.c_int64),
+                              len(hs), 1 if head else 0, _ptr(out, ctypes.c_int64)))
+        return out
+
     # kge_score
     def score(self, hs, rs, ts):
         hs, rs, ts = _i64(hs), _i64(rs), _i64(ts)
@@ -405,3 +415,10 @@ def init_local_group(cfg: Config, world_size: int, heads, rels, tails):
     arr = (ctypes.c_void_p * world_size)(*[h._h for h in hs])
     _check(lib().kge_connect_local(arr, world_size))
     return hs
+
+
+def link_metrics(ranks):
+    """MR, MRR and Hit@1/3/10 of link-prediction ranks (PAPER.md:652-665 [5.3])."""
+    r = np.asarray(ranks, dtype=np.float64)
+    return {"MR": float(r.mean()), "MRR": float((1.0 / r).mean()), "Hit@1": float((r <= 1).mean()),
+            "Hit@3": float((r <= 3).mean()), "Hit@10": float((r <= 10).mean())}
