@@ -146,13 +146,21 @@ int kge_train_batch_async(kge_handle* h, const int64_t* heads, const int64_t* re
  * float[n]. Synchronous. KGE_ERANGE on an out-of-range id. */
 int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, float* out);
 
-/* Link-prediction ranks (PAPER.md:652-665 [5.3] evaluation protocol), raw setting: for each test
- * triple the true tail (corrupt_head = 0) or head (corrupt_head = 1) is scored against every entity of the graph with
- * the current tables; ranks_out[i] = 1 + #{e : f(candidate e) > f(true)} (exact ties are not counted). Candidates and
- * the true triple are scored by the same arithmetic (o = combine(h, r) or combine'(r, t), then the pair score).
- * hs/rs/ts: host int64[n]; ranks_out: host int64[n]. Synchronous. KGE_ERANGE on an out-of-range id;
+/* Link-prediction ranks (PAPER.md:652-665 [5.3] evaluation methodology). For each test triple i
+ * the true tail (corrupt_head = 0) or head (corrupt_head = 1) is scored against a candidate set C_i with the current
+ * tables, candidates and the true triple through the same arithmetic (o = combine(h, r) or combine'(r, t), then the
+ * pair score of Table 1). rank_i = 1 + #{e in C_i \ F_i, e != true entity : f(e) >= f(true)} -- ties rank the
+ * positive last (reading c.15).
+ *   cand_off == NULL: C_i = every entity (first protocol; raw if filt_off == NULL).
+ *   cand_off/cand_ids: C_i = cand_ids[cand_off[i] .. cand_off[i+1]) (second protocol: the caller's 1000 uniform +
+ *     1000 degree-proportional draws; duplicates count once per occurrence, the true entity is skipped).
+ *   filt_off/filt_ids: F_i = filt_ids[filt_off[i] .. filt_off[i+1]) (first protocol, filtered: the corrupted
+ *     entities that form a known triple; duplicates removed here). Only with cand_off == NULL, else KGE_EINVAL.
+ * Offsets: host int64[n+1] from 0, non-decreasing (KGE_EINVAL otherwise); ids: host int64, each in [0, N_e)
+ * (KGE_ERANGE otherwise). hs/rs/ts: host int64[n]; ranks_out: host int64[n], owned by the caller. Synchronous.
  * KGE_EUNSUPPORTED for TransR or world_size > 1. MR / MRR / Hit@k follow from the ranks (kge.link_metrics). */
 int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, int32_t corrupt_head,
+             const int64_t* cand_off, const int64_t* cand_ids, const int64_t* filt_off, const int64_t* filt_ids,
              int64_t* ranks_out);
 
 /* Read / overwrite rows of a table: 0 entity [N_e x d], 1 relation [N_r x d_r] (d_r = d, or d/2 for RotatE),

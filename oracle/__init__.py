@@ -304,3 +304,37 @@ class Trainer:
     @property
     def step(self):
         return lib().orc_next_step(self.h)
+
+
+def link_rank(trainer, hs, rs, ts, head=False, candidates=None, known=None):
+    """Link-prediction ranks, PAPER.md:652-665 [5.3] step by step: for each positive triple build S_i = the positive
+    plus its negative triples (every corruption of the tail -- head=True: the head -- or, second protocol, the given
+    candidate entities; with `known` (a set of (h, r, t) tuples), first protocol filtered: corruptions that already
+    exist in the dataset are removed), score S_i with Table 1, order it by non-increasing score with the positive
+    LAST among equal scores (reading c.15), rank_i = the positive's 1-based position. candidates: list of entity-id
+    arrays, one per query. The corruption equal to the positive itself is not a negative triple."""
+    out = []
+    n_e = trainer.cfg.n_entities
+    for i in range(len(hs)):
+        h, r, t = int(hs[i]), int(rs[i]), int(ts[i])
+        true_e = h if head else t
+        ents = range(n_e) if candidates is None else [int(e) for e in candidates[i]]
+        neg = [(e, r, t) if head else (h, r, e) for e in ents if e != true_e]
+        if known is not None:
+            neg = [x for x in neg if x not in known]
+        trip = [(h, r, t)] + neg
+        sc = trainer.score_triples([x[0] for x in trip], [x[1] for x in trip], [x[2] for x in trip])
+        # non-increasing score; among equals the positive (index 0) goes last
+        order = sorted(range(len(trip)), key=lambda j: (-sc[j], j == 0))
+        out.append(order.index(0) + 1)
+    return np.array(out, np.int64)
+
+
+def link_metrics(ranks):
+    """Hit@k, MR and MRR, PAPER.md:660-664 [5.3] formulas."""
+    Q = len(ranks)
+    if Q == 0:
+        raise ValueError("metrics of an empty rank list")
+    return {"Hit@1": sum(1 for x in ranks if x <= 1) / Q, "Hit@3": sum(1 for x in ranks if x <= 3) / Q,
+            "Hit@10": sum(1 for x in ranks if x <= 10) / Q, "MR": sum(int(x) for x in ranks) / Q,
+            "MRR": sum(1.0 / int(x) for x in ranks) / Q}

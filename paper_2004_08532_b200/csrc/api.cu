@@ -1036,12 +1036,39 @@ int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t
   return KGE_OK;
 }
 
+// checks a CSR list (off[n+1] from 0, non-decreasing; ids in [0, n_entities)) and packs its ids as int32
+static int pack_list(const int64_t* off, const int64_t* ids, int64_t n, int64_t n_ent, bool dedup,
+                     std::vector<int64_t>& o, std::vector<int32_t>& v) {
+  if (off[0] != 0) { set_error("list offsets must start at 0"); return KGE_EINVAL; }
+  o.assign(1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (off[i + 1] < off[i]) { set_error("list offsets must be non-decreasing"); return KGE_EINVAL; }
+    if (off[i + 1] > off[i] && !ids) { set_error("NULL list ids"); return KGE_EINVAL; }
+    const size_t b = v.size();
+    for (int64_t j = off[i]; j < off[i + 1]; ++j) {
+      if (ids[j] < 0 || ids[j] >= n_ent) { set_error("list entity id out of range"); return KGE_ERANGE; }
+      v.push_back((int32_t)ids[j]);
+    }
+    if (dedup) {
+      std::sort(v.begin() + b, v.end());
+      v.erase(std::unique(v.begin() + b, v.end()), v.end());
+    }
+    o.push_back((int64_t)v.size());
+  }
+  return KGE_OK;
+}
+
 int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, int32_t corrupt_head,
+             const int64_t* cand_off, const int64_t* cand_ids, const int64_t* filt_off, const int64_t* filt_ids,
              int64_t* ranks_out) {
   if (!h || (n > 0 && (!hs || !rs || !ts || !ranks_out))) { set_error("NULL argument"); return KGE_EINVAL; }
   if (h->dims.model == KGE_TRANSR || h->P > 1) {
     set_error("kge_rank: TransR and world_size > 1 are not supported");
     return KGE_EUNSUPPORTED;
+  }
+  if (cand_off && filt_off) {
+    set_error("kge_rank: the filter applies to the all-entity protocol only (cand_off must be NULL)");
+    return KGE_EINVAL;
   }
   if (n == 0) return KGE_OK;
   std::vector<int32_t> ids((size_t)3 * n);
@@ -1055,17 +1082,38 @@ int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t*
     ids[n + i] = (int32_t)rs[i];
     ids[2 * n + i] = (int32_t)ts[i];
   }
+  std::vector<int64_t> co, fo;
+  std::vector<int32_t> cv, fv;
+  if (cand_off) {
+    const int rc = pack_list(cand_off, cand_ids, n, h->dims.n_entities, false, co, cv);
+    if (rc != KGE_OK) return rc;
+  }
+  if (filt_off) {
+    const int rc = pack_list(filt_off, filt_ids, n, h->dims.n_entities, true, fo, fv);
+    if (rc != KGE_OK) return rc;
+  }
   const int rj = join_updates(h);
   if (rj != KGE_OK) return rj;
-  int32_t* d_ids = nullptr;
-  int64_t* d_out = nullptr;
-  CK(cudaMallocAsync((void**)&d_ids, (size_t)3 * n * 4, h->stream));
-  CK(cudaMallocAsync((void**)&d_out, (size_t)n * 8, h->stream));
-  CK(cudaMemcpyAsync(d_ids, ids.data(), (size_t)3 * n * 4, cudaMemcpyHostToDevice, h->stream));
-  CK(launch_rank(h, d_ids, d_ids + n, d_ids + 2 * n, n, corrupt_head ? 1 : 0, d_out));
+  // one device block: ids | offsets (8-byte aligned) | list ids | ranks
+  const size_t b_ids = (size_t)3 * n * 4, b_co = co.size() * 8, b_fo = fo.size() * 8;
+  const size_t o_co = (b_ids + 7) & ~(size_t)7, o_fo = o_co + b_co, o_cv = o_fo + b_fo;
+  const size_t o_fv = o_cv + cv.size() * 4, o_out = (o_fv + fv.size() * 4 + 7) & ~(size_t)7;
+  char* d = nullptr;
+  CK(cudaMallocAsync((void**)&d, o_out + (size_t)n * 8, h->stream));
+  CK(cudaMemcpyAsync(d, ids.data(), b_ids, cudaMemcpyHostToDevice, h->stream));
+  if (b_co) CK(cudaMemcpyAsync(d + o_co, co.data(), b_co, cudaMemcpyHostToDevice, h->stream));
+  if (b_fo) CK(cudaMemcpyAsync(d + o_fo, fo.data(), b_fo, cudaMemcpyHostToDevice, h->stream));
+  if (!cv.empty()) CK(cudaMemcpyAsync(d + o_cv, cv.data(), cv.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  if (!fv.empty()) CK(cudaMemcpyAsync(d + o_fv, fv.data(), fv.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  const int32_t* di = reinterpret_cast<const int32_t*>(d);
+  int64_t* d_out = reinterpret_cast<int64_t*>(d + o_out);
+  CK(launch_rank(h, di, di + n, di + 2 * n, n, corrupt_head ? 1 : 0,
+                 cand_off ? reinterpret_cast<const int64_t*>(d + o_co) : nullptr,
+                 reinterpret_cast<const int32_t*>(d + o_cv),
+                 filt_off ? reinterpret_cast<const int64_t*>(d + o_fo) : nullptr,
+                 reinterpret_cast<const int32_t*>(d + o_fv), d_out));
   CK(cudaMemcpyAsync(ranks_out, d_out, (size_t)n * 8, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaFreeAsync(d_ids, h->stream));
-  CK(cudaFreeAsync(d_out, h->stream));
+  CK(cudaFreeAsync(d, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   return KGE_OK;
 }

@@ -322,6 +322,7 @@ cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, 
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step);
 cudaError_t launch_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, float* out);
 cudaError_t launch_rank(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, int head,
+                        const int64_t* cand_off, const int32_t* cand, const int64_t* filt_off, const int32_t* filt,
                         int64_t* ranks);
 cudaError_t launch_rows(kge_handle* h, float* tab, int32_t w, const int32_t* ids, int64_t n, float* buf, bool write);
 

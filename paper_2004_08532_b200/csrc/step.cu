@@ -1453,6 +1453,10 @@ struct RankArgs {
   const int32_t* rs;
   const int32_t* ts;
   int32_t head;      // 0: candidates replace the tail, 1: the head
+  const int64_t* cand_off;  // [n+1] or NULL (every entity is a candidate)
+  const int32_t* cand;
+  const int64_t* filt_off;  // [n+1] or NULL (raw); distinct ids, only with cand_off == NULL
+  const int32_t* filt;
   int64_t* ranks;
 };
 
@@ -1504,10 +1508,24 @@ __global__ void __launch_bounds__(256) k_rank(RankArgs a) {
   }
   __syncthreads();
   const float ft = s_true;
+  const int64_t tid = mode == 0 ? a.ts[i] : a.hs[i];
+  // pessimistic ties (reading c.15): every candidate other than the true entity scoring >= f(true) ranks above it
+  int64_t lo = 0, hi = dm.n_entities;
+  if (a.cand_off) lo = a.cand_off[i], hi = a.cand_off[i + 1];
   int cnt = 0;
-  for (int64_t e = warp; e < dm.n_entities; e += 8) {
+  for (int64_t j = lo + warp; j < hi; j += 8) {
+    const int64_t e = a.cand_off ? (int64_t)a.cand[j] : j;
+    if (e == tid) continue;
     const float f = pair_score_from(dm.family, pair_stat_row(dm.family, osm, a.ent.row(e), dm.d, lane), dm.gamma);
-    cnt += f > ft ? 1 : 0;
+    cnt += f >= ft ? 1 : 0;
+  }
+  if (a.filt_off) {  // filtered protocol: known triples among the candidates do not count
+    for (int64_t j = a.filt_off[i] + warp; j < a.filt_off[i + 1]; j += 8) {
+      const int64_t e = a.filt[j];
+      if (e == tid) continue;
+      const float f = pair_score_from(dm.family, pair_stat_row(dm.family, osm, a.ent.row(e), dm.d, lane), dm.gamma);
+      cnt -= f >= ft ? 1 : 0;
+    }
   }
   if (lane == 0) s_cnt[warp] = cnt;
   __syncthreads();
@@ -1519,8 +1537,9 @@ __global__ void __launch_bounds__(256) k_rank(RankArgs a) {
 }
 
 cudaError_t launch_rank(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, int head,
+                        const int64_t* cand_off, const int32_t* cand, const int64_t* filt_off, const int32_t* filt,
                         int64_t* ranks) {
-  RankArgs ra{h->dims, h->rows, h->rel, hs, rs, ts, head, ranks};
+  RankArgs ra{h->dims, h->rows, h->rel, hs, rs, ts, head, cand_off, cand, filt_off, filt, ranks};
   k_rank<<<(unsigned)n, 256, (size_t)h->dims.dp * 4, h->stream>>>(ra);
   ++h->launches;
   return cudaGetLastError();

@@ -77,7 +77,8 @@ def lib():
         L.kge_train_batch_async.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                             ctypes.c_void_p]
         L.kge_score.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, _fp]
-        L.kge_rank.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int32, _i64p]
+        L.kge_rank.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int32, _i64p, _i64p,
+                               _i64p, _i64p, _i64p]
         L.kge_get_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_set_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_table_width.argtypes = [ctypes.c_void_p, ctypes.c_int32]
@@ -260,12 +261,16 @@ class Handle:
             _check(rc)
 
     # kge_rank
-    def rank(self, hs, rs, ts, head=False):
-        """Raw link-prediction ranks of the true tail (head=True: head) among all entities."""
+    def rank(self, hs, rs, ts, head=False, candidates=None, filters=None):
+        """Link-prediction ranks (PAPER.md:652-665 [5.3]) of the true tail (head=True: head). candidates / filters:
+        None or a CSR pair (offsets[n+1], ids) -- see kge_rank in include/kge.h."""
         hs, rs, ts = _i64(hs), _i64(rs), _i64(ts)
         out = np.zeros(len(hs), np.int64)
-        _check(lib().kge_rank(self._h, _ptr(hs, ctypes.c_int64), _ptr(rs, ctypes.c_int64), _ptr(ts, ctypes.c_int64),
-                              len(hs), 1 if head else 0, _ptr(out, ctypes.c_int64)))
+        co, ci = (None, None) if candidates is None else (_i64(candidates[0]), _i64(candidates[1]))
+        fo, fi = (None, None) if filters is None else (_i64(filters[0]), _i64(filters[1]))
+        p = lambda a: None if a is None else _ptr(a, ctypes.c_int64)
+        _check(lib().kge_rank(self._h, p(hs), p(rs), p(ts), len(hs), 1 if head else 0, p(co), p(ci), p(fo), p(fi),
+                              p(out)))
         return out
 
     # kge_score
@@ -422,3 +427,33 @@ def link_metrics(ranks):
     r = np.asarray(ranks, dtype=np.float64)
     return {"MR": float(r.mean()), "MRR": float((1.0 / r).mean()), "Hit@1": float((r <= 1).mean()),
             "Hit@3": float((r <= 3).mean()), "Hit@10": float((r <= 10).mean())}
+
+
+def filter_lists(known, hs, rs, ts, head=False):
+    """CSR filter lists of the first protocol (PAPER.md:654-655 [5.3]): for query i, the entities e such that the
+    corrupted triple (h_i, r_i, e) -- head=True: (e, r_i, t_i) -- is a known triple. known: (heads, rels, tails)."""
+    kh, kr, kt = (np.asarray(a, np.int64) for a in known)
+    fixed_a, fixed_b, free = (kr, kt, kh) if head else (kh, kr, kt)
+    qa, qb = (np.asarray(rs, np.int64), np.asarray(ts, np.int64)) if head else (np.asarray(hs, np.int64),
+                                                                                 np.asarray(rs, np.int64))
+    order = np.lexsort((free, fixed_b, fixed_a))
+    ka, kb, kf = fixed_a[order], fixed_b[order], free[order]
+    key = lambda a, b: a * (int(max(kb.max(initial=0), qb.max(initial=0))) + 1) + b
+    kk, qk = key(ka, kb), key(qa, qb)
+    lo, hi = np.searchsorted(kk, qk, "left"), np.searchsorted(kk, qk, "right")
+    off = np.zeros(len(qk) + 1, np.int64)
+    off[1:] = np.cumsum(hi - lo)
+    ids = np.concatenate([kf[a:b] for a, b in zip(lo, hi)]) if len(qk) else np.zeros(0, np.int64)
+    return off, ids
+
+
+def sampled_candidates(n_queries, degree, n_uniform=1000, n_degree=1000, seed=0):
+    """Candidate lists of the second protocol (PAPER.md:656-658 [5.3]): per query n_uniform entities drawn uniformly
+    and n_degree drawn proportionally to the entity degree, with replacement, unfiltered (reading c.15)."""
+    degree = np.asarray(degree, np.float64)
+    rng = np.random.default_rng(seed)
+    uni = rng.integers(0, len(degree), (n_queries, n_uniform))
+    cdf = np.cumsum(degree)
+    deg = np.searchsorted(cdf, rng.random((n_queries, n_degree)) * cdf[-1], "right")
+    ids = np.concatenate([uni, np.minimum(deg, len(degree) - 1)], axis=1).reshape(-1)
+    return np.arange(n_queries + 1, dtype=np.int64) * (n_uniform + n_degree), ids.astype(np.int64)

@@ -1,7 +1,8 @@
-"""Link-prediction ranks (PAPER.md:652-665 [5.3], raw setting) on the CUDA path vs ranks counted
-from the oracle's per-triple scores. A candidate whose oracle score lies within fp32 rounding of the true score may
-legitimately fall on either side; the allowed rank difference is the number of such near-ties. Both sides score the
-same (CUDA-trained) tables."""
+"""Link-prediction ranks (PAPER.md:652-665 [5.3]; reading c.15) on the CUDA path vs the oracle's
+explicit-sort ranking (oracle.link_rank) on the same tables: raw and filtered first protocol, sampled second protocol.
+A candidate whose oracle score lies within fp32 rounding of the positive's may legitimately fall on either side; the
+allowed rank difference is the number of such near-ties (0 in almost every query). Both sides score the same
+(CUDA-trained) tables."""
 import numpy as np
 import pytest
 
@@ -12,40 +13,67 @@ from paper_2004_08532_b200 import kge
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("model", ["transe_l2", "transe_l1", "distmult", "complex", "rotate"])
-@pytest.mark.parametrize("head", [False, True])
-def test_ranks_match_oracle(model, head):
+def _trained(model, dim=32, steps=30):
     gr = synth.graph("tiny")
     trip = gr.triples()
-    cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=32, batch_size=128,
+    cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=dim, batch_size=128,
                      chunk_size=32, neg_k=32, gamma=12.0, lr=0.1, seed=2, neg_precision="fp32")
     gpu = kge.init(cfg, *trip)
-    orc = O.Trainer(model, gr.n_entities, gr.n_relations, 32, 128, 32, 32, gamma=12.0, lr=0.1, seed=2, triples=trip)
-    gpu.train_step(30)
-    # ranks are a function of the tables: score the oracle on the CUDA path's trained fp32 rows
+    orc = O.Trainer(model, gr.n_entities, gr.n_relations, dim, 128, 32, 32, gamma=12.0, lr=0.1, seed=2, triples=trip)
+    gpu.train_step(steps)
     for table, n in ((0, gr.n_entities), (1, gr.n_relations)):
         ids = np.arange(n)
         orc.set_rows(table, ids, gpu.get_rows(table, ids).astype(np.float64))
-    rng = np.random.default_rng(11)
-    test = rng.integers(0, gr.n_triples, 40)
+    return gr, trip, gpu, orc
+
+
+def _near_ties(orc, n_e, h, r, t, head, cands=None):
+    ents = np.arange(n_e) if cands is None else np.asarray(cands, np.int64)
+    f_true = orc.score_triples([h], [r], [t])[0]
+    if head:
+        f = orc.score_triples(ents, np.full_like(ents, r), np.full_like(ents, t))
+    else:
+        f = orc.score_triples(np.full_like(ents, h), np.full_like(ents, r), ents)
+    return int(np.sum(np.abs(f - f_true) <= 1e-4 * (np.abs(f_true) + 1.0)))
+
+
+@pytest.mark.parametrize("model", ["transe_l2", "transe_l1", "distmult", "complex", "rotate"])
+@pytest.mark.parametrize("head", [False, True])
+def test_ranks_raw_and_filtered(model, head):
+    gr, trip, gpu, orc = _trained(model)
+    test = np.random.default_rng(11).integers(0, gr.n_triples, 24)
     hs, rs, ts = trip[0][test], trip[1][test], trip[2][test]
-    got = gpu.rank(hs, rs, ts, head=head)
-    ents = np.arange(gr.n_entities)
+    known = set(zip(*(a.tolist() for a in trip)))
+    raw = gpu.rank(hs, rs, ts, head=head)
+    fil = gpu.rank(hs, rs, ts, head=head, filters=kge.filter_lists(trip, hs, rs, ts, head=head))
+    ref_raw = O.link_rank(orc, hs, rs, ts, head=head)
+    ref_fil = O.link_rank(orc, hs, rs, ts, head=head, known=known)
     for i in range(len(test)):
-        f_true = orc.score_triples([hs[i]], [rs[i]], [ts[i]])[0]
-        if head:
-            f = orc.score_triples(ents, np.full_like(ents, rs[i]), np.full_like(ents, ts[i]))
-        else:
-            f = orc.score_triples(np.full_like(ents, hs[i]), np.full_like(ents, rs[i]), ents)
-        ref = 1 + int(np.sum(f > f_true))
-        near = int(np.sum(np.abs(f - f_true) <= 1e-4 * (np.abs(f_true) + 1.0)))
-        assert abs(int(got[i]) - ref) <= near, (i, got[i], ref, near)
-    m = kge.link_metrics(got)
+        near = _near_ties(orc, gr.n_entities, hs[i], rs[i], ts[i], head)
+        assert abs(int(raw[i]) - int(ref_raw[i])) <= near, (i, raw[i], ref_raw[i], near)
+        assert abs(int(fil[i]) - int(ref_fil[i])) <= near, (i, fil[i], ref_fil[i], near)
+    assert np.all(fil <= raw)
+    m = kge.link_metrics(fil)
     assert 1.0 <= m["MR"] <= gr.n_entities and 0.0 < m["MRR"] <= 1.0 and m["Hit@1"] <= m["Hit@3"] <= m["Hit@10"]
 
 
-def test_rank_of_planted_triple_is_one():
-    # DistMult with a planted score: make the true tail's row the only one aligned with h * r -> rank 1
+@pytest.mark.parametrize("model", ["transe_l2", "distmult", "rotate"])
+def test_ranks_sampled_protocol(model):
+    gr, trip, gpu, orc = _trained(model)
+    test = np.random.default_rng(12).integers(0, gr.n_triples, 16)
+    hs, rs, ts = trip[0][test], trip[1][test], trip[2][test]
+    deg = np.bincount(np.concatenate([trip[0], trip[2]]), minlength=gr.n_entities)
+    off, ids = kge.sampled_candidates(len(test), deg, seed=3)
+    got = gpu.rank(hs, rs, ts, candidates=(off, ids))
+    cands = [ids[off[i]:off[i + 1]] for i in range(len(test))]
+    ref = O.link_rank(orc, hs, rs, ts, candidates=cands)
+    for i in range(len(test)):
+        near = _near_ties(orc, gr.n_entities, hs[i], rs[i], ts[i], False, cands[i])
+        assert abs(int(got[i]) - int(ref[i])) <= near, (i, got[i], ref[i], near)
+    assert np.all(got >= 1) and np.all(got <= 2001)
+
+
+def test_rank_planted_and_errors():
     gr = synth.graph("tiny")
     trip = gr.triples()
     cfg = kge.Config(model="distmult", n_entities=gr.n_entities, n_relations=gr.n_relations, dim=8, batch_size=64,
@@ -53,8 +81,17 @@ def test_rank_of_planted_triple_is_one():
     gpu = kge.init(cfg, *trip)
     ents = np.arange(gr.n_entities)
     gpu.set_rows(0, ents, np.zeros((gr.n_entities, 8), np.float32))
-    gpu.set_rows(0, [3, 7], np.array([[1] * 8, [1] * 8], np.float32))
+    gpu.set_rows(0, [3, 7], np.ones((2, 8), np.float32))
     gpu.set_rows(1, [0], np.ones((1, 8), np.float32))
-    assert gpu.rank([3], [0], [7])[0] == 1  # only e = 3, 7 score > 0; 3 ties 7 exactly (not counted)
-    gpu.set_rows(0, [5], np.full((1, 8), 2.0, np.float32))
-    assert gpu.rank([3], [0], [7])[0] == 2  # e = 5 now scores higher than the true tail
+    assert gpu.rank([3], [0], [7])[0] == 2  # e = 3 ties the true tail 7 exactly: pessimistic, it ranks above
+    gpu.set_rows(0, [3], np.full((1, 8), 0.5, np.float32))
+    assert gpu.rank([3], [0], [7])[0] == 1  # the true tail uniquely maximises
+    assert gpu.rank([3], [0], [7], filters=(np.array([0, 1]), np.array([3])))[0] == 1
+    assert gpu.rank([3], [0], [7], candidates=(np.array([0, 3]), np.array([7, 7, 5])))[0] == 1
+    assert gpu.rank([3], [0], [7], candidates=(np.array([0, 0]), np.zeros(0, np.int64)))[0] == 1  # empty list
+    with pytest.raises(kge.KgeError):
+        gpu.rank([3], [0], [7], candidates=(np.array([0, 1]), np.array([5])), filters=(np.array([0, 1]), np.array([5])))
+    with pytest.raises(kge.KgeError):
+        gpu.rank([3], [0], [7], filters=(np.array([0, 1]), np.array([gr.n_entities])))
+    with pytest.raises(kge.KgeError):
+        gpu.rank([3], [0], [7], candidates=(np.array([1, 0]), np.array([5])))

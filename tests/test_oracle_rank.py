@@ -1,0 +1,122 @@
+"""Pins of the oracle's link-prediction ranking (PAPER.md:652-665 [5.3]; reading c.15) and of the host-side evaluation
+helpers in kge.py (filter lists, sampled candidate lists, metrics). The ranks are checked against closed-form scores
+computed here from the raw tables (DistMult: sum h*r*t; TransE-L2: gamma - ||h + r - t||), not the oracle's scorer."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2004_08532_b200 import kge
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "link_metrics_spec.txt")
+
+
+def _toy(model="distmult", n_e=20, n_r=3, n_t=60, dim=8, seed=0):
+    rng = np.random.default_rng(seed)
+    trip = tuple(a.astype(np.int64) for a in (rng.integers(0, n_e, n_t), rng.integers(0, n_r, n_t),
+                                               rng.integers(0, n_e, n_t)))
+    orc = O.Trainer(model, n_e, n_r, dim, 4, 2, 2, gamma=4.0, lr=0.1, seed=1, triples=trip)
+    E = rng.normal(size=(n_e, dim))
+    R = rng.normal(size=(n_r, dim))
+    orc.set_rows(0, np.arange(n_e), E)
+    orc.set_rows(1, np.arange(n_r), R)
+    return orc, trip, E, R
+
+
+def _closed_form(model, E, R, h, r, t, gamma=4.0):
+    if model == "distmult":
+        return float(np.sum(E[h] * R[r] * E[t]))
+    return gamma - float(np.linalg.norm(E[h] + R[r] - E[t]))
+
+
+def test_metrics_golden():
+    vals = {ln.split()[0]: ln.split()[1:] for ln in open(GOLD) if ln.strip() and not ln.startswith("#")}
+    ranks = [int(x) for x in vals.pop("ranks")]
+    for m in (O.link_metrics(ranks), kge.link_metrics(ranks)):
+        for k, v in vals.items():
+            assert m[k] == pytest.approx(float(v[0]), abs=1e-12), k
+    assert O.link_metrics([1, 1, 1]) == {"Hit@1": 1.0, "Hit@3": 1.0, "Hit@10": 1.0, "MR": 1.0, "MRR": 1.0}
+    with pytest.raises(ValueError):
+        O.link_metrics([])
+
+
+@pytest.mark.parametrize("model", ["distmult", "transe_l2"])
+@pytest.mark.parametrize("head", [False, True])
+def test_rank_brute_force_closed_form(model, head):
+    orc, trip, E, R = _toy(model)
+    q = np.arange(12)
+    got = O.link_rank(orc, trip[0][q], trip[1][q], trip[2][q], head=head)
+    for i in q:
+        h, r, t = int(trip[0][i]), int(trip[1][i]), int(trip[2][i])
+        ft = _closed_form(model, E, R, h, r, t)
+        sc = [(_closed_form(model, E, R, e, r, t) if head else _closed_form(model, E, R, h, r, e), e)
+              for e in range(20) if e != (h if head else t)]
+        assert got[i] == 1 + sum(1 for f, _ in sc if f >= ft - 1e-12 * abs(ft)), i
+
+
+def test_rank_planted_and_all_equal():
+    orc, trip, E, R = _toy("distmult")
+    h, r, t = int(trip[0][0]), int(trip[1][0]), int(trip[2][0])
+    # the positive uniquely maximises the score -> rank 1
+    E2 = np.full((20, 8), 0.1)
+    E2[t] = 5.0
+    E2[h] = 1.0
+    orc.set_rows(0, np.arange(20), E2)
+    orc.set_rows(1, [r], np.ones((1, 8)))
+    assert O.link_rank(orc, [h], [r], [t])[0] == 1
+    # all scores equal -> the positive is last among the 20 (pessimistic ties) ...
+    orc.set_rows(0, np.arange(20), np.ones((20, 8)))
+    assert O.link_rank(orc, [h], [r], [t])[0] == 20
+    # ... and filtering removes exactly the known corruptions
+    known = set(zip(*(a.tolist() for a in trip)))
+    n_known = len({e for (a, b, e) in known if a == h and b == r and e != t})
+    assert O.link_rank(orc, [h], [r], [t], known=known)[0] == 20 - n_known
+
+
+def test_filter_never_worsens_and_order_invariance():
+    orc, trip, E, R = _toy("distmult", seed=3)
+    q = np.arange(20)
+    known = set(zip(*(a.tolist() for a in trip)))
+    raw = O.link_rank(orc, trip[0][q], trip[1][q], trip[2][q])
+    fil = O.link_rank(orc, trip[0][q], trip[1][q], trip[2][q], known=known)
+    assert np.all(fil <= raw) and np.all(fil >= 1)
+    orc.set_rows(0, np.arange(20), 3.0 * E)  # scores scale by 9 > 0: a strictly monotone transform
+    assert np.array_equal(O.link_rank(orc, trip[0][q], trip[1][q], trip[2][q]), raw)
+
+
+def test_sampled_protocol_candidates():
+    orc, trip, E, R = _toy("distmult")
+    deg = np.bincount(np.concatenate([trip[0], trip[2]]), minlength=20)
+    off, ids = kge.sampled_candidates(5, deg, n_uniform=1000, n_degree=1000, seed=4)
+    assert np.array_equal(np.diff(off), np.full(5, 2000)) and ids.min() >= 0 and ids.max() < 20  # |S_i| = 2001
+    assert not np.any(np.isin(np.nonzero(deg == 0)[0], ids.reshape(5, 2000)[:, 1000:]))  # degree 0: never drawn
+    cands = [ids[off[i]:off[i + 1]] for i in range(5)]
+    h, r, t = trip[0][:5], trip[1][:5], trip[2][:5]
+    got = O.link_rank(orc, h, r, t, candidates=cands)
+    for i in range(5):
+        ft = _closed_form("distmult", E, R, int(h[i]), int(r[i]), int(t[i]))
+        fs = [_closed_form("distmult", E, R, int(h[i]), int(r[i]), int(e)) for e in cands[i] if e != t[i]]
+        assert got[i] == 1 + sum(1 for f in fs if f >= ft - 1e-12 * abs(ft))
+
+
+def test_degree_draws_proportional():
+    deg = np.array([1, 2, 3, 4, 10, 0, 5], np.float64)
+    off, ids = kge.sampled_candidates(1000, deg, n_uniform=0, n_degree=1000, seed=5)  # 10^6 draws
+    freq = np.bincount(ids, minlength=len(deg)) / len(ids)
+    p = deg / deg.sum()
+    assert freq[5] == 0 and np.all(np.abs(freq - p) <= 0.02 * p + 1e-12)
+
+
+def test_filter_lists_match_set():
+    rng = np.random.default_rng(7)
+    known = tuple(rng.integers(0, 15, 300) for _ in range(3))
+    ks = set(zip(*(a.tolist() for a in known)))
+    q = rng.integers(0, 300, 40)
+    hs, rs, ts = known[0][q], known[1][q], known[2][q]
+    for head in (False, True):
+        off, ids = kge.filter_lists(known, hs, rs, ts, head=head)
+        for i in range(40):
+            want = sorted({e for (a, b, c) in ks for e in [a if head else c]
+                           if (b == rs[i] and c == ts[i] if head else a == hs[i] and b == rs[i])})
+            assert sorted(set(ids[off[i]:off[i + 1]].tolist())) == want
