@@ -1460,79 +1460,116 @@ struct RankArgs {
   int64_t* ranks;
 };
 
+// per-float4 increment of the pair statistic (one expression shared by every rank path, so equal rows give
+// bit-equal scores and ties are decided identically)
+__device__ __forceinline__ float stat4(int fam, const float4 ov, const float4 xv) {
+  if (fam == FAM_DOT) return ov.x * xv.x + ov.y * xv.y + ov.z * xv.z + ov.w * xv.w;
+  if (fam == FAM_L1) return fabsf(ov.x - xv.x) + fabsf(ov.y - xv.y) + fabsf(ov.z - xv.z) + fabsf(ov.w - xv.w);
+  const float a = ov.x - xv.x, b = ov.y - xv.y, c = ov.z - xv.z, e = ov.w - xv.w;
+  return a * a + b * b + c * c + e * e;
+}
+
+__device__ __forceinline__ float cmod1(const float* o, const float* x, int c, int hlf) {
+  const float ur = o[c] - x[c], ui = o[c + hlf] - x[c + hlf];
+  return sqrtf(ur * ur + ui * ui);
+}
+
 // pair statistic of o (shared memory) and an entity row x, reduced over the warp (families of step.cu)
 __device__ __forceinline__ float pair_stat_row(int fam, const float* o, const float* __restrict__ x, int d, int lane) {
   float st = 0.f;
   if (fam == FAM_CMOD) {
-    const int hlf = d >> 1;
-    for (int c = lane; c < hlf; c += 32) {
-      const float ur = o[c] - x[c], ui = o[c + hlf] - x[c + hlf];
-      st += sqrtf(ur * ur + ui * ui);
-    }
+    for (int c = lane; c < (d >> 1); c += 32) st += cmod1(o, x, c, d >> 1);
   } else {
-    for (int v = lane; v < (d >> 2); v += 32) {
-      const float4 ov = reinterpret_cast<const float4*>(o)[v];
-      const float4 xv = ld4(x, v);
-      if (fam == FAM_DOT) {
-        st += ov.x * xv.x + ov.y * xv.y + ov.z * xv.z + ov.w * xv.w;
-      } else if (fam == FAM_L1) {
-        st += fabsf(ov.x - xv.x) + fabsf(ov.y - xv.y) + fabsf(ov.z - xv.z) + fabsf(ov.w - xv.w);
-      } else {
-        const float a = ov.x - xv.x, b = ov.y - xv.y, c = ov.z - xv.z, e = ov.w - xv.w;
-        st += a * a + b * b + c * c + e * e;
-      }
-    }
+    for (int v = lane; v < (d >> 2); v += 32) st += stat4(fam, reinterpret_cast<const float4*>(o)[v], ld4(x, v));
   }
   return warp_sum(st);
 }
 
-__global__ void __launch_bounds__(256) k_rank(RankArgs a) {
-  extern __shared__ __align__(16) float osm[];  // o = combine(h, r) (tail) | combine'(r, t) (head), d floats
-  __shared__ float s_true;
-  __shared__ int s_cnt[8];
-  const Dims& dm = a.dm;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i = blockIdx.x;
-  const float* h = a.ent.row(a.hs[i]);
-  const float* t = a.ent.row(a.ts[i]);
-  const float* r = a.rel + (int64_t)a.rs[i] * dm.drel;
-  const int mode = a.head ? 1 : 0;
-  if (warp == 0) {
-    float st, on;
-    combine_row(dm.model, mode, h, r, t, osm, dm.d, lane, mode == 0 ? t : h, dm.family, st, on);
-  }
-  __syncthreads();
-  if (warp == 0) {  // the true entity through the same arithmetic as every candidate
-    const float st = pair_stat_row(dm.family, osm, mode == 0 ? t : h, dm.d, lane);
-    if (lane == 0) s_true = pair_score_from(dm.family, st, dm.gamma);
-  }
-  __syncthreads();
-  const float ft = s_true;
-  const int64_t tid = mode == 0 ? a.ts[i] : a.hs[i];
-  // pessimistic ties (reading c.15): every candidate other than the true entity scoring >= f(true) ranks above it
-  int64_t lo = 0, hi = dm.n_entities;
-  if (a.cand_off) lo = a.cand_off[i], hi = a.cand_off[i + 1];
-  int cnt = 0;
-  for (int64_t j = lo + warp; j < hi; j += 8) {
-    const int64_t e = a.cand_off ? (int64_t)a.cand[j] : j;
-    if (e == tid) continue;
-    const float f = pair_score_from(dm.family, pair_stat_row(dm.family, osm, a.ent.row(e), dm.d, lane), dm.gamma);
-    cnt += f >= ft ? 1 : 0;
-  }
-  if (a.filt_off) {  // filtered protocol: known triples among the candidates do not count
-    for (int64_t j = a.filt_off[i] + warp; j < a.filt_off[i + 1]; j += 8) {
-      const int64_t e = a.filt[j];
-      if (e == tid) continue;
-      const float f = pair_score_from(dm.family, pair_stat_row(dm.family, osm, a.ent.row(e), dm.d, lane), dm.gamma);
-      cnt -= f >= ft ? 1 : 0;
+// the same statistic of one entity row against QB query rows o_q = osm + q*dp: the row is read once for all queries
+template <int QB>
+__device__ __forceinline__ void pair_stat_rows(int fam, const float* osm, int dp, const float* __restrict__ x, int d,
+                                               int lane, float (&st)[QB]) {
+#pragma unroll
+  for (int q = 0; q < QB; ++q) st[q] = 0.f;
+  if (fam == FAM_CMOD) {
+    for (int c = lane; c < (d >> 1); c += 32) {
+#pragma unroll
+      for (int q = 0; q < QB; ++q) st[q] += cmod1(osm + q * dp, x, c, d >> 1);
+    }
+  } else {
+    for (int v = lane; v < (d >> 2); v += 32) {
+      const float4 xv = ld4(x, v);
+#pragma unroll
+      for (int q = 0; q < QB; ++q) st[q] += stat4(fam, reinterpret_cast<const float4*>(osm + q * dp)[v], xv);
     }
   }
-  if (lane == 0) s_cnt[warp] = cnt;
+#pragma unroll
+  for (int q = 0; q < QB; ++q) st[q] = warp_sum(st[q]);
+}
+
+// One CTA ranks QB queries of one corrupted side (QB > 1 only with every entity as the candidate set): warp q builds
+// o_q = combine(h, r) (tail) | combine'(r, t) (head) in shared memory and the positive's score through the same
+// arithmetic as every candidate; the 8 warps then stream the candidate rows, each row scored against all QB queries.
+template <int QB>
+__global__ void __launch_bounds__(256) k_rank(RankArgs a, int64_t n) {
+  extern __shared__ __align__(16) float osm[];  // QB x dp floats
+  __shared__ float s_true[QB];
+  __shared__ int64_t s_tid[QB];
+  __shared__ int s_cnt[8][QB];
+  const Dims& dm = a.dm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * QB;
+  const int nq = (int)(n - i0 < QB ? n - i0 : (int64_t)QB);
+  const int mode = a.head ? 1 : 0;
+  if (warp < nq) {
+    const int64_t i = i0 + warp;
+    const float* h = a.ent.row(a.hs[i]);
+    const float* t = a.ent.row(a.ts[i]);
+    const float* r = a.rel + (int64_t)a.rs[i] * dm.drel;
+    float st, on;
+    combine_row(dm.model, mode, h, r, t, osm + warp * dm.dp, dm.d, lane, mode == 0 ? t : h, dm.family, st, on);
+    __syncwarp();
+    const float sp = pair_stat_row(dm.family, osm + warp * dm.dp, mode == 0 ? t : h, dm.d, lane);
+    if (lane == 0) {
+      s_true[warp] = pair_score_from(dm.family, sp, dm.gamma);
+      s_tid[warp] = mode == 0 ? a.ts[i] : a.hs[i];
+    }
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  // pessimistic ties (reading c.15): every candidate other than the true entity scoring >= f(true) ranks above it
+  int cnt[QB];
+#pragma unroll
+  for (int q = 0; q < QB; ++q) cnt[q] = 0;
+  int64_t lo = 0, hi = dm.n_entities;
+  if (a.cand_off) lo = a.cand_off[i0], hi = a.cand_off[i0 + 1];  // QB == 1
+  for (int64_t j = lo + warp; j < hi; j += 8) {
+    const int64_t e = a.cand_off ? (int64_t)a.cand[j] : j;
+    float st[QB];
+    pair_stat_rows<QB>(dm.family, osm, dm.dp, a.ent.row(e), dm.d, lane, st);
+#pragma unroll
+    for (int q = 0; q < QB; ++q)
+      if (q < nq && e != s_tid[q]) cnt[q] += pair_score_from(dm.family, st[q], dm.gamma) >= s_true[q] ? 1 : 0;
+  }
+  if (a.filt_off) {  // filtered protocol: known triples among the candidates do not count
+    for (int q = 0; q < nq; ++q) {
+      for (int64_t j = a.filt_off[i0 + q] + warp; j < a.filt_off[i0 + q + 1]; j += 8) {
+        const int64_t e = a.filt[j];
+        if (e == s_tid[q]) continue;
+        const float f = pair_score_from(dm.family, pair_stat_row(dm.family, osm + q * dm.dp, a.ent.row(e), dm.d, lane),
+                                        dm.gamma);
+        cnt[q] -= f >= s_true[q] ? 1 : 0;
+      }
+    }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < QB; ++q) s_cnt[warp][q] = cnt[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < nq) {
     int64_t c = 0;
-    for (int w = 0; w < 8; ++w) c += s_cnt[w];
-    a.ranks[i] = 1 + c;
+    for (int w = 0; w < 8; ++w) c += s_cnt[w][threadIdx.x];
+    a.ranks[i0 + threadIdx.x] = 1 + c;
   }
 }
 
@@ -1540,7 +1577,12 @@ cudaError_t launch_rank(kge_handle* h, const int32_t* hs, const int32_t* rs, con
                         const int64_t* cand_off, const int32_t* cand, const int64_t* filt_off, const int32_t* filt,
                         int64_t* ranks) {
   RankArgs ra{h->dims, h->rows, h->rel, hs, rs, ts, head, cand_off, cand, filt_off, filt, ranks};
-  k_rank<<<(unsigned)n, 256, (size_t)h->dims.dp * 4, h->stream>>>(ra);
+  static const int qb_env = getenv("KGE_RANK_QB") ? atoi(getenv("KGE_RANK_QB")) : 8;
+  if (cand_off || qb_env == 1) {
+    k_rank<1><<<(unsigned)n, 256, (size_t)h->dims.dp * 4, h->stream>>>(ra, n);
+  } else {
+    k_rank<8><<<(unsigned)((n + 7) / 8), 256, (size_t)8 * h->dims.dp * 4, h->stream>>>(ra, n);
+  }
   ++h->launches;
   return cudaGetLastError();
 }

@@ -95,3 +95,20 @@ def test_rank_planted_and_errors():
         gpu.rank([3], [0], [7], filters=(np.array([0, 1]), np.array([gr.n_entities])))
     with pytest.raises(kge.KgeError):
         gpu.rank([3], [0], [7], candidates=(np.array([1, 0]), np.array([5])))
+
+
+@pytest.mark.parametrize("model", ["transe_l2", "distmult"])
+def test_training_improves_filtered_mrr(model):
+    """End-to-end sanity of the training step through the evaluation path: training-triple MRR rises with training."""
+    gr = synth.graph("tiny")
+    trip = gr.triples()
+    cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=64, batch_size=256,
+                     chunk_size=64, neg_k=64, gamma=12.0, lr=0.1, seed=5)
+    gpu = kge.init(cfg, *trip)
+    test = np.random.default_rng(13).integers(0, gr.n_triples, 200)
+    q = (trip[0][test], trip[1][test], trip[2][test])
+    filt = kge.filter_lists(trip, *q)
+    before = kge.link_metrics(gpu.rank(*q, filters=filt))["MRR"]
+    gpu.train_step(400)
+    after = kge.link_metrics(gpu.rank(*q, filters=filt))["MRR"]
+    assert after > 2.0 * before, (before, after)
