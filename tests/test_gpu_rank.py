@@ -99,7 +99,9 @@ def test_rank_planted_and_errors():
 
 @pytest.mark.parametrize("model", ["transe_l2", "distmult"])
 def test_training_improves_filtered_mrr(model):
-    """End-to-end sanity of the training step through the evaluation path: training-triple MRR rises with training."""
+    """End-to-end sanity of the training step through the evaluation path: training-triple MRR rises with training.
+    The oracle on the same configuration (double) gives filtered MRR 0.0265 -> 0.0865 (TransE-L2) and
+    0.0200 -> 0.3217 (DistMult) after 1600 steps; TransE-L2 with gamma = 12 moves slowly (0.0360 after 400 steps)."""
     gr = synth.graph("tiny")
     trip = gr.triples()
     cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=64, batch_size=256,
@@ -109,6 +111,6 @@ def test_training_improves_filtered_mrr(model):
     q = (trip[0][test], trip[1][test], trip[2][test])
     filt = kge.filter_lists(trip, *q)
     before = kge.link_metrics(gpu.rank(*q, filters=filt))["MRR"]
-    gpu.train_step(400)
+    gpu.train_step(1600)
     after = kge.link_metrics(gpu.rank(*q, filters=filt))["MRR"]
     assert after > 2.0 * before, (before, after)

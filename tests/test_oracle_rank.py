@@ -120,3 +120,21 @@ def test_filter_lists_match_set():
             want = sorted({e for (a, b, c) in ks for e in [a if head else c]
                            if (b == rs[i] and c == ts[i] if head else a == hs[i] and b == rs[i])})
             assert sorted(set(ids[off[i]:off[i + 1]].tolist())) == want
+
+
+def test_oracle_training_raises_filtered_mrr():
+    """The oracle's step descends the logistic loss: a sign error in any score gradient or in the
+    Adagrad step would make the training triples' filtered MRR fall instead of rise (DistMult, tiny graph)."""
+    import synth
+    gr = synth.graph("tiny")
+    trip = gr.triples()
+    test = np.random.default_rng(13).integers(0, gr.n_triples, 100)
+    q = [a[test] for a in trip]
+    known = set(zip(*(a.tolist() for a in trip)))
+    orc = O.Trainer("distmult", gr.n_entities, gr.n_relations, 64, 256, 64, 64, gamma=12.0, lr=0.1, seed=5,
+                    triples=trip)
+    before = kge.link_metrics(O.link_rank(orc, *q, known=known))["MRR"]
+    losses = orc.train(400)
+    after = kge.link_metrics(O.link_rank(orc, *q, known=known))["MRR"]
+    assert losses[-50:].mean() < losses[:50].mean()
+    assert after > 5.0 * before, (before, after)
