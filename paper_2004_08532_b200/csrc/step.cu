@@ -1458,6 +1458,7 @@ struct RankArgs {
   const int64_t* filt_off;  // [n+1] or NULL (raw); distinct ids, only with cand_off == NULL
   const int32_t* filt;
   int64_t* ranks;
+  int32_t nsplit;  // entity-range splits (blockIdx.y) of the all-entity protocol; > 1: ranks zeroed, partial counts added
 };
 
 // per-float4 increment of the pair statistic (one expression shared by every rank path, so equal rows give
@@ -1510,6 +1511,9 @@ __device__ __forceinline__ void pair_stat_rows(int fam, const float* osm, int dp
 // One CTA ranks QB queries of one corrupted side (QB > 1 only with every entity as the candidate set): warp q builds
 // o_q = combine(h, r) (tail) | combine'(r, t) (head) in shared memory and the positive's score through the same
 // arithmetic as every candidate; the 8 warps then stream the candidate rows, each row scored against all QB queries.
+// With every entity as the candidate set the entity range is split over blockIdx.y (a few thousand queries alone
+// would not fill 148 SMs); split 0 also handles the filter list and adds the 1; partial counts meet in integer
+// atomics (exact, order-free).
 template <int QB>
 __global__ void __launch_bounds__(256) k_rank(RankArgs a, int64_t n) {
   extern __shared__ __align__(16) float osm[];  // QB x dp floats
@@ -1542,6 +1546,12 @@ __global__ void __launch_bounds__(256) k_rank(RankArgs a, int64_t n) {
   for (int q = 0; q < QB; ++q) cnt[q] = 0;
   int64_t lo = 0, hi = dm.n_entities;
   if (a.cand_off) lo = a.cand_off[i0], hi = a.cand_off[i0 + 1];  // QB == 1
+  const int split = blockIdx.y;
+  if (gridDim.y > 1) {
+    const int64_t per = (hi + gridDim.y - 1) / gridDim.y;
+    lo = per * split;
+    hi = min(hi, lo + per);
+  }
   for (int64_t j = lo + warp; j < hi; j += 8) {
     const int64_t e = a.cand_off ? (int64_t)a.cand[j] : j;
     float st[QB];
@@ -1550,7 +1560,7 @@ __global__ void __launch_bounds__(256) k_rank(RankArgs a, int64_t n) {
     for (int q = 0; q < QB; ++q)
       if (q < nq && e != s_tid[q]) cnt[q] += pair_score_from(dm.family, st[q], dm.gamma) >= s_true[q] ? 1 : 0;
   }
-  if (a.filt_off) {  // filtered protocol: known triples among the candidates do not count
+  if (a.filt_off && split == 0) {  // filtered protocol: known triples among the candidates do not count
     for (int q = 0; q < nq; ++q) {
       for (int64_t j = a.filt_off[i0 + q] + warp; j < a.filt_off[i0 + q + 1]; j += 8) {
         const int64_t e = a.filt[j];
@@ -1569,19 +1579,35 @@ __global__ void __launch_bounds__(256) k_rank(RankArgs a, int64_t n) {
   if (threadIdx.x < nq) {
     int64_t c = 0;
     for (int w = 0; w < 8; ++w) c += s_cnt[w][threadIdx.x];
-    a.ranks[i0 + threadIdx.x] = 1 + c;
+    if (gridDim.y == 1)
+      a.ranks[i0 + threadIdx.x] = 1 + c;
+    else  // two's-complement wrap makes a negative partial (filter subtraction) exact
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.ranks + i0 + threadIdx.x),
+                (unsigned long long)(c + (split == 0 ? 1 : 0)));
   }
 }
 
 cudaError_t launch_rank(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, int head,
                         const int64_t* cand_off, const int32_t* cand, const int64_t* filt_off, const int32_t* filt,
                         int64_t* ranks) {
-  RankArgs ra{h->dims, h->rows, h->rel, hs, rs, ts, head, cand_off, cand, filt_off, filt, ranks};
+  RankArgs ra{h->dims, h->rows, h->rel, hs, rs, ts, head, cand_off, cand, filt_off, filt, ranks, 1};
   static const int qb_env = getenv("KGE_RANK_QB") ? atoi(getenv("KGE_RANK_QB")) : 8;
   if (cand_off || qb_env == 1) {
     k_rank<1><<<(unsigned)n, 256, (size_t)h->dims.dp * 4, h->stream>>>(ra, n);
   } else {
-    k_rank<8><<<(unsigned)((n + 7) / 8), 256, (size_t)8 * h->dims.dp * 4, h->stream>>>(ra, n);
+    // at least 4 splits (ncu kernel times, FB15k-sized table, d=400: 2000 queries 5.77 -> 3.56 ms TransE-L2, 4.80 ->
+    // 3.15 ms DistMult; 20000 queries 33.2 -> 31.4 / 30.1 -> 26.6 ms: shorter CTAs trim the last wave), more when the
+    // queries alone give fewer than ~4 CTAs per SM; each split streams at least 512 entity rows
+    const int64_t nb = (n + 7) / 8;
+    static const int split_env = getenv("KGE_RANK_SPLIT") ? atoi(getenv("KGE_RANK_SPLIT")) : 0;
+    int64_t S = split_env > 0 ? split_env : std::max<int64_t>(4, (4 * 148 + nb - 1) / nb);
+    S = std::max<int64_t>(1, std::min<int64_t>({S, h->dims.n_entities / 512, 65535}));
+    ra.nsplit = (int32_t)S;
+    if (S > 1) {
+      cudaError_t e = cudaMemsetAsync(ranks, 0, (size_t)n * sizeof(int64_t), h->stream);
+      if (e != cudaSuccess) return e;
+    }
+    k_rank<8><<<dim3((unsigned)nb, (unsigned)S), 256, (size_t)8 * h->dims.dp * 4, h->stream>>>(ra, n);
   }
   ++h->launches;
   return cudaGetLastError();

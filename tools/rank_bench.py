@@ -26,11 +26,11 @@ test = np.random.default_rng(1).integers(0, gr.n_triples, nq)
 q = (trip[0][test], trip[1][test], trip[2][test])
 filt = kge.filter_lists(trip, *q)
 out = {"model": model, "n_entities": gr.n_entities, "dim": 400, "queries": nq,
-       "qb": os.environ.get("KGE_RANK_QB", "8")}
+       "qb": os.environ.get("KGE_RANK_QB", "8"), "split": os.environ.get("KGE_RANK_SPLIT", "auto")}
 for name, kw in (("raw", {}), ("filtered", {"filters": filt})):
     h.rank(*q, **kw)
     t0 = time.perf_counter()
-    reps = 3
+    reps = int(os.environ.get("RANK_REPS", "3"))
     for _ in range(reps):
         r = h.rank(*q, **kw)
     dt = (time.perf_counter() - t0) / reps
