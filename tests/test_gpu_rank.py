@@ -57,6 +57,39 @@ def test_ranks_raw_and_filtered(model, head):
     assert 1.0 <= m["MR"] <= gr.n_entities and 0.0 < m["MRR"] <= 1.0 and m["Hit@1"] <= m["Hit@3"] <= m["Hit@10"]
 
 
+@pytest.mark.parametrize("model", ["transe_l2", "distmult"])
+@pytest.mark.parametrize("head", [False, True])
+def test_ranks_entity_split(model, head):
+    """FB15k-sized entity set: the all-entity kernel splits the entity range over S >= 4 CTAs per query group and adds
+    the integer partial counts (split 0 also carries the filter list); 19 queries leave a ragged last group of 3."""
+    gr = synth.graph("fb15k")
+    trip = gr.triples()
+    cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=32, batch_size=128,
+                     chunk_size=32, neg_k=32, gamma=12.0, lr=0.1, seed=4, neg_precision="fp32")
+    gpu = kge.init(cfg, *trip)
+    gpu.train_step(5)
+    orc = O.Trainer(model, gr.n_entities, gr.n_relations, 32, 128, 32, 32, gamma=12.0, lr=0.1, seed=4, triples=trip)
+    for table, n in ((0, gr.n_entities), (1, gr.n_relations)):
+        ids = np.arange(n)
+        orc.set_rows(table, ids, gpu.get_rows(table, ids).astype(np.float64))
+    test = np.random.default_rng(21).integers(0, gr.n_triples, 19)
+    hs, rs, ts = trip[0][test], trip[1][test], trip[2][test]
+    filt = kge.filter_lists(trip, hs, rs, ts, head=head)
+    known = set()
+    for i in range(len(test)):  # the known triples that can occur among these queries' corruptions
+        for e in filt[1][filt[0][i]:filt[0][i + 1]]:
+            known.add((int(e), int(rs[i]), int(ts[i])) if head else (int(hs[i]), int(rs[i]), int(e)))
+    raw = gpu.rank(hs, rs, ts, head=head)
+    fil = gpu.rank(hs, rs, ts, head=head, filters=filt)
+    ref_raw = O.link_rank(orc, hs, rs, ts, head=head)
+    ref_fil = O.link_rank(orc, hs, rs, ts, head=head, known=known)
+    for i in range(len(test)):
+        near = _near_ties(orc, gr.n_entities, hs[i], rs[i], ts[i], head)
+        assert abs(int(raw[i]) - int(ref_raw[i])) <= near, (i, raw[i], ref_raw[i], near)
+        assert abs(int(fil[i]) - int(ref_fil[i])) <= near, (i, fil[i], ref_fil[i], near)
+    assert np.all(fil <= raw) and np.all(fil >= 1) and np.all(raw <= gr.n_entities)
+
+
 @pytest.mark.parametrize("model", ["transe_l2", "distmult", "rotate"])
 def test_ranks_sampled_protocol(model):
     gr, trip, gpu, orc = _trained(model)
