@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define KGE_ABI_VERSION 2  /* 2: kge_config::neg_deg_k */
+#define KGE_ABI_VERSION 3  /* 2: kge_config::neg_deg_k; 3: kge_config::neg_local (validated: 0 or 1) */
 
 typedef struct kge_handle kge_handle; /* opaque, library-owned */
 
@@ -199,6 +199,22 @@ int kge_connect(kge_handle* h, const void* blobs /* world_size blobs, rank order
 /* Single-process emulation: ranks 0..P-1 as P handles on one device, connected directly (tests / one-GPU parity). */
 int kge_connect_local(kge_handle** hs, int32_t world_size);
 int kge_relation_owner(const kge_handle* h, int64_t relation); /* rank, -1 = split (replicated), -2 = bad id */
+
+/* Run-time options (diagnostics and robustness knobs; none changes the result of a step):
+ *   KGE_OPT_FFMA_SPLITK   : split-K factor of the FFMA negative kernels, 0 = automatic (default), else 1, 2, 4 or 8
+ *                           (forces the deterministic parked-partial reduction at any shape; KGE_EINVAL otherwise).
+ *   KGE_OPT_CAPTURE_NEG   : 1 = the following training steps (kge_train_step) also store every negative pair score
+ *                           f-_{i,j} (the g x k chunk products) into a library buffer read by
+ *                           kge_debug_neg_scores; 0 = off (default). Not captured into the caller-batch CUDA graphs.
+ *   KGE_OPT_BARRIER_MS    : P > 1 device-barrier timeout in milliseconds (default 120000). A rank that waits longer
+ *                           for a peer leaves the barrier, and the next synchronising call returns KGE_ECUDA
+ *                           ("device barrier timed out") instead of hanging or trapping the context. */
+enum { KGE_OPT_FFMA_SPLITK = 0, KGE_OPT_CAPTURE_NEG = 1, KGE_OPT_BARRIER_MS = 2 };
+int kge_set_option(kge_handle* h, int32_t option, int64_t value);
+/* Negative pair scores f-_{i,j} of the last step run with KGE_OPT_CAPTURE_NEG on: out = host float[B * k], row i =
+ * positive i of the batch (chunk i / g), column j = negative slot j of that chunk -- the scores the negative kernels
+ * fed into the loss (FP32 FFMA, TF32/BF16 tcgen05 or TransR path). Synchronous. KGE_ESTATE if capture is off. */
+int kge_debug_neg_scores(kge_handle* h, float* out);
 
 /* Diagnostics. Kernel ids for kge_profile_end. Between begin and end every kernel launch of the step is bracketed by
  * CUDA events on the stream it runs on, and programmatic dependent launch is off (each kernel starts after its

@@ -15,7 +15,7 @@ def build(force: bool = False) -> str:
     deps = src + [os.path.join(HERE, "oracle.h")]
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(p) for p in deps):
         return LIB
-    cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+    cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
            "-Wall", "-o", LIB] + src
     subprocess.check_call(cmd)
     return LIB

@@ -1,4 +1,5 @@
-// oracle.cpp -- TEST INFRASTRUCTURE ONLY (see oracle.h). Plain, slow, single-threaded CPU oracle of the
+// oracle.cpp -- TEST INFRASTRUCTURE ONLY (see oracle.h). Plain, slow, single-threaded (ORC_THREADS > 1: the
+// independent per-row loops of the step in parallel, bit-identical results) CPU oracle of the
 // DGL-KE mini-batch KGE training step. Every function cites the passage it follows; readings of the paper
 // where it is silent are SURVEY.md 8(c) c.1..c.14, restated in DESIGN.md "Readings of the paper".
 // Build: g++ -O2 -ffp-contract=off -fPIC -shared (no fast-math). Shares no code with the CUDA path.
@@ -7,12 +8,22 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <unordered_map>
 #include <vector>
 
 namespace {
+
+// Threads of the optional parallel loops of the training step (ORC_THREADS, default 1 = the single-threaded oracle).
+// The loops run over independent output rows (positive i, negative slot (c, j)); every value is computed by the same
+// operations in the same order as with one thread, and the loss is still summed serially -- results are identical.
+int threads() {
+  const char* v = std::getenv("ORC_THREADS");
+  const int n = v ? std::atoi(v) : 1;
+  return n > 1 ? n : 1;
+}
 
 // ------------------------------------------------------------------------------------------------
 // c.1 Philox4x32-10 (Salmon et al., Random123; the bijection CUDA's curand uses). Not in the paper:
@@ -562,8 +573,18 @@ struct Trainer : Base {
         }
         for (int64_t q = 0; q < (int64_t)Cn * k; ++q) eo[2 * B + q] = neg[(size_t)q];
         // (2)+(3) fetch rows and score: positives f+_i = f(h_i, r_i, t_i); negatives naive per triple (c.8)
+        // (rows are materialised serially first: the optional parallel loops below only read the stores)
+        for (int32_t i = 0; i < B; ++i) {
+          ent.row(hh[(size_t)i]);
+          ent.row(tt[(size_t)i]);
+          rel.row(rr[(size_t)i]);
+          if (has_proj) proj.row(rr[(size_t)i]);
+        }
+        for (int64_t q = 0; q < (int64_t)Cn * k; ++q) ent.row(neg[(size_t)q]);
+        const int nth = threads();
         std::vector<T> fpos((size_t)B), fneg((size_t)B * k), dpos((size_t)B), dneg((size_t)B * k);
         for (int32_t i = 0; i < B; ++i) fpos[(size_t)i] = score_ids(hh[(size_t)i], rr[(size_t)i], tt[(size_t)i]);
+#pragma omp parallel for num_threads(nth) schedule(dynamic, 8) if (nth > 1)
         for (int32_t i = 0; i < B; ++i) {
           int32_t c = i / g;
           for (int32_t j = 0; j < k; ++j) {
@@ -586,8 +607,9 @@ struct Trainer : Base {
         // backward: per-occurrence gradients (c.10); positive term first, then j = 0..k-1
         T* G = &Gent[(size_t)w * n_occ * d];
         T* GR = &Grel[(size_t)w * B * drel];
-        std::vector<T> sink((size_t)d, T(0));
+#pragma omp parallel for num_threads(nth) schedule(dynamic, 8) if (nth > 1)
         for (int32_t i = 0; i < B; ++i) {
+          std::vector<T> sink((size_t)d, T(0));
           int32_t c = i / g;
           T* gh = G + (size_t)i * d;
           T* gt = G + (size_t)(B + i) * d;
@@ -609,9 +631,10 @@ struct Trainer : Base {
           }
         }
         // negatives: sum over i in the chunk, ascending (c.10)
-        std::vector<T> junk_r((size_t)drel), junk_e((size_t)d), junk_m(has_proj ? (size_t)d * d : 0);
-        for (int32_t c = 0; c < Cn; ++c)
-          for (int32_t j = 0; j < k; ++j) {
+#pragma omp parallel for num_threads(nth) schedule(dynamic, 4) if (nth > 1)
+        for (int64_t cj = 0; cj < (int64_t)Cn * k; ++cj) {
+            const int32_t c = (int32_t)(cj / k), j = (int32_t)(cj % k);
+            std::vector<T> junk_r((size_t)drel), junk_e((size_t)d), junk_m(has_proj ? (size_t)d * d : 0);
             int64_t x = neg[(size_t)c * k + j];
             T* gx = G + (size_t)(2 * B + c * k + j) * d;
             for (int32_t i = c * g; i < (c + 1) * g; ++i) {
@@ -699,6 +722,15 @@ struct Trainer : Base {
     return 0;
   }
   int score_triples(const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, double* out) override {
+    const int nth = threads();
+    if (nth > 1)  // materialise lazily stored rows serially; the parallel loop then only reads the stores
+      for (int64_t i = 0; i < n; ++i) {
+        ent.row(hs[i]);
+        ent.row(ts[i]);
+        rel.row(rs[i]);
+        if (has_proj) proj.row(rs[i]);
+      }
+#pragma omp parallel for num_threads(nth) schedule(static) if (nth > 1)
     for (int64_t i = 0; i < n; ++i) out[i] = (double)score_ids(hs[i], rs[i], ts[i]);
     return 0;
   }

@@ -118,6 +118,11 @@ static int validate(const kge_config* c) {
   if (c->neg_precision < 0 || c->neg_precision > 1) { set_error("bad neg_precision"); return KGE_EINVAL; }
   if (c->lag != 0 && c->lag != 1) { set_error("lag must be 0 or 1"); return KGE_EINVAL; }
   if (c->neg_deg_k < 0 || c->neg_deg_k > c->neg_k) { set_error("neg_deg_k must be in [0, neg_k]"); return KGE_EINVAL; }
+  if (c->neg_local != 0 && c->neg_local != 1) { set_error("neg_local must be 0 or 1"); return KGE_EINVAL; }
+  if (c->neg_local && c->world_size > 1 && c->n_entities < c->world_size) {
+    set_error("neg_local needs n_entities >= world_size (every shard non-empty)");
+    return KGE_EINVAL;
+  }
   if (c->lag == 1 && (c->world_size > 1 || c->model == KGE_TRANSR)) {
     set_error("lag = 1 is implemented for one rank and the non-TransR models");
     return KGE_EUNSUPPORTED;
@@ -602,6 +607,10 @@ static int check_flags(kge_handle* h) {
   cudaError_t e = cudaMemcpyAsync(f, h->buf.flags, 16, cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sync");
+  if (f[1]) {
+    set_error("device barrier timed out: a peer rank did not reach the step (KGE_OPT_BARRIER_MS)");
+    return KGE_ECUDA;
+  }
   if (f[0]) {
     cudaMemsetAsync(h->buf.flags, 0, 4, h->stream);
     set_error("a step produced a non-finite loss; its update was skipped");
@@ -642,7 +651,7 @@ static int enqueue_step(kge_handle* h, const Slot& slot, int64_t s, int gi) {
   }
   h->next_slot = gi >= 0 ? d_slots(h) + h->ring + 1 + (gi + 1) % kge_handle::kGiven : d_slots(h) + (s + 1) % h->ring;
   if (e == cudaSuccess) e = launch_step(h, slot, s);
-  if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, slot);
+  if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, slot, s);
   if (e != cudaSuccess) return cuda_fail(e, "step");
   if (h->cfg.lag == 1) {
     if (h->pend_step >= 0) {
@@ -976,7 +985,8 @@ static int rows_io(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, 
   float* tab = table_ptr(h, table, &w, &rows);
   if (!tab) { set_error("table not present for this model"); return KGE_EINVAL; }
   if (n == 0) return KGE_OK;
-  const int rj = join_updates(h);
+  // lag = 1: the held-back entity update belongs to the table the caller reads / overwrites
+  const int rj = kge_flush(h);
   if (rj != KGE_OK) return rj;
   std::vector<int32_t> ids32(n);
   const bool sharded = h->P > 1 && (table == 0 || table == 3);
@@ -1021,7 +1031,7 @@ int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t
     ids[n + i] = (int32_t)rs[i];
     ids[2 * n + i] = (int32_t)ts[i];
   }
-  const int rj = join_updates(h);
+  const int rj = kge_flush(h);  // lag = 1: score the tables with every enqueued update applied
   if (rj != KGE_OK) return rj;
   int32_t* d_ids = nullptr;
   float* d_out = nullptr;
@@ -1092,7 +1102,7 @@ int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t*
     const int rc = pack_list(filt_off, filt_ids, n, h->dims.n_entities, true, fo, fv);
     if (rc != KGE_OK) return rc;
   }
-  const int rj = join_updates(h);
+  const int rj = kge_flush(h);  // lag = 1: rank against the tables with every enqueued update applied
   if (rj != KGE_OK) return rj;
   // one device block: ids | offsets (8-byte aligned) | list ids | ranks
   const size_t b_ids = (size_t)3 * n * 4, b_co = co.size() * 8, b_fo = fo.size() * 8;
@@ -1178,6 +1188,42 @@ int kge_profile_end(kge_handle* h, int32_t n_kernels, double* avg_ms, int64_t* l
 }
 
 int64_t kge_launch_count(const kge_handle* h) { return h ? h->launches : 0; }
+
+int kge_set_option(kge_handle* h, int32_t option, int64_t value) {
+  if (!h) { set_error("NULL handle"); return KGE_EINVAL; }
+  switch (option) {
+    case KGE_OPT_FFMA_SPLITK:
+      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8) {
+        set_error("KGE_OPT_FFMA_SPLITK must be 0 (automatic), 1, 2, 4 or 8");
+        return KGE_EINVAL;
+      }
+      h->ffma_ks_force = (int32_t)value;
+      return KGE_OK;
+    case KGE_OPT_CAPTURE_NEG:
+      if (value != 0 && value != 1) { set_error("KGE_OPT_CAPTURE_NEG must be 0 or 1"); return KGE_EINVAL; }
+      if (value && !h->fdbg_buf) {
+        h->fdbg_buf = (float*)dalloc(h, (size_t)h->dims.B * h->dims.k * 4);
+        if (!h->fdbg_buf) { set_error("out of device memory (capture buffer)"); return KGE_ENOMEM; }
+        CK(cudaMemsetAsync(h->fdbg_buf, 0xFF, (size_t)h->dims.B * h->dims.k * 4, h->stream));  // NaN until written
+      }
+      h->buf.fdbg = value ? h->fdbg_buf : nullptr;
+      return KGE_OK;
+    case KGE_OPT_BARRIER_MS:
+      if (value <= 0) { set_error("KGE_OPT_BARRIER_MS must be > 0"); return KGE_EINVAL; }
+      h->barrier_ns = value * 1000000ll;
+      return KGE_OK;
+  }
+  set_error("unknown option");
+  return KGE_EINVAL;
+}
+
+int kge_debug_neg_scores(kge_handle* h, float* out) {
+  if (!h || !out) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (!h->buf.fdbg) { set_error("negative-score capture is off (KGE_OPT_CAPTURE_NEG)"); return KGE_ESTATE; }
+  CK(cudaMemcpyAsync(out, h->buf.fdbg, (size_t)h->dims.B * h->dims.k * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return KGE_OK;
+}
 
 int kge_debug_trace(kge_handle* h, uint64_t* out, int64_t n) {
   if (!h || !out) { set_error("NULL argument"); return KGE_EINVAL; }

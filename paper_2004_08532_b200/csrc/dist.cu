@@ -14,8 +14,8 @@
 //     barrier the owner pulls the gradients of its rows from every rank (k_owner_collect), sums them in rank order and
 //     applies one Adagrad step per row (k_owner_update) -- the union-batch semantics of reading c.13;
 //   * split relations: per-rank sums in GrelSplit, pulled and summed in rank order by every replica (k_split_rel).
-// Device barriers (k_barrier: release/acquire flags at system scope in every peer) order the phases; a protocol bug
-// traps after ~2 s instead of hanging.
+// Device barriers (k_barrier: release/acquire flags at system scope in every peer) order the phases; a missing peer
+// raises an error flag after KGE_OPT_BARRIER_MS instead of hanging.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -92,7 +92,16 @@ struct PeerFlags {
   uint64_t* f[kMaxRanks];  // rank q's flag array (P entries, one per writer)
 };
 
-__global__ void k_barrier(PeerFlags pf, int P, int rank, uint64_t epoch) {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Device barrier of the P ranks. A rank that waits longer than timeout_ns (KGE_OPT_BARRIER_MS, default 2 min: a
+// peer's host may be checkpointing or evaluating) leaves the spin and raises flags[1]; the next synchronising call
+// reports it (KGE_ECUDA) -- a missing peer is an error, never a trapped context or an endless hang.
+__global__ void k_barrier(PeerFlags pf, int P, int rank, uint64_t epoch, uint64_t timeout_ns, int32_t* flags) {
   const int q = threadIdx.x;
   if (q < P) {
     __threadfence_system();
@@ -100,9 +109,13 @@ __global__ void k_barrier(PeerFlags pf, int P, int rank, uint64_t epoch) {
   }
   __syncthreads();
   if (q < P) {
-    const long long t0 = clock64();
+    const uint64_t t0 = globaltimer_ns();
     while (ld_acquire_sys(pf.f[rank] + q) < epoch) {
-      if (clock64() - t0 > 4000000000ll) __trap();  // a missing peer is an error, not a hang
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicExch(flags + 1, 1);
+        break;
+      }
+      __nanosleep(64);
     }
   }
   __syncthreads();
@@ -111,8 +124,8 @@ __global__ void k_barrier(PeerFlags pf, int P, int rank, uint64_t epoch) {
 struct OwnerArgs {
   Slot peer[kMaxRanks];         // every rank's sample slot of this step (peer pointers)
   const float* gu[kMaxRanks];   // every rank's per-unique gradient rows [n_occ x d]
-  const int32_t* lossflag[kMaxRanks];  // every rank's flags array ([1] = this step non-finite)
-  int32_t P, rank, n_occ, d;
+  const int32_t* lossflag[kMaxRanks];  // every rank's flags array ([2 + step parity] = this step non-finite)
+  int32_t P, rank, n_occ, d, par;  // par: this step's parity
   float lr, eps;
   int32_t* mark;     // [rows_local] slot of a touched local row, -1 otherwise
   int32_t* contrib;  // [P*n_occ x P] index of the row in rank w's unique list, -1 if absent
@@ -151,7 +164,7 @@ __global__ void __launch_bounds__(256) k_owner_update(OwnerArgs a) {
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (s >= *a.n_slots) return;
   bool skip = false;  // a non-finite loss on any rank skips the step's update everywhere
-  for (int w = 0; w < a.P; ++w) skip |= a.lossflag[w][1] != 0;
+  for (int w = 0; w < a.P; ++w) skip |= a.lossflag[w][2 + a.par] != 0;
   const int32_t l = a.slot_row[s];
   const int d = a.d, d4 = d >> 2;
   float* row = a.ent + (int64_t)l * d;
@@ -200,7 +213,7 @@ struct SplitArgs {
   const float* gs[kMaxRanks];          // every rank's GrelSplit [n_split x drel]
   const int32_t* lossflag[kMaxRanks];
   const int32_t* split_list;           // [n_split] relation ids
-  int32_t P, n_split, w;
+  int32_t P, n_split, w, par;
   float lr, eps;
   float* rel;
   float* rel_st;
@@ -212,7 +225,7 @@ __global__ void __launch_bounds__(256) k_split_rel(SplitArgs a) {
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (s >= a.n_split) return;
   for (int w = 0; w < a.P; ++w)
-    if (a.lossflag[w][1]) return;
+    if (a.lossflag[w][2 + a.par]) return;
   const int wd = a.w;
   float sq = 0.f;
   float* row = a.rel + (int64_t)a.split_list[s] * wd;
@@ -254,7 +267,7 @@ cudaError_t dist_preload() {  // see step_preload (lazy loading vs spinning barr
 
 cudaError_t dist_barrier(kge_handle* h) {
   ++h->dist.epoch;
-  k_barrier<<<1, 32, 0, h->stream>>>(peer_flags(h), h->P, h->rank, h->dist.epoch);
+  k_barrier<<<1, 32, 0, h->stream>>>(peer_flags(h), h->P, h->rank, h->dist.epoch, (uint64_t)h->barrier_ns, h->buf.flags);
   ++h->launches;
   return cudaGetLastError();
 }
@@ -269,7 +282,7 @@ static Slot peer_slot(const kge_handle* h, const Slot& mine, int q) {
   return s;
 }
 
-cudaError_t dist_exchange_update(kge_handle* h, const Slot& s) {
+cudaError_t dist_exchange_update(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
   Dist& D = h->dist;
   cudaError_t e = dist_barrier(h);  // B2: every rank's Gu / GrelSplit / sample slot is complete
@@ -285,6 +298,7 @@ cudaError_t dist_exchange_update(kge_handle* h, const Slot& s) {
   oa.rank = h->rank;
   oa.n_occ = dm.n_occ;
   oa.d = dm.d;
+  oa.par = (int32_t)(step & 1);
   oa.lr = dm.lr;
   oa.eps = dm.eps;
   oa.mark = D.mark;
@@ -309,6 +323,7 @@ cudaError_t dist_exchange_update(kge_handle* h, const Slot& s) {
     sa.P = h->P;
     sa.n_split = D.n_split;
     sa.w = dm.drel;
+    sa.par = (int32_t)(step & 1);
     sa.lr = dm.lr;
     sa.eps = dm.eps;
     sa.rel = h->rel;

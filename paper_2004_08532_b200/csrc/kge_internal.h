@@ -105,7 +105,9 @@ struct StepBuffers {
   uint32_t* flow;  // [2 C] dataflow counters of the tcgen05 path: [c] rows of chunk c gathered, [C + c] forward CTAs of
                    // chunk c done -- k_tc_fwd / k_tc_bwd start a chunk on these instead of waiting for the whole
                    // predecessor grid; k_update resets them for the next step
-  int32_t* flags;  // [4]: [0] non-finite seen
+  int32_t* flags;  // [4]: [0] non-finite seen, [1] device barrier timed out (P > 1), [2 + step parity] this step's
+                   // loss is non-finite (its update is skipped)
+  float* fdbg;     // [B x k] captured negative pair scores (KGE_OPT_CAPTURE_NEG), or nullptr
 };
 
 // TransR scratch (transr.cu)
@@ -207,6 +209,9 @@ struct kge_handle {
   float4* ffma_part = nullptr;
   int32_t* ffma_cnt = nullptr;
   int32_t ffma_ks_max = 1;  // the split factor the scratch was sized for
+  int32_t ffma_ks_force = 0;  // KGE_OPT_FFMA_SPLITK (0 = automatic)
+  float* fdbg_buf = nullptr;  // KGE_OPT_CAPTURE_NEG target, allocated on first use; buf.fdbg points here when on
+  int64_t barrier_ns = 120000000000ll;  // KGE_OPT_BARRIER_MS
   const kge::Slot* next_slot = nullptr;  // device slot of the step after the one being enqueued (row prefetch)
   cudaEvent_t ev_samp[2] = {}, ev_free[2] = {};
   int64_t half_first[2] = {-1, -1};  // first step held by each ring half (-1: none)
@@ -343,7 +348,7 @@ int64_t rank_list(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, int32_
 cudaError_t dist_barrier(kge_handle* h);
 cudaError_t dist_preload();
 cudaError_t step_preload();
-cudaError_t dist_exchange_update(kge_handle* h, const Slot& s);
+cudaError_t dist_exchange_update(kge_handle* h, const Slot& s, int64_t step);
 
 // tc.cu
 bool tc_init(kge_handle* h);

@@ -643,6 +643,7 @@ __global__ void __launch_bounds__(256, 2) k_neg_fwd(NegArgs a) {
           coef = -dLdf;
         }
         a.b.W[((int64_t)c * dm.g + i) * dm.kp + j] = coef;
+        if (a.b.fdbg) a.b.fdbg[((int64_t)c * dm.g + i) * dm.k + j] = f;  // KGE_OPT_CAPTURE_NEG
         lsum += -log_sigmoid(-f);
       }
     }
@@ -1281,7 +1282,8 @@ static void launch_neg(kge_handle* h, const NegArgs& na0) {
   na.cnt = h->ffma_cnt;
   const int kend = FAM == FAM_CMOD ? dm.d / 2 : dm.d, kstep = FAM == FAM_CMOD ? TK / 2 : TK;
   dim3 gf((dm.k + TN - 1) / TN, (dm.g + TM - 1) / TM, dm.C);
-  na.ks = std::min(ffma_splits(gf.x * gf.y * gf.z, (kend + kstep - 1) / kstep), h->ffma_ks_max);
+  na.ks = std::min(h->ffma_ks_force ? h->ffma_ks_force : ffma_splits(gf.x * gf.y * gf.z, (kend + kstep - 1) / kstep),
+                   h->ffma_ks_max);
   gf.z *= na.ks;
   launch_begin(h, KGE_K_NEG_FWD);
   launch_pdl(k_neg_fwd<FAM>, gf, 256, 0, h->stream, na);
@@ -1289,7 +1291,9 @@ static void launch_neg(kge_handle* h, const NegArgs& na0) {
   const int cols_per_tile = FAM == FAM_CMOD ? TN / 2 : TN;
   const int ncols = FAM == FAM_CMOD ? dm.d / 2 : dm.d;
   dim3 gb((ncols + cols_per_tile - 1) / cols_per_tile, (std::max(dm.g, dm.k) + TM - 1) / TM, 2 * dm.C);
-  na.ks = std::min(ffma_splits(gb.x * gb.y * gb.z, (std::min(dm.g, dm.k) + TK - 1) / TK), h->ffma_ks_max);
+  na.ks = std::min(h->ffma_ks_force ? h->ffma_ks_force
+                                   : ffma_splits(gb.x * gb.y * gb.z, (std::min(dm.g, dm.k) + TK - 1) / TK),
+                   h->ffma_ks_max);
   gb.z *= na.ks;
   launch_begin(h, KGE_K_NEG_BWD);
   launch_pdl(k_neg_bwd<FAM>, gb, 256, 0, h->stream, na);

@@ -87,6 +87,7 @@ struct TcArgs {
   uint32_t* flow;  // dataflow counters (StepBuffers::flow)
   int32_t fwd_per_chunk;  // forward CTAs per chunk (the backward's target on flow[C + c])
   int32_t fwd_cx;  // forward cluster size along x: the CTAs of one 128-positive tile share its O tile by TMA multicast
+  float* fdbg;     // KGE_OPT_CAPTURE_NEG: [B x k] negative pair scores, or nullptr
 };
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -276,6 +277,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         rD = fminf(rsqrtf(D2), 1e12f);
         f = dm.gamma - D2 * rD;
       }
+      if (a.fdbg) a.fdbg[((int64_t)c * dm.g + i) * dm.k + j] = f;
       // e = exp(-|f|): sigma(f) = f>=0 ? 1/(1+e) : e/(1+e);  -log sigma(-f) = max(f,0) + log1p(e). Three MUFU ops
       // per element (rsqrt, ex2, rcp): the log1p terms are summed as one log of their product (each factor in (1, 2],
       // 8 factors: no overflow; relative error ~8 ulp of the product, far inside the TC path's 2e-3)
@@ -796,7 +798,7 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
            h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128,
            tc_fuses_chain(h) ? 1 : 0, s, h->rows, h->buf.wpos, h->buf.pstat, h->buf.lpos, h->buf.Grel,
            h->buf.loss, h->buf.flags, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->xbuf, tc_flow() ? h->buf.flow : nullptr,
-           2 * ((dm.k + kNT - 1) / kNT) * ((dm.g + 127) / 128), st->fwd_cx};
+           2 * ((dm.k + kNT - 1) / kNT) * ((dm.g + 127) / 128), st->fwd_cx, h->buf.fdbg};
   dim3 gf(2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128, dm.C);  // x = 2 tile + split-K half
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(2 * tiles * kNSplit, dm.C, 2);  // x = 2 (row tile * kNSplit + column part) + split-K half

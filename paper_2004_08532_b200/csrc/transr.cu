@@ -558,6 +558,7 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
             s2 = fmaf(u, u, s2);
           }
           const float f = dm.gamma - s2;
+          if (a.b.fdbg) a.b.fdbg[(int64_t)a.s.rel_occ[rb + rr] * k + j0 + jj] = f;  // KGE_OPT_CAPTURE_NEG
           coef = -2.f * sigmoid(f) * inv_bk;  // dL/df * df/d(s2)
           lsum += -log_sigmoid(-f);
         }

@@ -28,6 +28,7 @@ PRECISION = {"fp32": 0, "tf32": 1}
 STATUS = {0: "KGE_OK", -1: "KGE_EINVAL", -2: "KGE_ERANGE", -3: "KGE_ENOMEM", -4: "KGE_ECUDA", -5: "KGE_ENCCL",
           -6: "KGE_ENONFINITE", -7: "KGE_ESTATE", -8: "KGE_EUNSUPPORTED"}
 KERNELS = ["k_sample", "k_gather", "k_neg_fwd", "k_neg_bwd", "k_chain", "k_update"]
+OPTIONS = {"ffma_splitk": 0, "capture_neg": 1, "barrier_ms": 2}  # kge_set_option (include/kge.h)
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
@@ -102,6 +103,8 @@ def lib():
         L.kge_relation_owner.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         L.kge_relation_owner.restype = ctypes.c_int
         L.kge_last_error.restype = ctypes.c_char_p
+        L.kge_set_option.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64]
+        L.kge_debug_neg_scores.argtypes = [ctypes.c_void_p, _fp]
         L.kge_kernel_name.argtypes = [ctypes.c_int32]
         L.kge_kernel_name.restype = ctypes.c_char_p
         _lib = L
@@ -265,9 +268,21 @@ class Handle:
         """Link-prediction ranks (PAPER.md:652-665 [5.3]) of the true tail (head=True: head). candidates / filters:
         None or a CSR pair (offsets[n+1], ids) -- see kge_rank in include/kge.h."""
         hs, rs, ts = _i64(hs), _i64(rs), _i64(ts)
+        if not (len(hs) == len(rs) == len(ts)):
+            raise ValueError("hs, rs, ts must have the same length")
         out = np.zeros(len(hs), np.int64)
         co, ci = (None, None) if candidates is None else (_i64(candidates[0]), _i64(candidates[1]))
         fo, fi = (None, None) if filters is None else (_i64(filters[0]), _i64(filters[1]))
+        for name, off, ids in (("candidates", co, ci), ("filters", fo, fi)):
+            # CSR size contract of kge_rank: offsets[n + 1] from 0, non-decreasing, ids[offsets[-1]]
+            if off is None:
+                continue
+            if off.ndim != 1 or len(off) != len(hs) + 1:
+                raise ValueError(f"{name}: offsets must have n + 1 = {len(hs) + 1} entries, got {off.shape}")
+            if off[0] != 0 or np.any(np.diff(off) < 0):
+                raise ValueError(f"{name}: offsets must start at 0 and be non-decreasing")
+            if len(ids) < off[-1]:
+                raise ValueError(f"{name}: {len(ids)} ids but offsets end at {off[-1]}")
         p = lambda a: None if a is None else _ptr(a, ctypes.c_int64)
         _check(lib().kge_rank(self._h, p(hs), p(rs), p(ts), len(hs), 1 if head else 0, p(co), p(ci), p(fo), p(fi),
                               p(out)))
@@ -279,6 +294,17 @@ class Handle:
         out = np.zeros(len(hs), np.float32)
         _check(lib().kge_score(self._h, _ptr(hs, ctypes.c_int64), _ptr(rs, ctypes.c_int64), _ptr(ts, ctypes.c_int64),
                                len(hs), _ptr(out, ctypes.c_float)))
+        return out
+
+    # kge_set_option
+    def set_option(self, name, value):
+        _check(lib().kge_set_option(self._h, OPTIONS[name] if isinstance(name, str) else name, int(value)))
+
+    # kge_debug_neg_scores: [B, k] negative pair scores of the last captured step
+    def neg_scores(self):
+        c = self.cfg
+        out = np.zeros((c.batch_size, c.neg_k), np.float32)
+        _check(lib().kge_debug_neg_scores(self._h, _ptr(out, ctypes.c_float)))
         return out
 
     def width(self, table):

@@ -28,7 +28,7 @@ def test_config_default():
     from paper_2004_08532_b200 import kge
     c = kge._Config()
     kge.lib().kge_config_default(ctypes.byref(c))
-    assert c.abi_version == 2 and c.neg_deg_k == 0 and c.dim == 400 and c.batch_size == 1024 and c.chunk_size == 256 and c.neg_k == 256
+    assert c.abi_version == 3 and c.neg_deg_k == 0 and c.neg_local == 0 and c.dim == 400 and c.batch_size == 1024 and c.chunk_size == 256 and c.neg_k == 256
 
 
 def _init_rc(**kw):
@@ -53,6 +53,8 @@ def _init_rc(**kw):
     (dict(abi_version=7), -1),
     (dict(n_entities=1 << 31), -2),            # ids must fit int32 on the device
     (dict(batch_size=8192, chunk_size=8, neg_k=256), -1),  # single-CTA dedup bound
+    (dict(neg_local=2), -1),                   # a flag: 0 or 1 (ABI 3)
+    (dict(neg_local=1, world_size=4, rank=0, n_entities=3), -1),  # local shards must be non-empty
 ])
 def test_validation_before_device(kw, code):
     rc, msg = _init_rc(**kw)
