@@ -144,6 +144,37 @@ def cpu_baseline(args, wl, budget_s=20.0):
             "steps": steps, "seconds": t_total}
 
 
+def spot_check(H, gr, wl, args):
+    """Oracle spot check after the timed region (outside it): the next step of the GPU run is replayed by the CPU
+    oracle teacher-forced -- the rows and Adagrad states that step touches are copied from the GPU into a lazily
+    materialised double oracle at the same step index, both run one step, and the loss and every updated row are
+    compared (bars of reading c.14 for the path's precision)."""
+    import oracle as O
+    gname, model, d, B, g, k = wl
+    try:
+        s = H.step
+        smp = H.sample(s)
+        ue, ur = smp["uniq_ent"], smp["uniq_rel"]
+        orc = O.Trainer(model, gr.n_entities, gr.n_relations, d, B, g, k, gamma=12.0, lr=0.1, seed=1, graph=gr,
+                        lazy_rows=True)
+        tabs = [(0, ue), (3, ue), (1, ur), (4, ur)] + ([(2, ur), (5, ur)] if model == "transr" else [])
+        for tab, ids in tabs:
+            orc.set_rows(tab, ids, H.get_rows(tab, ids).astype(np.float64))
+        orc.set_step(s)
+        t0 = time.perf_counter()
+        lo = float(orc.train(1)[0])
+        t_orc = time.perf_counter() - t0
+        lg = float(H.train_step(1)[0])
+        dE = float(np.abs(H.get_rows(0, ue) - orc.get_rows(0, ue)).max())
+        dR = float(np.abs(H.get_rows(1, ur) - orc.get_rows(1, ur)).max())
+        tol_l, tol_r = (1e-5, 1e-4) if args.precision == "fp32" else (2e-3, 5e-3)
+        rel = abs(lg - lo) / abs(lo)
+        return {"step": int(s), "loss_gpu": lg, "loss_oracle": lo, "loss_rel_err": rel, "rows_max_abs_err": max(dE, dR),
+                "pass": bool(rel <= tol_l and max(dE, dR) <= tol_r), "bars": [tol_l, tol_r], "oracle_s": t_orc}
+    except Exception as ex:  # context only; never fail the bench on it
+        return {"error": str(ex)}
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -165,7 +196,9 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=4000)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps; default: one full epoch of this rank's triples for the Freebase workload "
+                         "(SURVEY 8(d): ceil(N_loc / B) steps, 330,651 at N=1), 4000 otherwise")
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--workload", default="freebase", choices=sorted(WORKLOADS))
     ap.add_argument("--model", default=None)
@@ -188,6 +221,9 @@ def main():
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
         sys.exit(subprocess.call(cmd))
+    epoch_mode = args.steps is None and args.workload == "freebase"
+    if args.steps is None:
+        args.steps = 4000
     wl = list(WORKLOADS[args.workload])
     if args.model:
         wl[1] = args.model
@@ -229,8 +265,17 @@ def main():
     torch.cuda.synchronize()
     t_init = time.perf_counter() - t0
 
+    n_loc = gr.n_triples if ws == 1 else len(kge.partition(r_, gr.n_relations, ws, rank))
+    if epoch_mode:  # one full epoch of this rank's triple list (max over ranks: every rank runs the same step count)
+        ep = -(-n_loc // B)
+        if pg:
+            t = torch.tensor([ep], device="cuda" if pg.get_backend() == "nccl" else "cpu")
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            ep = int(t.item())
+        args.steps = ep
     H.train_step(args.warmup, return_loss=False)
     H.sync()
+    loss_warm = H.read_losses(max(0, args.warmup - 8), min(8, args.warmup))
 
     # ---- timed region: K steps, device-timed with CUDA events; barrier + sync on both sides ----
     if pg:
@@ -248,6 +293,8 @@ def main():
         wall = time.perf_counter() - w0
     ms_dev = e0.elapsed_time(e1)
     gpu_launches = H.launch_count - launches0
+    loss_end = H.read_losses(H.step - 64, 64)
+    spot = spot_check(H, gr, wl, args) if (rank == 0 and ws == 1 and not args.no_cpu_baseline) else None
     ms = max(ms_dev, 0.0)
     if pg:
         t = torch.tensor([ms], device="cuda" if pg.get_backend() == "nccl" else "cpu")
@@ -258,7 +305,7 @@ def main():
     # ---- roofline: per-kernel CUDA-event times over a K-step region (profiler on: each kernel bracketed by events on
     # its stream, programmatic dependent launch off so a kernel's time is its own, not the wait for its predecessor) ----
     H.profile_begin()
-    H.train_step(args.steps, return_loss=False)
+    H.train_step(min(args.steps, 4000), return_loss=False)
     prof2 = H.profile_end()
     s = H.sample(H.step)
     n_ue, n_ur = len(s["uniq_ent"]), len(s["uniq_rel"])
@@ -299,7 +346,7 @@ def main():
     roof["share_of_step"] = prof2[dominant][0] * prof2[dominant][1] / tot
     roof["per_kernel_ms"] = {k_: v[0] for k_, v in prof2.items()}
     roof["peak_source"] = src
-    roof["timing"] = ("CUDA events around every launch on its stream over a separate K-step region, programmatic "
+    roof["timing"] = ("CUDA events around every launch on its stream over a separate region of min(K, 4000) steps, programmatic "
                       "dependent launch off (isolated kernel times); traffic from the committed ncu capture")
     roof["kernels"] = {kn: kernel_roof(kn, v[0]) for kn, v in step_kernels.items() if kernel_roof(kn, v[0])}
     # whole step against the HBM roofline of the method's algorithmic bytes (gather + update rows)
@@ -359,6 +406,9 @@ def main():
                                                        "exchange over NVLink peer memory)" if ws > 1 else ""),
                            "l2": "inputs larger than L2 (entity table >> 126 MB)" if gr.n_entities * d * 4 > 2e9
                            else "tables L2-resident (no flush)"},
+                "epoch": {"full_epoch": epoch_mode, "triples_per_rank": n_loc, "steps": args.steps,
+                          "seconds": ms / 1000.0, "loss_after_warmup": float(np.mean(loss_warm)),
+                          "loss_last64_mean": float(np.mean(loss_end)), "spot_check": spot},
                 "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks,
                 "wall_s_timed": wall, "setup": {"graph_gen_s": t_gen, "init_s": t_init},
                 "uniq_rows_per_step": {"entity": n_ue, "relation": n_ur}}

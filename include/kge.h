@@ -64,7 +64,9 @@ typedef enum {
 typedef enum { KGE_CORRUPT_TAIL = 0, KGE_CORRUPT_HEAD = 1, KGE_CORRUPT_ALTERNATE = 2 } kge_corrupt;
 
 /* Arithmetic of the chunked negative contraction. FP32 = FFMA (all models; the parity path);
- * TF32 = tcgen05 tensor cores with TMEM accumulators (DistMult, ComplEx, TransE-L2 via ||o||^2 - 2 o.x + ||x||^2). */
+ * TF32 = tcgen05 tensor cores with TMEM accumulators (DistMult, ComplEx, and TransE-L2 / Table-1 RotatE via
+ * ||o - x||^2 = ||o||^2 - 2 o.x + ||x||^2; TransR projections); TransE-L1 and the RotatE modulus variant are not
+ * contractions and run FFMA at either setting (kge_neg_path reports which path a handle took). */
 typedef enum { KGE_PREC_FP32 = 0, KGE_PREC_TF32 = 1 } kge_precision;
 
 typedef struct {
@@ -169,6 +171,12 @@ int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t*
 int kge_get_rows(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, float* out);
 int kge_set_rows(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, const float* in);
 int32_t kge_table_width(const kge_handle* h, int32_t table);
+
+/* Arithmetic the chunked negative contraction of this handle runs in: KGE_PATH_FFMA (FP32 FFMA
+ * tiles: the FP32 precision, and TransE-L1 / the RotatE modulus variant at any precision), KGE_PATH_TF32 (tcgen05
+ * kind::tf32 with TMEM accumulators: DistMult, ComplEx, TransE-L2, Table-1 RotatE, TransR projections). -1 for NULL. */
+enum { KGE_PATH_FFMA = 0, KGE_PATH_TF32 = 1 };
+int32_t kge_neg_path(const kge_handle* h);
 
 /* Next step index (steps are counter-based: (seed, step) fixes every sample, so resume is exact). */
 int64_t kge_step(const kge_handle* h);

@@ -31,7 +31,8 @@ class Config(ctypes.Structure):
                 ("gamma", ctypes.c_float), ("lr", ctypes.c_float), ("eps", ctypes.c_float),
                 ("init_bound", ctypes.c_float), ("seed", ctypes.c_uint64), ("corrupt", ctypes.c_int32),
                 ("rotate_variant", ctypes.c_int32), ("world_size", ctypes.c_int32), ("lazy_rows", ctypes.c_int32),
-                ("lag", ctypes.c_int32), ("neg_deg_k", ctypes.c_int32), ("neg_local", ctypes.c_int32)]
+                ("lag", ctypes.c_int32), ("neg_deg_k", ctypes.c_int32), ("neg_local", ctypes.c_int32),
+                ("loss", ctypes.c_int32)]
 
 
 TRIPLE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, _i64p, _i64p, _i64p)
@@ -72,6 +73,8 @@ def lib():
         L.orc_logistic_loss.argtypes = [_dp, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                         _dp, _dp]
         L.orc_logistic_loss.restype = ctypes.c_double
+        L.orc_ranking_loss.argtypes = [_dp, _dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, _dp, _dp]
+        L.orc_ranking_loss.restype = ctypes.c_double
         L.orc_adagrad.argtypes = [_dp, _dp, _dp, ctypes.c_int32, ctypes.c_double, ctypes.c_double]
         L.orc_dedup.argtypes = [_i64p, ctypes.c_int64, _i64p, P(ctypes.c_int32), _i64p, _i64p]
         L.orc_dedup.restype = ctypes.c_int64
@@ -87,6 +90,7 @@ def lib():
         L.orc_score_triples.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, _dp]
         L.orc_next_step.argtypes = [ctypes.c_void_p]
         L.orc_next_step.restype = ctypes.c_int64
+        L.orc_set_step.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         L.orc_table_width.argtypes = [ctypes.c_void_p, ctypes.c_int32]
         L.orc_table_width.restype = ctypes.c_int32
         _lib = L
@@ -178,6 +182,19 @@ def logistic_loss(pos, neg, B, k):
     return L, dpos, dneg
 
 
+def ranking_loss(pos, neg, k, gamma):
+    """c.9' pairwise ranking loss: pos[B], neg[B*k] (row i = positive i's negatives)."""
+    pos, neg = d64(pos), d64(neg)
+    B = len(pos)
+    dpos, dneg = np.zeros_like(pos), np.zeros_like(neg)
+    dp = lambda a: _p(a, ctypes.c_double)
+    L = lib().orc_ranking_loss(dp(pos), dp(neg), B, k, float(gamma), dp(dpos), dp(dneg))
+    return L, dpos, dneg
+
+
+LOSSES = {"logistic": 0, "pairwise": 1}
+
+
 def adagrad(row, state, g, lr, eps=1e-10):
     row, g = d64(row).copy(), d64(g)
     st = np.array([state], dtype=np.float64)
@@ -218,13 +235,13 @@ class Trainer:
 
     def __init__(self, model, n_entities, n_relations, dim, batch, chunk, neg_k, gamma=12.0, lr=0.1, eps=1e-10,
                  init_bound=0.0, seed=1, corrupt=ALTERNATE, rotate_variant=0, world_size=1, precision=0,
-                 triples=None, graph=None, lazy_rows=False, lag=0, neg_deg_k=0, neg_local=0):
+                 triples=None, graph=None, lazy_rows=False, lag=0, neg_deg_k=0, neg_local=0, loss="logistic"):
         if isinstance(model, str):
             model = MODEL_IDS[model]
         self.model = model
         self.cfg = Config(model, precision, n_entities, n_relations, dim, batch, chunk, neg_k, gamma, lr, eps,
                           init_bound, seed, corrupt, rotate_variant, world_size, int(lazy_rows), int(lag),
-                          int(neg_deg_k), int(neg_local))
+                          int(neg_deg_k), int(neg_local), LOSSES[loss] if isinstance(loss, str) else int(loss))
         self._keep = []
         if triples is not None:
             h, r, t = [np.ascontiguousarray(a, dtype=np.int64) for a in triples]
@@ -304,6 +321,10 @@ class Trainer:
     @property
     def step(self):
         return lib().orc_next_step(self.h)
+
+    def set_step(self, s):
+        """Continue from step s (sampling is a pure function of (seed, step))."""
+        lib().orc_set_step(self.h, int(s))
 
 
 def link_rank(trainer, hs, rs, ts, head=False, candidates=None, known=None):

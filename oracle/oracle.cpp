@@ -328,6 +328,30 @@ T sigmoid(T x) {
   return e / (T(1) + e);
 }
 
+// c.9' pairwise ranking loss (PAPER.md:247-249 [2]): minimize sum over positives and their negatives of
+// max(0, gamma - f(h,r,t) + f(h',r',t')). The negatives of positive i are its chunk's k joint negatives (PAPER.md:
+// 417-422); the sum is normalised by the B*k pairs like the negative term of c.9 (the scale is irrelevant under
+// Adagrad up to eps). A hinge exactly at 0 contributes subgradient 0. fneg: [B x k], row i = positive i.
+template <typename T>
+T ranking_loss(const T* fpos, const T* fneg, int64_t B, int64_t k, T gamma, T* dpos, T* dneg) {
+  T ln = 0;
+  const T inv = T(1) / ((T)B * (T)k);
+  for (int64_t i = 0; i < B; ++i) {
+    int64_t active = 0;
+    for (int64_t j = 0; j < k; ++j) {
+      const T m = gamma - fpos[i] + fneg[i * k + j];
+      const bool on = m > T(0);
+      if (on) {
+        ln += m;
+        ++active;
+      }
+      if (dneg) dneg[i * k + j] = on ? inv : T(0);
+    }
+    if (dpos) dpos[i] = -(T)active * inv;
+  }
+  return ln * inv;
+}
+
 // ------------------------------------------------------------------------------------------------
 // Row stores. Dense, or lazily materialised from the init law (c.6) on first touch.
 // ------------------------------------------------------------------------------------------------
@@ -593,17 +617,20 @@ struct Trainer : Base {
                                                                   : score_ids(x, rr[(size_t)i], tt[(size_t)i]);
           }
         }
-        // logistic loss, c.9 normalisation
-        T lp = 0, ln = 0;
-        for (int32_t i = 0; i < B; ++i) {
-          lp += log_sigmoid(fpos[(size_t)i]);
-          dpos[(size_t)i] = -sigmoid(-fpos[(size_t)i]) / (T)B;
+        if (cfg.loss == ORC_LOSS_PAIRWISE) {  // pairwise ranking loss, reading c.9'
+          loss_total += ranking_loss<T>(fpos.data(), fneg.data(), B, k, (T)cfg.gamma, dpos.data(), dneg.data());
+        } else {  // logistic loss, c.9 normalisation
+          T lp = 0, ln = 0;
+          for (int32_t i = 0; i < B; ++i) {
+            lp += log_sigmoid(fpos[(size_t)i]);
+            dpos[(size_t)i] = -sigmoid(-fpos[(size_t)i]) / (T)B;
+          }
+          for (int64_t q = 0; q < (int64_t)B * k; ++q) {
+            ln += log_sigmoid(-fneg[(size_t)q]);
+            dneg[(size_t)q] = sigmoid(fneg[(size_t)q]) / ((T)B * (T)k);
+          }
+          loss_total += -lp / (T)B - ln / ((T)B * (T)k);
         }
-        for (int64_t q = 0; q < (int64_t)B * k; ++q) {
-          ln += log_sigmoid(-fneg[(size_t)q]);
-          dneg[(size_t)q] = sigmoid(fneg[(size_t)q]) / ((T)B * (T)k);
-        }
-        loss_total += -lp / (T)B - ln / ((T)B * (T)k);
         // backward: per-occurrence gradients (c.10); positive term first, then j = 0..k-1
         T* G = &Gent[(size_t)w * n_occ * d];
         T* GR = &Grel[(size_t)w * B * drel];
@@ -877,6 +904,10 @@ void orc_score_group(int32_t model, int32_t variant, double gamma, int32_t d, in
     for (int32_t j = 0; j < k; ++j) out[(size_t)i * k + j] = pair_score(model, variant, gamma, d, o.data(), X + (size_t)j * d, Mi);
   }
 }
+double orc_ranking_loss(const double* pos, const double* neg, int64_t B, int64_t k, double gamma, double* dpos,
+                        double* dneg) {
+  return ranking_loss<double>(pos, neg, B, k, gamma, dpos, dneg);
+}
 double orc_logistic_loss(const double* pos, int64_t n_pos, const double* neg, int64_t n_neg, int64_t B, int64_t k,
                          double* dpos, double* dneg) {
   double lp = 0, ln = 0;
@@ -981,6 +1012,8 @@ int orc_score_triples(void* h, const int64_t* hs, const int64_t* rs, const int64
   return static_cast<Base*>(h)->score_triples(hs, rs, ts, n, out);
 }
 int64_t orc_next_step(void* h) { return static_cast<Base*>(h)->step; }
+// continue from step s (counter-based sampling: (seed, s) fixes the sample; teacher-forced spot checks)
+void orc_set_step(void* h, int64_t s) { static_cast<Base*>(h)->step = s; }
 int32_t orc_table_width(void* h, int32_t table) { return static_cast<Base*>(h)->width(table); }
 
 }  // extern "C"

@@ -15,7 +15,8 @@
  *   - Table-1 score functions (PAPER.md:216-237 [2], Table 1) and their hand-derived gradients (c.10)
  *   - chunk decomposition o = combine(h, r) (PAPER.md:429-435 [3.3]) -- used only to pin that it
  *     equals the naive per-triple definition, which is what the step uses (c.8)
- *   - logistic loss (PAPER.md:239-246 [2], eq. at; normalisation c.9)
+ *   - logistic loss (PAPER.md:239-246 [2], eq. at; normalisation c.9) and pairwise ranking loss
+ *     (PAPER.md:247-249 [2]; reading c.9': mean over the B*k (positive, its chunk's negative) pairs)
  *   - sparse row-wise Adagrad after dedup-sum (c.11; PAPER.md:336-338 [3.1] "apply an optimization
  *     algorithm")
  *   - greedy relation partitioning with heavy-relation split (c.13; PAPER.md:484-495 [3.4])
@@ -50,7 +51,9 @@ typedef struct {
                                the rest uniform; 0 = all uniform */
   int32_t neg_local;        /* 1: uniform negatives of rank w are drawn from its own entity shard {e : e mod P == w}
                                ("local" negatives; no remote rows for them) */
+  int32_t loss;             /* ORC_LOSS_LOGISTIC (c.9) or ORC_LOSS_PAIRWISE (c.9') */
 } orc_config;
+enum { ORC_LOSS_LOGISTIC = 0, ORC_LOSS_PAIRWISE = 1 };
 
 typedef void (*orc_triple_fn)(void* ctx, int64_t i, int64_t* h, int64_t* r, int64_t* t);
 
@@ -82,6 +85,11 @@ void orc_score_grad(int32_t model, int32_t variant, double gamma, int32_t d, con
 void orc_score_group(int32_t model, int32_t variant, double gamma, int32_t d, int32_t mode, int32_t g, int32_t k,
                      const double* H, const double* R, const double* T, const double* M, const double* X,
                      double* out);
+/* c.9' pairwise ranking loss: L = (1/(B k)) sum_i sum_j max(0, gamma - f+_i + f-_ij) over
+ * pos[B] and neg[B*k] (row i = the negatives paired with positive i); dpos[B], dneg[B*k] = dL/df (hinge at 0:
+ * subgradient 0). Returns L. */
+double orc_ranking_loss(const double* pos, const double* neg, int64_t B, int64_t k, double gamma, double* dpos,
+                        double* dneg);
 double orc_logistic_loss(const double* pos, int64_t n_pos, const double* neg, int64_t n_neg, int64_t B, int64_t k,
                          double* dpos, double* dneg);
 void orc_adagrad(double* row, double* state, const double* g, int32_t w, double lr, double eps);
@@ -103,6 +111,7 @@ int orc_get_rows(void* h, int32_t table, const int64_t* ids, int64_t n, double* 
 int orc_set_rows(void* h, int32_t table, const int64_t* ids, int64_t n, const double* in);
 int orc_score_triples(void* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, double* out);
 int64_t orc_next_step(void* h);
+void orc_set_step(void* h, int64_t s);
 int32_t orc_table_width(void* h, int32_t table);
 
 #ifdef __cplusplus

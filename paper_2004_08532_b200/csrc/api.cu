@@ -1130,6 +1130,12 @@ int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t*
 
 int64_t kge_step(const kge_handle* h) { return h ? h->step : -1; }
 
+int32_t kge_neg_path(const kge_handle* h) {
+  if (!h) return -1;
+  if (h->dims.model == KGE_TRANSR) return h->tr_tc ? KGE_PATH_TF32 : KGE_PATH_FFMA;
+  return tc_supported(h) ? KGE_PATH_TF32 : KGE_PATH_FFMA;
+}
+
 int kge_read_losses(kge_handle* h, int64_t first_step, int64_t n, float* out) {
   if (!h || (n > 0 && !out)) { set_error("NULL argument"); return KGE_EINVAL; }
   if (first_step < 0 || first_step + n > h->step || first_step < h->step - h->ring) {

@@ -1332,13 +1332,19 @@ cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
   return cudaGetLastError();
 }
 
+// KGE_NO_PREFETCH=1: k_update does not warm L2 / the TLBs with the next step's entity rows (experiments)
+static bool no_row_prefetch() {
+  static const bool off = getenv("KGE_NO_PREFETCH") != nullptr;
+  return off;
+}
+
 cudaError_t launch_update_range(kge_handle* h, const Slot& s, int lo, int hi, cudaStream_t st, float* gocc) {
   const Dims& dm = h->dims;
   StepBuffers b = h->buf;
   b.Gocc = gocc;
   UpdateArgs ua{dm, s, h->ent, h->ent_st, h->rel, h->rel_st, b, h->P > 1 ? h->dist.gu : nullptr,
                 h->P > 1 ? h->dist.split_index : nullptr, h->dist.grel_split, h->seg_cnt, lo, hi,
-                lo == 0 && h->P == 1 ? h->next_slot : nullptr};
+                lo == 0 && h->P == 1 && !no_row_prefetch() ? h->next_slot : nullptr};
   const int wpc = row_warps();
   const int grid = (hi - lo + wpc - 1) / wpc;
   if (grid <= 0) return cudaSuccess;

@@ -90,6 +90,11 @@ struct TcArgs {
   float* fdbg;     // KGE_OPT_CAPTURE_NEG: [B x k] negative pair scores, or nullptr
 };
 
+// families scored through the expansion ||o - x||^2 = ||o||^2 - 2 o.x + ||x||^2 (reading c.8): TransE-L2 (f = gamma -
+// sqrt) and the Table-1 squared RotatE (f = gamma - ||o - x||^2 on the [re | im] rows, o = h e^{i theta} / t e^{-i theta})
+template <int FAM>
+__host__ __device__ constexpr bool expands() { return FAM == FAM_L2 || FAM == FAM_L2SQ; }
+
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
 }
@@ -212,10 +217,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int lg = warp & 3, hf = warp >> 2;
   const int rl = lg * 32 + lane, i = i0 + rl;
   const bool iok = i < dm.g;
-  const float on = iok && FAM == FAM_L2 ? a.onorm[(int64_t)c * dm.g + i] : 0.f;  // loaded while the MMAs run
+  const float on = iok && expands<FAM>() ? a.onorm[(int64_t)c * dm.g + i] : 0.f;  // loaded while the MMAs run
   if (threadIdx.x < kHalf) {
     const int jj = jf0 + threadIdx.x;
-    s_xn[threadIdx.x] = FAM == FAM_L2 && jj < dm.k ? a.xnorm[(int64_t)c * dm.k + jj] : 0.f;
+    s_xn[threadIdx.x] = expands<FAM>() && jj < dm.k ? a.xnorm[(int64_t)c * dm.k + jj] : 0.f;
   }
   mbar_wait(&done, 0);
   tc_fence_after();
@@ -272,10 +277,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       float f, rD = 1.f;
       if (FAM == FAM_DOT) {
         f = v[jj];
-      } else {  // TransE-L2 by expansion, clamped at 0 before the root (reading c.8)
+      } else if (FAM == FAM_L2) {  // TransE-L2 by expansion, clamped at 0 before the root (reading c.8)
         const float D2 = fmaxf(on - 2.f * v[jj] + s_xn[hf * 8 + jj], 0.f);
         rD = fminf(rsqrtf(D2), 1e12f);
         f = dm.gamma - D2 * rD;
+      } else {  // RotatE (Table 1, squared) by expansion: f = gamma - D^2, df/do = -2 (o - x)
+        const float D2 = fmaxf(on - 2.f * v[jj] + s_xn[hf * 8 + jj], 0.f);
+        rD = 2.f;
+        f = dm.gamma - D2;
       }
       if (a.fdbg) a.fdbg[((int64_t)c * dm.g + i) * dm.k + j] = f;
       // e = exp(-|f|): sigma(f) = f>=0 ? 1/(1+e) : e/(1+e);  -log sigma(-f) = max(f,0) + log1p(e). Three MUFU ops
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (jf0 + hf * 8 + jj < dm.k) wrow[jj] = v[jj];
     }
   }
-  if (FAM == FAM_L2) {
+  if (expands<FAM>()) {
     s_rs[hf][rl] = rsum;
     // column sums over this warp's 32 rows for its 8 columns: transposing butterfly (fixed order) over the low 3
     // lane bits, then the four 8-lane groups are added; lane l (< 8) ends with column l
@@ -329,7 +338,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (lane == 0) s_red[warp] = lsum;
   tc_fence_before();
   __syncthreads();
-  if (FAM == FAM_L2) {
+  if (expands<FAM>()) {
     if (threadIdx.x < 128 && i0 + (int)threadIdx.x < dm.g)  // one row-sum partial per (row, half tile): 16 columns
       a.rowsum_part[((int64_t)c * dm.g + i0 + threadIdx.x) * a.nrp + blockIdx.x] =
           s_rs[0][threadIdx.x] + s_rs[1][threadIdx.x];
@@ -437,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto prologue = [&]() {
 #pragma unroll
     for (int q = 0; q < 4; ++q) cpart[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (FAM == FAM_L2 && rok && bok) {
+    if (expands<FAM>() && rok && bok) {
       const int np = pass_x ? a.ncp : a.nrp;
       const float* pp = pass_x ? a.colsum_part + ((int64_t)c * dm.k + r) * a.ncp
                                : a.rowsum_part + ((int64_t)c * dm.g + r) * a.nrp;
@@ -501,8 +510,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (q == 0) {
       fence_proxy_async_global();  // the forward's W (acquired by thread 0 before the barrier) is read by TMA
       produce(kBwdStages);
-      if (FAM == FAM_L2) {
-        const bool fz = a.fuse && !pass_x;
+      if (expands<FAM>()) {
+        const bool fz = FAM == FAM_L2 && a.fuse && !pass_x;
         mbar_arrive_expect_tx(&selfbar, (fz ? 8 : 4) * 8192);
         tma_load_4d(self_smem, pass_x ? &mX_E : &mO_E, &selfbar, 0, r0 + rfin0, b0, c);
         if (fz) {  // gx rows of the uncorrupted entities (written by k_gather): [4 col blocks][64 rows][128 B]
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (bok) {
     // correction factor: the rowsum / colsum partials of W added in a fixed order
     float corr = cpart[0].x;
-    if (FAM == FAM_L2 && (pass_x ? a.ncp : a.nrp) == 16) {
+    if (expands<FAM>() && (pass_x ? a.ncp : a.nrp) == 16) {
       corr = 0.f;
 #pragma unroll
       for (int q = 0; q < 4; ++q) corr = (((corr + cpart[q].x) + cpart[q].y) + cpart[q].z) + cpart[q].w;
@@ -599,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gdst[1] = a.Gocc + ((int64_t)(mode == 0 ? dm.B : 0) + pi) * d;
     gdst[2] = a.Grel + (int64_t)pi * dm.drel;
     const float rsign = mode == 0 ? 1.f : -1.f;
-    if (FAM == FAM_L2) mbar_wait(&selfbar, 0);
+    if (expands<FAM>()) mbar_wait(&selfbar, 0);
     if (rok) {
       const uint8_t* rowp = self_smem + b * 8192 + fr * 128;
 #pragma unroll
@@ -609,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float4 t0 = ks == 0 ? make_float4(po.x + pp.x, po.y + pp.y, po.z + pp.z, po.w + pp.w)
                             : make_float4(pp.x + po.x, pp.y + po.y, pp.z + po.z, pp.w + po.w);
         float4 t1, t2;
-        if (FAM == FAM_L2) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D)
+        if (expands<FAM>()) {  // dO = rowsum o - W X' ; dX' = colsum x' - W^T O  (coef = -dL/df / D | -2 dL/df)
           const float4 sv = *reinterpret_cast<const float4*>(rowp + ((u ^ (fr & 7)) << 4));
           t0 = make_float4(corr * sv.x - t0.x, corr * sv.y - t0.y, corr * sv.z - t0.z, corr * sv.w - t0.w);
           if (fuse) {
@@ -707,7 +716,9 @@ static size_t bwd_smem(int dp) {
 
 bool tc_init(kge_handle* h) {
   const Dims& dm = h->dims;
-  if (!(dm.family == FAM_DOT || dm.family == FAM_L2)) return false;
+  // DistMult / ComplEx (dot), TransE-L2 and the Table-1 squared RotatE (expansion); TransE-L1 and the RotatE
+  // modulus variant are not contractions and stay on the FFMA path (north_star)
+  if (!(dm.family == FAM_DOT || dm.family == FAM_L2 || (dm.family == FAM_L2SQ && dm.model == KGE_ROTATE))) return false;
   if (h->dp > 512 || bwd_smem(h->dp) > 227 * 1024 || (dm.dp / 32 + kNSplit - 1) / kNSplit > 4 || h->kp % 32)
     return false;
   TcState* st = new TcState();
@@ -740,15 +751,16 @@ bool tc_init(kge_handle* h) {
     return false;
   }
   cudaError_t e = cudaSuccess;
-  if (dm.family == FAM_DOT) {
-    e = cudaFuncSetAttribute(k_tc_fwd<FAM_DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem());
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_tc_bwd<FAM_DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_smem(h->dp));
-  } else {
-    e = cudaFuncSetAttribute(k_tc_fwd<FAM_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem());
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_tc_bwd<FAM_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_smem(h->dp));
-  }
+  auto attrs = [&](auto fwd, auto bwd) {
+    e = cudaFuncSetAttribute(fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_smem(h->dp));
+  };
+  if (dm.family == FAM_DOT)
+    attrs(k_tc_fwd<FAM_DOT>, k_tc_bwd<FAM_DOT>);
+  else if (dm.family == FAM_L2)
+    attrs(k_tc_fwd<FAM_L2>, k_tc_bwd<FAM_L2>);
+  else
+    attrs(k_tc_fwd<FAM_L2SQ>, k_tc_bwd<FAM_L2SQ>);
   if (e != cudaSuccess) {
     cudaGetLastError();
     delete st;
@@ -803,25 +815,21 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(2 * tiles * kNSplit, dm.C, 2);  // x = 2 (row tile * kNSplit + column part) + split-K half
   const bool odd = h->buf.Gocc != h->gocc2[0];  // lag = 1: odd steps write the second Gocc buffer
-  launch_begin(h, KGE_K_NEG_FWD);
-  if (dm.family == FAM_DOT)
-    launch_pdl_cluster(k_tc_fwd<FAM_DOT>, gf, kFwdThreads, fwd_smem(), h->stream, 2 * st->fwd_cx, st->mO_F, st->mX_F, a);
-  else
-    launch_pdl_cluster(k_tc_fwd<FAM_L2>, gf, kFwdThreads, fwd_smem(), h->stream, 2 * st->fwd_cx, st->mO_F, st->mX_F, a);
-  launch_end(h, KGE_K_NEG_FWD);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  launch_begin(h, KGE_K_NEG_BWD);
-  if (dm.family == FAM_DOT)
-    launch_pdl_cluster(k_tc_bwd<FAM_DOT>, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN,
-                       st->mO_MN, st->mO_E, st->mX_E, odd ? st->mG_S1 : st->mG_S, st->mR_S, st->mD_S,
-                       odd ? st->mG_L1 : st->mG_L, a);
-  else
-    launch_pdl_cluster(k_tc_bwd<FAM_L2>, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN,
-                       st->mO_MN, st->mO_E, st->mX_E, odd ? st->mG_S1 : st->mG_S, st->mR_S, st->mD_S,
-                       odd ? st->mG_L1 : st->mG_L, a);
-  launch_end(h, KGE_K_NEG_BWD);
-  return cudaGetLastError();
+  auto run = [&](auto fwd, auto bwd) -> cudaError_t {
+    launch_begin(h, KGE_K_NEG_FWD);
+    launch_pdl_cluster(fwd, gf, kFwdThreads, fwd_smem(), h->stream, 2 * st->fwd_cx, st->mO_F, st->mX_F, a);
+    launch_end(h, KGE_K_NEG_FWD);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    launch_begin(h, KGE_K_NEG_BWD);
+    launch_pdl_cluster(bwd, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN,
+                       st->mO_E, st->mX_E, odd ? st->mG_S1 : st->mG_S, st->mR_S, st->mD_S, odd ? st->mG_L1 : st->mG_L, a);
+    launch_end(h, KGE_K_NEG_BWD);
+    return cudaGetLastError();
+  };
+  if (dm.family == FAM_DOT) return run(k_tc_fwd<FAM_DOT>, k_tc_bwd<FAM_DOT>);
+  if (dm.family == FAM_L2) return run(k_tc_fwd<FAM_L2>, k_tc_bwd<FAM_L2>);
+  return run(k_tc_fwd<FAM_L2SQ>, k_tc_bwd<FAM_L2SQ>);
 }
 
 }  // namespace kge

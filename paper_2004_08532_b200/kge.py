@@ -91,6 +91,8 @@ def lib():
         L.kge_sync.argtypes = [ctypes.c_void_p]
         L.kge_profile_begin.argtypes = [ctypes.c_void_p]
         L.kge_profile_end.argtypes = [ctypes.c_void_p, ctypes.c_int32, P(ctypes.c_double), _i64p]
+        L.kge_neg_path.argtypes = [ctypes.c_void_p]
+        L.kge_neg_path.restype = ctypes.c_int32
         L.kge_launch_count.argtypes = [ctypes.c_void_p]
         L.kge_launch_count.restype = ctypes.c_int64
         L.kge_destroy.argtypes = [ctypes.c_void_p]
@@ -323,6 +325,11 @@ class Handle:
     @property
     def step(self):
         return lib().kge_step(self._h)
+
+    @property
+    def neg_path(self):
+        """Arithmetic of the negative contraction: "ffma" or "tf32" (tcgen05), see kge_neg_path."""
+        return {0: "ffma", 1: "tf32"}[lib().kge_neg_path(self._h)]
 
     def read_losses(self, first_step, n):
         out = np.zeros(n, np.float32)

@@ -245,7 +245,7 @@ def test_rows_roundtrip_and_range_errors():
 
 
 # ---------------------------------------------------------------- tcgen05 (TF32) path: <= 2e-3 relative
-TC_MODELS = ["transe_l2", "distmult", "complex"]
+TC_MODELS = ["transe_l2", "distmult", "complex", "rotate"]  # rotate: Table-1 squared, by the L2 expansion
 
 
 @pytest.mark.parametrize("model", TC_MODELS)
@@ -255,6 +255,7 @@ def test_tc_train_parity(model, shape):
     gr = synth.graph("tiny")
     trip = gr.triples()
     gpu, orc = _pair(model, gr.n_entities, gr.n_relations, trip, d, B, g, k, precision="tf32")
+    assert gpu.neg_path == "tf32"
     n = 30 if B >= 1024 else 100
     lg, lo = gpu.train_step(n), orc.train(n)
     rel = np.abs(lg - lo) / np.abs(lo)

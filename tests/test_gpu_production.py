@@ -112,11 +112,13 @@ def test_production_fp32_teacher_forced(graph, model, variant):
         print(f"TransE-L1 kink coordinates exempted over 5 steps: {exempt}")
 
 
-@pytest.mark.parametrize("model", ["transe_l2", "distmult", "complex"])
-def test_production_tf32_pair_scores(model):
+@pytest.mark.parametrize("graph,model", [("fb15k", "transe_l2"), ("fb15k", "distmult"), ("fb15k", "complex"),
+                                         ("wn18", "rotate")])
+def test_production_tf32_pair_scores(graph, model):
     # the tcgen05 forward's per-pair f- (TF32 operands, fp32 TMEM accumulators), element by element at configs[1] /
-    # configs[4]'s shape, on tables the oracle and the GPU share (teacher-forced)
-    gr, trip, gpu, orc = _pair("fb15k", model, 400, precision="tf32")
+    # [2] / [4]'s shape, on tables the oracle and the GPU share (teacher-forced)
+    gr, trip, gpu, orc = _pair(graph, model, 400, precision="tf32")
+    assert gpu.neg_path == "tf32"
     heads, rels, tails = (np.asarray(a) for a in trip)
     orc.train(3)  # move off the init so the scores are not all near the same value
     U.copy_tables(orc, gpu, model, gr.n_entities, gr.n_relations)

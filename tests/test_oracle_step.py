@@ -25,13 +25,16 @@ def _tables(tr, n_e, n_r, has_proj, d):
 
 @pytest.mark.parametrize("model", MODELS)
 @pytest.mark.parametrize("world", [1, 2])
-def test_step_equals_torch_autograd(model, world):
+@pytest.mark.parametrize("loss", ["logistic", "pairwise"])
+def test_step_equals_torch_autograd(model, world, loss):
     n_e, n_r, n_t, d, B, g, k = 8, 2, 40, 4, 4, 2, 2
     gamma, lr, eps = 3.0, 0.1, 1e-10
+    if loss == "pairwise":  # a margin that leaves some hinges active and some not at these init scales (checked in
+        gamma = float(np.float32(0.05))  # tests/test_oracle_ranking_loss.py; the config stores gamma as float)
     variant = 1 if model == "rotate" and world == 2 else 0
     trip = _tiny_triples(n_e, n_r, n_t, 3 + MODELS.index(model))
     tr = O.Trainer(model, n_e, n_r, d, B, g, k, gamma=gamma, lr=lr, eps=eps, seed=11, world_size=world,
-                   rotate_variant=variant, triples=trip)
+                   rotate_variant=variant, triples=trip, loss=loss)
     has_proj = model == "transr"
     E, R, Pj = _tables(tr, n_e, n_r, has_proj, d)
     SE, SR = torch.zeros(n_e, dtype=torch.float64), torch.zeros(n_r, dtype=torch.float64)
@@ -41,7 +44,7 @@ def test_step_equals_torch_autograd(model, world):
         E.requires_grad_(True); R.requires_grad_(True)
         if Pj is not None:
             Pj.requires_grad_(True)
-        L = TR.step_loss(model, E, R, Pj, samples, trip, B, g, k, gamma, variant)
+        L = TR.step_loss(model, E, R, Pj, samples, trip, B, g, k, gamma, variant, loss)
         L.backward()
         loss_o = tr.train(1)[0]
         assert abs(loss_o - L.item()) < (1e-12 if step == 0 else 1e-7)

@@ -31,8 +31,9 @@ def score(model, h, r, t, M=None, variant=0, gamma=0.0):
     raise ValueError(model)
 
 
-def step_loss(model, E, R, Pj, samples, triples, B, g, k, gamma, variant):
-    """samples: list over ranks of (pos_idx, neg, mode). Loss = sum over ranks of c.9 loss."""
+def step_loss(model, E, R, Pj, samples, triples, B, g, k, gamma, variant, loss="logistic"):
+    """samples: list over ranks of (pos_idx, neg, mode). Loss = sum over ranks of the c.9 logistic loss, or of the
+    c.9' pairwise ranking loss sum_i sum_j relu(gamma - f+_i + f-_ij) / (B k)."""
     h_all, r_all, t_all = triples
     total = 0.0
     for pos, neg, mode in samples:
@@ -54,6 +55,9 @@ def step_loss(model, E, R, Pj, samples, triples, B, g, k, gamma, variant):
                 f = score(model, E[x], R[rr[i]].expand(k, -1), E[tt[i]].expand(k, -1), Mi, variant, gamma)
             fneg.append(f)
         fneg = torch.stack(fneg)
+        if loss == "pairwise":
+            total = total + torch.relu(gamma - fpos[:, None] + fneg).sum() / (B * k)
+            continue
         lp = torch.nn.functional.logsigmoid(fpos).sum()
         ln = torch.nn.functional.logsigmoid(-fneg).sum()
         total = total - lp / B - ln / (B * k)
