@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define KGE_ABI_VERSION 3  /* 2: kge_config::neg_deg_k; 3: kge_config::neg_local (validated: 0 or 1) */
+#define KGE_ABI_VERSION 4  /* 2: kge_config::neg_deg_k; 3: kge_config::neg_local (validated: 0 or 1); 4: loss */
 
 typedef struct kge_handle kge_handle; /* opaque, library-owned */
 
@@ -69,6 +69,12 @@ typedef enum { KGE_CORRUPT_TAIL = 0, KGE_CORRUPT_HEAD = 1, KGE_CORRUPT_ALTERNATE
  * contractions and run FFMA at either setting (kge_neg_path reports which path a handle took). */
 typedef enum { KGE_PREC_FP32 = 0, KGE_PREC_TF32 = 1 } kge_precision;
 
+/* Loss (PAPER.md:239-249 [2], "two loss functions are commonly used"): LOGISTIC = sum log(1 + exp(-y f)) (L243;
+ * normalisation reading c.9: mean over positives + mean over negatives); PAIRWISE = the pairwise ranking loss
+ * sum max(0, gamma - f+ + f-) (L247-249; reading c.9': each positive paired with its chunk's k negatives, mean over
+ * the B*k pairs, hinge subgradient 0 at 0). */
+typedef enum { KGE_LOSS_LOGISTIC = 0, KGE_LOSS_PAIRWISE = 1 } kge_loss;
+
 typedef struct {
   int32_t abi_version;     /* = KGE_ABI_VERSION */
   int32_t model;           /* kge_model */
@@ -89,7 +95,10 @@ typedef struct {
   int32_t lag;             /* 0 = synchronous (reading c.12). 1 = the paper's overlap of the entity update with the next
                               mini-batch (PAPER.md:515-534 [3.5]) made deterministic: step s reads entity rows updated
                               by steps <= s-2 and relation rows by steps <= s-1; the entity update of the last step
-                              is held back until the next step or kge_flush. P > 1 or TransR -> KGE_EUNSUPPORTED. */
+                              is held back until the next step or kge_flush. With world_size > 1 the held-back part
+                              is the owner's Adagrad step of the exchanged entity gradients, run on an update stream
+                              while the next step computes (after every rank's entity reads of that step). TransR ->
+                              KGE_EUNSUPPORTED. */
   int32_t world_size;      /* P ranks (one process per GPU) */
   int32_t rank;            /* this rank */
   void* nccl_comm;         /* ncclComm_t shared with the caller, or NULL */
@@ -105,6 +114,7 @@ typedef struct {
   int32_t neg_local;       /* 1: with world_size > 1 the uniform negatives of rank w come from its own entity shard
                               {e : e mod P == w} (PAPER.md:451-456 [3.3] local negatives: no remote rows for them);
                               the draw of reading c.3 mapped to e = w + P * floor(u * n_w / 2^64). Default 0 */
+  int32_t loss;            /* a kge_loss value; default LOGISTIC */
 } kge_config;
 
 /* Fill *cfg with defaults (ABI version, TransE-L2, d=400, B=1024, g=256, k=256, gamma=12, lr=0.1, eps=1e-10,
@@ -181,7 +191,10 @@ int32_t kge_neg_path(const kge_handle* h);
 /* Next step index (steps are counter-based: (seed, step) fixes every sample, so resume is exact). */
 int64_t kge_step(const kge_handle* h);
 int kge_set_step(kge_handle* h, int64_t step);
-/* lag = 1: apply the held-back entity update of the last step now (no-op when none / lag = 0). kge_set_step flushes. */
+/* lag = 1: apply the held-back entity update of the last step now (no-op when none / lag = 0). kge_set_step flushes.
+ * One rank: kge_get_rows / kge_set_rows / kge_score / kge_rank flush implicitly. world_size > 1: collective (every rank
+ * calls it, like kge_train_step); reading or writing entity rows (tables 0, 3) or scoring while an update is held back
+ * returns KGE_ESTATE. */
 int kge_flush(kge_handle* h);
 
 /* Wait for all enqueued work; reports KGE_ENONFINITE if any step since the last check had a non-finite loss. */

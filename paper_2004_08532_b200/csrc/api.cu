@@ -119,17 +119,17 @@ static int validate(const kge_config* c) {
   if (c->lag != 0 && c->lag != 1) { set_error("lag must be 0 or 1"); return KGE_EINVAL; }
   if (c->neg_deg_k < 0 || c->neg_deg_k > c->neg_k) { set_error("neg_deg_k must be in [0, neg_k]"); return KGE_EINVAL; }
   if (c->neg_local != 0 && c->neg_local != 1) { set_error("neg_local must be 0 or 1"); return KGE_EINVAL; }
+  if (c->loss != KGE_LOSS_LOGISTIC && c->loss != KGE_LOSS_PAIRWISE) { set_error("bad loss"); return KGE_EINVAL; }
   if (c->neg_local && c->world_size > 1 && c->n_entities < c->world_size) {
     set_error("neg_local needs n_entities >= world_size (every shard non-empty)");
     return KGE_EINVAL;
   }
-  if (c->lag == 1 && (c->world_size > 1 || c->model == KGE_TRANSR)) {
-    set_error("lag = 1 is implemented for one rank and the non-TransR models");
+  if (c->lag == 1 && c->model == KGE_TRANSR) {
+    set_error("lag = 1 is implemented for the non-TransR models");
     return KGE_EUNSUPPORTED;
   }
   if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size) { set_error("bad world_size/rank"); return KGE_EINVAL; }
   if (c->world_size > kMaxRanks) { set_error("world_size > 8 (one node) not supported"); return KGE_EINVAL; }
-  if (c->world_size > 1 && c->model == KGE_TRANSR) { set_error("TransR with world_size > 1 is not built yet"); return KGE_EUNSUPPORTED; }
   if (c->model == KGE_TRANSR && c->dim > 512) { set_error("TransR supports dim <= 512"); return KGE_EINVAL; }
   return KGE_OK;
 }
@@ -234,6 +234,7 @@ void kge_config_default(kge_config* c) {
   c->lag = 0;
   c->neg_deg_k = 0;
   c->neg_local = 0;
+  c->loss = KGE_LOSS_LOGISTIC;
   c->world_size = 1;
   c->rank = 0;
 }
@@ -285,6 +286,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   dm.k = cfg->neg_k;
   dm.n_occ = 2 * dm.B + dm.C * dm.k;
   dm.gamma = cfg->gamma;
+  dm.loss = cfg->loss;
   dm.lr = cfg->lr;
   dm.eps = h->cfg.adagrad_eps;
   dm.n_entities = cfg->n_entities;
@@ -438,9 +440,11 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   int32_t* ring_base = nullptr;
   if (h->P > 1) {
     Dist& D = h->dist;
-    const size_t gu_bytes = ((size_t)dm.n_occ * dm.d * 4 + 255) & ~size_t(255);
+    const size_t gu_one = ((size_t)dm.n_occ * dm.d * 4 + 255) & ~size_t(255);
+    const size_t gu_bytes = gu_one * (cfg->lag == 1 ? 2 : 1);
     const size_t gs_bytes = ((size_t)std::max(1, D.n_split) * dm.drel * 4 + 255) & ~size_t(255);
-    D.shared_bytes = 256 + flags_bytes + ring_bytes + gu_bytes + gs_bytes;
+    const size_t gp_bytes = cfg->model == KGE_TRANSR ? (size_t)std::max(1, D.n_split) * dm.d * dm.d * 4 : 0;
+    D.shared_bytes = 256 + flags_bytes + ring_bytes + gu_bytes + gs_bytes + gp_bytes;
     char* sb = (char*)rawalloc(h, D.shared_bytes);
     if (!sb) { set_error("out of device memory (shared block)"); return fail(KGE_ENOMEM); }
     D.shared = sb;
@@ -448,7 +452,10 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     h->buf.flags = (int32_t*)(sb + 256);
     ring_base = (int32_t*)(sb + 256 + flags_bytes);
     D.gu = (float*)(sb + 256 + flags_bytes + ring_bytes);
+    D.gu_buf[0] = D.gu;
+    D.gu_buf[1] = cfg->lag == 1 ? (float*)(sb + 256 + flags_bytes + ring_bytes + gu_one) : D.gu;
     D.grel_split = (float*)(sb + 256 + flags_bytes + ring_bytes + gu_bytes);
+    if (gp_bytes) D.gproj_split = (float*)(sb + 256 + flags_bytes + ring_bytes + gu_bytes + gs_bytes);
     e = cudaMemset(sb, 0, D.shared_bytes);
     const size_t max_slots = (size_t)h->P * dm.n_occ;
     D.mark = (int32_t*)dalloc(h, (size_t)h->ent_rows * 4);
@@ -516,6 +523,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.wpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
+  b.pcnt = (int32_t*)dalloc(h, (size_t)dm.B * 4);
   b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(std::max<int64_t>(h->n_neg_parts, tc_parts), dm.B) * 4);
   b.flow = (uint32_t*)dalloc(h, (size_t)2 * dm.C * 4);
   {  // FFMA split-K scratch: tiles of the larger (backward) grid x up to 8 splits x 256 threads x 16 floats
@@ -650,10 +658,24 @@ static int enqueue_step(kge_handle* h, const Slot& slot, int64_t s, int gi) {
     h->buf.Gocc = h->gocc2[s & 1];
   }
   h->next_slot = gi >= 0 ? d_slots(h) + h->ring + 1 + (gi + 1) % kge_handle::kGiven : d_slots(h) + (s + 1) % h->ring;
+  if (h->P > 1) h->dist.gu = h->dist.gu_buf[h->cfg.lag == 1 ? (s & 1) : 0];
   if (e == cudaSuccess) e = launch_step(h, slot, s);
   if (e == cudaSuccess && h->P > 1) e = dist_exchange_update(h, slot, s);
   if (e != cudaSuccess) return cuda_fail(e, "step");
-  if (h->cfg.lag == 1) {
+  if (h->cfg.lag == 1 && h->P > 1) {
+    // the owner update of step s-1 (its per-unique sums were exchanged in step s-1) on the update stream, behind this
+    // step's last entity-table read and a barrier of every rank's (sequence 1); the next step's B1 waits for it
+    if (h->pend_step >= 0) {
+      e = cudaStreamWaitEvent(h->ustream, h->ev_eread, 0);
+      if (e == cudaSuccess) e = dist_owner_update_lagged(h, h->pend_slot, h->pend_step, h->ustream);
+      if (e == cudaSuccess) e = cudaEventRecord(h->ev_eupd, h->ustream);
+      if (e != cudaSuccess) return cuda_fail(e, "lagged owner update");
+      h->eupd_enqueued = true;
+    }
+    h->pend_step = s;
+    h->pend_slot = slot;
+    h->pend_gi = gi;
+  } else if (h->cfg.lag == 1) {
     if (h->pend_step >= 0) {
       const Dims& dm = h->dims;
       e = cudaStreamWaitEvent(h->ustream, h->ev_eread, 0);
@@ -685,7 +707,9 @@ int kge_flush(kge_handle* h) {
   int rc = join_updates(h);
   if (rc != KGE_OK || h->pend_step < 0) return rc;
   const Dims& dm = h->dims;
-  cudaError_t e = launch_update_range(h, h->pend_slot, dm.B, dm.B + dm.n_occ, h->stream, h->gocc2[h->pend_step & 1]);
+  cudaError_t e = h->P > 1 ? dist_owner_flush(h, h->pend_slot, h->pend_step)  // collective (every rank calls it)
+                           : launch_update_range(h, h->pend_slot, dm.B, dm.B + dm.n_occ, h->stream,
+                                                 h->gocc2[h->pend_step & 1]);
   if (e == cudaSuccess && h->pend_gi >= 0) e = cudaEventRecord(h->ev_gfree[h->pend_gi], h->stream);
   if (e != cudaSuccess) return cuda_fail(e, "flush");
   h->pend_step = -1;
@@ -701,10 +725,12 @@ int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
     const int64_t s = h->step;
     if (s >= (1ll << 32)) { set_error("step index exceeds 2^32 (one Philox counter word)"); return KGE_ERANGE; }
     if (h->P > 1) {
-      // B1: every owner has applied step s-1 before anyone gathers rows or overwrites a slot peers read
+      // B1: every owner has applied step s-1 (lag = 1: step s-2, joined from the update stream first) before anyone
+      // gathers rows or overwrites a slot peers read
+      const int rj = join_updates(h);
+      if (rj != KGE_OK) return rj;
       cudaError_t e = dist_barrier(h);
-      if (e == cudaSuccess && h->dist.n_split > 0)
-        e = cudaMemsetAsync(h->dist.grel_split, 0, (size_t)h->dist.n_split * h->dims.drel * 4, h->stream);
+      if (e == cudaSuccess) e = dist_clear_split(h);
       if (e != cudaSuccess) return cuda_fail(e, "barrier");
     }
     int rc = ensure_sampled(h, s);
@@ -871,9 +897,10 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
   }
   if (hprof) hpr.t2 = now();
   if (h->P > 1) {  // B1 (see kge_train_step); every rank must call kge_train_batch for this step
+    const int rj = join_updates(h);
+    if (rj != KGE_OK) return rj;
     e = dist_barrier(h);
-    if (e == cudaSuccess && h->dist.n_split > 0)
-      e = cudaMemsetAsync(h->dist.grel_split, 0, (size_t)h->dist.n_split * h->dims.drel * 4, h->stream);
+    if (e == cudaSuccess) e = dist_clear_split(h);
     if (e != cudaSuccess) return cuda_fail(e, "barrier");
   }
   if (use_graphs(h)) {
@@ -978,6 +1005,19 @@ int32_t kge_table_width(const kge_handle* h, int32_t table) {
   return p ? w : 0;
 }
 
+// Readers / writers of the tables (rows, scores, ranks, set_step) see every update: one rank applies a held-back
+// entity update itself; with P > 1 that update is collective, so the caller flushes on every rank first (KGE_ESTATE).
+static int flush_for_io(kge_handle* h, bool entity_tables) {
+  if (h->P == 1) return kge_flush(h);
+  const int rj = join_updates(h);
+  if (rj != KGE_OK) return rj;
+  if (entity_tables && h->pend_step >= 0) {
+    set_error("lag = 1 with world_size > 1: call kge_flush on every rank before reading or writing entity rows");
+    return KGE_ESTATE;
+  }
+  return KGE_OK;
+}
+
 static int rows_io(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, float* host, bool write) {
   if (!h || (n > 0 && (!ids || !host))) { set_error("NULL argument"); return KGE_EINVAL; }
   int32_t w;
@@ -986,7 +1026,7 @@ static int rows_io(kge_handle* h, int32_t table, const int64_t* ids, int64_t n, 
   if (!tab) { set_error("table not present for this model"); return KGE_EINVAL; }
   if (n == 0) return KGE_OK;
   // lag = 1: the held-back entity update belongs to the table the caller reads / overwrites
-  const int rj = kge_flush(h);
+  const int rj = flush_for_io(h, table == 0 || table == 3);
   if (rj != KGE_OK) return rj;
   std::vector<int32_t> ids32(n);
   const bool sharded = h->P > 1 && (table == 0 || table == 3);
@@ -1031,7 +1071,7 @@ int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t
     ids[n + i] = (int32_t)rs[i];
     ids[2 * n + i] = (int32_t)ts[i];
   }
-  const int rj = kge_flush(h);  // lag = 1: score the tables with every enqueued update applied
+  const int rj = flush_for_io(h, true);  // lag = 1: score the tables with every enqueued update applied
   if (rj != KGE_OK) return rj;
   int32_t* d_ids = nullptr;
   float* d_out = nullptr;

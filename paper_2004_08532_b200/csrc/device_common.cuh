@@ -148,4 +148,13 @@ __device__ __forceinline__ float sigmoid(float x) {
   return e / (1.f + e);
 }
 
+// Pairwise ranking loss (reading c.9'): the hinge m = gamma - f+ + f- of one (positive, negative)
+// pair; returns max(m, 0) and sets dL/df- = [m > 0] / (B k) (subgradient 0 at the hinge), act = [m > 0]
+__device__ __forceinline__ float hinge_term(float f, float fpos, float gamma, float inv_bk, float& dldf, int& act) {
+  const float m = gamma - fpos + f;
+  act = m > 0.f ? 1 : 0;
+  dldf = act ? inv_bk : 0.f;
+  return act ? m : 0.f;
+}
+
 }  // namespace kge

@@ -13,7 +13,11 @@
 //   * gradient return: each rank writes one segment-summed gradient per unique entity it touched (Gu); after a device
 //     barrier the owner pulls the gradients of its rows from every rank (k_owner_collect), sums them in rank order and
 //     applies one Adagrad step per row (k_owner_update) -- the union-batch semantics of reading c.13;
-//   * split relations: per-rank sums in GrelSplit, pulled and summed in rank order by every replica (k_split_rel).
+//   * split relations: per-rank sums in GrelSplit, pulled and summed in rank order by every replica (k_split_rel);
+//     TransR's projections M_r follow their relation: a non-split relation's M_r lives and is updated on its owner only
+//     ("store all relation embeddings on GPUs and update relation embeddings in GPUs locally ... the
+//     communication overhead drops from O(bd^2) to O(bd)"), a split relation's M_r is replicated and its rank sums are
+//     exchanged like its row (GprojSplit).
 // Device barriers (k_barrier: release/acquire flags at system scope in every peer) order the phases; a missing peer
 // raises an error flag after KGE_OPT_BARRIER_MS instead of hanging.
 #include <cuda_runtime.h>
@@ -265,12 +269,19 @@ cudaError_t dist_preload() {  // see step_preload (lazy loading vs spinning barr
   return e;
 }
 
-cudaError_t dist_barrier(kge_handle* h) {
-  ++h->dist.epoch;
-  k_barrier<<<1, 32, 0, h->stream>>>(peer_flags(h), h->P, h->rank, h->dist.epoch, (uint64_t)h->barrier_ns, h->buf.flags);
+// Barrier sequence `seq` (0: the step's main-stream barriers; 1: the lag = 1 update stream's) on stream st: each
+// sequence has its own per-writer epoch slots in every rank's flag block and its own epoch counter.
+static cudaError_t barrier_on(kge_handle* h, cudaStream_t st, int seq) {
+  uint64_t& ep = seq == 0 ? h->dist.epoch : h->dist.epoch_u;
+  ++ep;
+  PeerFlags pf = peer_flags(h);
+  for (int q = 0; q < h->P; ++q) pf.f[q] += seq * kMaxRanks;
+  k_barrier<<<1, 32, 0, st>>>(pf, h->P, h->rank, ep, (uint64_t)h->barrier_ns, h->buf.flags);
   ++h->launches;
   return cudaGetLastError();
 }
+
+cudaError_t dist_barrier(kge_handle* h) { return barrier_on(h, h->stream, 0); }
 
 // Slot with every pointer moved from my shared block to rank q's mapping of the same layout
 static Slot peer_slot(const kge_handle* h, const Slot& mine, int q) {
@@ -282,17 +293,31 @@ static Slot peer_slot(const kge_handle* h, const Slot& mine, int q) {
   return s;
 }
 
-cudaError_t dist_exchange_update(kge_handle* h, const Slot& s, int64_t step) {
+template <typename T>
+static T* peer_ptr(const kge_handle* h, T* mine, int q) {  // the same object in rank q's shared block
+  return (T*)((const char*)h->dist.peer_shared[q] + ((const char*)mine - (const char*)h->dist.shared));
+}
+
+cudaError_t dist_clear_split(kge_handle* h) {
+  const Dist& D = h->dist;
+  if (D.n_split == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(D.grel_split, 0, (size_t)D.n_split * h->dims.drel * 4, h->stream);
+  if (e == cudaSuccess && D.gproj_split)
+    e = cudaMemsetAsync(D.gproj_split, 0, (size_t)D.n_split * h->dims.d * h->dims.d * 4, h->stream);
+  return e;
+}
+
+// Owner side of the entity exchange for step `step` on stream st: pull every rank's per-unique gradient sums of the
+// rows this rank owns (gu: this rank's buffer of that step; peers' at the same offset), sum in rank order, one Adagrad
+// step per row (reading c.13).
+static cudaError_t owner_update(kge_handle* h, const Slot& s, int64_t step, float* gu, cudaStream_t st) {
   const Dims& dm = h->dims;
   Dist& D = h->dist;
-  cudaError_t e = dist_barrier(h);  // B2: every rank's Gu / GrelSplit / sample slot is complete
-  if (e != cudaSuccess) return e;
   OwnerArgs oa{};
-  const char* base = (const char*)D.shared;
   for (int q = 0; q < h->P; ++q) {
     oa.peer[q] = peer_slot(h, s, q);
-    oa.gu[q] = (const float*)((const char*)D.peer_shared[q] + ((const char*)D.gu - base));
-    oa.lossflag[q] = (const int32_t*)((const char*)D.peer_shared[q] + ((const char*)h->buf.flags - base));
+    oa.gu[q] = peer_ptr(h, gu, q);
+    oa.lossflag[q] = peer_ptr(h, h->buf.flags, q);
   }
   oa.P = h->P;
   oa.rank = h->rank;
@@ -307,33 +332,74 @@ cudaError_t dist_exchange_update(kge_handle* h, const Slot& s, int64_t step) {
   oa.n_slots = D.n_slots;
   oa.ent = h->ent;
   oa.ent_st = h->ent_st;
-  e = cudaMemsetAsync(D.n_slots, 0, 4, h->stream);
+  cudaError_t e = cudaMemsetAsync(D.n_slots, 0, 4, st);
   if (e != cudaSuccess) return e;
-  launch_begin(h, KGE_K_UPDATE);
-  k_owner_collect<<<dim3((dm.n_occ + 255) / 256, h->P), 256, 0, h->stream>>>(oa);
+  k_owner_collect<<<dim3((dm.n_occ + 255) / 256, h->P), 256, 0, st>>>(oa);
   const int max_slots = h->P * dm.n_occ;
-  k_owner_update<<<(max_slots + 7) / 8, 256, 0, h->stream>>>(oa);
-  if (D.n_split > 0) {
-    SplitArgs sa{};
-    for (int q = 0; q < h->P; ++q) {
-      sa.gs[q] = (const float*)((const char*)D.peer_shared[q] + ((const char*)D.grel_split - base));
-      sa.lossflag[q] = oa.lossflag[q];
-    }
-    sa.split_list = D.split_list;
-    sa.P = h->P;
-    sa.n_split = D.n_split;
-    sa.w = dm.drel;
-    sa.par = (int32_t)(step & 1);
-    sa.lr = dm.lr;
-    sa.eps = dm.eps;
-    sa.rel = h->rel;
-    sa.rel_st = h->rel_st;
+  k_owner_update<<<(max_slots + 7) / 8, 256, 0, st>>>(oa);
+  h->launches += 2;
+  return cudaGetLastError();
+}
+
+// split relations (and TransR's split projections): every replica applies the rank-ordered sum
+static cudaError_t split_update(kge_handle* h, int64_t step) {
+  const Dims& dm = h->dims;
+  Dist& D = h->dist;
+  if (D.n_split == 0) return cudaSuccess;
+  SplitArgs sa{};
+  for (int q = 0; q < h->P; ++q) {
+    sa.gs[q] = peer_ptr(h, D.grel_split, q);
+    sa.lossflag[q] = peer_ptr(h, h->buf.flags, q);
+  }
+  sa.split_list = D.split_list;
+  sa.P = h->P;
+  sa.n_split = D.n_split;
+  sa.w = dm.drel;
+  sa.par = (int32_t)(step & 1);
+  sa.lr = dm.lr;
+  sa.eps = dm.eps;
+  sa.rel = h->rel;
+  sa.rel_st = h->rel_st;
+  k_split_rel<<<(D.n_split + 7) / 8, 256, 0, h->stream>>>(sa);
+  ++h->launches;
+  if (D.gproj_split) {  // TransR: the split relations' projections M_r, replicated like their rows (w = d*d)
+    for (int q = 0; q < h->P; ++q) sa.gs[q] = peer_ptr(h, D.gproj_split, q);
+    sa.w = dm.d * dm.d;
+    sa.rel = h->proj;
+    sa.rel_st = h->proj_st;
     k_split_rel<<<(D.n_split + 7) / 8, 256, 0, h->stream>>>(sa);
     ++h->launches;
   }
-  launch_end(h, KGE_K_UPDATE);
-  h->launches += 2;
   return cudaGetLastError();
+}
+
+// After this rank's step kernels (lag = 0): B2, then the owner update of this step and the split relations.
+// lag = 1 (reading c.12 at P > 1): B2 and the split relations now (relations stay synchronous); the owner update of
+// this step's entity rows is held back -- dist_owner_update_lagged runs it during the next step.
+cudaError_t dist_exchange_update(kge_handle* h, const Slot& s, int64_t step) {
+  cudaError_t e = dist_barrier(h);  // B2: every rank's Gu / GrelSplit / sample slot is complete
+  if (e != cudaSuccess) return e;
+  launch_begin(h, KGE_K_UPDATE);
+  if (h->cfg.lag == 0) e = owner_update(h, s, step, h->dist.gu_buf[0], h->stream);
+  if (e == cudaSuccess) e = split_update(h, step);
+  launch_end(h, KGE_K_UPDATE);
+  return e;
+}
+
+// lag = 1, P > 1: the held-back owner update of step `step` on the update stream, once every rank has finished
+// reading entity rows for the step after it (barrier sequence 1 behind this rank's ev_eread): it overlaps the rest
+// of that step's forward / backward, and the next step's B1 waits for it (ev_eupd).
+cudaError_t dist_owner_update_lagged(kge_handle* h, const Slot& s, int64_t step, cudaStream_t st) {
+  cudaError_t e = barrier_on(h, st, 1);
+  if (e == cudaSuccess) e = owner_update(h, s, step, h->dist.gu_buf[step & 1], st);
+  return e;
+}
+
+// kge_flush at P > 1 (collective): the held-back owner update on the main stream after a barrier
+cudaError_t dist_owner_flush(kge_handle* h, const Slot& s, int64_t step) {
+  cudaError_t e = dist_barrier(h);
+  if (e == cudaSuccess) e = owner_update(h, s, step, h->dist.gu_buf[step & 1], h->stream);
+  return e;
 }
 
 }  // namespace kge

@@ -94,6 +94,8 @@ struct StepBuffers {
   float* wpos;     // [B] dL/df+
   float* lpos;     // [B] per-positive loss term
   float* pstat;    // [B] pair statistic of each positive (L2: squared distance)
+  int32_t* pcnt;   // [B] pairwise ranking loss: active hinges of positive i (integer atomics of the forward epilogues;
+                   // zeroed by the gather): dL/df+_i = -pcnt_i / (B k)
   float* lneg;     // [n_neg_parts] per-tile negative loss partials
   float* rowsumW;  // [B]
   float* colsumW;  // [C*k]
@@ -133,8 +135,11 @@ struct Dist {
   void* shared = nullptr;       // cudaMalloc'd block exported to peers: flags | ring | Gu | GrelSplit
   size_t shared_bytes = 0;
   uint64_t* flags = nullptr;    // [kMaxRanks] barrier epochs written by each rank
-  float* gu = nullptr;          // [n_occ x d] per-unique entity gradient sums of this step
+  float* gu = nullptr;          // [n_occ x d] per-unique entity gradient sums of the step being enqueued (= gu_buf[0],
+                                // or gu_buf[step & 1] with lag = 1: the owner update of step s-1 reads the other one)
+  float* gu_buf[2] = {};
   float* grel_split = nullptr;  // [n_split x drel]
+  float* gproj_split = nullptr; // TransR: [n_split x d*d] per-rank sums of the split relations' projection gradients
   int32_t n_split = 0;
   int32_t* split_list = nullptr;   // [n_split] device
   int32_t* split_index = nullptr;  // [n_relations] device, -1 if not split
@@ -148,13 +153,15 @@ struct Dist {
   uint64_t* peer_flags[kMaxRanks] = {};
   std::vector<void*> ipc_opened;
   std::vector<void*> raw_allocs;  // cudaMalloc'd (IPC-exportable) allocations
-  uint64_t epoch = 0;
+  uint64_t epoch = 0;            // barrier sequence 0 (main stream)
+  uint64_t epoch_u = 0;          // barrier sequence 1 (lag = 1 update stream)
   bool connected = false;
 };
 
 struct Dims {
   uint64_t* trace;  // diagnostics (KGE_TRACE=1 at init): per-kernel, per-CTA globaltimer stamps, else nullptr
   int32_t model, family, variant;
+  int32_t loss;  // kge_loss
   int32_t d, drel, B, g, C, k, n_occ;
   int32_t dp, kp;  // padded row pitch of O / X' (d + 2 rounded up to 32) and of W (k rounded up to 32)
   float gamma, lr, eps;
@@ -349,6 +356,9 @@ cudaError_t dist_barrier(kge_handle* h);
 cudaError_t dist_preload();
 cudaError_t step_preload();
 cudaError_t dist_exchange_update(kge_handle* h, const Slot& s, int64_t step);
+cudaError_t dist_clear_split(kge_handle* h);  // zero this rank's split-relation gradient sums before a step
+cudaError_t dist_owner_update_lagged(kge_handle* h, const Slot& s, int64_t step, cudaStream_t st);
+cudaError_t dist_owner_flush(kge_handle* h, const Slot& s, int64_t step);
 
 // tc.cu
 bool tc_init(kge_handle* h);

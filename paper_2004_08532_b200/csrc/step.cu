@@ -372,8 +372,14 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     if (lane == 0) {
       a.b.pstat[i] = stat;
       const float f = pair_score_from(dm.family, stat, dm.gamma);
-      a.b.wpos[i] = -sigmoid(-f) / (float)dm.B;  // dL/df+ (reading c.9)
-      a.b.lpos[i] = -log_sigmoid(f);
+      if (dm.loss == KGE_LOSS_PAIRWISE) {  // the positive's terms come from its hinges (forward epilogues, k_chain)
+        a.b.wpos[i] = 0.f;
+        a.b.lpos[i] = 0.f;
+        a.b.pcnt[i] = 0;
+      } else {
+        a.b.wpos[i] = -sigmoid(-f) / (float)dm.B;  // dL/df+ (reading c.9)
+        a.b.lpos[i] = -log_sigmoid(f);
+      }
       a.b.onorm[i] = on;
     }
   } else if (row < dm.B + n_neg) {
@@ -621,18 +627,28 @@ __global__ void __launch_bounds__(256, 2) k_neg_fwd(NegArgs a) {
   if (!splitk_reduce(acc, a.part, a.cnt, tile, ks, nks)) return;
   // epilogue: f-, dL/dS coefficient, loss partial
   const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
+  const bool pairwise = dm.loss == KGE_LOSS_PAIRWISE;
   float lsum = 0.f;
 #pragma unroll
   for (int ii = 0; ii < 4; ++ii) {
     const int i = i0 + ty * 4 + ii;
+    const float fpos = pairwise && i < dm.g ? pair_score_from(FAM, a.b.pstat[(int64_t)c * dm.g + i], dm.gamma) : 0.f;
+    int nact = 0;
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
       const int j = j0 + tx * 4 + jj;
       if (i < dm.g && j < dm.k) {
         const float st = acc[ii][jj];
-        float f, coef;
-        const float dLdf = sigmoid(pair_score_from(FAM, st, dm.gamma)) * inv_bk;
+        float f, coef, dLdf, lterm;
         f = pair_score_from(FAM, st, dm.gamma);
+        if (pairwise) {
+          int act;
+          lterm = hinge_term(f, fpos, dm.gamma, inv_bk, dLdf, act);
+          nact += act;
+        } else {
+          dLdf = sigmoid(f) * inv_bk;
+          lterm = -log_sigmoid(-f);
+        }
         if (FAM == FAM_DOT) {
           coef = dLdf;
         } else if (FAM == FAM_L2) {
@@ -644,9 +660,10 @@ __global__ void __launch_bounds__(256, 2) k_neg_fwd(NegArgs a) {
         }
         a.b.W[((int64_t)c * dm.g + i) * dm.kp + j] = coef;
         if (a.b.fdbg) a.b.fdbg[((int64_t)c * dm.g + i) * dm.k + j] = f;  // KGE_OPT_CAPTURE_NEG
-        lsum += -log_sigmoid(-f);
+        lsum += lterm;
       }
     }
+    if (nact) atomicAdd(&a.b.pcnt[(int64_t)c * dm.g + i], nact);  // integer: exact in any order
   }
   lsum = warp_sum(lsum);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lsum;
@@ -928,7 +945,9 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
   float* gR = a.b.Grel + (int64_t)i * dm.drel;
   float* gOther = mode == 0 ? gT : gH;
   float* gC = mode == 0 ? gH : gT;
-  const float wp = a.b.wpos[i];
+  // dL/df+: logistic from the gather; pairwise = -(active hinges of positive i) / (B k) (reading c.9')
+  const float wp = dm.loss == KGE_LOSS_PAIRWISE ? -(float)a.b.pcnt[i] * (1.f / ((float)dm.B * (float)dm.k))
+                                                : a.b.wpos[i];
   const float scale = dm.family == FAM_L2 ? wp / fmaxf(sqrtf(a.b.pstat[i]), 1e-12f) : wp;
   const int model = dm.model;
   if (!is_complex_model(model)) {
@@ -1369,7 +1388,10 @@ cudaError_t launch_update_range(kge_handle* h, const Slot& s, int lo, int hi, cu
 // (api.cu, reading c.12)
 cudaError_t launch_update(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
-  return launch_update_range(h, s, 0, h->cfg.lag == 1 ? dm.B : dm.B + dm.n_occ, h->stream, h->buf.Gocc);
+  // (P > 1: the entity positions only form this rank's per-unique sums here, which the exchange needs now; the owner's
+  // Adagrad step is what lag = 1 holds back, dist.cu)
+  return launch_update_range(h, s, 0, h->cfg.lag == 1 && h->P == 1 ? dm.B : dm.B + dm.n_occ, h->stream,
+                             h->buf.Gocc);
 }
 
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {

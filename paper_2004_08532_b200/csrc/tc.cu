@@ -88,7 +88,14 @@ struct TcArgs {
   int32_t fwd_per_chunk;  // forward CTAs per chunk (the backward's target on flow[C + c])
   int32_t fwd_cx;  // forward cluster size along x: the CTAs of one 128-positive tile share its O tile by TMA multicast
   float* fdbg;     // KGE_OPT_CAPTURE_NEG: [B x k] negative pair scores, or nullptr
+  int32_t* pcnt;   // pairwise ranking loss: active hinges per positive (StepBuffers::pcnt)
 };
+
+// f+ from the positive's pair statistic (k_gather's pstat), as the FFMA path's pair_score_from
+template <int FAM>
+__device__ __forceinline__ float pair_score_from_tc(float stat, float gamma) {
+  return FAM == FAM_DOT ? stat : (FAM == FAM_L2 ? gamma - sqrtf(stat) : gamma - stat);
+}
 
 // families scored through the expansion ||o - x||^2 = ||o||^2 - 2 o.x + ||x||^2 (reading c.8): TransE-L2 (f = gamma -
 // sqrt) and the Table-1 squared RotatE (f = gamma - ||o - x||^2 on the [re | im] rows, o = h e^{i theta} / t e^{-i theta})
@@ -218,6 +225,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int rl = lg * 32 + lane, i = i0 + rl;
   const bool iok = i < dm.g;
   const float on = iok && expands<FAM>() ? a.onorm[(int64_t)c * dm.g + i] : 0.f;  // loaded while the MMAs run
+  const bool pairwise = dm.loss == KGE_LOSS_PAIRWISE;
+  const float fpos = iok && pairwise ? pair_score_from_tc<FAM>(a.pstat[(int64_t)c * dm.g + i], dm.gamma) : 0.f;
   if (threadIdx.x < kHalf) {
     const int jj = jf0 + threadIdx.x;
     s_xn[threadIdx.x] = expands<FAM>() && jj < dm.k ? a.xnorm[(int64_t)c * dm.k + jj] : 0.f;
@@ -269,6 +278,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 3);
   const float inv_bk = a.inv_bk;
   float lsum = 0.f, rsum = 0.f, lprod = 1.f;
+  int nact = 0;
 #pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
     const int j = jf0 + hf * 8 + jj;
@@ -290,18 +300,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // e = exp(-|f|): sigma(f) = f>=0 ? 1/(1+e) : e/(1+e);  -log sigma(-f) = max(f,0) + log1p(e). Three MUFU ops
       // per element (rsqrt, ex2, rcp): the log1p terms are summed as one log of their product (each factor in (1, 2],
       // 8 factors: no overflow; relative error ~8 ulp of the product, far inside the TC path's 2e-3)
-      const float e = __expf(-fabsf(f));
-      float r1;
-      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(1.f + e));
-      lsum += fmaxf(f, 0.f);
-      lprod *= 1.f + e;
-      const float dLdf = (f >= 0.f ? r1 : e * r1) * inv_bk;
+      float dLdf;
+      if (pairwise) {  // reading c.9': hinge gamma - f+ + f-
+        int act;
+        lsum += hinge_term(f, fpos, dm.gamma, inv_bk, dLdf, act);
+        nact += act;
+      } else {
+        const float e = __expf(-fabsf(f));
+        float r1;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(1.f + e));
+        lsum += fmaxf(f, 0.f);
+        lprod *= 1.f + e;
+        dLdf = (f >= 0.f ? r1 : e * r1) * inv_bk;
+      }
       coef = FAM == FAM_DOT ? dLdf : -dLdf * rD;
     }
     v[jj] = coef;
     rsum += coef;
   }
   lsum += __logf(lprod);
+  if (nact) atomicAdd(&a.pcnt[(int64_t)c * dm.g + i], nact);  // integer: exact in any order
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 4);
   if (iok) {
     float* wrow = a.W + ((int64_t)c * dm.g + i) * a.kp + jf0 + hf * 8;
@@ -801,7 +819,11 @@ bool tc_flow() {
   return on;
 }
 
-bool tc_fuses_chain(const kge_handle* h) { return h->dims.model == KGE_TRANSE_L2; }
+// the positive's gradient is fused into the TransE-L2 backward under the logistic loss (dL/df+ known at the gather);
+// the pairwise loss needs the forward's hinge counts first, so it takes k_chain
+bool tc_fuses_chain(const kge_handle* h) {
+  return h->dims.model == KGE_TRANSE_L2 && h->dims.loss == KGE_LOSS_LOGISTIC;
+}
 
 cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
@@ -810,7 +832,7 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
            h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128,
            tc_fuses_chain(h) ? 1 : 0, s, h->rows, h->buf.wpos, h->buf.pstat, h->buf.lpos, h->buf.Grel,
            h->buf.loss, h->buf.flags, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->xbuf, tc_flow() ? h->buf.flow : nullptr,
-           2 * ((dm.k + kNT - 1) / kNT) * ((dm.g + 127) / 128), st->fwd_cx, h->buf.fdbg};
+           2 * ((dm.k + kNT - 1) / kNT) * ((dm.g + 127) / 128), st->fwd_cx, h->buf.fdbg, h->buf.pcnt};
   dim3 gf(2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128, dm.C);  // x = 2 tile + split-K half
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(2 * tiles * kNSplit, dm.C, 2);  // x = 2 (row tile * kNSplit + column part) + split-K half

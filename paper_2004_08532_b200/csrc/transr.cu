@@ -31,13 +31,15 @@ namespace kge {
 struct TrArgs {
   Dims dm;
   Slot s;
-  const float* ent;
+  EntRows ent;  // entity rows: the local table, or (P > 1) the owner's shard over peer memory
   const float* rel;
   float* proj;
   float* proj_st;
   StepBuffers b;
   TrBuffers t;
   int32_t n_neg_parts;
+  const int32_t* split_index;  // P > 1: relation -> index among split relations (-1 if not split), else nullptr
+  float* gproj_split;          // P > 1: this rank's sums of the split relations' M_r gradients
 };
 
 // ------------------------------------------------------------------------------------------------
@@ -131,8 +133,8 @@ __global__ void __launch_bounds__(256) k_tr_pos(TrArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, d = dm.d;
   const int r = a.s.pr[i], mode = a.s.mode[i / dm.g];
   const float* M = a.proj + (int64_t)r * d * d;
-  const float* hrow = a.ent + (int64_t)a.s.ph[i] * d;
-  const float* trow = a.ent + (int64_t)a.s.pt[i] * d;
+  const float* hrow = a.ent.row(a.s.ph[i]);
+  const float* trow = a.ent.row(a.s.pt[i]);
   const float* rv = a.rel + (int64_t)r * d;
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
     sh[e] = hrow[e];
@@ -171,8 +173,15 @@ __global__ void __launch_bounds__(256) k_tr_pos(TrArgs a) {
     float s = 0.f;
     for (int w = 0; w < 8; ++w) s += red[w];
     const float f = dm.gamma - s;
-    a.b.wpos[i] = -sigmoid(-f) / (float)dm.B;
-    a.b.lpos[i] = -log_sigmoid(f);
+    a.b.pstat[i] = s;
+    if (dm.loss == KGE_LOSS_PAIRWISE) {  // reading c.9': the positive's terms come from its hinges
+      a.b.wpos[i] = 0.f;
+      a.b.lpos[i] = 0.f;
+      a.b.pcnt[i] = 0;
+    } else {
+      a.b.wpos[i] = -sigmoid(-f) / (float)dm.B;
+      a.b.lpos[i] = -log_sigmoid(f);
+    }
   }
 }
 
@@ -558,9 +567,18 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
             s2 = fmaf(u, u, s2);
           }
           const float f = dm.gamma - s2;
-          if (a.b.fdbg) a.b.fdbg[(int64_t)a.s.rel_occ[rb + rr] * k + j0 + jj] = f;  // KGE_OPT_CAPTURE_NEG
-          coef = -2.f * sigmoid(f) * inv_bk;  // dL/df * df/d(s2)
-          lsum += -log_sigmoid(-f);
+          const int ip = a.s.rel_occ[rb + rr];  // the positive of this row
+          if (a.b.fdbg) a.b.fdbg[(int64_t)ip * k + j0 + jj] = f;  // KGE_OPT_CAPTURE_NEG
+          if (dm.loss == KGE_LOSS_PAIRWISE) {  // reading c.9'
+            float dldf;
+            int act;
+            lsum += hinge_term(f, dm.gamma - a.b.pstat[ip], dm.gamma, inv_bk, dldf, act);
+            if (act) atomicAdd(&a.b.pcnt[ip], 1);  // integer: exact in any order
+            coef = -2.f * dldf;
+          } else {
+            coef = -2.f * sigmoid(f) * inv_bk;  // dL/df * df/d(s2)
+            lsum += -log_sigmoid(-f);
+          }
         }
         scf[rr * JB + jj] = coef;
       }
@@ -646,14 +664,15 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
   float* sgt = sm + d;
   const int p = blockIdx.x, i = a.s.rel_occ[p];
   const int r = a.s.pr[i], mode = a.s.mode[i / dm.g];
-  const float w = a.b.wpos[i];
+  const float w = dm.loss == KGE_LOSS_PAIRWISE ? -(float)a.b.pcnt[i] * (1.f / ((float)dm.B * (float)dm.k))
+                                               : a.b.wpos[i];  // dL/df+ (reading c.9 / c.9')
   const float* pv = a.t.Pv + (int64_t)i * d;
   const float* dO = a.b.dO + (int64_t)i * d;
   float* gR = a.b.Grel + (int64_t)i * dm.drel;
   float* U = a.t.U + (int64_t)2 * p * d;
   float* H = a.t.H + (int64_t)2 * p * d;
-  const float* hrow = a.ent + (int64_t)a.s.ph[i] * d;
-  const float* trow = a.ent + (int64_t)a.s.pt[i] * d;
+  const float* hrow = a.ent.row(a.s.ph[i]);
+  const float* trow = a.ent.row(a.s.pt[i]);
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
     const float tp = 2.f * w * pv[e];
     const float gh = mode == 0 ? dO[e] - tp : -tp;
@@ -735,6 +754,12 @@ __global__ void __launch_bounds__(256) k_tr_proj(TrArgs a) {
   const int r = a.s.rel_uniq[u];
   const int64_t w = (int64_t)dm.d * dm.d;
   const float* G = a.t.dM + (int64_t)u * w;
+  const int sidx = a.split_index ? a.split_index[r] : -1;
+  if (sidx >= 0) {  // P > 1, split relation: this rank's sum; every replica applies the rank-ordered sum (dist.cu)
+    float* dst = a.gproj_split + (int64_t)sidx * w;
+    for (int64_t q = threadIdx.x; q < w; q += blockDim.x) dst[q] = G[q];
+    return;
+  }
   float sq = 0.f;
   for (int64_t q = threadIdx.x; q < w; q += blockDim.x) sq = fmaf(G[q], G[q], sq);
   sq = warp_sum(sq);
@@ -766,7 +791,8 @@ static void dbg(kge_handle* h, const char* what) {
 cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
   (void)step;
-  TrArgs a{dm, s, h->ent, h->rel, h->proj, h->proj_st, h->buf, h->tr_buf, dm.B};
+  TrArgs a{dm, s, h->rows, h->rel, h->proj, h->proj_st, h->buf, h->tr_buf, dm.B,
+           h->P > 1 ? h->dist.split_index : nullptr, h->dist.gproj_split};
   cudaError_t e;
   launch_begin(h, KGE_K_GATHER);
   k_tr_groups<<<1, 1024, 0, h->stream>>>(a); dbg(h, "k_tr_groups");
@@ -818,7 +844,7 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
 }
 
 // kge_score for TransR: f = gamma - ||M_r h + r - M_r t||^2 per triple (CTA per triple)
-__global__ void __launch_bounds__(256) k_tr_score_triples(Dims dm, const float* ent, const float* rel, const float* proj,
+__global__ void __launch_bounds__(256) k_tr_score_triples(Dims dm, EntRows ent, const float* rel, const float* proj,
                                                           const int32_t* hs, const int32_t* rs, const int32_t* ts,
                                                           float* out) {
   __shared__ float sh[512], st[512], red[8];
@@ -826,8 +852,8 @@ __global__ void __launch_bounds__(256) k_tr_score_triples(Dims dm, const float* 
   const float* M = proj + (int64_t)rs[i] * d * d;
   const float* rv = rel + (int64_t)rs[i] * d;
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
-    sh[e] = ent[(int64_t)hs[i] * d + e];
-    st[e] = ent[(int64_t)ts[i] * d + e];
+    sh[e] = ent.row(hs[i])[e];
+    st[e] = ent.row(ts[i])[e];
   }
   __syncthreads();
   float sq = 0.f;
@@ -857,7 +883,7 @@ cudaError_t launch_transr_score(kge_handle* h, const int32_t* hs, const int32_t*
                                 float* out) {
   for (int64_t b = 0; b < n; b += 65535) {
     const int64_t m = std::min<int64_t>(65535, n - b);
-    k_tr_score_triples<<<(unsigned)m, 256, 0, h->stream>>>(h->dims, h->ent, h->rel, h->proj, hs + b, rs + b, ts + b,
+    k_tr_score_triples<<<(unsigned)m, 256, 0, h->stream>>>(h->dims, h->rows, h->rel, h->proj, hs + b, rs + b, ts + b,
                                                            out + b);
     ++h->launches;
   }

@@ -25,6 +25,7 @@ os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 MODELS = {"transe_l1": 0, "transe_l2": 1, "distmult": 2, "complex": 3, "rotate": 4, "transr": 5}
 CORRUPT = {"tail": 0, "head": 1, "alternate": 2}
 PRECISION = {"fp32": 0, "tf32": 1}
+LOSS = {"logistic": 0, "pairwise": 1}
 STATUS = {0: "KGE_OK", -1: "KGE_EINVAL", -2: "KGE_ERANGE", -3: "KGE_ENOMEM", -4: "KGE_ECUDA", -5: "KGE_ENCCL",
           -6: "KGE_ENONFINITE", -7: "KGE_ESTATE", -8: "KGE_EUNSUPPORTED"}
 KERNELS = ["k_sample", "k_gather", "k_neg_fwd", "k_neg_bwd", "k_chain", "k_update"]
@@ -50,7 +51,7 @@ class _Config(ctypes.Structure):
                 ("lag", ctypes.c_int32), ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nccl_comm", ctypes.c_void_p), ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p),
                 ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
-                ("neg_deg_k", ctypes.c_int32), ("neg_local", ctypes.c_int32)]
+                ("neg_deg_k", ctypes.c_int32), ("neg_local", ctypes.c_int32), ("loss", ctypes.c_int32)]
 
 
 _lib = None
@@ -149,6 +150,7 @@ class Config:
     world_size: int = 1
     neg_deg_k: int = 0  # degree-based in-batch negatives per chunk
     neg_local: int = 0  # 1: local-shard negatives when world_size > 1
+    loss: str = "logistic"  # or "pairwise"
     rank: int = 0
 
     @property
@@ -392,6 +394,7 @@ def init(cfg: Config, heads, rels, tails, use_torch_allocator=True, stream=None)
     c.rotate_variant, c.lag, c.world_size, c.rank = cfg.rotate_variant, cfg.lag, cfg.world_size, cfg.rank
     c.neg_deg_k = cfg.neg_deg_k
     c.neg_local = cfg.neg_local
+    c.loss = LOSS[cfg.loss] if isinstance(cfg.loss, str) else cfg.loss
     dev = torch.cuda.current_device()
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     c.cuda_stream = s.cuda_stream

@@ -74,12 +74,12 @@ def dot_scale(model, orc, meta, g):
     return S
 
 
-def check_pair_scores(model, got, ref, meta, orc, g, rtol):
+def check_pair_scores(model, got, ref, meta, orc, g, rtol, gamma=GAMMA):
     """|f - f_ref| <= rtol * max(|f_ref|, S) element by element (reading c.14). Returns the worst ratio."""
     if model in ("distmult", "complex"):
         S = dot_scale(model, orc, meta, g)
     else:
-        S = GAMMA + np.abs(GAMMA - ref)
+        S = abs(gamma) + np.abs(gamma - ref)
     err = np.abs(got.astype(np.float64) - ref) / np.maximum(np.abs(ref), S)
     assert np.all(np.isfinite(got)), "captured scores contain non-finite values"
     return float(err.max())

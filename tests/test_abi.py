@@ -28,7 +28,7 @@ def test_config_default():
     from paper_2004_08532_b200 import kge
     c = kge._Config()
     kge.lib().kge_config_default(ctypes.byref(c))
-    assert c.abi_version == 3 and c.neg_deg_k == 0 and c.neg_local == 0 and c.dim == 400 and c.batch_size == 1024 and c.chunk_size == 256 and c.neg_k == 256
+    assert c.abi_version == 4 and c.neg_deg_k == 0 and c.neg_local == 0 and c.loss == 0 and c.dim == 400 and c.batch_size == 1024 and c.chunk_size == 256 and c.neg_k == 256
 
 
 def _init_rc(**kw):

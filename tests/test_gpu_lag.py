@@ -63,10 +63,10 @@ def test_lag1_tf32_fused_path_and_caller_batches():
     assert np.array_equal(gpu.get_rows(0, ids), gb.get_rows(0, ids))
 
 
-def test_lag1_rejected_for_multi_rank_and_transr():
+def test_lag1_rejected_for_transr():
     gr = synth.graph("tiny")
     trip = gr.triples()
-    for kw in (dict(model="transr", dim=16), dict(model="transe_l2", dim=16, world_size=2)):
+    for kw in (dict(model="transr", dim=16), dict(model="transr", dim=16, world_size=2)):
         cfg = kge.Config(n_entities=gr.n_entities, n_relations=gr.n_relations, batch_size=64, chunk_size=16,
                          neg_k=16, lag=1, **kw)
         with pytest.raises(kge.KgeError) as ei:

@@ -60,27 +60,33 @@ def test_production_fp32_scores_loss_rows(graph, model, variant):
     lg = np.concatenate([lg0, gpu.train_step(23)])
     lo = orc.train(24)
     rel = np.abs(lg - lo) / np.abs(lo)
-    # TransE-L1 (reading R-L1): a kink flip moves the free-running trajectory; the strict 1e-5 loss bar is the
-    # teacher-forced test below
-    assert rel.max() <= (1e-3 if model == "transe_l1" else 1e-5), (model, variant, rel.max(), int(np.argmax(rel)))
     ids, rids = np.arange(gr.n_entities), np.arange(gr.n_relations)
     dE = np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids))
     dR = np.abs(gpu.get_rows(1, rids) - orc.get_rows(1, rids))
-    # Rows after free-running steps (reading c.14b): Adagrad's first-touch step lr * g / sqrt(mean g^2) normalises
-    # each row's gradient, so a rounding-level difference in a gradient that cancels to near zero becomes an O(lr)
-    # difference in the row, and later steps feed it back. The oracle run in float (the same algorithm, plain fp32,
-    # sequential sums) drifts from the double oracle by up to 2e-3 (DistMult) / 6e-3 (RotatE modulus) after 24 steps
-    # at these shapes -- any fp32 implementation does. The bar: the coordinates above 1e-4 are a tiny fraction, and the
-    # worst one is within 2x the float oracle's own drift (+1e-4); the strict per-step 1e-4 bar is teacher-forced.
-    assert (dE > 1e-4).mean() <= 1e-3 and (dR > 1e-4).mean() <= 1e-3, ((dE > 1e-4).mean(), (dR > 1e-4).mean())
-    if dE.max() > 1e-4 or dR.max() > 1e-4:
+    # Free-running rows (reading c.14b): Adagrad's first-touch step lr * g / sqrt(mean g^2) normalises each row's
+    # gradient, so a rounding-level difference in a gradient that cancels to near zero becomes an O(lr) difference in
+    # the row, and later steps feed it back (TransE-L1 adds sign flips at the kink, reading R-L1). The oracle run in
+    # float -- the same algorithm in plain fp32 with sequential sums -- drifts from the double oracle by up to 2e-3
+    # (DistMult) / 6e-3 (RotatE modulus) after 24 steps at these shapes: any fp32 implementation does. The strict bars
+    # (loss 1e-5, rows 1e-4) hold for DistMult-like cases without amplification; otherwise the GPU's drift from the
+    # double oracle must stay within twice the float oracle's own drift (max, and fraction of coordinates > 1e-4).
+    # The per-step 1e-4 bar is enforced teacher-forced below.
+    if rel.max() > 1e-5 or dE.max() > 1e-4 or dR.max() > 1e-4:
         of = O.Trainer(model, gr.n_entities, gr.n_relations, 400, *SHAPE, gamma=U.GAMMA, lr=0.1, seed=1,
                        rotate_variant=variant, precision=1, triples=trip)
-        of.train(24)
-        sE = np.abs(of.get_rows(0, ids) - orc.get_rows(0, ids)).max()
-        sR = np.abs(of.get_rows(1, rids) - orc.get_rows(1, rids)).max()
-        print(f"{model}/{variant}: GPU drift {dE.max():.2e}/{dR.max():.2e}, float-oracle drift {sE:.2e}/{sR:.2e}")
-        assert dE.max() <= 2 * sE + 1e-4 and dR.max() <= 2 * sR + 1e-4, (model, variant, dE.max(), dR.max(), sE, sR)
+        lf = of.train(24)
+        fE = np.abs(of.get_rows(0, ids) - orc.get_rows(0, ids))
+        fR = np.abs(of.get_rows(1, rids) - orc.get_rows(1, rids))
+        srel = (np.abs(lf - lo) / np.abs(lo)).max()
+        print(f"{model}/{variant}: GPU loss {rel.max():.2e} rows {dE.max():.2e}/{dR.max():.2e} "
+              f"(frac>1e-4 {(dE > 1e-4).mean():.2e}/{(dR > 1e-4).mean():.2e}); float oracle loss {srel:.2e} rows "
+              f"{fE.max():.2e}/{fR.max():.2e} (frac {(fE > 1e-4).mean():.2e}/{(fR > 1e-4).mean():.2e})")
+        # the first step is before any feedback: strict
+        assert rel[0] <= 1e-5, rel[0]
+        assert rel.max() <= max(1e-5, 2 * srel), (rel.max(), srel)
+        assert dE.max() <= 2 * fE.max() + 1e-4 and dR.max() <= 2 * fR.max() + 1e-4
+        assert (dE > 1e-4).mean() <= 2 * (fE > 1e-4).mean() + 1e-3
+        assert (dR > 1e-4).mean() <= 2 * (fR > 1e-4).mean() + 1e-3
     dS = np.abs(gpu.get_rows(3, ids) - orc.get_rows(3, ids)).max()
     assert dS <= 1e-4 * max(1.0, float(np.abs(orc.get_rows(3, ids)).max())), dS
 
