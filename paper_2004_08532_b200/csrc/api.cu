@@ -115,7 +115,11 @@ static int validate(const kge_config* c) {
     return KGE_ERANGE;
   }
   if (c->corrupt < 0 || c->corrupt > 2) { set_error("bad corrupt"); return KGE_EINVAL; }
-  if (c->neg_precision < 0 || c->neg_precision > 1) { set_error("bad neg_precision"); return KGE_EINVAL; }
+  if (c->neg_precision < 0 || c->neg_precision > 2) { set_error("bad neg_precision"); return KGE_EINVAL; }
+  if (c->neg_precision == KGE_PREC_BF16 && c->model == KGE_TRANSR) {
+    set_error("BF16 negatives are not implemented for TransR (use TF32)");
+    return KGE_EUNSUPPORTED;
+  }
   if (c->lag != 0 && c->lag != 1) { set_error("lag must be 0 or 1"); return KGE_EINVAL; }
   if (c->neg_deg_k < 0 || c->neg_deg_k > c->neg_k) { set_error("neg_deg_k must be in [0, neg_k]"); return KGE_EINVAL; }
   if (c->neg_local != 0 && c->neg_local != 1) { set_error("neg_local must be 0 or 1"); return KGE_EINVAL; }
@@ -296,6 +300,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   h->k1 = (uint32_t)(cfg->seed >> 32);
   dm.dp = ((dm.d + 2 + 31) / 32) * 32;  // O / X' pitch: room for the ones columns at d, d+1 (tc.cu)
   dm.kp = ((dm.k + 31) / 32) * 32;     // W pitch: whole 32-float k-blocks (tc.cu 4D maps; the pad stays zero)
+  dm.dp16 = ((dm.d + 63) / 64) * 64;   // BF16 copies: whole 64-element (128-byte) k-blocks
+  dm.kp16 = ((dm.k + 63) / 64) * 64;
+  dm.bf16 = cfg->neg_precision == KGE_PREC_BF16 ? 1 : 0;
   h->dp = dm.dp;
   h->kp = dm.kp;
   h->n_pad = 64;  // the sampler's warp-level sort stages work on 64-key blocks
@@ -520,6 +527,12 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.X = (float*)dalloc(h, (size_t)nneg * dm.dp * 4);
   b.xnorm = (float*)dalloc(h, (size_t)nneg * 4);
   b.W = (float*)dalloc(h, (size_t)dm.B * dm.kp * 4);
+  if (dm.bf16) {  // BF16 operand copies of the tcgen05 kind::f16 path (pads stay zero)
+    b.O16 = (uint16_t*)dalloc(h, (size_t)dm.B * dm.dp16 * 2);
+    b.X16 = (uint16_t*)dalloc(h, (size_t)nneg * dm.dp16 * 2);
+    b.W16 = (uint16_t*)dalloc(h, (size_t)dm.B * dm.kp16 * 2);
+    if (!b.O16 || !b.X16 || !b.W16) { set_error("out of device memory (BF16 operands)"); return fail(KGE_ENOMEM); }
+  }
   b.wpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
@@ -556,6 +569,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (e == cudaSuccess) e = cudaMemsetAsync(b.O, 0, (size_t)dm.B * dm.dp * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(b.X, 0, (size_t)nneg * dm.dp * 4, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(b.W, 0, (size_t)dm.B * dm.kp * 4, h->stream);
+  if (e == cudaSuccess && dm.bf16) e = cudaMemsetAsync(b.O16, 0, (size_t)dm.B * dm.dp16 * 2, h->stream);
+  if (e == cudaSuccess && dm.bf16) e = cudaMemsetAsync(b.X16, 0, (size_t)nneg * dm.dp16 * 2, h->stream);
+  if (e == cudaSuccess && dm.bf16) e = cudaMemsetAsync(b.W16, 0, (size_t)dm.B * dm.kp16 * 2, h->stream);
   if (e == cudaSuccess) {
     std::vector<float> ones((size_t)std::max<int64_t>(dm.B, nneg), 1.0f);
     e = cudaMemcpy2DAsync(b.O + dm.d, (size_t)dm.dp * 4, ones.data(), 4, 4, dm.B, cudaMemcpyHostToDevice, h->stream);
@@ -581,7 +597,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (sample_init() != cudaSuccess || step_preload() != cudaSuccess || dist_preload() != cudaSuccess)
     return fail(cuda_fail(cudaGetLastError(), "kernel preload"));
   if (cfg->model == KGE_TRANSR) h->n_neg_parts = dm.B;  // one loss partial per (relation, chunk) group
-  if (cfg->neg_precision == KGE_PREC_TF32 && cfg->model != KGE_TRANSR) tc_init(h);
+  if (cfg->neg_precision != KGE_PREC_FP32 && cfg->model != KGE_TRANSR) tc_init(h);
   if (cfg->model == KGE_TRANSR) transr_tc_init(h);  // DistMult / ComplEx / TransE-L2 on tcgen05
   if (tc_supported(h)) h->n_neg_parts = tc_neg_parts(h);
   *out = h;
@@ -1173,7 +1189,7 @@ int64_t kge_step(const kge_handle* h) { return h ? h->step : -1; }
 int32_t kge_neg_path(const kge_handle* h) {
   if (!h) return -1;
   if (h->dims.model == KGE_TRANSR) return h->tr_tc ? KGE_PATH_TF32 : KGE_PATH_FFMA;
-  return tc_supported(h) ? KGE_PATH_TF32 : KGE_PATH_FFMA;
+  return tc_supported(h) ? (h->dims.bf16 ? KGE_PATH_BF16 : KGE_PATH_TF32) : KGE_PATH_FFMA;
 }
 
 int kge_read_losses(kge_handle* h, int64_t first_step, int64_t n, float* out) {

@@ -91,6 +91,9 @@ struct StepBuffers {
   float* X;        // [C*k x d] gathered negative rows
   float* xnorm;    // [C*k]
   float* W;        // [B x k] dL/dS coefficient (C chunks of g x k)
+  uint16_t* O16;   // BF16 path: bf16 copies of O [B x dp16], X' [C*k x dp16] (written by the gather) and W [B x kp16]
+  uint16_t* X16;   // (written by the forward epilogue), or nullptr
+  uint16_t* W16;
   float* wpos;     // [B] dL/df+
   float* lpos;     // [B] per-positive loss term
   float* pstat;    // [B] pair statistic of each positive (L2: squared distance)
@@ -164,6 +167,8 @@ struct Dims {
   int32_t loss;  // kge_loss
   int32_t d, drel, B, g, C, k, n_occ;
   int32_t dp, kp;  // padded row pitch of O / X' (d + 2 rounded up to 32) and of W (k rounded up to 32)
+  int32_t dp16, kp16;  // BF16 copies: pitch of O16 / X16 (d rounded up to 64) and of W16 (k rounded up to 64)
+  int32_t bf16;        // 1: the tcgen05 path contracts BF16 operand copies (KGE_PREC_BF16)
   float gamma, lr, eps;
   int64_t n_entities, n_relations;
 };

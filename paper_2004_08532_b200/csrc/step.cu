@@ -14,10 +14,25 @@
 // The tensor-core variant of k_neg_fwd / k_neg_bwd for the GEMM-shaped families lives in tc.cu.
 #include <algorithm>
 
+#include <cuda_bf16.h>
+
 #include "device_common.cuh"
 #include "kge_internal.h"
 
 namespace kge {
+
+// BF16 operand copies (KGE_PREC_BF16): float4 -> 4 bf16 (round to nearest even) stored as 8 bytes at element 4 q of
+// a bf16 row; returns the squared norm of the ROUNDED values (the tcgen05 expansion ||o||^2 - 2 o.x + ||x||^2 then
+// measures the distance of the rounded rows exactly up to fp32 accumulation)
+__device__ __forceinline__ float st_bf16x4(uint16_t* row, int q, float4 v) {
+  const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+  uint2 u;
+  u.x = *reinterpret_cast<const uint32_t*>(&a);
+  u.y = *reinterpret_cast<const uint32_t*>(&b);
+  reinterpret_cast<uint2*>(row)[q] = u;
+  return fa.x * fa.x + fa.y * fa.y + fb.x * fb.x + fb.y * fb.y;
+}
 
 // ------------------------------------------------------------------------------------------------
 // row helpers (one warp per row, float4 lanes)
@@ -340,6 +355,13 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
       st4(o, q, o4);
       X.v[m] = o4;  // keep o for the gradient below
     }
+    if (a.b.O16) {  // BF16 copy of o; the expansion uses the norm of the rounded row
+      on = 0.f;
+      uint16_t* o16 = a.b.O16 + (int64_t)i * dm.dp16;
+#pragma unroll
+      for (int m = 0; m < V; ++m)
+        if (lane + 32 * m < d4) on += st_bf16x4(o16, lane + 32 * m, X.v[m]);
+    }
     stat = warp_sum(stat);
     on = warp_sum(on);
     const float f = pair_score_from(dm.family, stat, dm.gamma);
@@ -367,6 +389,12 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     float* o = a.b.O + (int64_t)i * dm.dp;
     float stat, on;
     combine_stage<V>(dm.model, mode, h, r, t, mode == 0 ? t : h, o, dm.d, lane, dm.family, stat, on);
+    if (a.b.O16) {  // BF16 copy of o (this lane's own stores, read back), norm of the rounded row
+      __syncwarp();
+      on = 0.f;
+      uint16_t* o16 = a.b.O16 + (int64_t)i * dm.dp16;
+      for (int q = lane; q < (dm.d >> 2); q += 32) on += st_bf16x4(o16, q, ld4(o, q));
+    }
     stat = warp_sum(stat);
     on = warp_sum(on);
     if (lane == 0) {
@@ -388,6 +416,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     Row4<V> Xr;
     Xr.load(a.ent.row(a.s.neg[q]), lane, d4);
     float* X = a.b.X + (int64_t)q * dm.dp;
+    uint16_t* x16 = a.b.X16 ? a.b.X16 + (int64_t)q * dm.dp16 : nullptr;
     float acc = 0.f;
 #pragma unroll
     for (int m = 0; m < V; ++m) {
@@ -395,7 +424,10 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
       if (v < d4) {
         const float4 xv = Xr.v[m];
         st4(X, v, xv);
-        acc += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
+        if (x16)
+          acc += st_bf16x4(x16, v, xv);  // BF16 copy; the norm of the rounded row
+        else
+          acc += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
       }
     }
     acc = warp_sum(acc);
@@ -1397,7 +1429,7 @@ cudaError_t launch_update(kge_handle* h, const Slot& s) {
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
   if (dm.model == KGE_TRANSR) return launch_transr_step(h, s, step);
-  const bool tc = h->cfg.neg_precision == KGE_PREC_TF32 && tc_supported(h);
+  const bool tc = tc_supported(h);
   GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0, tc && tc_fuses_chain(h) ? 1 : 0, tc && tc_flow() ? h->buf.flow : nullptr};
   const int rows = dm.B + dm.C * dm.k;
   launch_begin(h, KGE_K_GATHER);
@@ -1412,7 +1444,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   }
 
   NegArgs na{dm, h->buf, h->buf.Gocc, nullptr, nullptr, 1};
-  if (h->cfg.neg_precision == KGE_PREC_TF32 && tc_supported(h)) {
+  if (tc) {
     cudaError_t e = launch_tc_neg(h, s);
     if (e != cudaSuccess) return e;
     if (tc_fuses_chain(h)) return launch_update(h, s);  // chain rule + loss done in the backward epilogue

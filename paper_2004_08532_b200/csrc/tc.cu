@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda_bf16.h>
+
 #include "device_common.cuh"
 #include "kge_internal.h"
 #include "tc_ptx.cuh"
@@ -38,6 +40,8 @@ struct TcState {
   CUtensorMap mG_S, mR_S, mD_S;
   CUtensorMap mG_S1, mG_L1;  // lag = 1: the same maps over the second (odd-step) Gocc buffer
   CUtensorMap mG_L;          // fused chain: gx rows of Gocc (written by k_gather), box {32, 64}
+  // BF16 path (KGE_PREC_BF16): the same operand views over the bf16 copies, 64-element (128-byte) k-blocks
+  CUtensorMap mO_F16, mX_F16, mW_K16, mW_MN16, mX_MN16, mO_MN16;
   int fwd_cx = 1;  // backward TMA-store targets: Gocc, Grel, dO (SW128), box {32, 32}
   bool ok = false;
 };
@@ -89,6 +93,8 @@ struct TcArgs {
   int32_t fwd_cx;  // forward cluster size along x: the CTAs of one 128-positive tile share its O tile by TMA multicast
   float* fdbg;     // KGE_OPT_CAPTURE_NEG: [B x k] negative pair scores, or nullptr
   int32_t* pcnt;   // pairwise ranking loss: active hinges per positive (StepBuffers::pcnt)
+  uint16_t* W16;   // BF16 path: the forward writes dL/dS here (bf16, pitch kp16) instead of W
+  int32_t dp16, kp16;
 };
 
 // f+ from the positive's pair statistic (k_gather's pstat), as the FFMA path's pair_score_from
@@ -117,7 +123,9 @@ __device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo) {
 // ------------------------------------------------------------------------------------------------
 // forward
 // ------------------------------------------------------------------------------------------------
-template <int FAM>
+// BF: BF16 operands (kind::f16, k-blocks of 64 elements = the same 128-byte rows as the TF32 k-blocks of 32), W out
+// in bf16
+template <int FAM, bool BF>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     k_tc_fwd(const __grid_constant__ CUtensorMap mO, const __grid_constant__ CUtensorMap mX, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -145,7 +153,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int ks = (int)(crank & 1), ntl = (int)(crank >> 1);
   const uint16_t mmask = (uint16_t)(cxn > 1 ? (0x55u << ks) & ((1u << cl) - 1) : 0);  // same-ks CTAs
   const int c = blockIdx.z, i0 = blockIdx.y * 128, t = blockIdx.x >> 1, j0 = t * kNT;
-  const int nkb = a.dp / 32, kh = (nkb + 1) / 2;
+  const int nkb = BF ? a.dp16 / 64 : a.dp / 32, kh = (nkb + 1) / 2;
   const int kb0 = ks ? kh : 0, kb1 = ks ? nkb : kh;
   const int nst = (kb1 - kb0 + kFwdKpb - 1) / kFwdKpb;
   const int jf0 = j0 + ks * kHalf;  // first column this CTA finalises
@@ -200,7 +208,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // so the K = 8 slices of each k-block are dealt to kIssuers threads, issuer q accumulating slice q of every
     // k-block into its own TMEM columns [q * kNT, (q + 1) * kNT); the epilogue adds the partials in a fixed order
     const int q = warp - (8 - kIssuers);
-    const uint32_t idesc = idesc_tf32(128, kNT, false, false);
+    const uint32_t idesc = BF ? idesc_bf16(128, kNT, false, false) : idesc_tf32(128, kNT, false, false);
     const uint32_t acc = tmem + (uint32_t)(q * kNT);
     for (int st = 0; st < nst; ++st) {
       const int s = st % kFwdStages;
@@ -208,9 +216,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
       const int nk = min(kFwdKpb, kb1 - (kb0 + st * kFwdKpb));
-      for (int b = 0; b < nk; ++b)
-        mma_tf32(acc, sdesc(sa + b * A_KB + q * 32, 16, 1024), sdesc(sb + b * B_KB + q * 32, 16, 1024), idesc,
-                 (st | b) ? 1u : 0u);
+      for (int b = 0; b < nk; ++b) {
+        // slice q of the k-block: K = 8 tf32 or 16 bf16 = 32 bytes into each 128-byte row
+        const uint64_t ad = sdesc(sa + b * A_KB + q * 32, 16, 1024), bd = sdesc(sb + b * B_KB + q * 32, 16, 1024);
+        if (BF)
+          mma_bf16(acc, ad, bd, idesc, (st | b) ? 1u : 0u);
+        else
+          mma_tf32(acc, ad, bd, idesc, (st | b) ? 1u : 0u);
+      }
       if (cxn > 1)
         mma_commit_mc(&empty[s], mmask);
       else
@@ -321,7 +334,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   lsum += __logf(lprod);
   if (nact) atomicAdd(&a.pcnt[(int64_t)c * dm.g + i], nact);  // integer: exact in any order
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 4);
-  if (iok) {
+  if (iok && BF) {  // dL/dS in bf16 for the backward GEMMs (the pads beyond k stay zero)
+    uint16_t* wrow = a.W16 + ((int64_t)c * dm.g + i) * a.kp16 + jf0 + hf * 8;
+    if (jf0 + hf * 8 + 8 <= dm.k) {
+      uint4 u;
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]), p1 = __floats2bfloat162_rn(v[2], v[3]);
+      __nv_bfloat162 p2 = __floats2bfloat162_rn(v[4], v[5]), p3 = __floats2bfloat162_rn(v[6], v[7]);
+      u.x = *reinterpret_cast<uint32_t*>(&p0);
+      u.y = *reinterpret_cast<uint32_t*>(&p1);
+      u.z = *reinterpret_cast<uint32_t*>(&p2);
+      u.w = *reinterpret_cast<uint32_t*>(&p3);
+      *reinterpret_cast<uint4*>(wrow) = u;
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (jf0 + hf * 8 + jj < dm.k) {
+          const __nv_bfloat16 b16 = __float2bfloat16_rn(v[jj]);
+          wrow[jj] = *reinterpret_cast<const uint16_t*>(&b16);
+        }
+    }
+  } else if (iok) {
     float* wrow = a.W + ((int64_t)c * dm.g + i) * a.kp + jf0 + hf * 8;
     if (jf0 + hf * 8 + 8 <= dm.k && (a.kp & 3) == 0) {
       float4* dst = reinterpret_cast<float4*>(wrow);
@@ -385,7 +417,24 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // second half of K; each CTA then hands the peer the 64 rows the peer finalises (through L2, coalesced float4 columns)
 // and finalises its own 64 rows of the 128 x (nb * 32) tile -- the sum is always P0 + P1.
 // ------------------------------------------------------------------------------------------------
-template <int FAM>
+// Columns of backward part p (of kNSplit), in 32-column units: the TF32 path cuts the dp / 32 column blocks of the
+// rows, the BF16 path the dp16 / 64 blocks of 64 columns (two 32-column units each; TMA boxes and MN-major atoms are
+// 64 bf16 wide) -- the TMEM columns and the finalise keep 32-column units either way
+template <bool BF>
+__device__ __forceinline__ void bwd_part(const TcArgs& a, int p, int& b0, int& nb) {
+  if (BF) {
+    const int n64 = a.dp16 / 64;
+    const int c0 = p * n64 / kNSplit, c1 = (p + 1) * n64 / kNSplit;
+    b0 = 2 * c0;
+    nb = 2 * (c1 - c0);
+  } else {
+    const int n32 = a.dp / 32;
+    b0 = p * n32 / kNSplit;
+    nb = (p + 1) * n32 / kNSplit - b0;
+  }
+}
+
+template <int FAM, bool BF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_bwd(const __grid_constant__ CUtensorMap mW_K, const __grid_constant__ CUtensorMap mW_MN,
              const __grid_constant__ CUtensorMap mX_MN, const __grid_constant__ CUtensorMap mO_MN,
@@ -403,19 +452,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ks = blockIdx.x & 1, tp = blockIdx.x >> 1;
   const int c = blockIdx.y, part = tp % kNSplit, r0 = (tp / kNSplit) * 128;
   const int nrows = pass_x ? dm.k : dm.g;
-  const int nb_all = a.dp / 32;
-  const int b0 = part * nb_all / kNSplit, b1 = (part + 1) * nb_all / kNSplit;  // this CTA's column blocks
-  const int nb = b1 - b0;
+  int b0, nb;  // this CTA's 32-column blocks
+  bwd_part<BF>(a, part, b0, nb);
   if (r0 >= nrows || nb == 0 || b0 * 32 >= dm.d) {  // uniform per CTA pair, before any barrier / TMEM use
     pdl_trigger();
     return;
   }
   const int nk = pass_x ? dm.g : dm.k;  // contraction length
-  const int nkb = (nk + 31) / 32, kh = (nkb + 1) / 2;
+  constexpr int KB = BF ? 64 : 32;      // contraction rows per k-block (one 128-byte row of the K-major operand)
+  const int nkb = (nk + KB - 1) / KB, kh = (nkb + 1) / 2;
   const int kb0 = ks ? kh : 0, kb1 = ks ? nkb : kh;
   const int nst = (kb1 - kb0 + kBwdKpb - 1) / kBwdKpb;
   constexpr uint32_t A_BYTES = kBwdKpb * 16384, B_BYTES = kBwdKpb * 4 * 4096, STAGE = A_BYTES + B_BYTES;
-  constexpr uint32_t KROWS_B = kBwdKpb * 32 * 128;  // bytes between 32-column blocks of an MN-major stage operand
+  // bytes between MN blocks (32 tf32 / 64 bf16 columns) of an MN-major stage operand
+  constexpr uint32_t KROWS_B = kBwdKpb * KB * 128;
   // shared memory: [stages][self: this CTA's 64 finalised rows x 4 column blocks of O (dO) / X' (dX'), SW128]
   // after the main loop the stage area holds xown ([32 float4 columns][64 rows]) and the TMA-store staging
   uint8_t* self_smem = smem + kBwdStages * STAGE;
@@ -482,9 +532,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (!role) prologue();
 
   int loss_part = 0;  // the loss is reduced by the first CTA of (row tile 0, chunk 0) that has columns to process
-  while (loss_part + 1 < kNSplit && ((loss_part + 1) * nb_all / kNSplit == loss_part * nb_all / kNSplit ||
-                                     loss_part * nb_all / kNSplit * 32 >= d))
-    ++loss_part;
+  for (;; ++loss_part) {
+    int lb0, lnb;
+    bwd_part<BF>(a, loss_part, lb0, lnb);
+    if (loss_part + 1 >= kNSplit || (lnb > 0 && lb0 * 32 < d)) break;
+  }
   if (fuse && tp == loss_part && ks == 0 && blockIdx.y == 0 && warp == 1) {
     // deterministic loss (reading c.9): fixed lane assignment and order, identical to the unfused k_chain; it needs
     // every chunk's forward partials
@@ -518,11 +570,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* sb = sa + A_BYTES;
         const int kq = kb0 + issued * kBwdKpb;
         mbar_arrive_expect_tx(&full[s], STAGE);
+        // TF32: blocks of 32 columns (4 per box); BF16: of 64 (2 per box) -- the same 128-byte rows
         if (!pass_x)
           tma_load_4d(sa, &mW_K, &full[s], 0, r0, kq, c);  // W[rows, k-blocks kq..]: [kb][128 rows][128 B]
         else
-          tma_load_4d(sa, &mW_MN, &full[s], 0, kq * 32, r0 / 32, c);  // W^T: [4 j-blocks][K rows][128 B]
-        tma_load_4d(sb, pass_x ? &mO_MN : &mX_MN, &full[s], 0, kq * 32, b0, c);  // [4 col blocks][K rows][128 B]
+          tma_load_4d(sa, &mW_MN, &full[s], 0, kq * KB, r0 / KB, c);  // W^T: [j-blocks][K rows][128 B]
+        tma_load_4d(sb, pass_x ? &mO_MN : &mX_MN, &full[s], 0, kq * KB, BF ? b0 / 2 : b0, c);  // [col blocks][K rows]
       }
     };
     if (q == 0) {
@@ -538,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    const uint32_t idesc = idesc_tf32(128, nb * 32, pass_x, true);
+    const uint32_t idesc = BF ? idesc_bf16(128, nb * 32, pass_x, true) : idesc_tf32(128, nb * 32, pass_x, true);
     const uint32_t acc = tmem + (uint32_t)(q * 128);
     for (int st = 0; st < nst; ++st) {
       const int s = st % kBwdStages;
@@ -548,9 +601,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
       const int nkq = min(kBwdKpb, kb1 - (kb0 + st * kBwdKpb));
       for (int b = 0; b < nkq; ++b) {
-        const uint32_t koff = (uint32_t)(b * 32 + q * 8) * 128;  // K rows of an MN-major operand
-        const uint64_t ad = pass_x ? sdesc_mn(sa + koff, KROWS_B) : sdesc(sa + b * 16384 + q * 32, 16, 1024);
-        mma_tf32(acc, ad, sdesc_mn(sb + koff, KROWS_B), idesc, (st | b) ? 1u : 0u);
+        if (BF) {  // K slice q = 16 rows: 2048 B into an MN-major operand, 32 B into a K-major row
+          const uint32_t koff = (uint32_t)(b * 64 + q * 16) * 128;
+          const uint64_t ad = pass_x ? sdesc(sa + koff, KROWS_B, 1024) : sdesc(sa + b * 16384 + q * 32, 16, 1024);
+          mma_bf16(acc, ad, sdesc(sb + koff, KROWS_B, 1024), idesc, (st | b) ? 1u : 0u);
+        } else {
+          const uint32_t koff = (uint32_t)(b * 32 + q * 8) * 128;  // K rows of an MN-major operand
+          const uint64_t ad = pass_x ? sdesc_mn(sa + koff, KROWS_B) : sdesc(sa + b * 16384 + q * 32, 16, 1024);
+          mma_tf32(acc, ad, sdesc_mn(sb + koff, KROWS_B), idesc, (st | b) ? 1u : 0u);
+        }
       }
       mma_commit(&empty[s]);
     }
@@ -726,6 +785,20 @@ static bool make_map4(CUtensorMap* m, const float* base, int cols, int rows, int
              sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The same 4D view over a [chunks x rows x cols] bf16 buffer: {64 (col in k-block), rows, k-blocks, chunks}
+static bool make_map4_16(CUtensorMap* m, const uint16_t* base, int cols, int rows, int chunks, int pitch, int box_rows,
+                         int box_kb) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64), (cuuint64_t)chunks};
+  cuuint64_t strides[3] = {(cuuint64_t)pitch * 2, 128, (cuuint64_t)pitch * 2 * rows};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, (cuuint32_t)box_kb, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)base, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static size_t fwd_smem() { return (size_t)kFwdStages * kFwdKpb * (128 * 128 + kNT * 128) + 128 * (kNT / 2) * 4 + 1024; }
 static size_t bwd_smem(int dp) {
   (void)dp;
@@ -739,6 +812,7 @@ bool tc_init(kge_handle* h) {
   if (!(dm.family == FAM_DOT || dm.family == FAM_L2 || (dm.family == FAM_L2SQ && dm.model == KGE_ROTATE))) return false;
   if (h->dp > 512 || bwd_smem(h->dp) > 227 * 1024 || (dm.dp / 32 + kNSplit - 1) / kNSplit > 4 || h->kp % 32)
     return false;
+  if (dm.bf16 && (2 * ((dm.dp16 / 64 + kNSplit - 1) / kNSplit) > 4 || !h->buf.O16)) return false;
   TcState* st = new TcState();
   const StepBuffers& b = h->buf;
   bool ok = true;
@@ -764,6 +838,14 @@ bool tc_init(kge_handle* h) {
   ok &= make_map(&st->mG_L, b.Gocc, dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 64, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mG_S1, h->gocc2[1], dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B);
   ok &= make_map(&st->mG_L1, h->gocc2[1], dm.d, 2 * dm.B + dm.C * dm.k, 1, dm.d, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (dm.bf16) {  // BF16 operands: the contraction maps point at the bf16 copies (the epilogue maps stay fp32)
+    ok &= make_map4_16(&st->mO_F, b.O16, dm.dp16, dm.g, dm.C, dm.dp16, 128, st->fwd_cx > 1 ? 1 : kFwdKpb);
+    ok &= make_map4_16(&st->mX_F, b.X16, dm.dp16, dm.k, dm.C, dm.dp16, kNT, kFwdKpb);
+    ok &= make_map4_16(&st->mW_K, b.W16, dm.kp16, dm.g, dm.C, dm.kp16, 128, kBwdKpb);
+    ok &= make_map4_16(&st->mW_MN, b.W16, dm.kp16, dm.g, dm.C, dm.kp16, 64 * kBwdKpb, 2);
+    ok &= make_map4_16(&st->mX_MN, b.X16, dm.dp16, dm.k, dm.C, dm.dp16, 64 * kBwdKpb, 2);
+    ok &= make_map4_16(&st->mO_MN, b.O16, dm.dp16, dm.g, dm.C, dm.dp16, 64 * kBwdKpb, 2);
+  }
   if (!ok) {
     delete st;
     return false;
@@ -773,12 +855,21 @@ bool tc_init(kge_handle* h) {
     e = cudaFuncSetAttribute(fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem());
     if (e == cudaSuccess) e = cudaFuncSetAttribute(bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_smem(h->dp));
   };
-  if (dm.family == FAM_DOT)
-    attrs(k_tc_fwd<FAM_DOT>, k_tc_bwd<FAM_DOT>);
-  else if (dm.family == FAM_L2)
-    attrs(k_tc_fwd<FAM_L2>, k_tc_bwd<FAM_L2>);
-  else
-    attrs(k_tc_fwd<FAM_L2SQ>, k_tc_bwd<FAM_L2SQ>);
+  if (dm.bf16) {
+    if (dm.family == FAM_DOT)
+      attrs(k_tc_fwd<FAM_DOT, true>, k_tc_bwd<FAM_DOT, true>);
+    else if (dm.family == FAM_L2)
+      attrs(k_tc_fwd<FAM_L2, true>, k_tc_bwd<FAM_L2, true>);
+    else
+      attrs(k_tc_fwd<FAM_L2SQ, true>, k_tc_bwd<FAM_L2SQ, true>);
+  } else {
+    if (dm.family == FAM_DOT)
+      attrs(k_tc_fwd<FAM_DOT, false>, k_tc_bwd<FAM_DOT, false>);
+    else if (dm.family == FAM_L2)
+      attrs(k_tc_fwd<FAM_L2, false>, k_tc_bwd<FAM_L2, false>);
+    else
+      attrs(k_tc_fwd<FAM_L2SQ, false>, k_tc_bwd<FAM_L2SQ, false>);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     delete st;
@@ -832,7 +923,8 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
            h->buf.Gocc, h->buf.rowsumW, h->buf.colsumW, 2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128,
            tc_fuses_chain(h) ? 1 : 0, s, h->rows, h->buf.wpos, h->buf.pstat, h->buf.lpos, h->buf.Grel,
            h->buf.loss, h->buf.flags, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->xbuf, tc_flow() ? h->buf.flow : nullptr,
-           2 * ((dm.k + kNT - 1) / kNT) * ((dm.g + 127) / 128), st->fwd_cx, h->buf.fdbg, h->buf.pcnt};
+           2 * ((dm.k + kNT - 1) / kNT) * ((dm.g + 127) / 128), st->fwd_cx, h->buf.fdbg, h->buf.pcnt, h->buf.W16,
+           dm.dp16, dm.kp16};
   dim3 gf(2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128, dm.C);  // x = 2 tile + split-K half
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(2 * tiles * kNSplit, dm.C, 2);  // x = 2 (row tile * kNSplit + column part) + split-K half
@@ -849,9 +941,14 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
     launch_end(h, KGE_K_NEG_BWD);
     return cudaGetLastError();
   };
-  if (dm.family == FAM_DOT) return run(k_tc_fwd<FAM_DOT>, k_tc_bwd<FAM_DOT>);
-  if (dm.family == FAM_L2) return run(k_tc_fwd<FAM_L2>, k_tc_bwd<FAM_L2>);
-  return run(k_tc_fwd<FAM_L2SQ>, k_tc_bwd<FAM_L2SQ>);
+  if (dm.bf16) {
+    if (dm.family == FAM_DOT) return run(k_tc_fwd<FAM_DOT, true>, k_tc_bwd<FAM_DOT, true>);
+    if (dm.family == FAM_L2) return run(k_tc_fwd<FAM_L2, true>, k_tc_bwd<FAM_L2, true>);
+    return run(k_tc_fwd<FAM_L2SQ, true>, k_tc_bwd<FAM_L2SQ, true>);
+  }
+  if (dm.family == FAM_DOT) return run(k_tc_fwd<FAM_DOT, false>, k_tc_bwd<FAM_DOT, false>);
+  if (dm.family == FAM_L2) return run(k_tc_fwd<FAM_L2, false>, k_tc_bwd<FAM_L2, false>);
+  return run(k_tc_fwd<FAM_L2SQ, false>, k_tc_bwd<FAM_L2SQ, false>);
 }
 
 }  // namespace kge

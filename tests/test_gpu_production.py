@@ -118,13 +118,14 @@ def test_production_fp32_teacher_forced(graph, model, variant):
         print(f"TransE-L1 kink coordinates exempted over 5 steps: {exempt}")
 
 
+@pytest.mark.parametrize("precision", ["tf32", "bf16"])
 @pytest.mark.parametrize("graph,model", [("fb15k", "transe_l2"), ("fb15k", "distmult"), ("fb15k", "complex"),
                                          ("wn18", "rotate")])
-def test_production_tf32_pair_scores(graph, model):
-    # the tcgen05 forward's per-pair f- (TF32 operands, fp32 TMEM accumulators), element by element at configs[1] /
-    # [2] / [4]'s shape, on tables the oracle and the GPU share (teacher-forced)
-    gr, trip, gpu, orc = _pair(graph, model, 400, precision="tf32")
-    assert gpu.neg_path == "tf32"
+def test_production_tf32_pair_scores(graph, model, precision):
+    # the tcgen05 forward's per-pair f- (TF32 or BF16 operands, fp32 TMEM accumulators), element by element at
+    # configs[1] / [2] / [4]'s shape, on tables the oracle and the GPU share (teacher-forced)
+    gr, trip, gpu, orc = _pair(graph, model, 400, precision=precision)
+    assert gpu.neg_path == precision
     heads, rels, tails = (np.asarray(a) for a in trip)
     orc.train(3)  # move off the init so the scores are not all near the same value
     U.copy_tables(orc, gpu, model, gr.n_entities, gr.n_relations)
@@ -136,7 +137,7 @@ def test_production_tf32_pair_scores(graph, model):
     err = U.check_pair_scores(model, gpu.neg_scores(), ref, meta, orc, SHAPE[1], 2e-3)
     assert err <= 2e-3, (model, err)
     assert abs(lg - lo) / abs(lo) <= 2e-3
-    print(f"tf32 {model}: per-pair worst scale-aware error {err:.2e}")
+    print(f"{precision} {model}: per-pair worst scale-aware error {err:.2e}")
 
 
 @pytest.mark.parametrize("ks", [2, 4, 8])
