@@ -75,6 +75,8 @@ def lib():
         L.orc_logistic_loss.restype = ctypes.c_double
         L.orc_ranking_loss.argtypes = [_dp, _dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, _dp, _dp]
         L.orc_ranking_loss.restype = ctypes.c_double
+        L.orc_eval_candidates.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _i64p, _i64p, ctypes.c_int64,
+                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _i64p, P(ctypes.c_int32)]
         L.orc_adagrad.argtypes = [_dp, _dp, _dp, ctypes.c_int32, ctypes.c_double, ctypes.c_double]
         L.orc_dedup.argtypes = [_i64p, ctypes.c_int64, _i64p, P(ctypes.c_int32), _i64p, _i64p]
         L.orc_dedup.restype = ctypes.c_int64
@@ -327,20 +329,43 @@ class Trainer:
         lib().orc_set_step(self.h, int(s))
 
 
+def eval_candidates(seed, n_entities, heads, tails, n_queries, n_uniform, n_degree, both):
+    """Reading c.15' second-protocol candidates: per query n_uniform uniform and n_degree
+    degree-proportional corruptions from the counter-based stream EVAL; returns (entities, sides) [n_queries x m]."""
+    th, tt = np.ascontiguousarray(heads, np.int64), np.ascontiguousarray(tails, np.int64)
+    m = n_uniform + n_degree
+    ent = np.zeros((n_queries, m), np.int64)
+    side = np.zeros((n_queries, m), np.int32)
+    lib().orc_eval_candidates(int(seed), int(n_entities), len(th), _p(th, ctypes.c_int64), _p(tt, ctypes.c_int64),
+                              n_queries, n_uniform, n_degree, int(both), _p(ent, ctypes.c_int64),
+                              _p(side, ctypes.c_int32))
+    return ent, side
+
+
 def link_rank(trainer, hs, rs, ts, head=False, candidates=None, known=None):
     """Link-prediction ranks, PAPER.md:652-665 [5.3] step by step: for each positive triple build S_i = the positive
-    plus its negative triples (every corruption of the tail -- head=True: the head -- or, second protocol, the given
-    candidate entities; with `known` (a set of (h, r, t) tuples), first protocol filtered: corruptions that already
-    exist in the dataset are removed), score S_i with Table 1, order it by non-increasing score with the positive
-    LAST among equal scores (reading c.15), rank_i = the positive's 1-based position. candidates: list of entity-id
-    arrays, one per query. The corruption equal to the positive itself is not a negative triple."""
+    plus its negative triples (every corruption of the tail -- head=True: the head; head="both": every corruption of
+    the head AND of the tail in one list, as the paper's "(h', r, t) and (h, r, t')" -- or, second protocol, the given
+    candidates; with `known` (a set of (h, r, t) tuples), first protocol filtered: corruptions that already exist in
+    the dataset are removed), score S_i with Table 1, order it by non-increasing score with the positive LAST among
+    equal scores (reading c.15), rank_i = the positive's 1-based position. candidates: per query an array of entity
+    ids (one side), or with head="both" a pair (entities, sides: 0 = tail replaced, 1 = head replaced). The corruption
+    equal to the positive itself is not a negative triple."""
     out = []
     n_e = trainer.cfg.n_entities
+    both = isinstance(head, str) and head == "both"
     for i in range(len(hs)):
         h, r, t = int(hs[i]), int(rs[i]), int(ts[i])
-        true_e = h if head else t
-        ents = range(n_e) if candidates is None else [int(e) for e in candidates[i]]
-        neg = [(e, r, t) if head else (h, r, e) for e in ents if e != true_e]
+        if both:
+            if candidates is None:
+                cs = [(e, 0) for e in range(n_e)] + [(e, 1) for e in range(n_e)]
+            else:
+                cs = [(int(e), int(sd)) for e, sd in zip(*candidates[i])]
+            neg = [(e, r, t) if sd else (h, r, e) for e, sd in cs if e != (h if sd else t)]
+        else:
+            true_e = h if head else t
+            ents = range(n_e) if candidates is None else [int(e) for e in candidates[i]]
+            neg = [(e, r, t) if head else (h, r, e) for e in ents if e != true_e]
         if known is not None:
             neg = [x for x in neg if x not in known]
         trip = [(h, r, t)] + neg

@@ -31,7 +31,7 @@ int threads() {
 // ------------------------------------------------------------------------------------------------
 const uint32_t PHILOX_M0 = 0xD2511F53u, PHILOX_M1 = 0xCD9E8D57u;
 const uint32_t PHILOX_W0 = 0x9E3779B9u, PHILOX_W1 = 0xBB67AE85u;
-const uint32_t TAG_NEG = 1, TAG_PERM = 2, TAG_INIT = 3, TAG_DEG = 4;
+const uint32_t TAG_NEG = 1, TAG_PERM = 2, TAG_INIT = 3, TAG_DEG = 4, TAG_EVAL = 5;
 
 void philox(const uint32_t in[4], const uint32_t key_in[2], uint32_t out[4]) {
   uint32_t x0 = in[0], x1 = in[1], x2 = in[2], x3 = in[3];
@@ -116,6 +116,36 @@ int64_t deg_pos(uint64_t seed, int64_t B, uint32_t step, uint32_t cg, uint32_t j
   uint64_t u = (j & 1u) ? (((uint64_t)o[3] << 32) | o[2]) : (((uint64_t)o[1] << 32) | o[0]);
   unsigned __int128 prod = (unsigned __int128)u * (uint64_t)B;
   return (int64_t)(uint64_t)(prod >> 64);
+}
+
+// c.15' second-protocol candidates (PAPER.md:656-658 [5.3]: "we use only 2000 negative triplets; 1000 sampled
+// uniformly from the entire set of negative samples and 1000 sampled proportionally to the degree of the corrupted
+// entities"): slot j of query i draws u from Philox(ctr=(j/2, lo32(i), hi32(i), EVAL), key = eval seed), words as in
+// c.3. Uniform slots (j < n_uniform): an entity uniform over the N_e entities -- with both sides pooled (mode 2) a
+// corruption uniform over the 2 N_e (side, entity) pairs: p = floor(u * 2 N_e / 2^64), side = p & 1, e = p >> 1.
+// Degree slots: an endpoint uniform over the 2 N_t triple endpoints (entity drawn proportionally to its degree in the
+// graph): p = floor(u * 2 N_t / 2^64) (mode 2: * 4 N_t, side = p & 1, p >>= 1), e = (p & 1) ? t[p >> 1] : h[p >> 1].
+// side 0 = the tail is replaced, 1 = the head.
+void eval_candidate(uint64_t seed, int64_t n_ent, int64_t n_trip, const int64_t* th, const int64_t* tt, int64_t i,
+                    int64_t j, int64_t n_uniform, int32_t both, int64_t* ent, int32_t* side) {
+  uint32_t key[2];
+  seed_key(seed, key);
+  uint32_t ctr[4] = {(uint32_t)(j / 2), (uint32_t)i, (uint32_t)((uint64_t)i >> 32), TAG_EVAL}, o[4];
+  philox(ctr, key, o);
+  uint64_t u = (j & 1) ? (((uint64_t)o[3] << 32) | o[2]) : (((uint64_t)o[1] << 32) | o[0]);
+  const uint64_t range = j < n_uniform ? (uint64_t)n_ent * (both ? 2u : 1u) : (uint64_t)n_trip * (both ? 4u : 2u);
+  uint64_t p = (uint64_t)(((unsigned __int128)u * range) >> 64);
+  *side = 0;
+  if (both) {
+    *side = (int32_t)(p & 1u);
+    p >>= 1;
+  }
+  if (j < n_uniform) {
+    *ent = (int64_t)p;
+  } else {
+    const int64_t q = (int64_t)(p >> 1);
+    *ent = (p & 1u) ? tt[q] : th[q];
+  }
 }
 
 // c.4 corruption schedule; "corrupt the head entities in a similar fashion".
@@ -903,6 +933,14 @@ void orc_score_group(int32_t model, int32_t variant, double gamma, int32_t d, in
     combine(model, d, mode, H + (size_t)i * d, R + (size_t)i * drel, T + (size_t)i * d, Mi, o.data());
     for (int32_t j = 0; j < k; ++j) out[(size_t)i * k + j] = pair_score(model, variant, gamma, d, o.data(), X + (size_t)j * d, Mi);
   }
+}
+void orc_eval_candidates(uint64_t seed, int64_t n_ent, int64_t n_trip, const int64_t* th, const int64_t* tt,
+                         int64_t n_queries, int64_t n_uniform, int64_t n_degree, int32_t both, int64_t* ent,
+                         int32_t* side) {
+  const int64_t m = n_uniform + n_degree;
+  for (int64_t i = 0; i < n_queries; ++i)
+    for (int64_t j = 0; j < m; ++j) eval_candidate(seed, n_ent, n_trip, th, tt, i, j, n_uniform, both, ent + i * m + j,
+                                                   side + i * m + j);
 }
 double orc_ranking_loss(const double* pos, const double* neg, int64_t B, int64_t k, double gamma, double* dpos,
                         double* dneg) {

@@ -85,6 +85,11 @@ void orc_score_grad(int32_t model, int32_t variant, double gamma, int32_t d, con
 void orc_score_group(int32_t model, int32_t variant, double gamma, int32_t d, int32_t mode, int32_t g, int32_t k,
                      const double* H, const double* R, const double* T, const double* M, const double* X,
                      double* out);
+/* c.15' second-protocol candidates of n_queries queries: ent/side [n_queries x (n_uniform +
+ * n_degree)], side 0 = tail replaced, 1 = head replaced (both = 0: all 0). th/tt: the graph's heads and tails. */
+void orc_eval_candidates(uint64_t seed, int64_t n_ent, int64_t n_trip, const int64_t* th, const int64_t* tt,
+                         int64_t n_queries, int64_t n_uniform, int64_t n_degree, int32_t both, int64_t* ent,
+                         int32_t* side);
 /* c.9' pairwise ranking loss: L = (1/(B k)) sum_i sum_j max(0, gamma - f+_i + f-_ij) over
  * pos[B] and neg[B*k] (row i = the negatives paired with positive i); dpos[B], dneg[B*k] = dL/df (hinge at 0:
  * subgradient 0). Returns L. */

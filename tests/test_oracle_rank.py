@@ -86,26 +86,78 @@ def test_filter_never_worsens_and_order_invariance():
 
 
 def test_sampled_protocol_candidates():
+    # second protocol (reading c.15'): 1000 uniform + 1000 degree-proportional candidates per query
     orc, trip, E, R = _toy("distmult")
     deg = np.bincount(np.concatenate([trip[0], trip[2]]), minlength=20)
-    off, ids = kge.sampled_candidates(5, deg, n_uniform=1000, n_degree=1000, seed=4)
-    assert np.array_equal(np.diff(off), np.full(5, 2000)) and ids.min() >= 0 and ids.max() < 20  # |S_i| = 2001
-    assert not np.any(np.isin(np.nonzero(deg == 0)[0], ids.reshape(5, 2000)[:, 1000:]))  # degree 0: never drawn
-    cands = [ids[off[i]:off[i + 1]] for i in range(5)]
+    ent, side = O.eval_candidates(4, 20, trip[0], trip[2], 5, 1000, 1000, both=False)
+    assert ent.shape == (5, 2000) and ent.min() >= 0 and ent.max() < 20 and not side.any()  # |S_i| = 2001
+    assert not np.any(np.isin(np.nonzero(deg == 0)[0], ent[:, 1000:]))  # degree 0: never drawn
     h, r, t = trip[0][:5], trip[1][:5], trip[2][:5]
-    got = O.link_rank(orc, h, r, t, candidates=cands)
+    got = O.link_rank(orc, h, r, t, candidates=list(ent))
     for i in range(5):
         ft = _closed_form("distmult", E, R, int(h[i]), int(r[i]), int(t[i]))
-        fs = [_closed_form("distmult", E, R, int(h[i]), int(r[i]), int(e)) for e in cands[i] if e != t[i]]
+        fs = [_closed_form("distmult", E, R, int(h[i]), int(r[i]), int(e)) for e in ent[i] if e != t[i]]
         assert got[i] == 1 + sum(1 for f in fs if f >= ft - 1e-12 * abs(ft))
 
 
-def test_degree_draws_proportional():
-    deg = np.array([1, 2, 3, 4, 10, 0, 5], np.float64)
-    off, ids = kge.sampled_candidates(1000, deg, n_uniform=0, n_degree=1000, seed=5)  # 10^6 draws
-    freq = np.bincount(ids, minlength=len(deg)) / len(ids)
-    p = deg / deg.sum()
-    assert freq[5] == 0 and np.all(np.abs(freq - p) <= 0.02 * p + 1e-12)
+@pytest.mark.parametrize("both", [False, True])
+def test_candidate_draws_uniform_and_degree_proportional(both):
+    # 10^6 draws per part: uniform slots are uniform over the entities (both sides pooled: over the (side, entity)
+    # pairs); degree slots follow the endpoint degree of the graph ("proportionally to the degree")
+    th = np.array([0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 6, 6, 6, 6, 6], np.int64)
+    tt = np.array([4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 6, 6, 6, 6, 6], np.int64)
+    n_e = 8
+    ent, side = O.eval_candidates(9, n_e, th, tt, 1000, 1000, 1000, both=both)
+    uni, dg, su, sd = ent[:, :1000].ravel(), ent[:, 1000:].ravel(), side[:, :1000].ravel(), side[:, 1000:].ravel()
+    cells = np.bincount(uni * 2 + su if both else uni, minlength=2 * n_e if both else n_e) / len(uni)
+    assert np.all(np.abs(cells - cells.mean()) <= 0.02 * cells.mean())
+    degree = np.bincount(np.concatenate([th, tt]), minlength=n_e).astype(np.float64)
+    freq = np.bincount(dg, minlength=n_e) / len(dg)
+    p = degree / degree.sum()
+    assert freq[5] == 0 and freq[7] == 0 and np.all(np.abs(freq - p) <= 0.02 * p + 1e-12)
+    if both:
+        assert abs(sd.mean() - 0.5) < 0.01 and abs(su.mean() - 0.5) < 0.01
+    else:
+        assert not su.any() and not sd.any()
+    # counter-based: the same (seed, query, slot) gives the same draw; another seed does not
+    e2, _ = O.eval_candidates(9, n_e, th, tt, 3, 1000, 1000, both=both)
+    assert np.array_equal(e2, ent[:3]) and not np.array_equal(O.eval_candidates(10, n_e, th, tt, 3, 1000, 1000,
+                                                                                   both=both)[0], ent[:3])
+
+
+@pytest.mark.parametrize("model", ["distmult", "transe_l2"])
+def test_rank_both_sides_one_list(model):
+    # S_i holds the corruptions (h', r, t) AND (h, r, t') of the positive; with closed-form scores
+    orc, trip, E, R = _toy(model)
+    q = np.arange(10)
+    known = set(zip(*(a.tolist() for a in trip)))
+    for kn in (None, known):
+        got = O.link_rank(orc, trip[0][q], trip[1][q], trip[2][q], head="both", known=kn)
+        for i in q:
+            h, r, t = int(trip[0][i]), int(trip[1][i]), int(trip[2][i])
+            ft = _closed_form(model, E, R, h, r, t)
+            negs = [(e, r, t) for e in range(20) if e != h] + [(h, r, e) for e in range(20) if e != t]
+            if kn is not None:
+                negs = [x for x in negs if x not in kn]
+            fs = [_closed_form(model, E, R, *x) for x in negs]
+            assert got[i] == 1 + sum(1 for f in fs if f >= ft - 1e-12 * abs(ft)), i
+        # the pooled list is the union of the two one-sided lists (the positive counted once)
+        rt = O.link_rank(orc, trip[0][q], trip[1][q], trip[2][q], head=False, known=kn)
+        rh = O.link_rank(orc, trip[0][q], trip[1][q], trip[2][q], head=True, known=kn)
+        assert np.array_equal(got, rt + rh - 1)
+
+
+def test_rank_both_sampled_candidates():
+    orc, trip, E, R = _toy("distmult")
+    ent, side = O.eval_candidates(2, 20, trip[0], trip[2], 4, 30, 30, both=True)
+    h, r, t = trip[0][:4], trip[1][:4], trip[2][:4]
+    got = O.link_rank(orc, h, r, t, head="both", candidates=list(zip(ent, side)))
+    for i in range(4):
+        ft = _closed_form("distmult", E, R, int(h[i]), int(r[i]), int(t[i]))
+        fs = [_closed_form("distmult", E, R, int(e), int(r[i]), int(t[i])) if sd else
+              _closed_form("distmult", E, R, int(h[i]), int(r[i]), int(e))
+              for e, sd in zip(ent[i], side[i]) if e != (h[i] if sd else t[i])]
+        assert got[i] == 1 + sum(1 for f in fs if f >= ft - 1e-12 * abs(ft))
 
 
 def test_filter_lists_match_set():
