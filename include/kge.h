@@ -161,21 +161,38 @@ int kge_train_batch_async(kge_handle* h, const int64_t* heads, const int64_t* re
 int kge_score(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, float* out);
 
 /* Link-prediction ranks (PAPER.md:652-665 [5.3] evaluation methodology). For each test triple i
- * the true tail (corrupt_head = 0) or head (corrupt_head = 1) is scored against a candidate set C_i with the current
- * tables, candidates and the true triple through the same arithmetic (o = combine(h, r) or combine'(r, t), then the
- * pair score of Table 1). rank_i = 1 + #{e in C_i \ F_i, e != true entity : f(e) >= f(true)} -- ties rank the
- * positive last (reading c.15).
- *   cand_off == NULL: C_i = every entity (first protocol; raw if filt_off == NULL).
- *   cand_off/cand_ids: C_i = cand_ids[cand_off[i] .. cand_off[i+1]) (second protocol: the caller's 1000 uniform +
- *     1000 degree-proportional draws; duplicates count once per occurrence, the true entity is skipped).
- *   filt_off/filt_ids: F_i = filt_ids[filt_off[i] .. filt_off[i+1]) (first protocol, filtered: the corrupted
- *     entities that form a known triple; duplicates removed here). Only with cand_off == NULL, else KGE_EINVAL.
- * Offsets: host int64[n+1] from 0, non-decreasing (KGE_EINVAL otherwise); ids: host int64, each in [0, N_e)
+ * the true entity is scored against its corruptions with the current tables -- candidates and the true triple through
+ * the same arithmetic (o = combine(h, r) or combine'(r, t), then the pair score of Table 1). corrupt_head: 0 = the
+ * tail is replaced, 1 = the head, 2 = both: one list S_i holding the corruptions (h', r, t) AND (h, r, t') (the
+ * paper's first protocol, reading c.15'). rank_i = 1 + #{corruptions c != the positive, not filtered : f(c) >=
+ * f(true)} -- ties rank the positive last (reading c.15).
+ *   cand_off == NULL: every entity corrupts the side(s) (first protocol; raw if filt_off == NULL).
+ *   cand_off/cand_ids: the side's candidates cand_ids[cand_off[i] .. cand_off[i+1]) (duplicates count once per
+ *     occurrence, the true entity is skipped); not with corrupt_head = 2 (KGE_EINVAL: see kge_rank_sampled).
+ *   filt_off/filt_ids: filtered first protocol -- the corrupted entities that form a known triple are removed
+ *     (never scored); per query list i = filt_ids[filt_off[i] .. filt_off[i+1]) (duplicates removed here). With
+ *     corrupt_head = 2 there are 2n lists (offsets [2n+1]): lists 0..n-1 hold the tail side, n..2n-1 the head side.
+ *     Only with cand_off == NULL, else KGE_EINVAL.
+ * Offsets: host int64, from 0, non-decreasing (KGE_EINVAL otherwise); ids: host int64, each in [0, N_e)
  * (KGE_ERANGE otherwise). hs/rs/ts: host int64[n]; ranks_out: host int64[n], owned by the caller. Synchronous.
- * KGE_EUNSUPPORTED for TransR or world_size > 1. MR / MRR / Hit@k follow from the ranks (kge.link_metrics). */
+ * KGE_EUNSUPPORTED for TransR or world_size > 1. */
 int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, int32_t corrupt_head,
              const int64_t* cand_off, const int64_t* cand_ids, const int64_t* filt_off, const int64_t* filt_ids,
              int64_t* ranks_out);
+
+/* Second protocol (PAPER.md:656-658 [5.3]: "2000 negative triplets; 1000 sampled uniformly from the entire set of
+ * negative samples and 1000 sampled proportionally to the degree of the corrupted entities", unfiltered), candidates
+ * drawn on the device (reading c.15'): slot j < n_uniform + n_degree of query i draws u from Philox(ctr = (j/2,
+ * lo32(i), hi32(i), EVAL = 5), key = eval_seed); uniform slots take an entity uniform over N_e (corrupt = 2: a
+ * (side, entity) pair uniform over the 2 N_e corruptions), degree slots a uniform endpoint of the graph's triples (an
+ * entity drawn proportionally to its degree; corrupt = 2: plus a uniform side bit). Ranks as kge_rank over these
+ * candidates (corrupt 0 / 1 / 2 as there). Synchronous; errors as kge_rank, KGE_EINVAL for negative counts. */
+int kge_rank_sampled(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n,
+                     int32_t corrupt, int32_t n_uniform, int32_t n_degree, uint64_t eval_seed, int64_t* ranks_out);
+
+/* Hit@1, Hit@3, Hit@10, MR and MRR of n ranks (PAPER.md:660-664 [5.3] formulas) into out[5] (host). KGE_EINVAL for
+ * n <= 0 or a rank < 1. */
+int kge_link_metrics(const int64_t* ranks, int64_t n, double* out);
 
 /* Read / overwrite rows of a table: 0 entity [N_e x d], 1 relation [N_r x d_r] (d_r = d, or d/2 for RotatE),
  * 2 TransR projection [N_r x d*d], 3 entity Adagrad state [N_e x 1], 4 relation state, 5 projection state.

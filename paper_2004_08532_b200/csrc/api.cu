@@ -1124,20 +1124,16 @@ static int pack_list(const int64_t* off, const int64_t* ids, int64_t n, int64_t 
   return KGE_OK;
 }
 
-int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, int32_t corrupt_head,
-             const int64_t* cand_off, const int64_t* cand_ids, const int64_t* filt_off, const int64_t* filt_ids,
-             int64_t* ranks_out) {
-  if (!h || (n > 0 && (!hs || !rs || !ts || !ranks_out))) { set_error("NULL argument"); return KGE_EINVAL; }
+// validates and narrows the query triples; common to kge_rank / kge_rank_sampled
+static int rank_queries(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n,
+                        int32_t corrupt, std::vector<int32_t>& ids) {
+  if (!h || (n > 0 && (!hs || !rs || !ts))) { set_error("NULL argument"); return KGE_EINVAL; }
   if (h->dims.model == KGE_TRANSR || h->P > 1) {
     set_error("kge_rank: TransR and world_size > 1 are not supported");
     return KGE_EUNSUPPORTED;
   }
-  if (cand_off && filt_off) {
-    set_error("kge_rank: the filter applies to the all-entity protocol only (cand_off must be NULL)");
-    return KGE_EINVAL;
-  }
-  if (n == 0) return KGE_OK;
-  std::vector<int32_t> ids((size_t)3 * n);
+  if (corrupt < 0 || corrupt > 2) { set_error("corrupt_head must be 0 (tail), 1 (head) or 2 (both)"); return KGE_EINVAL; }
+  ids.resize((size_t)3 * n);
   for (int64_t i = 0; i < n; ++i) {
     if (hs[i] < 0 || hs[i] >= h->dims.n_entities || ts[i] < 0 || ts[i] >= h->dims.n_entities || rs[i] < 0 ||
         rs[i] >= h->dims.n_relations) {
@@ -1148,24 +1144,46 @@ int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t*
     ids[n + i] = (int32_t)rs[i];
     ids[2 * n + i] = (int32_t)ts[i];
   }
+  return flush_for_io(h, true);  // lag = 1: rank against the tables with every enqueued update applied
+}
+
+// both sides pooled in one S_i (reading c.15'): rank = 1 + #{tail side >=} + #{head side >=} = r_tail + r_head - 1
+static void pool_sides(const std::vector<int64_t>& r, int64_t n, int32_t corrupt, int64_t* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = corrupt == 2 ? r[(size_t)i] + r[(size_t)(n + i)] - 1 : r[(size_t)i];
+}
+
+int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n, int32_t corrupt_head,
+             const int64_t* cand_off, const int64_t* cand_ids, const int64_t* filt_off, const int64_t* filt_ids,
+             int64_t* ranks_out) {
+  std::vector<int32_t> ids;
+  if (n > 0 && !ranks_out) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (cand_off && filt_off) {
+    set_error("kge_rank: the filter applies to the all-entity protocol only (cand_off must be NULL)");
+    return KGE_EINVAL;
+  }
+  if (cand_off && corrupt_head == 2) {
+    set_error("kge_rank: pooled sides with candidate lists is kge_rank_sampled (the lists carry one side each)");
+    return KGE_EINVAL;
+  }
+  int rc = rank_queries(h, hs, rs, ts, n, corrupt_head, ids);
+  if (rc != KGE_OK || n == 0) return rc;
+  const int nside = corrupt_head == 2 ? 2 : 1;
   std::vector<int64_t> co, fo;
   std::vector<int32_t> cv, fv;
   if (cand_off) {
-    const int rc = pack_list(cand_off, cand_ids, n, h->dims.n_entities, false, co, cv);
+    rc = pack_list(cand_off, cand_ids, n, h->dims.n_entities, false, co, cv);
     if (rc != KGE_OK) return rc;
   }
-  if (filt_off) {
-    const int rc = pack_list(filt_off, filt_ids, n, h->dims.n_entities, true, fo, fv);
+  if (filt_off) {  // pooled sides: 2n lists, the tail side's first
+    rc = pack_list(filt_off, filt_ids, nside * n, h->dims.n_entities, true, fo, fv);
     if (rc != KGE_OK) return rc;
   }
-  const int rj = kge_flush(h);  // lag = 1: rank against the tables with every enqueued update applied
-  if (rj != KGE_OK) return rj;
   // one device block: ids | offsets (8-byte aligned) | list ids | ranks
   const size_t b_ids = (size_t)3 * n * 4, b_co = co.size() * 8, b_fo = fo.size() * 8;
   const size_t o_co = (b_ids + 7) & ~(size_t)7, o_fo = o_co + b_co, o_cv = o_fo + b_fo;
   const size_t o_fv = o_cv + cv.size() * 4, o_out = (o_fv + fv.size() * 4 + 7) & ~(size_t)7;
   char* d = nullptr;
-  CK(cudaMallocAsync((void**)&d, o_out + (size_t)n * 8, h->stream));
+  CK(cudaMallocAsync((void**)&d, o_out + (size_t)nside * n * 8, h->stream));
   CK(cudaMemcpyAsync(d, ids.data(), b_ids, cudaMemcpyHostToDevice, h->stream));
   if (b_co) CK(cudaMemcpyAsync(d + o_co, co.data(), b_co, cudaMemcpyHostToDevice, h->stream));
   if (b_fo) CK(cudaMemcpyAsync(d + o_fo, fo.data(), b_fo, cudaMemcpyHostToDevice, h->stream));
@@ -1173,14 +1191,73 @@ int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t*
   if (!fv.empty()) CK(cudaMemcpyAsync(d + o_fv, fv.data(), fv.size() * 4, cudaMemcpyHostToDevice, h->stream));
   const int32_t* di = reinterpret_cast<const int32_t*>(d);
   int64_t* d_out = reinterpret_cast<int64_t*>(d + o_out);
-  CK(launch_rank(h, di, di + n, di + 2 * n, n, corrupt_head ? 1 : 0,
-                 cand_off ? reinterpret_cast<const int64_t*>(d + o_co) : nullptr,
-                 reinterpret_cast<const int32_t*>(d + o_cv),
-                 filt_off ? reinterpret_cast<const int64_t*>(d + o_fo) : nullptr,
-                 reinterpret_cast<const int32_t*>(d + o_fv), d_out));
-  CK(cudaMemcpyAsync(ranks_out, d_out, (size_t)n * 8, cudaMemcpyDeviceToHost, h->stream));
+  for (int sd = 0; sd < nside; ++sd)
+    CK(launch_rank(h, di, di + n, di + 2 * n, n, nside == 2 ? sd : (corrupt_head ? 1 : 0),
+                   cand_off ? reinterpret_cast<const int64_t*>(d + o_co) : nullptr,
+                   reinterpret_cast<const int32_t*>(d + o_cv),
+                   filt_off ? reinterpret_cast<const int64_t*>(d + o_fo) + (size_t)sd * n : nullptr,
+                   reinterpret_cast<const int32_t*>(d + o_fv), d_out + (size_t)sd * n));
+  std::vector<int64_t> r((size_t)nside * n);
+  CK(cudaMemcpyAsync(r.data(), d_out, (size_t)nside * n * 8, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaFreeAsync(d, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  pool_sides(r, n, corrupt_head, ranks_out);
+  return KGE_OK;
+}
+
+int kge_rank_sampled(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n,
+                     int32_t corrupt, int32_t n_uniform, int32_t n_degree, uint64_t eval_seed, int64_t* ranks_out) {
+  std::vector<int32_t> ids;
+  if (n > 0 && !ranks_out) { set_error("NULL argument"); return KGE_EINVAL; }
+  if (n_uniform < 0 || n_degree < 0 || (int64_t)n_uniform + n_degree > (1 << 24)) {
+    set_error("n_uniform, n_degree must be >= 0 with a sum <= 2^24");
+    return KGE_EINVAL;
+  }
+  int rc = rank_queries(h, hs, rs, ts, n, corrupt, ids);
+  if (rc != KGE_OK || n == 0) return rc;
+  const int nside = corrupt == 2 ? 2 : 1;
+  const int64_t m = (int64_t)n_uniform + n_degree;
+  std::vector<int64_t> co((size_t)n + 1);
+  for (int64_t i = 0; i <= n; ++i) co[(size_t)i] = i * m;
+  // one device block: ids | offsets | candidates of side 0 | of side 1 | ranks
+  const size_t b_ids = ((size_t)3 * n * 4 + 7) & ~(size_t)7, b_co = co.size() * 8, b_c = (size_t)n * m * 4;
+  const size_t o_co = b_ids, o_c0 = o_co + b_co, o_c1 = o_c0 + b_c, o_out = (o_c1 + (nside - 1) * b_c + 7) & ~(size_t)7;
+  char* d = nullptr;
+  CK(cudaMallocAsync((void**)&d, o_out + (size_t)nside * n * 8, h->stream));
+  CK(cudaMemcpyAsync(d, ids.data(), (size_t)3 * n * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(d + o_co, co.data(), b_co, cudaMemcpyHostToDevice, h->stream));
+  int32_t* c0 = reinterpret_cast<int32_t*>(d + o_c0);
+  int32_t* c1 = nside == 2 ? reinterpret_cast<int32_t*>(d + o_c1) : nullptr;
+  CK(launch_eval_cand(h, n, n_uniform, n_degree, corrupt == 2 ? 1 : 0, eval_seed, c0, c1));
+  const int32_t* di = reinterpret_cast<const int32_t*>(d);
+  int64_t* d_out = reinterpret_cast<int64_t*>(d + o_out);
+  for (int sd = 0; sd < nside; ++sd)
+    CK(launch_rank(h, di, di + n, di + 2 * n, n, nside == 2 ? sd : (corrupt ? 1 : 0),
+                   reinterpret_cast<const int64_t*>(d + o_co), sd ? c1 : c0, nullptr, nullptr, d_out + (size_t)sd * n));
+  std::vector<int64_t> r((size_t)nside * n);
+  CK(cudaMemcpyAsync(r.data(), d_out, (size_t)nside * n * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaFreeAsync(d, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  pool_sides(r, n, corrupt, ranks_out);
+  return KGE_OK;
+}
+
+int kge_link_metrics(const int64_t* ranks, int64_t n, double* out) {
+  if (!ranks || !out || n <= 0) { set_error("kge_link_metrics: empty rank list or NULL argument"); return KGE_EINVAL; }
+  double h1 = 0, h3 = 0, h10 = 0, mr = 0, mrr = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (ranks[i] < 1) { set_error("ranks must be >= 1"); return KGE_EINVAL; }
+    h1 += ranks[i] <= 1;
+    h3 += ranks[i] <= 3;
+    h10 += ranks[i] <= 10;
+    mr += (double)ranks[i];
+    mrr += 1.0 / (double)ranks[i];
+  }
+  out[0] = h1 / n;
+  out[1] = h3 / n;
+  out[2] = h10 / n;
+  out[3] = mr / n;
+  out[4] = mrr / n;
   return KGE_OK;
 }
 

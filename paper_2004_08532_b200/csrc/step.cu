@@ -1539,20 +1539,11 @@ __device__ __forceinline__ float cmod1(const float* o, const float* x, int c, in
   return sqrtf(ur * ur + ui * ui);
 }
 
-// pair statistic of o (shared memory) and an entity row x, reduced over the warp (families of step.cu)
-__device__ __forceinline__ float pair_stat_row(int fam, const float* o, const float* __restrict__ x, int d, int lane) {
-  float st = 0.f;
-  if (fam == FAM_CMOD) {
-    for (int c = lane; c < (d >> 1); c += 32) st += cmod1(o, x, c, d >> 1);
-  } else {
-    for (int v = lane; v < (d >> 2); v += 32) st += stat4(fam, reinterpret_cast<const float4*>(o)[v], ld4(x, v));
-  }
-  return warp_sum(st);
-}
-
-// the same statistic of one entity row against QB query rows o_q = osm + q*dp: the row is read once for all queries
+// the same statistic of one entity row against QB query rows o_q = osm + q*dp: the row is read once for all queries.
+// Not inlined: the positive's own score and every candidate's come out of this one compiled body, so a candidate
+// whose row equals the positive's ties it bit-exactly (pessimistic ties, reading c.15)
 template <int QB>
-__device__ __forceinline__ void pair_stat_rows(int fam, const float* osm, int dp, const float* __restrict__ x, int d,
+__device__ __noinline__ void pair_stat_rows(int fam, const float* osm, int dp, const float* __restrict__ x, int d,
                                                int lane, float (&st)[QB]) {
 #pragma unroll
   for (int q = 0; q < QB; ++q) st[q] = 0.f;
@@ -1596,10 +1587,18 @@ __global__ void __launch_bounds__(256) k_rank(RankArgs a, int64_t n) {
     const float* r = a.rel + (int64_t)a.rs[i] * dm.drel;
     float st, on;
     combine_row(dm.model, mode, h, r, t, osm + warp * dm.dp, dm.d, lane, mode == 0 ? t : h, dm.family, st, on);
-    __syncwarp();
-    const float sp = pair_stat_row(dm.family, osm + warp * dm.dp, mode == 0 ? t : h, dm.d, lane);
+  }
+  __syncthreads();  // every o_q is in shared memory
+  if (warp < nq) {  // the positive's score through the candidates' arithmetic
+    const int64_t i = i0 + warp;
+    float sp[QB];
+    pair_stat_rows<QB>(dm.family, osm, dm.dp, a.ent.row(mode == 0 ? a.ts[i] : a.hs[i]), dm.d, lane, sp);
+    float mine = sp[0];
+#pragma unroll
+    for (int q = 1; q < QB; ++q)
+      if (q == warp) mine = sp[q];
     if (lane == 0) {
-      s_true[warp] = pair_score_from(dm.family, sp, dm.gamma);
+      s_true[warp] = pair_score_from(dm.family, mine, dm.gamma);
       s_tid[warp] = mode == 0 ? a.ts[i] : a.hs[i];
     }
   }
@@ -1616,23 +1615,32 @@ __global__ void __launch_bounds__(256) k_rank(RankArgs a, int64_t n) {
     lo = per * split;
     hi = min(hi, lo + per);
   }
+  // filtered protocol: a known triple among the candidates is skipped, never scored -- each warp walks its queries'
+  // sorted filter lists with a cursor that only moves forward (its candidates ascend), so the filter decision does
+  // not depend on a second evaluation of the score
+  int64_t fc[QB], fe[QB];
+#pragma unroll
+  for (int q = 0; q < QB; ++q) {
+    fc[q] = fe[q] = 0;
+    if (a.filt_off && q < nq) {
+      fc[q] = a.filt_off[i0 + q];
+      fe[q] = a.filt_off[i0 + q + 1];
+      while (fc[q] < fe[q] && a.filt[fc[q]] < lo + warp) ++fc[q];
+    }
+  }
   for (int64_t j = lo + warp; j < hi; j += 8) {
     const int64_t e = a.cand_off ? (int64_t)a.cand[j] : j;
+    if (e < 0) continue;  // a sampled slot that belongs to the other corrupted side
     float st[QB];
     pair_stat_rows<QB>(dm.family, osm, dm.dp, a.ent.row(e), dm.d, lane, st);
 #pragma unroll
-    for (int q = 0; q < QB; ++q)
-      if (q < nq && e != s_tid[q]) cnt[q] += pair_score_from(dm.family, st[q], dm.gamma) >= s_true[q] ? 1 : 0;
-  }
-  if (a.filt_off && split == 0) {  // filtered protocol: known triples among the candidates do not count
-    for (int q = 0; q < nq; ++q) {
-      for (int64_t j = a.filt_off[i0 + q] + warp; j < a.filt_off[i0 + q + 1]; j += 8) {
-        const int64_t e = a.filt[j];
-        if (e == s_tid[q]) continue;
-        const float f = pair_score_from(dm.family, pair_stat_row(dm.family, osm + q * dm.dp, a.ent.row(e), dm.d, lane),
-                                        dm.gamma);
-        cnt[q] -= f >= s_true[q] ? 1 : 0;
+    for (int q = 0; q < QB; ++q) {
+      bool skip = q >= nq || e == s_tid[q];
+      if (a.filt_off && q < nq) {
+        while (fc[q] < fe[q] && a.filt[fc[q]] < e) ++fc[q];
+        skip |= fc[q] < fe[q] && a.filt[fc[q]] == e;
       }
+      if (!skip) cnt[q] += pair_score_from(dm.family, st[q], dm.gamma) >= s_true[q] ? 1 : 0;
     }
   }
   if (lane == 0) {
@@ -1649,6 +1657,51 @@ __global__ void __launch_bounds__(256) k_rank(RankArgs a, int64_t n) {
       atomicAdd(reinterpret_cast<unsigned long long*>(a.ranks + i0 + threadIdx.x),
                 (unsigned long long)(c + (split == 0 ? 1 : 0)));
   }
+}
+
+// Second-protocol candidates (reading c.15'): slot j of query i draws u from Philox(ctr=(j/2,
+// lo32(i), hi32(i), EVAL), key = eval seed); uniform slots: an entity (both sides: a (side, entity) pair) uniform;
+// degree slots: a uniform endpoint of the graph's triples (both sides: and a side bit). Writes the entity into the
+// list of its side and -1 into the other's (both = 0: side 0 only).
+__global__ void k_eval_cand(int64_t n, int32_t m, int32_t n_uniform, int32_t both, uint32_t k0, uint32_t k1,
+                            int64_t n_ent, int64_t n_trip, const int32_t* __restrict__ th,
+                            const int32_t* __restrict__ tt, int32_t* __restrict__ cand_t, int32_t* __restrict__ cand_h) {
+  const int64_t total = n * m;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / m;
+    const int32_t j = (int32_t)(q - i * m);
+    const uint4 o = philox4x32_10(make_uint4((uint32_t)j >> 1, (uint32_t)i, (uint32_t)((uint64_t)i >> 32), kTagEval),
+                                  k0, k1);
+    const uint64_t u = (j & 1) ? (((uint64_t)o.w << 32) | o.z) : (((uint64_t)o.y << 32) | o.x);
+    const uint64_t range = j < n_uniform ? (uint64_t)n_ent * (both ? 2u : 1u) : (uint64_t)n_trip * (both ? 4u : 2u);
+    uint64_t p = __umul64hi(u, range);
+    int side = 0;
+    if (both) {
+      side = (int)(p & 1u);
+      p >>= 1;
+    }
+    int32_t e;
+    if (j < n_uniform) {
+      e = (int32_t)p;
+    } else {
+      const int64_t tq = (int64_t)(p >> 1);
+      e = (p & 1u) ? tt[tq] : th[tq];
+    }
+    cand_t[q] = side == 0 ? e : -1;
+    if (cand_h) cand_h[q] = side == 1 ? e : -1;
+  }
+}
+
+cudaError_t launch_eval_cand(kge_handle* h, int64_t n, int32_t n_uniform, int32_t n_degree, int32_t both,
+                             uint64_t seed, int32_t* cand_t, int32_t* cand_h) {
+  const int64_t total = n * (int64_t)(n_uniform + n_degree);
+  const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (total == 0) return cudaSuccess;
+  k_eval_cand<<<grid, 256, 0, h->stream>>>(n, n_uniform + n_degree, n_uniform, both, (uint32_t)seed,
+                                          (uint32_t)(seed >> 32), h->dims.n_entities, h->n_triples, h->th, h->tt,
+                                          cand_t, cand_h);
+  ++h->launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rank(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, int head,

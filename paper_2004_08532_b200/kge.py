@@ -81,6 +81,9 @@ def lib():
         L.kge_score.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, _fp]
         L.kge_rank.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int32, _i64p, _i64p,
                                _i64p, _i64p, _i64p]
+        L.kge_rank_sampled.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int32,
+                                       ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, _i64p]
+        L.kge_link_metrics.argtypes = [_i64p, ctypes.c_int64, P(ctypes.c_double)]
         L.kge_get_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_set_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_table_width.argtypes = [ctypes.c_void_p, ctypes.c_int32]
@@ -269,26 +272,36 @@ class Handle:
 
     # kge_rank
     def rank(self, hs, rs, ts, head=False, candidates=None, filters=None):
-        """Link-prediction ranks (PAPER.md:652-665 [5.3]) of the true tail (head=True: head). candidates / filters:
-        None or a CSR pair (offsets[n+1], ids) -- see kge_rank in include/kge.h."""
+        """Link-prediction ranks (PAPER.md:652-665 [5.3]) of the true tail (head=True: head; head="both": one list with
+        both corruption sides). candidates / filters: None or a CSR pair (offsets, ids) -- see kge_rank in
+        include/kge.h (head="both": 2n filter lists, the tail side's first)."""
         hs, rs, ts = _i64(hs), _i64(rs), _i64(ts)
         if not (len(hs) == len(rs) == len(ts)):
             raise ValueError("hs, rs, ts must have the same length")
+        side = 2 if isinstance(head, str) and head == "both" else (1 if head else 0)
         out = np.zeros(len(hs), np.int64)
         co, ci = (None, None) if candidates is None else (_i64(candidates[0]), _i64(candidates[1]))
         fo, fi = (None, None) if filters is None else (_i64(filters[0]), _i64(filters[1]))
-        for name, off, ids in (("candidates", co, ci), ("filters", fo, fi)):
-            # CSR size contract of kge_rank: offsets[n + 1] from 0, non-decreasing, ids[offsets[-1]]
+        for name, off, ids, nl in (("candidates", co, ci, len(hs)), ("filters", fo, fi, len(hs) * (2 if side == 2 else 1))):
+            # CSR size contract of kge_rank: offsets[n_lists + 1], ids[max offset] (value errors: the library)
             if off is None:
                 continue
-            if off.ndim != 1 or len(off) != len(hs) + 1:
-                raise ValueError(f"{name}: offsets must have n + 1 = {len(hs) + 1} entries, got {off.shape}")
-            # (offsets that do not start at 0 or decrease are rejected by the library: KGE_EINVAL)
+            if off.ndim != 1 or len(off) != nl + 1:
+                raise ValueError(f"{name}: offsets must have {nl + 1} entries, got {off.shape}")
             if len(ids) < max(int(off.max()), 0):
-                raise ValueError(f"{name}: {len(ids)} ids but offsets end at {off[-1]}")
+                raise ValueError(f"{name}: {len(ids)} ids but offsets reach {off.max()}")
         p = lambda a: None if a is None else _ptr(a, ctypes.c_int64)
-        _check(lib().kge_rank(self._h, p(hs), p(rs), p(ts), len(hs), 1 if head else 0, p(co), p(ci), p(fo), p(fi),
-                              p(out)))
+        _check(lib().kge_rank(self._h, p(hs), p(rs), p(ts), len(hs), side, p(co), p(ci), p(fo), p(fi), p(out)))
+        return out
+
+    # kge_rank_sampled
+    def rank_sampled(self, hs, rs, ts, head=False, n_uniform=1000, n_degree=1000, seed=0):
+        """Second protocol: candidates drawn on the device (reading c.15')."""
+        hs, rs, ts = _i64(hs), _i64(rs), _i64(ts)
+        side = 2 if isinstance(head, str) and head == "both" else (1 if head else 0)
+        out = np.zeros(len(hs), np.int64)
+        p = lambda a: _ptr(a, ctypes.c_int64)
+        _check(lib().kge_rank_sampled(self._h, p(hs), p(rs), p(ts), len(hs), side, n_uniform, n_degree, seed, p(out)))
         return out
 
     # kge_score
@@ -458,15 +471,21 @@ def init_local_group(cfg: Config, world_size: int, heads, rels, tails):
 
 
 def link_metrics(ranks):
-    """MR, MRR and Hit@1/3/10 of link-prediction ranks (PAPER.md:652-665 [5.3])."""
-    r = np.asarray(ranks, dtype=np.float64)
-    return {"MR": float(r.mean()), "MRR": float((1.0 / r).mean()), "Hit@1": float((r <= 1).mean()),
-            "Hit@3": float((r <= 3).mean()), "Hit@10": float((r <= 10).mean())}
+    """Hit@1/3/10, MR, MRR (PAPER.md:660-664 [5.3]), computed by the library (kge_link_metrics)."""
+    r = _i64(ranks)
+    out = np.zeros(5, np.float64)
+    _check(lib().kge_link_metrics(_ptr(r, ctypes.c_int64), len(r), out.ctypes.data_as(P(ctypes.c_double))))
+    return dict(zip(["Hit@1", "Hit@3", "Hit@10", "MR", "MRR"], out.tolist()))
 
 
 def filter_lists(known, hs, rs, ts, head=False):
     """CSR filter lists of the first protocol (PAPER.md:654-655 [5.3]): for query i, the entities e such that the
-    corrupted triple (h_i, r_i, e) -- head=True: (e, r_i, t_i) -- is a known triple. known: (heads, rels, tails)."""
+    corrupted triple (h_i, r_i, e) -- head=True: (e, r_i, t_i) -- is a known triple. known: (heads, rels, tails).
+    head="both": the 2n lists of kge_rank's pooled protocol (the tail side's n lists, then the head side's)."""
+    if isinstance(head, str) and head == "both":
+        ot, it = filter_lists(known, hs, rs, ts, head=False)
+        oh, ih = filter_lists(known, hs, rs, ts, head=True)
+        return np.concatenate([ot, oh[1:] + ot[-1]]), np.concatenate([it, ih])
     kh, kr, kt = (np.asarray(a, np.int64) for a in known)
     fixed_a, fixed_b, free = (kr, kt, kh) if head else (kh, kr, kt)
     qa, qb = (np.asarray(rs, np.int64), np.asarray(ts, np.int64)) if head else (np.asarray(hs, np.int64),
@@ -480,15 +499,3 @@ def filter_lists(known, hs, rs, ts, head=False):
     off[1:] = np.cumsum(hi - lo)
     ids = np.concatenate([kf[a:b] for a, b in zip(lo, hi)]) if len(qk) else np.zeros(0, np.int64)
     return off, ids
-
-
-def sampled_candidates(n_queries, degree, n_uniform=1000, n_degree=1000, seed=0):
-    """Candidate lists of the second protocol (PAPER.md:656-658 [5.3]): per query n_uniform entities drawn uniformly
-    and n_degree drawn proportionally to the entity degree, with replacement, unfiltered (reading c.15)."""
-    degree = np.asarray(degree, np.float64)
-    rng = np.random.default_rng(seed)
-    uni = rng.integers(0, len(degree), (n_queries, n_uniform))
-    cdf = np.cumsum(degree)
-    deg = np.searchsorted(cdf, rng.random((n_queries, n_degree)) * cdf[-1], "right")
-    ids = np.concatenate([uni, np.minimum(deg, len(degree) - 1)], axis=1).reshape(-1)
-    return np.arange(n_queries + 1, dtype=np.int64) * (n_uniform + n_degree), ids.astype(np.int64)

@@ -91,19 +91,83 @@ def test_ranks_entity_split(model, head):
 
 
 @pytest.mark.parametrize("model", ["transe_l2", "distmult", "rotate"])
-def test_ranks_sampled_protocol(model):
+@pytest.mark.parametrize("side", [False, True, "both"])
+def test_ranks_sampled_protocol(model, side):
+    # second protocol, candidates drawn on the device (reading c.15'); the oracle draws the same counter-based ids
     gr, trip, gpu, orc = _trained(model)
     test = np.random.default_rng(12).integers(0, gr.n_triples, 16)
     hs, rs, ts = trip[0][test], trip[1][test], trip[2][test]
-    deg = np.bincount(np.concatenate([trip[0], trip[2]]), minlength=gr.n_entities)
-    off, ids = kge.sampled_candidates(len(test), deg, seed=3)
-    got = gpu.rank(hs, rs, ts, candidates=(off, ids))
-    cands = [ids[off[i]:off[i + 1]] for i in range(len(test))]
-    ref = O.link_rank(orc, hs, rs, ts, candidates=cands)
+    got = gpu.rank_sampled(hs, rs, ts, head=side, n_uniform=1000, n_degree=1000, seed=3)
+    ent, sd = O.eval_candidates(3, gr.n_entities, trip[0], trip[2], len(test), 1000, 1000, both=side == "both")
+    if side == "both":
+        ref = O.link_rank(orc, hs, rs, ts, head="both", candidates=list(zip(ent, sd)))
+    else:
+        ref = O.link_rank(orc, hs, rs, ts, head=side, candidates=list(ent))
     for i in range(len(test)):
-        near = _near_ties(orc, gr.n_entities, hs[i], rs[i], ts[i], False, cands[i])
+        near = 0
+        for hd in ((False, True) if side == "both" else (side,)):
+            c = ent[i][sd[i] == (1 if hd else 0)] if side == "both" else ent[i]
+            near += _near_ties(orc, gr.n_entities, hs[i], rs[i], ts[i], hd, c)
         assert abs(int(got[i]) - int(ref[i])) <= near, (i, got[i], ref[i], near)
     assert np.all(got >= 1) and np.all(got <= 2001)
+
+
+@pytest.mark.parametrize("model", ["transe_l2", "distmult"])
+def test_ranks_both_sides_one_list(model):
+    # first protocol as PAPER.md:654-655 states it: S_i = the corruptions (h', r, t) and (h, r, t'), raw and filtered
+    gr, trip, gpu, orc = _trained(model)
+    test = np.random.default_rng(13).integers(0, gr.n_triples, 20)
+    hs, rs, ts = trip[0][test], trip[1][test], trip[2][test]
+    known = set(zip(*(a.tolist() for a in trip)))
+    raw = gpu.rank(hs, rs, ts, head="both")
+    fil = gpu.rank(hs, rs, ts, head="both", filters=kge.filter_lists(trip, hs, rs, ts, head="both"))
+    ref_raw = O.link_rank(orc, hs, rs, ts, head="both")
+    ref_fil = O.link_rank(orc, hs, rs, ts, head="both", known=known)
+    for i in range(len(test)):
+        near = sum(_near_ties(orc, gr.n_entities, hs[i], rs[i], ts[i], hd) for hd in (False, True))
+        assert abs(int(raw[i]) - int(ref_raw[i])) <= near and abs(int(fil[i]) - int(ref_fil[i])) <= near, i
+    assert np.all(fil <= raw) and np.all(raw <= 2 * gr.n_entities - 1)
+
+
+@pytest.mark.parametrize("model", ["transe_l2", "distmult", "complex"])
+def test_ranks_production_dim_and_filtered_ties(model):
+    # d = 400 (configs[1]/[4]) on the FB15k-sized entity set (entity-split path), plus planted exact ties under a
+    # filter: entities whose rows equal the true entity's tie it bit-exactly (pessimistic: they rank above it) unless
+    # filtered, in which case they are never scored
+    gr = synth.graph("fb15k")
+    trip = gr.triples()
+    cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=400, batch_size=1024,
+                     chunk_size=256, neg_k=256, gamma=12.0, lr=0.1, seed=4, neg_precision="fp32")
+    gpu = kge.init(cfg, *trip)
+    gpu.train_step(3)
+    orc = O.Trainer(model, gr.n_entities, gr.n_relations, 400, 1024, 256, 256, gamma=12.0, lr=0.1, seed=4,
+                    triples=trip)
+    test = np.random.default_rng(5).integers(0, gr.n_triples, 10)
+    hs, rs, ts = trip[0][test], trip[1][test], trip[2][test]
+    # plant: copy the true tail's row of query 0 onto 3 other entities; filter 2 of them
+    twins = [e for e in (11, 222, 3333) if e not in (int(ts[0]), int(hs[0]))]
+    gpu.set_rows(0, twins, np.repeat(gpu.get_rows(0, [ts[0]]), len(twins), 0))
+    for table, n in ((0, gr.n_entities), (1, gr.n_relations)):
+        ids = np.arange(n)
+        orc.set_rows(table, ids, gpu.get_rows(table, ids).astype(np.float64))
+    off, ids = kge.filter_lists(trip, hs, rs, ts)
+    lists = [list(ids[off[i]:off[i + 1]]) for i in range(len(test))]
+    lists[0] += twins[:2]
+    off = np.concatenate([[0], np.cumsum([len(x) for x in lists])]).astype(np.int64)
+    ids = np.concatenate([np.asarray(x, np.int64) for x in lists])
+    fil = gpu.rank(hs, rs, ts, filters=(off, ids))
+    raw = gpu.rank(hs, rs, ts)
+    known = {(int(hs[i]), int(rs[i]), int(e)) for i in range(len(test)) for e in lists[i]}
+    ref_fil = O.link_rank(orc, hs, rs, ts, known=known)
+    ref_raw = O.link_rank(orc, hs, rs, ts)
+    for i in range(len(test)):
+        near = _near_ties(orc, gr.n_entities, hs[i], rs[i], ts[i], False)
+        if i == 0:
+            near -= len(twins)  # the exact twins are decided exactly (bit-equal scores), not near-ties
+        assert abs(int(raw[i]) - int(ref_raw[i])) <= near and abs(int(fil[i]) - int(ref_fil[i])) <= near, (i, raw[i],
+                                                                                                           ref_raw[i])
+    # the unfiltered twin ties the positive and ranks above it; the filtered ones never count
+    assert raw[0] - fil[0] >= 2
 
 
 def test_rank_planted_and_errors():
