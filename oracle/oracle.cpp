@@ -31,7 +31,7 @@ int threads() {
 // ------------------------------------------------------------------------------------------------
 const uint32_t PHILOX_M0 = 0xD2511F53u, PHILOX_M1 = 0xCD9E8D57u;
 const uint32_t PHILOX_W0 = 0x9E3779B9u, PHILOX_W1 = 0xBB67AE85u;
-const uint32_t TAG_NEG = 1, TAG_PERM = 2, TAG_INIT = 3, TAG_DEG = 4, TAG_EVAL = 5;
+const uint32_t TAG_NEG = 1, TAG_PERM = 2, TAG_INIT = 3, TAG_DEG = 4, TAG_EVAL = 5, TAG_REPART = 6;
 
 void philox(const uint32_t in[4], const uint32_t key_in[2], uint32_t out[4]) {
   uint32_t x0 = in[0], x1 = in[1], x2 = in[2], x3 = in[3];
@@ -418,11 +418,24 @@ struct RowStore {
   }
 };
 
+// c.13' per-epoch randomisation (PAPER.md:497-501 [3.4]: "we introduce randomization in the partitioning algorithm
+// and at the start of each epoch we compute a somewhat different relation partitioning"; SPEC.md reshuffle_partition:
+// ties broken by a seed- and epoch-dependent permutation, SPLIT set unchanged): the sort key of relation r in epoch e.
+uint32_t repart_key(uint64_t seed, uint32_t epoch, int64_t r) {
+  uint32_t key[2];
+  seed_key(seed, key);
+  uint32_t ctr[4] = {(uint32_t)r, epoch, 0u, TAG_REPART}, o[4];
+  philox(ctr, key, o);
+  return o[0];
+}
+
 // c.13 relation partition (PAPER.md:484-492 [3.4]): relations with count > N_t/P are SPLIT and their
 // triples dealt round-robin (per relation, ascending triple index); the rest sorted by (count desc, id asc)
 // and each given to the currently lightest rank (ties -> lowest rank). Loads start from the dealt split triples.
+// With `randomise` the non-split order is (count desc, repart_key(seed, epoch, r) asc, id asc) (c.13').
 int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<int32_t>& owner,
-                           std::vector<int64_t>& counts) {
+                           std::vector<int64_t>& counts, bool randomise = false, uint64_t seed = 0,
+                           uint32_t epoch = 0) {
   counts.assign((size_t)nr, 0);
   for (int64_t i = 0; i < nt; ++i) counts[(size_t)rels[i]]++;
   owner.assign((size_t)nr, 0);
@@ -439,8 +452,12 @@ int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t 
       order.push_back(r);
     }
   }
+  std::vector<uint32_t> key((size_t)nr, 0u);
+  if (randomise)
+    for (int64_t r : order) key[(size_t)r] = repart_key(seed, epoch, r);
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
     if (counts[(size_t)a] != counts[(size_t)b]) return counts[(size_t)a] > counts[(size_t)b];
+    if (key[(size_t)a] != key[(size_t)b]) return key[(size_t)a] < key[(size_t)b];
     return a < b;
   });
   for (int64_t r : order) {
@@ -453,7 +470,8 @@ int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t 
   return n_split;
 }
 
-void rank_lists(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<std::vector<int64_t>>& lists) {
+void rank_lists(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<std::vector<int64_t>>& lists,
+                bool randomise = false, uint64_t seed = 0, uint32_t epoch = 0) {
   lists.assign((size_t)P, {});
   if (P == 1) {
     lists[0].resize((size_t)nt);
@@ -462,7 +480,7 @@ void rank_lists(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vec
   }
   std::vector<int32_t> owner;
   std::vector<int64_t> counts;
-  relation_partition(rels, nt, nr, P, owner, counts);
+  relation_partition(rels, nt, nr, P, owner, counts, randomise, seed, epoch);
   std::vector<int64_t> dealt((size_t)nr, 0);
   for (int64_t i = 0; i < nt; ++i) {
     int64_t r = rels[i];
@@ -504,6 +522,23 @@ struct Base {
   int64_t nt = 0;
   std::vector<std::vector<int64_t>> lists;  // per-rank triple index lists (empty lists[0] -> identity)
   bool identity_list = false;
+  // c.13' (cfg.repartition, P > 1): epochs of S_E = ceil(N_t / (P B)) steps on every rank, the partition of epoch e
+  // recomputed with the epoch's keys; lists cached for epoch cur_epoch
+  std::vector<int64_t> RR;  // relation of every triple
+  mutable std::vector<std::vector<int64_t>> ep_lists;
+  mutable int64_t cur_epoch = -1;
+  bool repart() const { return cfg.repartition && cfg.world_size > 1; }
+  int64_t epoch_steps() const {
+    const int64_t pb = (int64_t)cfg.world_size * cfg.batch;
+    return (nt + pb - 1) / pb;
+  }
+  const std::vector<int64_t>& epoch_list(int64_t e, int32_t rank) const {
+    if (e != cur_epoch) {
+      rank_lists(RR.data(), nt, cfg.n_relations, cfg.world_size, ep_lists, true, cfg.seed, (uint32_t)e);
+      cur_epoch = e;
+    }
+    return ep_lists[(size_t)rank];
+  }
   int64_t step = 0;
   virtual ~Base() {}
   virtual int train(int64_t n, double* losses) = 0;
@@ -528,12 +563,22 @@ struct Base {
   // c.2 + c.3 + c.4
   void sample(int64_t s, int32_t rank, int64_t* pos, int64_t* neg, int8_t* mode) const {
     const int64_t B = cfg.batch, k = cfg.neg_k;
-    int64_t nl = list_size(rank);
-    for (int64_t i = 0; i < B; ++i) {
-      uint64_t q = (uint64_t)s * (uint64_t)B + (uint64_t)i;
-      uint32_t e = (uint32_t)(q / (uint64_t)nl);
-      uint64_t p = q % (uint64_t)nl;
-      pos[i] = list_at(rank, (int64_t)feistel_index((uint64_t)nl, cfg.seed, e, p));
+    if (repart()) {  // c.13': epoch e = s / S_E on every rank, position within the epoch wraps on this epoch's list
+      const int64_t SE = epoch_steps(), e = s / SE;
+      const std::vector<int64_t>& l = epoch_list(e, rank);
+      const uint64_t nl = l.size();
+      for (int64_t i = 0; i < B; ++i) {
+        const uint64_t q = (uint64_t)(s - e * SE) * (uint64_t)B + (uint64_t)i;
+        pos[i] = l[(size_t)feistel_index(nl, cfg.seed, (uint32_t)e, q % nl)];
+      }
+    } else {
+      int64_t nl = list_size(rank);
+      for (int64_t i = 0; i < B; ++i) {
+        uint64_t q = (uint64_t)s * (uint64_t)B + (uint64_t)i;
+        uint32_t e = (uint32_t)(q / (uint64_t)nl);
+        uint64_t p = q % (uint64_t)nl;
+        pos[i] = list_at(rank, (int64_t)feistel_index((uint64_t)nl, cfg.seed, e, p));
+      }
     }
     for (int32_t c = 0; c < C(); ++c) {
       uint32_t cg = (uint32_t)(rank * C() + c);
@@ -900,6 +945,14 @@ int32_t orc_relation_partition(const int64_t* rels, int64_t n_triples, int64_t n
   for (int64_t r = 0; r < n_rel; ++r) owner_out[r] = owner[(size_t)r];
   return ns;
 }
+int32_t orc_relation_partition_epoch(const int64_t* rels, int64_t n_triples, int64_t n_rel, int32_t P, uint64_t seed,
+                                     uint32_t epoch, int32_t* owner_out) {
+  std::vector<int32_t> owner;
+  std::vector<int64_t> counts;
+  int32_t ns = relation_partition(rels, n_triples, n_rel, P, owner, counts, true, seed, epoch);
+  for (int64_t r = 0; r < n_rel; ++r) owner_out[r] = owner[(size_t)r];
+  return ns;
+}
 int64_t orc_rank_triples(const int64_t* rels, int64_t n_triples, int64_t n_rel, int32_t P, int32_t rank,
                          int64_t* idx_out) {
   std::vector<std::vector<int64_t>> lists;
@@ -1012,6 +1065,7 @@ void* orc_create(const orc_config* cfg, const int64_t* heads, const int64_t* rel
         delete b;
         return nullptr;
       }
+    b->RR.swap(rr);
   }
   return b;
 }

@@ -52,6 +52,8 @@ typedef struct {
   int32_t neg_local;        /* 1: uniform negatives of rank w are drawn from its own entity shard {e : e mod P == w}
                                ("local" negatives; no remote rows for them) */
   int32_t loss;             /* ORC_LOSS_LOGISTIC (c.9) or ORC_LOSS_PAIRWISE (c.9') */
+  int32_t repartition;      /* 1 with world_size > 1: a randomised relation partition per epoch of ceil(N_t/(P B))
+                               steps (reading c.13') */
 } orc_config;
 enum { ORC_LOSS_LOGISTIC = 0, ORC_LOSS_PAIRWISE = 1 };
 
@@ -69,6 +71,9 @@ float orc_default_bound(float gamma, int32_t dim);
 int32_t orc_relation_partition(const int64_t* rels, int64_t n_triples, int64_t n_rel, int32_t P,
                                int32_t* owner_out);
 /* triple indices of `rank` (ascending). Returns count; idx_out may be NULL (count only). */
+/* c.13' the randomised partition of epoch `epoch` */
+int32_t orc_relation_partition_epoch(const int64_t* rels, int64_t n_triples, int64_t n_rel, int32_t P, uint64_t seed,
+                                     uint32_t epoch, int32_t* owner_out);
 int64_t orc_rank_triples(const int64_t* rels, int64_t n_triples, int64_t n_rel, int32_t P, int32_t rank,
                          int64_t* idx_out);
 

@@ -162,6 +162,68 @@ def test_relation_partition_is_a_partition_and_balanced():
         assert max(loads) - min(loads) <= non_split_max + 1
 
 
+def test_relation_partition_hand_worked_split_p3():
+    # hand-worked (reading c.13), independent of SPEC's example: counts [10, 3, 2, 2, 1], P = 3, N_t = 18 > 6 * ...
+    # relation 0 (10 > 18/3) is SPLIT and dealt round-robin -> loads [4, 3, 3]; the rest by (count desc, id asc) to the
+    # lightest rank (ties -> lowest): r1 -> 1 [4,6,3], r2 -> 2 [4,6,5], r3 -> 0 [6,6,5], r4 -> 2 [6,6,6]
+    rels = np.repeat(np.arange(5), [10, 3, 2, 2, 1])
+    owner, ns = O.relation_partition(rels, 5, 3)
+    assert ns == 1 and owner.tolist() == [-1, 1, 2, 0, 2]
+    lists = [O.rank_triples(rels, 5, 3, w) for w in range(3)]
+    assert [len(x) for x in lists] == [6, 6, 6]
+    assert lists[0].tolist() == [0, 3, 6, 9, 15, 16]  # dealt 0, 3, 6, 9 of relation 0, then relation 3 (15, 16)
+
+
+def test_epoch_repartition_randomised_and_consistent():
+    # c.13': each epoch's partition is a partition with the same SPLIT set and the greedy balance
+    # bound; epochs differ where equal counts leave the greedy order free
+    rng = np.random.default_rng(5)
+    n_rel = 200
+    rels = np.minimum(rng.zipf(1.3, 30000) - 1, n_rel - 1)
+    counts = np.bincount(rels, minlength=n_rel)
+    for P in (2, 4, 8):
+        base, ns = O.relation_partition(rels, n_rel, P)
+        owners = [O.relation_partition(rels, n_rel, P, seed=7, epoch=e)[0] for e in range(4)]
+        for ow in owners:
+            assert np.array_equal(ow == -1, base == -1)  # SPLIT set unchanged
+            loads = np.zeros(P, np.int64)
+            for r in range(n_rel):
+                if ow[r] == -1:
+                    loads += counts[r] // P + (np.arange(P) < counts[r] % P)
+                else:
+                    loads[ow[r]] += counts[r]
+            assert loads.sum() == len(rels) and loads.max() - loads.min() <= counts[ow >= 0].max()
+        assert any(not np.array_equal(owners[0], ow) for ow in owners[1:])
+        assert not np.array_equal(owners[0], base)
+    # seeds matter, the epoch's partition is a pure function of (seed, epoch)
+    assert np.array_equal(O.relation_partition(rels, n_rel, 4, seed=7, epoch=2)[0], owners[2] if P == 4 else
+                          O.relation_partition(rels, n_rel, 4, seed=7, epoch=2)[0])
+
+
+def test_trainer_repartition_epochs():
+    # P = 2 with repartition: epoch e spans S_E = ceil(N_t / (P B)) steps on both ranks; a rank's positives in epoch e
+    # come from its epoch-e list (the relations it owns in that epoch, plus its share of the split ones)
+    rng = np.random.default_rng(2)
+    n_rel, n_t = 40, 4000
+    trip = (rng.integers(0, 300, n_t), np.minimum(rng.zipf(1.4, n_t) - 1, n_rel - 1), rng.integers(0, 300, n_t))
+    B = 64
+    tr = O.Trainer("distmult", 300, n_rel, 8, B, 16, 8, seed=3, world_size=2, triples=trip, repartition=1)
+    SE = -(-n_t // (2 * B))
+    for e in (0, 1, 2):
+        owner, _ = O.relation_partition(trip[1], n_rel, 2, seed=3, epoch=e)
+        for w in range(2):
+            rels_seen = set()
+            for s in (e * SE, e * SE + SE // 2, e * SE + SE - 1):
+                pos, _, _ = tr.sample(s, w)
+                rels_seen |= set(trip[1][pos].tolist())
+            assert all(owner[r] in (w, -1) for r in rels_seen), (e, w)
+    # within an epoch, a rank visits its list without repetition while it lasts (Feistel permutation per epoch)
+    owner0, _ = O.relation_partition(trip[1], n_rel, 2, seed=3, epoch=0)
+    n0 = int(sum(1 for i in range(n_t) if owner0[trip[1][i]] == 0) + 0)
+    seen = np.concatenate([tr.sample(s, 0)[0] for s in range(SE)])
+    assert len(np.unique(seen[:min(len(seen), n0)])) == min(len(seen), n0)
+
+
 def test_init_law():
     # c.6: v = bound * ((float)(int32)u * 2^-31), u = Philox(ctr=(col,row_lo,row_hi^(tab<<24),INIT))[0]
     seed, bound = 7, O.default_bound(12.0, 400)
