@@ -117,6 +117,12 @@ typedef struct {
                               {e : e mod P == w} (PAPER.md:451-456 [3.3] local negatives: no remote rows for them);
                               the draw of reading c.3 mapped to e = w + P * floor(u * n_w / 2^64). Default 0 */
   int32_t loss;            /* a kge_loss value; default LOGISTIC */
+  int32_t repartition;     /* 1 with world_size > 1: a different, randomised relation partition every epoch (PAPER.md:
+                              497-501 [3.4]; reading c.13': epochs of ceil(N_t / (P B)) steps on every rank, the
+                              non-split relations ordered by (count desc, Philox(r, epoch, REPART = 6) asc); the SPLIT
+                              set is unchanged). At an epoch boundary kge_train_step re-partitions (host) and every rank
+                              pulls the relations it did not own from their previous owner. Default 0; sampled steps
+                              only (kge_train_batch with repartition: KGE_EUNSUPPORTED) */
 } kge_config;
 
 /* Fill *cfg with defaults (ABI version, TransE-L2, d=400, B=1024, g=256, k=256, gamma=12, lr=0.1, eps=1e-10,

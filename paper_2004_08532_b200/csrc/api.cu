@@ -124,6 +124,7 @@ static int validate(const kge_config* c) {
   if (c->neg_deg_k < 0 || c->neg_deg_k > c->neg_k) { set_error("neg_deg_k must be in [0, neg_k]"); return KGE_EINVAL; }
   if (c->neg_local != 0 && c->neg_local != 1) { set_error("neg_local must be 0 or 1"); return KGE_EINVAL; }
   if (c->loss != KGE_LOSS_LOGISTIC && c->loss != KGE_LOSS_PAIRWISE) { set_error("bad loss"); return KGE_EINVAL; }
+  if (c->repartition != 0 && c->repartition != 1) { set_error("repartition must be 0 or 1"); return KGE_EINVAL; }
   if (c->neg_local && c->world_size > 1 && c->n_entities < c->world_size) {
     set_error("neg_local needs n_entities >= world_size (every shard non-empty)");
     return KGE_EINVAL;
@@ -204,6 +205,7 @@ static SampleParams sample_params(const kge_handle* h, bool given, int gi = 0) {
   p.kd = h->cfg.neg_deg_k;
   p.local_P = h->cfg.neg_local && h->P > 1 ? h->P : 0;
   p.local_rank = h->rank;
+  p.epoch_steps = h->epoch_steps;  // repartition: epochs of a fixed step count, the list is this epoch's
   return p;
 }
 
@@ -239,6 +241,7 @@ void kge_config_default(kge_config* c) {
   c->neg_deg_k = 0;
   c->neg_local = 0;
   c->loss = KGE_LOSS_LOGISTIC;
+  c->repartition = 0;
   c->world_size = 1;
   c->rank = 0;
 }
@@ -366,10 +369,19 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   h->n_list = n_triples;
   if (h->P > 1) {  // relation partition (reading c.13) -> this rank's triple list
     std::vector<int32_t> owner, lst;
-    relation_partition(rels, n_triples, cfg->n_relations, h->P, owner);
+    const bool rp = cfg->repartition != 0;
+    relation_partition(rels, n_triples, cfg->n_relations, h->P, owner, rp, cfg->seed, 0);
     rank_list(rels, n_triples, cfg->n_relations, h->P, h->rank, owner, &lst);
     if (lst.empty()) { set_error("this rank received no triples"); return fail(KGE_EINVAL); }
-    h->list = (int32_t*)dalloc(h, lst.size() * 4);
+    // repartition: room for any epoch's list, the relation column kept on the host for the per-epoch partitions
+    h->list = (int32_t*)dalloc(h, (rp ? (size_t)n_triples : lst.size()) * 4);
+    if (rp) {
+      h->host_rels.assign(rels, rels + n_triples);
+      h->epoch_steps = (n_triples + (int64_t)h->P * dm.B - 1) / ((int64_t)h->P * dm.B);
+      h->cur_epoch = 0;
+      h->d_owner_prev = (int32_t*)dalloc(h, (size_t)cfg->n_relations * 4);
+      if (!h->d_owner_prev) return fail(KGE_ENOMEM);
+    }
     std::vector<int32_t> split_list, split_index((size_t)cfg->n_relations, -1);
     for (int64_t r = 0; r < cfg->n_relations; ++r)
       if (owner[(size_t)r] < 0) {
@@ -395,8 +407,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   h->ent_rows = h->P > 1 ? (Ne - h->rank + h->P - 1) / h->P : Ne;  // shard: owner e mod P, local row e div P
   h->ent = (float*)(h->P > 1 ? rawalloc(h, (size_t)h->ent_rows * dm.d * 4) : dalloc(h, (size_t)Ne * dm.d * 4));
   h->ent_st = (float*)dalloc(h, (size_t)h->ent_rows * 4);
-  h->rel = (float*)dalloc(h, (size_t)Nr * dm.drel * 4);
-  h->rel_st = (float*)dalloc(h, (size_t)Nr * 4);
+  // P > 1: relation tables IPC-exportable too (per-epoch repartition pulls rows from their previous owner)
+  h->rel = (float*)(h->P > 1 ? rawalloc(h, (size_t)Nr * dm.drel * 4) : dalloc(h, (size_t)Nr * dm.drel * 4));
+  h->rel_st = (float*)(h->P > 1 ? rawalloc(h, (size_t)Nr * 4) : dalloc(h, (size_t)Nr * 4));
   if (!h->ent || !h->ent_st || !h->rel || !h->rel_st) { set_error("out of device memory (tables)"); return fail(KGE_ENOMEM); }
   const float bound = cfg->init_bound > 0.f ? cfg->init_bound : default_bound(cfg->gamma, cfg->dim);
   const float rbound = cfg->model == KGE_ROTATE ? (float)M_PI : bound;
@@ -410,8 +423,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (e == cudaSuccess) e = cudaMemsetAsync(h->rel_st, 0, (size_t)Nr * 4, h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "table init"));
   if (cfg->model == KGE_TRANSR) {  // M_r, d x d row-major, same uniform law (reading c.6 / Q12)
-    h->proj = (float*)dalloc(h, (size_t)Nr * dm.d * dm.d * 4);
-    h->proj_st = (float*)dalloc(h, (size_t)Nr * 4);
+    h->proj = (float*)(h->P > 1 ? rawalloc(h, (size_t)Nr * dm.d * dm.d * 4) : dalloc(h, (size_t)Nr * dm.d * dm.d * 4));
+    h->proj_st = (float*)(h->P > 1 ? rawalloc(h, (size_t)Nr * 4) : dalloc(h, (size_t)Nr * 4));
     if (!h->proj || !h->proj_st) { set_error("out of device memory (TransR projections)"); return fail(KGE_ENOMEM); }
     e = launch_init_table(h, h->proj, Nr, dm.d * dm.d, 2, bound);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->proj_st, 0, (size_t)Nr * 4, h->stream);
@@ -605,6 +618,12 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
 }
 
 static int ensure_sampled(kge_handle* h, int64_t s) {
+  if (h->epoch_steps > 0) {  // repartition: the list changes at epoch boundaries, so every step is sampled on its own
+    cudaError_t e = launch_sample(h, sample_params(h, false), d_slots(h), h->ring, s, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "sample");
+    h->half_first[0] = h->half_first[1] = -1;
+    return KGE_OK;
+  }
   const int H = h->ring / 2;
   const int64_t hs = s - s % H;  // first step of s's ring half
   const int q = (int)((hs / H) % 2);
@@ -733,6 +752,44 @@ int kge_flush(kge_handle* h) {
   return KGE_OK;
 }
 
+// repartition (reading c.13'): the partition of epoch e; every rank pulls the relation rows (states, TransR M_r) it did
+// not own in the previous epoch from their owner, between two barriers, then samples from its epoch-e list
+static int switch_epoch(kge_handle* h, int64_t e) {
+  const int64_t Nr = h->dims.n_relations;
+  std::vector<int32_t> owner, lst;
+  relation_partition(h->host_rels.data(), (int64_t)h->host_rels.size(), Nr, h->P, owner, true, h->cfg.seed,
+                     (uint32_t)e);
+  rank_list(h->host_rels.data(), (int64_t)h->host_rels.size(), Nr, h->P, h->rank, owner, &lst);
+  if (lst.empty()) { set_error("this rank received no triples in an epoch's partition"); return KGE_EINVAL; }
+  h->owner_prev = h->dist.rel_owner;  // kept alive for the asynchronous copy
+  cudaError_t err = cudaMemcpyAsync(h->d_owner_prev, h->owner_prev.data(), (size_t)Nr * 4, cudaMemcpyHostToDevice,
+                                    h->stream);
+  if (err == cudaSuccess) err = dist_barrier(h);  // every rank finished the previous epoch's updates
+  if (err == cudaSuccess) err = dist_pull_relations(h, h->d_owner_prev);
+  if (err == cudaSuccess) err = dist_barrier(h);  // nobody updates a row a peer is still pulling
+  // the new list through one of two pinned staging buffers (no stream synchronisation: with several ranks driven by one
+  // host thread a synchronising copy would wait on a barrier the other ranks have not enqueued yet); a buffer is
+  // reused two switches later, after its copy's event
+  const int b = h->list_flip;
+  h->list_flip ^= 1;
+  if (err == cudaSuccess && !h->pin_list[b]) {
+    err = cudaMallocHost((void**)&h->pin_list[b], h->host_rels.size() * 4);
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&h->ev_list[b], cudaEventDisableTiming);
+  } else if (err == cudaSuccess) {
+    err = cudaEventSynchronize(h->ev_list[b]);
+  }
+  if (err == cudaSuccess) {
+    std::copy(lst.begin(), lst.end(), h->pin_list[b]);
+    err = cudaMemcpyAsync(h->list, h->pin_list[b], lst.size() * 4, cudaMemcpyHostToDevice, h->stream);
+  }
+  if (err == cudaSuccess) err = cudaEventRecord(h->ev_list[b], h->stream);
+  if (err != cudaSuccess) return cuda_fail(err, "epoch repartition");
+  h->n_list = (int64_t)lst.size();
+  h->dist.rel_owner = owner;
+  h->cur_epoch = e;
+  return KGE_OK;
+}
+
 int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
   if (!h) { set_error("NULL handle"); return KGE_EINVAL; }
   if (n_steps < 0) { set_error("n_steps < 0"); return KGE_EINVAL; }
@@ -743,7 +800,8 @@ int kge_train_step(kge_handle* h, int64_t n_steps, float* loss_out) {
     if (h->P > 1) {
       // B1: every owner has applied step s-1 (lag = 1: step s-2, joined from the update stream first) before anyone
       // gathers rows or overwrites a slot peers read
-      const int rj = join_updates(h);
+      int rj = join_updates(h);
+      if (rj == KGE_OK && h->epoch_steps > 0 && s / h->epoch_steps != h->cur_epoch) rj = switch_epoch(h, s / h->epoch_steps);
       if (rj != KGE_OK) return rj;
       cudaError_t e = dist_barrier(h);
       if (e == cudaSuccess) e = dist_clear_split(h);
@@ -912,6 +970,10 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
     st[2 * B + i] = (int32_t)tails[i];
   }
   if (hprof) hpr.t2 = now();
+  if (h->epoch_steps > 0) {
+    set_error("kge_train_batch: caller batches with repartition = 1 are not supported (the partition is the sampler's)");
+    return KGE_EUNSUPPORTED;
+  }
   if (h->P > 1) {  // B1 (see kge_train_step); every rank must call kge_train_batch for this step
     const int rj = join_updates(h);
     if (rj != KGE_OK) return rj;
@@ -1386,6 +1448,10 @@ void kge_destroy(kge_handle* h) {
   for (int i = 0; i < kge_handle::kStage; ++i)
     if (h->stage_ev[i]) cudaEventDestroy(h->stage_ev[i]);
   if (h->pinned_loss) cudaFreeHost(h->pinned_loss);
+  for (int b = 0; b < 2; ++b) {
+    if (h->pin_list[b]) cudaFreeHost(h->pin_list[b]);
+    if (h->ev_list[b]) cudaEventDestroy(h->ev_list[b]);
+  }
   if (h->side) cudaStreamSynchronize(h->side);
   if (h->ustream) {
     cudaStreamSynchronize(h->ustream);

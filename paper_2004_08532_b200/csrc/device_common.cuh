@@ -8,7 +8,7 @@ namespace kge {
 // ---- Philox4x32-10 (reading c.1: the counter RNG the north_star names; Random123 constants) ----
 constexpr uint32_t kPhiloxM0 = 0xD2511F53u, kPhiloxM1 = 0xCD9E8D57u;
 constexpr uint32_t kPhiloxW0 = 0x9E3779B9u, kPhiloxW1 = 0xBB67AE85u;
-constexpr uint32_t kTagNeg = 1, kTagPerm = 2, kTagInit = 3, kTagDeg = 4, kTagEval = 5;
+constexpr uint32_t kTagNeg = 1, kTagPerm = 2, kTagInit = 3, kTagDeg = 4, kTagEval = 5, kTagRepart = 6;
 
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll

@@ -35,7 +35,27 @@ namespace kge {
 // ------------------------------------------------------------------------------------------------
 // host: relation partition (reading c.13)
 // ------------------------------------------------------------------------------------------------
-int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<int32_t>& owner) {
+// Philox4x32-10 on the host (the partition is computed by the host): the device helper's bijection
+static uint32_t philox_host_x(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+  for (int round = 0; round < 10; ++round) {
+    if (round) {
+      k0 += kPhiloxW0;
+      k1 += kPhiloxW1;
+    }
+    const uint64_t p0 = (uint64_t)kPhiloxM0 * c0, p1 = (uint64_t)kPhiloxM1 * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+  }
+  return c0;
+}
+
+// randomise (reading c.13'): the non-split relations are ordered by (count desc, Philox(ctr = (r,
+// epoch, 0, REPART), seed).x asc, id asc) -- a different greedy assignment every epoch, the SPLIT set unchanged
+int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<int32_t>& owner,
+                           bool randomise, uint64_t seed, uint32_t epoch) {
   std::vector<int64_t> cnt((size_t)nr, 0);
   for (int64_t i = 0; i < nt; ++i) cnt[(size_t)rels[i]]++;
   owner.assign((size_t)nr, 0);
@@ -51,8 +71,14 @@ int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t 
       rest.push_back(r);
     }
   }
+  std::vector<uint32_t> key(randomise ? (size_t)nr : 0);
+  if (randomise)
+    for (int64_t r : rest) key[(size_t)r] = philox_host_x((uint32_t)r, epoch, 0u, kTagRepart, (uint32_t)seed,
+                                                          (uint32_t)(seed >> 32));
   std::stable_sort(rest.begin(), rest.end(), [&](int64_t a, int64_t b) {
-    return cnt[(size_t)a] != cnt[(size_t)b] ? cnt[(size_t)a] > cnt[(size_t)b] : a < b;
+    if (cnt[(size_t)a] != cnt[(size_t)b]) return cnt[(size_t)a] > cnt[(size_t)b];
+    if (randomise && key[(size_t)a] != key[(size_t)b]) return key[(size_t)a] < key[(size_t)b];
+    return a < b;
   });
   for (int64_t r : rest) {
     int32_t best = 0;
@@ -251,6 +277,59 @@ __global__ void __launch_bounds__(256) k_split_rel(SplitArgs a) {
   if (lane == 0) a.rel_st[a.split_list[s]] = st;
 }
 
+struct PullArgs {
+  const float* rel[kMaxRanks];
+  const float* rel_st[kMaxRanks];
+  const float* proj[kMaxRanks];
+  const float* proj_st[kMaxRanks];
+  const int32_t* owner_prev;  // [n_relations] owner in the epoch being left, -1 = split (replicas agree)
+  int64_t nr;
+  int32_t rank, drel, wproj;  // wproj: d*d (TransR) or 0
+  float* rel_mine;
+  float* rel_st_mine;
+  float* proj_mine;
+  float* proj_st_mine;
+};
+
+// epoch switch (repartition): copy every relation this rank did not own in the previous epoch from its owner (warp per
+// relation: row, Adagrad state, TransR projection and its state)
+__global__ void __launch_bounds__(256) k_pull_rel(PullArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= a.nr) return;
+  const int o = a.owner_prev[r];
+  if (o < 0 || o == a.rank) return;
+  for (int e = lane; e < a.drel; e += 32) a.rel_mine[r * a.drel + e] = a.rel[o][r * a.drel + e];
+  if (a.wproj)
+    for (int64_t e = lane; e < a.wproj; e += 32) a.proj_mine[r * a.wproj + e] = a.proj[o][r * a.wproj + e];
+  if (lane == 0) {
+    a.rel_st_mine[r] = a.rel_st[o][r];
+    if (a.wproj) a.proj_st_mine[r] = a.proj_st[o][r];
+  }
+}
+
+cudaError_t dist_pull_relations(kge_handle* h, const int32_t* owner_prev) {
+  PullArgs a{};
+  for (int q = 0; q < h->P; ++q) {
+    a.rel[q] = h->dist.peer_rel[q];
+    a.rel_st[q] = h->dist.peer_rel_st[q];
+    a.proj[q] = h->dist.peer_proj[q];
+    a.proj_st[q] = h->dist.peer_proj_st[q];
+  }
+  a.owner_prev = owner_prev;
+  a.nr = h->dims.n_relations;
+  a.rank = h->rank;
+  a.drel = h->dims.drel;
+  a.wproj = h->proj ? h->dims.d * h->dims.d : 0;
+  a.rel_mine = h->rel;
+  a.rel_st_mine = h->rel_st;
+  a.proj_mine = h->proj;
+  a.proj_st_mine = h->proj_st;
+  k_pull_rel<<<(unsigned)((a.nr + 7) / 8), 256, 0, h->stream>>>(a);
+  ++h->launches;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------------------------
 // host orchestration
 // ------------------------------------------------------------------------------------------------
@@ -266,6 +345,7 @@ cudaError_t dist_preload() {  // see step_preload (lazy loading vs spinning barr
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, (const void*)k_owner_collect);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, (const void*)k_owner_update);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, (const void*)k_split_rel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&at, (const void*)k_pull_rel);
   return e;
 }
 
@@ -432,12 +512,18 @@ int kge_partition(const int64_t* rels, int64_t n_triples, int64_t n_relations, i
 int kge_export(kge_handle* h, void* blob, size_t* blob_bytes) {
   if (!h || !blob_bytes) { set_error("NULL argument"); return KGE_EINVAL; }
   if (h->P < 2) { set_error("kge_export needs world_size > 1"); return KGE_ESTATE; }
-  const size_t need = 2 * sizeof(cudaIpcMemHandle_t);
+  // entity shard, shared block, relation table and states, TransR projections and states (non-TransR: the relation
+  // table's handle again in slots 4 and 5, ignored by kge_connect)
+  const size_t need = 6 * sizeof(cudaIpcMemHandle_t);
   if (!blob) { *blob_bytes = need; return KGE_OK; }
   if (*blob_bytes < need) { set_error("blob too small"); return KGE_EINVAL; }
-  cudaIpcMemHandle_t hs[2];
+  cudaIpcMemHandle_t hs[6];
   cudaError_t e = cudaIpcGetMemHandle(&hs[0], h->ent);
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hs[1], h->dist.shared);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hs[2], h->rel);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hs[3], h->rel_st);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hs[4], h->proj ? h->proj : h->rel);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hs[5], h->proj_st ? h->proj_st : h->rel);
   if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
   std::memcpy(blob, hs, need);
   *blob_bytes = need;
@@ -464,16 +550,25 @@ int kge_connect(kge_handle* h, const void* blobs, int32_t world_size) {
     if (q == h->rank) {
       D.peer_ent[q] = h->ent;
       D.peer_shared[q] = D.shared;
+      D.peer_rel[q] = h->rel;
+      D.peer_rel_st[q] = h->rel_st;
+      D.peer_proj[q] = h->proj;
+      D.peer_proj_st[q] = h->proj_st;
       continue;
     }
-    void *pe = nullptr, *ps = nullptr;
-    cudaError_t e = cudaIpcOpenMemHandle(&pe, hs[2 * q], cudaIpcMemLazyEnablePeerAccess);
-    if (e == cudaSuccess) e = cudaIpcOpenMemHandle(&ps, hs[2 * q + 1], cudaIpcMemLazyEnablePeerAccess);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
-    D.peer_ent[q] = (float*)pe;
-    D.peer_shared[q] = ps;
-    D.ipc_opened.push_back(pe);
-    D.ipc_opened.push_back(ps);
+    void* p[6] = {};
+    const int nh = h->proj ? 6 : 4;
+    for (int k = 0; k < nh; ++k) {
+      cudaError_t e = cudaIpcOpenMemHandle(&p[k], hs[6 * q + k], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+      D.ipc_opened.push_back(p[k]);
+    }
+    D.peer_ent[q] = (float*)p[0];
+    D.peer_shared[q] = p[1];
+    D.peer_rel[q] = (float*)p[2];
+    D.peer_rel_st[q] = (float*)p[3];
+    D.peer_proj[q] = (float*)p[4];
+    D.peer_proj_st[q] = (float*)p[5];
   }
   return finish_connect(h);
 }
@@ -488,6 +583,10 @@ int kge_connect_local(kge_handle** hs, int32_t P) {
     for (int q = 0; q < P; ++q) {
       hs[w]->dist.peer_ent[q] = hs[q]->ent;
       hs[w]->dist.peer_shared[q] = hs[q]->dist.shared;
+      hs[w]->dist.peer_rel[q] = hs[q]->rel;
+      hs[w]->dist.peer_rel_st[q] = hs[q]->rel_st;
+      hs[w]->dist.peer_proj[q] = hs[q]->proj;
+      hs[w]->dist.peer_proj_st[q] = hs[q]->proj_st;
     }
     finish_connect(hs[w]);
   }

@@ -83,6 +83,8 @@ struct SampleParams {
   uint32_t cg_base;  // rank * C
   int32_t kd;        // degree-based in-batch slots per chunk (kge_config::neg_deg_k)
   int32_t local_P, local_rank;  // local-shard negatives (kge_config::neg_local): P > 1 and this rank, else local_P = 0
+  int64_t epoch_steps;  // repartition (reading c.13'): steps per epoch (epoch e = s / epoch_steps, position within it),
+                        // 0 = the classic per-rank epochs of reading c.2
 };
 
 struct StepBuffers {
@@ -153,6 +155,10 @@ struct Dist {
   int32_t* n_slots = nullptr;   // [1]
   float* peer_ent[kMaxRanks] = {};
   void* peer_shared[kMaxRanks] = {};
+  float* peer_rel[kMaxRanks] = {};     // every rank's relation table, states and (TransR) projections: the per-epoch
+  float* peer_rel_st[kMaxRanks] = {};  // repartition pulls a relation from its previous owner
+  float* peer_proj[kMaxRanks] = {};
+  float* peer_proj_st[kMaxRanks] = {};
   uint64_t* peer_flags[kMaxRanks] = {};
   std::vector<void*> ipc_opened;
   std::vector<void*> raw_allocs;  // cudaMalloc'd (IPC-exportable) allocations
@@ -201,6 +207,14 @@ struct kge_handle {
   int32_t* tt = nullptr;
   int32_t* list = nullptr;
   int64_t n_triples = 0, n_list = 0;
+  // per-epoch repartition (kge_config::repartition, P > 1)
+  std::vector<int64_t> host_rels;
+  int64_t epoch_steps = 0, cur_epoch = -1;
+  int32_t* d_owner_prev = nullptr;  // [n_relations] owner map of the epoch being left (device, for the pull)
+  std::vector<int32_t> owner_prev;  // its host source
+  int32_t* pin_list[2] = {};        // pinned staging of the epoch lists
+  cudaEvent_t ev_list[2] = {};
+  int list_flip = 0;
   // sampling ring
   int32_t ring = 0;
   std::vector<kge::Slot> slots;
@@ -356,7 +370,8 @@ void transr_destroy(kge_handle* h);
 void transr_tc_init(kge_handle* h);  // tcgen05 projections (TF32 negatives path)
 
 // dist.cu
-int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<int32_t>& owner);
+int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<int32_t>& owner,
+                           bool randomise = false, uint64_t seed = 0, uint32_t epoch = 0);
 int64_t rank_list(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, int32_t rank,
                   const std::vector<int32_t>& owner, std::vector<int32_t>* out);
 cudaError_t dist_barrier(kge_handle* h);
@@ -364,6 +379,7 @@ cudaError_t dist_preload();
 cudaError_t step_preload();
 cudaError_t dist_exchange_update(kge_handle* h, const Slot& s, int64_t step);
 cudaError_t dist_clear_split(kge_handle* h);  // zero this rank's split-relation gradient sums before a step
+cudaError_t dist_pull_relations(kge_handle* h, const int32_t* owner_prev);  // epoch switch (repartition)
 cudaError_t dist_owner_update_lagged(kge_handle* h, const Slot& s, int64_t step, cudaStream_t st);
 cudaError_t dist_owner_flush(kge_handle* h, const Slot& s, int64_t step);
 

@@ -85,8 +85,13 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
       rv = p.given_r[i];
       tv = p.given_t[i];
     } else {
-      const uint64_t q = (uint64_t)s * (uint64_t)p.B + (uint64_t)i;
-      const uint32_t epoch = (uint32_t)(q / (uint64_t)p.n_list);
+      uint64_t q = (uint64_t)s * (uint64_t)p.B + (uint64_t)i;
+      uint32_t epoch = (uint32_t)(q / (uint64_t)p.n_list);
+      if (p.epoch_steps > 0) {  // repartition (reading c.13'): epoch e = s / S_E, the position within it
+        const int64_t e = s / p.epoch_steps;
+        epoch = (uint32_t)e;
+        q = (uint64_t)(s - e * p.epoch_steps) * (uint64_t)p.B + (uint64_t)i;
+      }
       const uint64_t pp = q % (uint64_t)p.n_list;
       const uint64_t idx = feistel_index(dom, p.k0, p.k1, epoch, pp);
       trip = p.list ? p.list[idx] : (int32_t)idx;

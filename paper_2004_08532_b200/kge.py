@@ -51,7 +51,8 @@ class _Config(ctypes.Structure):
                 ("lag", ctypes.c_int32), ("world_size", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("nccl_comm", ctypes.c_void_p), ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p),
                 ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
-                ("neg_deg_k", ctypes.c_int32), ("neg_local", ctypes.c_int32), ("loss", ctypes.c_int32)]
+                ("neg_deg_k", ctypes.c_int32), ("neg_local", ctypes.c_int32), ("loss", ctypes.c_int32),
+                ("repartition", ctypes.c_int32)]
 
 
 _lib = None
@@ -154,6 +155,7 @@ class Config:
     neg_deg_k: int = 0  # degree-based in-batch negatives per chunk
     neg_local: int = 0  # 1: local-shard negatives when world_size > 1
     loss: str = "logistic"  # or "pairwise"
+    repartition: int = 0  # 1: a randomised relation partition every epoch when world_size > 1
     rank: int = 0
 
     @property
@@ -408,6 +410,7 @@ def init(cfg: Config, heads, rels, tails, use_torch_allocator=True, stream=None)
     c.neg_deg_k = cfg.neg_deg_k
     c.neg_local = cfg.neg_local
     c.loss = LOSS[cfg.loss] if isinstance(cfg.loss, str) else cfg.loss
+    c.repartition = cfg.repartition
     dev = torch.cuda.current_device()
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     c.cuda_stream = s.cuda_stream

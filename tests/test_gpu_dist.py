@@ -12,16 +12,17 @@ from paper_2004_08532_b200 import kge
 pytestmark = pytest.mark.gpu
 
 
-def _run(model, P, shape, steps, precision="fp32", graph="tiny", variant=0, neg_local=0, neg_deg_k=0, lag=0):
+def _run(model, P, shape, steps, precision="fp32", graph="tiny", variant=0, neg_local=0, neg_deg_k=0, lag=0,
+         repartition=0):
     B, g, k, d = shape
     gr = synth.graph(graph)
     trip = gr.triples()
     cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=d, batch_size=B,
                      chunk_size=g, neg_k=k, neg_precision=precision, rotate_variant=variant, neg_local=neg_local,
-                     neg_deg_k=neg_deg_k, lag=lag)
+                     neg_deg_k=neg_deg_k, lag=lag, repartition=repartition)
     hs = kge.init_local_group(cfg, P, *trip)
     orc = O.Trainer(model, gr.n_entities, gr.n_relations, d, B, g, k, world_size=P, triples=trip,
-                    rotate_variant=variant, neg_local=neg_local, neg_deg_k=neg_deg_k, lag=lag)
+                    rotate_variant=variant, neg_local=neg_local, neg_deg_k=neg_deg_k, lag=lag, repartition=repartition)
     # integer half per rank: bit-exact
     for w in range(P):
         s = hs[w].sample(3)
@@ -146,3 +147,31 @@ def test_dist_lag1_overlapped_owner_update(model, precision, P):
     # and it really is the lag-1 trajectory, not lag 0
     _, _, _, lg0, _ = _run(model, P, (128, 32, 32, 32), 5, precision=precision, lag=0)
     assert lg[0] == pytest.approx(lg0[0], rel=1e-6) and np.any(np.abs(lg[2:5] - lg0[2:5]) > 1e-7)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("model", ["transe_l2", "transr"])
+def test_dist_epoch_repartition(model, P):
+    # per-epoch randomised relation repartition (reading c.13'): the tiny graph at B = 128 has
+    # S_E = ceil(10000 / (P 128)) = 40 / 20 steps per epoch, so 1 / 2 epoch switches happen in the 60-step run (the
+    # loss ring keeps 64 steps); positives bit-exact per rank and step, losses and tables vs the oracle's P-rank
+    # simulation with the same per-epoch partitions
+    d = 16 if model == "transr" else 32
+    steps = 60
+    gr, hs, orc, lg, lo = _run(model, P, (128, 32, 32, d), steps, repartition=1)
+    SE = -(-gr.n_triples // (P * 128))
+    assert steps > SE
+    for w in range(P):  # sampling bit-exact in the last epoch
+        s = hs[w].sample(steps - 1)
+        assert np.array_equal(s["pos"], orc.sample(steps - 1, w)[0])
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5, (lg[:4], lo[:4])
+    ids, rids = np.arange(gr.n_entities), np.arange(gr.n_relations)
+    got = np.stack([hs[e % P].get_rows(0, [e])[0] for e in ids])
+    assert np.abs(got - orc.get_rows(0, ids)).max() <= 1e-4
+    # relation rows: the current epoch's owner (or any replica of a split relation) holds the oracle's row
+    owners = [hs[0].relation_owner(r) for r in rids]
+    rel = np.stack([hs[max(o, 0)].get_rows(1, [r])[0] for r, o in zip(rids, owners)])
+    assert np.abs(rel - orc.get_rows(1, rids)).max() <= 1e-4
+    e_now = (steps - 1) // SE
+    o_now, _ = O.relation_partition(gr.triples()[1], gr.n_relations, P, seed=1, epoch=e_now)
+    assert owners == o_now.tolist()
