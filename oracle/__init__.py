@@ -14,8 +14,8 @@ import numpy as np
 from .build import LIB
 from .build import build as build_lib
 
-TRANSE_L1, TRANSE_L2, DISTMULT, COMPLEX, ROTATE, TRANSR = range(6)
-MODEL_IDS = {"transe_l1": 0, "transe_l2": 1, "distmult": 2, "complex": 3, "rotate": 4, "transr": 5}
+TRANSE_L1, TRANSE_L2, DISTMULT, COMPLEX, ROTATE, TRANSR, RESCAL = range(7)
+MODEL_IDS = {"transe_l1": 0, "transe_l2": 1, "distmult": 2, "complex": 3, "rotate": 4, "transr": 5, "rescal": 6}
 TAIL, HEAD, ALTERNATE = 0, 1, 2
 
 P = ctypes.POINTER

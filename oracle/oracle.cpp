@@ -229,6 +229,15 @@ T score_t(int32_t model, int32_t variant, T gamma, int32_t d, const T* h, const 
       }
       return gamma - s;
     }
+    case ORC_RESCAL: {  // h^T M_r t = sum_a sum_b h_a M_ab t_b (Table 1)
+      T s = 0;
+      for (int32_t a = 0; a < d; ++a) {
+        T mt = 0;
+        for (int32_t b = 0; b < d; ++b) mt += M[(int64_t)a * d + b] * t[b];
+        s += h[a] * mt;
+      }
+      return s;
+    }
     case ORC_TRANSR: {  // -||M_r h + r - M_r t||_2^2
       T s = 0;
       for (int32_t a = 0; a < d; ++a) {
@@ -319,6 +328,23 @@ void grad_t(int32_t model, int32_t variant, int32_t d, const T* h, const T* r, c
         dt[e + n] += up * (fac * v);
         dr[e] += up * (-fac * (u * (-a * sn - b * c) + v * (a * c - b * sn)));
       }
+      return;
+    }
+    case ORC_RESCAL: {  // dh_a = sum_b M_ab t_b, dt_b = sum_a h_a M_ab, dM_ab = h_a t_b; no relation vector
+      for (int32_t a = 0; a < d; ++a) {
+        T mt = 0;
+        for (int32_t b = 0; b < d; ++b) mt += M[(int64_t)a * d + b] * t[b];
+        dh[a] += up * mt;
+      }
+      for (int32_t b = 0; b < d; ++b) {
+        T hm = 0;
+        for (int32_t a = 0; a < d; ++a) hm += h[a] * M[(int64_t)a * d + b];
+        dt[b] += up * hm;
+      }
+      if (dM)
+        for (int32_t a = 0; a < d; ++a)
+          for (int32_t b = 0; b < d; ++b) dM[(int64_t)a * d + b] += up * (h[a] * t[b]);
+      (void)dr;
       return;
     }
     case ORC_TRANSR: {
@@ -612,7 +638,7 @@ struct Trainer : Base {
   void setup() {
     d = cfg.dim;
     drel = cfg.model == ORC_ROTATE ? d / 2 : d;
-    has_proj = cfg.model == ORC_TRANSR;
+    has_proj = cfg.model == ORC_TRANSR || cfg.model == ORC_RESCAL;
     float bound = cfg.init_bound > 0 ? cfg.init_bound : default_bound(cfg.gamma, d);
     float rbound = cfg.model == ORC_ROTATE ? (float)M_PI : bound;  // RotatE phases in [-pi, pi)
     bool lazy = cfg.lazy_rows != 0;
@@ -875,6 +901,13 @@ void combine(int32_t model, int32_t d, int32_t mode, const double* h, const doub
         }
       }
       return;
+    case ORC_RESCAL:  // tail: o = M^T h (f = o . t'); head: o = M t (f = h' . o)
+      for (int32_t a = 0; a < d; ++a) {
+        double acc = 0;
+        for (int32_t b = 0; b < d; ++b) acc += mode == 0 ? h[b] * M[(int64_t)b * d + a] : M[(int64_t)a * d + b] * t[b];
+        o[a] = acc;
+      }
+      return;
     case ORC_TRANSR:
       for (int32_t a = 0; a < d; ++a) {
         double acc = 0;
@@ -899,6 +932,7 @@ double pair_score(int32_t model, int32_t variant, double gamma, int32_t d, const
       return gamma - std::sqrt(s);
     case ORC_DISTMULT:
     case ORC_COMPLEX:
+    case ORC_RESCAL:
       for (int32_t e = 0; e < d; ++e) s += o[e] * x[e];
       return s;
     case ORC_ROTATE:

@@ -30,7 +30,8 @@
 extern "C" {
 #endif
 
-enum { ORC_TRANSE_L1 = 0, ORC_TRANSE_L2 = 1, ORC_DISTMULT = 2, ORC_COMPLEX = 3, ORC_ROTATE = 4, ORC_TRANSR = 5 };
+enum { ORC_TRANSE_L1 = 0, ORC_TRANSE_L2 = 1, ORC_DISTMULT = 2, ORC_COMPLEX = 3, ORC_ROTATE = 4, ORC_TRANSR = 5,
+       ORC_RESCAL = 6 /* h^T M_r t (Table 1); M_r d x d row-major in table 2, no relation vector */ };
 enum { ORC_TAIL = 0, ORC_HEAD = 1, ORC_ALTERNATE = 2 };
 
 typedef struct {

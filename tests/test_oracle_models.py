@@ -15,7 +15,7 @@ import torch
 import oracle as O
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-MODELS = ["transe_l1", "transe_l2", "distmult", "complex", "rotate", "transr"]
+MODELS = ["transe_l1", "transe_l2", "distmult", "complex", "rotate", "transr", "rescal"]
 
 
 def _mid(name):
@@ -47,7 +47,7 @@ def _rand_args(model, d, rng, scale=0.5):
     t = rng.uniform(-scale, scale, d)
     dr = d // 2 if model == "rotate" else d
     r = rng.uniform(-np.pi, np.pi, dr) if model == "rotate" else rng.uniform(-scale, scale, dr)
-    M = rng.uniform(-scale, scale, (d, d)) if model == "transr" else None
+    M = rng.uniform(-scale, scale, (d, d)) if model in ("transr", "rescal") else None
     return h, r, t, M
 
 
@@ -106,6 +106,8 @@ def _torch_score(model, h, r, t, M, variant, gamma):
         return gamma - (m2.sum() if variant == 0 else m2.sqrt().sum())
     if model == "transr":
         return gamma - ((M @ h + r - M @ t) ** 2).sum()
+    if model == "rescal":
+        return h @ (M @ t) + 0.0 * r.sum()  # no relation vector (its gradient is 0)
     raise ValueError(model)
 
 
@@ -182,7 +184,7 @@ def test_joint_equals_naive(model, mode, variant):
     dr = d // 2 if model == "rotate" else d
     H, T, X = rng.uniform(-1, 1, (3, g, d))[0], rng.uniform(-1, 1, (g, d)), rng.uniform(-1, 1, (k, d))
     R = rng.uniform(-np.pi, np.pi, (g, dr)) if model == "rotate" else rng.uniform(-1, 1, (g, dr))
-    M = rng.uniform(-1, 1, (g, d, d)) if model == "transr" else None
+    M = rng.uniform(-1, 1, (g, d, d)) if model in ("transr", "rescal") else None
     grp = O.score_group(mid, mode, H, R, T, X, M=M, gamma=2.0, variant=variant)
     for i in range(g):
         for j in range(k):
@@ -229,3 +231,20 @@ def test_loss_properties():
     # saturation
     L, dp, _ = O.logistic_loss([60.0], [], 1, 1)
     assert L < 1e-25 and abs(dp[0]) < 1e-25
+
+
+def test_rescal_closed_form_and_reductions():
+    # Table 1: h^T M_r t. Hand-worked: h = [1, 2], M = [[1, 2], [3, 4]], t = [5, 6]:
+    # M t = [17, 39] -> 1*17 + 2*39 = 95; dh = M t = [17, 39], dt = h^T M = [7, 10], dM = h t^T = [[5, 6], [10, 12]]
+    h, t, M = np.array([1.0, 2.0]), np.array([5.0, 6.0]), np.array([[1.0, 2.0], [3.0, 4.0]])
+    assert O.score(O.RESCAL, h, np.zeros(2), t, M=M) == 95.0
+    dh, dr, dt, dM = O.score_grad(O.RESCAL, h, np.zeros(2), t, M=M)
+    assert dh.tolist() == [17.0, 39.0] and dt.tolist() == [7.0, 10.0] and not dr.any()
+    assert dM.reshape(2, 2).tolist() == [[5.0, 6.0], [10.0, 12.0]]
+    # M_r = diag(r) reduces RESCAL to DistMult; M_r = M_r^T makes it symmetric in (h, t)
+    rng = np.random.default_rng(4)
+    h, r, t = rng.normal(size=(3, 9))
+    assert abs(O.score(O.RESCAL, h, r, t, M=np.diag(r)) - O.score(O.DISTMULT, h, r, t)) < 1e-12
+    A = rng.normal(size=(9, 9))
+    S = A + A.T
+    assert abs(O.score(O.RESCAL, h, r, t, M=S) - O.score(O.RESCAL, t, r, h, M=S)) < 1e-12

@@ -8,7 +8,7 @@ import torch
 import oracle as O
 from tests import torch_ref as TR
 
-MODELS = ["transe_l1", "transe_l2", "distmult", "complex", "rotate", "transr"]
+MODELS = ["transe_l1", "transe_l2", "distmult", "complex", "rotate", "transr", "rescal"]
 
 
 def _tiny_triples(n_e, n_r, n_t, seed):
@@ -35,7 +35,7 @@ def test_step_equals_torch_autograd(model, world, loss):
     trip = _tiny_triples(n_e, n_r, n_t, 3 + MODELS.index(model))
     tr = O.Trainer(model, n_e, n_r, d, B, g, k, gamma=gamma, lr=lr, eps=eps, seed=11, world_size=world,
                    rotate_variant=variant, triples=trip, loss=loss)
-    has_proj = model == "transr"
+    has_proj = model in ("transr", "rescal")
     E, R, Pj = _tables(tr, n_e, n_r, has_proj, d)
     SE, SR = torch.zeros(n_e, dtype=torch.float64), torch.zeros(n_r, dtype=torch.float64)
     SP = torch.zeros(n_r, dtype=torch.float64)

@@ -28,6 +28,8 @@ def score(model, h, r, t, M=None, variant=0, gamma=0.0):
     if model == "transr":
         p = (M @ h.unsqueeze(-1)).squeeze(-1) + r - (M @ t.unsqueeze(-1)).squeeze(-1)
         return gamma - (p ** 2).sum(-1)
+    if model == "rescal":  # h^T M_r t; no relation vector
+        return (h * (M @ t.unsqueeze(-1)).squeeze(-1)).sum(-1) + 0.0 * r.sum(-1)
     raise ValueError(model)
 
 
