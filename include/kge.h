@@ -38,14 +38,16 @@ extern "C" {
 
 typedef struct kge_handle kge_handle; /* opaque, library-owned */
 
-/* Table 1 models. RESCAL is out of scope. */
+/* Table 1 models. */
 typedef enum {
   KGE_TRANSE_L1 = 0, /* gamma - ||h + r - t||_1 */
   KGE_TRANSE_L2 = 1, /* gamma - ||h + r - t||_2 (not squared) */
   KGE_DISTMULT = 2,  /* h^T diag(r) t */
   KGE_COMPLEX = 3,   /* Re(h^T diag(r) conj(t)); rows [re(d/2) | im(d/2)] */
   KGE_ROTATE = 4,    /* gamma - ||h o e^{i theta} - t||^2 (variant 1: gamma - sum_j |.|); relation = d/2 phases */
-  KGE_TRANSR = 5     /* gamma - ||M_r h + r - M_r t||_2^2, M_r d x d row-major */
+  KGE_TRANSR = 5,    /* gamma - ||M_r h + r - M_r t||_2^2, M_r d x d row-major */
+  KGE_RESCAL = 6     /* h^T M_r t, M_r d x d row-major in table 2; the relation table (1, 4) is unused
+                        (never updated); TF32 / FP32 negatives only (BF16, lag = 1: KGE_EUNSUPPORTED) */
 } kge_model;
 
 typedef enum {

@@ -95,7 +95,11 @@ static float default_bound(float gamma, int dim) {
 static int validate(const kge_config* c) {
   if (!c) { set_error("cfg is NULL"); return KGE_EINVAL; }
   if (c->abi_version != KGE_ABI_VERSION) { set_error("abi_version mismatch"); return KGE_EINVAL; }
-  if (c->model < 0 || c->model > KGE_TRANSR) { set_error("unknown model"); return KGE_EINVAL; }
+  if (c->model < 0 || c->model > KGE_RESCAL) { set_error("unknown model"); return KGE_EINVAL; }
+  if (c->model == KGE_RESCAL && (c->neg_precision == KGE_PREC_BF16 || c->lag == 1)) {
+    set_error("RESCAL: BF16 negatives and lag = 1 are not implemented");
+    return KGE_EUNSUPPORTED;
+  }
   if (c->dim <= 0 || c->dim % 4 != 0) { set_error("dim must be a positive multiple of 4"); return KGE_EINVAL; }
   if ((c->model == KGE_COMPLEX || c->model == KGE_ROTATE) && c->dim % 8 != 0) {
     set_error("ComplEx/RotatE need dim % 8 == 0 (d/2 complex coordinates, float4 halves)");
@@ -135,7 +139,10 @@ static int validate(const kge_config* c) {
   }
   if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size) { set_error("bad world_size/rank"); return KGE_EINVAL; }
   if (c->world_size > kMaxRanks) { set_error("world_size > 8 (one node) not supported"); return KGE_EINVAL; }
-  if (c->model == KGE_TRANSR && c->dim > 512) { set_error("TransR supports dim <= 512"); return KGE_EINVAL; }
+  if ((c->model == KGE_TRANSR || c->model == KGE_RESCAL) && c->dim > 512) {
+    set_error("TransR / RESCAL support dim <= 512");
+    return KGE_EINVAL;
+  }
   return KGE_OK;
 }
 
@@ -422,7 +429,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   h->rows.d = dm.d;
   if (e == cudaSuccess) e = cudaMemsetAsync(h->rel_st, 0, (size_t)Nr * 4, h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "table init"));
-  if (cfg->model == KGE_TRANSR) {  // M_r, d x d row-major, same uniform law (reading c.6 / Q12)
+  if (cfg->model == KGE_TRANSR || cfg->model == KGE_RESCAL) {  // M_r, d x d row-major, same uniform law (c.6 / Q12)
     h->proj = (float*)(h->P > 1 ? rawalloc(h, (size_t)Nr * dm.d * dm.d * 4) : dalloc(h, (size_t)Nr * dm.d * dm.d * 4));
     h->proj_st = (float*)(h->P > 1 ? rawalloc(h, (size_t)Nr * 4) : dalloc(h, (size_t)Nr * 4));
     if (!h->proj || !h->proj_st) { set_error("out of device memory (TransR projections)"); return fail(KGE_ENOMEM); }
@@ -432,8 +439,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     TrBuffers& T = h->tr_buf;
     const size_t B = dm.B;
     int32_t* ib = (int32_t*)dalloc(h, (1 + 4 * B + (B + 1) + (dm.C + 1) + B) * 4);
-    T.QX = (float*)dalloc(h, B * dm.k * dm.d * 4);
-    T.dQ = (float*)dalloc(h, B * dm.k * dm.d * 4);
+    const bool tr = cfg->model == KGE_TRANSR;  // RESCAL needs only dM and the U / V (H) factor rows
+    T.QX = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 : 4);
+    T.dQ = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 : 4);
     T.dM = (float*)dalloc(h, B * dm.d * dm.d * 4);
     T.Pv = (float*)dalloc(h, B * dm.d * 4);
     T.U = (float*)dalloc(h, 2 * B * dm.d * 4);
@@ -447,7 +455,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     T.rg_off = ib; ib += B + 1;
     T.cg_off = ib; ib += dm.C + 1;
     T.cg_list = ib; ib += B;
-    if (!transr_init(h)) { set_error("TransR kernel setup failed"); return fail(KGE_ECUDA); }
+    if (!(tr ? transr_init(h) : rescal_init(h))) { set_error("TransR / RESCAL kernel setup failed"); return fail(KGE_ECUDA); }
   }
 
   // ---- sample ring + debug slot ----
@@ -463,7 +471,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     const size_t gu_one = ((size_t)dm.n_occ * dm.d * 4 + 255) & ~size_t(255);
     const size_t gu_bytes = gu_one * (cfg->lag == 1 ? 2 : 1);
     const size_t gs_bytes = ((size_t)std::max(1, D.n_split) * dm.drel * 4 + 255) & ~size_t(255);
-    const size_t gp_bytes = cfg->model == KGE_TRANSR ? (size_t)std::max(1, D.n_split) * dm.d * dm.d * 4 : 0;
+    const size_t gp_bytes = cfg->model == KGE_TRANSR || cfg->model == KGE_RESCAL
+                                ? (size_t)std::max(1, D.n_split) * dm.d * dm.d * 4 : 0;
     D.shared_bytes = 256 + flags_bytes + ring_bytes + gu_bytes + gs_bytes + gp_bytes;
     char* sb = (char*)rawalloc(h, D.shared_bytes);
     if (!sb) { set_error("out of device memory (shared block)"); return fail(KGE_ENOMEM); }
@@ -1190,8 +1199,8 @@ static int pack_list(const int64_t* off, const int64_t* ids, int64_t n, int64_t 
 static int rank_queries(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t* ts, int64_t n,
                         int32_t corrupt, std::vector<int32_t>& ids) {
   if (!h || (n > 0 && (!hs || !rs || !ts))) { set_error("NULL argument"); return KGE_EINVAL; }
-  if (h->dims.model == KGE_TRANSR || h->P > 1) {
-    set_error("kge_rank: TransR and world_size > 1 are not supported");
+  if (h->dims.model == KGE_TRANSR || h->dims.model == KGE_RESCAL || h->P > 1) {
+    set_error("kge_rank: TransR, RESCAL and world_size > 1 are not supported");
     return KGE_EUNSUPPORTED;
   }
   if (corrupt < 0 || corrupt > 2) { set_error("corrupt_head must be 0 (tail), 1 (head) or 2 (both)"); return KGE_EINVAL; }

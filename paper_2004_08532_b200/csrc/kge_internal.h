@@ -27,6 +27,7 @@ inline Family family_of(int model, int rotate_variant) {
     case KGE_DISTMULT:
     case KGE_COMPLEX: return FAM_DOT;
     case KGE_ROTATE: return rotate_variant ? FAM_CMOD : FAM_L2SQ;
+    case KGE_RESCAL: return FAM_DOT;  // o = M^T h | M t, then o . x' (rescal.cu)
     default: return FAM_L2SQ;
   }
 }
@@ -365,6 +366,10 @@ cudaError_t launch_update_range(kge_handle* h, const Slot& s, int lo, int hi, cu
 
 // transr.cu
 cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step);
+cudaError_t launch_proj_update(kge_handle* h, const Slot& s);
+// rescal.cu
+cudaError_t launch_rescal_step(kge_handle* h, const Slot& s, int64_t step);
+bool rescal_init(kge_handle* h);
 bool transr_init(kge_handle* h);
 void transr_destroy(kge_handle* h);
 void transr_tc_init(kge_handle* h);  // tcgen05 projections (TF32 negatives path)

@@ -1426,9 +1426,18 @@ cudaError_t launch_update(kge_handle* h, const Slot& s) {
                              h->buf.Gocc);
 }
 
+// the dot family's chunked negatives and their backward (RESCAL after its per-positive matrix-vector products)
+cudaError_t launch_dot_negatives(kge_handle* h, const Slot& s) {
+  if (tc_supported(h)) return launch_tc_neg(h, s);
+  NegArgs na{h->dims, h->buf, h->buf.Gocc, nullptr, nullptr, 1};
+  launch_neg<FAM_DOT>(h, na);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
   if (dm.model == KGE_TRANSR) return launch_transr_step(h, s, step);
+  if (dm.model == KGE_RESCAL) return launch_rescal_step(h, s, step);
   const bool tc = tc_supported(h);
   GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0, tc && tc_fuses_chain(h) ? 1 : 0, tc && tc_flow() ? h->buf.flow : nullptr};
   const int rows = dm.B + dm.C * dm.k;
@@ -1505,6 +1514,8 @@ __global__ void __launch_bounds__(256) k_score(ScoreArgs a) {
 
 cudaError_t launch_transr_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n,
                                 float* out);  // transr.cu
+cudaError_t launch_rescal_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n,
+                                float* out);  // rescal.cu
 
 // ------------------------------------------------------------------------------------------------
 // k_rank: link-prediction rank of the true entity among all entities (raw setting), one CTA per test triple
@@ -1732,6 +1743,7 @@ cudaError_t launch_rank(kge_handle* h, const int32_t* hs, const int32_t* rs, con
 
 cudaError_t launch_score(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, float* out) {
   if (h->dims.model == KGE_TRANSR) return launch_transr_score(h, hs, rs, ts, n, out);
+  if (h->dims.model == KGE_RESCAL) return launch_rescal_score(h, hs, rs, ts, n, out);
   // scratch: reuse the X buffer in chunks of its capacity
   const int64_t cap = (int64_t)h->dims.C * h->dims.k;
   for (int64_t b = 0; b < n; b += cap) {

@@ -788,6 +788,16 @@ static void dbg(kge_handle* h, const char* what) {
   fprintf(stderr, "[kge] %s -> %s\n", what, cudaGetErrorString(e));
 }
 
+// Adagrad on the projection matrices of the step's unique relations (TransR, RESCAL: one state per matrix)
+cudaError_t launch_proj_update(kge_handle* h, const Slot& s) {
+  const Dims& dm = h->dims;
+  TrArgs a{dm, s, h->rows, h->rel, h->proj, h->proj_st, h->buf, h->tr_buf, dm.B,
+           h->P > 1 ? h->dist.split_index : nullptr, h->dist.gproj_split};
+  k_tr_proj<<<dm.B, 256, 0, h->stream>>>(a);
+  ++h->launches;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   const Dims& dm = h->dims;
   (void)step;

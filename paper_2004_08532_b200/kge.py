@@ -22,7 +22,7 @@ from .build import LIB
 # multi-rank device barriers (a lazily loaded kernel may wait for a spinning barrier kernel).
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
-MODELS = {"transe_l1": 0, "transe_l2": 1, "distmult": 2, "complex": 3, "rotate": 4, "transr": 5}
+MODELS = {"transe_l1": 0, "transe_l2": 1, "distmult": 2, "complex": 3, "rotate": 4, "transr": 5, "rescal": 6}
 CORRUPT = {"tail": 0, "head": 1, "alternate": 2}
 PRECISION = {"fp32": 0, "tf32": 1, "bf16": 2}
 LOSS = {"logistic": 0, "pairwise": 1}

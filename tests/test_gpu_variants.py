@@ -135,3 +135,68 @@ def test_pairwise_multi_rank(model):
     for w, h in enumerate(hs):
         lg += h.read_losses(0, 10)
     assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5, (lg, lo)
+
+
+# ---------------------------------------------------------------- RESCAL (Table 1: h^T M_r t)
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+@pytest.mark.parametrize("loss", ["logistic", "pairwise"])
+def test_rescal_parity(precision, loss):
+    # o = M_r^T h (tail) / M_r t (head), then the dot family's chunked negatives (FFMA or tcgen05); dM per unique
+    # relation in a fixed order, one Adagrad state per matrix
+    gamma = 12.0 if loss == "logistic" else 0.002
+    gr, trip, gpu, orc = _pair("rescal", 32, 256, 64, 64, precision=precision, gamma=gamma, loss=loss,
+                               init_bound=0.1 if loss == "pairwise" else 0.0, lr=0.05)
+    assert gpu.neg_path == precision.replace("fp32", "ffma")
+    heads, rels, tails = (np.asarray(a) for a in trip)
+    rng = np.random.default_rng(1)
+    q = rng.integers(0, gr.n_triples, 300)
+    tol = 1e-5 if precision == "fp32" else 2e-3
+    f, ref = gpu.score(heads[q], rels[q], tails[q]), orc.score_triples(heads[q], rels[q], tails[q])
+    assert np.max(np.abs(f - ref)) <= 1e-5 * max(1.0, np.abs(ref).max())
+    # per-pair negative scores of step 0
+    gpu.set_option("capture_neg", 1)
+    ref0, meta = U.pair_scores(orc, 0, heads, rels, tails, 64)
+    lg = gpu.train_step(1)
+    got = gpu.neg_scores()
+    S = np.abs(ref0).max() + 1e-3
+    assert np.max(np.abs(got - ref0)) <= tol * S, np.max(np.abs(got - ref0))
+    gpu.set_option("capture_neg", 0)
+    n = 30
+    lg = np.concatenate([lg, gpu.train_step(n - 1)])
+    lo = orc.train(n)
+    rel = np.abs(lg - lo) / np.abs(lo)
+    if loss == "logistic":
+        assert rel.max() <= tol, (rel.max(), int(np.argmax(rel)))
+    else:  # reading c.9': strict first steps, then the hinge flips separate the trajectories
+        assert rel[:3].max() <= tol and abs(np.log(lg[-1] / lo[-1])) <= 0.1
+    if loss == "logistic":
+        ids, rids = np.arange(gr.n_entities), np.arange(gr.n_relations)
+        rtol = 1e-4 if precision == "fp32" else 2e-2
+        assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= rtol
+        assert np.abs(gpu.get_rows(2, rids) - orc.get_rows(2, rids)).max() <= rtol
+        ps = orc.get_rows(5, rids)
+        assert np.abs(gpu.get_rows(5, rids) - ps).max() <= (1e-6 if precision == "fp32" else 2e-3) * max(1.0, ps.max())
+        # no relation vector: table 1 keeps its initial rows, its Adagrad states stay 0
+        assert not gpu.get_rows(4, rids).any()
+
+
+def test_rescal_teacher_forced_and_multi_rank():
+    # FB15k-shaped graph at d = 64: one FP32 step from the oracle's tables at a time (rows 1e-4), then P = 2
+    gr, trip, gpu, orc = _pair("rescal", 64, 1024, 256, 256, graph="fb15k", lr=0.05)
+    ids, rids = np.arange(gr.n_entities), np.arange(gr.n_relations)
+    for s in range(3):
+        U.copy_tables(orc, gpu, "transr", gr.n_entities, gr.n_relations)  # every table incl. the projections
+        lg, lo = gpu.train_step(1)[0], orc.train(1)[0]
+        assert abs(lg - lo) / abs(lo) <= 1e-5
+        assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 1e-4
+        assert np.abs(gpu.get_rows(2, rids) - orc.get_rows(2, rids)).max() <= 1e-4
+    gr, trip, hs, orc = _pair("rescal", 16, 128, 32, 32, world=2, lr=0.05)
+    for _ in range(10):
+        for h in hs:
+            h.train_step(1, return_loss=False)
+    lg = sum(h.read_losses(0, 10).astype(np.float64) for h in hs)
+    lo = orc.train(10)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5
+    ids = np.arange(gr.n_entities)
+    got = np.stack([hs[e % 2].get_rows(0, [e])[0] for e in ids])
+    assert np.abs(got - orc.get_rows(0, ids)).max() <= 1e-4
