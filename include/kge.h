@@ -69,9 +69,11 @@ typedef enum { KGE_CORRUPT_TAIL = 0, KGE_CORRUPT_HEAD = 1, KGE_CORRUPT_ALTERNATE
  * TF32 = tcgen05 tensor cores with TMEM accumulators (DistMult, ComplEx, and TransE-L2 / Table-1 RotatE via
  * ||o - x||^2 = ||o||^2 - 2 o.x + ||x||^2; TransR projections); BF16 = the same contractions (forward S = O X'^T and
  * both backward GEMMs) on BF16 copies of O, X' and W with fp32 TMEM accumulators (kind::f16; not for TransR:
- * KGE_EUNSUPPORTED). TransE-L1 and the RotatE modulus variant are not contractions and run FFMA at any setting
- * (kge_neg_path reports which path a handle took). */
-typedef enum { KGE_PREC_FP32 = 0, KGE_PREC_TF32 = 1, KGE_PREC_BF16 = 2 } kge_precision;
+ * KGE_EUNSUPPORTED). 3XTF32 = the same contractions in split precision: every operand x =
+ * hi + lo (hi a tf32 value, lo = x - hi exact), S = hi.hi + hi.lo + lo.hi on the tensor cores -- FP32-level
+ * accuracy at three MMAs per K slice (not for TransR / RESCAL: KGE_EUNSUPPORTED). TransE-L1 and the RotatE modulus
+ * variant are not contractions and run FFMA at any setting (kge_neg_path reports which path a handle took). */
+typedef enum { KGE_PREC_FP32 = 0, KGE_PREC_TF32 = 1, KGE_PREC_BF16 = 2, KGE_PREC_3XTF32 = 3 } kge_precision;
 
 /* Loss (PAPER.md:239-249 [2], "two loss functions are commonly used"): LOGISTIC = sum log(1 + exp(-y f)) (L243;
  * normalisation reading c.9: mean over positives + mean over negatives); PAIRWISE = the pairwise ranking loss
@@ -213,7 +215,7 @@ int32_t kge_table_width(const kge_handle* h, int32_t table);
  * tiles: the FP32 precision, and TransE-L1 / the RotatE modulus variant at any precision), KGE_PATH_TF32 (tcgen05
  * kind::tf32 with TMEM accumulators: DistMult, ComplEx, TransE-L2, Table-1 RotatE, TransR projections), KGE_PATH_BF16
  * (tcgen05 kind::f16 on BF16 operands, the same models but TransR). -1 for NULL. */
-enum { KGE_PATH_FFMA = 0, KGE_PATH_TF32 = 1, KGE_PATH_BF16 = 2 };
+enum { KGE_PATH_FFMA = 0, KGE_PATH_TF32 = 1, KGE_PATH_BF16 = 2, KGE_PATH_3XTF32 = 3 };
 int32_t kge_neg_path(const kge_handle* h);
 
 /* Next step index (steps are counter-based: (seed, step) fixes every sample, so resume is exact). */

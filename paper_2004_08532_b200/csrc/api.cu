@@ -96,8 +96,9 @@ static int validate(const kge_config* c) {
   if (!c) { set_error("cfg is NULL"); return KGE_EINVAL; }
   if (c->abi_version != KGE_ABI_VERSION) { set_error("abi_version mismatch"); return KGE_EINVAL; }
   if (c->model < 0 || c->model > KGE_RESCAL) { set_error("unknown model"); return KGE_EINVAL; }
-  if (c->model == KGE_RESCAL && (c->neg_precision == KGE_PREC_BF16 || c->lag == 1)) {
-    set_error("RESCAL: BF16 negatives and lag = 1 are not implemented");
+  if (c->model == KGE_RESCAL && (c->neg_precision == KGE_PREC_BF16 || c->neg_precision == KGE_PREC_3XTF32 ||
+                                  c->lag == 1)) {
+    set_error("RESCAL: BF16 / 3xTF32 negatives and lag = 1 are not implemented");
     return KGE_EUNSUPPORTED;
   }
   if (c->dim <= 0 || c->dim % 4 != 0) { set_error("dim must be a positive multiple of 4"); return KGE_EINVAL; }
@@ -119,9 +120,9 @@ static int validate(const kge_config* c) {
     return KGE_ERANGE;
   }
   if (c->corrupt < 0 || c->corrupt > 2) { set_error("bad corrupt"); return KGE_EINVAL; }
-  if (c->neg_precision < 0 || c->neg_precision > 2) { set_error("bad neg_precision"); return KGE_EINVAL; }
-  if (c->neg_precision == KGE_PREC_BF16 && c->model == KGE_TRANSR) {
-    set_error("BF16 negatives are not implemented for TransR (use TF32)");
+  if (c->neg_precision < 0 || c->neg_precision > 3) { set_error("bad neg_precision"); return KGE_EINVAL; }
+  if ((c->neg_precision == KGE_PREC_BF16 || c->neg_precision == KGE_PREC_3XTF32) && c->model == KGE_TRANSR) {
+    set_error("BF16 / 3xTF32 negatives are not implemented for TransR (use TF32)");
     return KGE_EUNSUPPORTED;
   }
   if (c->lag != 0 && c->lag != 1) { set_error("lag must be 0 or 1"); return KGE_EINVAL; }
@@ -313,6 +314,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   dm.dp16 = ((dm.d + 63) / 64) * 64;   // BF16 copies: whole 64-element (128-byte) k-blocks
   dm.kp16 = ((dm.k + 63) / 64) * 64;
   dm.bf16 = cfg->neg_precision == KGE_PREC_BF16 ? 1 : 0;
+  dm.x3 = cfg->neg_precision == KGE_PREC_3XTF32 ? 1 : 0;
   h->dp = dm.dp;
   h->kp = dm.kp;
   h->n_pad = 64;  // the sampler's warp-level sort stages work on 64-key blocks
@@ -555,6 +557,18 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     b.W16 = (uint16_t*)dalloc(h, (size_t)dm.B * dm.kp16 * 2);
     if (!b.O16 || !b.X16 || !b.W16) { set_error("out of device memory (BF16 operands)"); return fail(KGE_ENOMEM); }
   }
+  if (dm.x3) {  // 3xTF32 hi / lo splits (pads stay zero)
+    b.O_hi = (float*)dalloc(h, (size_t)dm.B * dm.dp * 4);
+    b.O_lo = (float*)dalloc(h, (size_t)dm.B * dm.dp * 4);
+    b.X_hi = (float*)dalloc(h, (size_t)nneg * dm.dp * 4);
+    b.X_lo = (float*)dalloc(h, (size_t)nneg * dm.dp * 4);
+    b.W_hi = (float*)dalloc(h, (size_t)dm.B * dm.kp * 4);
+    b.W_lo = (float*)dalloc(h, (size_t)dm.B * dm.kp * 4);
+    if (!b.O_hi || !b.O_lo || !b.X_hi || !b.X_lo || !b.W_hi || !b.W_lo) {
+      set_error("out of device memory (3xTF32 operands)");
+      return fail(KGE_ENOMEM);
+    }
+  }
   b.wpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
@@ -594,6 +608,12 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (e == cudaSuccess && dm.bf16) e = cudaMemsetAsync(b.O16, 0, (size_t)dm.B * dm.dp16 * 2, h->stream);
   if (e == cudaSuccess && dm.bf16) e = cudaMemsetAsync(b.X16, 0, (size_t)nneg * dm.dp16 * 2, h->stream);
   if (e == cudaSuccess && dm.bf16) e = cudaMemsetAsync(b.W16, 0, (size_t)dm.B * dm.kp16 * 2, h->stream);
+  for (float* p : {b.O_hi, b.O_lo})
+    if (e == cudaSuccess && p) e = cudaMemsetAsync(p, 0, (size_t)dm.B * dm.dp * 4, h->stream);
+  for (float* p : {b.X_hi, b.X_lo})
+    if (e == cudaSuccess && p) e = cudaMemsetAsync(p, 0, (size_t)nneg * dm.dp * 4, h->stream);
+  for (float* p : {b.W_hi, b.W_lo})
+    if (e == cudaSuccess && p) e = cudaMemsetAsync(p, 0, (size_t)dm.B * dm.kp * 4, h->stream);
   if (e == cudaSuccess) {
     std::vector<float> ones((size_t)std::max<int64_t>(dm.B, nneg), 1.0f);
     e = cudaMemcpy2DAsync(b.O + dm.d, (size_t)dm.dp * 4, ones.data(), 4, 4, dm.B, cudaMemcpyHostToDevice, h->stream);
@@ -1337,7 +1357,8 @@ int64_t kge_step(const kge_handle* h) { return h ? h->step : -1; }
 int32_t kge_neg_path(const kge_handle* h) {
   if (!h) return -1;
   if (h->dims.model == KGE_TRANSR) return h->tr_tc ? KGE_PATH_TF32 : KGE_PATH_FFMA;
-  return tc_supported(h) ? (h->dims.bf16 ? KGE_PATH_BF16 : KGE_PATH_TF32) : KGE_PATH_FFMA;
+  if (!tc_supported(h)) return KGE_PATH_FFMA;
+  return h->dims.bf16 ? KGE_PATH_BF16 : (h->dims.x3 ? KGE_PATH_3XTF32 : KGE_PATH_TF32);
 }
 
 int kge_read_losses(kge_handle* h, int64_t first_step, int64_t n, float* out) {

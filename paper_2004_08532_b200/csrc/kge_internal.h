@@ -97,6 +97,12 @@ struct StepBuffers {
   uint16_t* O16;   // BF16 path: bf16 copies of O [B x dp16], X' [C*k x dp16] (written by the gather) and W [B x kp16]
   uint16_t* X16;   // (written by the forward epilogue), or nullptr
   uint16_t* W16;
+  float* O_hi;     // 3xTF32 path: tf32 hi / lo splits of O, X' (gather) and W (forward epilogue), pitch dp / kp
+  float* O_lo;
+  float* X_hi;
+  float* X_lo;
+  float* W_hi;
+  float* W_lo;
   float* wpos;     // [B] dL/df+
   float* lpos;     // [B] per-positive loss term
   float* pstat;    // [B] pair statistic of each positive (L2: squared distance)
@@ -176,6 +182,7 @@ struct Dims {
   int32_t dp, kp;  // padded row pitch of O / X' (d + 2 rounded up to 32) and of W (k rounded up to 32)
   int32_t dp16, kp16;  // BF16 copies: pitch of O16 / X16 (d rounded up to 64) and of W16 (k rounded up to 64)
   int32_t bf16;        // 1: the tcgen05 path contracts BF16 operand copies (KGE_PREC_BF16)
+  int32_t x3;          // 1: 3xTF32 split precision (KGE_PREC_3XTF32)
   float gamma, lr, eps;
   int64_t n_entities, n_relations;
 };

@@ -21,6 +21,16 @@
 
 namespace kge {
 
+// 3xTF32 split (KGE_PREC_3XTF32): hi = x with the low 13 mantissa bits cleared (a tf32 value), lo = x - hi (exact)
+__device__ __forceinline__ void st_split4(float* hi_row, float* lo_row, int q, float4 v) {
+  const float4 h = make_float4(__uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u),
+                               __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u),
+                               __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u),
+                               __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u));
+  reinterpret_cast<float4*>(hi_row)[q] = h;
+  reinterpret_cast<float4*>(lo_row)[q] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+}
+
 // BF16 operand copies (KGE_PREC_BF16): float4 -> 4 bf16 (round to nearest even) stored as 8 bytes at element 4 q of
 // a bf16 row; returns the squared norm of the ROUNDED values (the tcgen05 expansion ||o||^2 - 2 o.x + ||x||^2 then
 // measures the distance of the rounded rows exactly up to fp32 accumulation)
@@ -355,6 +365,12 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
       st4(o, q, o4);
       X.v[m] = o4;  // keep o for the gradient below
     }
+    if (a.b.O_hi) {  // 3xTF32 split of o
+#pragma unroll
+      for (int m = 0; m < V; ++m)
+        if (lane + 32 * m < d4)
+          st_split4(a.b.O_hi + (int64_t)i * dm.dp, a.b.O_lo + (int64_t)i * dm.dp, lane + 32 * m, X.v[m]);
+    }
     if (a.b.O16) {  // BF16 copy of o; the expansion uses the norm of the rounded row
       on = 0.f;
       uint16_t* o16 = a.b.O16 + (int64_t)i * dm.dp16;
@@ -389,6 +405,11 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     float* o = a.b.O + (int64_t)i * dm.dp;
     float stat, on;
     combine_stage<V>(dm.model, mode, h, r, t, mode == 0 ? t : h, o, dm.d, lane, dm.family, stat, on);
+    if (a.b.O_hi) {  // 3xTF32 split of o (read back after the warp's stores)
+      __syncwarp();
+      for (int q = lane; q < (dm.d >> 2); q += 32)
+        st_split4(a.b.O_hi + (int64_t)i * dm.dp, a.b.O_lo + (int64_t)i * dm.dp, q, ld4(o, q));
+    }
     if (a.b.O16) {  // BF16 copy of o (this lane's own stores, read back), norm of the rounded row
       __syncwarp();
       on = 0.f;
@@ -424,6 +445,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
       if (v < d4) {
         const float4 xv = Xr.v[m];
         st4(X, v, xv);
+        if (a.b.X_hi) st_split4(a.b.X_hi + (int64_t)q * dm.dp, a.b.X_lo + (int64_t)q * dm.dp, v, xv);
         if (x16)
           acc += st_bf16x4(x16, v, xv);  // BF16 copy; the norm of the rounded row
         else

@@ -42,6 +42,8 @@ struct TcState {
   CUtensorMap mG_L;          // fused chain: gx rows of Gocc (written by k_gather), box {32, 64}
   // BF16 path (KGE_PREC_BF16): the same operand views over the bf16 copies, 64-element (128-byte) k-blocks
   CUtensorMap mO_F16, mX_F16, mW_K16, mW_MN16, mX_MN16, mO_MN16;
+  // 3xTF32 path (KGE_PREC_3XTF32): the contraction maps above point at the hi parts, these at the lo parts
+  CUtensorMap mO_Fl, mX_Fl, mW_Kl, mW_MNl, mX_MNl, mO_MNl;
   int fwd_cx = 1;  // backward TMA-store targets: Gocc, Grel, dO (SW128), box {32, 32}
   bool ok = false;
 };
@@ -95,6 +97,8 @@ struct TcArgs {
   int32_t* pcnt;   // pairwise ranking loss: active hinges per positive (StepBuffers::pcnt)
   uint16_t* W16;   // BF16 path: the forward writes dL/dS here (bf16, pitch kp16) instead of W
   int32_t dp16, kp16;
+  float* W_hi;     // 3xTF32 path: dL/dS split into tf32 hi + lo (pitch kp) instead of W
+  float* W_lo;
 };
 
 // f+ from the positive's pair statistic (k_gather's pstat), as the FFMA path's pair_score_from
@@ -125,13 +129,19 @@ __device__ __forceinline__ uint64_t sdesc_mn(uint32_t saddr, uint32_t lbo) {
 // ------------------------------------------------------------------------------------------------
 // BF: BF16 operands (kind::f16, k-blocks of 64 elements = the same 128-byte rows as the TF32 k-blocks of 32), W out
 // in bf16
-template <int FAM, bool BF>
+// X3: 3xTF32 split precision (KGE_PREC_3XTF32): every operand x = hi + lo with hi = x with the low 13 mantissa bits
+// cleared (exactly a tf32 value) and lo = x - hi (exact); S = O_hi X_hi^T + O_hi X_lo^T + O_lo X_hi^T accumulated in
+// fp32 TMEM -- the dropped O_lo X_lo^T term is ~2^-22 relative, FP32-level accuracy on the tensor cores. A stage
+// holds the hi and the lo operands of half as many k-blocks (the same shared-memory footprint).
+template <int FAM, bool BF, bool X3 = false>
 __global__ void __launch_bounds__(kFwdThreads, 1)
-    k_tc_fwd(const __grid_constant__ CUtensorMap mO, const __grid_constant__ CUtensorMap mX, TcArgs a) {
+    k_tc_fwd(const __grid_constant__ CUtensorMap mO, const __grid_constant__ CUtensorMap mX,
+             const __grid_constant__ CUtensorMap mOl, const __grid_constant__ CUtensorMap mXl, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
+  constexpr int KPB = X3 ? kFwdKpb / 2 : kFwdKpb;  // k-blocks per stage
   constexpr uint32_t A_KB = 128 * 128, B_KB = kNT * 128;  // one k-block of A (O rows) / B (X' rows)
-  constexpr uint32_t A_BYTES = kFwdKpb * A_KB, STAGE = kFwdKpb * (A_KB + B_KB);
+  constexpr uint32_t A_BYTES = KPB * A_KB, HALF = KPB * (A_KB + B_KB), STAGE = (X3 ? 2 : 1) * HALF;
   constexpr int kHalf = kNT / 2;  // columns this CTA finalises
   __shared__ uint64_t full[kFwdStages], empty[kFwdStages], done;
   __shared__ uint32_t tbase;
@@ -155,7 +165,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int c = blockIdx.z, i0 = blockIdx.y * 128, t = blockIdx.x >> 1, j0 = t * kNT;
   const int nkb = BF ? a.dp16 / 64 : a.dp / 32, kh = (nkb + 1) / 2;
   const int kb0 = ks ? kh : 0, kb1 = ks ? nkb : kh;
-  const int nst = (kb1 - kb0 + kFwdKpb - 1) / kFwdKpb;
+  const int nst = (kb1 - kb0 + KPB - 1) / KPB;
   const int jf0 = j0 + ks * kHalf;  // first column this CTA finalises
   if (threadIdx.x == 0) {
     for (int s = 0; s < kFwdStages; ++s) {
@@ -194,14 +204,18 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       uint8_t* sa = smem + s * STAGE;
       // a box always delivers its full size (out-of-range rows / k-blocks are zero-filled); with multicast only the
       // k-blocks of this half that exist are loaded (one box each)
-      const int kq = kb0 + q * kFwdKpb, nk = min(kFwdKpb, kb1 - kq);
-      mbar_arrive_expect_tx(&full[s], (cxn > 1 ? nk : kFwdKpb) * A_KB + kFwdKpb * B_KB);
+      const int kq = kb0 + q * KPB, nk = min(KPB, kb1 - kq);
+      mbar_arrive_expect_tx(&full[s], (cxn > 1 ? nk * A_KB + KPB * B_KB : STAGE));
       if (cxn > 1) {
         if (ntl < nk) tma_load_4d_mc(sa + ntl * A_KB, &mO, &full[s], 0, i0, kq + ntl, c, mmask);
       } else {
         tma_load_4d(sa, &mO, &full[s], 0, i0, kq, c);
       }
       tma_load_4d(sa + A_BYTES, &mX, &full[s], 0, j0, kq, c);
+      if (X3) {  // the lo halves of the same k-blocks
+        tma_load_4d(sa + HALF, &mOl, &full[s], 0, i0, kq, c);
+        tma_load_4d(sa + HALF + A_BYTES, &mXl, &full[s], 0, j0, kq, c);
+      }
     }
   } else if (warp >= 8 - kIssuers && lane == 0) {
     // MMA issuers: a single thread issues one tcgen05.mma per ~130 cycles whatever N is (measured, tools/mma_probe.cu),
@@ -215,14 +229,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_wait(&full[s], (st / kFwdStages) & 1);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
-      const int nk = min(kFwdKpb, kb1 - (kb0 + st * kFwdKpb));
+      const int nk = min(KPB, kb1 - (kb0 + st * KPB));
       for (int b = 0; b < nk; ++b) {
         // slice q of the k-block: K = 8 tf32 or 16 bf16 = 32 bytes into each 128-byte row
         const uint64_t ad = sdesc(sa + b * A_KB + q * 32, 16, 1024), bd = sdesc(sb + b * B_KB + q * 32, 16, 1024);
-        if (BF)
+        if (BF) {
           mma_bf16(acc, ad, bd, idesc, (st | b) ? 1u : 0u);
-        else
+        } else {
           mma_tf32(acc, ad, bd, idesc, (st | b) ? 1u : 0u);
+          if (X3) {  // + hi x lo + lo x hi
+            mma_tf32(acc, ad, sdesc(sb + HALF + b * B_KB + q * 32, 16, 1024), idesc, 1u);
+            mma_tf32(acc, sdesc(sa + HALF + b * A_KB + q * 32, 16, 1024), bd, idesc, 1u);
+          }
+        }
       }
       if (cxn > 1)
         mma_commit_mc(&empty[s], mmask);
@@ -334,7 +353,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   lsum += __logf(lprod);
   if (nact) atomicAdd(&a.pcnt[(int64_t)c * dm.g + i], nact);  // integer: exact in any order
   trace_stamp(dm.trace, KGE_K_NEG_FWD, 4);
-  if (iok && BF) {  // dL/dS in bf16 for the backward GEMMs (the pads beyond k stay zero)
+  if (iok && X3) {  // dL/dS split hi + lo for the 3xTF32 backward GEMMs
+    float* hrow = a.W_hi + ((int64_t)c * dm.g + i) * a.kp + jf0 + hf * 8;
+    float* lrow = a.W_lo + ((int64_t)c * dm.g + i) * a.kp + jf0 + hf * 8;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+      if (jf0 + hf * 8 + jj < dm.k) {
+        const float hi = __uint_as_float(__float_as_uint(v[jj]) & 0xFFFFE000u);
+        hrow[jj] = hi;
+        lrow[jj] = v[jj] - hi;
+      }
+  } else if (iok && BF) {  // dL/dS in bf16 for the backward GEMMs (the pads beyond k stay zero)
     uint16_t* wrow = a.W16 + ((int64_t)c * dm.g + i) * a.kp16 + jf0 + hf * 8;
     if (jf0 + hf * 8 + 8 <= dm.k) {
       uint4 u;
@@ -434,13 +463,15 @@ __device__ __forceinline__ void bwd_part(const TcArgs& a, int p, int& b0, int& n
   }
 }
 
-template <int FAM, bool BF>
+template <int FAM, bool BF, bool X3 = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_bwd(const __grid_constant__ CUtensorMap mW_K, const __grid_constant__ CUtensorMap mW_MN,
              const __grid_constant__ CUtensorMap mX_MN, const __grid_constant__ CUtensorMap mO_MN,
              const __grid_constant__ CUtensorMap mO_E, const __grid_constant__ CUtensorMap mX_E,
              const __grid_constant__ CUtensorMap mG_S, const __grid_constant__ CUtensorMap mR_S,
-             const __grid_constant__ CUtensorMap mD_S, const __grid_constant__ CUtensorMap mG_L, TcArgs a) {
+             const __grid_constant__ CUtensorMap mD_S, const __grid_constant__ CUtensorMap mG_L,
+             const __grid_constant__ CUtensorMap mW_Kl, const __grid_constant__ CUtensorMap mW_MNl,
+             const __grid_constant__ CUtensorMap mX_MNl, const __grid_constant__ CUtensorMap mO_MNl, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   __shared__ uint64_t full[kBwdStages], empty[kBwdStages], done, selfbar;
@@ -462,10 +493,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int KB = BF ? 64 : 32;      // contraction rows per k-block (one 128-byte row of the K-major operand)
   const int nkb = (nk + KB - 1) / KB, kh = (nkb + 1) / 2;
   const int kb0 = ks ? kh : 0, kb1 = ks ? nkb : kh;
-  const int nst = (kb1 - kb0 + kBwdKpb - 1) / kBwdKpb;
-  constexpr uint32_t A_BYTES = kBwdKpb * 16384, B_BYTES = kBwdKpb * 4 * 4096, STAGE = A_BYTES + B_BYTES;
+  constexpr int KPB = X3 ? kBwdKpb / 2 : kBwdKpb;  // k-blocks per stage (3xTF32: hi and lo of half as many)
+  const int nst = (kb1 - kb0 + KPB - 1) / KPB;
+  constexpr uint32_t A_BYTES = KPB * 16384, B_BYTES = KPB * 4 * 4096, HALF = A_BYTES + B_BYTES;
+  constexpr uint32_t STAGE = (X3 ? 2 : 1) * HALF;
   // bytes between MN blocks (32 tf32 / 64 bf16 columns) of an MN-major stage operand
-  constexpr uint32_t KROWS_B = kBwdKpb * KB * 128;
+  constexpr uint32_t KROWS_B = KPB * KB * 128;
   // shared memory: [stages][self: this CTA's 64 finalised rows x 4 column blocks of O (dO) / X' (dX'), SW128]
   // after the main loop the stage area holds xown ([32 float4 columns][64 rows]) and the TMA-store staging
   uint8_t* self_smem = smem + kBwdStages * STAGE;
@@ -568,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (issued >= kBwdStages) mbar_wait(&empty[s], ((issued / kBwdStages) - 1) & 1);
         uint8_t* sa = smem + s * STAGE;
         uint8_t* sb = sa + A_BYTES;
-        const int kq = kb0 + issued * kBwdKpb;
+        const int kq = kb0 + issued * KPB;
         mbar_arrive_expect_tx(&full[s], STAGE);
         // TF32: blocks of 32 columns (4 per box); BF16: of 64 (2 per box) -- the same 128-byte rows
         if (!pass_x)
@@ -576,6 +609,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
           tma_load_4d(sa, &mW_MN, &full[s], 0, kq * KB, r0 / KB, c);  // W^T: [j-blocks][K rows][128 B]
         tma_load_4d(sb, pass_x ? &mO_MN : &mX_MN, &full[s], 0, kq * KB, BF ? b0 / 2 : b0, c);  // [col blocks][K rows]
+        if (X3) {  // the lo halves
+          if (!pass_x)
+            tma_load_4d(sa + HALF, &mW_Kl, &full[s], 0, r0, kq, c);
+          else
+            tma_load_4d(sa + HALF, &mW_MNl, &full[s], 0, kq * KB, r0 / KB, c);
+          tma_load_4d(sb + HALF, pass_x ? &mO_MNl : &mX_MNl, &full[s], 0, kq * KB, b0, c);
+        }
       }
     };
     if (q == 0) {
@@ -599,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&full[s], (st / kBwdStages) & 1);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
-      const int nkq = min(kBwdKpb, kb1 - (kb0 + st * kBwdKpb));
+      const int nkq = min(KPB, kb1 - (kb0 + st * KPB));
       for (int b = 0; b < nkq; ++b) {
         if (BF) {  // K slice q = 16 rows: 2048 B into an MN-major operand, 32 B into a K-major row
           const uint32_t koff = (uint32_t)(b * 64 + q * 16) * 128;
@@ -608,7 +648,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           const uint32_t koff = (uint32_t)(b * 32 + q * 8) * 128;  // K rows of an MN-major operand
           const uint64_t ad = pass_x ? sdesc_mn(sa + koff, KROWS_B) : sdesc(sa + b * 16384 + q * 32, 16, 1024);
-          mma_tf32(acc, ad, sdesc_mn(sb + koff, KROWS_B), idesc, (st | b) ? 1u : 0u);
+          const uint64_t bd = sdesc_mn(sb + koff, KROWS_B);
+          mma_tf32(acc, ad, bd, idesc, (st | b) ? 1u : 0u);
+          if (X3) {  // + hi x lo + lo x hi
+            const uint64_t al = pass_x ? sdesc_mn(sa + HALF + koff, KROWS_B)
+                                       : sdesc(sa + HALF + b * 16384 + q * 32, 16, 1024);
+            mma_tf32(acc, ad, sdesc_mn(sb + HALF + koff, KROWS_B), idesc, 1u);
+            mma_tf32(acc, al, bd, idesc, 1u);
+          }
         }
       }
       mma_commit(&empty[s]);
@@ -813,6 +860,7 @@ bool tc_init(kge_handle* h) {
   if (h->dp > 512 || bwd_smem(h->dp) > 227 * 1024 || (dm.dp / 32 + kNSplit - 1) / kNSplit > 4 || h->kp % 32)
     return false;
   if (dm.bf16 && (2 * ((dm.dp16 / 64 + kNSplit - 1) / kNSplit) > 4 || !h->buf.O16)) return false;
+  if (dm.x3 && !h->buf.O_hi) return false;
   TcState* st = new TcState();
   const StepBuffers& b = h->buf;
   bool ok = true;
@@ -820,7 +868,7 @@ bool tc_init(kge_handle* h) {
   // O multicast across cxn = kFwdKpb tiles (clusters of 8 CTAs) is off by default: measured on the Freebase step, the
   // 8-CTA clusters wait for room in one GPC while the gather kernel drains, which costs more than the L2 reads saved
   // (37.3 vs 42.8 us per step); KGE_FWD_MC=1 turns it on for experiments
-  st->fwd_cx = getenv("KGE_FWD_MC") && fx % kFwdKpb == 0 ? kFwdKpb : 1;
+  st->fwd_cx = getenv("KGE_FWD_MC") && fx % kFwdKpb == 0 && !dm.x3 ? kFwdKpb : 1;
   ok &= make_map4(&st->mO_F, b.O, h->dp, dm.g, dm.C, h->dp, 128, st->fwd_cx > 1 ? 1 : kFwdKpb);
   ok &= make_map4(&st->mX_F, b.X, h->dp, dm.k, dm.C, h->dp, kNT, kFwdKpb);
   // backward operands (4D {32, rows, 32-column blocks, chunk}): W K-major (dO's A), W / X' / O MN-major with K = rows
@@ -846,6 +894,28 @@ bool tc_init(kge_handle* h) {
     ok &= make_map4_16(&st->mX_MN, b.X16, dm.dp16, dm.k, dm.C, dm.dp16, 64 * kBwdKpb, 2);
     ok &= make_map4_16(&st->mO_MN, b.O16, dm.dp16, dm.g, dm.C, dm.dp16, 64 * kBwdKpb, 2);
   }
+  if (dm.x3) {  // 3xTF32: hi and lo parts, half as many k-blocks per stage (k_tc_fwd / k_tc_bwd X3)
+    const int kf = kFwdKpb / 2, kb = kBwdKpb / 2;
+    ok &= make_map4(&st->mO_F, b.O_hi, h->dp, dm.g, dm.C, h->dp, 128, kf);
+    ok &= make_map4(&st->mO_Fl, b.O_lo, h->dp, dm.g, dm.C, h->dp, 128, kf);
+    ok &= make_map4(&st->mX_F, b.X_hi, h->dp, dm.k, dm.C, h->dp, kNT, kf);
+    ok &= make_map4(&st->mX_Fl, b.X_lo, h->dp, dm.k, dm.C, h->dp, kNT, kf);
+    ok &= make_map4(&st->mW_K, b.W_hi, h->kp, dm.g, dm.C, h->kp, 128, kb);
+    ok &= make_map4(&st->mW_Kl, b.W_lo, h->kp, dm.g, dm.C, h->kp, 128, kb);
+    ok &= make_map4(&st->mW_MN, b.W_hi, h->kp, dm.g, dm.C, h->kp, 32 * kb, 4, mn);
+    ok &= make_map4(&st->mW_MNl, b.W_lo, h->kp, dm.g, dm.C, h->kp, 32 * kb, 4, mn);
+    ok &= make_map4(&st->mX_MN, b.X_hi, h->dp, dm.k, dm.C, h->dp, 32 * kb, 4, mn);
+    ok &= make_map4(&st->mX_MNl, b.X_lo, h->dp, dm.k, dm.C, h->dp, 32 * kb, 4, mn);
+    ok &= make_map4(&st->mO_MN, b.O_hi, h->dp, dm.g, dm.C, h->dp, 32 * kb, 4, mn);
+    ok &= make_map4(&st->mO_MNl, b.O_lo, h->dp, dm.g, dm.C, h->dp, 32 * kb, 4, mn);
+  } else {  // unused parameters of the other instantiations
+    st->mO_Fl = st->mO_F;
+    st->mX_Fl = st->mX_F;
+    st->mW_Kl = st->mW_K;
+    st->mW_MNl = st->mW_MN;
+    st->mX_MNl = st->mX_MN;
+    st->mO_MNl = st->mO_MN;
+  }
   if (!ok) {
     delete st;
     return false;
@@ -855,7 +925,14 @@ bool tc_init(kge_handle* h) {
     e = cudaFuncSetAttribute(fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem());
     if (e == cudaSuccess) e = cudaFuncSetAttribute(bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_smem(h->dp));
   };
-  if (dm.bf16) {
+  if (dm.x3) {
+    if (dm.family == FAM_DOT)
+      attrs(k_tc_fwd<FAM_DOT, false, true>, k_tc_bwd<FAM_DOT, false, true>);
+    else if (dm.family == FAM_L2)
+      attrs(k_tc_fwd<FAM_L2, false, true>, k_tc_bwd<FAM_L2, false, true>);
+    else
+      attrs(k_tc_fwd<FAM_L2SQ, false, true>, k_tc_bwd<FAM_L2SQ, false, true>);
+  } else if (dm.bf16) {
     if (dm.family == FAM_DOT)
       attrs(k_tc_fwd<FAM_DOT, true>, k_tc_bwd<FAM_DOT, true>);
     else if (dm.family == FAM_L2)
@@ -924,23 +1001,30 @@ cudaError_t launch_tc_neg(kge_handle* h, const Slot& s) {
            tc_fuses_chain(h) ? 1 : 0, s, h->rows, h->buf.wpos, h->buf.pstat, h->buf.lpos, h->buf.Grel,
            h->buf.loss, h->buf.flags, h->n_neg_parts, 1.f / ((float)dm.B * (float)dm.k), st->xbuf, tc_flow() ? h->buf.flow : nullptr,
            2 * ((dm.k + kNT - 1) / kNT) * ((dm.g + 127) / 128), st->fwd_cx, h->buf.fdbg, h->buf.pcnt, h->buf.W16,
-           dm.dp16, dm.kp16};
+           dm.dp16, dm.kp16, h->buf.W_hi, h->buf.W_lo};
   dim3 gf(2 * ((dm.k + kNT - 1) / kNT), (dm.g + 127) / 128, dm.C);  // x = 2 tile + split-K half
   const int tiles = (std::max(dm.g, dm.k) + 127) / 128;
   dim3 gb(2 * tiles * kNSplit, dm.C, 2);  // x = 2 (row tile * kNSplit + column part) + split-K half
   const bool odd = h->buf.Gocc != h->gocc2[0];  // lag = 1: odd steps write the second Gocc buffer
   auto run = [&](auto fwd, auto bwd) -> cudaError_t {
     launch_begin(h, KGE_K_NEG_FWD);
-    launch_pdl_cluster(fwd, gf, kFwdThreads, fwd_smem(), h->stream, 2 * st->fwd_cx, st->mO_F, st->mX_F, a);
+    launch_pdl_cluster(fwd, gf, kFwdThreads, fwd_smem(), h->stream, 2 * st->fwd_cx, st->mO_F, st->mX_F, st->mO_Fl,
+                       st->mX_Fl, a);
     launch_end(h, KGE_K_NEG_FWD);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     launch_begin(h, KGE_K_NEG_BWD);
     launch_pdl_cluster(bwd, gb, kThreads, bwd_smem(h->dp), h->stream, 2, st->mW_K, st->mW_MN, st->mX_MN, st->mO_MN,
-                       st->mO_E, st->mX_E, odd ? st->mG_S1 : st->mG_S, st->mR_S, st->mD_S, odd ? st->mG_L1 : st->mG_L, a);
+                       st->mO_E, st->mX_E, odd ? st->mG_S1 : st->mG_S, st->mR_S, st->mD_S, odd ? st->mG_L1 : st->mG_L,
+                       st->mW_Kl, st->mW_MNl, st->mX_MNl, st->mO_MNl, a);
     launch_end(h, KGE_K_NEG_BWD);
     return cudaGetLastError();
   };
+  if (dm.x3) {
+    if (dm.family == FAM_DOT) return run(k_tc_fwd<FAM_DOT, false, true>, k_tc_bwd<FAM_DOT, false, true>);
+    if (dm.family == FAM_L2) return run(k_tc_fwd<FAM_L2, false, true>, k_tc_bwd<FAM_L2, false, true>);
+    return run(k_tc_fwd<FAM_L2SQ, false, true>, k_tc_bwd<FAM_L2SQ, false, true>);
+  }
   if (dm.bf16) {
     if (dm.family == FAM_DOT) return run(k_tc_fwd<FAM_DOT, true>, k_tc_bwd<FAM_DOT, true>);
     if (dm.family == FAM_L2) return run(k_tc_fwd<FAM_L2, true>, k_tc_bwd<FAM_L2, true>);

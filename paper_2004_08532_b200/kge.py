@@ -24,7 +24,7 @@ os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 MODELS = {"transe_l1": 0, "transe_l2": 1, "distmult": 2, "complex": 3, "rotate": 4, "transr": 5, "rescal": 6}
 CORRUPT = {"tail": 0, "head": 1, "alternate": 2}
-PRECISION = {"fp32": 0, "tf32": 1, "bf16": 2}
+PRECISION = {"fp32": 0, "tf32": 1, "bf16": 2, "3xtf32": 3}
 LOSS = {"logistic": 0, "pairwise": 1}
 STATUS = {0: "KGE_OK", -1: "KGE_EINVAL", -2: "KGE_ERANGE", -3: "KGE_ENOMEM", -4: "KGE_ECUDA", -5: "KGE_ENCCL",
           -6: "KGE_ENONFINITE", -7: "KGE_ESTATE", -8: "KGE_EUNSUPPORTED"}
@@ -346,7 +346,7 @@ class Handle:
     @property
     def neg_path(self):
         """Arithmetic of the negative contraction: "ffma", "tf32" or "bf16" (tcgen05), see kge_neg_path."""
-        return {0: "ffma", 1: "tf32", 2: "bf16"}[lib().kge_neg_path(self._h)]
+        return {0: "ffma", 1: "tf32", 2: "bf16", 3: "3xtf32"}[lib().kge_neg_path(self._h)]
 
     def read_losses(self, first_step, n):
         out = np.zeros(n, np.float32)

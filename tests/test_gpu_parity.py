@@ -357,3 +357,18 @@ def test_degree_negatives_bit_exact_and_training(kd):
     orc.train(1)
     ids = np.arange(gr.n_entities)
     assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 1e-4
+
+
+# ---------------------------------------------------------------- 3xTF32 split precision on the tensor cores
+@pytest.mark.parametrize("model", TC_MODELS)
+def test_3xtf32_meets_the_fp32_bars(model):
+    # hi + lo splits of O, X' and W, three tcgen05 MMAs per K slice -- the FP32 bars of the
+    # north_star on the tensor cores: loss 1e-5 relative every step, rows 1e-4 absolute after 100 steps
+    gpu, orc, trip = _tiny(model, dim=64, precision="3xtf32")
+    assert gpu.neg_path == "3xtf32"
+    lg, lo = gpu.train_step(100), orc.train(100)
+    rel = np.abs(lg - lo) / np.abs(lo)
+    assert rel.max() <= 1e-5, (model, rel.max(), int(np.argmax(rel)))
+    ids, rids = np.arange(orc.cfg.n_entities), np.arange(orc.cfg.n_relations)
+    assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 1e-4
+    assert np.abs(gpu.get_rows(1, rids) - orc.get_rows(1, rids)).max() <= 1e-4

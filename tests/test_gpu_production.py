@@ -226,3 +226,22 @@ def test_freebase_bench_configuration():
     # TF32 rows are reported and loosely bounded (reading c.14: ~2^-11 relative gradient error x the O(lr) step)
     assert drift <= 5e-3, drift
     print(f"freebase tf32: per-pair {err:.2e}, loss {np.max(np.abs(lg - lo) / np.abs(lo)):.2e}, row drift {drift:.2e}")
+
+
+@pytest.mark.parametrize("graph,model", [("fb15k", "transe_l2"), ("fb15k", "distmult"), ("wn18", "rotate")])
+def test_production_3xtf32_fp32_bars(graph, model):
+    # 3xTF32 at configs[1]/[2]/[4]'s shape: per-pair scores and the loss at the FP32 bar (1e-5), teacher-forced rows
+    # at 1e-4
+    gr, trip, gpu, orc = _pair(graph, model, 400, precision="3xtf32")
+    assert gpu.neg_path == "3xtf32"
+    heads, rels, tails = (np.asarray(a) for a in trip)
+    ids, rids = np.arange(gr.n_entities), np.arange(gr.n_relations)
+    for s in range(3):
+        U.copy_tables(orc, gpu, model, gr.n_entities, gr.n_relations)
+        gpu.set_option("capture_neg", 1)
+        ref, meta = U.pair_scores(orc, s, heads, rels, tails, SHAPE[1])
+        lg, lo = gpu.train_step(1)[0], orc.train(1)[0]
+        assert U.check_pair_scores(model, gpu.neg_scores(), ref, meta, orc, SHAPE[1], 1e-5) <= 1e-5
+        assert abs(lg - lo) / abs(lo) <= 1e-5
+        assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 1e-4
+        assert np.abs(gpu.get_rows(1, rids) - orc.get_rows(1, rids)).max() <= 1e-4
