@@ -202,7 +202,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--workload", default="freebase", choices=sorted(WORKLOADS))
     ap.add_argument("--model", default=None)
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16", "fp32"])
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16", "3xtf32", "fp32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1000)
@@ -314,8 +314,8 @@ def main():
     tf32_peak = bf16_tf * (1.1 / 2.25)  # B200_PROFILING.md nominal dense tf32 / bf16 ratio x the measured bf16 burst
     alu_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # FFMA: 148 SMs x 128 FP32 lanes x FMA x 1.965 GHz
     path = H.neg_path  # what the library actually runs (kge_neg_path): "ffma", "tf32" or "bf16"
-    tc = path in ("tf32", "bf16")
-    tc_peak = bf16_tf if path == "bf16" else tf32_peak
+    tc = path in ("tf32", "bf16", "3xtf32")
+    tc_peak = bf16_tf if path == "bf16" else (tf32_peak / 3 if path == "3xtf32" else tf32_peak)
     flops_neg = 2.0 * B * k * d  # one contraction of the chunked negatives (S = O X'^T)
     traffic = ncu_traffic()
 
@@ -331,7 +331,9 @@ def main():
             ach = fl / (ms / 1000.0) / 1e12
             r = {"bound": "tensor" if tc else "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                  "frac": ach / peak, "alg_flops_per_launch": fl,
-                 "peak_note": ((f"{src} bf16 burst" if path == "bf16" else f"tf32 = (1.1/2.25) x {src} bf16 burst")
+                 "peak_note": ((f"{src} bf16 burst" if path == "bf16" else
+                                ("3xtf32 = tf32 / 3 (three MMAs per product)" if path == "3xtf32" else
+                                 f"tf32 = (1.1/2.25) x {src} bf16 burst"))
                                if tc else "148 SM x 128 FP32 lanes x FMA x 1.965 GHz"),
                  "impl": ("k_tc_fwd" if name == "k_neg_fwd" else "k_tc_bwd") if tc else name}
         else:
@@ -401,7 +403,7 @@ def main():
         clocks = clk.summary()
         line = {"metric": METRIC, "value": value, "unit": "positive triples/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": {"ffma": "f32", "tf32": "tf32", "bf16": "bf16"}[path], "data": "synthetic",
+                "vs_baseline": None, "dtype": {"ffma": "f32", "tf32": "tf32", "bf16": "bf16", "3xtf32": "3xtf32"}[path], "data": "synthetic",
                 "config": {"workload": f"{gname}-shaped synthetic (BASELINE.json configs)", "model": model, "dim": d,
                            "batch": B, "chunk": g, "neg_k": k, "lag": args.lag, "n_entities": gr.n_entities,
                            "n_relations": gr.n_relations, "n_triples": gr.n_triples,
