@@ -269,8 +269,10 @@ int kge_debug_neg_scores(kge_handle* h, float* out);
 
 /* Diagnostics. Kernel ids for kge_profile_end. Between begin and end every kernel launch of the step is bracketed by
  * CUDA events on the stream it runs on, and programmatic dependent launch is off (each kernel starts after its
- * predecessor completed), so the durations are those of each kernel alone; end synchronises and returns the average
- * device duration (ms) and the number of launches per kernel id. kge_launch_count: total kernel launches the handle
+ * predecessor completed), so the durations are those of each kernel alone; begin also holds the main stream behind a
+ * gate kernel that end releases, so the bracketed launches are all queued when the GPU reaches them and the event
+ * pairs exclude the host's submission latency (keep a profiled region to a few dozen steps: the gate gives up after
+ * 2 s); end synchronises and returns the average device duration (ms) and the number of launches per kernel id. kge_launch_count: total kernel launches the handle
  * has issued. */
 enum { KGE_K_SAMPLE = 0, KGE_K_GATHER = 1, KGE_K_NEG_FWD = 2, KGE_K_NEG_BWD = 3, KGE_K_CHAIN = 4, KGE_K_UPDATE = 5,
        KGE_K_COUNT = 6 };

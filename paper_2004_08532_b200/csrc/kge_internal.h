@@ -278,6 +278,8 @@ struct kge_handle {
   int64_t step = 0;
   int64_t launches = 0;
   kge::Profiler prof;
+  int32_t* prof_gate = nullptr;  // mapped pinned flag of the profiling gate (kge_profile_begin / end)
+  bool prof_gated = false;
   std::vector<void*> allocs;
   // sizes
   uint32_t k0 = 0, k1 = 0;

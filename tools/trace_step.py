@@ -14,12 +14,17 @@ s = torch.cuda.Stream()
 with torch.cuda.stream(s):
     h = kge.init(cfg, *trip, stream=s)
 steady = "steady" in sys.argv  # steady: the traced step is the last of a back-to-back run (host far ahead)
+prof = "prof" in sys.argv  # the bench's isolated-kernel mode: profiler on (events around launches, PDL off)
 if steady:
     h.train_step(71, return_loss=False)
 else:
     h.train_step(70, return_loss=False)
     h.sync()
+    if prof:
+        h.profile_begin()
     h.train_step(1, return_loss=False)
+    if prof:
+        print("profile (ms):", {k: round(v[0], 4) for k, v in h.profile_end().items() if v[1]})
 h.sync()
 L = kge.lib()
 L.kge_debug_trace.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]
