@@ -1282,16 +1282,26 @@ int kge_rank(kge_handle* h, const int64_t* hs, const int64_t* rs, const int64_t*
   if (!fv.empty()) CK(cudaMemcpyAsync(d + o_fv, fv.data(), fv.size() * 4, cudaMemcpyHostToDevice, h->stream));
   const int32_t* di = reinterpret_cast<const int32_t*>(d);
   int64_t* d_out = reinterpret_cast<int64_t*>(d + o_out);
-  for (int sd = 0; sd < nside; ++sd)
-    CK(launch_rank(h, di, di + n, di + 2 * n, n, nside == 2 ? sd : (corrupt_head ? 1 : 0),
-                   cand_off ? reinterpret_cast<const int64_t*>(d + o_co) : nullptr,
-                   reinterpret_cast<const int32_t*>(d + o_cv),
-                   filt_off ? reinterpret_cast<const int64_t*>(d + o_fo) + (size_t)sd * n : nullptr,
-                   reinterpret_cast<const int32_t*>(d + o_fv), d_out + (size_t)sd * n));
+  // every entity a candidate on a TF32 handle of a contraction family: the tcgen05 ranking kernel (rank_tc.cu) -- it
+  // returns the counts, the rank is 1 + count; otherwise the FFMA streaming kernel
+  const bool tcr = !cand_off && rank_tc_supported(h) && getenv("KGE_RANK_FFMA") == nullptr;
+  for (int sd = 0; sd < nside; ++sd) {
+    const int side = nside == 2 ? sd : (corrupt_head ? 1 : 0);
+    const int64_t* fo_d = filt_off ? reinterpret_cast<const int64_t*>(d + o_fo) + (size_t)sd * n : nullptr;
+    if (tcr)
+      CK(launch_rank_tc(h, di, di + n, di + 2 * n, n, side, fo_d, reinterpret_cast<const int32_t*>(d + o_fv),
+                        d_out + (size_t)sd * n));
+    else
+      CK(launch_rank(h, di, di + n, di + 2 * n, n, side, cand_off ? reinterpret_cast<const int64_t*>(d + o_co) : nullptr,
+                     reinterpret_cast<const int32_t*>(d + o_cv), fo_d, reinterpret_cast<const int32_t*>(d + o_fv),
+                     d_out + (size_t)sd * n));
+  }
   std::vector<int64_t> r((size_t)nside * n);
   CK(cudaMemcpyAsync(r.data(), d_out, (size_t)nside * n * 8, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaFreeAsync(d, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  if (tcr)
+    for (auto& x : r) x += 1;
   pool_sides(r, n, corrupt_head, ranks_out);
   return KGE_OK;
 }

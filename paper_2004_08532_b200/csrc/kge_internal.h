@@ -366,6 +366,9 @@ cudaError_t launch_rank(kge_handle* h, const int32_t* hs, const int32_t* rs, con
                         const int64_t* cand_off, const int32_t* cand, const int64_t* filt_off, const int32_t* filt,
                         int64_t* ranks);
 cudaError_t launch_rows(kge_handle* h, float* tab, int32_t w, const int32_t* ids, int64_t n, float* buf, bool write);
+bool rank_tc_supported(const kge_handle* h);  // rank_tc.cu: tcgen05 all-entity ranking for this handle
+cudaError_t launch_rank_tc(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n, int head,
+                           const int64_t* filt_off, const int32_t* filt, int64_t* ranks);  // ranks - 1 (counts)
 cudaError_t launch_eval_cand(kge_handle* h, int64_t n, int32_t n_uniform, int32_t n_degree, int32_t both,
                              uint64_t seed, int32_t* cand_t, int32_t* cand_h);
 

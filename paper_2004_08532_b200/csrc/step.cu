@@ -1692,6 +1692,36 @@ __global__ void __launch_bounds__(256) k_rank(RankArgs a, int64_t n) {
   }
 }
 
+// tcgen05 ranking prep (rank_tc.cu): per query (warp) o_q = combine(h, r) | combine'(r, t) into O (pitch dp),
+// ||o_q||^2, the true entity's row into T and its id
+__global__ void k_rank_prep(Dims dm, EntRows ent, const float* rel, const int32_t* hs, const int32_t* rs,
+                            const int32_t* ts, int64_t n, int head, float* O, float* onorm, float* T, int32_t* true_e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (q >= n) return;
+  const float* h = ent.row(hs[q]);
+  const float* t = ent.row(ts[q]);
+  const float* r = rel + (int64_t)rs[q] * dm.drel;
+  const float* x = head ? h : t;
+  float st, on;
+  combine_row(dm.model, head, h, r, t, O + q * dm.dp, dm.d, lane, x, dm.family, st, on);
+  on = warp_sum(on);
+  for (int v = lane; v < (dm.d >> 2); v += 32) st4(T + q * dm.dp, v, ld4(x, v));
+  if (lane == 0) {
+    onorm[q] = on;
+    true_e[q] = head ? hs[q] : ts[q];
+  }
+}
+
+cudaError_t launch_rank_prep(kge_handle* h, const int32_t* hs, const int32_t* rs, const int32_t* ts, int64_t n,
+                             int head, float* O, float* onorm, float* T, int32_t* true_e) {
+  if (n == 0) return cudaSuccess;
+  k_rank_prep<<<(unsigned)((n * 32 + 255) / 256), 256, 0, h->stream>>>(h->dims, h->rows, h->rel, hs, rs, ts, n, head, O,
+                                                                       onorm, T, true_e);
+  ++h->launches;
+  return cudaGetLastError();
+}
+
 // Second-protocol candidates (reading c.15'): slot j of query i draws u from Philox(ctr=(j/2,
 // lo32(i), hi32(i), EVAL), key = eval seed); uniform slots: an entity (both sides: a (side, entity) pair) uniform;
 // degree slots: a uniform endpoint of the graph's triples (both sides: and a side bit). Writes the entity into the

@@ -211,3 +211,51 @@ def test_training_improves_filtered_mrr(model):
     gpu.train_step(1600)
     after = kge.link_metrics(gpu.rank(*q, filters=filt))["MRR"]
     assert after > 2.0 * before, (before, after)
+
+
+@pytest.mark.parametrize("model", ["transe_l2", "distmult", "complex", "rotate"])
+def test_ranks_tcgen05_all_entity(model):
+    # on a TF32 handle the all-entity protocol is the tcgen05 contraction S = O E^T (rank_tc.cu). FB15k-sized
+    # entity set (117 entity tiles), d = 96, raw / filtered / both sides; against the oracle's explicit-sort ranks with
+    # the TF32 near-tie window (candidates whose oracle score lies within 2e-3 (|f_true| + 1) of the positive's may fall
+    # on either side), and planted twins of a true entity tie it exactly (pessimistic) unless filtered
+    gr = synth.graph("fb15k")
+    trip = gr.triples()
+    d = 96
+    cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=d, batch_size=256,
+                     chunk_size=64, neg_k=64, gamma=12.0, lr=0.1, seed=4, neg_precision="tf32")
+    gpu = kge.init(cfg, *trip)
+    assert gpu.neg_path == "tf32"
+    gpu.train_step(5)
+    test = np.random.default_rng(8).integers(0, gr.n_triples, 150)  # 2 query tiles, the second ragged
+    hs, rs, ts = trip[0][test], trip[1][test], trip[2][test]
+    twins = [e for e in (17, 2222, 9999) if e not in (int(ts[0]), int(hs[0]))]
+    gpu.set_rows(0, twins, np.repeat(gpu.get_rows(0, [ts[0]]), len(twins), 0))
+    orc = O.Trainer(model, gr.n_entities, gr.n_relations, d, 256, 64, 64, gamma=12.0, lr=0.1, seed=4, triples=trip)
+    for table, n in ((0, gr.n_entities), (1, gr.n_relations)):
+        ids = np.arange(n)
+        orc.set_rows(table, ids, gpu.get_rows(table, ids).astype(np.float64))
+    off, ids = kge.filter_lists(trip, hs, rs, ts)
+    lists = [list(ids[off[i]:off[i + 1]]) for i in range(len(test))]
+    lists[0] += twins[:2]
+    off = np.concatenate([[0], np.cumsum([len(x) for x in lists])]).astype(np.int64)
+    fl = np.concatenate([np.asarray(x, np.int64) for x in lists])
+    raw, fil = gpu.rank(hs, rs, ts), gpu.rank(hs, rs, ts, filters=(off, fl))
+    known = {(int(hs[i]), int(rs[i]), int(e)) for i in range(len(test)) for e in lists[i]}
+    ref_raw, ref_fil = O.link_rank(orc, hs, rs, ts), O.link_rank(orc, hs, rs, ts, known=known)
+
+    def near(i, head=False):
+        f_true = orc.score_triples([hs[i]], [rs[i]], [ts[i]])[0]
+        ents = np.arange(gr.n_entities)
+        f = (orc.score_triples(ents, np.full_like(ents, rs[i]), np.full_like(ents, ts[i])) if head else
+             orc.score_triples(np.full_like(ents, hs[i]), np.full_like(ents, rs[i]), ents))
+        nt = int(np.sum(np.abs(f - f_true) <= 2e-3 * (abs(f_true) + 1.0)))
+        return nt - (len(twins) if (i == 0 and not head) else 0)  # exact twins are decided exactly
+
+    for i in range(len(test)):
+        w = near(i)
+        assert abs(int(raw[i]) - int(ref_raw[i])) <= w and abs(int(fil[i]) - int(ref_fil[i])) <= w, (i, raw[i], ref_raw[i])
+    assert raw[0] - fil[0] >= 2  # the filtered twins never count; the unfiltered one ties and ranks above
+    # pooled sides on the tensor-core path: = tail + head - 1 with the one-sided ranks of the same kernel
+    both = gpu.rank(hs[:40], rs[:40], ts[:40], head="both")
+    assert np.array_equal(both, gpu.rank(hs[:40], rs[:40], ts[:40]) + gpu.rank(hs[:40], rs[:40], ts[:40], head=True) - 1)
