@@ -32,7 +32,7 @@ class Config(ctypes.Structure):
                 ("init_bound", ctypes.c_float), ("seed", ctypes.c_uint64), ("corrupt", ctypes.c_int32),
                 ("rotate_variant", ctypes.c_int32), ("world_size", ctypes.c_int32), ("lazy_rows", ctypes.c_int32),
                 ("lag", ctypes.c_int32), ("neg_deg_k", ctypes.c_int32), ("neg_local", ctypes.c_int32),
-                ("loss", ctypes.c_int32), ("repartition", ctypes.c_int32)]
+                ("loss", ctypes.c_int32), ("repartition", ctypes.c_int32), ("placement", ctypes.c_int32)]
 
 
 TRIPLE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, _i64p, _i64p, _i64p)
@@ -62,6 +62,9 @@ def lib():
         L.orc_relation_partition_epoch.argtypes = [_i64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                                    ctypes.c_uint64, ctypes.c_uint32, P(ctypes.c_int32)]
         L.orc_relation_partition_epoch.restype = ctypes.c_int32
+        L.orc_locality_order.argtypes = [_i64p, _i64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _i64p,
+                                         P(ctypes.c_int32)]
+        L.orc_locality_order.restype = ctypes.c_int64
         L.orc_rank_triples.argtypes = [_i64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _i64p]
         L.orc_rank_triples.restype = ctypes.c_int64
         L.orc_score.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, _dp, _dp, _dp, _dp]
@@ -232,6 +235,16 @@ def relation_partition(rels, n_rel, P_, seed=None, epoch=None):
     return owner, ns
 
 
+def locality_order(heads, tails, n_entities, P_):
+    """c.13'' BFS-grown balanced parts (SPEC partition_graph_greedy) and the shard renumbering: (new_id, part, cut)."""
+    h, t = np.ascontiguousarray(heads, np.int64), np.ascontiguousarray(tails, np.int64)
+    nid = np.zeros(n_entities, np.int64)
+    part = np.zeros(n_entities, np.int32)
+    cut = lib().orc_locality_order(_p(h, ctypes.c_int64), _p(t, ctypes.c_int64), len(h), n_entities, P_,
+                                   _p(nid, ctypes.c_int64), _p(part, ctypes.c_int32))
+    return nid, part, cut
+
+
 def rank_triples(rels, n_rel, P_, rank):
     rels = np.ascontiguousarray(rels, dtype=np.int64)
     n = lib().orc_rank_triples(_p(rels, ctypes.c_int64), len(rels), n_rel, P_, rank, None)
@@ -246,14 +259,14 @@ class Trainer:
     def __init__(self, model, n_entities, n_relations, dim, batch, chunk, neg_k, gamma=12.0, lr=0.1, eps=1e-10,
                  init_bound=0.0, seed=1, corrupt=ALTERNATE, rotate_variant=0, world_size=1, precision=0,
                  triples=None, graph=None, lazy_rows=False, lag=0, neg_deg_k=0, neg_local=0, loss="logistic",
-                 repartition=0):
+                 repartition=0, placement=0):
         if isinstance(model, str):
             model = MODEL_IDS[model]
         self.model = model
         self.cfg = Config(model, precision, n_entities, n_relations, dim, batch, chunk, neg_k, gamma, lr, eps,
                           init_bound, seed, corrupt, rotate_variant, world_size, int(lazy_rows), int(lag),
                           int(neg_deg_k), int(neg_local), LOSSES[loss] if isinstance(loss, str) else int(loss),
-                          int(repartition))
+                          int(repartition), int(placement))
         self._keep = []
         if triples is not None:
             h, r, t = [np.ascontiguousarray(a, dtype=np.int64) for a in triples]

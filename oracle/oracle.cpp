@@ -496,6 +496,71 @@ int32_t relation_partition(const int64_t* rels, int64_t nt, int64_t nr, int32_t 
   return n_split;
 }
 
+// c.13'' head-owner placement (PAPER.md:395-406 [3.2]: a machine holds "all entities and triplets incident to the
+// entities" of its partition; SPEC: single ownership by the head's part): triple i belongs to the rank owning its
+// head, h_i mod P; every relation may then appear on every rank (all replicated, their gradients summed in rank
+// order -- the union-step semantics of c.13 do not change).
+void head_owner_lists(const std::vector<int64_t>& heads, int32_t P, std::vector<std::vector<int64_t>>& lists) {
+  lists.assign((size_t)P, {});
+  for (size_t i = 0; i < heads.size(); ++i) lists[(size_t)(heads[i] % P)].push_back((int64_t)i);
+}
+
+// c.13'' METIS-style locality ordering (PAPER.md:395-406 deploys METIS; SPEC's built-in substitute
+// partition_graph_greedy: BFS-grown balanced parts). Part w takes exactly n_w = ceil((N_e - w) / P) entities (the
+// size of rank w's shard under owner = e mod P): starting from the lowest-id unassigned entity, breadth-first over the
+// undirected entity graph of the triples (neighbours in ascending id, an entity joins the part when discovered) until
+// the part is full (a new seed = the lowest unassigned id when the frontier empties). The renumbering new(e) = P j + w
+// (j = position of e among part w's entities in ascending old id) puts part w on rank w's shard. Returns the edge cut
+// (triples whose head and tail fall in different parts).
+int64_t locality_order(const int64_t* heads, const int64_t* tails, int64_t nt, int64_t ne, int32_t P,
+                       std::vector<int64_t>& new_id, std::vector<int32_t>& part) {
+  std::vector<std::vector<int64_t>> adj((size_t)ne);
+  for (int64_t i = 0; i < nt; ++i) {
+    if (heads[i] == tails[i]) continue;
+    adj[(size_t)heads[i]].push_back(tails[i]);
+    adj[(size_t)tails[i]].push_back(heads[i]);
+  }
+  for (auto& a : adj) {
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+  }
+  part.assign((size_t)ne, -1);
+  int64_t next_seed = 0;
+  for (int32_t w = 0; w < P; ++w) {
+    const int64_t target = (ne - w + P - 1) / P;
+    int64_t size = 0;
+    std::vector<int64_t> queue;
+    size_t head = 0;
+    while (size < target) {
+      if (head == queue.size()) {  // frontier empty: seed with the lowest unassigned entity
+        while (part[(size_t)next_seed] >= 0) ++next_seed;
+        part[(size_t)next_seed] = w;
+        ++size;
+        queue.push_back(next_seed);
+        continue;
+      }
+      const int64_t v = queue[head++];
+      for (int64_t u : adj[(size_t)v]) {
+        if (size >= target) break;
+        if (part[(size_t)u] < 0) {
+          part[(size_t)u] = w;
+          ++size;
+          queue.push_back(u);
+        }
+      }
+    }
+  }
+  new_id.assign((size_t)ne, -1);
+  std::vector<int64_t> cnt((size_t)P, 0);
+  for (int64_t e = 0; e < ne; ++e) {
+    const int32_t w = part[(size_t)e];
+    new_id[(size_t)e] = (int64_t)P * cnt[(size_t)w]++ + w;
+  }
+  int64_t cut = 0;
+  for (int64_t i = 0; i < nt; ++i) cut += part[(size_t)heads[i]] != part[(size_t)tails[i]];
+  return cut;
+}
+
 void rank_lists(const int64_t* rels, int64_t nt, int64_t nr, int32_t P, std::vector<std::vector<int64_t>>& lists,
                 bool randomise = false, uint64_t seed = 0, uint32_t epoch = 0) {
   lists.assign((size_t)P, {});
@@ -979,6 +1044,15 @@ int32_t orc_relation_partition(const int64_t* rels, int64_t n_triples, int64_t n
   for (int64_t r = 0; r < n_rel; ++r) owner_out[r] = owner[(size_t)r];
   return ns;
 }
+int64_t orc_locality_order(const int64_t* heads, const int64_t* tails, int64_t n_triples, int64_t n_entities, int32_t P,
+                           int64_t* new_id_out, int32_t* part_out) {
+  std::vector<int64_t> nid;
+  std::vector<int32_t> part;
+  const int64_t cut = locality_order(heads, tails, n_triples, n_entities, P, nid, part);
+  std::copy(nid.begin(), nid.end(), new_id_out);
+  if (part_out) std::copy(part.begin(), part.end(), part_out);
+  return cut;
+}
 int32_t orc_relation_partition_epoch(const int64_t* rels, int64_t n_triples, int64_t n_rel, int32_t P, uint64_t seed,
                                      uint32_t epoch, int32_t* owner_out) {
   std::vector<int32_t> owner;
@@ -1093,7 +1167,17 @@ void* orc_create(const orc_config* cfg, const int64_t* heads, const int64_t* rel
       b->triple(i, h, r, t);
       rr[(size_t)i] = r;
     }
-    rank_lists(rr.data(), n_triples, cfg->n_relations, cfg->world_size, b->lists);
+    if (cfg->placement == 1) {  // c.13'' head-owner placement
+      std::vector<int64_t> hh((size_t)n_triples);
+      for (int64_t i = 0; i < n_triples; ++i) {
+        int64_t h, r, t;
+        b->triple(i, h, r, t);
+        hh[(size_t)i] = h;
+      }
+      head_owner_lists(hh, cfg->world_size, b->lists);
+    } else {
+      rank_lists(rr.data(), n_triples, cfg->n_relations, cfg->world_size, b->lists);
+    }
     for (const auto& l : b->lists)
       if (l.empty()) {
         delete b;

@@ -55,6 +55,7 @@ typedef struct {
   int32_t loss;             /* ORC_LOSS_LOGISTIC (c.9) or ORC_LOSS_PAIRWISE (c.9') */
   int32_t repartition;      /* 1 with world_size > 1: a randomised relation partition per epoch of ceil(N_t/(P B))
                                steps (reading c.13') */
+  int32_t placement;        /* 0: relation partition (c.13); 1: head-owner placement (c.13'') */
 } orc_config;
 enum { ORC_LOSS_LOGISTIC = 0, ORC_LOSS_PAIRWISE = 1 };
 
@@ -73,6 +74,10 @@ int32_t orc_relation_partition(const int64_t* rels, int64_t n_triples, int64_t n
                                int32_t* owner_out);
 /* triple indices of `rank` (ascending). Returns count; idx_out may be NULL (count only). */
 /* c.13' the randomised partition of epoch `epoch` */
+/* c.13'' BFS-grown balanced partition of the entity graph and the renumbering that puts part w on rank w's shard
+ * (new_id_out [n_entities], part_out [n_entities] or NULL); returns the edge cut */
+int64_t orc_locality_order(const int64_t* heads, const int64_t* tails, int64_t n_triples, int64_t n_entities, int32_t P,
+                           int64_t* new_id_out, int32_t* part_out);
 int32_t orc_relation_partition_epoch(const int64_t* rels, int64_t n_triples, int64_t n_rel, int32_t P, uint64_t seed,
                                      uint32_t epoch, int32_t* owner_out);
 int64_t orc_rank_triples(const int64_t* rels, int64_t n_triples, int64_t n_rel, int32_t P, int32_t rank,
