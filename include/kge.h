@@ -127,6 +127,11 @@ typedef struct {
                               set is unchanged). At an epoch boundary kge_train_step re-partitions (host) and every rank
                               pulls the relations it did not own from their previous owner. Default 0; sampled steps
                               only (kge_train_batch with repartition: KGE_EUNSUPPORTED) */
+  int32_t placement;       /* world_size > 1: 0 = relation partition (reading c.13); 1 = head-owner
+                              placement (PAPER.md:395-406 [3.2], reading c.13''): triple i trains on the rank owning its
+                              head (h mod P), so every head row is local; all relations are then replicated and their
+                              gradients exchanged (the SPLIT path). With kge_locality_order's renumbering and
+                              neg_local = 1 most rows of a step are local. Default 0; not with repartition */
 } kge_config;
 
 /* Fill *cfg with defaults (ABI version, TransE-L2, d=400, B=1024, g=256, k=256, gamma=12, lr=0.1, eps=1e-10,
@@ -242,6 +247,16 @@ int kge_read_losses(kge_handle* h, int64_t first_step, int64_t n, float* out);
  * order, to kge_connect. kge_train_step is then collective: gather reads rows from their owners over NVLink, owners pull
  * the per-rank gradient sums of their rows and apply one Adagrad step per row (the union-batch semantics of c.13).
  * For table 0 / 3, kge_get_rows / kge_set_rows take global ids owned by this rank. */
+/* METIS-style locality ordering (PAPER.md:395-406 [3.2] deploys METIS; reading c.13'', SPEC's BFS-grown balanced
+ * partitioner): part w of the entity graph (the undirected edges (h_i, t_i)) takes exactly ceil((N_e - w) / P)
+ * entities -- from the lowest-id unassigned entity, breadth-first with neighbours in ascending id, an entity joining
+ * when discovered, a new seed when the frontier empties -- and new_id[e] = P j + w (j = e's position in part w by
+ * ascending old id) puts part w on rank w's shard (owner = id mod P). The caller renumbers its triples (and evaluation
+ * data) with new_id before kge_init; with placement = 1 a triple's head and tail then share a rank unless the edge is
+ * cut. new_id_out: host int64[n_entities]; edge_cut_out: triples whose endpoints fall in different parts (or NULL).
+ * Host only; KGE_EINVAL / KGE_ERANGE for bad sizes or ids. */
+int kge_locality_order(const int64_t* heads, const int64_t* tails, int64_t n_triples, int64_t n_entities,
+                       int32_t world_size, int64_t* new_id_out, int64_t* edge_cut_out);
 int kge_partition(const int64_t* rels, int64_t n_triples, int64_t n_relations, int32_t world_size, int32_t rank,
                   int32_t* owner_out /* [n_relations] rank or -1 = split, or NULL */,
                   int64_t* list_out /* this rank's triple indices (ascending), or NULL */, int64_t* n_list);

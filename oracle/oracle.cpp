@@ -877,13 +877,27 @@ struct Trainer : Base {
     std::vector<int64_t> uniq((size_t)n), seg_off((size_t)n + 1), seg_occ((size_t)n);
     std::vector<int32_t> inv((size_t)n);
     int64_t nu = dedup(ids.data(), n, uniq.data(), inv.data(), seg_off.data(), seg_occ.data());
-    std::vector<T> gsum((size_t)w);
+    // c.13: with P ranks the occurrences are rank-major; each rank's occurrences of a row are summed first (in
+    // occurrence order) and the rank sums are added in rank order -- "entity gradients meet at the owner and are
+    // summed", "split relations ... all-gathered and summed in rank order". P = 1: one plain sum.
+    const int64_t per = n / cfg.world_size;
+    std::vector<T> gsum((size_t)w), gpart((size_t)w);
     for (int64_t u = 0; u < nu; ++u) {
       std::fill(gsum.begin(), gsum.end(), T(0));
+      std::fill(gpart.begin(), gpart.end(), T(0));
+      int64_t cur = -1;
       for (int64_t p = seg_off[(size_t)u]; p < seg_off[(size_t)u + 1]; ++p) {
-        const T* go = &G[(size_t)seg_occ[(size_t)p] * w];
-        for (int32_t c = 0; c < w; ++c) gsum[(size_t)c] += go[c];
+        const int64_t o = seg_occ[(size_t)p];
+        if (o / per != cur) {
+          if (cur >= 0)
+            for (int32_t c = 0; c < w; ++c) gsum[(size_t)c] += gpart[(size_t)c];
+          std::fill(gpart.begin(), gpart.end(), T(0));
+          cur = o / per;
+        }
+        const T* go = &G[(size_t)o * w];
+        for (int32_t c = 0; c < w; ++c) gpart[(size_t)c] += go[c];
       }
+      for (int32_t c = 0; c < w; ++c) gsum[(size_t)c] += gpart[(size_t)c];
       T* row = tab.row(uniq[(size_t)u]);
       T* s = st.row(uniq[(size_t)u]);
       T sq = 0;

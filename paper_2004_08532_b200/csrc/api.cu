@@ -130,6 +130,8 @@ static int validate(const kge_config* c) {
   if (c->neg_local != 0 && c->neg_local != 1) { set_error("neg_local must be 0 or 1"); return KGE_EINVAL; }
   if (c->loss != KGE_LOSS_LOGISTIC && c->loss != KGE_LOSS_PAIRWISE) { set_error("bad loss"); return KGE_EINVAL; }
   if (c->repartition != 0 && c->repartition != 1) { set_error("repartition must be 0 or 1"); return KGE_EINVAL; }
+  if (c->placement != 0 && c->placement != 1) { set_error("placement must be 0 or 1"); return KGE_EINVAL; }
+  if (c->placement == 1 && c->repartition) { set_error("placement = 1 replaces the relation partition (repartition = 0)"); return KGE_EINVAL; }
   if (c->neg_local && c->world_size > 1 && c->n_entities < c->world_size) {
     set_error("neg_local needs n_entities >= world_size (every shard non-empty)");
     return KGE_EINVAL;
@@ -250,6 +252,7 @@ void kge_config_default(kge_config* c) {
   c->neg_local = 0;
   c->loss = KGE_LOSS_LOGISTIC;
   c->repartition = 0;
+  c->placement = 0;
   c->world_size = 1;
   c->rank = 0;
 }
@@ -379,8 +382,14 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (h->P > 1) {  // relation partition (reading c.13) -> this rank's triple list
     std::vector<int32_t> owner, lst;
     const bool rp = cfg->repartition != 0;
-    relation_partition(rels, n_triples, cfg->n_relations, h->P, owner, rp, cfg->seed, 0);
-    rank_list(rels, n_triples, cfg->n_relations, h->P, h->rank, owner, &lst);
+    if (cfg->placement == 1) {  // head-owner placement (reading c.13''): every relation replicated (SPLIT)
+      owner.assign((size_t)cfg->n_relations, -1);
+      for (int64_t i = 0; i < n_triples; ++i)
+        if (heads[i] % h->P == h->rank) lst.push_back((int32_t)i);
+    } else {
+      relation_partition(rels, n_triples, cfg->n_relations, h->P, owner, rp, cfg->seed, 0);
+      rank_list(rels, n_triples, cfg->n_relations, h->P, h->rank, owner, &lst);
+    }
     if (lst.empty()) { set_error("this rank received no triples"); return fail(KGE_EINVAL); }
     // repartition: room for any epoch's list, the relation column kept on the host for the per-epoch partitions
     h->list = (int32_t*)dalloc(h, (rp ? (size_t)n_triples : lst.size()) * 4);

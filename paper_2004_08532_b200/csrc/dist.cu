@@ -509,6 +509,78 @@ int kge_partition(const int64_t* rels, int64_t n_triples, int64_t n_relations, i
   return KGE_OK;
 }
 
+int kge_locality_order(const int64_t* heads, const int64_t* tails, int64_t n_triples, int64_t n_entities,
+                       int32_t world_size, int64_t* new_id_out, int64_t* edge_cut_out) {
+  if (!heads || !tails || !new_id_out || n_triples < 0 || n_entities <= 0 || world_size < 1 ||
+      world_size > n_entities) {
+    set_error("bad locality-order arguments");
+    return KGE_EINVAL;
+  }
+  // CSR of the undirected entity graph, neighbours ascending and distinct (self-loops dropped)
+  std::vector<int64_t> deg((size_t)n_entities + 1, 0);
+  for (int64_t i = 0; i < n_triples; ++i) {
+    if (heads[i] < 0 || heads[i] >= n_entities || tails[i] < 0 || tails[i] >= n_entities) {
+      set_error("entity id out of range");
+      return KGE_ERANGE;
+    }
+    if (heads[i] != tails[i]) {
+      ++deg[(size_t)heads[i] + 1];
+      ++deg[(size_t)tails[i] + 1];
+    }
+  }
+  for (int64_t e = 0; e < n_entities; ++e) deg[(size_t)e + 1] += deg[(size_t)e];
+  std::vector<int64_t> nb((size_t)deg[(size_t)n_entities]), fill(deg.begin(), deg.end() - 1);
+  for (int64_t i = 0; i < n_triples; ++i)
+    if (heads[i] != tails[i]) {
+      nb[(size_t)fill[(size_t)heads[i]]++] = tails[i];
+      nb[(size_t)fill[(size_t)tails[i]]++] = heads[i];
+    }
+  std::vector<int64_t> start((size_t)n_entities), stop((size_t)n_entities);
+  for (int64_t e = 0; e < n_entities; ++e) {
+    auto b = nb.begin() + deg[(size_t)e], en = nb.begin() + deg[(size_t)e + 1];
+    std::sort(b, en);
+    start[(size_t)e] = deg[(size_t)e];
+    stop[(size_t)e] = deg[(size_t)e] + (std::unique(b, en) - b);
+  }
+  // grow part w to exactly its shard size ceil((N_e - w) / P) breadth-first
+  const int32_t P = world_size;
+  std::vector<int32_t> part((size_t)n_entities, -1);
+  std::vector<int64_t> frontier;
+  int64_t seed = 0;
+  for (int32_t w = 0; w < P; ++w) {
+    const int64_t want = (n_entities - w + P - 1) / P;
+    int64_t got = 0;
+    frontier.clear();
+    size_t at = 0;
+    while (got < want) {
+      if (at == frontier.size()) {
+        while (part[(size_t)seed] >= 0) ++seed;
+        part[(size_t)seed] = w;
+        ++got;
+        frontier.push_back(seed);
+        continue;
+      }
+      const int64_t v = frontier[at++];
+      for (int64_t q = start[(size_t)v]; q < stop[(size_t)v] && got < want; ++q) {
+        const int64_t u = nb[(size_t)q];
+        if (part[(size_t)u] < 0) {
+          part[(size_t)u] = w;
+          ++got;
+          frontier.push_back(u);
+        }
+      }
+    }
+  }
+  std::vector<int64_t> next((size_t)P, 0);
+  for (int64_t e = 0; e < n_entities; ++e) new_id_out[e] = (int64_t)P * next[(size_t)part[(size_t)e]]++ + part[(size_t)e];
+  if (edge_cut_out) {
+    int64_t cut = 0;
+    for (int64_t i = 0; i < n_triples; ++i) cut += part[(size_t)heads[i]] != part[(size_t)tails[i]];
+    *edge_cut_out = cut;
+  }
+  return KGE_OK;
+}
+
 int kge_export(kge_handle* h, void* blob, size_t* blob_bytes) {
   if (!h || !blob_bytes) { set_error("NULL argument"); return KGE_EINVAL; }
   if (h->P < 2) { set_error("kge_export needs world_size > 1"); return KGE_ESTATE; }

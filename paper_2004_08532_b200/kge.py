@@ -52,7 +52,7 @@ class _Config(ctypes.Structure):
                 ("nccl_comm", ctypes.c_void_p), ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p),
                 ("dev_alloc", ALLOC_FN), ("dev_free", FREE_FN), ("alloc_ctx", ctypes.c_void_p),
                 ("neg_deg_k", ctypes.c_int32), ("neg_local", ctypes.c_int32), ("loss", ctypes.c_int32),
-                ("repartition", ctypes.c_int32)]
+                ("repartition", ctypes.c_int32), ("placement", ctypes.c_int32)]
 
 
 _lib = None
@@ -85,6 +85,7 @@ def lib():
         L.kge_rank_sampled.argtypes = [ctypes.c_void_p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int32,
                                        ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, _i64p]
         L.kge_link_metrics.argtypes = [_i64p, ctypes.c_int64, P(ctypes.c_double)]
+        L.kge_locality_order.argtypes = [_i64p, _i64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, _i64p, _i64p]
         L.kge_get_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_set_rows.argtypes = [ctypes.c_void_p, ctypes.c_int32, _i64p, ctypes.c_int64, _fp]
         L.kge_table_width.argtypes = [ctypes.c_void_p, ctypes.c_int32]
@@ -156,6 +157,7 @@ class Config:
     neg_local: int = 0  # 1: local-shard negatives when world_size > 1
     loss: str = "logistic"  # or "pairwise"
     repartition: int = 0  # 1: a randomised relation partition every epoch when world_size > 1
+    placement: int = 0  # 1: head-owner triple placement when world_size > 1
     rank: int = 0
 
     @property
@@ -411,6 +413,7 @@ def init(cfg: Config, heads, rels, tails, use_torch_allocator=True, stream=None)
     c.neg_local = cfg.neg_local
     c.loss = LOSS[cfg.loss] if isinstance(cfg.loss, str) else cfg.loss
     c.repartition = cfg.repartition
+    c.placement = cfg.placement
     dev = torch.cuda.current_device()
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     c.cuda_stream = s.cuda_stream
@@ -424,6 +427,16 @@ def init(cfg: Config, heads, rels, tails, use_torch_allocator=True, stream=None)
     _check(lib().kge_init(ctypes.byref(out), ctypes.byref(c), _ptr(h, ctypes.c_int64), _ptr(r, ctypes.c_int64),
                           _ptr(t, ctypes.c_int64), len(h)))
     return Handle(out.value, cfg, keep)
+
+
+def locality_order(heads, tails, n_entities, world_size):
+    """kge_locality_order: the entity renumbering (new_id[e]) of the BFS-grown balanced parts and the edge cut."""
+    h, t = _i64(heads), _i64(tails)
+    nid = np.zeros(n_entities, np.int64)
+    cut = np.zeros(1, np.int64)
+    _check(lib().kge_locality_order(_ptr(h, ctypes.c_int64), _ptr(t, ctypes.c_int64), len(h), n_entities, world_size,
+                                    _ptr(nid, ctypes.c_int64), _ptr(cut, ctypes.c_int64)))
+    return nid, int(cut[0])
 
 
 def partition(rels, n_relations, world_size, rank):

@@ -175,3 +175,37 @@ def test_dist_epoch_repartition(model, P):
     e_now = (steps - 1) // SE
     o_now, _ = O.relation_partition(gr.triples()[1], gr.n_relations, P, seed=1, epoch=e_now)
     assert owners == o_now.tolist()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("model", ["transe_l2", "distmult"])
+def test_dist_head_owner_placement_locality(model, P):
+    # reading c.13'': the graph renumbered by kge_locality_order, head-owner placement and local
+    # negatives: every head row and every uniform negative is local; parity with the oracle's P-rank union step
+    gr = synth.graph("tiny")
+    h0, r0, t0 = gr.triples()
+    nid, cut = kge.locality_order(h0, t0, gr.n_entities, P)
+    trip = (nid[h0], r0, nid[t0])
+    B, g, k, d = 128, 32, 32, 32
+    cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=d, batch_size=B,
+                     chunk_size=g, neg_k=k, placement=1, neg_local=1, neg_precision="fp32")
+    hs = kge.init_local_group(cfg, P, *trip)
+    orc = O.Trainer(model, gr.n_entities, gr.n_relations, d, B, g, k, world_size=P, triples=trip, placement=1,
+                    neg_local=1)
+    for w in range(P):
+        s = hs[w].sample(2)
+        assert np.array_equal(s["pos"], orc.sample(2, w)[0]) and np.all(trip[0][s["pos"]] % P == w)
+        assert np.all(s["neg"] % P == w)
+    steps = 20
+    for _ in range(steps):
+        for h in hs:
+            h.train_step(1, return_loss=False)
+    lg = sum(h.read_losses(0, steps).astype(np.float64) for h in hs)
+    lo = orc.train(steps)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 1e-5
+    ids, rids = np.arange(gr.n_entities), np.arange(gr.n_relations)
+    got = np.stack([hs[e % P].get_rows(0, [e])[0] for e in ids])
+    assert np.abs(got - orc.get_rows(0, ids)).max() <= 1e-4
+    rel = hs[0].get_rows(1, rids)  # every relation replicated: all replicas agree with the union step
+    assert np.abs(rel - orc.get_rows(1, rids)).max() <= 1e-4
+    assert all(np.array_equal(rel, h.get_rows(1, rids)) for h in hs[1:])

@@ -60,3 +60,15 @@ def test_head_owner_placement():
     n0 = int(np.sum(trip[0] % 4 == 0))
     seen = np.concatenate([tr.sample(s, 0)[0] for s in range(n0 // 32)])
     assert len(np.unique(seen)) == len(seen)
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_library_locality_order_equals_oracle(P):
+    # the library's host partitioner (kge_locality_order, independent code) gives the oracle's renumbering bit-exactly
+    from paper_2004_08532_b200 import kge
+    import synth
+    gr = synth.graph("tiny")
+    h, r, t = gr.triples()
+    nid_o, part, cut_o = O.locality_order(h, t, gr.n_entities, P)
+    nid_l, cut_l = kge.locality_order(h, t, gr.n_entities, P)
+    assert np.array_equal(nid_o, nid_l) and cut_o == cut_l
