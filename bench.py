@@ -293,7 +293,7 @@ def main():
         wall = time.perf_counter() - w0
     ms_dev = e0.elapsed_time(e1)
     gpu_launches = H.launch_count - launches0
-    loss_end = H.read_losses(H.step - 64, 64)
+    loss_end = H.read_losses(H.step - min(64, H.step), min(64, H.step))
     spot = spot_check(H, gr, wl, args) if (rank == 0 and ws == 1 and not args.no_cpu_baseline) else None
     ms = max(ms_dev, 0.0)
     if pg:

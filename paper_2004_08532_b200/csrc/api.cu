@@ -449,14 +449,15 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     if (e != cudaSuccess) return fail(cuda_fail(e, "projection init"));
     TrBuffers& T = h->tr_buf;
     const size_t B = dm.B;
-    int32_t* ib = (int32_t*)dalloc(h, (1 + 4 * B + (B + 1) + (dm.C + 1) + B) * 4);
+    int32_t* ib = (int32_t*)dalloc(h, (1 + 4 * B + (B + 1) + (dm.C + 1) + B + (B + 1)) * 4);
     const bool tr = cfg->model == KGE_TRANSR;  // RESCAL needs only dM and the U / V (H) factor rows
     T.QX = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 : 4);
     T.dQ = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 : 4);
     T.dM = (float*)dalloc(h, B * dm.d * dm.d * 4);
     T.Pv = (float*)dalloc(h, B * dm.d * 4);
-    T.U = (float*)dalloc(h, 2 * B * dm.d * 4);
-    T.H = (float*)dalloc(h, 2 * B * dm.d * 4);
+    const size_t urows = tr ? 2 * B + 32 * B : B;  // TransR: padded per-relation blocks (k_tr_dm_tc); RESCAL: B rows
+    T.U = (float*)dalloc(h, urows * dm.d * 4);
+    T.H = (float*)dalloc(h, urows * dm.d * 4);
     if (!ib || !T.QX || !T.dQ || !T.dM || !T.Pv || !T.U || !T.H) { set_error("out of device memory (TransR)"); return fail(KGE_ENOMEM); }
     T.n_groups = ib; ib += 1;
     T.grp_u = ib; ib += B;
@@ -466,6 +467,10 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     T.rg_off = ib; ib += B + 1;
     T.cg_off = ib; ib += dm.C + 1;
     T.cg_list = ib; ib += B;
+    T.pad_off = ib; ib += B + 1;
+    if (cudaMemsetAsync(T.U, 0, urows * dm.d * 4, h->stream) != cudaSuccess ||
+        cudaMemsetAsync(T.H, 0, urows * dm.d * 4, h->stream) != cudaSuccess)
+      return fail(cuda_fail(cudaGetLastError(), "TransR scratch"));
     if (!(tr ? transr_init(h) : rescal_init(h))) { set_error("TransR / RESCAL kernel setup failed"); return fail(KGE_ECUDA); }
   }
 

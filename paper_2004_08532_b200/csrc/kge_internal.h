@@ -138,8 +138,9 @@ struct TrBuffers {
   float* dQ;          // [B x k x d]
   float* dM;          // [B x d x d] per unique relation
   float* Pv;          // [B x d]  p = Mh + r - Mt
-  float* U;           // [2B x d] gMh, gMt rows (relation-sorted)
-  float* H;           // [2B x d] h, t rows (relation-sorted)
+  float* U;           // [(2B + 32 B) x d] gMh, gMt rows (relation-sorted; relation u's 2 n_u rows start at pad_off[u],
+  float* H;           // padded to whole 32-row k-blocks with zero rows) / h, t rows, the same layout
+  int32_t* pad_off;   // [B + 1] first U / H row of each unique relation (multiples of 32)
 };
 
 // multi-rank state (dist.cu)

@@ -116,6 +116,20 @@ __global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
     base += tot;
   }
   if (tid == 0) T.cg_off[dm.C] = base;
+  // per unique relation: its first row in the padded U / H layout (2 n_u rows rounded up to 32), a contiguous run of
+  // relations per thread
+  __syncthreads();
+  const int per_u = (n_rel + blockDim.x - 1) / blockDim.x;
+  const int u0 = min(n_rel, tid * per_u), u1 = min(n_rel, u0 + per_u);
+  auto padded = [&](int u) { return (2 * (a.s.rel_off[u + 1] - a.s.rel_off[u]) + 31) / 32 * 32; };
+  int tot_u = 0;
+  for (int u = u0; u < u1; ++u) tot_u += padded(u);
+  int po = scan(tot_u);
+  for (int u = u0; u < u1; ++u) {
+    T.pad_off[u] = po;
+    po += padded(u);
+  }
+  if (tid == 0) T.pad_off[n_rel] = s_total;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -260,8 +274,8 @@ __global__ void __launch_bounds__(256) k_tr_gemm(TrArgs a) {
       const int c = T.grp_c[g];
       run_term(T.dQ + (int64_t)g * k * d, d, true, a.b.X + (int64_t)c * k * dm.dp, dm.dp, false, k);
     }
-    const int q0 = 2 * a.s.rel_off[u], q1 = 2 * a.s.rel_off[u + 1];
-    run_term(T.U + (int64_t)q0 * d, d, true, T.H + (int64_t)q0 * d, d, false, q1 - q0);
+    const int q0 = T.pad_off[u], nq = 2 * (a.s.rel_off[u + 1] - a.s.rel_off[u]);
+    run_term(T.U + (int64_t)q0 * d, d, true, T.H + (int64_t)q0 * d, d, false, nq);
     out = T.dM + (int64_t)u * d * d;
   }
 #pragma unroll
@@ -289,9 +303,10 @@ struct TrTc {
   CUtensorMap mdQ;  // dQ [B groups][k rows][d cols], box {32, 128}
   CUtensorMap mdQn;  // dQ, box {32, 32}, SWIZZLE_128B_ATOM_32B (A = dQ_g^T of dM, MN-major)
   CUtensorMap mXn;   // X' [C*k rows x d cols], box {32, 32}, SWIZZLE_128B_ATOM_32B (B of dM, MN-major)
+  CUtensorMap mUn, mHn;  // padded U / H rows, box {32, 32}, SWIZZLE_128B_ATOM_32B (the U^T H term of dM)
   int N = 0;        // d rounded up to 16
 };
-constexpr int kTrStages = 4;
+constexpr int kTrStages = 2;  // two stages and one 256-column accumulator: two CTAs per SM (smem ~91 KB, TMEM 2 x 256)
 
 __device__ __forceinline__ uint64_t sdesc_mn32(uint32_t saddr, uint32_t lbo) {
   // tf32 MN-major: SWIZZLE_128B_BASE32B (layout type 1), SBO = 512 B between 4-row K atoms (see tc.cu)
@@ -321,12 +336,12 @@ __global__ void __launch_bounds__(128, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTrStages; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 2);
+      tc::mbar_init(&empty[s], N > 128 ? 2 : 1);
     }
-    tc::mbar_init(&done, 2);
+    tc::mbar_init(&done, N > 128 ? 2 : 1);
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc(&tbase, 512);
+  if (warp == 0) tc::tmem_alloc(&tbase, 256);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -347,20 +362,24 @@ __global__ void __launch_bounds__(128, 1)
           tc::tma_load_3d(sa + A_BYTES + nb * 4096, &mB, &full[s], nb * 32, kb * 32, r);
       }
     }
-  } else if (warp >= 2 && lane == 0) {  // MMA issuers q = 0, 1: slices 2q, 2q + 1 of each k-block
-    const int q = warp - 2;
-    const uint32_t idesc = tc::idesc_tf32(128, N, false, MODE == 1);
-    const uint32_t acc = tmem + (uint32_t)(q * 256);
+  } else if ((warp == 2 || warp == 3) && lane == 0 && (warp == 2 || N > 128)) {
+    // MMA issuers split N: issuer 0 columns [0, 128), issuer 1 [128, N) -- two issue streams in parallel, one
+    // complete accumulator per column, 256 TMEM columns in all (two CTAs per SM)
+    const int qi = warp - 2;
+    const int n0 = qi * 128, nn = qi ? N - 128 : (N < 128 ? N : 128);
+    const uint32_t idesc = tc::idesc_tf32(128, nn, false, MODE == 1);
+    const uint32_t acc = tmem + (uint32_t)n0;
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % kTrStages;
       tc::mbar_wait(&full[s], (kb / kTrStages) & 1);
       tc::tc_fence_after();
       const uint32_t sa = tc::smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int sl = 2 * q + h2;
-        const uint64_t bd = MODE == 0 ? tc::sdesc(sb + sl * 32, 16, 1024) : sdesc_mn32(sb + sl * 1024, 4096);
-        tc::mma_tf32(acc, tc::sdesc(sa + sl * 32, 16, 1024), bd, idesc, (kb | h2) ? 1u : 0u);
+      for (int sl = 0; sl < 4; ++sl) {
+        // N offset: K-major B = 128 rows of 128 B further; MN-major B = 4 blocks of 32 columns further
+        const uint64_t bd = MODE == 0 ? tc::sdesc(sb + n0 * 128 + sl * 32, 16, 1024)
+                                      : sdesc_mn32(sb + (n0 / 32) * 4096 + sl * 1024, 4096);
+        tc::mma_tf32(acc, tc::sdesc(sa + sl * 32, 16, 1024), bd, idesc, (kb | sl) ? 1u : 0u);
       }
       tc::mma_commit(&empty[s]);
     }
@@ -374,9 +393,8 @@ __global__ void __launch_bounds__(128, 1)
   float* out = T.QX + (int64_t)grp * k * d + (int64_t)row * d;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   for (int cb = 0; cb * 32 < d; ++cb) {
-    uint32_t p0[32], p1[32];
+    uint32_t p0[32];
     tc::tmem_ld32_nw(trow + cb * 32, p0);
-    tc::tmem_ld32_nw(trow + 256 + cb * 32, p1);
     tc::tmem_wait_ld();
     if (row < k) {
 #pragma unroll
@@ -384,23 +402,22 @@ __global__ void __launch_bounds__(128, 1)
         const int col = cb * 32 + 4 * v;
         if (col < d)
           *reinterpret_cast<float4*>(out + col) =
-              make_float4(__uint_as_float(p0[4 * v]) + __uint_as_float(p1[4 * v]),
-                          __uint_as_float(p0[4 * v + 1]) + __uint_as_float(p1[4 * v + 1]),
-                          __uint_as_float(p0[4 * v + 2]) + __uint_as_float(p1[4 * v + 2]),
-                          __uint_as_float(p0[4 * v + 3]) + __uint_as_float(p1[4 * v + 3]));
+              make_float4(__uint_as_float(p0[4 * v]), __uint_as_float(p0[4 * v + 1]), __uint_as_float(p0[4 * v + 2]),
+                          __uint_as_float(p0[4 * v + 3]));
       }
     }
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
 }
 
 // dM_u = sum over the relation's groups g (in group order) of dQ_g^T X'_c  on tcgen05 (A = dQ_g^T and B = X'_c both
 // MN-major, accumulated in TMEM), then + sum_q U_q^T H_q over its positives (K = 2 n_u, a few rows) in FFMA in the
 // epilogue. CTA = 128 rows a of dM_u x N columns b; blockIdx.y = unique relation.
 __global__ void __launch_bounds__(128, 1)
-    k_tr_dm_tc(const __grid_constant__ CUtensorMap mdQn, const __grid_constant__ CUtensorMap mXn, TrArgs a, int N) {
+    k_tr_dm_tc(const __grid_constant__ CUtensorMap mdQn, const __grid_constant__ CUtensorMap mXn,
+               const __grid_constant__ CUtensorMap mUn, const __grid_constant__ CUtensorMap mHn, TrArgs a, int N) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kTrStages], empty[kTrStages], done;
@@ -413,17 +430,19 @@ __global__ void __launch_bounds__(128, 1)
   const int d = dm.d, k = dm.k, m0 = blockIdx.x * 128;
   const int g0 = T.rg_off[u], g1 = T.rg_off[u + 1];
   const int nkg = (k + 31) / 32, nnb = (N + 31) / 32;
-  const int nk = (g1 - g0) * nkg;  // k-blocks over all groups of the relation
+  const int nkq = (g1 - g0) * nkg;  // k-blocks over all groups of the relation, then over its padded U / H rows
+  const int uq0 = T.pad_off[u], nku = (T.pad_off[u + 1] - uq0) / 32;
+  const int nk = nkq + nku;
   const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)nnb * 4096;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTrStages; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 2);
+      tc::mbar_init(&empty[s], N > 128 ? 2 : 1);
     }
-    tc::mbar_init(&done, 2);
+    tc::mbar_init(&done, N > 128 ? 2 : 1);
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc(&tbase, 512);
+  if (warp == 0) tc::tmem_alloc(&tbase, 256);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -432,29 +451,34 @@ __global__ void __launch_bounds__(128, 1)
     for (int q = 0; q < nk; ++q) {
       const int s = q % kTrStages;
       if (q >= kTrStages) tc::mbar_wait(&empty[s], ((q / kTrStages) - 1) & 1);
-      const int g = g0 + q / nkg, kb = q % nkg, c = T.grp_c[g];
       uint8_t* sa = smem + s * STAGE;
       tc::mbar_arrive_expect_tx(&full[s], STAGE);
-      for (int b = 0; b < 4; ++b)  // A = dQ_g^T: [4 M-blocks of 32 a][32 K rows j][128 B]
-        tc::tma_load_3d(sa + b * 4096, &mdQn, &full[s], m0 + b * 32, kb * 32, g);
-      for (int nb = 0; nb < nnb; ++nb)  // B = X'_c: [N-blocks of 32 b][32 K rows j][128 B]
-        tc::tma_load_3d(sa + A_BYTES + nb * 4096, &mXn, &full[s], nb * 32, c * k + kb * 32, 0);
+      if (q < nkq) {
+        const int g = g0 + q / nkg, kb = q % nkg, c = T.grp_c[g];
+        for (int b = 0; b < 4; ++b)  // A = dQ_g^T: [4 M-blocks of 32 a][32 K rows j][128 B]
+          tc::tma_load_3d(sa + b * 4096, &mdQn, &full[s], m0 + b * 32, kb * 32, g);
+        for (int nb = 0; nb < nnb; ++nb)  // B = X'_c: [N-blocks of 32 b][32 K rows j][128 B]
+          tc::tma_load_3d(sa + A_BYTES + nb * 4096, &mXn, &full[s], nb * 32, c * k + kb * 32, 0);
+      } else {  // + U^T H over the relation's positions: A = U^T (MN-major), B = H (MN-major), K = 32 rows
+        const int row = uq0 + (q - nkq) * 32;
+        for (int b = 0; b < 4; ++b) tc::tma_load_3d(sa + b * 4096, &mUn, &full[s], m0 + b * 32, row, 0);
+        for (int nb = 0; nb < nnb; ++nb) tc::tma_load_3d(sa + A_BYTES + nb * 4096, &mHn, &full[s], nb * 32, row, 0);
+      }
     }
-  } else if (warp >= 2 && lane == 0) {  // MMA issuers q = 0, 1: slices 2q, 2q + 1 of each k-block
+  } else if ((warp == 2 || warp == 3) && lane == 0 && (warp == 2 || N > 128)) {  // issuers split N (see k_tr_tc)
     const int qi = warp - 2;
-    const uint32_t idesc = tc::idesc_tf32(128, N, true, true);
-    const uint32_t acc = tmem + (uint32_t)(qi * 256);
+    const int n0 = qi * 128, nn = qi ? N - 128 : (N < 128 ? N : 128);
+    const uint32_t idesc = tc::idesc_tf32(128, nn, true, true);
+    const uint32_t acc = tmem + (uint32_t)n0;
     for (int q = 0; q < nk; ++q) {
       const int s = q % kTrStages;
       tc::mbar_wait(&full[s], (q / kTrStages) & 1);
       tc::tc_fence_after();
       const uint32_t sa = tc::smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int sl = 2 * qi + h2;
-        tc::mma_tf32(acc, sdesc_mn32(sa + sl * 1024, 4096), sdesc_mn32(sb + sl * 1024, 4096), idesc,
-                     (q | h2) ? 1u : 0u);
-      }
+      for (int sl = 0; sl < 4; ++sl)
+        tc::mma_tf32(acc, sdesc_mn32(sa + sl * 1024, 4096), sdesc_mn32(sb + (n0 / 32) * 4096 + sl * 1024, 4096),
+                     idesc, (q | sl) ? 1u : 0u);
       tc::mma_commit(&empty[s]);
     }
     tc::mma_commit(&done);
@@ -464,40 +488,21 @@ __global__ void __launch_bounds__(128, 1)
     tc::mbar_wait(&done, 0);
     tc::tc_fence_after();
   }
-  // epilogue: row a = m0 + 32 warp + lane: TMEM p0 + p1, + sum_q U[q][a] H[q][b] over the relation's positives in q
-  // order. The H rows are staged 32 at a time in (free) pipeline shared memory by the whole CTA: a hub relation
-  // carries ~260 rows and per-thread global loads serialised it.
+  // epilogue: row a = m0 + 32 warp + lane of dM_u straight from TMEM (the U^T H term was accumulated by the MMAs)
   const int row = m0 + warp * 32 + lane;
-  const int q0 = 2 * a.s.rel_off[u], q1 = 2 * a.s.rel_off[u + 1];
   float* out = T.dM + (int64_t)u * d * d + (int64_t)row * d;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  float* hs = reinterpret_cast<float*>(smem);  // [32 q][33]
   for (int cb = 0; cb * 32 < d; ++cb) {
     float v[32];
     if (nk > 0) {
-      uint32_t p0[32], p1[32];
+      uint32_t p0[32];
       tc::tmem_ld32_nw(trow + cb * 32, p0);
-      tc::tmem_ld32_nw(trow + 256 + cb * 32, p1);
       tc::tmem_wait_ld();
 #pragma unroll
-      for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(p0[x]) + __uint_as_float(p1[x]);
+      for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(p0[x]);
     } else {
 #pragma unroll
       for (int x = 0; x < 32; ++x) v[x] = 0.f;
-    }
-    for (int qc = q0; qc < q1; qc += 32) {
-      const int nq = min(32, q1 - qc);
-      __syncthreads();  // the previous chunk's reads of hs are done
-      for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
-        const int qq = idx >> 5, x = idx & 31, col = cb * 32 + x;
-        hs[qq * 33 + x] = qq < nq && col < d ? T.H[(int64_t)(qc + qq) * d + col] : 0.f;
-      }
-      __syncthreads();
-      for (int qq = 0; qq < nq; ++qq) {
-        const float ua = row < d ? T.U[(int64_t)(qc + qq) * d + row] : 0.f;
-#pragma unroll
-        for (int x = 0; x < 32; ++x) v[x] = fmaf(ua, hs[qq * 33 + x], v[x]);
-      }
     }
     if (row < d) {
 #pragma unroll
@@ -507,7 +512,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
 }
 
 static size_t tr_tc_smem(int N) { return (size_t)kTrStages * (128 * 128 + (size_t)((N + 31) / 32) * 4096) + 1024; }
@@ -541,17 +546,46 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
   float lsum = 0.f;
   for (int rb = p0; rb < p1; rb += RB) {
     const int nr = min(RB, p1 - rb);
-    for (int idx = threadIdx.x; idx < RB * d; idx += blockDim.x) {
-      const int rr = idx / d, e = idx % d;
-      so[rr * ds + e] = rr < nr ? a.b.O[(int64_t)a.s.rel_occ[rb + rr] * dm.dp + e] : 0.f;
-      sdo[rr * ds + e] = 0.f;
+    // row-by-warp loops (no integer division by the runtime d: the index arithmetic dominated the kernel)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int rr = warp; rr < RB; rr += 8) {
+      const float* orow = rr < nr ? a.b.O + (int64_t)a.s.rel_occ[rb + rr] * dm.dp : nullptr;
+      for (int e = lane; e < d; e += 32) {
+        so[rr * ds + e] = orow ? orow[e] : 0.f;
+        sdo[rr * ds + e] = 0.f;
+      }
     }
     for (int j0 = 0; j0 < k; j0 += JB) {
       const int nj = min(JB, k - j0);
       __syncthreads();
-      for (int idx = threadIdx.x; idx < JB * d; idx += blockDim.x) {
-        const int jj = idx / d, e = idx % d;
-        sq[jj * ds + e] = jj < nj ? QX[(int64_t)(j0 + jj) * d + e] : 0.f;
+      {  // the tile's rows (4 per warp) with all of a lane's float4 loads in flight before the stores (the kernel was
+         // bound on one outstanding load per thread: QX streams from DRAM)
+        const int d4 = d >> 2;
+        float4 v[4][4];
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4) {
+          const int jj = warp + 8 * r4;
+          const float4* qrow = reinterpret_cast<const float4*>(QX + (int64_t)(j0 + jj) * d);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int c = lane + 32 * m;
+            v[r4][m] = jj < nj && c < d4 ? __ldcs(qrow + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4) {
+          float* dst = sq + (warp + 8 * r4) * ds;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int c = lane + 32 * m;
+            if (c < d4) {
+              dst[4 * c] = v[r4][m].x;
+              dst[4 * c + 1] = v[r4][m].y;
+              dst[4 * c + 2] = v[r4][m].z;
+              dst[4 * c + 3] = v[r4][m].w;
+            }
+          }
+        }
       }
       __syncthreads();
       // pair statistics: RB x JB pairs, 2 per thread
@@ -584,27 +618,27 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
       }
       __syncthreads();
       // dO rows: sum_j coef (o - q);   dQ rows: sum_i coef (q - o)  (fixed summation order)
-      for (int idx = threadIdx.x; idx < RB * d; idx += blockDim.x) {
-        const int rr = idx / d, e = idx % d;
-        if (rr >= nr) continue;
-        float acc = sdo[rr * ds + e];
-        const float ov = so[rr * ds + e];
-        for (int jj = 0; jj < nj; ++jj) acc = fmaf(scf[rr * JB + jj], ov - sq[jj * ds + e], acc);
-        sdo[rr * ds + e] = acc;
-      }
-      for (int idx = threadIdx.x; idx < JB * d; idx += blockDim.x) {
-        const int jj = idx / d, e = idx % d;
-        if (jj >= nj) continue;
-        float acc = rb == p0 ? 0.f : dQ[(int64_t)(j0 + jj) * d + e];
-        const float qv = sq[jj * ds + e];
-        for (int rr = 0; rr < nr; ++rr) acc = fmaf(scf[rr * JB + jj], qv - so[rr * ds + e], acc);
-        dQ[(int64_t)(j0 + jj) * d + e] = acc;
+      for (int rr = warp; rr < nr; rr += 8)
+        for (int e = lane; e < d; e += 32) {
+          float acc = sdo[rr * ds + e];
+          const float ov = so[rr * ds + e];
+          for (int jj = 0; jj < nj; ++jj) acc = fmaf(scf[rr * JB + jj], ov - sq[jj * ds + e], acc);
+          sdo[rr * ds + e] = acc;
+        }
+      for (int jj = warp; jj < nj; jj += 8) {
+        float* qrow = dQ + (int64_t)(j0 + jj) * d;
+        for (int e = lane; e < d; e += 32) {
+          float acc = rb == p0 ? 0.f : qrow[e];
+          const float qv = sq[jj * ds + e];
+          for (int rr = 0; rr < nr; ++rr) acc = fmaf(scf[rr * JB + jj], qv - so[rr * ds + e], acc);
+          qrow[e] = acc;
+        }
       }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < RB * d; idx += blockDim.x) {
-      const int rr = idx / d, e = idx % d;
-      if (rr < nr) a.b.dO[(int64_t)a.s.rel_occ[rb + rr] * d + e] = sdo[rr * ds + e];
+    for (int rr = warp; rr < nr; rr += 8) {
+      float* drow = a.b.dO + (int64_t)a.s.rel_occ[rb + rr] * d;
+      for (int e = lane; e < d; e += 32) drow[e] = sdo[rr * ds + e];
     }
     __syncthreads();
   }
@@ -669,8 +703,16 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
   const float* pv = a.t.Pv + (int64_t)i * d;
   const float* dO = a.b.dO + (int64_t)i * d;
   float* gR = a.b.Grel + (int64_t)i * dm.drel;
-  float* U = a.t.U + (int64_t)2 * p * d;
-  float* H = a.t.H + (int64_t)2 * p * d;
+  const int u = a.s.rel_inv[i], pr0 = a.s.rel_off[u], pr1 = a.s.rel_off[u + 1];
+  const int64_t urow = a.t.pad_off[u] + 2 * (p - pr0);  // padded per-relation layout (k_tr_groups)
+  float* U = a.t.U + urow * d;
+  float* H = a.t.H + urow * d;
+  if (p == pr1 - 1)  // the relation's last position clears the padding rows after its 2 n_u rows
+    for (int64_t q = (a.t.pad_off[u] + 2 * (pr1 - pr0)) * d + threadIdx.x; q < (int64_t)a.t.pad_off[u + 1] * d;
+         q += blockDim.x) {
+      a.t.U[q] = 0.f;
+      a.t.H[q] = 0.f;
+    }
   const float* hrow = a.ent.row(a.s.ph[i]);
   const float* trow = a.ent.row(a.s.pt[i]);
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
@@ -744,12 +786,12 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
 }
 
 // Adagrad on M_u, one state per matrix (w = d*d)
-__global__ void __launch_bounds__(256) k_tr_proj(TrArgs a) {
+__global__ void __launch_bounds__(1024) k_tr_proj(TrArgs a) {
   const Dims& dm = a.dm;
   if (a.b.flags[2 + (a.s.info[0] & 1)]) return;
   const int u = blockIdx.x;
   if (u >= *a.s.rel_n) return;
-  __shared__ float red[8];
+  __shared__ float red[32];
   __shared__ float s_step;
   const int r = a.s.rel_uniq[u];
   const int64_t w = (int64_t)dm.d * dm.d;
@@ -767,7 +809,7 @@ __global__ void __launch_bounds__(256) k_tr_proj(TrArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     float s = 0.f;
-    for (int ww = 0; ww < 8; ++ww) s += red[ww];
+    for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww) s += red[ww];
     const float st = a.proj_st[r] + s / (float)w;
     a.proj_st[r] = st;
     s_step = dm.lr / sqrtf(st + dm.eps);
@@ -793,7 +835,7 @@ cudaError_t launch_proj_update(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
   TrArgs a{dm, s, h->rows, h->rel, h->proj, h->proj_st, h->buf, h->tr_buf, dm.B,
            h->P > 1 ? h->dist.split_index : nullptr, h->dist.gproj_split};
-  k_tr_proj<<<dm.B, 256, 0, h->stream>>>(a);
+  k_tr_proj<<<dm.B, 1024, 0, h->stream>>>(a);  // one matrix of d*d per CTA: 1024 threads stream it
   ++h->launches;
   return cudaGetLastError();
 }
@@ -839,7 +881,8 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   const dim3 gm((dm.d + GT - 1) / GT, (dm.d + GT - 1) / GT, dm.B);
   if (h->tr_tc) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
-    k_tr_dm_tc<<<dim3((dm.d + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream>>>(tt->mdQn, tt->mXn, a, tt->N);
+    k_tr_dm_tc<<<dim3((dm.d + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream>>>(tt->mdQn, tt->mXn, tt->mUn,
+                                                                                       tt->mHn, a, tt->N);
     dbg(h, "k_tr_dm_tc");
   } else {
     k_tr_gemm<2><<<gm, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<2>");
@@ -848,7 +891,7 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   e = launch_update(h, s);
   dbg(h, "update");
   if (e != cudaSuccess) return e;
-  k_tr_proj<<<dm.B, 256, 0, h->stream>>>(a); dbg(h, "k_tr_proj");
+  k_tr_proj<<<dm.B, 1024, 0, h->stream>>>(a); dbg(h, "k_tr_proj");
   h->launches += 9;
   return cudaGetLastError();
 }
@@ -925,6 +968,9 @@ void transr_tc_init(kge_handle* h) {
     ok = ok && make_map(&tt->mdQ, h->tr_buf.dQ, dm.d, dm.k, dm.B, dm.d, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     ok = ok && make_map(&tt->mdQn, h->tr_buf.dQ, dm.d, dm.k, dm.B, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     ok = ok && make_map(&tt->mXn, h->buf.X, dm.d, dm.C * dm.k, 1, dm.dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    const int urows = 2 * dm.B + 32 * dm.B;  // the padded U / H layout (k_tr_groups)
+    ok = ok && make_map(&tt->mUn, h->tr_buf.U, dm.d, urows, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    ok = ok && make_map(&tt->mHn, h->tr_buf.H, dm.d, urows, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const size_t smem = tr_tc_smem(tt->N);
     ok = ok && cudaFuncSetAttribute(k_tr_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
     ok = ok && cudaFuncSetAttribute(k_tr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;

@@ -20,6 +20,8 @@ from paper_2004_08532_b200 import kge  # noqa: E402
 def main():
     model, steps, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
     lag = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    extra = sys.argv[5] if len(sys.argv) > 5 else ""  # "repartition" | "placement" | ""
+    opts = {"repartition": dict(repartition=1), "placement": dict(placement=1, neg_local=1)}.get(extra, {})
     rank, ws = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = rank if torch.cuda.device_count() >= ws else 0
     torch.cuda.set_device(dev)
@@ -28,7 +30,7 @@ def main():
     trip = gr.triples()
     B, g, k, d = 128, 32, 32, 32
     cfg = kge.Config(model=model, n_entities=gr.n_entities, n_relations=gr.n_relations, dim=d, batch_size=B,
-                     chunk_size=g, neg_k=k, neg_precision="fp32", world_size=ws, rank=rank, lag=lag)
+                     chunk_size=g, neg_k=k, neg_precision="fp32", world_size=ws, rank=rank, lag=lag, **opts)
     h = kge.init_distributed(cfg, *trip)
     h.set_option("barrier_ms", 120000)
     losses = h.train_step(steps)
@@ -44,7 +46,7 @@ def main():
     dist.all_gather_object(res, dict(losses=losses, own=own, rows=rows, st=st, rids=mine, rel=rel))
     if rank == 0:
         import oracle as O  # test infrastructure: the check runs in the test's worker, never in the product
-        orc = O.Trainer(model, gr.n_entities, gr.n_relations, d, B, g, k, world_size=ws, triples=trip, lag=lag)
+        orc = O.Trainer(model, gr.n_entities, gr.n_relations, d, B, g, k, world_size=ws, triples=trip, lag=lag, **opts)
         lo = orc.train(steps)
         orc.flush()
         lg = sum(r["losses"].astype(np.float64) for r in res)
