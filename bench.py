@@ -395,7 +395,7 @@ def main():
     e2e = {"value": ws * B * e2e_steps / e2e_s, "unit": "positive triples/s", "h2d_bytes_per_step": 3 * B * 4,
            "d2h_bytes_per_step": 4, "steps": e2e_steps,
            "how": "kge_train_batch_async per step: host int64 (h,r,t)[B] from pinned memory, range-checked and "
-                  "narrowed to int32 on the host, H2D copy + sample + step enqueued every step (CUDA graphs), the "
+                  "narrowed to int32 on the host, H2D copy + sample (one CUDA graph on a side stream) + step kernels (PDL, behind a device-side sample gate) enqueued every step, the "
                   "step's loss stored by the device into the caller's pinned float; one sync at the end; host wall "
                   "clock after 16 warm-up calls"}
     if not np.all(np.isfinite(loss_buf.numpy())):

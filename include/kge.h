@@ -167,7 +167,9 @@ int kge_train_batch(kge_handle* h, const int64_t* heads, const int64_t* rels, co
 /* Asynchronous kge_train_batch for a pipelined host loop: the batch is range-checked and staged synchronously (the
  * caller's arrays may be reused on return), the H2D copy, the step and -- if loss_host is not NULL -- the D2H copy of
  * the step's loss into loss_host are enqueued and the call returns. loss_host should be pinned (cudaMallocHost /
- * torch pin_memory) and is valid after the next kge_sync; KGE_ENONFINITE is reported by that kge_sync. */
+ * torch pin_memory) and is valid after the next kge_sync; KGE_ENONFINITE is reported by that kge_sync.
+ * The upload and sample run on a side stream; the step's first kernel waits for them on the device (a ready counter,
+ * 5 s limit: KGE_ECUDA "sample gate timed out" from the next synchronising call, which should never happen). */
 int kge_train_batch_async(kge_handle* h, const int64_t* heads, const int64_t* rels, const int64_t* tails,
                           float* loss_host);
 

@@ -543,6 +543,12 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
         cudaEventCreateWithFlags(&h->ev_gfree[i], cudaEventDisableTiming) != cudaSuccess)
       return fail(cuda_fail(cudaGetLastError(), "events"));
   h->given = (int32_t*)dalloc(h, (size_t)kge_handle::kGiven * 3 * dm.B * 4);
+  h->gready = (uint32_t*)dalloc(h, kge_handle::kGiven * 4);
+  if (!h->given || !h->gready || cudaMemsetAsync(h->gready, 0, kge_handle::kGiven * 4, h->stream) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("out of device memory (caller-batch slots)");
+    return fail(KGE_ENOMEM);
+  }
   for (int i = 0; i < kge_handle::kStage; ++i)
     if (cudaEventCreateWithFlags(&h->stage_ev[i], cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
@@ -693,6 +699,10 @@ static int check_flags(kge_handle* h) {
   cudaError_t e = cudaMemcpyAsync(f, h->buf.flags, 16, cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   if (e != cudaSuccess) return cuda_fail(e, "sync");
+  if (f[1] == 2) {
+    set_error("caller-batch sample gate timed out (the side-stream sample of a step never completed)");
+    return KGE_ECUDA;
+  }
   if (f[1]) {
     set_error("device barrier timed out: a peer rank did not reach the step (KGE_OPT_BARRIER_MS)");
     return KGE_ECUDA;
@@ -918,6 +928,60 @@ static cudaError_t capture_graph(kge_handle* h, cudaStream_t st, const std::func
     cudaError_t _e = (call);                        \
     if (_e != cudaSuccess) return cuda_fail(_e, what); \
   } while (0)
+// device-visible address of a caller's pinned loss float (0: pageable, the loss is copied back instead)
+static uint64_t loss_device_address(float* loss_host) {
+  if (!loss_host) return 0;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, loss_host) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
+    return (uint64_t)(uintptr_t)at.devicePointer;
+  cudaGetLastError();
+  return 0;
+}
+
+// Caller batch behind a device gate (P == 1, lag 0, the gather-first step of every model but TransR / RESCAL): the
+// upload + sample run as one graph on the slot's side stream as in batch_graphs, but the main stream does not wait
+// for it with a stream event. The step kernels are launched directly, each with PDL, behind k_wait_ready -- one CTA
+// that spins on the slot's ready counter (bumped by both k_sample CTAs) and then waits for the previous step's last
+// kernel. A cross-stream event wait or a graph boundary ends the PDL chain (the next step's kernels could only launch
+// once the previous step had fully drained, ~3.7 us per step measured end to end); with the gate the chain runs from
+// one step's update into the next step's gather as in kge_train_step.
+static bool use_gate(const kge_handle* h) {
+  static const bool off = getenv("KGE_NO_GATE") != nullptr;
+  return !off && use_graphs(h) && h->dims.model != KGE_TRANSR && h->dims.model != KGE_RESCAL;
+}
+
+static int batch_gated(kge_handle* h, int gi, int64_t s, float* loss_host) {
+  const int B = h->dims.B;
+  SampleParams p = sample_params(h, true, gi);
+  const Slot* gslot = d_slots(h) + h->ring + 1 + gi;
+  cudaStream_t ss = h->gside[gi];
+  uint32_t* rd = h->gready + gi;
+  if (!h->g_samp[gi]) {
+    int32_t* st = h->pinned_given + (size_t)gi * 3 * B;
+    int32_t* gb = h->given + (size_t)gi * 3 * B;
+    KGE_GCHK(capture_graph(h, ss, [&]() {
+               cudaError_t x = cudaMemcpyAsync(gb, st, (size_t)3 * B * 4, cudaMemcpyHostToDevice, ss);
+               return x == cudaSuccess ? launch_sample(h, p, gslot, 1, s, 1, ss, 0, rd) : x;
+             }, &h->g_samp[gi], cudaGraphNodeTypeKernel, &h->g_samp_node[gi]), "capture sample graph");
+  }
+  const uint64_t dst = loss_device_address(loss_host);
+  KGE_GCHK(cudaStreamWaitEvent(ss, h->ev_gfree[gi], 0), "wait slot");
+  KGE_GCHK(sample_graph_set(h, h->g_samp[gi], h->g_samp_node[gi], p, gslot, 1, s, 1, dst, rd), "sample node params");
+  KGE_GCHK(cudaGraphLaunch(h->g_samp[gi], ss), "sample graph launch");
+  KGE_GCHK(cudaEventRecord(h->stage_ev[gi], ss), "event");
+  ++h->launches;
+  h->gcount[gi] += 1;
+  KGE_GCHK(launch_wait_ready(h, rd, 2u * h->gcount[gi]), "sample gate");
+  ++h->launches;
+  const int rc = enqueue_step(h, h->given_slots[gi], s, gi);
+  if (rc != KGE_OK) return rc;
+  KGE_GCHK(cudaEventRecord(h->ev_gfree[gi], h->stream), "event");
+  if (loss_host && !dst)
+    KGE_GCHK(cudaMemcpyAsync(loss_host, h->buf.loss + (s % h->ring), 4, cudaMemcpyDeviceToHost, h->stream),
+             "loss readback");
+  return KGE_OK;
+}
+
 static int batch_graphs(kge_handle* h, int gi, int64_t s, float* loss_host) {
   const int B = h->dims.B;
   SampleParams p = sample_params(h, true, gi);
@@ -942,14 +1006,7 @@ static int batch_graphs(kge_handle* h, int gi, int64_t s, float* loss_host) {
   const int32_t kernels = h->g_launches;
   // the loss goes straight from the kernel that reduces it to the caller's pinned (device-visible) float: a 4-byte
   // D2H copy node costs ~10 us on the step's critical path. Pageable targets keep the copy.
-  uint64_t dst = 0;
-  if (loss_host) {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, loss_host) == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer)
-      dst = (uint64_t)(uintptr_t)at.devicePointer;
-    else
-      cudaGetLastError();
-  }
+  const uint64_t dst = loss_device_address(loss_host);
   KGE_GCHK(cudaStreamWaitEvent(ss, h->ev_gfree[gi], 0), "wait slot");
   KGE_GCHK(sample_graph_set(h, h->g_samp[gi], h->g_samp_node[gi], p, gslot, 1, s, 1, dst), "sample node params");
   KGE_GCHK(cudaGraphLaunch(h->g_samp[gi], ss), "sample graph launch");
@@ -1024,8 +1081,8 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
     if (e == cudaSuccess) e = dist_clear_split(h);
     if (e != cudaSuccess) return cuda_fail(e, "barrier");
   }
-  if (use_graphs(h)) {
-    const int rc = batch_graphs(h, si, s, loss_host);
+  if (use_gate(h) || use_graphs(h)) {
+    const int rc = use_gate(h) ? batch_gated(h, si, s, loss_host) : batch_graphs(h, si, s, loss_host);
     if (rc != KGE_OK) return rc;
     h->step = s + 1;
     return KGE_OK;

@@ -269,6 +269,10 @@ struct kge_handle {
   int32_t g_launches = 0;       // kernels per captured step (launch counter)
   float* pinned_sink = nullptr;  // readback target when the caller passes no loss pointer
   int32_t* given = nullptr;  // [kGiven][3 x B] device copies of caller positives (one per given slot)
+  // device-side sample gate (P == 1, lag 0, step kernels launched directly with PDL): k_sample of given slot i bumps
+  // gready[i] once per CTA, the step's k_wait_ready waits for 2 x (samples enqueued into slot i) = 2 x gcount[i]
+  uint32_t* gready = nullptr;
+  uint32_t gcount[kGiven] = {};
   static constexpr int kStage = kGiven;  // staging buffer i feeds given slot i (the captured upload reads it)
   int32_t* pinned_given = nullptr;  // host pinned staging: kStage buffers of 3B int32 (caller-supplied batches)
   cudaEvent_t stage_ev[kStage] = {};  // recorded after each staging buffer's H2D copy
@@ -352,10 +356,14 @@ void launch_end(kge_handle* h, int kid);
 size_t sample_smem_bytes(int n_pad);
 cudaError_t sample_init();
 cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev_array, int ring, int64_t step0, int n_steps,
-                          cudaStream_t stream = nullptr, uint64_t loss_dst = 0);  // nullptr: h->stream
+                          cudaStream_t stream = nullptr, uint64_t loss_dst = 0,
+                          uint32_t* ready = nullptr);  // nullptr stream: h->stream
+// main-stream gate for a side-stream sample (see k_wait_ready)
+cudaError_t launch_wait_ready(kge_handle* h, const uint32_t* ready, uint32_t want);
 // re-point a captured k_sample node at another first step
 cudaError_t sample_graph_set(kge_handle* h, cudaGraphExec_t exec, cudaGraphNode_t node, const SampleParams& p,
-                             const Slot* slots_dev_array, int ring, int64_t step0, int n_steps, uint64_t loss_dst);
+                             const Slot* slots_dev_array, int ring, int64_t step0, int n_steps, uint64_t loss_dst,
+                             uint32_t* ready = nullptr);
 cudaError_t launch_init_table(kge_handle* h, float* tab, int64_t rows, int32_t w, uint32_t table_id, float bound,
                               int64_t row_stride = 1, int64_t row_offset = 0);
 cudaError_t launch_convert_ids(kge_handle* h, const int64_t* src, int32_t* dst, int64_t n, int64_t limit, int32_t* bad);

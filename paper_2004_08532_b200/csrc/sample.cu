@@ -29,6 +29,8 @@ struct SampleArgs {
   int64_t step0;
   uint64_t* trace;    // KGE_TRACE diagnostics or nullptr
   uint64_t loss_dst;  // device-visible host address for the loss of step0 (n_steps == 1), or 0
+  uint32_t* ready;    // n_steps == 1: counter each of the two CTAs bumps (release) once its half of the slot is
+                      // written (k_wait_ready on the main stream acquires it), or nullptr
 };
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
@@ -208,7 +210,38 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs a) {
     else
       *slot.rel_n = total;
   }
+  if (a.ready) {  // publish: every thread's slot writes, then one fenced increment per CTA
+    __syncthreads();
+    if (tid == 0) flow_release(a.ready, 1u);
+  }
   trace_stamp(a.trace, KGE_K_SAMPLE, 7);
+}
+
+// Main-stream gate of a caller batch whose sample runs on a side stream (kge_train_batch): spins until the slot's
+// counter reaches `want` (both k_sample CTAs published), then waits for its own stream predecessor, so the step's
+// kernels that follow by PDL see the sample and the previous step complete. One CTA: the side-stream sampler always
+// finds an SM. Times out after timeout_ns (flags[1] = 2: reported by the next flag check) instead of hanging.
+__global__ void k_wait_ready(const uint32_t* ready, uint32_t want, uint64_t timeout_ns, int32_t* flags) {
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    uint64_t t0 = 0;
+    for (int it = 0;; ++it) {
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
+      if ((int32_t)(v - want) >= 0) break;
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (it == 0) t0 = t;
+      else if (t - t0 > timeout_ns) { atomicExch(flags + 1, 2); break; }
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  pdl_wait();
+}
+
+cudaError_t launch_wait_ready(kge_handle* h, const uint32_t* ready, uint32_t want) {
+  return launch_pdl(k_wait_ready, dim3(1), dim3(32), 0, h->stream, ready, want, (uint64_t)5000000000ull, h->buf.flags);
 }
 
 size_t sample_smem_bytes(int n_pad) { return (size_t)n_pad * sizeof(unsigned long long); }
@@ -218,7 +251,7 @@ cudaError_t sample_init() {
 }
 
 cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slots_dev, int ring, int64_t step0, int n_steps,
-                          cudaStream_t stream, uint64_t loss_dst) {
+                          cudaStream_t stream, uint64_t loss_dst, uint32_t* ready) {
   SampleArgs a;
   a.p = p;
   a.fe_half = make_feistel_domain((uint64_t)p.n_list).half;
@@ -228,6 +261,7 @@ cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slot
   a.step0 = step0;
   a.trace = h->dims.trace;
   a.loss_dst = loss_dst;
+  a.ready = ready;
   size_t smem = sample_smem_bytes(p.n_pad);  // opt-in raised once by sample_init (never in the step path: the call
                                               // may synchronise, which would stall the multi-rank emulation)
   cudaStream_t main = h->stream;
@@ -240,7 +274,8 @@ cudaError_t launch_sample(kge_handle* h, const SampleParams& p, const Slot* slot
 }
 
 cudaError_t sample_graph_set(kge_handle* h, cudaGraphExec_t exec, cudaGraphNode_t node, const SampleParams& p,
-                             const Slot* slots_dev, int ring, int64_t step0, int n_steps, uint64_t loss_dst) {
+                             const Slot* slots_dev, int ring, int64_t step0, int n_steps, uint64_t loss_dst,
+                             uint32_t* ready) {
   SampleArgs a;
   a.p = p;
   a.fe_half = make_feistel_domain((uint64_t)p.n_list).half;
@@ -250,6 +285,7 @@ cudaError_t sample_graph_set(kge_handle* h, cudaGraphExec_t exec, cudaGraphNode_
   a.step0 = step0;
   a.trace = h->dims.trace;
   a.loss_dst = loss_dst;
+  a.ready = ready;
   void* args[] = {&a};
   cudaKernelNodeParams kp = {};
   kp.func = (void*)k_sample;
