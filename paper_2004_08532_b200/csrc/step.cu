@@ -477,6 +477,26 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     }
   }
   trace_stamp(dm.trace, KGE_K_GATHER, 7);
+  if (dm.trace && blockIdx.x == 0) {
+    // diagnostics: the previous step's k_update end (max over its CTAs' end stamps, not yet overwritten by this
+    // step's) into CTA 0's slot 2 -- the gap to this step's release (slot 1) is the inter-step PDL hand-over
+    // (slot 3: the last k_update CTA start, early-leaving CTAs included)
+    __shared__ unsigned long long s_mx, s_m0;
+    if (threadIdx.x == 0) s_mx = s_m0 = 0;
+    __syncthreads();
+    unsigned long long mx = 0, m0 = 0;
+    for (int c = threadIdx.x; c < kTraceCtas; c += blockDim.x) {
+      mx = max(mx, (unsigned long long)dm.trace[((size_t)KGE_K_UPDATE * kTraceCtas + c) * kTraceSlots + 7]);
+      m0 = max(m0, (unsigned long long)dm.trace[((size_t)KGE_K_UPDATE * kTraceCtas + c) * kTraceSlots + 0]);
+    }
+    atomicMax(&s_mx, mx);
+    atomicMax(&s_m0, m0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      dm.trace[((size_t)KGE_K_GATHER * kTraceCtas) * kTraceSlots + 2] = s_mx;
+      dm.trace[((size_t)KGE_K_GATHER * kTraceCtas) * kTraceSlots + 3] = s_m0;
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -43,10 +43,17 @@ for k in range(1, 6):
     en = T[k][:, 7][m]
     en = en[en > 0] - t0 if (en > 0).any() else np.array([0])
     line = f"{names[k]:10s} ctas={m.sum():5d} start[min/med/max]={st.min()/1e3:6.2f}/{np.median(st)/1e3:6.2f}/{st.max()/1e3:6.2f} us  end med/max={np.median(en)/1e3:6.2f}/{en.max()/1e3:6.2f} us"
+    r1 = T[k][:, 1][m]
+    r1 = r1[r1 > 0]
+    if len(r1):
+        line += f" | released(s1) min/med {(r1.min() - t0)/1e3:6.2f}/{(np.median(r1) - t0)/1e3:6.2f}"
     if k == 1 and (T[k][:, 1][m] > 0).any():
         s1 = T[k][:, 1][m]
         s1 = s1[s1 > 0] - t0
         line += f" | after pdl_wait min/med/max {s1.min()/1e3:6.2f}/{np.median(s1)/1e3:6.2f}/{s1.max()/1e3:6.2f}"
+        if T[k][0, 2] > 0:
+            line += f" | prev update end {(int(T[k][0, 2]) - t0)/1e3:6.2f}"
+            line += f", last start {(int(T[k][0, 3]) - t0)/1e3:6.2f}"
     if k in (2, 3):
         s1 = T[k][:, 1][m] - t0
         s2 = T[k][:, 2][m] - t0
