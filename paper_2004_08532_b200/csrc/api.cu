@@ -458,7 +458,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     const size_t urows = tr ? 2 * B + 32 * B : B;  // TransR: padded per-relation blocks (k_tr_dm_tc); RESCAL: B rows
     T.U = (float*)dalloc(h, urows * dm.d * 4);
     T.H = (float*)dalloc(h, urows * dm.d * 4);
-    if (!ib || !T.QX || !T.dQ || !T.dM || !T.Pv || !T.U || !T.H) { set_error("out of device memory (TransR)"); return fail(KGE_ENOMEM); }
+    T.dOp = (float*)dalloc(h, tr ? (size_t)tr_jtiles(dm.k) * B * dm.d * 4 : 4);
+    if (!ib || !T.QX || !T.dQ || !T.dM || !T.Pv || !T.U || !T.H || !T.dOp) { set_error("out of device memory (TransR)"); return fail(KGE_ENOMEM); }
     T.n_groups = ib; ib += 1;
     T.grp_u = ib; ib += B;
     T.grp_c = ib; ib += B;
@@ -593,7 +594,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pcnt = (int32_t*)dalloc(h, (size_t)dm.B * 4);
-  b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(std::max<int64_t>(h->n_neg_parts, tc_parts), dm.B) * 4);
+  const int64_t tr_parts = cfg->model == KGE_TRANSR ? (int64_t)dm.B * tr_jtiles(dm.k) : 0;
+  b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(std::max<int64_t>(std::max<int64_t>(h->n_neg_parts, tc_parts),
+                                                                         tr_parts), dm.B) * 4);
   b.flow = (uint32_t*)dalloc(h, (size_t)2 * dm.C * 4);
   {  // FFMA split-K scratch: tiles of the larger (backward) grid x up to 8 splits x 256 threads x 16 floats
     const int64_t tiles = (int64_t)((dm.d + 63) / 64) * ((std::max(dm.g, dm.k) + 63) / 64) * 2 * dm.C;
@@ -658,7 +661,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   }
   if (sample_init() != cudaSuccess || step_preload() != cudaSuccess || dist_preload() != cudaSuccess)
     return fail(cuda_fail(cudaGetLastError(), "kernel preload"));
-  if (cfg->model == KGE_TRANSR) h->n_neg_parts = dm.B;  // one loss partial per (relation, chunk) group
+  if (cfg->model == KGE_TRANSR) h->n_neg_parts = dm.B * tr_jtiles(dm.k);  // per (group, tile of 32 negatives)
   if (cfg->neg_precision != KGE_PREC_FP32 && cfg->model != KGE_TRANSR) tc_init(h);
   if (cfg->model == KGE_TRANSR) transr_tc_init(h);  // DistMult / ComplEx / TransE-L2 on tcgen05
   if (tc_supported(h)) h->n_neg_parts = tc_neg_parts(h);

@@ -100,6 +100,18 @@ __device__ __forceinline__ void trace_stamp(uint64_t* trace, int kid, int slot) 
   trace[((size_t)kid * kTraceCtas + cta) * kTraceSlots + slot] = t;
 }
 
+// last warp of the CTA to finish (slot 6, atomic max over the warps' lane 0): the CTA's true end when thread 0's
+// warp is not the last one (row-parallel kernels whose warps work independently)
+__device__ __forceinline__ void trace_warp_end(uint64_t* trace, int kid) {
+  if (trace == nullptr || (threadIdx.x & 31) != 0) return;
+  const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (cta >= kTraceCtas) return;
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMax(reinterpret_cast<unsigned long long*>(trace + ((size_t)kid * kTraceCtas + cta) * kTraceSlots + 6),
+            (unsigned long long)t);
+}
+
 // ---- programmatic dependent launch: kernels of the step are launched with PDL so the next kernel's CTAs launch and
 // run their prologue while this one drains; every kernel waits for its predecessor before touching its outputs ----
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

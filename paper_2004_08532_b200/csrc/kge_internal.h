@@ -141,7 +141,11 @@ struct TrBuffers {
   float* U;           // [(2B + 32 B) x d] gMh, gMt rows (relation-sorted; relation u's 2 n_u rows start at pad_off[u],
   float* H;           // padded to whole 32-row k-blocks with zero rows) / h, t rows, the same layout
   int32_t* pad_off;   // [B + 1] first U / H row of each unique relation (multiples of 32)
+  float* dOp;         // [kTrJt-tiles x B x d] dO partials of k_tr_score, one per tile of 32 negatives (summed in tile
+                      // order by k_tr_chain)
 };
+constexpr int kTrJt = 32;  // negatives per k_tr_score CTA
+__host__ __device__ inline int tr_jtiles(int k) { return (k + kTrJt - 1) / kTrJt; }
 
 // multi-rank state (dist.cu)
 struct Dist {

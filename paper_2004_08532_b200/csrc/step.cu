@@ -455,6 +455,8 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     acc = warp_sum(acc);
     if (lane == 0) a.b.xnorm[q] = acc;
   }
+  if (dm.trace) __threadfence();  // diagnostics: the warp's stores performed before its end stamp
+  trace_warp_end(dm.trace, KGE_K_GATHER);
   if (a.flow) {  // rows of each chunk done: k_tc_fwd starts a chunk as soon as its g + k rows are here
     __shared__ int s_chunk[8];
     if (lane == 0)
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     __syncthreads();
     unsigned long long mx = 0, m0 = 0;
     for (int c = threadIdx.x; c < kTraceCtas; c += blockDim.x) {
-      mx = max(mx, (unsigned long long)dm.trace[((size_t)KGE_K_UPDATE * kTraceCtas + c) * kTraceSlots + 7]);
+      mx = max(mx, (unsigned long long)dm.trace[((size_t)KGE_K_UPDATE * kTraceCtas + c) * kTraceSlots + 6]);
       m0 = max(m0, (unsigned long long)dm.trace[((size_t)KGE_K_UPDATE * kTraceCtas + c) * kTraceSlots + 0]);
     }
     atomicMax(&s_mx, mx);
@@ -1322,7 +1324,10 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
     int32_t* cnt = a.seg_cnt + (rel ? 0 : dm.B) + u;
     int last = 0;
     if (lane == 0) last = atomicAdd(cnt, 1) == nseg - 1;
-    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    if (!__shfl_sync(0xffffffffu, last, 0)) {
+      trace_warp_end(dm.trace, KGE_K_UPDATE);
+      return;
+    }
     __threadfence();
     if (lane == 0) *cnt = 0;  // ready for the next step
     acc.zero();
@@ -1348,12 +1353,14 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
 #pragma unroll
     for (int m = 0; m < V; ++m)
       if (lane + 32 * m < w4) st4(row, lane + 32 * m, acc.g[m]);
+    trace_warp_end(dm.trace, KGE_K_UPDATE);
     return;
   }
   float4 row_v[V];
   prefetch_row<V>(row, row_v, w4, lane);
   const float st0 = *st;
   adagrad_row<V>(row, st, acc, row_v, st0, w4, w, dm.lr, dm.eps, lane);
+  trace_warp_end(dm.trace, KGE_K_UPDATE);
   trace_stamp(dm.trace, KGE_K_UPDATE, 7);
 }
 

@@ -45,6 +45,36 @@ __global__ void kR(float* tab, long long nrows, int random, uint64_t* stamp, int
   if (threadIdx.x == 0) stamp[blockIdx.x] = gt();
 }
 
+// A'' = chain member whose odd CTAs leave before griddepcontrol.wait (as k_update's CTAs without a segment start)
+__global__ void kE(uint64_t* stamp, int spin_ns, int early) {
+  if (early && (blockIdx.x & 1)) return;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint64_t t0 = gt();
+  while (gt() - t0 < (uint64_t)spin_ns) {}
+  __syncthreads();
+  if (threadIdx.x == 0) stamp[blockIdx.x] = gt();
+}
+
+// A''' = gather-like (dynamic smem limits residency), B' = fwd-like (200 KB smem, optional cluster of 2)
+__global__ void kG(uint64_t* stamp, int spin_ns) {
+  extern __shared__ float sm[];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint64_t t0 = gt();
+  while (gt() - t0 < (uint64_t)spin_ns) {}
+  sm[threadIdx.x] = 1.f;
+  __syncthreads();
+  if (threadIdx.x == 0) stamp[blockIdx.x] = gt();
+}
+__global__ void kF(uint64_t* stamp, uint64_t* start) {
+  extern __shared__ float sm[];
+  if (threadIdx.x == 0) start[blockIdx.x] = gt();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  sm[threadIdx.x] = 2.f;
+  if (threadIdx.x == 0) stamp[blockIdx.x] = gt();
+}
+
 __global__ void kB(uint64_t* stamp, uint64_t* start) {
   if (threadIdx.x == 0) start[blockIdx.x] = gt();
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -150,6 +180,85 @@ int main() {
       }
     }
     cudaFree(tab);
+  }
+  for (int early : {0, 1}) {
+    const int G = 512;
+    std::vector<double> gmed;
+    for (int rep = 0; rep < 20; ++rep) {
+      cudaMemset(sa, 0, G * 8);
+      kA<<<148, 256>>>(buf, 0, sb, 1, 3000);  // a predecessor, so kE is itself a PDL secondary
+      {
+        cudaLaunchConfig_t c = {};
+        c.gridDim = G;
+        c.blockDim = 256;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        c.attrs = at;
+        c.numAttrs = 1;
+        cudaLaunchKernelEx(&c, kE, sa, 8000, early);
+      }
+      launch_pdl(kB, 256, sb, sst, 1);
+      cudaDeviceSynchronize();
+      std::vector<uint64_t> a(G), b(256);
+      cudaMemcpy(a.data(), sa, G * 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(b.data(), sb, 256 * 8, cudaMemcpyDeviceToHost);
+      const uint64_t ae = *std::max_element(a.begin(), a.end());
+      std::sort(b.begin(), b.end());
+      if (rep >= 5) gmed.push_back(((double)b[128] - (double)ae) / 1e3);
+    }
+    std::sort(gmed.begin(), gmed.end());
+    printf("chain A -> E (G=512, odd CTAs leave before the wait: %d) -> B: B release - E last end: med %.2f us\n", early,
+           gmed[gmed.size() / 2]);
+  }
+  cudaFuncSetAttribute(kG, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+  cudaFuncSetAttribute(kF, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int gsm : {0, 100}) {
+    for (int cl : {1, 2}) {
+      std::vector<double> g0, gm, gs;
+      for (int rep = 0; rep < 20; ++rep) {
+        cudaLaunchConfig_t c = {};
+        c.gridDim = 256;
+        c.blockDim = 256;
+        c.dynamicSmemBytes = (gsm ? gsm : 1) * 1024;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        c.attrs = at;
+        c.numAttrs = 1;
+        kA<<<148, 256>>>(buf, 0, sb, 1, 3000);
+        cudaLaunchKernelEx(&c, kG, sa, 4000);
+        cudaLaunchConfig_t f = {};
+        f.gridDim = 128;
+        f.blockDim = 256;
+        f.dynamicSmemBytes = 200 * 1024;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = cl;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        f.attrs = at;
+        f.numAttrs = 2;
+        cudaLaunchKernelEx(&f, kF, sb, sst);
+        cudaDeviceSynchronize();
+        std::vector<uint64_t> a(256), b(128), bs(128);
+        cudaMemcpy(a.data(), sa, 256 * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(b.data(), sb, 128 * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(bs.data(), sst, 128 * 8, cudaMemcpyDeviceToHost);
+        const uint64_t ae = *std::max_element(a.begin(), a.end());
+        std::sort(b.begin(), b.end());
+        std::sort(bs.begin(), bs.end());
+        if (rep >= 5) {
+          g0.push_back(((double)b[0] - (double)ae) / 1e3);
+          gm.push_back(((double)b[64] - (double)ae) / 1e3);
+          gs.push_back(((double)bs[127] - (double)ae) / 1e3);
+        }
+      }
+      std::sort(g0.begin(), g0.end());
+      std::sort(gm.begin(), gm.end());
+      std::sort(gs.begin(), gs.end());
+      printf("gather-like (256 CTAs, %3d KB smem) -> fwd-like (128 CTAs, 200 KB, cluster %d): release - A end: first %.2f med %.2f; last B start - A end %.2f us (err %s)\n",
+             gsm, cl, g0[g0.size() / 2], gm[gm.size() / 2], gs[gs.size() / 2], cudaGetErrorString(cudaGetLastError()));
+    }
   }
   cudaMemset(cnt, 0, 4);
   kBar<<<148, 256>>>(cnt, arr, rel, R);

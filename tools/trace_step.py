@@ -43,6 +43,11 @@ for k in range(1, 6):
     en = T[k][:, 7][m]
     en = en[en > 0] - t0 if (en > 0).any() else np.array([0])
     line = f"{names[k]:10s} ctas={m.sum():5d} start[min/med/max]={st.min()/1e3:6.2f}/{np.median(st)/1e3:6.2f}/{st.max()/1e3:6.2f} us  end med/max={np.median(en)/1e3:6.2f}/{en.max()/1e3:6.2f} us"
+    if k in (1, 5):
+        w6 = T[k][:, 6][m]
+        w6 = w6[w6 > 0]
+        if len(w6):
+            line += f" | last warp end {(w6.max() - t0)/1e3:6.2f}"
     r1 = T[k][:, 1][m]
     r1 = r1[r1 > 0]
     if len(r1):
