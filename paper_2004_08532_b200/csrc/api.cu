@@ -441,7 +441,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   if (e == cudaSuccess) e = cudaMemsetAsync(h->rel_st, 0, (size_t)Nr * 4, h->stream);
   if (e != cudaSuccess) return fail(cuda_fail(e, "table init"));
   if (cfg->model == KGE_TRANSR || cfg->model == KGE_RESCAL) {  // M_r, d x d row-major, same uniform law (c.6 / Q12)
-    h->proj = (float*)(h->P > 1 ? rawalloc(h, (size_t)Nr * dm.d * dm.d * 4) : dalloc(h, (size_t)Nr * dm.d * dm.d * 4));
+    // + 256 B: the 4D TMA views of TransR read a ragged last column block past the last row (make_map4c)
+    h->proj = (float*)(h->P > 1 ? rawalloc(h, (size_t)Nr * dm.d * dm.d * 4 + 256) : dalloc(h, (size_t)Nr * dm.d * dm.d * 4 + 256));
     h->proj_st = (float*)(h->P > 1 ? rawalloc(h, (size_t)Nr * 4) : dalloc(h, (size_t)Nr * 4));
     if (!h->proj || !h->proj_st) { set_error("out of device memory (TransR projections)"); return fail(KGE_ENOMEM); }
     e = launch_init_table(h, h->proj, Nr, dm.d * dm.d, 2, bound);
@@ -449,15 +450,15 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     if (e != cudaSuccess) return fail(cuda_fail(e, "projection init"));
     TrBuffers& T = h->tr_buf;
     const size_t B = dm.B;
-    int32_t* ib = (int32_t*)dalloc(h, (1 + 4 * B + (B + 1) + (dm.C + 1) + B + (B + 1)) * 4);
+    int32_t* ib = (int32_t*)dalloc(h, (1 + 4 * B + (B + 1) + (dm.C + 1) + B + (B + 1) + 1 + 2 * (B + B / 8 + 1)) * 4);
     const bool tr = cfg->model == KGE_TRANSR;  // RESCAL needs only dM and the U / V (H) factor rows
     T.QX = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 : 4);
-    T.dQ = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 : 4);
+    T.dQ = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 + 256 : 4);
     T.dM = (float*)dalloc(h, B * dm.d * dm.d * 4);
     T.Pv = (float*)dalloc(h, B * dm.d * 4);
     const size_t urows = tr ? 2 * B + 32 * B : B;  // TransR: padded per-relation blocks (k_tr_dm_tc); RESCAL: B rows
-    T.U = (float*)dalloc(h, urows * dm.d * 4);
-    T.H = (float*)dalloc(h, urows * dm.d * 4);
+    T.U = (float*)dalloc(h, urows * dm.d * 4 + 256);
+    T.H = (float*)dalloc(h, urows * dm.d * 4 + 256);
     T.dOp = (float*)dalloc(h, tr ? (size_t)tr_jtiles(dm.k) * B * dm.d * 4 : 4);
     if (!ib || !T.QX || !T.dQ || !T.dM || !T.Pv || !T.U || !T.H || !T.dOp) { set_error("out of device memory (TransR)"); return fail(KGE_ENOMEM); }
     T.n_groups = ib; ib += 1;
@@ -469,6 +470,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     T.cg_off = ib; ib += dm.C + 1;
     T.cg_list = ib; ib += B;
     T.pad_off = ib; ib += B + 1;
+    T.n_items = ib; ib += 1;
+    T.item_u = ib; ib += B + B / 8 + 1;
+    T.item_p = ib; ib += B + B / 8 + 1;
     if (cudaMemsetAsync(T.U, 0, urows * dm.d * 4, h->stream) != cudaSuccess ||
         cudaMemsetAsync(T.H, 0, urows * dm.d * 4, h->stream) != cudaSuccess)
       return fail(cuda_fail(cudaGetLastError(), "TransR scratch"));

@@ -141,6 +141,9 @@ struct TrBuffers {
   float* U;           // [(2B + 32 B) x d] gMh, gMt rows (relation-sorted; relation u's 2 n_u rows start at pad_off[u],
   float* H;           // padded to whole 32-row k-blocks with zero rows) / h, t rows, the same layout
   int32_t* pad_off;   // [B + 1] first U / H row of each unique relation (multiples of 32)
+  int32_t* n_items;   // [1] k_tr_mv work items: runs of <= 8 positions of one relation
+  int32_t* item_u;    // [B + B/8 + 1] unique relation of item
+  int32_t* item_p;    // [B + B/8 + 1] first relation-sorted position of item
   float* dOp;         // [kTrJt-tiles x B x d] dO partials of k_tr_score, one per tile of 32 negatives (summed in tile
                       // order by k_tr_chain)
 };
@@ -349,6 +352,25 @@ inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 bl
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// plain (stream-ordered, no PDL) launch with a thread-block cluster of (cx, 1, 1)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                  unsigned cx, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cx;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 void set_error(const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 
@@ -428,5 +450,7 @@ bool tc_flow();  // chunk-level dataflow counters on (KGE_FLOW=1)
 // columns / rows read as zeros
 bool make_map(CUtensorMap* m, const float* base, int cols, int rows, int chunks, int pitch, int box_rows,
               CUtensorMapSwizzle sw);
+bool make_map4c(CUtensorMap* m, const float* base, int cols, int rows, int chunks, int pitch, int box_rows, int box_kb,
+                CUtensorMapSwizzle sw);  // tc.cu
 
 }  // namespace kge

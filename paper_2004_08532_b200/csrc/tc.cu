@@ -832,6 +832,21 @@ static bool make_map4(CUtensorMap* m, const float* base, int cols, int rows, int
              sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The 4D view with ceil(cols / 32) k-blocks (a ragged last block reads past the row end into the next row: only for
+// operands whose columns are an M or N dimension of the MMA, where those lanes land in discarded outputs -- and the
+// buffer needs 128 bytes of slack after its last row)
+bool make_map4c(CUtensorMap* m, const float* base, int cols, int rows, int chunks, int pitch, int box_rows, int box_kb,
+                CUtensorMapSwizzle sw) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {32, (cuuint64_t)rows, (cuuint64_t)((cols + 31) / 32), (cuuint64_t)chunks};
+  cuuint64_t strides[3] = {(cuuint64_t)pitch * 4, 128, (cuuint64_t)pitch * 4 * rows};
+  cuuint32_t box[4] = {32, (cuuint32_t)box_rows, (cuuint32_t)box_kb, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // The same 4D view over a [chunks x rows x cols] bf16 buffer: {64 (col in k-block), rows, k-blocks, chunks}
 static bool make_map4_16(CUtensorMap* m, const uint16_t* base, int cols, int rows, int chunks, int pitch, int box_rows,
                          int box_kb) {

@@ -46,6 +46,8 @@ struct TrArgs {
 // group table
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
+  pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
+  pdl_trigger();
   const Dims& dm = a.dm;
   const TrBuffers& T = a.t;
   __shared__ int warp_tot[32];
@@ -130,47 +132,135 @@ __global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
     po += padded(u);
   }
   if (tid == 0) T.pad_off[n_rel] = s_total;
+  // k_tr_mv work items: each relation's positions cut into runs of 8 (uniform items, so a hub relation is spread
+  // over many CTAs)
+  auto nitems = [&](int u) { return (a.s.rel_off[u + 1] - a.s.rel_off[u] + 7) / 8; };
+  int tot_i = 0;
+  for (int u = u0; u < u1; ++u) tot_i += nitems(u);
+  int io = scan(tot_i);
+  for (int u = u0; u < u1; ++u)
+    for (int q = 0; q < nitems(u); ++q, ++io) {
+      T.item_u[io] = u;
+      T.item_p[io] = a.s.rel_off[u] + 8 * q;
+    }
+  if (tid == 0) *T.n_items = s_total;
 }
 
 // ------------------------------------------------------------------------------------------------
-// positives: one CTA per relation-sorted position p
+// batched projections: CTA (block of 32 output coordinates x0.., y) takes the work items y, y + gridDim.y, ... of
+// k_tr_groups (a run of <= 8 positions of one relation u): the 32 x d slab of M_u is staged in shared memory and applied
+// to the item's 16 vectors -- M_u is read once per 8 positives instead of once per positive, and a hub relation's
+// positions are spread over many CTAs.
+//   BWD = 0: Mh_i = M_u h_i, Mt_i = M_u t_i  -> U rows urow, urow + 1 (slab[x][kk] = M[x0 + x][kk])
+//   BWD = 1: dh_i = M_u^T gMh_i, dt_i = M_u^T gMt_i (U rows, k_tr_chain) -> occurrence rows i, B + i
+//            (slab[x][kk] = M[kk][x0 + x])
+// urow = pad_off[u] + 2 (p - rel_off[u]) is the relation-sorted padded layout of k_tr_groups. Thread = (x = tid / 8,
+// part q = tid % 8): partial sums over kk = q, q + 8, ..., added over the 8 lanes of x by a butterfly (every lane gets
+// the same bits; fixed order).
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_tr_pos(TrArgs a) {
+static size_t tr_mv_smem(int d) { return (size_t)(32 * (d + 1) + 16 * d) * sizeof(float); }
+
+template <int BWD>
+__global__ void __launch_bounds__(256) k_tr_mv(TrArgs a) {
+  pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
+  pdl_trigger();
   const Dims& dm = a.dm;
   extern __shared__ float sm[];
-  float* sh = sm;             // h [d]
-  float* st = sm + dm.d;      // t [d]
-  float* smh = st + dm.d;     // Mh [d]
-  float* smt = smh + dm.d;    // Mt [d]
+  const int d = dm.d, lda = d + 1, x0 = blockIdx.x * 32;
+  float* slab = sm;             // [32][d + 1]
+  float* vec = sm + 32 * lda;   // [16][d]
+  const int tid = threadIdx.x, x = tid >> 3, q = tid & 7;
+  const int n_items = *a.t.n_items;
+  for (int it = blockIdx.y; it < n_items; it += gridDim.y) {
+    const int u = a.t.item_u[it], pb = a.t.item_p[it];
+    const int pr0 = a.s.rel_off[u], np = min(8, a.s.rel_off[u + 1] - pb);
+    const int64_t ubase = a.t.pad_off[u];
+    const float* M = a.proj + (int64_t)a.s.rel_uniq[u] * d * d;
+    __syncthreads();  // the previous item's slab and vectors are consumed
+    // staged loads: 8 independent global loads in flight per thread before their shared-memory stores
+    constexpr int kLd = 8;
+    for (int e0 = tid; e0 < 32 * d; e0 += kLd * 256) {
+      float t[kLd];
+#pragma unroll
+      for (int l = 0; l < kLd; ++l) {
+        const int e = e0 + l * 256, xx = BWD ? e & 31 : e / d, kk = BWD ? e >> 5 : e - (e / d) * d;
+        t[l] = e < 32 * d && x0 + xx < d ? (BWD ? __ldg(M + (int64_t)kk * d + x0 + xx) : __ldg(M + (int64_t)(x0 + xx) * d + kk))
+                                         : 0.f;
+      }
+#pragma unroll
+      for (int l = 0; l < kLd; ++l) {
+        const int e = e0 + l * 256, xx = BWD ? e & 31 : e / d, kk = BWD ? e >> 5 : e - (e / d) * d;
+        if (e < 32 * d) slab[xx * lda + kk] = t[l];
+      }
+    }
+    for (int e0 = tid; e0 < 16 * d; e0 += kLd * 256) {
+      float t[kLd];
+#pragma unroll
+      for (int l = 0; l < kLd; ++l) {
+        const int e = e0 + l * 256, v = e / d, kk = e - v * d, pp = v >> 1;
+        float val = 0.f;
+        if (e < 16 * d && pp < np) {
+          const int p = pb + pp;
+          if (BWD) {
+            val = a.t.U[(ubase + 2 * (p - pr0) + (v & 1)) * d + kk];
+          } else {
+            const int i = a.s.rel_occ[p];
+            val = a.ent.row((v & 1) ? a.s.pt[i] : a.s.ph[i])[kk];
+          }
+        }
+        t[l] = val;
+      }
+#pragma unroll
+      for (int l = 0; l < kLd; ++l)
+        if (e0 + l * 256 < 16 * d) vec[e0 + l * 256] = t[l];
+    }
+    __syncthreads();
+    float acc[16];
+#pragma unroll
+    for (int v = 0; v < 16; ++v) acc[v] = 0.f;
+    const float* sr = slab + x * lda;
+    for (int kk = q; kk < d; kk += 8) {
+      const float m = sr[kk];
+#pragma unroll
+      for (int v = 0; v < 16; ++v) acc[v] = fmaf(m, vec[v * d + kk], acc[v]);
+    }
+#pragma unroll
+    for (int v = 0; v < 16; ++v) {
+      acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 1);
+      acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 2);
+      acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 4);
+    }
+    if (x0 + x < d) {
+#pragma unroll
+      for (int v = 0; v < 16; ++v) {
+        if ((v & 7) != q || (v >> 1) >= np) continue;  // lane q stores vectors q and q + 8
+        const int p = pb + (v >> 1);
+        if (BWD) {
+          const int i = a.s.rel_occ[p];
+          a.b.Gocc[((int64_t)((v & 1) ? dm.B + i : i)) * d + x0 + x] = acc[v];
+        } else {
+          a.t.U[(ubase + 2 * (p - pr0) + (v & 1)) * d + x0 + x] = acc[v];
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// positives: one CTA per relation-sorted position p, from Mh / Mt of k_tr_mv<0>
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_tr_pos(TrArgs a) {
+  pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
+  pdl_trigger();
+  const Dims& dm = a.dm;
   __shared__ float red[8];
   const int p = blockIdx.x, i = a.s.rel_occ[p];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, d = dm.d;
   const int r = a.s.pr[i], mode = a.s.mode[i / dm.g];
-  const float* M = a.proj + (int64_t)r * d * d;
-  const float* hrow = a.ent.row(a.s.ph[i]);
-  const float* trow = a.ent.row(a.s.pt[i]);
+  const int u = a.s.rel_inv[i];
+  const float* smh = a.t.U + (a.t.pad_off[u] + 2 * (int64_t)(p - a.s.rel_off[u])) * d;  // Mh, then Mt
+  const float* smt = smh + d;
   const float* rv = a.rel + (int64_t)r * d;
-  for (int e = threadIdx.x; e < d; e += blockDim.x) {
-    sh[e] = hrow[e];
-    st[e] = trow[e];
-  }
-  __syncthreads();
-  for (int row = warp; row < d; row += 8) {
-    const float* mr = M + (int64_t)row * d;
-    float ah = 0.f, at = 0.f;
-    for (int b = lane; b < d; b += 32) {
-      const float m = mr[b];
-      ah = fmaf(m, sh[b], ah);
-      at = fmaf(m, st[b], at);
-    }
-    ah = warp_sum(ah);
-    at = warp_sum(at);
-    if (lane == 0) {
-      smh[row] = ah;
-      smt[row] = at;
-    }
-  }
-  __syncthreads();
   float sq = 0.f;
   float* o = a.b.O + (int64_t)i * dm.dp;
   float* pv = a.t.Pv + (int64_t)i * d;
@@ -209,6 +299,8 @@ constexpr int GT = 64, GK = 16;
 
 template <int MODE>
 __global__ void __launch_bounds__(256) k_tr_gemm(TrArgs a) {
+  pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
+  pdl_trigger();
   const Dims& dm = a.dm;
   const TrBuffers& T = a.t;
   const int grp = blockIdx.z;
@@ -326,12 +418,21 @@ __global__ void __launch_bounds__(128, 1)
   __shared__ uint32_t tbase;
   const Dims& dm = a.dm;
   const TrBuffers& T = a.t;
-  const int grp = blockIdx.y;
-  if (grp >= *T.n_groups) return;  // uniform per CTA, before any barrier / TMEM use
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = dm.d, k = dm.k, m0 = blockIdx.x * 128;
-  const int u = T.grp_u[grp], c = T.grp_c[grp], r = a.s.rel_uniq[u];
   const int nkb = (d + 31) / 32, nnb = (N + 31) / 32;
+  // MODE 0: blockIdx.y = group. MODE 1: blockIdx.y = chunk c, blockIdx.z = slice of the chunk's group list: the
+  // slice's P_g = dQ_g M_u are accumulated in TMEM (one partial sum per slice, k_tr_reduce adds the slices in order)
+  int grp = blockIdx.y, l0 = 0, nsteps = nkb;
+  if (MODE == 0) {
+    if (grp >= *T.n_groups) return;  // uniform per CTA, before any barrier / TMEM use
+  } else {
+    const int c = blockIdx.y, S = gridDim.z, z = blockIdx.z;
+    const int gb = T.cg_off[c], ng = T.cg_off[c + 1] - gb;
+    l0 = gb + (int)(((int64_t)ng * z) / S);
+    nsteps = (gb + (int)(((int64_t)ng * (z + 1)) / S) - l0) * nkb;
+  }
+  auto step_group = [&](int q) { return MODE == 0 ? grp : T.cg_list[l0 + q / nkb]; };
   const uint32_t A_BYTES = 128 * 128, STAGE = A_BYTES + (uint32_t)nnb * 4096;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTrStages; ++s) {
@@ -346,10 +447,13 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tbase;
+  pdl_wait();  // barriers / TMEM set up while the predecessor finished
+  pdl_trigger();
   if (warp == 0 && lane == 0) {  // TMA producer
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kTrStages;
-      if (kb >= kTrStages) tc::mbar_wait(&empty[s], ((kb / kTrStages) - 1) & 1);
+    for (int q = 0; q < nsteps; ++q) {
+      const int s = q % kTrStages, kb = q % nkb, g = step_group(q);
+      const int c = T.grp_c[g], r = a.s.rel_uniq[T.grp_u[g]];
+      if (q >= kTrStages) tc::mbar_wait(&empty[s], ((q / kTrStages) - 1) & 1);
       uint8_t* sa = smem + s * STAGE;
       if (MODE == 0) {
         tc::mbar_arrive_expect_tx(&full[s], A_BYTES + (uint32_t)N * 128);
@@ -357,9 +461,9 @@ __global__ void __launch_bounds__(128, 1)
         tc::tma_load_3d(sa + A_BYTES, &mB, &full[s], kb * 32, 0, r);
       } else {
         tc::mbar_arrive_expect_tx(&full[s], STAGE);
-        tc::tma_load_3d(sa, &mA, &full[s], kb * 32, m0, grp);
-        for (int nb = 0; nb < nnb; ++nb)  // rows a = kb*32.., columns b = nb*32..: [32 K rows][32 N] per block
-          tc::tma_load_3d(sa + A_BYTES + nb * 4096, &mB, &full[s], nb * 32, kb * 32, r);
+        tc::tma_load_3d(sa, &mA, &full[s], kb * 32, m0, g);
+        // rows a = kb*32.., every column block b = nb*32..: [nnb][32 K rows][32 N] in one 4D box
+        tc::tma_load_4d(sa + A_BYTES, &mB, &full[s], 0, kb * 32, 0, r);
       }
     }
   } else if ((warp == 2 || warp == 3) && lane == 0 && (warp == 2 || N > 128)) {
@@ -369,9 +473,9 @@ __global__ void __launch_bounds__(128, 1)
     const int n0 = qi * 128, nn = qi ? N - 128 : (N < 128 ? N : 128);
     const uint32_t idesc = tc::idesc_tf32(128, nn, false, MODE == 1);
     const uint32_t acc = tmem + (uint32_t)n0;
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kTrStages;
-      tc::mbar_wait(&full[s], (kb / kTrStages) & 1);
+    for (int q = 0; q < nsteps; ++q) {
+      const int s = q % kTrStages;
+      tc::mbar_wait(&full[s], (q / kTrStages) & 1);
       tc::tc_fence_after();
       const uint32_t sa = tc::smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
 #pragma unroll
@@ -379,23 +483,32 @@ __global__ void __launch_bounds__(128, 1)
         // N offset: K-major B = 128 rows of 128 B further; MN-major B = 4 blocks of 32 columns further
         const uint64_t bd = MODE == 0 ? tc::sdesc(sb + n0 * 128 + sl * 32, 16, 1024)
                                       : sdesc_mn32(sb + (n0 / 32) * 4096 + sl * 1024, 4096);
-        tc::mma_tf32(acc, tc::sdesc(sa + sl * 32, 16, 1024), bd, idesc, (kb | sl) ? 1u : 0u);
+        tc::mma_tf32(acc, tc::sdesc(sa + sl * 32, 16, 1024), bd, idesc, (q | sl) ? 1u : 0u);
       }
       tc::mma_commit(&empty[s]);
     }
     tc::mma_commit(&done);
   }
   __syncwarp();
-  tc::mbar_wait(&done, 0);
-  tc::tc_fence_after();
-  // epilogue: thread <-> row m0 + 32 warp + lane; p0 + p1 per 32-column chunk, stored to row pitch d
+  if (nsteps > 0) {
+    tc::mbar_wait(&done, 0);
+    tc::tc_fence_after();
+  }
+  // epilogue: thread <-> row m0 + 32 warp + lane, stored to row pitch d (MODE 0: QX_g; MODE 1: the slice's partial
+  // sum, slot (z C + c) of the same buffer)
   const int row = m0 + warp * 32 + lane;
-  float* out = T.QX + (int64_t)grp * k * d + (int64_t)row * d;
+  const int64_t slot = MODE == 0 ? grp : (int64_t)blockIdx.z * dm.C + blockIdx.y;
+  float* out = T.QX + slot * k * d + (int64_t)row * d;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   for (int cb = 0; cb * 32 < d; ++cb) {
     uint32_t p0[32];
-    tc::tmem_ld32_nw(trow + cb * 32, p0);
-    tc::tmem_wait_ld();
+    if (nsteps > 0) {
+      tc::tmem_ld32_nw(trow + cb * 32, p0);
+      tc::tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int x = 0; x < 32; ++x) p0[x] = 0u;
+    }
     if (row < k) {
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
@@ -447,6 +560,8 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = tbase;
+  pdl_wait();  // barriers / TMEM set up while the predecessor finished
+  pdl_trigger();
   if (warp == 0 && lane == 0) {  // TMA producer
     for (int q = 0; q < nk; ++q) {
       const int s = q % kTrStages;
@@ -455,14 +570,13 @@ __global__ void __launch_bounds__(128, 1)
       tc::mbar_arrive_expect_tx(&full[s], STAGE);
       if (q < nkq) {
         const int g = g0 + q / nkg, kb = q % nkg, c = T.grp_c[g];
-        for (int b = 0; b < 4; ++b)  // A = dQ_g^T: [4 M-blocks of 32 a][32 K rows j][128 B]
-          tc::tma_load_3d(sa + b * 4096, &mdQn, &full[s], m0 + b * 32, kb * 32, g);
-        for (int nb = 0; nb < nnb; ++nb)  // B = X'_c: [N-blocks of 32 b][32 K rows j][128 B]
-          tc::tma_load_3d(sa + A_BYTES + nb * 4096, &mXn, &full[s], nb * 32, c * k + kb * 32, 0);
+        // A = dQ_g^T: [4 M-blocks of 32 a][32 K rows j][128 B]; B = X'_c: [N-blocks of 32 b][32 K rows j][128 B]
+        tc::tma_load_4d(sa, &mdQn, &full[s], 0, kb * 32, m0 / 32, g);
+        tc::tma_load_4d(sa + A_BYTES, &mXn, &full[s], 0, c * k + kb * 32, 0, 0);
       } else {  // + U^T H over the relation's positions: A = U^T (MN-major), B = H (MN-major), K = 32 rows
         const int row = uq0 + (q - nkq) * 32;
-        for (int b = 0; b < 4; ++b) tc::tma_load_3d(sa + b * 4096, &mUn, &full[s], m0 + b * 32, row, 0);
-        for (int nb = 0; nb < nnb; ++nb) tc::tma_load_3d(sa + A_BYTES + nb * 4096, &mHn, &full[s], nb * 32, row, 0);
+        tc::tma_load_4d(sa, &mUn, &full[s], 0, row, m0 / 32, 0);
+        tc::tma_load_4d(sa + A_BYTES, &mHn, &full[s], 0, row, 0, 0);
       }
     }
   } else if ((warp == 2 || warp == 3) && lane == 0 && (warp == 2 || N > 128)) {  // issuers split N (see k_tr_tc)
@@ -488,26 +602,82 @@ __global__ void __launch_bounds__(128, 1)
     tc::mbar_wait(&done, 0);
     tc::tc_fence_after();
   }
-  // epilogue: row a = m0 + 32 warp + lane of dM_u straight from TMEM (the U^T H term was accumulated by the MMAs)
+  // epilogue: row a = m0 + 32 warp + lane of dM_u straight from TMEM (the U^T H term was accumulated by the MMAs),
+  // fused with the projection's Adagrad (reading c.11: one state per matrix, w = d*d). The CTAs of relation u -- one
+  // cluster over the row blocks of dM_u -- add their sums of squares in cluster-rank order through distributed shared
+  // memory; each then applies M_u -= lr dM_u / sqrt(state + eps) to its rows from TMEM (no dM round trip through HBM
+  // and no separate pass over it). A split relation at P > 1 stores this rank's sum instead (dist.cu applies the
+  // rank-ordered sum on every replica); a non-finite loss skips the update (KGE_ENONFINITE).
+  __shared__ float s_sq[4];
+  __shared__ float s_part;
   const int row = m0 + warp * 32 + lane;
-  float* out = T.dM + (int64_t)u * d * d + (int64_t)row * d;
+  const int r = a.s.rel_uniq[u];
+  const int sidx = a.split_index ? a.split_index[r] : -1;
+  const bool skip = a.b.flags[2 + (a.s.info[0] & 1)] != 0;
+  const int64_t w = (int64_t)d * d;
+  const float st_old = a.proj_st[r];  // every CTA reads it before cluster rank 0 overwrites it (after the barrier)
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  auto chunk = [&](int cb, float* v) {
+    uint32_t p0[32];
+    tc::tmem_ld32_nw(trow + cb * 32, p0);
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(p0[x]);
+  };
+  float sq = 0.f;
   for (int cb = 0; cb * 32 < d; ++cb) {
     float v[32];
-    if (nk > 0) {
-      uint32_t p0[32];
-      tc::tmem_ld32_nw(trow + cb * 32, p0);
-      tc::tmem_wait_ld();
+    chunk(cb, v);
+    if (row < d && !skip) {
+      if (sidx >= 0) {
+        float* out = a.gproj_split + (int64_t)sidx * w + (int64_t)row * d;
 #pragma unroll
-      for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(p0[x]);
-    } else {
+        for (int x = 0; x < 32; x += 4)
+          if (cb * 32 + x < d)
+            *reinterpret_cast<float4*>(out + cb * 32 + x) = make_float4(v[x], v[x + 1], v[x + 2], v[x + 3]);
+      } else {
 #pragma unroll
-      for (int x = 0; x < 32; ++x) v[x] = 0.f;
+        for (int x = 0; x < 32; ++x)
+          if (cb * 32 + x < d) sq = fmaf(v[x], v[x], sq);
+      }
     }
-    if (row < d) {
+  }
+  sq = warp_sum(sq);
+  if (lane == 0) s_sq[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) s_part = ((s_sq[0] + s_sq[1]) + s_sq[2]) + s_sq[3];
+  tc::cluster_sync();
+  float total = 0.f;
+  for (unsigned q = 0; q < gridDim.x; ++q) total += tc::ld_cluster_f32(tc::mapa_shared(tc::smem_u32(&s_part), q));
+  const float st_new = st_old + total / (float)w;
+  const float step = dm.lr / sqrtf(st_new + dm.eps);
+  tc::cluster_sync();  // the peers' reads of s_part are done before any CTA leaves
+  if (!skip && sidx < 0) {
+    if (tc::cluster_ctarank() == 0 && threadIdx.x == 0) a.proj_st[r] = st_new;
+    // each warp's 32 x 32 gradient chunk is transposed through shared memory (the pipeline stages are free once the
+    // MMAs completed), so every M_u row segment is read and written by one coalesced 128-byte warp access
+    float* tw = reinterpret_cast<float*>(smem) + warp * (32 * 33);
+    const int rbase = m0 + warp * 32;
+    float* Mw = a.proj + (int64_t)r * w;
+    for (int cb = 0; cb * 32 < d; ++cb) {
+      float v[32];
+      chunk(cb, v);
 #pragma unroll
-      for (int x = 0; x < 32; x += 4)
-        if (cb * 32 + x < d) *reinterpret_cast<float4*>(out + cb * 32 + x) = make_float4(v[x], v[x + 1], v[x + 2], v[x + 3]);
+      for (int x = 0; x < 32; ++x) tw[lane * 33 + x] = v[x];
+      __syncwarp();
+      const int col = cb * 32 + lane;
+#pragma unroll
+      for (int h2 = 0; h2 < 32; h2 += 16) {
+        float m[16];
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr)
+          m[rr] = rbase + h2 + rr < d && col < d ? Mw[(int64_t)(rbase + h2 + rr) * d + col] : 0.f;
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr)
+          if (rbase + h2 + rr < d && col < d)
+            Mw[(int64_t)(rbase + h2 + rr) * d + col] = m[rr] - step * tw[(h2 + rr) * 33 + lane];
+      }
+      __syncwarp();
     }
   }
   tc::tc_fence_before();
@@ -527,6 +697,8 @@ static size_t tr_tc_smem(int N) { return (size_t)kTrStages * (128 * 128 + (size_
 // ------------------------------------------------------------------------------------------------
 template <int V>
 __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
+  pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
+  pdl_trigger();
   constexpr int RB = 4 / V;  // positives per block (registers: (2 JU + 2 RB) V float4 per lane)
   constexpr int JU = kTrJt / 8;  // negatives per warp
   const Dims& dm = a.dm;
@@ -663,7 +835,10 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
 static int tr_score_v(int d) { return d <= 128 ? 1 : (d <= 256 ? 2 : 4); }
 
 // dX'_c[j][e] = sum over the chunk's groups (ascending group id) of P_g[j][e]  -> occurrence rows 2B + c*k + j
-__global__ void k_tr_reduce(TrArgs a) {
+// (nslice > 0: the tcgen05 path's per-slice partial sums, slot z C + c, added in slice order)
+__global__ void k_tr_reduce(TrArgs a, int nslice) {
+  pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
+  pdl_trigger();
   const Dims& dm = a.dm;
   const TrBuffers& T = a.t;
   const int64_t total = (int64_t)dm.C * dm.k * dm.d;
@@ -671,7 +846,10 @@ __global__ void k_tr_reduce(TrArgs a) {
     const int c = (int)(q / ((int64_t)dm.k * dm.d));
     const int64_t je = q - (int64_t)c * dm.k * dm.d;
     float acc = 0.f;
-    for (int l = T.cg_off[c]; l < T.cg_off[c + 1]; ++l) acc += T.QX[(int64_t)T.cg_list[l] * dm.k * dm.d + je];
+    if (nslice > 0)
+      for (int z = 0; z < nslice; ++z) acc += T.QX[((int64_t)z * dm.C + c) * dm.k * dm.d + je];
+    else
+      for (int l = T.cg_off[c]; l < T.cg_off[c + 1]; ++l) acc += T.QX[(int64_t)T.cg_list[l] * dm.k * dm.d + je];
     a.b.Gocc[((int64_t)2 * dm.B + (int64_t)c * dm.k) * dm.d + je] = acc;
   }
 }
@@ -683,6 +861,8 @@ __global__ void k_tr_reduce(TrArgs a) {
 //   dh = M^T gMh, dt = M^T gMt ; dM_u += gMh h^T + gMt t^T (rows U/H at 2p, 2p+1)
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
+  pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
+  pdl_trigger();
   const Dims& dm = a.dm;
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == gridDim.x - 1) {
@@ -702,10 +882,7 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
     }
     return;
   }
-  extern __shared__ float sm[];
   const int d = dm.d;
-  float* sgh = sm;
-  float* sgt = sm + d;
   const int p = blockIdx.x, i = a.s.rel_occ[p];
   const int r = a.s.pr[i], mode = a.s.mode[i / dm.g];
   const float w = dm.loss == KGE_LOSS_PAIRWISE ? -(float)a.b.pcnt[i] * (1.f / ((float)dm.B * (float)dm.k))
@@ -733,74 +910,19 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
     for (int t = 1; t < njt; ++t) dO += dOp[t * tstride + e];  // the negative tiles in order
     const float gh = mode == 0 ? dO - tp : -tp;
     const float gt = mode == 0 ? tp : dO + tp;
-    sgh[e] = gh;
-    sgt[e] = gt;
     gR[e] = mode == 0 ? gh : -gt;
     U[e] = gh;
     U[d + e] = gt;
     H[e] = hrow[e];
     H[d + e] = trow[e];
   }
-  __syncthreads();
-  const float* M = a.proj + (int64_t)r * d * d;
-  float* gH = a.b.Gocc + (int64_t)i * d;
-  float* gT = a.b.Gocc + (int64_t)(dm.B + i) * d;
-  // dh = M^T gMh, dt = M^T gMt: warp w takes rows w, w + 8, ... (coalesced row reads, 2 x kCol independent chains per
-  // lane), the 8 warp partials are added in warp order (deterministic)
-  constexpr int kCol = 8;  // columns per lane: d <= 256
-  float* part = sm + 2 * d;  // [8 warps][2][d]
-  const int wid = threadIdx.x >> 5;
-  if (d <= 32 * kCol) {
-    float ah[kCol], at[kCol];
-#pragma unroll
-    for (int j = 0; j < kCol; ++j) ah[j] = at[j] = 0.f;
-    for (int row = wid; row < d; row += 8) {
-      const float* mr = M + (int64_t)row * d;
-      const float gh = sgh[row], gt = sgt[row];
-#pragma unroll
-      for (int j = 0; j < kCol; ++j) {
-        const int b = lane + 32 * j;
-        if (b < d) {
-          const float m = __ldg(mr + b);
-          ah[j] = fmaf(m, gh, ah[j]);
-          at[j] = fmaf(m, gt, at[j]);
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kCol; ++j) {
-      const int b = lane + 32 * j;
-      if (b < d) {
-        part[(wid * 2) * d + b] = ah[j];
-        part[(wid * 2 + 1) * d + b] = at[j];
-      }
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < d; b += blockDim.x) {
-      float sh = 0.f, st = 0.f;
-      for (int w8 = 0; w8 < 8; ++w8) {
-        sh += part[(w8 * 2) * d + b];
-        st += part[(w8 * 2 + 1) * d + b];
-      }
-      gH[b] = sh;
-      gT[b] = st;
-    }
-    return;
-  }
-  for (int b = threadIdx.x; b < d; b += blockDim.x) {
-    float ah = 0.f, at = 0.f;
-    for (int row = 0; row < d; ++row) {
-      const float m = M[(int64_t)row * d + b];
-      ah = fmaf(m, sgh[row], ah);
-      at = fmaf(m, sgt[row], at);
-    }
-    gH[b] = ah;
-    gT[b] = at;
-  }
+  (void)r;  // dh = M^T gMh, dt = M^T gMt: k_tr_mv<1> over the U rows written here
 }
 
 // Adagrad on M_u, one state per matrix (w = d*d)
 __global__ void __launch_bounds__(1024) k_tr_proj(TrArgs a) {
+  pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
+  pdl_trigger();
   const Dims& dm = a.dm;
   if (a.b.flags[2 + (a.s.info[0] & 1)]) return;
   const int u = blockIdx.x;
@@ -849,7 +971,7 @@ cudaError_t launch_proj_update(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
   TrArgs a{dm, s, h->rows, h->rel, h->proj, h->proj_st, h->buf, h->tr_buf, h->n_neg_parts,
            h->P > 1 ? h->dist.split_index : nullptr, h->dist.gproj_split};
-  k_tr_proj<<<dm.B, 1024, 0, h->stream>>>(a);  // one matrix of d*d per CTA: 1024 threads stream it
+  launch_pdl(k_tr_proj, dm.B, 1024, 0, h->stream, a);  // one matrix of d*d per CTA: 1024 threads stream it
   ++h->launches;
   return cudaGetLastError();
 }
@@ -861,57 +983,73 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
            h->P > 1 ? h->dist.split_index : nullptr, h->dist.gproj_split};
   cudaError_t e;
   launch_begin(h, KGE_K_GATHER);
-  k_tr_groups<<<1, 1024, 0, h->stream>>>(a); dbg(h, "k_tr_groups");
+  launch_pdl(k_tr_groups, 1, 1024, 0, h->stream, a); dbg(h, "k_tr_groups");
   e = launch_gather_neg(h, s);
   dbg(h, "gather_neg");
   if (e != cudaSuccess) return e;
-  k_tr_pos<<<dm.B, 256, 4 * dm.d * sizeof(float), h->stream>>>(a); dbg(h, "k_tr_pos");
+  // k_tr_mv: about one item (<= B / 8 + n_rel_u of them) per CTA
+  const dim3 gmv((dm.d + 31) / 32, dm.B / 8 + dm.B / 2 + 1);
+  launch_pdl(k_tr_mv<0>, gmv, 256, tr_mv_smem(dm.d), h->stream, a); dbg(h, "k_tr_mv<0>");
+  launch_pdl(k_tr_pos, dm.B, 256, 0, h->stream, a); dbg(h, "k_tr_pos");
   launch_end(h, KGE_K_GATHER);
   const dim3 gk((dm.d + GT - 1) / GT, (dm.k + GT - 1) / GT, dm.B);
   launch_begin(h, KGE_K_NEG_FWD);
   if (h->tr_tc) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
-    k_tr_tc<0><<<dim3((dm.k + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream>>>(tt->mX, tt->mM, a, tt->N);
+    launch_pdl(k_tr_tc<0>, dim3((dm.k + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream, tt->mX, tt->mM, a, tt->N);
     dbg(h, "k_tr_tc<0>");
   } else {
-    k_tr_gemm<0><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<0>");
+    launch_pdl(k_tr_gemm<0>, gk, 256, 0, h->stream, a); dbg(h, "k_tr_gemm<0>");
   }
   const dim3 gs(tr_jtiles(dm.k), dm.B);
   switch (tr_score_v(dm.d)) {
-    case 1: k_tr_score<1><<<gs, 256, 0, h->stream>>>(a); break;
-    case 2: k_tr_score<2><<<gs, 256, 0, h->stream>>>(a); break;
-    default: k_tr_score<4><<<gs, 256, 0, h->stream>>>(a); break;
+    case 1: launch_pdl(k_tr_score<1>, gs, 256, 0, h->stream, a); break;
+    case 2: launch_pdl(k_tr_score<2>, gs, 256, 0, h->stream, a); break;
+    default: launch_pdl(k_tr_score<4>, gs, 256, 0, h->stream, a); break;
   }
   dbg(h, "k_tr_score");
   launch_end(h, KGE_K_NEG_FWD);
   launch_begin(h, KGE_K_NEG_BWD);
+  // k_tr_tc<1>: CTAs (tile of 128 negatives, chunk, slice of the chunk's groups), about two per SM; the slices' partial
+  // sums take slots z C + c of the QX buffer (B slots of k x d)
+  const int jt = (dm.k + 127) / 128;
+  const int nslice = std::max(1, std::min(2 * 148 / (jt * dm.C), dm.B / dm.C));
   if (h->tr_tc) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
-    k_tr_tc<1><<<dim3((dm.k + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream>>>(tt->mdQ, tt->mMn, a, tt->N);
+    launch_pdl(k_tr_tc<1>, dim3(jt, dm.C, nslice), 128, tr_tc_smem(tt->N), h->stream, tt->mdQ, tt->mMn, a, tt->N);
     dbg(h, "k_tr_tc<1>");
   } else {
-    k_tr_gemm<1><<<gk, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<1>");
+    launch_pdl(k_tr_gemm<1>, gk, 256, 0, h->stream, a); dbg(h, "k_tr_gemm<1>");
   }
   const int64_t tot = (int64_t)dm.C * dm.k * dm.d;
-  k_tr_reduce<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, h->stream>>>(a); dbg(h, "k_tr_reduce");
+  launch_pdl(k_tr_reduce, (unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, h->stream, a,
+             h->tr_tc ? nslice : 0);
+  dbg(h, "k_tr_reduce");
   launch_end(h, KGE_K_NEG_BWD);
   launch_begin(h, KGE_K_CHAIN);
-  k_tr_chain<<<dm.B + 1, 256, 18 * dm.d * sizeof(float), h->stream>>>(a); dbg(h, "k_tr_chain");
+  launch_pdl(k_tr_chain, dm.B + 1, 256, 0, h->stream, a); dbg(h, "k_tr_chain");
+  launch_pdl(k_tr_mv<1>, gmv, 256, tr_mv_smem(dm.d), h->stream, a); dbg(h, "k_tr_mv<1>");
   const dim3 gm((dm.d + GT - 1) / GT, (dm.d + GT - 1) / GT, dm.B);
   if (h->tr_tc) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
-    k_tr_dm_tc<<<dim3((dm.d + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream>>>(tt->mdQn, tt->mXn, tt->mUn,
-                                                                                       tt->mHn, a, tt->N);
+    // cluster = the row blocks of one relation's dM (the fused Adagrad adds their sums of squares through DSMEM)
+    const unsigned cx = (unsigned)((dm.d + 127) / 128);
+    e = launch_pdl_cluster(k_tr_dm_tc, dim3(cx, dm.B), 128, tr_tc_smem(tt->N), h->stream, cx, tt->mdQn, tt->mXn, tt->mUn,
+                       tt->mHn, a, tt->N);
+    if (e != cudaSuccess) return e;
     dbg(h, "k_tr_dm_tc");
   } else {
-    k_tr_gemm<2><<<gm, 256, 0, h->stream>>>(a); dbg(h, "k_tr_gemm<2>");
+    launch_pdl(k_tr_gemm<2>, gm, 256, 0, h->stream, a); dbg(h, "k_tr_gemm<2>");
   }
   launch_end(h, KGE_K_CHAIN);
   e = launch_update(h, s);
   dbg(h, "update");
   if (e != cudaSuccess) return e;
-  k_tr_proj<<<dm.B, 1024, 0, h->stream>>>(a); dbg(h, "k_tr_proj");
-  h->launches += 9;
+  if (!h->tr_tc) {  // the tcgen05 path applies it in k_tr_dm_tc's epilogue
+    launch_pdl(k_tr_proj, dm.B, 1024, 0, h->stream, a);
+    dbg(h, "k_tr_proj");
+  }
+  h->launches += h->tr_tc ? 7 : 8;  // kernels launched here beyond the four launch_begin brackets (k_update counts itself)
   return cudaGetLastError();
 }
 
@@ -964,8 +1102,9 @@ cudaError_t launch_transr_score(kge_handle* h, const int32_t* hs, const int32_t*
 
 
 bool transr_init(kge_handle* h) {
-  (void)h;
-  return true;
+  const int smem = (int)tr_mv_smem(h->dims.d);
+  return cudaFuncSetAttribute(k_tr_mv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess &&
+         cudaFuncSetAttribute(k_tr_mv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
 }
 
 // after the step buffers exist (the maps name X' and the projection table)
@@ -977,14 +1116,15 @@ void transr_tc_init(kge_handle* h) {
     tt->N = (dm.d + 15) / 16 * 16;
     bool ok = make_map(&tt->mX, h->buf.X, dm.d, dm.C * dm.k, 1, dm.dp, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     ok = ok && make_map(&tt->mM, h->proj, dm.d, dm.d, (int)dm.n_relations, dm.d, tt->N, CU_TENSOR_MAP_SWIZZLE_128B);
-    ok = ok && make_map(&tt->mMn, h->proj, dm.d, dm.d, (int)dm.n_relations, dm.d, 32,
-                        CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    const int nnb = (tt->N + 31) / 32;
+    ok = ok && make_map4c(&tt->mMn, h->proj, dm.d, dm.d, (int)dm.n_relations, dm.d, 32, nnb,
+                          CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     ok = ok && make_map(&tt->mdQ, h->tr_buf.dQ, dm.d, dm.k, dm.B, dm.d, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-    ok = ok && make_map(&tt->mdQn, h->tr_buf.dQ, dm.d, dm.k, dm.B, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    ok = ok && make_map(&tt->mXn, h->buf.X, dm.d, dm.C * dm.k, 1, dm.dp, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    ok = ok && make_map4c(&tt->mdQn, h->tr_buf.dQ, dm.d, dm.k, dm.B, dm.d, 32, 4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    ok = ok && make_map4c(&tt->mXn, h->buf.X, dm.d, dm.C * dm.k, 1, dm.dp, 32, nnb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const int urows = 2 * dm.B + 32 * dm.B;  // the padded U / H layout (k_tr_groups)
-    ok = ok && make_map(&tt->mUn, h->tr_buf.U, dm.d, urows, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    ok = ok && make_map(&tt->mHn, h->tr_buf.H, dm.d, urows, 1, dm.d, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    ok = ok && make_map4c(&tt->mUn, h->tr_buf.U, dm.d, urows, 1, dm.d, 32, 4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    ok = ok && make_map4c(&tt->mHn, h->tr_buf.H, dm.d, urows, 1, dm.d, 32, nnb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const size_t smem = tr_tc_smem(tt->N);
     ok = ok && cudaFuncSetAttribute(k_tr_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
     ok = ok && cudaFuncSetAttribute(k_tr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;

@@ -1,7 +1,7 @@
 # TransR iteration: tests (-k transr), bench line, launch list
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-if [ -z "$NOTEST" ]; then timeout 900 python -m pytest tests -q -m gpu -k "transr" -x -rfE > gpurun_out/pt.txt 2>&1; fi
+if [ -z "$NOTEST" ]; then timeout 900 python -m pytest tests -q -m gpu -k "transr or rescal" -x -rfE > gpurun_out/pt.txt 2>&1; fi
 python bench.py --workload fb15k_transr --steps 300 --warmup 20 --no-cpu-baseline --e2e-steps 50 > gpurun_out/b.txt 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 40 --csv --log-file gpurun_out/tr_launches.csv python bench.py --workload fb15k_transr --steps 10 --warmup 5 --no-cpu-baseline --e2e-steps 5 > /dev/null 2>&1
 python - <<'PY'

@@ -6,7 +6,10 @@ import numpy as np, torch
 import synth
 from paper_2004_08532_b200 import kge
 wl = sys.argv[1] if len(sys.argv) > 1 else "freebase"
-gr = synth.graph(wl)
+ov = {}
+if os.environ.get("KGE_TRACE_NE"):  # experiments: a smaller entity table (and triple list) of the same shape
+    ov = dict(n_entities=int(os.environ["KGE_TRACE_NE"]), n_triples=int(os.environ.get("KGE_TRACE_NT", 20_000_000)))
+gr = synth.graph(wl, **ov)
 trip = gr.triples()
 cfg = kge.Config(model="transe_l2", n_entities=gr.n_entities, n_relations=gr.n_relations, dim=400, batch_size=1024,
                  chunk_size=256, neg_k=256, neg_precision="tf32")
