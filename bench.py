@@ -325,9 +325,28 @@ def main():
     tc_peak = bf16_tf if path == "bf16" else (tf32_peak / 3 if path == "3xtf32" else tf32_peak)
     flops_neg = 2.0 * B * k * d  # one contraction of the chunked negatives (S = O X'^T)
     traffic = ncu_traffic()
+    if model == "transr":
+        # TransR: per group (relation, chunk) the chunk's k negatives are projected by M_r
+        # (QX = X' M^T, k d^2 MACs), their gradients projected back (P = dQ M) and the dM_r contraction (dQ^T X');
+        # G = the step's distinct (relation, chunk) pairs. The brackets: k_neg_fwd = projection + scores, k_neg_bwd =
+        # back-projection + group reduction, k_chain = chain rule, positive back-projections and dM_r (+ U^T H)
+        inv_rel = np.asarray(s["inv_rel"])
+        n_grp = len(set(zip(inv_rel.tolist(), (np.arange(B) // g).tolist())))
+        tr_flops = {"k_neg_fwd": 2.0 * n_grp * k * d * d + 3.0 * B * k * d,
+                    "k_neg_bwd": 2.0 * n_grp * k * d * d,
+                    "k_chain": 2.0 * n_grp * k * d * d + 2.0 * (2 * B) * d * d * 2}
 
     def kernel_roof(name, ms):
-        if name in ("k_update", "k_gather"):
+        if model == "transr" and name in ("k_neg_fwd", "k_neg_bwd", "k_chain"):
+            fl = tr_flops[name]
+            peak = tf32_peak if tc else alu_peak
+            ach = fl / (ms / 1000.0) / 1e12
+            r = {"bound": "tensor" if tc else "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                 "frac": ach / peak, "alg_flops_per_launch": fl, "groups": n_grp,
+                 "peak_note": f"tf32 = (1.1/2.25) x {src} bf16 burst" if tc else "148 SM x 128 FP32 lanes x FMA x 1.965 GHz",
+                 "impl": {"k_neg_fwd": "k_tr_tc<0> + k_tr_score", "k_neg_bwd": "k_tr_tc<1> + k_tr_reduce",
+                          "k_chain": "k_tr_chain + k_tr_mv<1> + k_tr_dm_tc"}[name]}
+        elif name in ("k_update", "k_gather"):
             alg = algorithmic_bytes(n_ue, n_ur, d, drel) if name == "k_update" else (n_ue * d * 4 + n_ur * drel * 4)
             ach = alg / (ms / 1000.0) / 1e9
             r = {"bound": "hbm", "achieved": ach, "peak": hbm_gbs, "unit": "GB/s", "frac": ach / hbm_gbs,

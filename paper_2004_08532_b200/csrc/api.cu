@@ -450,7 +450,9 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     if (e != cudaSuccess) return fail(cuda_fail(e, "projection init"));
     TrBuffers& T = h->tr_buf;
     const size_t B = dm.B;
-    int32_t* ib = (int32_t*)dalloc(h, (1 + 4 * B + (B + 1) + (dm.C + 1) + B + (B + 1) + 1 + 2 * (B + B / 8 + 1)) * 4);
+    const size_t njt = (size_t)tr_jtiles(dm.k), nsi = B + B / kTrSlice + 1;
+    int32_t* ib = (int32_t*)dalloc(h, (1 + 4 * B + (B + 1) + (dm.C + 1) + B + (B + 1) + 1 + 2 * (B + B / 8 + 1) + 1 +
+                                       2 * nsi + B + B * njt + B) * 4);
     const bool tr = cfg->model == KGE_TRANSR;  // RESCAL needs only dM and the U / V (H) factor rows
     T.QX = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 : 4);
     T.dQ = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 + 256 : 4);
@@ -473,6 +475,17 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     T.n_items = ib; ib += 1;
     T.item_u = ib; ib += B + B / 8 + 1;
     T.item_p = ib; ib += B + B / 8 + 1;
+    T.n_sitems = ib; ib += 1;
+    T.sitem_g = ib; ib += nsi;
+    T.sitem_p = ib; ib += nsi;
+    T.ms_off = ib; ib += B;
+    T.scnt = ib; ib += B * njt;
+    T.rel_order = ib; ib += B;
+    T.dQs = (float*)dalloc(h, tr ? (2 * B / kTrSlice + 2) * dm.k * dm.d * 4 : 4);
+    if (!T.dQs || cudaMemsetAsync(T.scnt, 0, B * njt * 4, h->stream) != cudaSuccess) {
+      set_error("out of device memory (TransR)");
+      return fail(KGE_ENOMEM);
+    }
     if (cudaMemsetAsync(T.U, 0, urows * dm.d * 4, h->stream) != cudaSuccess ||
         cudaMemsetAsync(T.H, 0, urows * dm.d * 4, h->stream) != cudaSuccess)
       return fail(cuda_fail(cudaGetLastError(), "TransR scratch"));
@@ -598,7 +611,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   b.lpos = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pstat = (float*)dalloc(h, (size_t)dm.B * 4);
   b.pcnt = (int32_t*)dalloc(h, (size_t)dm.B * 4);
-  const int64_t tr_parts = cfg->model == KGE_TRANSR ? (int64_t)dm.B * tr_jtiles(dm.k) : 0;
+  const int64_t tr_parts = cfg->model == KGE_TRANSR ? (int64_t)(dm.B + dm.B / kTrSlice + 1) * tr_jtiles(dm.k) : 0;
   b.lneg = (float*)dalloc(h, (size_t)std::max<int64_t>(std::max<int64_t>(std::max<int64_t>(h->n_neg_parts, tc_parts),
                                                                          tr_parts), dm.B) * 4);
   b.flow = (uint32_t*)dalloc(h, (size_t)2 * dm.C * 4);
@@ -665,7 +678,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
   }
   if (sample_init() != cudaSuccess || step_preload() != cudaSuccess || dist_preload() != cudaSuccess)
     return fail(cuda_fail(cudaGetLastError(), "kernel preload"));
-  if (cfg->model == KGE_TRANSR) h->n_neg_parts = dm.B * tr_jtiles(dm.k);  // per (group, tile of 32 negatives)
+  if (cfg->model == KGE_TRANSR)  // per (score item, tile of 32 negatives)
+    h->n_neg_parts = (dm.B + dm.B / kTrSlice + 1) * tr_jtiles(dm.k);
   if (cfg->neg_precision != KGE_PREC_FP32 && cfg->model != KGE_TRANSR) tc_init(h);
   if (cfg->model == KGE_TRANSR) transr_tc_init(h);  // DistMult / ComplEx / TransE-L2 on tcgen05
   if (tc_supported(h)) h->n_neg_parts = tc_neg_parts(h);

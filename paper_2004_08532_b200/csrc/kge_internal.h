@@ -144,10 +144,18 @@ struct TrBuffers {
   int32_t* n_items;   // [1] k_tr_mv work items: runs of <= 8 positions of one relation
   int32_t* item_u;    // [B + B/8 + 1] unique relation of item
   int32_t* item_p;    // [B + B/8 + 1] first relation-sorted position of item
+  int32_t* n_sitems;  // [1] k_tr_score work items: slices of <= kTrSlice positions of one group
+  int32_t* sitem_g;   // [B + B/kTrSlice + 1] group of item
+  int32_t* sitem_p;   // [B + B/kTrSlice + 1] first relation-sorted position of item
+  int32_t* ms_off;    // [B] groups with several slices: first slot of their dQ partials in dQs, else -1
+  int32_t* scnt;      // [B x k/32] arrival counters per (group, tile) of the multi-slice groups (reset by the last)
+  float* dQs;         // [(2 B / kTrSlice + 2) x k x d] per-slice dQ partials of the multi-slice groups
+  int32_t* rel_order;  // [B] unique relations by descending group count (k_tr_dm_tc: the longest CTAs start first)
   float* dOp;         // [kTrJt-tiles x B x d] dO partials of k_tr_score, one per tile of 32 negatives (summed in tile
                       // order by k_tr_chain)
 };
-constexpr int kTrJt = 32;  // negatives per k_tr_score CTA
+constexpr int kTrJt = 32;     // negatives per k_tr_score CTA
+constexpr int kTrSlice = 16;  // positives per k_tr_score CTA (a group with more is cut into slices)
 __host__ __device__ inline int tr_jtiles(int k) { return (k + kTrJt - 1) / kTrJt; }
 
 // multi-rank state (dist.cu)

@@ -1331,22 +1331,28 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
     __threadfence();
     if (lane == 0) *cnt = 0;  // ready for the next step
     acc.zero();
-    constexpr int UNR2 = V >= 4 ? 1 : 4;
-    for (int q0 = 0; q0 < nseg; q0 += UNR2) {  // segment sums, in segment order
-      float4 x[UNR2][V];
+    constexpr int UNR2 = V >= 4 ? 2 : 4;
+    for (int b0 = 0; b0 < nseg; b0 += 32) {
+      // the home rows of up to 32 segments in one round trip (lane q: segment b0 + q), then the sums in segment order
+      const int hq = b0 + lane < nseg ? occ_sorted[r0 + (b0 + lane) * kSeg] : 0;
+      const int nq = min(32, nseg - b0);
+      for (int q0 = 0; q0 < nq; q0 += UNR2) {
+        float4 x[UNR2][V];
 #pragma unroll
-      for (int q = 0; q < UNR2; ++q) {
-        const float* src = q0 + q < nseg ? G + (int64_t)occ_sorted[r0 + (q0 + q) * kSeg] * w : nullptr;
+        for (int q = 0; q < UNR2; ++q) {
+          const int hrow = __shfl_sync(0xffffffffu, hq, (q0 + q) & 31);
+          const float* src = q0 + q < nq ? G + (int64_t)hrow * w : nullptr;
 #pragma unroll
-        for (int m = 0; m < V; ++m) {
-          const int v = lane + 32 * m;
-          x[q][m] = (src && v < w4) ? __ldcg(reinterpret_cast<const float4*>(src) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int m = 0; m < V; ++m) {
+            const int v = lane + 32 * m;
+            x[q][m] = (src && v < w4) ? __ldcg(reinterpret_cast<const float4*>(src) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
         }
+#pragma unroll
+        for (int q = 0; q < UNR2; ++q)
+#pragma unroll
+          for (int m = 0; m < V; ++m) acc.add(x[q][m], m);
       }
-#pragma unroll
-      for (int q = 0; q < UNR2; ++q)
-#pragma unroll
-        for (int m = 0; m < V; ++m) acc.add(x[q][m], m);
     }
   }
   if (plain_sum) {

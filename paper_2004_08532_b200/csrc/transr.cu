@@ -144,6 +144,40 @@ __global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
       T.item_p[io] = a.s.rel_off[u] + 8 * q;
     }
   if (tid == 0) *T.n_items = s_total;
+  // k_tr_score work items: each group's positions cut into slices of kTrSlice (a hub group is spread over many CTAs);
+  // the slices of a group with several get consecutive slots for their dQ partials
+  __syncthreads();
+  auto nsl = [&](int q) { return (T.grp_p1[q] - T.grp_p0[q] + kTrSlice - 1) / kTrSlice; };
+  int tot_s = 0, tot_m = 0;
+  for (int q = g0; q < g1; ++q) {
+    tot_s += nsl(q);
+    tot_m += nsl(q) > 1 ? nsl(q) : 0;
+  }
+  int so = scan(tot_s);
+  const int n_s = s_total;
+  int mo = scan(tot_m);
+  for (int q = g0; q < g1; ++q) {
+    const int ns = nsl(q);
+    T.ms_off[q] = ns > 1 ? mo : -1;
+    if (ns > 1) mo += ns;
+    for (int t = 0; t < ns; ++t, ++so) {
+      T.sitem_g[so] = q;
+      T.sitem_p[so] = T.grp_p0[q] + t * kTrSlice;
+    }
+  }
+  if (tid == 0) *T.n_sitems = n_s;
+  // k_tr_dm_tc order: unique relations by descending group count (<= C; stable), so the CTAs with the most k-blocks
+  // start in the first wave instead of forming the kernel's tail
+  int rbase = 0;
+  for (int ng = dm.C; ng >= 1; --ng) {
+    int cc = 0;
+    for (int u = u0; u < u1; ++u) cc += T.rg_off[u + 1] - T.rg_off[u] == ng;
+    int pos = scan(cc);
+    const int tot = s_total;
+    for (int u = u0; u < u1; ++u)
+      if (T.rg_off[u + 1] - T.rg_off[u] == ng) T.rel_order[rbase + pos++] = u;
+    rbase += tot;
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -158,7 +192,15 @@ __global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
 // part q = tid % 8): partial sums over kk = q, q + 8, ..., added over the 8 lanes of x by a butterfly (every lane gets
 // the same bits; fixed order).
 // ------------------------------------------------------------------------------------------------
-static size_t tr_mv_smem(int d) { return (size_t)(32 * (d + 1) + 16 * d) * sizeof(float); }
+static size_t tr_mv_smem(int d) { return (size_t)2 * (32 * (d + 1) + 16 * d) * sizeof(float); }
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int BWD>
 __global__ void __launch_bounds__(256) k_tr_mv(TrArgs a) {
@@ -167,83 +209,107 @@ __global__ void __launch_bounds__(256) k_tr_mv(TrArgs a) {
   const Dims& dm = a.dm;
   extern __shared__ float sm[];
   const int d = dm.d, lda = d + 1, x0 = blockIdx.x * 32;
-  float* slab = sm;             // [32][d + 1]
-  float* vec = sm + 32 * lda;   // [16][d]
-  const int tid = threadIdx.x, x = tid >> 3, q = tid & 7;
+  const int buf_floats = 32 * lda + 16 * d;  // per buffer: slab [32][d + 1], then vectors [16][d]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_items = *a.t.n_items;
+  // items it = blockIdx.y, + gridDim.y, ... through two shared-memory buffers: the cp.async copies of item i + 1 are
+  // in flight while item i is computed (zero-filled where out of range; warp w: slab rows / vectors w, w + 8, ...,
+  // lanes along the contiguous dimension)
+  auto stage = [&](int it, float* buf) {
+    const int u = a.t.item_u[it], pb = a.t.item_p[it];
+    const int pr0 = a.s.rel_off[u], np = min(8, a.s.rel_off[u + 1] - pb);
+    const float* M = a.proj + (int64_t)a.s.rel_uniq[u] * d * d;
+    float* slab = buf;
+    float* vec = buf + 32 * lda;
+    if (BWD) {  // slab[xx][kk] = M[kk][x0 + xx]
+      const bool ok = x0 + lane < d;
+      for (int kk = warp; kk < d; kk += 8) cp_async4(slab + lane * lda + kk, M + (int64_t)kk * d + (ok ? x0 + lane : 0), ok);
+    } else {  // slab[xx][kk] = M[x0 + xx][kk]
+      for (int xx = warp; xx < 32; xx += 8) {
+        const bool ok = x0 + xx < d;
+        const float* row = M + (int64_t)(ok ? x0 + xx : 0) * d;
+        for (int kk = lane; kk < d; kk += 32) cp_async4(slab + xx * lda + kk, row + kk, ok);
+      }
+    }
+    const int p = pb + warp;  // vectors 2 warp, 2 warp + 1 (BWD: the gMh / gMt rows of U; else h / t)
+    const bool ok = warp < np;
+    const float* src0 = M;
+    const float* src1 = M;
+    if (ok) {
+      if (BWD) {
+        src0 = a.t.U + (a.t.pad_off[u] + 2 * (int64_t)(p - pr0)) * d;
+        src1 = src0 + d;
+      } else {
+        const int i = a.s.rel_occ[p];
+        src0 = a.ent.row(a.s.ph[i]);
+        src1 = a.ent.row(a.s.pt[i]);
+      }
+    }
+    for (int kk = lane; kk < d; kk += 32) {
+      cp_async4(vec + (2 * warp) * d + kk, src0 + (ok ? kk : 0), ok);
+      cp_async4(vec + (2 * warp + 1) * d + kk, src1 + (ok ? kk : 0), ok);
+    }
+  };
+  int cur = 0;
+  if ((int)blockIdx.y < n_items) stage(blockIdx.y, sm);
+  cp_async_commit();
   for (int it = blockIdx.y; it < n_items; it += gridDim.y) {
+    const int nit = it + gridDim.y;
+    if (nit < n_items) stage(nit, sm + (cur ^ 1) * buf_floats);
+    cp_async_commit();
+    cp_async_wait<1>();  // this item's copies landed (the next item's may still be in flight)
+    __syncthreads();
+    const float* slab = sm + cur * buf_floats;
+    const float* vec = slab + 32 * lda;
     const int u = a.t.item_u[it], pb = a.t.item_p[it];
     const int pr0 = a.s.rel_off[u], np = min(8, a.s.rel_off[u + 1] - pb);
     const int64_t ubase = a.t.pad_off[u];
-    const float* M = a.proj + (int64_t)a.s.rel_uniq[u] * d * d;
-    __syncthreads();  // the previous item's slab and vectors are consumed
-    // staged loads: 8 independent global loads in flight per thread before their shared-memory stores
-    constexpr int kLd = 8;
-    for (int e0 = tid; e0 < 32 * d; e0 += kLd * 256) {
-      float t[kLd];
+    // warp w: outputs x = w + 8 xi (xi < 4) of all 16 vectors, lane = K part (kk = lane, lane + 32, ...): 4 slab and
+    // 16 vector loads per 64 FMAs; then a reduce-scatter butterfly over the 32 lanes (each level hands half of the
+    // values to the partner, the lane with bit o set keeping the upper half: 62 shuffles) leaves lane l with the
+    // complete sums of outputs j + 2 l, j < 2 -- a fixed association, so the result is deterministic
+    float acc[64];
 #pragma unroll
-      for (int l = 0; l < kLd; ++l) {
-        const int e = e0 + l * 256, xx = BWD ? e & 31 : e / d, kk = BWD ? e >> 5 : e - (e / d) * d;
-        t[l] = e < 32 * d && x0 + xx < d ? (BWD ? __ldg(M + (int64_t)kk * d + x0 + xx) : __ldg(M + (int64_t)(x0 + xx) * d + kk))
-                                         : 0.f;
-      }
+    for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+    for (int kk = lane; kk < d; kk += 32) {
+      float m[4];
 #pragma unroll
-      for (int l = 0; l < kLd; ++l) {
-        const int e = e0 + l * 256, xx = BWD ? e & 31 : e / d, kk = BWD ? e >> 5 : e - (e / d) * d;
-        if (e < 32 * d) slab[xx * lda + kk] = t[l];
-      }
-    }
-    for (int e0 = tid; e0 < 16 * d; e0 += kLd * 256) {
-      float t[kLd];
-#pragma unroll
-      for (int l = 0; l < kLd; ++l) {
-        const int e = e0 + l * 256, v = e / d, kk = e - v * d, pp = v >> 1;
-        float val = 0.f;
-        if (e < 16 * d && pp < np) {
-          const int p = pb + pp;
-          if (BWD) {
-            val = a.t.U[(ubase + 2 * (p - pr0) + (v & 1)) * d + kk];
-          } else {
-            const int i = a.s.rel_occ[p];
-            val = a.ent.row((v & 1) ? a.s.pt[i] : a.s.ph[i])[kk];
-          }
-        }
-        t[l] = val;
-      }
-#pragma unroll
-      for (int l = 0; l < kLd; ++l)
-        if (e0 + l * 256 < 16 * d) vec[e0 + l * 256] = t[l];
-    }
-    __syncthreads();
-    float acc[16];
-#pragma unroll
-    for (int v = 0; v < 16; ++v) acc[v] = 0.f;
-    const float* sr = slab + x * lda;
-    for (int kk = q; kk < d; kk += 8) {
-      const float m = sr[kk];
-#pragma unroll
-      for (int v = 0; v < 16; ++v) acc[v] = fmaf(m, vec[v * d + kk], acc[v]);
-    }
-#pragma unroll
-    for (int v = 0; v < 16; ++v) {
-      acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 1);
-      acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 2);
-      acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], 4);
-    }
-    if (x0 + x < d) {
+      for (int xi = 0; xi < 4; ++xi) m[xi] = slab[(warp + 8 * xi) * lda + kk];
 #pragma unroll
       for (int v = 0; v < 16; ++v) {
-        if ((v & 7) != q || (v >> 1) >= np) continue;  // lane q stores vectors q and q + 8
-        const int p = pb + (v >> 1);
-        if (BWD) {
-          const int i = a.s.rel_occ[p];
-          a.b.Gocc[((int64_t)((v & 1) ? dm.B + i : i)) * d + x0 + x] = acc[v];
-        } else {
-          a.t.U[(ubase + 2 * (p - pr0) + (v & 1)) * d + x0 + x] = acc[v];
-        }
+        const float vv = vec[v * d + kk];
+#pragma unroll
+        for (int xi = 0; xi < 4; ++xi) acc[xi * 16 + v] = fmaf(m[xi], vv, acc[xi * 16 + v]);
       }
     }
+#pragma unroll
+    for (int lv = 0; lv < 5; ++lv) {
+      const int o = 16 >> lv, half = 32 >> lv;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const float give = up ? acc[j] : acc[j + half];
+        const float keep = up ? acc[j + half] : acc[j];
+        acc[j] = keep + __shfl_xor_sync(0xffffffffu, give, o);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int idx = j + 2 * lane, xi = idx >> 4, v = idx & 15;
+      const int xx = warp + 8 * xi;
+      if (x0 + xx >= d || (v >> 1) >= np) continue;
+      const int p = pb + (v >> 1);
+      if (BWD) {
+        const int i = a.s.rel_occ[p];
+        a.b.Gocc[((int64_t)((v & 1) ? dm.B + i : i)) * d + x0 + xx] = acc[j];
+      } else {
+        a.t.U[(ubase + 2 * (p - pr0) + (v & 1)) * d + x0 + xx] = acc[j];
+      }
+    }
+    __syncthreads();  // buffer cur is consumed before the copies of item it + 2 gridDim.y land in it
+    cur ^= 1;
   }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -411,7 +477,7 @@ __device__ __forceinline__ uint64_t sdesc_mn32(uint32_t saddr, uint32_t lbo) {
 // MODE 0: QX_g = X'_c M_u^T (k_tr_gemm<0>); MODE 1: P_g = dQ_g M_u (k_tr_gemm<1>), both into T.QX + g k d
 template <int MODE>
 __global__ void __launch_bounds__(128, 1)
-    k_tr_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, TrArgs a, int N) {
+    k_tr_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, TrArgs a, int N, int chunk) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kTrStages], empty[kTrStages], done;
@@ -424,8 +490,12 @@ __global__ void __launch_bounds__(128, 1)
   // MODE 0: blockIdx.y = group. MODE 1: blockIdx.y = chunk c, blockIdx.z = slice of the chunk's group list: the
   // slice's P_g = dQ_g M_u are accumulated in TMEM (one partial sum per slice, k_tr_reduce adds the slices in order)
   int grp = blockIdx.y, l0 = 0, nsteps = nkb;
-  if (MODE == 0) {
+  if (MODE == 0 && chunk < 0) {  // blockIdx.y = group, QX slot = group
     if (grp >= *T.n_groups) return;  // uniform per CTA, before any barrier / TMEM use
+  } else if (MODE == 0) {  // one chunk: blockIdx.y = the chunk's y-th group, QX slot y
+    const int gb = T.cg_off[chunk];
+    if ((int)blockIdx.y >= T.cg_off[chunk + 1] - gb) return;
+    grp = T.cg_list[gb + blockIdx.y];
   } else {
     const int c = blockIdx.y, S = gridDim.z, z = blockIdx.z;
     const int gb = T.cg_off[c], ng = T.cg_off[c + 1] - gb;
@@ -497,7 +567,7 @@ __global__ void __launch_bounds__(128, 1)
   // epilogue: thread <-> row m0 + 32 warp + lane, stored to row pitch d (MODE 0: QX_g; MODE 1: the slice's partial
   // sum, slot (z C + c) of the same buffer)
   const int row = m0 + warp * 32 + lane;
-  const int64_t slot = MODE == 0 ? grp : (int64_t)blockIdx.z * dm.C + blockIdx.y;
+  const int64_t slot = MODE == 0 ? (int64_t)blockIdx.y : (int64_t)blockIdx.z * dm.C + blockIdx.y;  // = grp if chunk < 0
   float* out = T.QX + slot * k * d + (int64_t)row * d;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   for (int cb = 0; cb * 32 < d; ++cb) {
@@ -537,10 +607,18 @@ __global__ void __launch_bounds__(128, 1)
   __shared__ uint32_t tbase;
   const Dims& dm = a.dm;
   const TrBuffers& T = a.t;
-  const int u = blockIdx.y;
-  if (u >= *a.s.rel_n) return;  // uniform per CTA
+  if ((int)blockIdx.y >= *a.s.rel_n) return;  // uniform per CTA
+  const int u = T.rel_order[blockIdx.y];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = dm.d, k = dm.k, m0 = blockIdx.x * 128;
+  {  // warm L2 with this CTA's rows of M_u for the fused Adagrad epilogue (HBM latency off its critical path)
+    const float* Mu = a.proj + (int64_t)a.s.rel_uniq[u] * d * d;
+    const int lines = (d + 31) / 32;
+    for (int l = threadIdx.x; l < 128 * lines; l += blockDim.x) {
+      const int rr = m0 + l / lines, cb = l - (l / lines) * lines;
+      if (rr < d) asm volatile("prefetch.global.L2 [%0];" ::"l"(Mu + (int64_t)rr * d + 32 * cb));
+    }
+  }
   const int g0 = T.rg_off[u], g1 = T.rg_off[u + 1];
   const int nkg = (k + 31) / 32, nnb = (N + 31) / 32;
   const int nkq = (g1 - g0) * nkg;  // k-blocks over all groups of the relation, then over its padded U / H rows
@@ -696,23 +774,25 @@ static size_t tr_tc_smem(int N) { return (size_t)kTrStages * (128 * 128 + (size_
 // holding most of a chunk) is spread over k / 32 CTAs instead of one.
 // ------------------------------------------------------------------------------------------------
 template <int V>
-__global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
+__global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk) {
   pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
   pdl_trigger();
   constexpr int RB = 4 / V;  // positives per block (registers: (2 JU + 2 RB) V float4 per lane)
   constexpr int JU = kTrJt / 8;  // negatives per warp
   const Dims& dm = a.dm;
   const TrBuffers& T = a.t;
-  const int grp = blockIdx.y, jt = blockIdx.x, njt = gridDim.x;
+  // launched per chunk (after k_tr_tc<0> of the chunk): blockIdx.y = the chunk's y-th group, its QX in slot y
+  const int jt = blockIdx.x, njt = gridDim.x;
   __shared__ float red[8];
   __shared__ float4 sdo4[8][RB][32 * V];  // per-warp dO partials of a block of positives
-  if (grp >= *T.n_groups) {
-    if (threadIdx.x == 0) a.b.lneg[(int64_t)grp * njt + jt] = 0.f;
-    return;
-  }
+  // blockIdx.y = work item (k_tr_groups): slice [pa, pb) of <= kTrSlice positions of group grp
+  (void)chunk;
+  const int item = blockIdx.y;
+  if (item >= *T.n_sitems) return;
+  const int grp = T.sitem_g[item];
   const int d = dm.d, d4 = d >> 2, k = dm.k;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p0 = T.grp_p0[grp], p1 = T.grp_p1[grp];
+  const int p0 = T.sitem_p[item], p1 = min(p0 + kTrSlice, T.grp_p1[grp]);
   const float4* QX = reinterpret_cast<const float4*>(T.QX + (int64_t)grp * k * d);
   float4* dQ = reinterpret_cast<float4*>(T.dQ + (int64_t)grp * k * d);
   const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
@@ -814,21 +894,58 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a) {
     }
     __syncthreads();
   }
+  // dQ_g rows of this tile: a group of one slice stores them; the slices of a larger group park their partials in
+  // dQs, and the last to arrive (integer counter per (group, tile)) adds them in slice order and stores dQ_g
+  const int ms = T.ms_off[grp];
+  const int sl = (p0 - T.grp_p0[grp]) / kTrSlice;
+  float4* dst = ms < 0 ? dQ : reinterpret_cast<float4*>(T.dQs + (int64_t)(ms + sl) * k * d);
 #pragma unroll
   for (int u = 0; u < JU; ++u) {
     const int j = jt * kTrJt + warp + 8 * u;
     if (j < k)
 #pragma unroll
       for (int m = 0; m < V; ++m)
-        if (lane + 32 * m < d4) dQ[(int64_t)j * d4 + lane + 32 * m] = dq[u][m];
+        if (lane + 32 * m < d4) dst[(int64_t)j * d4 + lane + 32 * m] = dq[u][m];
   }
   lsum = warp_sum(lsum);
   if (lane == 0) red[warp] = lsum;
+  __shared__ int s_last;
+  if (ms >= 0) __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     float t = 0.f;
     for (int w = 0; w < 8; ++w) t += red[w];
-    a.b.lneg[(int64_t)grp * njt + jt] = t;
+    a.b.lneg[(int64_t)item * njt + jt] = t;
+    if (ms >= 0) {
+      const int ns = (T.grp_p1[grp] - T.grp_p0[grp] + kTrSlice - 1) / kTrSlice;
+      int* cnt = T.scnt + (int64_t)grp * njt + jt;
+      s_last = atomicAdd(cnt, 1) == ns - 1;
+      if (s_last) *cnt = 0;  // ready for the next step
+    }
+  }
+  __syncthreads();
+  if (ms >= 0 && s_last) {
+    __threadfence();
+    const int ns = (T.grp_p1[grp] - T.grp_p0[grp] + kTrSlice - 1) / kTrSlice;
+#pragma unroll
+    for (int u = 0; u < JU; ++u) {
+      const int j = jt * kTrJt + warp + 8 * u;
+      if (j >= k) continue;
+#pragma unroll
+      for (int m = 0; m < V; ++m) {
+        const int c = lane + 32 * m;
+        if (c >= d4) continue;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < ns; ++q) {  // slice order
+          const float4 y = __ldcg(reinterpret_cast<const float4*>(T.dQs + (int64_t)(ms + q) * k * d) + (int64_t)j * d4 + c);
+          acc.x += y.x;
+          acc.y += y.y;
+          acc.z += y.z;
+          acc.w += y.w;
+        }
+        dQ[(int64_t)j * d4 + c] = acc;
+      }
+    }
   }
 }
 
@@ -869,7 +986,8 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
     if (threadIdx.x < 32) {
       float sp = 0.f, sn = 0.f;
       for (int i = lane; i < dm.B; i += 32) sp += a.b.lpos[i];
-      for (int q = lane; q < a.n_neg_parts; q += 32) sn += a.b.lneg[q];
+      const int nparts = *a.t.n_sitems * tr_jtiles(dm.k);  // per (score item, tile of 32 negatives), k_tr_score
+      for (int q = lane; q < nparts; q += 32) sn += a.b.lneg[q];
       sp = warp_sum(sp);
       sn = warp_sum(sn);
       if (lane == 0) {
@@ -987,27 +1105,34 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   e = launch_gather_neg(h, s);
   dbg(h, "gather_neg");
   if (e != cudaSuccess) return e;
-  // k_tr_mv: about one item (<= B / 8 + n_rel_u of them) per CTA
-  const dim3 gmv((dm.d + 31) / 32, dm.B / 8 + dm.B / 2 + 1);
+  // k_tr_mv: one wave (two CTAs per SM), each CTA walking its items with the next one's slab prefetched into L2
+  const dim3 gmv((dm.d + 31) / 32, std::max(1, 2 * 148 / ((dm.d + 31) / 32)));
   launch_pdl(k_tr_mv<0>, gmv, 256, tr_mv_smem(dm.d), h->stream, a); dbg(h, "k_tr_mv<0>");
   launch_pdl(k_tr_pos, dm.B, 256, 0, h->stream, a); dbg(h, "k_tr_pos");
   launch_end(h, KGE_K_GATHER);
   const dim3 gk((dm.d + GT - 1) / GT, (dm.k + GT - 1) / GT, dm.B);
   launch_begin(h, KGE_K_NEG_FWD);
+  auto score = [&](dim3 gs, int chunk) {
+    switch (tr_score_v(dm.d)) {
+      case 1: launch_pdl(k_tr_score<1>, gs, 256, 0, h->stream, a, chunk); break;
+      case 2: launch_pdl(k_tr_score<2>, gs, 256, 0, h->stream, a, chunk); break;
+      default: launch_pdl(k_tr_score<4>, gs, 256, 0, h->stream, a, chunk); break;
+    }
+  };
   if (h->tr_tc) {
+    // every group at once (chunk by chunk -- so a chunk's QX stays in L2 -- measured slower: the per-chunk score
+    // kernels each wait for their hub group's tail, 4 x 58 us vs 115 us)
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
-    launch_pdl(k_tr_tc<0>, dim3((dm.k + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream, tt->mX, tt->mM, a, tt->N);
+    launch_pdl(k_tr_tc<0>, dim3((dm.k + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream, tt->mX, tt->mM, a,
+               tt->N, -1);
     dbg(h, "k_tr_tc<0>");
+    score(dim3(tr_jtiles(dm.k), dm.B + dm.B / kTrSlice + 1), -1);
+    dbg(h, "k_tr_score");
   } else {
     launch_pdl(k_tr_gemm<0>, gk, 256, 0, h->stream, a); dbg(h, "k_tr_gemm<0>");
+    score(dim3(tr_jtiles(dm.k), dm.B + dm.B / kTrSlice + 1), -1);  // every group at once, QX slot = group
+    dbg(h, "k_tr_score");
   }
-  const dim3 gs(tr_jtiles(dm.k), dm.B);
-  switch (tr_score_v(dm.d)) {
-    case 1: launch_pdl(k_tr_score<1>, gs, 256, 0, h->stream, a); break;
-    case 2: launch_pdl(k_tr_score<2>, gs, 256, 0, h->stream, a); break;
-    default: launch_pdl(k_tr_score<4>, gs, 256, 0, h->stream, a); break;
-  }
-  dbg(h, "k_tr_score");
   launch_end(h, KGE_K_NEG_FWD);
   launch_begin(h, KGE_K_NEG_BWD);
   // k_tr_tc<1>: CTAs (tile of 128 negatives, chunk, slice of the chunk's groups), about two per SM; the slices' partial
@@ -1016,7 +1141,7 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   const int nslice = std::max(1, std::min(2 * 148 / (jt * dm.C), dm.B / dm.C));
   if (h->tr_tc) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
-    launch_pdl(k_tr_tc<1>, dim3(jt, dm.C, nslice), 128, tr_tc_smem(tt->N), h->stream, tt->mdQ, tt->mMn, a, tt->N);
+    launch_pdl(k_tr_tc<1>, dim3(jt, dm.C, nslice), 128, tr_tc_smem(tt->N), h->stream, tt->mdQ, tt->mMn, a, tt->N, 0);
     dbg(h, "k_tr_tc<1>");
   } else {
     launch_pdl(k_tr_gemm<1>, gk, 256, 0, h->stream, a); dbg(h, "k_tr_gemm<1>");

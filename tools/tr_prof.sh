@@ -8,3 +8,6 @@ for k in $(echo "${KRE:-k_tr_mv|k_tr_dm_tc}" | tr '|' ' '); do
   ncu -i gpurun_out/tr_full.ncu-rep -k regex:$k --page details --csv > gpurun_out/tr_details_$k.csv 2>/dev/null
 done
 echo done
+for k in $(echo "${KRE:-k_tr_mv|k_tr_dm_tc}" | tr '|' ' '); do
+  ncu -i gpurun_out/tr_full.ncu-rep -k regex:$k --page source --csv --print-source sass > gpurun_out/tr_src_$k.csv 2>/dev/null
+done
