@@ -107,8 +107,10 @@ typedef struct {
                               KGE_EUNSUPPORTED. */
   int32_t world_size;      /* P ranks (one process per GPU) */
   int32_t rank;            /* this rank */
-  void* nccl_comm;         /* ncclComm_t shared with the caller, or NULL */
-  const void* nccl_unique_id; /* 128-byte ncclUniqueId when nccl_comm == NULL and world_size > 1 */
+  void* nccl_comm;         /* reserved, ignored: the P > 1 exchange runs over CUDA-IPC peer memory inside the step
+                              kernels (handles from kge_export / kge_connect, rendezvous by the caller's process group;
+                              DESIGN.md §6 gives the bytes / latency argument against an NCCL all-to-all) */
+  const void* nccl_unique_id; /* reserved, ignored (as nccl_comm) */
   void* cuda_stream;       /* cudaStream_t to enqueue on, or NULL */
   void* (*dev_alloc)(size_t bytes, void* ctx); /* optional device allocator */
   void (*dev_free)(void* ptr, void* ctx);

@@ -264,47 +264,78 @@ __global__ void __launch_bounds__(256) k_tr_mv(TrArgs a) {
     const int u = a.t.item_u[it], pb = a.t.item_p[it];
     const int pr0 = a.s.rel_off[u], np = min(8, a.s.rel_off[u + 1] - pb);
     const int64_t ubase = a.t.pad_off[u];
-    // warp w: outputs x = w + 8 xi (xi < 4) of all 16 vectors, lane = K part (kk = lane, lane + 32, ...): 4 slab and
-    // 16 vector loads per 64 FMAs; then a reduce-scatter butterfly over the 32 lanes (each level hands half of the
-    // values to the partner, the lane with bit o set keeping the upper half: 62 shuffles) leaves lane l with the
-    // complete sums of outputs j + 2 l, j < 2 -- a fixed association, so the result is deterministic
-    float acc[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) acc[j] = 0.f;
-    for (int kk = lane; kk < d; kk += 32) {
-      float m[4];
-#pragma unroll
-      for (int xi = 0; xi < 4; ++xi) m[xi] = slab[(warp + 8 * xi) * lda + kk];
-#pragma unroll
-      for (int v = 0; v < 16; ++v) {
-        const float vv = vec[v * d + kk];
-#pragma unroll
-        for (int xi = 0; xi < 4; ++xi) acc[xi * 16 + v] = fmaf(m[xi], vv, acc[xi * 16 + v]);
-      }
-    }
-#pragma unroll
-    for (int lv = 0; lv < 5; ++lv) {
-      const int o = 16 >> lv, half = 32 >> lv;
-      const bool up = (lane & o) != 0;
-#pragma unroll
-      for (int j = 0; j < half; ++j) {
-        const float give = up ? acc[j] : acc[j + half];
-        const float keep = up ? acc[j + half] : acc[j];
-        acc[j] = keep + __shfl_xor_sync(0xffffffffu, give, o);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int idx = j + 2 * lane, xi = idx >> 4, v = idx & 15;
-      const int xx = warp + 8 * xi;
-      if (x0 + xx >= d || (v >> 1) >= np) continue;
+    // warp w: outputs x = w + 8 xi (xi < 4) of the item's NV vectors (NV = 4 when it has <= 2 positions -- most items
+    // -- else 16), lane = K part (kk = lane, lane + 32, ...): 4 slab and NV vector loads per 4 NV FMAs; then a
+    // reduce-scatter butterfly over the 32 lanes (each level hands half of the values to the partner, the lane with
+    // bit o set keeping the upper half) -- a fixed association, so the result is deterministic
+    auto store = [&](int idx, float val) {  // idx = xi * NV + v
+      const int nv = np <= 2 ? 4 : 16;
+      const int xi = idx / nv, v = idx - xi * nv, xx = warp + 8 * xi;
+      if (x0 + xx >= d || (v >> 1) >= np) return;
       const int p = pb + (v >> 1);
       if (BWD) {
         const int i = a.s.rel_occ[p];
-        a.b.Gocc[((int64_t)((v & 1) ? dm.B + i : i)) * d + x0 + xx] = acc[j];
+        a.b.Gocc[((int64_t)((v & 1) ? dm.B + i : i)) * d + x0 + xx] = val;
       } else {
-        a.t.U[(ubase + 2 * (p - pr0) + (v & 1)) * d + x0 + xx] = acc[j];
+        a.t.U[(ubase + 2 * (p - pr0) + (v & 1)) * d + x0 + xx] = val;
       }
+    };
+    if (np <= 2) {
+      float acc[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+      for (int kk = lane; kk < d; kk += 32) {
+        float m[4];
+#pragma unroll
+        for (int xi = 0; xi < 4; ++xi) m[xi] = slab[(warp + 8 * xi) * lda + kk];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const float vv = vec[v * d + kk];
+#pragma unroll
+          for (int xi = 0; xi < 4; ++xi) acc[xi * 4 + v] = fmaf(m[xi], vv, acc[xi * 4 + v]);
+        }
+      }
+#pragma unroll
+      for (int lv = 0; lv < 4; ++lv) {  // 16 values -> 1 per lane pair (lane l: output l >> 1)
+        const int o = 16 >> lv, half = 8 >> lv;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int j = 0; j < half; ++j) {
+          const float give = up ? acc[j] : acc[j + half];
+          const float keep = up ? acc[j + half] : acc[j];
+          acc[j] = keep + __shfl_xor_sync(0xffffffffu, give, o);
+        }
+      }
+      acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+      if ((lane & 1) == 0) store(lane >> 1, acc[0]);
+    } else {
+      float acc[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+      for (int kk = lane; kk < d; kk += 32) {
+        float m[4];
+#pragma unroll
+        for (int xi = 0; xi < 4; ++xi) m[xi] = slab[(warp + 8 * xi) * lda + kk];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) {
+          const float vv = vec[v * d + kk];
+#pragma unroll
+          for (int xi = 0; xi < 4; ++xi) acc[xi * 16 + v] = fmaf(m[xi], vv, acc[xi * 16 + v]);
+        }
+      }
+#pragma unroll
+      for (int lv = 0; lv < 5; ++lv) {  // 64 values -> 2 per lane (lane l: outputs 2 l, 2 l + 1)
+        const int o = 16 >> lv, half = 32 >> lv;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int j = 0; j < half; ++j) {
+          const float give = up ? acc[j] : acc[j + half];
+          const float keep = up ? acc[j + half] : acc[j];
+          acc[j] = keep + __shfl_xor_sync(0xffffffffu, give, o);
+        }
+      }
+      store(2 * lane, acc[0]);
+      store(2 * lane + 1, acc[1]);
     }
     __syncthreads();  // buffer cur is consumed before the copies of item it + 2 gridDim.y land in it
     cur ^= 1;
