@@ -213,7 +213,6 @@ struct GatherArgs {
   int32_t fuse_pos;   // TransE-L2 on the tcgen05 path: also write the positive-score gradient of the uncorrupted
                       // entity, gx = w+ (o - x) / ||o - x||, into its occurrence row of Gocc (read back by k_tc_bwd)
   uint32_t* flow;     // tcgen05 path: publish rows done per chunk (StepBuffers::flow), else nullptr
-  int32_t proxy_fence;  // experiment (KGE_GATHER_FENCE=1): fence.proxy.async.global at the end of every warp
 };
 
 // Register-staged rows: every lane issues all of its row loads before any arithmetic or store, so a warp has its whole
@@ -456,9 +455,6 @@ __global__ void __launch_bounds__(256) k_gather(GatherArgs a) {
     acc = warp_sum(acc);
     if (lane == 0) a.b.xnorm[q] = acc;
   }
-  // the rows written here are read by k_tc_fwd's TMA (async proxy): each warp makes its own stores visible to the
-  // async proxy as it finishes (experiment KGE_GATHER_FENCE; off by default)
-  if (a.proxy_fence) fence_proxy_async_global();
   if (dm.trace) __threadfence();  // diagnostics: the warp's stores performed before its end stamp
   trace_warp_end(dm.trace, KGE_K_GATHER);
   if (a.flow) {  // rows of each chunk done: k_tc_fwd starts a chunk as soon as its g + k rows are here
@@ -1436,7 +1432,7 @@ static void launch_gather_v(kge_handle* h, const GatherArgs& ga, int rows) {
 
 cudaError_t launch_gather_neg(kge_handle* h, const Slot& s) {
   const Dims& dm = h->dims;
-  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, dm.B, 0, nullptr, 0};
+  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, dm.B, 0, nullptr};
   const int rows = dm.C * dm.k;
   launch_gather_v(h, ga, rows);
   return cudaGetLastError();
@@ -1498,9 +1494,7 @@ cudaError_t launch_step(kge_handle* h, const Slot& s, int64_t step) {
   if (dm.model == KGE_TRANSR) return launch_transr_step(h, s, step);
   if (dm.model == KGE_RESCAL) return launch_rescal_step(h, s, step);
   const bool tc = tc_supported(h);
-  static const bool gfence = getenv("KGE_GATHER_FENCE") != nullptr;
-  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0, tc && tc_fuses_chain(h) ? 1 : 0, tc && tc_flow() ? h->buf.flow : nullptr,
-                tc && gfence ? 1 : 0};
+  GatherArgs ga{dm, s, h->rows, h->rel, h->buf, 0, tc && tc_fuses_chain(h) ? 1 : 0, tc && tc_flow() ? h->buf.flow : nullptr};
   const int rows = dm.B + dm.C * dm.k;
   launch_begin(h, KGE_K_GATHER);
   launch_gather_v(h, ga, rows);
