@@ -452,7 +452,7 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     const size_t B = dm.B;
     const size_t njt = (size_t)tr_jtiles(dm.k), nsi = B + B / kTrSlice + 1;
     int32_t* ib = (int32_t*)dalloc(h, (1 + 4 * B + (B + 1) + (dm.C + 1) + B + (B + 1) + 1 + 2 * (B + B / 8 + 1) + 1 +
-                                       2 * nsi + B + B * njt + B) * 4);
+                                       2 * nsi + B + B * njt + B + B + dm.C + 1) * 4);
     const bool tr = cfg->model == KGE_TRANSR;  // RESCAL needs only dM and the U / V (H) factor rows
     T.QX = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 : 4);
     T.dQ = (float*)dalloc(h, tr ? B * dm.k * dm.d * 4 + 256 : 4);
@@ -481,6 +481,8 @@ int kge_init(kge_handle** out, const kge_config* cfg, const int64_t* heads, cons
     T.ms_off = ib; ib += B;
     T.scnt = ib; ib += B * njt;
     T.rel_order = ib; ib += B;
+    T.grp_lc = ib; ib += B;
+    T.si_off = ib; ib += dm.C + 1;
     T.dQs = (float*)dalloc(h, tr ? (2 * B / kTrSlice + 2) * dm.k * dm.d * 4 : 4);
     if (!T.dQs || cudaMemsetAsync(T.scnt, 0, B * njt * 4, h->stream) != cudaSuccess) {
       set_error("out of device memory (TransR)");

@@ -151,6 +151,8 @@ struct TrBuffers {
   int32_t* scnt;      // [B x k/32] arrival counters per (group, tile) of the multi-slice groups (reset by the last)
   float* dQs;         // [(2 B / kTrSlice + 2) x k x d] per-slice dQ partials of the multi-slice groups
   int32_t* rel_order;  // [B] unique relations by descending group count (k_tr_dm_tc: the longest CTAs start first)
+  int32_t* grp_lc;     // [B] index of a group within its chunk's list
+  int32_t* si_off;     // [C + 1] score items of chunk c: [si_off[c], si_off[c + 1])
   float* dOp;         // [kTrJt-tiles x B x d] dO partials of k_tr_score, one per tile of 32 negatives (summed in tile
                       // order by k_tr_chain)
 };

@@ -113,7 +113,10 @@ __global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
     int pos = scan(cc);
     const int tot = s_total;
     for (int q = g0; q < g1; ++q)
-      if (T.grp_c[q] == c) T.cg_list[base + pos++] = q;
+      if (T.grp_c[q] == c) {
+        T.grp_lc[q] = pos;  // index of the group within its chunk (QX slot of the chunk-wise projections)
+        T.cg_list[base + pos++] = q;
+      }
     if (tid == 0) T.cg_off[c] = base;
     base += tot;
   }
@@ -146,18 +149,22 @@ __global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
   if (tid == 0) *T.n_items = s_total;
   // k_tr_score work items: each group's positions cut into slices of kTrSlice (a hub group is spread over many CTAs);
   // the slices of a group with several get consecutive slots for their dQ partials
+  // Items follow the chunk-ordered group list (cg_list), so each chunk's items are one range [si_off[c], si_off[c+1]).
   __syncthreads();
   auto nsl = [&](int q) { return (T.grp_p1[q] - T.grp_p0[q] + kTrSlice - 1) / kTrSlice; };
   int tot_s = 0, tot_m = 0;
-  for (int q = g0; q < g1; ++q) {
+  for (int l = g0; l < g1; ++l) {
+    const int q = T.cg_list[l];
     tot_s += nsl(q);
     tot_m += nsl(q) > 1 ? nsl(q) : 0;
   }
   int so = scan(tot_s);
   const int n_s = s_total;
   int mo = scan(tot_m);
-  for (int q = g0; q < g1; ++q) {
-    const int ns = nsl(q);
+  for (int l = g0; l < g1; ++l) {
+    const int q = T.cg_list[l], ns = nsl(q);
+    for (int c = 0; c < dm.C; ++c)
+      if (T.cg_off[c] == l) T.si_off[c] = so;  // (a chunk has >= 1 group, so every cg_off[c] < n_groups is hit)
     T.ms_off[q] = ns > 1 ? mo : -1;
     if (ns > 1) mo += ns;
     for (int t = 0; t < ns; ++t, ++so) {
@@ -165,7 +172,10 @@ __global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
       T.sitem_p[so] = T.grp_p0[q] + t * kTrSlice;
     }
   }
-  if (tid == 0) *T.n_sitems = n_s;
+  if (tid == 0) {
+    *T.n_sitems = n_s;
+    T.si_off[dm.C] = n_s;
+  }
   // k_tr_dm_tc order: unique relations by descending group count (<= C; stable), so the CTAs with the most k-blocks
   // start in the first wave instead of forming the kernel's tail
   int rbase = 0;
@@ -597,9 +607,12 @@ __global__ void __launch_bounds__(128, 1)
   }
   // epilogue: thread <-> row m0 + 32 warp + lane, stored to row pitch d (MODE 0: QX_g; MODE 1: the slice's partial
   // sum, slot (z C + c) of the same buffer)
-  const int row = m0 + warp * 32 + lane;
+  // Each warp's 32 x 32 chunk is transposed through shared memory (the pipeline stages are free once the MMAs
+  // completed) so that every row segment is written by one coalesced 128-byte warp store.
   const int64_t slot = MODE == 0 ? (int64_t)blockIdx.y : (int64_t)blockIdx.z * dm.C + blockIdx.y;  // = grp if chunk < 0
-  float* out = T.QX + slot * k * d + (int64_t)row * d;
+  float* outw = T.QX + slot * k * d + (int64_t)(m0 + warp * 32) * d;  // this warp's first row
+  const int nrow = min(32, k - (m0 + warp * 32));
+  float* tw = reinterpret_cast<float*>(smem) + warp * (32 * 33);
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   for (int cb = 0; cb * 32 < d; ++cb) {
     uint32_t p0[32];
@@ -610,16 +623,13 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
       for (int x = 0; x < 32; ++x) p0[x] = 0u;
     }
-    if (row < k) {
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const int col = cb * 32 + 4 * v;
-        if (col < d)
-          *reinterpret_cast<float4*>(out + col) =
-              make_float4(__uint_as_float(p0[4 * v]), __uint_as_float(p0[4 * v + 1]), __uint_as_float(p0[4 * v + 2]),
-                          __uint_as_float(p0[4 * v + 3]));
-      }
-    }
+    for (int x = 0; x < 32; ++x) tw[lane * 33 + x] = __uint_as_float(p0[x]);
+    __syncwarp();
+    const int col = cb * 32 + lane;
+    if (col < d)
+      for (int rr = 0; rr < nrow; ++rr) outw[(int64_t)rr * d + col] = tw[rr * 33 + lane];
+    __syncwarp();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -816,15 +826,17 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk) {
   const int jt = blockIdx.x, njt = gridDim.x;
   __shared__ float red[8];
   __shared__ float4 sdo4[8][RB][32 * V];  // per-warp dO partials of a block of positives
-  // blockIdx.y = work item (k_tr_groups): slice [pa, pb) of <= kTrSlice positions of group grp
-  (void)chunk;
-  const int item = blockIdx.y;
-  if (item >= *T.n_sitems) return;
+  // work item (k_tr_groups): a slice of <= kTrSlice positions of group grp. chunk < 0: blockIdx.y = item, QX slot =
+  // group; chunk >= 0 (launched per chunk after that chunk's projections): item si_off[chunk] + blockIdx.y, QX slot =
+  // the group's index within the chunk
+  const int item = chunk < 0 ? (int)blockIdx.y : T.si_off[chunk] + (int)blockIdx.y;
+  if (item >= (chunk < 0 ? *T.n_sitems : T.si_off[chunk + 1])) return;
   const int grp = T.sitem_g[item];
+  const int qslot = chunk < 0 ? grp : T.grp_lc[grp];
   const int d = dm.d, d4 = d >> 2, k = dm.k;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p0 = T.sitem_p[item], p1 = min(p0 + kTrSlice, T.grp_p1[grp]);
-  const float4* QX = reinterpret_cast<const float4*>(T.QX + (int64_t)grp * k * d);
+  const float4* QX = reinterpret_cast<const float4*>(T.QX + (int64_t)qslot * k * d);
   float4* dQ = reinterpret_cast<float4*>(T.dQ + (int64_t)grp * k * d);
   const float inv_bk = 1.f / ((float)dm.B * (float)dm.k);
   const bool pairwise = dm.loss == KGE_LOSS_PAIRWISE;
@@ -958,24 +970,38 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk) {
   if (ms >= 0 && s_last) {
     __threadfence();
     const int ns = (T.grp_p1[grp] - T.grp_p0[grp] + kTrSlice - 1) / kTrSlice;
+    // slice order; every (row, column) load of a slice in flight at once (one L2 round trip per slice)
+#pragma unroll
+    for (int u = 0; u < JU; ++u)
+#pragma unroll
+      for (int m = 0; m < V; ++m) dq[u][m] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < ns; ++q) {
+      const float4* src = reinterpret_cast<const float4*>(T.dQs + (int64_t)(ms + q) * k * d);
+      float4 y[JU][V];
+#pragma unroll
+      for (int u = 0; u < JU; ++u)
+#pragma unroll
+        for (int m = 0; m < V; ++m) {
+          const int j = jt * kTrJt + warp + 8 * u, c = lane + 32 * m;
+          y[u][m] = j < k && c < d4 ? __ldcg(src + (int64_t)j * d4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int u = 0; u < JU; ++u)
+#pragma unroll
+        for (int m = 0; m < V; ++m) {
+          dq[u][m].x += y[u][m].x;
+          dq[u][m].y += y[u][m].y;
+          dq[u][m].z += y[u][m].z;
+          dq[u][m].w += y[u][m].w;
+        }
+    }
 #pragma unroll
     for (int u = 0; u < JU; ++u) {
       const int j = jt * kTrJt + warp + 8 * u;
       if (j >= k) continue;
 #pragma unroll
-      for (int m = 0; m < V; ++m) {
-        const int c = lane + 32 * m;
-        if (c >= d4) continue;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int q = 0; q < ns; ++q) {  // slice order
-          const float4 y = __ldcg(reinterpret_cast<const float4*>(T.dQs + (int64_t)(ms + q) * k * d) + (int64_t)j * d4 + c);
-          acc.x += y.x;
-          acc.y += y.y;
-          acc.z += y.z;
-          acc.w += y.w;
-        }
-        dQ[(int64_t)j * d4 + c] = acc;
-      }
+      for (int m = 0; m < V; ++m)
+        if (lane + 32 * m < d4) dQ[(int64_t)j * d4 + lane + 32 * m] = dq[u][m];
     }
   }
 }
@@ -1150,15 +1176,24 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
       default: launch_pdl(k_tr_score<4>, gs, 256, 0, h->stream, a, chunk); break;
     }
   };
-  if (h->tr_tc) {
-    // every group at once (chunk by chunk -- so a chunk's QX stays in L2 -- measured slower: the per-chunk score
-    // kernels each wait for their hub group's tail, 4 x 58 us vs 115 us)
+  // every group in one launch; KGE_TR_CHUNKED=1 (experiment) runs projections + scores chunk by chunk so a chunk's QX
+  // stays in L2 -- measured slower (1.74 vs 2.02 M pos/s: each chunk's score launch pays the latency of its longest
+  // items again)
+  static const bool global_fwd = getenv("KGE_TR_CHUNKED") == nullptr;
+  if (h->tr_tc && global_fwd) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
     launch_pdl(k_tr_tc<0>, dim3((dm.k + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream, tt->mX, tt->mM, a,
                tt->N, -1);
-    dbg(h, "k_tr_tc<0>");
     score(dim3(tr_jtiles(dm.k), dm.B + dm.B / kTrSlice + 1), -1);
-    dbg(h, "k_tr_score");
+  } else if (h->tr_tc) {  // chunk by chunk: the chunk's projected negatives go to the first QX slots
+    const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
+    for (int c = 0; c < dm.C; ++c) {
+      launch_pdl(k_tr_tc<0>, dim3((dm.k + 127) / 128, dm.g), 128, tr_tc_smem(tt->N), h->stream, tt->mX, tt->mM, a,
+                 tt->N, c);
+      dbg(h, "k_tr_tc<0>");
+      score(dim3(tr_jtiles(dm.k), dm.g + dm.g / kTrSlice + 1), c);
+      dbg(h, "k_tr_score");
+    }
   } else {
     launch_pdl(k_tr_gemm<0>, gk, 256, 0, h->stream, a); dbg(h, "k_tr_gemm<0>");
     score(dim3(tr_jtiles(dm.k), dm.B + dm.B / kTrSlice + 1), -1);  // every group at once, QX slot = group
@@ -1205,7 +1240,7 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
     launch_pdl(k_tr_proj, dm.B, 1024, 0, h->stream, a);
     dbg(h, "k_tr_proj");
   }
-  h->launches += h->tr_tc ? 7 : 8;  // kernels launched here beyond the four launch_begin brackets (k_update counts itself)
+  h->launches += h->tr_tc ? (global_fwd ? 7 : 5 + 2 * dm.C) : 8;  // kernels launched here beyond the four launch_begin brackets (k_update counts itself)
   return cudaGetLastError();
 }
 
