@@ -849,6 +849,29 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk) {
       q[u][m] = j < k && c < d4 ? __ldcs(QX + (int64_t)j * d4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
       dq[u][m] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+  // the slice's o rows (d <= 256) are staged in shared memory once, together with the q loads: the positive blocks
+  // below then wait on no global load
+  constexpr bool STAGE = V <= 2;
+  __shared__ float4 o_s[STAGE ? kTrSlice : 1][32 * V];
+  __shared__ int ip_s[kTrSlice];
+  if (STAGE) {
+    constexpr int PER = (kTrSlice * 32 * V) / 256;
+    float4 t[PER];
+#pragma unroll
+    for (int l = 0; l < PER; ++l) {
+      const int x = threadIdx.x + 256 * l, rr = x / (32 * V), c = x % (32 * V);
+      t[l] = p0 + rr < p1 && c < d4
+                 ? reinterpret_cast<const float4*>(a.b.O + (int64_t)a.s.rel_occ[p0 + rr] * dm.dp)[c]
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int l = 0; l < PER; ++l) {
+      const int x = threadIdx.x + 256 * l;
+      o_s[x / (32 * V)][x % (32 * V)] = t[l];
+    }
+  }
+  if (threadIdx.x < kTrSlice) ip_s[threadIdx.x] = p0 + (int)threadIdx.x < p1 ? a.s.rel_occ[p0 + threadIdx.x] : 0;
+  __syncthreads();
   float lsum = 0.f;
   for (int rb = p0; rb < p1; rb += RB) {
     const int nr = min(RB, p1 - rb);
@@ -857,13 +880,16 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk) {
     float fpos[RB];
 #pragma unroll
     for (int rr = 0; rr < RB; ++rr) {
-      ip[rr] = rr < nr ? a.s.rel_occ[rb + rr] : 0;
+      ip[rr] = rr < nr ? ip_s[rb - p0 + rr] : 0;
       fpos[rr] = rr < nr && pairwise ? dm.gamma - a.b.pstat[ip[rr]] : 0.f;
       const float4* orow = reinterpret_cast<const float4*>(a.b.O + (int64_t)ip[rr] * dm.dp);
 #pragma unroll
       for (int m = 0; m < V; ++m) {
         const int c = lane + 32 * m;
-        o[rr][m] = rr < nr && c < d4 ? orow[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (STAGE)
+          o[rr][m] = o_s[STAGE ? rb - p0 + rr : 0][c];  // zero beyond the slice / d4
+        else
+          o[rr][m] = rr < nr && c < d4 ? orow[c] : make_float4(0.f, 0.f, 0.f, 0.f);
         g[rr][m] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
@@ -933,7 +959,7 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk) {
         acc.z += y.z;
         acc.w += y.w;
       }
-      reinterpret_cast<float4*>(T.dOp + ((int64_t)jt * dm.B + a.s.rel_occ[rb + rr]) * d)[c] = acc;
+      reinterpret_cast<float4*>(T.dOp + ((int64_t)jt * dm.B + ip_s[rb - p0 + rr]) * d)[c] = acc;
     }
     __syncthreads();
   }
