@@ -200,6 +200,34 @@ def test_transr_production_shape_fp32():
     assert np.abs(gpu.get_rows(5, rids) - orc.get_rows(5, rids)).max() <= 1e-6
 
 
+def test_transr_production_shape_tf32():
+    # configs[3] exactly as bench.py times it (the tcgen05 projection path): FB15k-shaped graph, d = 200, B = 1024,
+    # g = k = 256 -- hub groups cut into several score slices, the slice-accumulated back-projection, the
+    # cluster-fused projection Adagrad and the batched positive projections all at their production sizes. TF32 bars
+    # (reading c.14): per-pair scores and loss 2e-3, rows 5e-3 after three free-running steps, projection states 1e-2
+    # relative.
+    gr, trip, gpu, orc = _pair("fb15k", "transr", 200, precision="tf32", lr=0.05)
+    assert gpu.neg_path == "tf32"
+    heads, rels, tails = (np.asarray(a) for a in trip)
+    gpu.set_option("capture_neg", 1)
+    ref, meta = U.pair_scores(orc, 0, heads, rels, tails, SHAPE[1])
+    lg = gpu.train_step(1)
+    got = gpu.neg_scores()
+    err = U.check_pair_scores("transr", got, ref, meta, orc, SHAPE[1], 2e-3)
+    assert err <= 2e-3, err
+    gpu.set_option("capture_neg", 0)
+    lg = np.concatenate([lg, gpu.train_step(2)])
+    lo = orc.train(3)
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) <= 2e-3, (lg, lo)
+    ids = np.unique(np.concatenate([gpu.sample(s)["uniq_ent"] for s in range(3)]))
+    rids = np.unique(np.concatenate([gpu.sample(s)["uniq_rel"] for s in range(3)]))
+    assert np.abs(gpu.get_rows(0, ids) - orc.get_rows(0, ids)).max() <= 5e-3
+    assert np.abs(gpu.get_rows(1, rids) - orc.get_rows(1, rids)).max() <= 5e-3
+    assert np.abs(gpu.get_rows(2, rids) - orc.get_rows(2, rids)).max() <= 5e-3
+    st_g, st_o = gpu.get_rows(5, rids), orc.get_rows(5, rids)
+    assert np.all(np.abs(st_g - st_o) <= 1e-2 * np.abs(st_o) + 1e-12), np.max(np.abs(st_g - st_o) / np.abs(st_o))
+
+
 def test_freebase_bench_configuration():
     # configs[4] exactly as bench.py times it: Freebase-shaped graph (86,054,151 entities, 338,586,276 triples),
     # TransE-L2, d = 400, B = 1024, g = k = 256, TF32 tcgen05 path. Sampling bit-exact (incl. the first epoch
