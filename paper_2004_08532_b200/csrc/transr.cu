@@ -208,6 +208,10 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool val
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(src), "r"(valid ? 4 : 0) : "memory");
 }
+__device__ __forceinline__ void cp_async16(float4* dst, const float4* src, bool valid) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -518,7 +522,8 @@ __device__ __forceinline__ uint64_t sdesc_mn32(uint32_t saddr, uint32_t lbo) {
 // MODE 0: QX_g = X'_c M_u^T (k_tr_gemm<0>); MODE 1: P_g = dQ_g M_u (k_tr_gemm<1>), both into T.QX + g k d
 template <int MODE>
 __global__ void __launch_bounds__(128, 1)
-    k_tr_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, TrArgs a, int N, int chunk) {
+    k_tr_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, TrArgs a, int N, int chunk,
+            int xmode) {  // xmode (timing experiments only, KGE_TR_XMODE): 1 = no epilogue stores
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kTrStages], empty[kTrStages], done;
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(128, 1)
     for (int x = 0; x < 32; ++x) tw[lane * 33 + x] = __uint_as_float(p0[x]);
     __syncwarp();
     const int col = cb * 32 + lane;
-    if (col < d)
+    if (col < d && xmode != 1)
       for (int rr = 0; rr < nrow; ++rr) outw[(int64_t)rr * d + col] = tw[rr * 33 + lane];
     __syncwarp();
   }
@@ -641,7 +646,8 @@ __global__ void __launch_bounds__(128, 1)
 // epilogue. CTA = 128 rows a of dM_u x N columns b; blockIdx.y = unique relation.
 __global__ void __launch_bounds__(128, 1)
     k_tr_dm_tc(const __grid_constant__ CUtensorMap mdQn, const __grid_constant__ CUtensorMap mXn,
-               const __grid_constant__ CUtensorMap mUn, const __grid_constant__ CUtensorMap mHn, TrArgs a, int N) {
+               const __grid_constant__ CUtensorMap mUn, const __grid_constant__ CUtensorMap mHn, TrArgs a, int N,
+               int mode) {  // mode (timing experiments only, KGE_TR_DM_MODE): 1 = no M update, 2 = no epilogue
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[kTrStages], empty[kTrStages], done;
@@ -744,7 +750,7 @@ __global__ void __launch_bounds__(128, 1)
     for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(p0[x]);
   };
   float sq = 0.f;
-  for (int cb = 0; cb * 32 < d; ++cb) {
+  for (int cb = 0; cb * 32 < d && mode < 2; ++cb) {
     float v[32];
     chunk(cb, v);
     if (row < d && !skip) {
@@ -771,33 +777,40 @@ __global__ void __launch_bounds__(128, 1)
   const float st_new = st_old + total / (float)w;
   const float step = dm.lr / sqrtf(st_new + dm.eps);
   tc::cluster_sync();  // the peers' reads of s_part are done before any CTA leaves
-  if (!skip && sidx < 0) {
+  if (!skip && sidx < 0 && mode == 0) {
     if (tc::cluster_ctarank() == 0 && threadIdx.x == 0) a.proj_st[r] = st_new;
-    // each warp's 32 x 32 gradient chunk is transposed through shared memory (the pipeline stages are free once the
-    // MMAs completed), so every M_u row segment is read and written by one coalesced 128-byte warp access
-    float* tw = reinterpret_cast<float*>(smem) + warp * (32 * 33);
-    const int rbase = m0 + warp * 32;
-    float* Mw = a.proj + (int64_t)r * w;
+    // The warp's 32 rows of M_u are copied into shared memory in one cp.async round trip (the pipeline stages are
+    // free once the MMAs completed; row pitch P4 float4, odd, so the row-per-thread float4 accesses below are
+    // conflict-free), updated there from TMEM (thread = row), and written back with coalesced row stores.
+    const int d4 = d >> 2, P4 = d4 | 1, rw0 = m0 + warp * 32, nrw = min(32, d - rw0);
+    float4* Ms = reinterpret_cast<float4*>(smem) + warp * 32 * P4;
+    float4* Mg = reinterpret_cast<float4*>(a.proj + (int64_t)r * w) + (int64_t)rw0 * d4;
+    for (int rr = 0; rr < nrw; ++rr)
+      for (int c = lane; c < d4; c += 32) cp_async16(Ms + rr * P4 + c, Mg + (int64_t)rr * d4 + c, true);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
     for (int cb = 0; cb * 32 < d; ++cb) {
       float v[32];
-      chunk(cb, v);
+      chunk(cb, v);  // warp-collective
+      if (lane < nrw) {
 #pragma unroll
-      for (int x = 0; x < 32; ++x) tw[lane * 33 + x] = v[x];
-      __syncwarp();
-      const int col = cb * 32 + lane;
-#pragma unroll
-      for (int h2 = 0; h2 < 32; h2 += 16) {
-        float m[16];
-#pragma unroll
-        for (int rr = 0; rr < 16; ++rr)
-          m[rr] = rbase + h2 + rr < d && col < d ? Mw[(int64_t)(rbase + h2 + rr) * d + col] : 0.f;
-#pragma unroll
-        for (int rr = 0; rr < 16; ++rr)
-          if (rbase + h2 + rr < d && col < d)
-            Mw[(int64_t)(rbase + h2 + rr) * d + col] = m[rr] - step * tw[(h2 + rr) * 33 + lane];
+        for (int x4 = 0; x4 < 8; ++x4) {
+          const int c4 = cb * 8 + x4;
+          if (c4 < d4) {
+            float4 m = Ms[lane * P4 + c4];
+            m.x -= step * v[4 * x4];
+            m.y -= step * v[4 * x4 + 1];
+            m.z -= step * v[4 * x4 + 2];
+            m.w -= step * v[4 * x4 + 3];
+            Ms[lane * P4 + c4] = m;
+          }
+        }
       }
-      __syncwarp();
     }
+    __syncwarp();
+    for (int rr = 0; rr < nrw; ++rr)
+      for (int c = lane; c < d4; c += 32) Mg[(int64_t)rr * d4 + c] = Ms[rr * P4 + c];
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -805,6 +818,8 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 static size_t tr_tc_smem(int N) { return (size_t)kTrStages * (128 * 128 + (size_t)((N + 31) / 32) * 4096) + 1024; }
+// k_tr_dm_tc: the pipeline stages, reused after the main loop for the 128 rows of M_u (pitch (d/4 | 1) float4)
+static size_t tr_dm_smem(int N, int d) { return std::max(tr_tc_smem(N), (size_t)128 * ((d / 4) | 1) * 16 + 1024); }
 
 // ------------------------------------------------------------------------------------------------
 // per-group scores. CTA (t, g) = 32 negatives j of group g (warp w: j = 32 t + w + 8 u, u < 4, held in registers as
@@ -815,7 +830,8 @@ static size_t tr_tc_smem(int N) { return (size_t)kTrStages * (128 * 128 + (size_
 // holding most of a chunk) is spread over k / 32 CTAs instead of one.
 // ------------------------------------------------------------------------------------------------
 template <int V>
-__global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk) {
+__global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk, int xmode) {
+  // xmode (timing experiments only, KGE_TR_XMODE): 2 = no pair loop, 3 = no dQ stores
   pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
   pdl_trigger();
   constexpr int RB = 4 / V;  // positives per block (registers: (2 JU + 2 RB) V float4 per lane)
@@ -873,7 +889,7 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk) {
   if (threadIdx.x < kTrSlice) ip_s[threadIdx.x] = p0 + (int)threadIdx.x < p1 ? a.s.rel_occ[p0 + threadIdx.x] : 0;
   __syncthreads();
   float lsum = 0.f;
-  for (int rb = p0; rb < p1; rb += RB) {
+  for (int rb = p0; rb < p1 && xmode != 2; rb += RB) {
     const int nr = min(RB, p1 - rb);
     float4 o[RB][V], g[RB][V];
     int ip[RB];
@@ -971,7 +987,7 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk) {
 #pragma unroll
   for (int u = 0; u < JU; ++u) {
     const int j = jt * kTrJt + warp + 8 * u;
-    if (j < k)
+    if (j < k && xmode != 3)
 #pragma unroll
       for (int m = 0; m < V; ++m)
         if (lane + 32 * m < d4) dst[(int64_t)j * d4 + lane + 32 * m] = dq[u][m];
@@ -1195,11 +1211,12 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   launch_end(h, KGE_K_GATHER);
   const dim3 gk((dm.d + GT - 1) / GT, (dm.k + GT - 1) / GT, dm.B);
   launch_begin(h, KGE_K_NEG_FWD);
+  static const int xmode = getenv("KGE_TR_XMODE") ? atoi(getenv("KGE_TR_XMODE")) : 0;  // timing experiments only
   auto score = [&](dim3 gs, int chunk) {
     switch (tr_score_v(dm.d)) {
-      case 1: launch_pdl(k_tr_score<1>, gs, 256, 0, h->stream, a, chunk); break;
-      case 2: launch_pdl(k_tr_score<2>, gs, 256, 0, h->stream, a, chunk); break;
-      default: launch_pdl(k_tr_score<4>, gs, 256, 0, h->stream, a, chunk); break;
+      case 1: launch_pdl(k_tr_score<1>, gs, 256, 0, h->stream, a, chunk, xmode); break;
+      case 2: launch_pdl(k_tr_score<2>, gs, 256, 0, h->stream, a, chunk, xmode); break;
+      default: launch_pdl(k_tr_score<4>, gs, 256, 0, h->stream, a, chunk, xmode); break;
     }
   };
   // every group in one launch; KGE_TR_CHUNKED=1 (experiment) runs projections + scores chunk by chunk so a chunk's QX
@@ -1209,13 +1226,13 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   if (h->tr_tc && global_fwd) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
     launch_pdl(k_tr_tc<0>, dim3((dm.k + 127) / 128, dm.B), 128, tr_tc_smem(tt->N), h->stream, tt->mX, tt->mM, a,
-               tt->N, -1);
+               tt->N, -1, xmode);
     score(dim3(tr_jtiles(dm.k), dm.B + dm.B / kTrSlice + 1), -1);
   } else if (h->tr_tc) {  // chunk by chunk: the chunk's projected negatives go to the first QX slots
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
     for (int c = 0; c < dm.C; ++c) {
       launch_pdl(k_tr_tc<0>, dim3((dm.k + 127) / 128, dm.g), 128, tr_tc_smem(tt->N), h->stream, tt->mX, tt->mM, a,
-                 tt->N, c);
+                 tt->N, c, xmode);
       dbg(h, "k_tr_tc<0>");
       score(dim3(tr_jtiles(dm.k), dm.g + dm.g / kTrSlice + 1), c);
       dbg(h, "k_tr_score");
@@ -1233,7 +1250,7 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   const int nslice = std::max(1, std::min(2 * 148 / (jt * dm.C), dm.B / dm.C));
   if (h->tr_tc) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
-    launch_pdl(k_tr_tc<1>, dim3(jt, dm.C, nslice), 128, tr_tc_smem(tt->N), h->stream, tt->mdQ, tt->mMn, a, tt->N, 0);
+    launch_pdl(k_tr_tc<1>, dim3(jt, dm.C, nslice), 128, tr_tc_smem(tt->N), h->stream, tt->mdQ, tt->mMn, a, tt->N, 0, 0);
     dbg(h, "k_tr_tc<1>");
   } else {
     launch_pdl(k_tr_gemm<1>, gk, 256, 0, h->stream, a); dbg(h, "k_tr_gemm<1>");
@@ -1251,8 +1268,9 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
     const TrTc* tt = static_cast<const TrTc*>(h->tr_tc);
     // cluster = the row blocks of one relation's dM (the fused Adagrad adds their sums of squares through DSMEM)
     const unsigned cx = (unsigned)((dm.d + 127) / 128);
-    e = launch_pdl_cluster(k_tr_dm_tc, dim3(cx, dm.B), 128, tr_tc_smem(tt->N), h->stream, cx, tt->mdQn, tt->mXn, tt->mUn,
-                       tt->mHn, a, tt->N);
+    static const int dm_mode = getenv("KGE_TR_DM_MODE") ? atoi(getenv("KGE_TR_DM_MODE")) : 0;
+    e = launch_pdl_cluster(k_tr_dm_tc, dim3(cx, dm.B), 128, tr_dm_smem(tt->N, dm.d), h->stream, cx, tt->mdQn, tt->mXn, tt->mUn,
+                           tt->mHn, a, tt->N, dm_mode);
     if (e != cudaSuccess) return e;
     dbg(h, "k_tr_dm_tc");
   } else {
@@ -1345,7 +1363,8 @@ void transr_tc_init(kge_handle* h) {
     const size_t smem = tr_tc_smem(tt->N);
     ok = ok && cudaFuncSetAttribute(k_tr_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
     ok = ok && cudaFuncSetAttribute(k_tr_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
-    ok = ok && cudaFuncSetAttribute(k_tr_dm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+    ok = ok && cudaFuncSetAttribute(k_tr_dm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)tr_dm_smem(tt->N, dm.d)) == cudaSuccess;
     if (ok) {
       h->tr_tc = tt;
     } else {
