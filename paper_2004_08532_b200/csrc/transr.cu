@@ -888,7 +888,7 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk, int xmode
   }
   if (threadIdx.x < kTrSlice) ip_s[threadIdx.x] = p0 + (int)threadIdx.x < p1 ? a.s.rel_occ[p0 + threadIdx.x] : 0;
   __syncthreads();
-  float lsum = 0.f;
+  float lsum = 0.f, lprod = 1.f;
   for (int rb = p0; rb < p1 && xmode != 2; rb += RB) {
     const int nr = min(RB, p1 - rb);
     float4 o[RB][V], g[RB][V];
@@ -926,7 +926,7 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk, int xmode
           s2 = fmaf(uz, uz, s2);
           s2 = fmaf(uw, uw, s2);
         }
-        s2 = __shfl_sync(0xffffffffu, warp_sum(s2), 0);  // one value for every lane
+        s2 = warp_sum(s2);  // xor butterfly: every lane holds the same bits
         const float f = dm.gamma - s2;
         float coef;
         if (pairwise) {  // reading c.9'
@@ -939,8 +939,17 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk, int xmode
           }
           coef = -2.f * dldf;
         } else {
-          coef = -2.f * sigmoid(f) * inv_bk;  // dL/df * df/d(s2)
-          if (lane == 0) lsum += -log_sigmoid(-f);
+          // e = exp(-|f|): sigma(f) = f >= 0 ? 1/(1+e) : e/(1+e); -log sigma(-f) = max(f, 0) + log1p(e), the log1p
+          // terms summed as one log of their product (each factor in (1, 2], <= 64 per lane: no overflow) -- the
+          // three-MUFU form of the tcgen05 forward epilogue
+          const float e = __expf(-fabsf(f));
+          float r1;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(1.f + e));
+          coef = -2.f * (f >= 0.f ? r1 : e * r1) * inv_bk;  // dL/df * df/d(s2)
+          if (lane == 0) {
+            lsum += fmaxf(f, 0.f);
+            lprod *= 1.f + e;
+          }
         }
         if (lane == 0 && a.b.fdbg) a.b.fdbg[(int64_t)ip[rr] * k + j] = f;  // KGE_OPT_CAPTURE_NEG
 #pragma unroll
@@ -992,6 +1001,7 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk, int xmode
       for (int m = 0; m < V; ++m)
         if (lane + 32 * m < d4) dst[(int64_t)j * d4 + lane + 32 * m] = dq[u][m];
   }
+  lsum += __logf(lprod);
   lsum = warp_sum(lsum);
   if (lane == 0) red[warp] = lsum;
   __shared__ int s_last;
