@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(1024) k_tr_groups(TrArgs a) {
 // part q = tid % 8): partial sums over kk = q, q + 8, ..., added over the 8 lanes of x by a butterfly (every lane gets
 // the same bits; fixed order).
 // ------------------------------------------------------------------------------------------------
-static size_t tr_mv_smem(int d) { return (size_t)2 * (32 * (d + 1) + 16 * d) * sizeof(float); }
+static size_t tr_mv_smem(int d) { return (size_t)2 * (32 * (d + 4) + 16 * d) * sizeof(float); }
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src, bool valid) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
@@ -222,8 +222,10 @@ __global__ void __launch_bounds__(256) k_tr_mv(TrArgs a) {
   pdl_trigger();
   const Dims& dm = a.dm;
   extern __shared__ float sm[];
-  const int d = dm.d, lda = d + 1, x0 = blockIdx.x * 32;
-  const int buf_floats = 32 * lda + 16 * d;  // per buffer: slab [32][d + 1], then vectors [16][d]
+  // slab pitch: d + 1 for the transposed (4-byte) copies of BWD (conflict-free column writes), d + 4 for FWD so its
+  // rows stay 16-byte aligned for 16-byte copies
+  const int d = dm.d, lda = BWD ? d + 1 : d + 4, x0 = blockIdx.x * 32, d4 = d >> 2;
+  const int buf_floats = 32 * lda + 16 * d;  // per buffer: slab [32][lda], then vectors [16][d]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n_items = *a.t.n_items;
   // items it = blockIdx.y, + gridDim.y, ... through two shared-memory buffers: the cp.async copies of item i + 1 are
@@ -238,11 +240,11 @@ __global__ void __launch_bounds__(256) k_tr_mv(TrArgs a) {
     if (BWD) {  // slab[xx][kk] = M[kk][x0 + xx]
       const bool ok = x0 + lane < d;
       for (int kk = warp; kk < d; kk += 8) cp_async4(slab + lane * lda + kk, M + (int64_t)kk * d + (ok ? x0 + lane : 0), ok);
-    } else {  // slab[xx][kk] = M[x0 + xx][kk]
+    } else {  // slab[xx][kk] = M[x0 + xx][kk], 16-byte copies
       for (int xx = warp; xx < 32; xx += 8) {
         const bool ok = x0 + xx < d;
-        const float* row = M + (int64_t)(ok ? x0 + xx : 0) * d;
-        for (int kk = lane; kk < d; kk += 32) cp_async4(slab + xx * lda + kk, row + kk, ok);
+        const float4* row = reinterpret_cast<const float4*>(M + (int64_t)(ok ? x0 + xx : 0) * d);
+        for (int c = lane; c < d4; c += 32) cp_async16(reinterpret_cast<float4*>(slab + xx * lda) + c, row + c, ok);
       }
     }
     const int p = pb + warp;  // vectors 2 warp, 2 warp + 1 (BWD: the gMh / gMt rows of U; else h / t)
@@ -259,9 +261,10 @@ __global__ void __launch_bounds__(256) k_tr_mv(TrArgs a) {
         src1 = a.ent.row(a.s.pt[i]);
       }
     }
-    for (int kk = lane; kk < d; kk += 32) {
-      cp_async4(vec + (2 * warp) * d + kk, src0 + (ok ? kk : 0), ok);
-      cp_async4(vec + (2 * warp + 1) * d + kk, src1 + (ok ? kk : 0), ok);
+    for (int c = lane; c < d4; c += 32) {  // 16-byte copies (rows of d floats, d % 4 == 0)
+      cp_async16(reinterpret_cast<float4*>(vec + (2 * warp) * d) + c, reinterpret_cast<const float4*>(src0) + (ok ? c : 0), ok);
+      cp_async16(reinterpret_cast<float4*>(vec + (2 * warp + 1) * d) + c, reinterpret_cast<const float4*>(src1) + (ok ? c : 0),
+                 ok);
     }
   };
   int cur = 0;
