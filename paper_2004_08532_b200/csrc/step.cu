@@ -915,16 +915,18 @@ __global__ void __launch_bounds__(256, 2) k_neg_bwd(NegArgs a) {
           if (FAM == FAM_DOT) {
             acc[ii][ee] = fmaf(w[ii], t_, acc[ii][ee]);
           } else if (FAM == FAM_L1) {
-            // w * sgn(o - x) with sgn(0) = 0 (reading c.10): (o > x) - (o < x), set as 1.0 / 0.0 in one instruction each
-            const float o_ = pass_x ? t_ : s_, x_ = pass_x ? s_ : t_;
-            const float sg = (o_ > x_ ? 1.f : 0.f) - (o_ < x_ ? 1.f : 0.f);
-            acc[ii][ee] = fmaf(w[ii], pass_x ? -sg : sg, acc[ii][ee]);
+            // dO: w sgn(o - x) with o = self; dX': -w sgn(o - x) = w sgn(x - o) with x = self -- both are
+            // w sgn(self - other), sgn(0) = 0 (reading c.10), formed as (s > t) - (s < t) (one FSET each): no
+            // per-element selects on the pass (the same exact +-1 / 0 factors as before)
+            const float sg = (s_ > t_ ? 1.f : 0.f) - (s_ < t_ ? 1.f : 0.f);
+            acc[ii][ee] = fmaf(w[ii], sg, acc[ii][ee]);
           } else if (FAM == FAM_CMOD) {
-            const float ur = pass_x ? (t_ - s_) : (s_ - t_);
-            const float ui = pass_x ? (oi[ee] - si[ii][ee]) : (si[ii][ee] - oi[ee]);
+            // dO: w (o - x) / |o - x|, dX': -w (o - x) / |o - x| = w (x - o) / |x - o|: both w (self - other) / |.|
+            // (x - o == -(o - x) exactly), so no per-element selects on the pass
+            const float ur = s_ - t_, ui = si[ii][ee] - oi[ee];
             const float inv = 1.f / fmaxf(sqrtf(ur * ur + ui * ui), 1e-12f);
             const float comp = imag_lane ? ui : ur;
-            acc[ii][ee] = fmaf(w[ii], (pass_x ? -comp : comp) * inv, acc[ii][ee]);
+            acc[ii][ee] = fmaf(w[ii], comp * inv, acc[ii][ee]);
           } else {  // L2, L2SQ: phi_o = o - x
             const float u = s_ - t_;  // self - other: = (o - x) for dO, = (x - o) = -phi_o for dX'
             acc[ii][ee] = fmaf(w[ii], u, acc[ii][ee]);
