@@ -1095,14 +1095,34 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
   const Dims& dm = a.dm;
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == gridDim.x - 1) {
-    if (threadIdx.x < 32) {
-      float sp = 0.f, sn = 0.f;
-      for (int i = lane; i < dm.B; i += 32) sp += a.b.lpos[i];
-      const int nparts = *a.t.n_sitems * tr_jtiles(dm.k);  // per (score item, tile of 32 negatives), k_tr_score
-      for (int q = lane; q < nparts; q += 32) sn += a.b.lneg[q];
-      sp = warp_sum(sp);
-      sn = warp_sum(sn);
-      if (lane == 0) {
+    // the loss: every thread of the CTA sums a strided share (eight loads in flight), then the 8 warps' sums are
+    // added in warp order -- a fixed association
+    __shared__ float s_sp[8], s_sn[8];
+    float sp = 0.f, sn = 0.f;
+    for (int i = threadIdx.x; i < dm.B; i += blockDim.x) sp += a.b.lpos[i];
+    const int nparts = *a.t.n_sitems * tr_jtiles(dm.k);  // per (score item, tile of 32 negatives), k_tr_score
+    for (int q0 = threadIdx.x; q0 < nparts; q0 += 8 * blockDim.x) {
+      float y[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) y[t] = q0 + t * (int)blockDim.x < nparts ? a.b.lneg[q0 + t * blockDim.x] : 0.f;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) sn += y[t];
+    }
+    sp = warp_sum(sp);
+    sn = warp_sum(sn);
+    if (lane == 0) {
+      s_sp[threadIdx.x >> 5] = sp;
+      s_sn[threadIdx.x >> 5] = sn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sp = 0.f;
+      sn = 0.f;
+      for (int w8 = 0; w8 < 8; ++w8) {
+        sp += s_sp[w8];
+        sn += s_sn[w8];
+      }
+      {
         const float L = sp / (float)dm.B + sn / ((float)dm.B * (float)dm.k);
         store_loss(a.b.loss, a.s.info, L);
         const bool bad = !isfinite(L);
@@ -1137,7 +1157,14 @@ __global__ void __launch_bounds__(256) k_tr_chain(TrArgs a) {
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
     const float tp = 2.f * w * pv[e];
     float dO = dOp[e];
-    for (int t = 1; t < njt; ++t) dO += dOp[t * tstride + e];  // the negative tiles in order
+    for (int t0 = 1; t0 < njt; t0 += 8) {  // the negative tiles in order, eight loads in flight
+      float y[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) y[t] = t0 + t < njt ? dOp[(t0 + t) * tstride + e] : 0.f;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        if (t0 + t < njt) dO += y[t];
+    }
     const float gh = mode == 0 ? dO - tp : -tp;
     const float gt = mode == 0 ? tp : dO + tp;
     gR[e] = mode == 0 ? gh : -gt;
