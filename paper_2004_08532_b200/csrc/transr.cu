@@ -833,7 +833,7 @@ static size_t tr_dm_smem(int N, int d) { return std::max(tr_tc_smem(N), (size_t)
 // holding most of a chunk) is spread over k / 32 CTAs instead of one.
 // ------------------------------------------------------------------------------------------------
 template <int V>
-__global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk, int xmode) {
+__global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk, int xmode, int fast) {
   // xmode (timing experiments only, KGE_TR_XMODE): 2 = no pair loop, 3 = no dQ stores
   pdl_wait();  // the predecessor's outputs are final (programmatic dependent launch)
   pdl_trigger();
@@ -945,13 +945,19 @@ __global__ void __launch_bounds__(256) k_tr_score(TrArgs a, int chunk, int xmode
           // e = exp(-|f|): sigma(f) = f >= 0 ? 1/(1+e) : e/(1+e); -log sigma(-f) = max(f, 0) + log1p(e), the log1p
           // terms summed as one log of their product (each factor in (1, 2], <= 64 per lane: no overflow) -- the
           // three-MUFU form of the tcgen05 forward epilogue
-          const float e = __expf(-fabsf(f));
-          float r1;
-          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(1.f + e));
-          coef = -2.f * (f >= 0.f ? r1 : e * r1) * inv_bk;  // dL/df * df/d(s2)
-          if (lane == 0) {
-            lsum += fmaxf(f, 0.f);
-            lprod *= 1.f + e;
+          // (the FP32 path -- FFMA projections -- keeps the accurate expf / log1pf forms of its 1e-5 bars)
+          if (fast) {
+            const float e = __expf(-fabsf(f));
+            float r1;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(1.f + e));
+            coef = -2.f * (f >= 0.f ? r1 : e * r1) * inv_bk;  // dL/df * df/d(s2)
+            if (lane == 0) {
+              lsum += fmaxf(f, 0.f);
+              lprod *= 1.f + e;
+            }
+          } else {
+            coef = -2.f * sigmoid(f) * inv_bk;
+            if (lane == 0) lsum += -log_sigmoid(-f);
           }
         }
         if (lane == 0 && a.b.fdbg) a.b.fdbg[(int64_t)ip[rr] * k + j] = f;  // KGE_OPT_CAPTURE_NEG
@@ -1252,11 +1258,12 @@ cudaError_t launch_transr_step(kge_handle* h, const Slot& s, int64_t step) {
   const dim3 gk((dm.d + GT - 1) / GT, (dm.k + GT - 1) / GT, dm.B);
   launch_begin(h, KGE_K_NEG_FWD);
   static const int xmode = getenv("KGE_TR_XMODE") ? atoi(getenv("KGE_TR_XMODE")) : 0;  // timing experiments only
+  const int fast = h->tr_tc ? 1 : 0;  // three-MUFU logistic form on the TF32 path only
   auto score = [&](dim3 gs, int chunk) {
     switch (tr_score_v(dm.d)) {
-      case 1: launch_pdl(k_tr_score<1>, gs, 256, 0, h->stream, a, chunk, xmode); break;
-      case 2: launch_pdl(k_tr_score<2>, gs, 256, 0, h->stream, a, chunk, xmode); break;
-      default: launch_pdl(k_tr_score<4>, gs, 256, 0, h->stream, a, chunk, xmode); break;
+      case 1: launch_pdl(k_tr_score<1>, gs, 256, 0, h->stream, a, chunk, xmode, fast); break;
+      case 2: launch_pdl(k_tr_score<2>, gs, 256, 0, h->stream, a, chunk, xmode, fast); break;
+      default: launch_pdl(k_tr_score<4>, gs, 256, 0, h->stream, a, chunk, xmode, fast); break;
     }
   };
   // every group in one launch; KGE_TR_CHUNKED=1 (experiment) runs projections + scores chunk by chunk so a chunk's QX
