@@ -1082,15 +1082,23 @@ static int train_batch_enqueue(kge_handle* h, const int64_t* heads, const int64_
                 hp[0] / *hn, hp[1] / *hn, hp[2] / *hn, (long long)*hn);
     }
   } hpr{hprof, t0, t1, hp, &hn, +now};
-  for (int i = 0; i < B; ++i) {
-    if (heads[i] < 0 || heads[i] >= h->dims.n_entities || tails[i] < 0 || tails[i] >= h->dims.n_entities ||
-        rels[i] < 0 || rels[i] >= h->dims.n_relations) {
+  {  // branch-free (vectorisable) narrowing and range check; the error is reported after the loop
+    const uint64_t ne = (uint64_t)h->dims.n_entities, nr = (uint64_t)h->dims.n_relations;
+    uint64_t bad = 0;
+    int32_t* sh = st;
+    int32_t* sr = st + B;
+    int32_t* stt = st + 2 * B;
+    for (int i = 0; i < B; ++i) {  // unsigned compares: negative ids wrap to huge values
+      bad |= (uint64_t)((uint64_t)heads[i] >= ne) | (uint64_t)((uint64_t)tails[i] >= ne) |
+             (uint64_t)((uint64_t)rels[i] >= nr);
+      sh[i] = (int32_t)heads[i];
+      sr[i] = (int32_t)rels[i];
+      stt[i] = (int32_t)tails[i];
+    }
+    if (bad) {
       set_error("batch id out of range");
       return KGE_ERANGE;
     }
-    st[i] = (int32_t)heads[i];
-    st[B + i] = (int32_t)rels[i];
-    st[2 * B + i] = (int32_t)tails[i];
   }
   if (hprof) hpr.t2 = now();
   if (h->epoch_steps > 0) {
