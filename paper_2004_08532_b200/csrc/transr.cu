@@ -752,6 +752,16 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
     for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(p0[x]);
   };
+  // this warp's 32 rows of M_u into the freed pipeline shared memory (row pitch P4 float4, odd: the row-per-thread
+  // float4 accesses below are conflict-free), in flight during the sums of squares and the cluster barriers
+  const int d4 = d >> 2, P4 = d4 | 1, rw0 = m0 + warp * 32, nrw = min(32, d - rw0);
+  float4* Ms = reinterpret_cast<float4*>(smem) + warp * 32 * P4;
+  float4* Mg = reinterpret_cast<float4*>(a.proj + (int64_t)r * w) + (int64_t)rw0 * d4;
+  const bool upd = !skip && sidx < 0 && mode == 0;
+  if (upd)
+    for (int rr = 0; rr < nrw; ++rr)
+      for (int c = lane; c < d4; c += 32) cp_async16(Ms + rr * P4 + c, Mg + (int64_t)rr * d4 + c, true);
+  cp_async_commit();
   float sq = 0.f;
   for (int cb = 0; cb * 32 < d && mode < 2; ++cb) {
     float v[32];
@@ -785,13 +795,7 @@ __global__ void __launch_bounds__(128, 1)
     // The warp's 32 rows of M_u are copied into shared memory in one cp.async round trip (the pipeline stages are
     // free once the MMAs completed; row pitch P4 float4, odd, so the row-per-thread float4 accesses below are
     // conflict-free), updated there from TMEM (thread = row), and written back with coalesced row stores.
-    const int d4 = d >> 2, P4 = d4 | 1, rw0 = m0 + warp * 32, nrw = min(32, d - rw0);
-    float4* Ms = reinterpret_cast<float4*>(smem) + warp * 32 * P4;
-    float4* Mg = reinterpret_cast<float4*>(a.proj + (int64_t)r * w) + (int64_t)rw0 * d4;
-    for (int rr = 0; rr < nrw; ++rr)
-      for (int c = lane; c < d4; c += 32) cp_async16(Ms + rr * P4 + c, Mg + (int64_t)rr * d4 + c, true);
-    cp_async_commit();
-    cp_async_wait<0>();
+    cp_async_wait<0>();  // the M_u rows issued before the sums of squares
     __syncwarp();
     for (int cb = 0; cb * 32 < d; ++cb) {
       float v[32];
