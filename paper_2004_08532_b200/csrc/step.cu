@@ -1230,6 +1230,15 @@ __device__ __forceinline__ void prefetch_row(const float* __restrict__ row, floa
 // Everything not produced by the backward pass (sample-slot indices, current rows and Adagrad state -- written by
 // kernels that completed before the forward pass started) is loaded before griddepcontrol.wait.
 constexpr int kSeg = 8;
+constexpr int kStg = 3;  // k_update (V <= 4): rows per warp staged in shared memory by cp.async
+
+__device__ __forceinline__ void cpa16(float4* dst, const float4* src) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 
 template <int V>
 __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
@@ -1296,9 +1305,33 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
   if (a.b.flags[2 + (a.s.info[0] & 1)]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
   RowAcc<V> acc;
   acc.zero();
+  // V <= 4: the rows of kStg occurrences at a time are copied into this warp's shared-memory staging area by cp.async
+  // (no registers held, so more rows are in flight than the 64-register budget allows) and added in occurrence
+  // order -- the same additions as the register path. 48 KB per CTA keeps 4 CTAs per SM (one resident wave).
+  __shared__ float4 stg[8][V <= 4 ? kStg : 1][V <= 4 ? 32 * V : 1];
+  auto staged_sum = [&](int nrows, auto rowptr) {  // acc += rows 0..nrows-1 (rowptr(q): const float* of row q)
+    float4* my = &stg[threadIdx.x >> 5][0][0];
+    for (int j = 0; j < nrows; j += kStg) {
+      const int nb = min(kStg, nrows - j);
+      for (int q = 0; q < nb; ++q) {
+        const float4* src = reinterpret_cast<const float4*>(rowptr(j + q));
+#pragma unroll
+        for (int m = 0; m < V; ++m)
+          if (lane + 32 * m < w4) cpa16(my + q * 32 * V + lane + 32 * m, src + lane + 32 * m);
+      }
+      cpa_wait_all();  // a lane reads back only what it copied
+      for (int q = 0; q < nb; ++q)
+#pragma unroll
+        for (int m = 0; m < V; ++m)
+          if (lane + 32 * m < w4) acc.add(my[q * 32 * V + lane + 32 * m], m);
+    }
+  };
   // loads of UNR occurrences in flight, additions in occurrence order; V = 4 (d <= 512) keeps two in flight so the
   // kernel fits 4 CTAs (32 warps) per SM: the whole grid (B + n_occ warps) is resident in one wave
   constexpr int UNR = V >= 4 ? 2 : 4;
+  if (V <= 4) {
+    staged_sum(n, [&](int q) { return G + (int64_t)__shfl_sync(0xffffffffu, oj, q & 31) * w; });
+  } else
   for (int j = 0; j < n; j += UNR) {
     float4 x[UNR][V];
 #pragma unroll
@@ -1338,6 +1371,10 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
       // the home rows of up to 32 segments in one round trip (lane q: segment b0 + q), then the sums in segment order
       const int hq = b0 + lane < nseg ? occ_sorted[r0 + (b0 + lane) * kSeg] : 0;
       const int nq = min(32, nseg - b0);
+      if (V <= 4) {
+        staged_sum(nq, [&](int q) { return G + (int64_t)__shfl_sync(0xffffffffu, hq, q & 31) * w; });
+        continue;
+      }
       for (int q0 = 0; q0 < nq; q0 += UNR2) {
         float4 x[UNR2][V];
 #pragma unroll
