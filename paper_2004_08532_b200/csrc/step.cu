@@ -1171,6 +1171,7 @@ struct UpdateArgs {
   int32_t* seg_cnt;            // [B + n_occ] per-unique-row segment arrival counters (zero between steps)
   int32_t pos_lo, pos_hi;      // positions handled: [0, B) relations, [B, B + n_occ) entities (lag = 1 splits them)
   const Slot* next;            // device slot of the next step (P == 1), or nullptr: its entity rows are prefetched
+  int32_t stg_rows;            // V <= 4: rows per warp staged in dynamic shared memory (pitch w4 float4)
 };
 
 // Row accumulator: V float4 per lane.
@@ -1230,7 +1231,7 @@ __device__ __forceinline__ void prefetch_row(const float* __restrict__ row, floa
 // Everything not produced by the backward pass (sample-slot indices, current rows and Adagrad state -- written by
 // kernels that completed before the forward pass started) is loaded before griddepcontrol.wait.
 constexpr int kSeg = 8;
-constexpr int kStg = 3;  // k_update (V <= 4): rows per warp staged in shared memory by cp.async
+constexpr int kStgBytes = 56 * 1024;  // k_update (V <= 4): staging budget per CTA (4 CTAs per SM)
 
 __device__ __forceinline__ void cpa16(float4* dst, const float4* src) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
@@ -1305,25 +1306,26 @@ __global__ void __launch_bounds__(256, V >= 8 ? 1 : 4) k_update(UpdateArgs a) {
   if (a.b.flags[2 + (a.s.info[0] & 1)]) return;  // non-finite loss: skip this step's update (KGE_ENONFINITE)
   RowAcc<V> acc;
   acc.zero();
-  // V <= 4: the rows of kStg occurrences at a time are copied into this warp's shared-memory staging area by cp.async
-  // (no registers held, so more rows are in flight than the 64-register budget allows) and added in occurrence
-  // order -- the same additions as the register path. 48 KB per CTA keeps 4 CTAs per SM (one resident wave).
-  __shared__ float4 stg[8][V <= 4 ? kStg : 1][V <= 4 ? 32 * V : 1];
+  // V <= 4: the rows of stg_rows occurrences at a time are copied into this warp's shared-memory staging area by
+  // cp.async (no registers held, so more rows are in flight than the 64-register budget allows) and added in
+  // occurrence order -- the same additions as the register path. <= 56 KB per CTA keeps 4 CTAs per SM (one wave).
+  extern __shared__ float4 stg_dyn[];  // [warps][stg_rows][w4]
   auto staged_sum = [&](int nrows, auto rowptr) {  // acc += rows 0..nrows-1 (rowptr(q): const float* of row q)
-    float4* my = &stg[threadIdx.x >> 5][0][0];
-    for (int j = 0; j < nrows; j += kStg) {
-      const int nb = min(kStg, nrows - j);
+    const int ns = a.stg_rows;
+    float4* my = stg_dyn + (int64_t)(threadIdx.x >> 5) * ns * w4;
+    for (int j = 0; j < nrows; j += ns) {
+      const int nb = min(ns, nrows - j);
       for (int q = 0; q < nb; ++q) {
         const float4* src = reinterpret_cast<const float4*>(rowptr(j + q));
 #pragma unroll
         for (int m = 0; m < V; ++m)
-          if (lane + 32 * m < w4) cpa16(my + q * 32 * V + lane + 32 * m, src + lane + 32 * m);
+          if (lane + 32 * m < w4) cpa16(my + q * w4 + lane + 32 * m, src + lane + 32 * m);
       }
       cpa_wait_all();  // a lane reads back only what it copied
       for (int q = 0; q < nb; ++q)
 #pragma unroll
         for (int m = 0; m < V; ++m)
-          if (lane + 32 * m < w4) acc.add(my[q * 32 * V + lane + 32 * m], m);
+          if (lane + 32 * m < w4) acc.add(my[q * w4 + lane + 32 * m], m);
     }
   };
   // loads of UNR occurrences in flight, additions in occurrence order; V = 4 (d <= 512) keeps two in flight so the
@@ -1494,15 +1496,18 @@ cudaError_t launch_update_range(kge_handle* h, const Slot& s, int lo, int hi, cu
   const int grid = (hi - lo + wpc - 1) / wpc;
   if (grid <= 0) return cudaSuccess;
   const int w4 = std::max(dm.d, dm.drel) / 4;
+  // staged rows per warp: as many (<= kSeg) as the per-CTA budget holds at this row width
+  ua.stg_rows = std::max(1, std::min(kSeg, kStgBytes / (wpc * w4 * 16)));
+  const size_t stg = (size_t)wpc * ua.stg_rows * w4 * 16;
   cudaStream_t main = h->stream;
   h->stream = st;  // the profiler brackets the launch on the stream it runs on
   launch_begin(h, KGE_K_UPDATE);
   if (w4 <= 32)
-    launch_pdl(k_update<1>, grid, 32 * wpc, 0, st, ua);
+    launch_pdl(k_update<1>, grid, 32 * wpc, stg, st, ua);
   else if (w4 <= 64)
-    launch_pdl(k_update<2>, grid, 32 * wpc, 0, st, ua);
+    launch_pdl(k_update<2>, grid, 32 * wpc, stg, st, ua);
   else if (w4 <= 128)
-    launch_pdl(k_update<4>, grid, 32 * wpc, 0, st, ua);
+    launch_pdl(k_update<4>, grid, 32 * wpc, stg, st, ua);
   else
     launch_pdl(k_update<8>, grid, 32 * wpc, 0, st, ua);
   launch_end(h, KGE_K_UPDATE);
@@ -1925,6 +1930,9 @@ cudaError_t step_preload() {
   preload(k_update<1>, e);
   preload(k_update<2>, e);
   preload(k_update<4>, e);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_update<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStgBytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_update<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStgBytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_update<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStgBytes);
   preload(k_update<8>, e);
   preload(k_neg_fwd<FAM_DOT>, e);
   preload(k_neg_fwd<FAM_L2>, e);
